@@ -1,0 +1,163 @@
+/*
+ * vdi_b200.h -- C ABI of the B200-native VDI generation / VDI raycasting path.
+ *
+ * The reference (vdikit 0.1.0, /root/reference/pkg) has no FFI: its hot path
+ * is two numba kernels behind the Python functions `generate_vdi` and
+ * `render_vdi`. The entry points below are the flat, C-like cut of those
+ * kernels; the Python package paper_2206_08660_b200 binds
+ * them with ctypes and keeps the reference's Python signatures on top.
+ *
+ *   vdi_gen_launch     replaces generate.py:276-319  _generate_kernel
+ *                      (with _find_gamma_list generate.py:219-273,
+ *                       _gen_list_pass generate.py:89-216, _emit generate.py:53-86)
+ *   vdi_grid_launch    replaces generate.py:322-346  _accumulate_grid
+ *   vdi_render_launch  replaces raycast.py:275-456   _render_kernel
+ *                      (with _find_first raycast.py:79-141, _bins raycast.py:51-62)
+ *   vdi_find_first_batch  batch form of raycast.py:144-156 find_first_supersegment
+ *   vdi_segs_to_aos / vdi_segs_from_aos  device layout <-> the reference's
+ *                      (H, W, n_sg, 6) f32 array (vdi.py:3-7, 23-24)
+ *
+ * Conventions
+ *   - every pointer is a DEVICE pointer unless its name ends in _host;
+ *   - matrices are row-major f64[16] holding the host's exact bits
+ *     (Camera.proj_view / inv_proj_view, camera.py:108-112);
+ *   - no entry point allocates or synchronises; all work is enqueued on
+ *     `stream` (a cudaStream_t; NULL = legacy default stream);
+ *   - return 0 on success, < 0 on bad arguments (VDI_EINVAL) or a launch
+ *     error (VDI_ELAUNCH); vdi_last_error() gives a thread-local message.
+ *
+ * Device segment layout (VDI_LAYOUT_LIST_SOA): each list owns n_sg*6 floats
+ *   [front[0..n_sg) | back[0..n_sg) | rgba[0..n_sg) as float4]
+ * so the Alg. 2 search touches only the contiguous `back` run and each
+ * supersegment's colour is one 16-byte load. VDI_LAYOUT_AOS is the
+ * reference's [front, back, r, g, b, a] per supersegment.
+ *
+ * Row sharding: a "band map" (band_rows, band_stride, band_offset) selects
+ * the image rows r with ((r / band_rows) % band_stride) == band_offset and
+ * packs them densely, in order, into the output arrays ("local rows").
+ * (band_rows, 1, 0) is the whole image in natural order.
+ */
+#ifndef VDI_B200_H
+#define VDI_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VDI_ABI_VERSION 1
+
+#define VDI_OK 0
+#define VDI_EINVAL (-1)
+#define VDI_ELAUNCH (-2)
+
+#define VDI_VOXEL_U8 0
+#define VDI_VOXEL_U16 1
+#define VDI_VOXEL_F32 2
+
+#define VDI_LAYOUT_LIST_SOA 0
+#define VDI_LAYOUT_AOS 1
+
+typedef void* vdi_stream_t; /* cudaStream_t */
+
+/* Generation: one ray per viewport pixel, per-ray gamma bisection (Alg. 1 as
+ * implemented in generate.py:219-273), supersegments written in
+ * VDI_LAYOUT_LIST_SOA. Outputs are indexed by local row (band map). */
+typedef struct VdiGenArgs {
+  const void* volume;   /* (nz, ny, nx) x-fastest, voxel_type elements */
+  const float* lut;     /* (lut_n, 4) f32, TransferFunction.lut */
+  int32_t* counts;      /* OUT (local_h, width) */
+  float* segs;          /* OUT (local_h, width, n_sg*6) list-SoA */
+  double* gammas;       /* OUT (local_h, width), may be NULL */
+  int32_t* passes;      /* OUT (local_h, width), may be NULL */
+  int32_t* samples;     /* OUT executed samples per ray (R's loop semantics), may be NULL */
+  void* workspace;      /* vdi_gen_workspace_bytes() bytes, any content */
+  double pv[16];        /* generation proj*view */
+  double inv_pv[16];
+  double eye[3];
+  double aabb[6];       /* lo xyz, hi xyz (volume.py:57-60) */
+  double eps;           /* GenParams.epsilon */
+  double gamma_init;
+  double step;          /* resolved step (generate.py:38-50) */
+  double lref;
+  int32_t voxel_type;
+  int32_t nx, ny, nz;
+  int32_t lut_n;
+  int32_t width, height;
+  int32_t n_sg, delta;
+  int32_t band_rows, band_stride, band_offset;
+} VdiGenArgs;
+
+/* AccelGrid: per-cell supersegment counts (generate.py:322-346). `grid` is
+ * (gz, gy, gx) u32 and is accumulated into (zero it first, or pass
+ * clear=1). */
+typedef struct VdiGridArgs {
+  const float* segs;      /* list-SoA, local rows */
+  const int32_t* counts;  /* local rows */
+  uint32_t* grid;
+  double near, far, proj_a, proj_b;
+  int32_t width, height, n_sg;
+  int32_t gx, gy, gz;
+  int32_t band_rows, band_stride, band_offset;
+  int32_t clear;
+} VdiGridArgs;
+
+/* Novel-view rendering (raycast.py:275-456). The VDI is read through a band
+ * map too (vdi_band_rows, vdi_band_world): list row r lives at storage row
+ * ((r/b) / W)*b + (r%b) + ((r/b) % W) * rows_per_rank -- i.e. the layout an
+ * all-gather of band-sharded generation leaves behind. (b, 1) = natural. */
+typedef struct VdiRenderArgs {
+  const float* segs;            /* list-SoA */
+  const int32_t* counts;
+  const uint32_t* grid;         /* (gz, gy, gx) */
+  double* image;                /* OUT (local_out_h, out_w, 4) f64 premultiplied */
+  int32_t* lists_visited;       /* OUT per pixel, may be NULL */
+  int32_t* segs_intersected;    /* OUT per pixel, may be NULL */
+  int32_t* lists_searched;      /* OUT per pixel, may be NULL */
+  unsigned long long* stat_sums;/* OUT [3] += (visited, intersected, searched), may be NULL */
+  double gen_pv[16];
+  double gen_inv_pv[16];
+  double new_inv_pv[16];
+  double eye[3];                /* new camera position */
+  double aabb[6];               /* Vdi.volume_aabb */
+  double bg[4];                 /* straight RGBA background */
+  double near, far, proj_a, proj_b;
+  double early_term;
+  int32_t vdi_w, vdi_h, n_sg;
+  int32_t gx, gy, gz;
+  int32_t out_w, out_h;
+  int32_t use_ess;
+  int32_t vdi_band_rows, vdi_band_world, vdi_rows_per_rank;
+  int32_t band_rows, band_stride, band_offset;  /* output-row sharding */
+} VdiRenderArgs;
+
+const char* vdi_last_error(void);
+int vdi_abi_version(void);
+
+size_t vdi_gen_workspace_bytes(const VdiGenArgs* args);
+int vdi_gen_launch(const VdiGenArgs* args, vdi_stream_t stream);
+int vdi_grid_launch(const VdiGridArgs* args, vdi_stream_t stream);
+int vdi_render_launch(const VdiRenderArgs* args, vdi_stream_t stream);
+
+/* Alg. 2 search over a batch of independent queries (raycast.py:79-156).
+ * fronts/backs: (n_queries, n_max) f32, counts: (n_queries,), d_entry /
+ * d_exit: f64, seeds: p. out_index = -1 for a miss. */
+int vdi_find_first_batch(const float* fronts, const float* backs,
+                         const int32_t* counts, int32_t n_max,
+                         const double* d_entry, const double* d_exit,
+                         const int32_t* seeds, int32_t* out_index,
+                         int32_t* out_seed, int64_t n_queries,
+                         vdi_stream_t stream);
+
+/* Layout conversion for n_lists lists of n_sg supersegments. */
+int vdi_segs_to_aos(const float* soa, float* aos, int64_t n_lists,
+                    int32_t n_sg, vdi_stream_t stream);
+int vdi_segs_from_aos(const float* aos, float* soa, int64_t n_lists,
+                      int32_t n_sg, vdi_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VDI_B200_H */

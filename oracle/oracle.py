@@ -1,0 +1,151 @@
+"""ctypes front end of the CPU oracle (TEST INFRASTRUCTURE ONLY).
+
+The oracle restates the reference's numba kernels in C (vdi_oracle.c, which
+cites generate.py / raycast.py line by line). Only tests/, __graft_entry__.smoke()
+and bench.py's CPU-baseline leg import this module; the product package never
+does. Array conventions are the reference's: segs (H, W, n_sg, 6) f32 AoS,
+image (h, w, 4) f64, grid (gz, gy, gx) u32.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "libvdi_oracle.so")
+_lib = None
+
+_f32 = np.ctypeslib.ndpointer(np.float32, flags="C_CONTIGUOUS")
+_f64 = np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS")
+_i32 = np.ctypeslib.ndpointer(np.int32, flags="C_CONTIGUOUS")
+_i64 = np.ctypeslib.ndpointer(np.int64, flags="C_CONTIGUOUS")
+_u32 = np.ctypeslib.ndpointer(np.uint32, flags="C_CONTIGUOUS")
+_vp = ctypes.c_void_p
+_int = ctypes.c_int
+_dbl = ctypes.c_double
+
+
+def build(force: bool = False) -> str:
+    """Compile libvdi_oracle.so with the committed Makefile."""
+    src = os.path.join(_HERE, "vdi_oracle.c")
+    if force or not os.path.exists(_LIB_PATH) or \
+            os.path.getmtime(_LIB_PATH) < os.path.getmtime(src):
+        subprocess.run(["make", "-s", "-C", _HERE], check=True)
+    return _LIB_PATH
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        L = ctypes.CDLL(_LIB_PATH)
+        L.vdio_generate.argtypes = [
+            _f32, _int, _int, _int, _f32, _int, _f64, _f64, _f64, _f64,
+            _int, _int, _int, _int, _dbl, _dbl, _dbl, _dbl,
+            _vp, _int, _int, _i32, _f32, _f64, _i32, _i64]
+        L.vdio_accumulate_grid.argtypes = [
+            _i32, _f32, _int, _int, _int, _int, _int, _int,
+            _dbl, _dbl, _dbl, _dbl, _u32]
+        L.vdio_render.argtypes = [
+            _f32, _i32, _int, _int, _int, _f64, _f64, _f64, _f64, _f64,
+            _int, _int, _int, _u32, _int, _int, _int,
+            _dbl, _dbl, _dbl, _dbl, _dbl, _f64,
+            _vp, _int, _int, _f64, _i64, _i64, _i64]
+        L.vdio_find_first.argtypes = [_f32, _f32, ctypes.c_int64, _dbl, _dbl,
+                                      ctypes.c_int64,
+                                      ctypes.POINTER(ctypes.c_int64)]
+        L.vdio_find_first.restype = ctypes.c_int64
+        L.vdio_max_threads.restype = _int
+        _lib = L
+    return _lib
+
+
+def max_threads() -> int:
+    return int(lib().vdio_max_threads())
+
+
+def _m(a):
+    return np.ascontiguousarray(np.asarray(a, dtype=np.float64).reshape(-1))
+
+
+def _rows(rows):
+    if rows is None:
+        return None, 0, None
+    r = np.ascontiguousarray(rows, dtype=np.int32)
+    return r.ctypes.data_as(ctypes.c_void_p), len(r), r
+
+
+def generate(vol_norm, lut, pv, inv_pv, eye, aabb, width, height, n_sg, delta,
+             eps, gamma_init, step, lref, rows=None, threads=0):
+    """_generate_kernel (generate.py:276-319) + executed-sample counter.
+
+    vol_norm is the f32 (nz, ny, nx) array R samples (Volume.normalized)."""
+    vol = np.ascontiguousarray(vol_norm, dtype=np.float32)
+    nz, ny, nx = vol.shape
+    lut = np.ascontiguousarray(lut, dtype=np.float32)
+    counts = np.zeros((height, width), np.int32)
+    segs = np.zeros((height, width, n_sg, 6), np.float32)
+    gammas = np.zeros((height, width), np.float64)
+    passes = np.zeros((height, width), np.int32)
+    samples = np.zeros((height, width), np.int64)
+    rp, nr, _keep = _rows(rows)
+    lib().vdio_generate(vol, nx, ny, nz, lut, lut.shape[0], _m(pv), _m(inv_pv),
+                        _m(eye), _m(aabb), width, height, n_sg, delta,
+                        float(eps), float(gamma_init), float(step), float(lref),
+                        rp, nr, threads, counts, segs, gammas, passes, samples)
+    return dict(counts=counts, segs=segs, gammas=gammas, passes=passes,
+                samples=samples)
+
+
+def accumulate_grid(counts, segs, dims, near, far, proj_a, proj_b):
+    """_accumulate_grid (generate.py:322-346)."""
+    gx, gy, gz = dims
+    height, width, n_sg, _ = segs.shape
+    g = np.zeros((gz, gy, gx), np.uint32)
+    lib().vdio_accumulate_grid(np.ascontiguousarray(counts, np.int32),
+                               np.ascontiguousarray(segs, np.float32),
+                               width, height, n_sg, gx, gy, gz, float(near),
+                               float(far), float(proj_a), float(proj_b), g)
+    return g
+
+
+def depth_consts(near, far):
+    """generate.py:349-354 / raycast.py:471-472."""
+    return (far + near) / (far - near), 2.0 * far * near / (far - near)
+
+
+def render(segs, counts, gen_pv, gen_inv_pv, aabb, new_inv_pv, eye, out_w,
+           out_h, grid, near, far, use_ess=True, early_term=0.999,
+           bg=(0.0, 0.0, 0.0, 1.0), rows=None, threads=0):
+    """_render_kernel (raycast.py:275-456) with per-pixel counters."""
+    segs = np.ascontiguousarray(segs, np.float32)
+    vdi_h, vdi_w, n_sg, _ = segs.shape
+    grid = np.ascontiguousarray(grid, np.uint32)
+    gz, gy, gx = grid.shape
+    pa, pb = depth_consts(near, far)
+    img = np.zeros((out_h, out_w, 4), np.float64)
+    lv = np.zeros((out_h, out_w), np.int64)
+    si = np.zeros((out_h, out_w), np.int64)
+    ls = np.zeros((out_h, out_w), np.int64)
+    rp, nr, _keep = _rows(rows)
+    lib().vdio_render(segs, np.ascontiguousarray(counts, np.int32), vdi_w,
+                      vdi_h, n_sg, _m(gen_pv), _m(gen_inv_pv), _m(aabb),
+                      _m(new_inv_pv), _m(eye), out_w, out_h, int(bool(use_ess)),
+                      grid, gx, gy, gz, float(near), float(far), pa, pb,
+                      float(early_term), _m(bg), rp, nr, threads, img, lv, si, ls)
+    return dict(image=img, lists_visited=lv, segs_intersected=si,
+                lists_searched=ls)
+
+
+def find_first(fronts, backs, count, d_entry, d_exit, p):
+    """_find_first (raycast.py:79-141): returns (index or -1, seed)."""
+    fr = np.ascontiguousarray(fronts, np.float32)
+    bk = np.ascontiguousarray(backs, np.float32)
+    seed = ctypes.c_int64(0)
+    idx = lib().vdio_find_first(fr, bk, int(count), float(d_entry),
+                                float(d_exit), int(p), ctypes.byref(seed))
+    return int(idx), int(seed.value)

@@ -1,0 +1,348 @@
+"""Generate the golden parity fixtures from the REFERENCE itself.
+
+Run in the build container (where /root/reference exists):
+
+    python tests/golden/make_golden.py
+
+It imports vdikit from /root/reference/pkg/src (numba JIT, writable
+NUMBA_CACHE_DIR), runs R's own kernels on small deterministic scenes and writes
+tests/golden/<case>.npz. Nothing at test time reads /root/reference: the
+fixtures are the committed record of R's outputs.
+
+Counters R does not expose (executed samples per ray, lists searched per
+pixel) come from instrumented copies of generate.py / raycast.py built at run
+time from R's source text: one counter line is inserted, everything else is
+verbatim, and the instrumented outputs are asserted identical to R's.
+"""
+
+from __future__ import annotations
+
+import math
+import os
+import re
+import sys
+import types
+
+import numpy as np
+
+REF = "/root/reference/pkg/src"
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache_golden")
+sys.path.insert(0, REF)
+sys.path.insert(0, ROOT)
+
+import vdikit as vk  # noqa: E402
+from vdikit import generate as rgen  # noqa: E402
+from vdikit import raycast as rray  # noqa: E402
+
+from paper_2206_08660_b200 import synth  # noqa: E402
+
+
+# ------------------------------------------------------------ instrumentation
+
+def _load_instrumented(modname, path, edits):
+    src = open(path).read()
+    src = src.replace("from ._geom", "from vdikit._geom")
+    src = src.replace("from .camera", "from vdikit.camera")
+    src = src.replace("from .vdi", "from vdikit.vdi")
+    src = src.replace("from .volume", "from vdikit.volume")
+    src = src.replace("from .image", "from vdikit.image")
+    src = src.replace("cache=True", "cache=False")
+    for old, new, count in edits:
+        n = src.count(old)
+        assert n == count, (modname, old, n)
+        src = src.replace(old, new)
+    mod = types.ModuleType(modname)
+    mod.__file__ = path
+    sys.modules[modname] = mod
+    exec(compile(src, path, "exec"), mod.__dict__)
+    return mod
+
+
+def instrumented_generate():
+    path = os.path.join(REF, "vdikit/generate.py")
+    return _load_instrumented("gen_instr", path, [
+        ("capped, out_seg, tseg):", "capped, out_seg, tseg, ctr):", 1),
+        ("        if tb <= ta:\n            break\n",
+         "        if tb <= ta:\n            break\n        ctr[0] += 1\n", 1),
+        ("True, out_seg, tseg)", "True, out_seg, tseg, ctr)", 1),
+        ("False, out_seg, tseg)", "False, out_seg, tseg, ctr)", 1),
+        ("out_seg, tseg, high_seg):", "out_seg, tseg, high_seg, ctr):", 1),
+        ("                                   out_seg, tseg, high_seg)",
+         "                                   out_seg, tseg, high_seg, ctr[idx:idx + 1])", 1),
+        ("counts, segs, gammas, passes):", "counts, segs, gammas, passes, ctr):", 1),
+    ])
+
+
+def instrumented_render():
+    path = os.path.join(REF, "vdikit/raycast.py")
+    return _load_instrumented("ray_instr", path, [
+        ("early_term, bg, img, lists_vis, segs_int):",
+         "early_term, bg, img, lists_vis, segs_int, srch):", 1),
+        ("                if search:\n                    fronts",
+         "                if search:\n                    srch[row, col] += 1\n"
+         "                    fronts", 1),
+    ])
+
+
+GI = instrumented_generate()
+RI = instrumented_render()
+
+
+# ---------------------------------------------------------------- helpers
+
+def r_volume(vol):
+    """R Volume holding exactly the samples our Volume holds."""
+    if vol.voxel_type == "f32":
+        arr = np.ascontiguousarray(vol.data, np.float32)
+        return vk.Volume(dims=vol.dims, voxel_type="u8", spacing=vol.spacing,
+                         data=arr, value_range=vol.value_range, normalized=arr)
+    return vk.make_volume(vol.data, vol.voxel_type, vol.spacing)
+
+
+def r_camera(cam):
+    return vk.Camera(position=tuple(float(v) for v in cam.position),
+                     orientation=tuple(float(v) for v in cam.orientation),
+                     fov_y=float(cam.fov_y), near=float(cam.near),
+                     far=float(cam.far), viewport=tuple(int(v) for v in cam.viewport))
+
+
+def cam_record(prefix, rcam):
+    return {
+        f"{prefix}_pose": np.array([*rcam.position, *rcam.orientation, rcam.fov_y,
+                                    rcam.near, rcam.far], np.float64),
+        f"{prefix}_viewport": np.array(rcam.viewport, np.int64),
+        f"{prefix}_pv": rcam.proj_view(),
+        f"{prefix}_inv_pv": rcam.inv_proj_view(),
+    }
+
+
+def pack_segs(counts, segs):
+    """Valid supersegments only, in list order (the VDI1 packing)."""
+    h, w = counts.shape
+    mask = np.arange(segs.shape[2])[None, None, :] < counts[:, :, None]
+    return segs[mask]
+
+
+def run_generate(rvol, rtf, rcam, params):
+    delta, step, lref = params.resolve(rvol)
+    w, h = rcam.viewport
+    counts = np.zeros((h, w), np.int32)
+    segs = np.zeros((h, w, params.n_sg, 6), np.float32)
+    gammas = np.zeros((h, w), np.float64)
+    passes = np.zeros((h, w), np.int32)
+    ctr = np.zeros(h * w, np.int64)
+    aabb = rvol.aabb
+    GI._generate_kernel(rvol.normalized, rtf.lut, rcam.proj_view(), rcam.inv_proj_view(),
+                        *np.asarray(rcam.position, dtype=np.float64),
+                        *aabb[0], *aabb[1], w, h, params.n_sg, delta, params.epsilon,
+                        params.gamma_init, step, lref, counts, segs, gammas, passes, ctr)
+    vdi, grid, st = vk.generate_vdi(rvol, rtf, rcam, params, with_stats=True)
+    assert np.array_equal(vdi.counts, counts)
+    assert np.array_equal(vdi.segs.view(np.uint32), segs.view(np.uint32))
+    assert np.array_equal(st.gammas, gammas) and np.array_equal(st.passes, passes)
+    return vdi, grid, st, ctr.reshape(h, w), (delta, step, lref)
+
+
+def run_render(vdi, grid, rcam_new, opts):
+    out_w, out_h = rcam_new.viewport
+    img = np.zeros((out_h, out_w, 4), np.float64)
+    lv = np.zeros((out_h, out_w), np.int64)
+    si = np.zeros((out_h, out_w), np.int64)
+    srch = np.zeros((out_h, out_w), np.int64)
+    gen = vdi.gen_camera
+    gx, gy, gz = grid.dims
+    n, f = gen.near, gen.far
+    pa = (f + n) / (f - n)
+    pb = 2.0 * f * n / (f - n)
+    RI._render_kernel(vdi.segs, vdi.counts, vdi.width, vdi.height, gen.proj_view(),
+                      gen.inv_proj_view(), *vdi.volume_aabb[0], *vdi.volume_aabb[1],
+                      rcam_new.inv_proj_view(),
+                      *np.asarray(rcam_new.position, dtype=np.float64), out_w, out_h,
+                      opts.use_ess, grid.counts, gx, gy, gz, grid.near, grid.far, pa, pb,
+                      opts.early_term_alpha, np.asarray(opts.background, np.float64),
+                      img, lv, si, srch)
+    ref_img, st = vk.render_vdi(vdi, grid, rcam_new, opts, with_stats=True)
+    assert np.array_equal(ref_img.data.view(np.uint64), img.view(np.uint64))
+    assert st.lists_visited == lv.sum() and st.supersegments_intersected == si.sum()
+    return img, lv, si, srch
+
+
+def render_record(tag, rcam, opts, res):
+    img, lv, si, srch = res
+    rec = cam_record(tag, rcam)
+    rec.update({
+        f"{tag}_opts": np.array([float(opts.use_ess), opts.early_term_alpha,
+                                 *opts.background], np.float64),
+        f"{tag}_image": img, f"{tag}_lists_visited": lv.astype(np.int32),
+        f"{tag}_segs_intersected": si.astype(np.int32),
+        f"{tag}_lists_searched": srch.astype(np.int32),
+    })
+    return rec
+
+
+def save(name, rec):
+    path = os.path.join(HERE, f"{name}.npz")
+    np.savez_compressed(path, **rec)
+    print(f"wrote {path} ({os.path.getsize(path) / 1024:.0f} KiB)")
+
+
+def volume_case(name, vol, tf, gen_cam, render_specs, n_sg, delta=None, eps=1e-6,
+                volume_from=None):
+    rvol, rtf, rgc = r_volume(vol), vk.TransferFunction(tf.control_points), r_camera(gen_cam)
+    assert np.array_equal(rtf.lut, tf.lut)
+    params = vk.GenParams(n_sg=n_sg, delta=delta, epsilon=eps)
+    vdi, grid, st, ctr, (dl, step, lref) = run_generate(rvol, rtf, rgc, params)
+    rec = {
+        "voxel_type": np.array(vol.voxel_type),
+        "volume": vol.data if volume_from is None else np.zeros(0, vol.data.dtype),
+        "volume_from": np.array(volume_from or ""),
+        "volume_shape": np.array(vol.data.shape, np.int64),
+        "spacing": np.array(vol.spacing, np.float64), "aabb": rvol.aabb,
+        "lut": rtf.lut, "tf_points": np.array(tf.control_points, np.float64),
+        "n_sg": np.array(n_sg), "delta": np.array(dl), "eps": np.array(params.epsilon),
+        "gamma_init": np.array(params.gamma_init), "step": np.array(step),
+        "lref": np.array(lref),
+        "counts": vdi.counts, "segs_packed": pack_segs(vdi.counts, vdi.segs),
+        "gammas": st.gammas, "passes": st.passes, "samples": ctr.astype(np.int32),
+        "grid": grid.counts, "grid_dims": np.array(grid.dims, np.int64),
+    }
+    rec.update(cam_record("gen", rgc))
+    for i, (cam, opts) in enumerate(render_specs):
+        rc = r_camera(cam)
+        rec.update(render_record(f"r{i}", rc, opts, run_render(vdi, grid, rc, opts)))
+    rec["n_renders"] = np.array(len(render_specs))
+    hist = np.bincount(st.passes.ravel(), minlength=23)
+    print(f"{name}: hit rays {int((st.passes > 0).sum())}, passes hist {hist.tolist()}, "
+          f"samples {int(ctr.sum())}, segs {int(vdi.counts.sum())}")
+    save(name, rec)
+
+
+def random_vdi_case(name, seeds):
+    """The reference's A2 scenario (test_acceptance.py:104-119, conftest.py:92-125):
+    invariant-respecting random VDIs rendered from random orbit views."""
+    sys.path.insert(0, "/root/reference/pkg/tests")
+    from conftest import random_vdi  # noqa: E402
+    rec = {"seeds": np.array(seeds)}
+    for s in seeds:
+        rng = np.random.default_rng(s)
+        vdi, grid = random_vdi(rng, width=32, height=32, n_sg=8)
+        az = float(rng.uniform(0, 360))
+        el = float(rng.uniform(-60, 60))
+        cam = vk.orbit_camera((0.0, 0.0, 2.5), float(rng.uniform(3.0, 6.0)), az, el,
+                              fov_y=0.8, near=0.3, far=25.0, viewport=(32, 32))
+        t = f"s{s}"
+        rec[f"{t}_counts"] = vdi.counts
+        rec[f"{t}_segs"] = vdi.segs
+        rec[f"{t}_grid"] = grid.counts
+        rec[f"{t}_aabb"] = vdi.volume_aabb
+        rec.update(cam_record(f"{t}_gen", vdi.gen_camera))
+        for j, opts in enumerate((vk.RenderOptions(use_ess=True),
+                                  vk.RenderOptions(use_ess=False),
+                                  vk.RenderOptions(early_term_alpha=0.5,
+                                                   background=(0.2, 0.3, 0.4, 0.7)))):
+            rec.update(render_record(f"{t}_r{j}", cam, opts,
+                                     run_render(vdi, grid, cam, opts)))
+    save(name, rec)
+
+
+def search_case(name, n_cases=20000):
+    """find_first_supersegment vectors on a quantised grid that forces exact
+    ties (test_acceptance.py:78-101) plus uniform queries."""
+    rng = np.random.default_rng(1)
+    grid = np.linspace(-1.0, 1.0, 17)
+    n_max = 8
+    fr = np.zeros((n_cases, n_max), np.float32)
+    bk = np.zeros((n_cases, n_max), np.float32)
+    cnt = np.zeros(n_cases, np.int32)
+    de = np.zeros(n_cases, np.float64)
+    dx = np.zeros(n_cases, np.float64)
+    pp = np.zeros(n_cases, np.int32)
+    oi = np.zeros(n_cases, np.int32)
+    os_ = np.zeros(n_cases, np.int32)
+    i = 0
+    while i < n_cases:
+        n = int(rng.integers(1, n_max + 1))
+        vals = np.sort(rng.choice(grid, size=2 * n))
+        if any(vals[2 * j] >= vals[2 * j + 1] for j in range(n)):
+            continue
+        segs = np.zeros((n, 6), np.float32)
+        segs[:, 0] = vals[0::2]
+        segs[:, 1] = vals[1::2]
+        segs[:, 5] = 0.5
+        for _ in range(min(25, n_cases - i)):
+            if rng.random() < 0.5:
+                d1, d2 = rng.choice(grid, size=2)
+            else:
+                d1, d2 = rng.uniform(-1.1, 1.1, size=2)
+            p = int(rng.integers(-1, n + 1))
+            idx, seed = vk.find_first_supersegment(segs, d1, d2, p=p)
+            fr[i, :n] = segs[:, 0]
+            bk[i, :n] = segs[:, 1]
+            cnt[i], de[i], dx[i], pp[i] = n, d1, d2, p
+            oi[i] = -1 if idx is None else idx
+            os_[i] = seed
+            i += 1
+    save(name, dict(fronts=fr, backs=bk, counts=cnt, d_entry=de, d_exit=dx,
+                    seeds=pp, index=oi, seed_out=os_))
+
+
+def main():
+    deg = math.radians
+    RO = vk.RenderOptions
+    # C1: the BASELINE config the CPU reference runs (blobs 64^3 f32, 128^2, n_sg 20)
+    vol, tf, gcam, rcam, n_sg = synth.config("C1")
+    c_el = synth.sweep_camera(vol, 25.0, (128, 128), elevation_deg=10.0)
+    c_big = synth.sweep_camera(vol, 30.0, (160, 96))
+    volume_case("c1_blobs64", vol, tf, gcam,
+                [(rcam, RO()), (rcam, RO(use_ess=False)), (gcam, RO()),
+                 (c_el, RO()), (c_big, RO(early_term_alpha=1.0))], n_sg)
+
+    # R's own sphere fixture (conftest.py:33-39): u8 sphere 64^3, 128^2, n_sg 12
+    sph = synth.preset_volume("sphere", 64)
+    stf = synth.preset_tf("sphere")
+    scam = synth.sweep_camera(sph, 0.0, (128, 128))
+    center = (32.0, 32.0, 32.0)
+    radius = float(np.linalg.norm(np.asarray(scam.position) - 32.0))
+    from paper_2206_08660_b200.camera import orbit_camera
+    s25 = orbit_camera(center, radius, 25.0, 10.0, fov_y=scam.fov_y, near=scam.near,
+                       far=scam.far, viewport=scam.viewport)
+    s30 = orbit_camera(center, radius, 30.0, 0.0, fov_y=scam.fov_y, near=scam.near,
+                       far=scam.far, viewport=scam.viewport)
+    volume_case("sphere64_u8", sph, stf, scam,
+                [(scam, RO()), (s25, RO(use_ess=True)), (s25, RO(use_ess=False)),
+                 (scam, RO(early_term_alpha=0.1)), (s30, RO())], 12)
+
+    # bands at a tight budget: exercises aborted counting passes, epsilon
+    # exits with the cached high segments, and capped passes
+    bands = synth.preset_volume("bands", 64)
+    bu16 = synth.make_volume(bands.data.astype(np.uint16) * 257 + 3, "u16")
+    btf = synth.preset_tf("bands")
+    bcam = synth.sweep_camera(bands, 20.0, (64, 64), elevation_deg=35.0)
+    bview = synth.sweep_camera(bands, 50.0, (64, 64), elevation_deg=-20.0)
+    volume_case("bands64_u16_nsg4", bu16, btf, bcam, [(bview, RO()), (bcam, RO())], 4,
+                delta=1)
+    volume_case("blobs64_nsg3", vol, tf, synth.sweep_camera(vol, 40.0, (48, 48)),
+                [(synth.sweep_camera(vol, 70.0, (48, 48)), RO())], 3, delta=1,
+                volume_from="c1_blobs64")
+    # coarse epsilon + zero slack: most multi-pass rays leave through the
+    # epsilon test and return the cached high-gamma segments
+    volume_case("blobs64_eps", vol, tf, synth.sweep_camera(vol, 10.0, (40, 40)),
+                [(synth.sweep_camera(vol, 35.0, (40, 40)), RO())], 5, delta=0,
+                eps=0.02, volume_from="c1_blobs64")
+    # more separated opaque layers than the budget: count > n_sg for every
+    # gamma, so the bisection ends in the capped pass (generate.py:248-252)
+    z = np.arange(32)[:, None, None]
+    stripes = np.broadcast_to(np.where(z % 6 < 3, 200, 0), (32, 32, 32)).astype(np.uint8)
+    svol = synth.make_volume(stripes, "u8")
+    volume_case("stripes32_capped", svol, synth.preset_tf("sphere"),
+                synth.sweep_camera(svol, 0.0, (24, 24), elevation_deg=80.0),
+                [(synth.sweep_camera(svol, 30.0, (24, 24), elevation_deg=60.0), RO())], 3)
+
+    random_vdi_case("random_vdi", [0, 1, 2, 3, 4, 5])
+    search_case("search_fuzz")
+
+
+if __name__ == "__main__":
+    main()

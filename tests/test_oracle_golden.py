@@ -1,0 +1,91 @@
+"""Pin the CPU oracle (oracle/vdi_oracle.c) to the reference's own outputs.
+
+Every fixture in tests/golden/ was produced by the reference (vdikit) itself;
+the oracle must reproduce it bit for bit before it is trusted as the checker
+of the B200 path.
+"""
+
+import numpy as np
+import pytest
+
+import golden_io as gio
+from oracle import oracle
+
+
+@pytest.mark.parametrize("case", gio.VOLUME_CASES)
+def test_generate_bit_exact(case):
+    g = gio.load(case)
+    out = oracle.generate(gio.normalized(g), g["lut"], **gio.gen_inputs(g))
+    assert np.array_equal(out["counts"], g["counts"])
+    assert np.array_equal(out["segs"].view(np.uint32), gio.expected_segs(g).view(np.uint32))
+    assert np.array_equal(out["gammas"].view(np.uint64), g["gammas"].view(np.uint64))
+    assert np.array_equal(out["passes"], g["passes"])
+    assert np.array_equal(out["samples"], g["samples"])
+
+
+@pytest.mark.parametrize("case", gio.VOLUME_CASES)
+def test_grid_bit_exact(case):
+    g = gio.load(case)
+    gc = gio.camera(g, "gen")
+    pa, pb = oracle.depth_consts(gc.near, gc.far)
+    grid = oracle.accumulate_grid(g["counts"], gio.expected_segs(g),
+                                  tuple(g["grid_dims"]), gc.near, gc.far, pa, pb)
+    assert np.array_equal(grid, g["grid"])
+
+
+@pytest.mark.parametrize("case", gio.VOLUME_CASES)
+def test_render_bit_exact(case):
+    g = gio.load(case)
+    gc = gio.camera(g, "gen")
+    segs = gio.expected_segs(g)
+    for spec in gio.render_specs(g):
+        t = spec["tag"]
+        out = oracle.render(segs, g["counts"], g["gen_pv"], g["gen_inv_pv"], g["aabb"],
+                            spec["inv_pv"], spec["eye"], *spec["viewport"], g["grid"],
+                            gc.near, gc.far, spec["use_ess"], spec["early_term"],
+                            spec["bg"])
+        assert np.array_equal(out["image"].view(np.uint64), g[f"{t}_image"].view(np.uint64)), t
+        assert np.array_equal(out["lists_visited"], g[f"{t}_lists_visited"]), t
+        assert np.array_equal(out["segs_intersected"], g[f"{t}_segs_intersected"]), t
+        assert np.array_equal(out["lists_searched"], g[f"{t}_lists_searched"]), t
+
+
+def test_render_random_vdis_bit_exact():
+    g = gio.load("random_vdi")
+    for s in g["seeds"]:
+        t = f"s{s}"
+        pose = g[f"{t}_gen_pose"]
+        near, far = pose[8], pose[9]
+        for j in range(3):
+            r = f"{t}_r{j}"
+            o = g[f"{r}_opts"]
+            vp = g[f"{r}_viewport"]
+            out = oracle.render(g[f"{t}_segs"], g[f"{t}_counts"], g[f"{t}_gen_pv"],
+                                g[f"{t}_gen_inv_pv"], g[f"{t}_aabb"], g[f"{r}_inv_pv"],
+                                g[f"{r}_pose"][:3], int(vp[0]), int(vp[1]), g[f"{t}_grid"],
+                                near, far, bool(o[0]), float(o[1]), o[2:6])
+            assert np.array_equal(out["image"].view(np.uint64),
+                                  g[f"{r}_image"].view(np.uint64)), r
+            assert np.array_equal(out["lists_visited"], g[f"{r}_lists_visited"]), r
+            assert np.array_equal(out["segs_intersected"], g[f"{r}_segs_intersected"]), r
+
+
+def test_search_fuzz_matches_reference():
+    g = gio.load("search_fuzz")
+    for i in range(len(g["counts"])):
+        idx, seed = oracle.find_first(g["fronts"][i], g["backs"][i], g["counts"][i],
+                                      g["d_entry"][i], g["d_exit"][i], g["seeds"][i])
+        assert idx == g["index"][i], i
+        assert seed == g["seed_out"][i], i
+
+
+def test_camera_matrices_bit_exact():
+    """Our host Camera yields R's exact proj_view / inv_proj_view bits."""
+    for case in gio.VOLUME_CASES:
+        g = gio.load(case)
+        tags = ["gen"] + [s["tag"] for s in gio.render_specs(g)]
+        for t in tags:
+            cam = gio.camera(g, t)
+            assert np.array_equal(cam.proj_view().view(np.uint64), g[f"{t}_pv"].view(np.uint64))
+            assert np.array_equal(cam.inv_proj_view().view(np.uint64),
+                                  g[f"{t}_inv_pv"].view(np.uint64))
