@@ -1,0 +1,345 @@
+"""Benchmark: VDI generation + novel-view VDI rendering on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3]
+    python bench.py --impl reference ...      # CPU reference arm (oracle port)
+
+Workload (BASELINE.json configs[2], the 1920x1080 config the metric is quoted
+on): Kingsnake-shaped 1024x1024x795 u8 volume, 1920x1080 generation viewport,
+n_sg 20, generate at azimuth 0 and render a novel view at 15 deg. One step =
+one generate_vdi (generation + AccelGrid) + one render_vdi of that VDI; the
+rays of a step are the 1920x1080 generation rays plus the 1920x1080 render
+rays. Multi-GPU: interleaved 16-row bands of both viewports per rank, NCCL
+all-reduce of the grid + all-gather of the VDI between the two passes and an
+all-gather of the image rows at the end. The frame is fixed as N grows, so
+scaling is "strong".
+
+One JSON line on rank 0 (see the driver contract in the task statement).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "VDI gen & render Mrays/s (fps @1920×1080) at 1/2/4/8 B200; % HBM roofline"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    p.add_argument("--config", default="C3")
+    p.add_argument("--cpu-seconds", type=float, default=12.0,
+                   help="target CPU time of the bounded cpu_baseline sample")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--e2e-steps", type=int, default=3)
+    return p.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ------------------------------------------------------------------ clocks
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        with open(self.path) as f:
+            for line in f:
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) < 9:
+                    continue
+                try:
+                    sm.append(float(parts[1]))
+                    smax.append(float(parts[2]))
+                except ValueError:
+                    continue
+                for n, v in zip(names, parts[5:9]):
+                    if v.lower().startswith("active"):
+                        reasons.add(n)
+        os.unlink(self.path)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": float(max(smax)) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- workload
+
+def workload(name):
+    from paper_2206_08660_b200 import synth
+    vol, tf, gcam, rcam, n_sg = synth.config(name)
+    return vol, tf, gcam, rcam, n_sg
+
+
+def sample_rows(height, nrows):
+    nrows = max(1, min(height, nrows))
+    return np.unique(np.linspace(0, height - 1, nrows).round().astype(np.int64))
+
+
+def cpu_time_sample(vol, tf, gcam, rcam, n_sg, vdi_counts, vdi_segs, grid, rows, threads):
+    """Oracle (C port of the reference kernels) on `rows` of both passes."""
+    from oracle import oracle
+    from paper_2206_08660_b200.generate import GenParams
+    params = GenParams(n_sg=n_sg)
+    delta, step, lref = params.resolve(vol)
+    w, h = gcam.viewport
+    norm = vol.normalized
+    t0 = time.perf_counter()
+    oracle.generate(norm, tf.lut, gcam.proj_view(), gcam.inv_proj_view(),
+                    np.asarray(gcam.position), vol.aabb, w, h, n_sg, delta, params.epsilon,
+                    params.gamma_init, step, lref, rows=rows, threads=threads)
+    t1 = time.perf_counter()
+    oracle.render(vdi_segs, vdi_counts, gcam.proj_view(), gcam.inv_proj_view(), vol.aabb,
+                  rcam.inv_proj_view(), np.asarray(rcam.position), *rcam.viewport, grid,
+                  gcam.near, gcam.far, rows=rows, threads=threads)
+    t2 = time.perf_counter()
+    return t1 - t0, t2 - t1
+
+
+def calibrated_rows(vol, tf, gcam, rcam, n_sg, counts, segs, grid, threads, seconds, height):
+    probe = sample_rows(height, 8)
+    tg, tr = cpu_time_sample(vol, tf, gcam, rcam, n_sg, counts, segs, grid, probe, threads)
+    per_row = (tg + tr) / len(probe)
+    return sample_rows(height, int(seconds / max(per_row, 1e-6)))
+
+
+# ---------------------------------------------------------------- reference
+
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    from oracle import oracle
+    vol, tf, gcam, rcam, n_sg = workload(args.config)
+    w, h = gcam.viewport
+    threads = os.cpu_count() or 1
+    from paper_2206_08660_b200.generate import GenParams
+    params = GenParams(n_sg=n_sg)
+    delta, step, lref = params.resolve(vol)
+    # untimed setup: the full VDI the sampled render rows traverse
+    ref = oracle.generate(vol.normalized, tf.lut, gcam.proj_view(), gcam.inv_proj_view(),
+                          np.asarray(gcam.position), vol.aabb, w, h, n_sg, delta,
+                          params.epsilon, params.gamma_init, step, lref, threads=threads)
+    from paper_2206_08660_b200.vdi import default_grid_dims
+    pa, pb = oracle.depth_consts(gcam.near, gcam.far)
+    grid = oracle.accumulate_grid(ref["counts"], ref["segs"], default_grid_dims(w, h),
+                                  gcam.near, gcam.far, pa, pb)
+    budget = max(2.0, 150.0 / max(1, args.steps + args.warmup))
+    rows = calibrated_rows(vol, tf, gcam, rcam, n_sg, ref["counts"], ref["segs"], grid, threads,
+                           budget, h)
+    times = []
+    for i in range(args.warmup + args.steps):
+        tg, tr = cpu_time_sample(vol, tf, gcam, rcam, n_sg, ref["counts"], ref["segs"], grid,
+                                 rows, threads)
+        if i >= args.warmup:
+            times.append(tg + tr)
+    rays = 2 * len(rows) * w
+    t = float(np.mean(times))
+    value = rays / t / 1e6
+    sample = f"{len(rows)} of {h} rows (every ~{h / len(rows):.1f}th) of both passes per step"
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "Mrays/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_dict(args, gcam, n_sg, "oracle port (C, OpenMP) of vdikit kernels"),
+        "cpu_baseline": {"value": value, "unit": "Mrays/s", "cores": threads, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": "Mrays/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def config_dict(args, gcam, n_sg, note=None):
+    w, h = gcam.viewport
+    d = {"workload": f"{args.config}: Kingsnake-shaped 1024x1024x795 u8, {w}x{h}, "
+                     f"n_sg {n_sg}, generate @0deg + render @15deg",
+         "rays_per_step": 2 * w * h, "viewport": [w, h], "n_sg": n_sg,
+         "parallelism": f"ray-band shard x{args.gpus}",
+         "l2": "256 MiB L2-flush write between timed steps; volume (795 MiB) > L2"}
+    if note:
+        d["note"] = note
+    return d
+
+
+# --------------------------------------------------------------------- B200
+
+def run_b200(args):
+    import torch
+    import torch.distributed as tdist
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2206_08660_b200 import device as dv
+    from paper_2206_08660_b200 import shard
+    from paper_2206_08660_b200.generate import GenParams
+
+    vol, tf, gcam, rcam, n_sg = workload(args.config)
+    params = GenParams(n_sg=n_sg)
+    w, h = gcam.viewport
+    pipe = shard.Pipeline(vol, tf, gcam, rcam, params, world=world, rank=rank)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device="cuda")
+
+    def barrier():
+        if world > 1:
+            tdist.barrier()
+
+    for _ in range(args.warmup):
+        pipe.step()
+    torch.cuda.synchronize()
+    S = pipe.samples_executed()            # this rank's executed samples (R semantics)
+    stats = pipe.render_stats()            # this rank's (L, K, L_s)
+
+    clocks = ClockSampler(local)
+    step_ms, gen_ms, grid_ms, coll_ms, ren_ms = [], [], [], [], []
+    clocks.start()
+    for _ in range(args.steps):
+        flush.fill_(1)
+        barrier()
+        torch.cuda.synchronize()
+        ev = pipe.step(timed=True)
+        torch.cuda.synchronize()
+        barrier()
+        step_ms.append(ev["step"])
+        gen_ms.append(ev["gen"])
+        grid_ms.append(ev["grid"])
+        coll_ms.append(ev["collective"])
+        ren_ms.append(ev["render"])
+    clk = clocks.stop()
+
+    total = torch.tensor([sum(step_ms)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        tdist.all_reduce(total, op=tdist.ReduceOp.MAX)
+    t_step = float(total.item()) / args.steps / 1e3          # seconds, max over ranks
+    rays = 2 * w * h
+    value = rays / t_step / 1e6
+
+    # ---- roofline of the dominant kernel (algorithmic bytes / event time)
+    gx, gy, gz = pipe.grid_dims
+    n_rays_local = pipe.local_gen_rays
+    b_gen = 32 * S + n_rays_local * (4 + 24 * n_sg) + 4 * gx * gy * gz
+    L, K, Ls = stats
+    b_ren = 4 * L + 8 * Ls + 24 * K + 32 * pipe.local_render_pixels
+    peak, peak_kind = peaks()
+    g_ms, r_ms = float(np.mean(gen_ms)), float(np.mean(ren_ms))
+    gen_gbs = b_gen / (g_ms * 1e-3) / 1e9
+    ren_gbs = b_ren / (r_ms * 1e-3) / 1e9
+    dominant = "vdi_gen" if g_ms >= r_ms else "vdi_render"
+    ach = gen_gbs if dominant == "vdi_gen" else ren_gbs
+    roof = {"kernel": dominant, "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
+            "frac": ach / peak, "peak_kind": peak_kind, "traffic": None,
+            "algorithmic_bytes": b_gen if dominant == "vdi_gen" else b_ren,
+            "gen": {"ms": g_ms, "bytes": b_gen, "GBps": gen_gbs, "frac": gen_gbs / peak,
+                    "samples": S, "Gsamples_per_s": S / (g_ms * 1e-3) / 1e9},
+            "render": {"ms": r_ms, "bytes": b_ren, "GBps": ren_gbs, "frac": ren_gbs / peak,
+                       "lists_visited": L, "segs_intersected": K, "lists_searched": Ls}}
+
+    # ---- end to end through the public API with host buffers
+    e2e = pipe.e2e(args.e2e_steps)
+
+    line = None
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "Mrays/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic", "config": config_dict(args, gcam, n_sg),
+            "fps": 1.0 / t_step,
+            "phases_ms": {"gen": g_ms, "grid": float(np.mean(grid_ms)),
+                          "collective": float(np.mean(coll_ms)), "render": r_ms},
+            "gen_mrays_s": w * h / (g_ms * 1e-3) / 1e6,
+            "render_mrays_s": w * h / (r_ms * 1e-3) / 1e6,
+            "roofline": roof, "e2e": e2e, "clocks": clk,
+            "gpu_launches": pipe.launches_per_step * args.steps,
+        }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = pipe_cpu_baseline(vol, tf, gcam, rcam, n_sg, pipe, args)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        tdist.barrier()
+        tdist.destroy_process_group()
+
+
+def pipe_cpu_baseline(vol, tf, gcam, rcam, n_sg, pipe, args):
+    threads = os.cpu_count() or 1
+    counts, segs, grid = pipe.host_vdi()
+    w, h = gcam.viewport
+    rows = calibrated_rows(vol, tf, gcam, rcam, n_sg, counts, segs, grid, threads,
+                           args.cpu_seconds, h)
+    tg, tr = cpu_time_sample(vol, tf, gcam, rcam, n_sg, counts, segs, grid, rows, threads)
+    rays = 2 * len(rows) * w
+    return {"value": rays / (tg + tr) / 1e6, "unit": "Mrays/s", "cores": threads,
+            "kind": "port",
+            "sample": f"{len(rows)} of {h} evenly spaced rows of both passes "
+                      f"(gen {tg:.2f} s + render {tr:.2f} s)"}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

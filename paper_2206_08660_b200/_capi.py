@@ -1,0 +1,103 @@
+"""ctypes binding of libvdi_b200.so (include/vdi_b200.h).
+
+The structures below mirror the header field for field. Loading fails loudly:
+there is no CPU fallback for the product path.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "lib", "libvdi_b200.so")
+
+VOXEL = {"u8": 0, "u16": 1, "f32": 2}
+_P = ctypes.c_void_p
+_D = ctypes.c_double
+_I = ctypes.c_int32
+
+
+class VdiGenArgs(ctypes.Structure):
+    _fields_ = [
+        ("volume", _P), ("lut", _P), ("counts", _P), ("segs", _P), ("gammas", _P),
+        ("passes", _P), ("samples", _P), ("workspace", _P),
+        ("pv", _D * 16), ("inv_pv", _D * 16), ("eye", _D * 3), ("aabb", _D * 6),
+        ("eps", _D), ("gamma_init", _D), ("step", _D), ("lref", _D),
+        ("voxel_type", _I), ("nx", _I), ("ny", _I), ("nz", _I), ("lut_n", _I),
+        ("width", _I), ("height", _I), ("n_sg", _I), ("delta", _I),
+        ("band_rows", _I), ("band_stride", _I), ("band_offset", _I),
+    ]
+
+
+class VdiGridArgs(ctypes.Structure):
+    _fields_ = [
+        ("segs", _P), ("counts", _P), ("grid", _P),
+        ("near", _D), ("far", _D), ("proj_a", _D), ("proj_b", _D),
+        ("width", _I), ("height", _I), ("n_sg", _I), ("gx", _I), ("gy", _I), ("gz", _I),
+        ("band_rows", _I), ("band_stride", _I), ("band_offset", _I), ("clear", _I),
+    ]
+
+
+class VdiRenderArgs(ctypes.Structure):
+    _fields_ = [
+        ("segs", _P), ("counts", _P), ("grid", _P), ("image", _P),
+        ("lists_visited", _P), ("segs_intersected", _P), ("lists_searched", _P),
+        ("stat_sums", _P),
+        ("gen_pv", _D * 16), ("gen_inv_pv", _D * 16), ("new_inv_pv", _D * 16),
+        ("eye", _D * 3), ("aabb", _D * 6), ("bg", _D * 4),
+        ("near", _D), ("far", _D), ("proj_a", _D), ("proj_b", _D), ("early_term", _D),
+        ("vdi_w", _I), ("vdi_h", _I), ("n_sg", _I), ("gx", _I), ("gy", _I), ("gz", _I),
+        ("out_w", _I), ("out_h", _I), ("use_ess", _I),
+        ("vdi_band_rows", _I), ("vdi_band_world", _I), ("vdi_rows_per_rank", _I),
+        ("band_rows", _I), ("band_stride", _I), ("band_offset", _I),
+    ]
+
+
+EXPORTS = ["vdi_last_error", "vdi_abi_version", "vdi_gen_workspace_bytes", "vdi_gen_launch",
+           "vdi_grid_launch", "vdi_render_launch", "vdi_find_first_batch",
+           "vdi_segs_to_aos", "vdi_segs_from_aos"]
+
+_lib = None
+
+
+class VdiError(RuntimeError):
+    pass
+
+
+def load():
+    """Load the built library (never builds, never falls back)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise VdiError(f"{LIB_PATH} is not built; run `python -m paper_2206_08660_b200.build` "
+                       "(there is no CPU fallback)")
+    L = ctypes.CDLL(LIB_PATH)
+    L.vdi_last_error.restype = ctypes.c_char_p
+    L.vdi_abi_version.restype = ctypes.c_int
+    L.vdi_gen_workspace_bytes.restype = ctypes.c_size_t
+    L.vdi_gen_workspace_bytes.argtypes = [ctypes.POINTER(VdiGenArgs)]
+    L.vdi_gen_launch.argtypes = [ctypes.POINTER(VdiGenArgs), _P]
+    L.vdi_grid_launch.argtypes = [ctypes.POINTER(VdiGridArgs), _P]
+    L.vdi_render_launch.argtypes = [ctypes.POINTER(VdiRenderArgs), _P]
+    L.vdi_find_first_batch.argtypes = [_P, _P, _P, _I, _P, _P, _P, _P, _P, ctypes.c_int64, _P]
+    L.vdi_segs_to_aos.argtypes = [_P, _P, ctypes.c_int64, _I, _P]
+    L.vdi_segs_from_aos.argtypes = [_P, _P, ctypes.c_int64, _I, _P]
+    for name in ("vdi_gen_launch", "vdi_grid_launch", "vdi_render_launch",
+                 "vdi_find_first_batch", "vdi_segs_to_aos", "vdi_segs_from_aos"):
+        getattr(L, name).restype = ctypes.c_int
+    if L.vdi_abi_version() != 1:
+        raise VdiError("libvdi_b200.so ABI mismatch")
+    _lib = L
+    return L
+
+
+def check(rc: int) -> None:
+    if rc != 0:
+        raise VdiError(f"vdi_b200 error {rc}: {load().vdi_last_error().decode()}")
+
+
+def fill(arr, values) -> None:
+    for i, v in enumerate(values):
+        arr[i] = float(v)

@@ -1,0 +1,93 @@
+// vdi_capi.cu -- the extern "C" entry points of include/vdi_b200.h:
+// argument validation (mirroring the reference's ValueErrors where the Python
+// layer has not already raised them), thread-local error text, dispatch.
+#include <cstdarg>
+#include <cstdio>
+
+#include "vdi_internal.h"
+
+namespace vdi {
+
+static thread_local char g_err[512] = "";
+
+int set_error(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+}  // namespace vdi
+
+using vdi::set_error;
+
+extern "C" {
+
+const char* vdi_last_error(void) { return vdi::g_err; }
+
+int vdi_abi_version(void) { return VDI_ABI_VERSION; }
+
+size_t vdi_gen_workspace_bytes(const VdiGenArgs*) { return 256; }
+
+int vdi_gen_launch(const VdiGenArgs* a, vdi_stream_t stream) {
+  if (!a) return set_error(VDI_EINVAL, "null args");
+  if (!a->volume || !a->lut || !a->counts || !a->segs || !a->workspace)
+    return set_error(VDI_EINVAL, "null device pointer");
+  if (a->nx < 2 || a->ny < 2 || a->nz < 2)
+    return set_error(VDI_EINVAL, "dims components must be >= 2 for trilinear sampling");
+  if (a->lut_n < 2 || a->lut_n > 4096) return set_error(VDI_EINVAL, "lut_n out of range");
+  if (a->width < 1 || a->height < 1) return set_error(VDI_EINVAL, "empty viewport");
+  if (a->n_sg < 1) return set_error(VDI_EINVAL, "n_sg must be >= 1");
+  if (!(a->eps > 0 && a->eps < 1)) return set_error(VDI_EINVAL, "epsilon must be in (0, 1)");
+  if (!(a->step > 0) || !(a->lref > 0)) return set_error(VDI_EINVAL, "step must be > 0");
+  if (a->band_stride > 1 && (a->band_offset < 0 || a->band_offset >= a->band_stride))
+    return set_error(VDI_EINVAL, "band_offset out of range");
+  if (reinterpret_cast<uintptr_t>(a->segs) % 16 != 0 || (a->n_sg * 6 * 4) % 16 != 0)
+    return set_error(VDI_EINVAL, "segs must be 16-byte aligned per list");
+  return vdi::gen_launch(a, static_cast<cudaStream_t>(stream));
+}
+
+int vdi_grid_launch(const VdiGridArgs* a, vdi_stream_t stream) {
+  if (!a) return set_error(VDI_EINVAL, "null args");
+  if (!a->segs || !a->counts || !a->grid) return set_error(VDI_EINVAL, "null device pointer");
+  if (a->gx < 1 || a->gy < 1 || a->gz < 1) return set_error(VDI_EINVAL, "bad grid dims");
+  return vdi::grid_launch(a, static_cast<cudaStream_t>(stream));
+}
+
+int vdi_render_launch(const VdiRenderArgs* a, vdi_stream_t stream) {
+  if (!a) return set_error(VDI_EINVAL, "null args");
+  if (!a->segs || !a->counts || !a->grid || !a->image)
+    return set_error(VDI_EINVAL, "null device pointer");
+  if (!(a->early_term > 0.0 && a->early_term <= 1.0))
+    return set_error(VDI_EINVAL, "early_term_alpha must be in (0, 1]");
+  if (a->vdi_w < 1 || a->vdi_h < 1 || a->n_sg < 1 || a->out_w < 1 || a->out_h < 1)
+    return set_error(VDI_EINVAL, "bad sizes");
+  if (a->gx < 1 || a->gy < 1 || a->gz < 1) return set_error(VDI_EINVAL, "bad grid dims");
+  if (reinterpret_cast<uintptr_t>(a->segs) % 16 != 0 || (a->n_sg * 6 * 4) % 16 != 0)
+    return set_error(VDI_EINVAL, "segs must be 16-byte aligned per list");
+  return vdi::render_launch(a, static_cast<cudaStream_t>(stream));
+}
+
+int vdi_find_first_batch(const float* fronts, const float* backs, const int32_t* counts,
+                         int32_t n_max, const double* d_entry, const double* d_exit,
+                         const int32_t* seeds, int32_t* out_index, int32_t* out_seed,
+                         int64_t n_queries, vdi_stream_t stream) {
+  if (n_queries < 0 || n_max < 1) return set_error(VDI_EINVAL, "bad sizes");
+  return vdi::find_first_batch(fronts, backs, counts, n_max, d_entry, d_exit, seeds, out_index,
+                               out_seed, n_queries, static_cast<cudaStream_t>(stream));
+}
+
+int vdi_segs_to_aos(const float* soa, float* aos, int64_t n_lists, int32_t n_sg,
+                    vdi_stream_t stream) {
+  if (n_lists < 0 || n_sg < 1) return set_error(VDI_EINVAL, "bad sizes");
+  return vdi::segs_convert(soa, aos, n_lists, n_sg, true, static_cast<cudaStream_t>(stream));
+}
+
+int vdi_segs_from_aos(const float* aos, float* soa, int64_t n_lists, int32_t n_sg,
+                      vdi_stream_t stream) {
+  if (n_lists < 0 || n_sg < 1) return set_error(VDI_EINVAL, "bad sizes");
+  return vdi::segs_convert(aos, soa, n_lists, n_sg, false, static_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,33 @@
+// vdi_internal.h -- host-side glue shared by the .cu translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "../../include/vdi_b200.h"
+
+namespace vdi {
+
+int set_error(int code, const char* fmt, ...);
+
+// Number of image rows r in [0, h) with ((r / band_rows) % stride) == offset.
+inline int local_rows(int h, int band_rows, int stride, int offset) {
+  if (stride <= 1) return h;
+  int n = 0;
+  for (int b = offset; b * band_rows < h; b += stride) {
+    const int rem = h - b * band_rows;
+    n += rem < band_rows ? rem : band_rows;
+  }
+  return n;
+}
+
+int gen_launch(const VdiGenArgs* a, cudaStream_t stream);
+int grid_launch(const VdiGridArgs* a, cudaStream_t stream);
+int render_launch(const VdiRenderArgs* a, cudaStream_t stream);
+int find_first_batch(const float* fronts, const float* backs, const int32_t* counts,
+                     int32_t n_max, const double* d_entry, const double* d_exit,
+                     const int32_t* seeds, int32_t* out_index, int32_t* out_seed,
+                     int64_t n, cudaStream_t stream);
+int segs_convert(const float* src, float* dst, int64_t n_lists, int32_t n_sg, bool to_aos,
+                 cudaStream_t stream);
+
+}  // namespace vdi

@@ -1,0 +1,362 @@
+// vdi_render.cu -- novel-view VDI raycasting on sm_100a.
+//
+// Semantics: the reference's _render_kernel (raycast.py:275-456): per output
+// pixel an eye ray is clipped to the volume box and the GENERATION frustum,
+// projected to an NDC chord, and walked through the W x H list grid with the
+// Amanatides-Woo DDA (x before y on ties); per list the ESS cell-range test
+// (_grid_cell_range, 258-272) gates the Alg. 2 seeded search (_find_first,
+// 79-141, with _bins 51-62 / _bins_front 65-76); intersected supersegments are
+// composited front to back with the Eq. 2 length correction and early ray
+// termination. f64 throughout, f32 depths promoted before every compare.
+//
+// Layout: lists are list-SoA (include/vdi_b200.h), so the search reads only
+// the contiguous back[] run of a list and a supersegment's colour is one
+// float4. A warp owns an 8x4 pixel tile; neighbouring pixels walk
+// neighbouring lists, which keeps the count/back/rgba loads L1-coherent.
+#include "vdi_common.cuh"
+#include "vdi_internal.h"
+
+namespace vdi {
+
+constexpr int kRenderThreads = 128;
+
+// raycast.py:51-62: smallest j in [start, stop] with backs[j] >= d.
+__device__ __forceinline__ int bins(const float* backs, double d, int start, int stop) {
+  int lo = start, hi = stop;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if ((double)backs[mid] >= d) hi = mid;
+    else lo = mid + 1;
+  }
+  return lo;
+}
+
+// raycast.py:65-76: largest j in [start, stop] with fronts[j] <= d.
+__device__ __forceinline__ int bins_front(const float* fronts, double d, int start, int stop) {
+  int lo = start, hi = stop;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if ((double)fronts[mid] <= d) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+
+// raycast.py:79-141 _find_first. Returns index or -1; `seed` gets the seed.
+__device__ __forceinline__ int find_first(const float* fronts, const float* backs, int count,
+                                          double d_entry, double d_exit, int p, int& seed) {
+  if (count == 0) {
+    seed = p;
+    return -1;
+  }
+  int index;
+  if (d_entry <= d_exit) {
+    index = -1;
+    int bs_start = -1, bs_end = -1;
+    if (p < 0) {
+      bs_start = 0;
+      bs_end = count - 1;
+    } else {
+      const double b1 = p < count ? (double)backs[p] : INFINITY;
+      const double b0 = (p - 1 >= 0 && p - 1 < count) ? (double)backs[p - 1] : -INFINITY;
+      const int interval = (b1 >= d_entry ? 1 : 0) + (b0 >= d_entry ? 1 : 0);
+      if (interval == 0) {
+        bs_start = p + 1;
+        bs_end = count - 1;
+      } else if (interval == 2) {
+        bs_start = 0;
+        bs_end = p - 1;
+      } else if (p < count) {
+        index = p;
+      } else {
+        bs_start = 0;
+        bs_end = count - 1;
+      }
+    }
+    if (bs_end != -1) {
+      if (bs_start > bs_end) {
+        index = bs_start < 0 ? 0 : bs_start;
+        if (index > count - 1) index = count - 1;
+      } else {
+        index = bins(backs, d_entry, bs_start, bs_end < count - 1 ? bs_end : count - 1);
+      }
+    }
+    seed = index;
+    if ((double)backs[index] < d_entry) return -1;
+    if ((double)fronts[index] > d_exit) return -1;
+    return index;
+  }
+  if (p < 0) {
+    index = bins_front(fronts, d_entry, 0, count - 1);
+  } else {
+    const double f1 = p < count ? (double)fronts[p] : INFINITY;
+    const double f0 = (p + 1 >= 0 && p + 1 < count) ? (double)fronts[p + 1] : INFINITY;
+    if (p < count && f1 <= d_entry && f0 > d_entry) {
+      index = p;
+    } else if (f1 > d_entry) {
+      index = bins_front(fronts, d_entry, 0, p - 1 > 0 ? p - 1 : 0);
+    } else {
+      index = bins_front(fronts, d_entry, p + 1 < count - 1 ? p + 1 : count - 1, count - 1);
+    }
+  }
+  if (index > count - 1) index = count - 1;
+  seed = index;
+  if ((double)fronts[index] > d_entry) return -1;
+  if ((double)backs[index] < d_exit) return -1;
+  return index;
+}
+
+__device__ __forceinline__ long long floor_ll(double x) { return (long long)floor(x); }
+__device__ __forceinline__ int clampi(long long v, int lo, int hi) {
+  return (int)(v < lo ? lo : (v > hi ? hi : v));
+}
+
+struct RenderConst {
+  VdiRenderArgs a;
+  int tiles_x;
+  int local_h;
+  long long n_slots;
+};
+
+__global__ void __launch_bounds__(kRenderThreads) render_kernel(const RenderConst c) {
+  const VdiRenderArgs& a = c.a;
+  const long long slot = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned long long st_vis = 0, st_int = 0, st_srch = 0;
+  if (slot < c.n_slots) {
+    const long long tile = slot >> 5;
+    const int w = (int)(slot & 31);
+    const int col = (int)(tile % c.tiles_x) * kTileW + (w & 7);
+    const int lrow = (int)(tile / c.tiles_x) * kTileH + (w >> 3);
+    if (col < a.out_w && lrow < c.local_h) {
+      const int row = band_global_row(lrow, a.band_rows, a.band_stride, a.band_offset);
+      const int vdi_w = a.vdi_w, vdi_h = a.vdi_h, n_sg = a.n_sg;
+      double acc_r = 0.0, acc_g = 0.0, acc_b = 0.0, acc_a = 0.0;
+      int nvis = 0, nint = 0, nsearch = 0;
+      double d[3];
+      pixel_ray(a.new_inv_pv, a.eye, col, row, a.out_w, a.out_h, d);
+      const double* eye = a.eye;
+      double ta, tb, fa, fb, t0 = 0.0, t1 = 0.0;
+      bool ok = false;
+      if (clip_aabb(eye, d, a.aabb, ta, tb) && clip_frustum(a.gen_pv, eye, d, fa, fb)) {
+        t0 = dmax(dmax(ta, fa), 0.0);
+        t1 = dmin(tb, fb);
+        ok = t1 > t0;
+      }
+      if (ok) {
+        double a0x, a0y, a0z, a1x, a1y, a1z;
+        xform(a.gen_pv, eye[0] + t0 * d[0], eye[1] + t0 * d[1], eye[2] + t0 * d[2], a0x, a0y, a0z);
+        xform(a.gen_pv, eye[0] + t1 * d[0], eye[1] + t1 * d[1], eye[2] + t1 * d[2], a1x, a1y, a1z);
+        const double cdx = a1x - a0x, cdy = a1y - a0y, cdz = a1z - a0z;
+        int cx = clampi(floor_ll((a0x + 1.0) * vdi_w / 2.0), 0, vdi_w - 1);
+        int cy = clampi(floor_ll((a0y + 1.0) * vdi_h / 2.0), 0, vdi_h - 1);
+        const int step_x = cdx > 0 ? 1 : (cdx < 0 ? -1 : 0);
+        const int step_y = cdy > 0 ? 1 : (cdy < 0 ? -1 : 0);
+        double t_max_x, t_delta_x, t_max_y, t_delta_y;
+        if (step_x != 0) {
+          const double bx = -1.0 + 2.0 * (double)(cx + (step_x > 0 ? 1 : 0)) / vdi_w;
+          t_max_x = (bx - a0x) / cdx;
+          t_delta_x = (2.0 / vdi_w) / fabs(cdx);
+        } else {
+          t_max_x = INFINITY;
+          t_delta_x = INFINITY;
+        }
+        if (step_y != 0) {
+          const double by = -1.0 + 2.0 * (double)(cy + (step_y > 0 ? 1 : 0)) / vdi_h;
+          t_max_y = (by - a0y) / cdy;
+          t_delta_y = (2.0 / vdi_h) / fabs(cdy);
+        } else {
+          t_max_y = INFINITY;
+          t_delta_y = INFINITY;
+        }
+        int p = -1;
+        double s_cur = 0.0;
+        bool done = false;
+        const int max_iter = vdi_w + vdi_h + 4;
+        const int gx = a.gx, gy = a.gy, gz = a.gz;
+        for (int it = 0; it < max_iter; ++it) {
+          double s_exit = dmin(dmin(t_max_x, t_max_y), 1.0);
+          if (s_exit < s_cur) s_exit = s_cur;
+          const double d_entry = a0z + s_cur * cdz;
+          const double d_exit = a0z + s_exit * cdz;
+          nvis += 1;
+          const long long lidx =
+              (long long)vdi_storage_row(cy, a.vdi_band_rows, a.vdi_band_world,
+                                         a.vdi_rows_per_rank) * vdi_w + cx;
+          const int count = __ldg(a.counts + lidx);
+          bool search = count > 0;
+          if (search && a.use_ess) {
+            const double x_a = a0x + s_cur * cdx, y_a = a0y + s_cur * cdy;
+            const double x_b = a0x + s_exit * cdx, y_b = a0y + s_exit * cdy;
+            const double dep_a = a.proj_b / (a.proj_a - d_entry);
+            const double dep_b = a.proj_b / (a.proj_a - d_exit);
+            const int cgx0 = clampi(floor_ll((dmin(x_a, x_b) + 1.0) * gx / 2.0), 0, gx - 1);
+            const int cgx1 = clampi(floor_ll((dmax(x_a, x_b) + 1.0) * gx / 2.0), 0, gx - 1);
+            const int cgy0 = clampi(floor_ll((dmin(y_a, y_b) + 1.0) * gy / 2.0), 0, gy - 1);
+            const int cgy1 = clampi(floor_ll((dmax(y_a, y_b) + 1.0) * gy / 2.0), 0, gy - 1);
+            const double fn = a.far - a.near;
+            const int cz0 = clampi(floor_ll((dmin(dep_a, dep_b) - a.near) / fn * gz), 0, gz - 1);
+            const int cz1 = clampi(floor_ll((dmax(dep_a, dep_b) - a.near) / fn * gz), 0, gz - 1);
+            bool empty = true;
+            for (int cz = cz0; cz <= cz1 && empty; ++cz)
+              for (int cgy = cgy0; cgy <= cgy1 && empty; ++cgy)
+                for (int cgx = cgx0; cgx <= cgx1; ++cgx)
+                  if (__ldg(a.grid + ((long long)cz * gy + cgy) * gx + cgx) > 0u) {
+                    empty = false;
+                    break;
+                  }
+            if (empty) search = false;
+          }
+          if (search) {
+            nsearch += 1;
+            const float* ls = a.segs + lidx * (long long)(n_sg * 6);
+            const float* fronts = ls;
+            const float* backs = ls + n_sg;
+            const float4* rgba = reinterpret_cast<const float4*>(ls + 2 * n_sg);
+            int seed;
+            const int j = find_first(fronts, backs, count, d_entry, d_exit, p, seed);
+            p = seed;
+            if (j >= 0) {
+              const bool fwd = d_entry <= d_exit;
+              const double zlo = dmin(d_entry, d_exit), zhi = dmax(d_entry, d_exit);
+              const double xc = -1.0 + 2.0 * (cx + 0.5) / vdi_w;
+              const double yc = -1.0 + 2.0 * (cy + 0.5) / vdi_h;
+              int k = j;
+              while (0 <= k && k < count) {
+                const double fk = fronts[k], bk = backs[k];
+                const double ilo = dmax(fk, zlo), ihi = dmin(bk, zhi);
+                if (ilo > ihi) break;
+                double s_a, s_b;
+                if (fabs(cdz) < 1e-12) {
+                  s_a = s_cur;
+                  s_b = s_exit;
+                } else {
+                  s_a = (ilo - a0z) / cdz;
+                  s_b = (ihi - a0z) / cdz;
+                  if (s_a > s_b) {
+                    const double t = s_a;
+                    s_a = s_b;
+                    s_b = t;
+                  }
+                  if (s_a < s_cur) s_a = s_cur;
+                  if (s_b > s_exit) s_b = s_exit;
+                }
+                double w0x, w0y, w0z, w1x, w1y, w1z;
+                xform(a.gen_inv_pv, a0x + s_a * cdx, a0y + s_a * cdy, a0z + s_a * cdz, w0x, w0y, w0z);
+                xform(a.gen_inv_pv, a0x + s_b * cdx, a0y + s_b * cdy, a0z + s_b * cdz, w1x, w1y, w1z);
+                const double ex = w1x - w0x, ey = w1y - w0y, ez = w1z - w0z;
+                const double l = sqrt(ex * ex + ey * ey + ez * ez);
+                double wfx, wfy, wfz, wbx, wby, wbz;
+                xform(a.gen_inv_pv, xc, yc, fk, wfx, wfy, wfz);
+                xform(a.gen_inv_pv, xc, yc, bk, wbx, wby, wbz);
+                const double tx = wbx - wfx, ty = wby - wfy, tz = wbz - wfz;
+                const double thick = sqrt(tx * tx + ty * ty + tz * tz);
+                const float4 c4 = rgba[k];
+                const double alpha = c4.w;
+                if (alpha > 0.0 && thick > 0.0) {
+                  const double a_t = 1.0 - pow(1.0 - alpha, l / thick);
+                  const double scale = a_t / alpha;
+                  const double wgt = 1.0 - acc_a;
+                  acc_r += wgt * (double)c4.x * scale;
+                  acc_g += wgt * (double)c4.y * scale;
+                  acc_b += wgt * (double)c4.z * scale;
+                  acc_a += wgt * a_t;
+                }
+                nint += 1;
+                p = k;
+                if (acc_a >= a.early_term) {
+                  done = true;
+                  break;
+                }
+                k += fwd ? 1 : -1;
+              }
+            }
+          }
+          if (done || acc_a >= a.early_term) break;
+          if (s_exit >= 1.0) break;
+          if (t_max_x <= t_max_y) {
+            cx += step_x;
+            s_cur = t_max_x;
+            t_max_x += t_delta_x;
+          } else {
+            cy += step_y;
+            s_cur = t_max_y;
+            t_max_y += t_delta_y;
+          }
+          if (cx < 0 || cx >= vdi_w || cy < 0 || cy >= vdi_h) break;
+        }
+      }
+      const double wgt = 1.0 - acc_a;
+      const long long pix = (long long)lrow * a.out_w + col;
+      double2* o = reinterpret_cast<double2*>(a.image + pix * 4);
+      o[0] = make_double2(acc_r + wgt * a.bg[0] * a.bg[3], acc_g + wgt * a.bg[1] * a.bg[3]);
+      o[1] = make_double2(acc_b + wgt * a.bg[2] * a.bg[3], acc_a + wgt * a.bg[3]);
+      if (a.lists_visited) a.lists_visited[pix] = nvis;
+      if (a.segs_intersected) a.segs_intersected[pix] = nint;
+      if (a.lists_searched) a.lists_searched[pix] = nsearch;
+      st_vis = nvis;
+      st_int = nint;
+      st_srch = nsearch;
+    }
+  }
+  if (a.stat_sums) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      st_vis += __shfl_xor_sync(0xffffffffu, st_vis, off);
+      st_int += __shfl_xor_sync(0xffffffffu, st_int, off);
+      st_srch += __shfl_xor_sync(0xffffffffu, st_srch, off);
+    }
+    if ((threadIdx.x & 31) == 0) {
+      atomicAdd(a.stat_sums + 0, st_vis);
+      atomicAdd(a.stat_sums + 1, st_int);
+      atomicAdd(a.stat_sums + 2, st_srch);
+    }
+  }
+}
+
+int render_launch(const VdiRenderArgs* args, cudaStream_t stream) {
+  RenderConst c;
+  c.a = *args;
+  if (c.a.band_rows <= 0) c.a.band_rows = 16;
+  if (c.a.band_stride <= 0) c.a.band_stride = 1;
+  if (c.a.vdi_band_rows <= 0) c.a.vdi_band_rows = 16;
+  if (c.a.vdi_band_world <= 0) c.a.vdi_band_world = 1;
+  c.local_h = local_rows(args->out_h, c.a.band_rows, c.a.band_stride, c.a.band_offset);
+  c.tiles_x = (args->out_w + kTileW - 1) / kTileW;
+  const long long tiles_y = (c.local_h + kTileH - 1) / kTileH;
+  c.n_slots = (long long)c.tiles_x * tiles_y * 32;
+  if (c.n_slots == 0) return VDI_OK;
+  const long long blocks = (c.n_slots + kRenderThreads - 1) / kRenderThreads;
+  render_kernel<<<(unsigned)blocks, kRenderThreads, 0, stream>>>(c);
+  const cudaError_t err = cudaGetLastError();
+  if (err != cudaSuccess)
+    return set_error(VDI_ELAUNCH, "render launch: %s", cudaGetErrorString(err));
+  return VDI_OK;
+}
+
+// Batch form of find_first_supersegment (raycast.py:144-156) for the A1 fuzz.
+__global__ void find_first_batch_kernel(const float* fronts, const float* backs,
+                                        const int32_t* counts, int n_max, const double* d_entry,
+                                        const double* d_exit, const int32_t* seeds,
+                                        int32_t* out_index, int32_t* out_seed, long long n) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int seed;
+  out_index[i] = find_first(fronts + i * n_max, backs + i * n_max, counts[i], d_entry[i],
+                            d_exit[i], seeds[i], seed);
+  out_seed[i] = seed;
+}
+
+int find_first_batch(const float* fronts, const float* backs, const int32_t* counts,
+                     int32_t n_max, const double* d_entry, const double* d_exit,
+                     const int32_t* seeds, int32_t* out_index, int32_t* out_seed,
+                     int64_t n, cudaStream_t stream) {
+  if (n <= 0) return VDI_OK;
+  find_first_batch_kernel<<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(
+      fronts, backs, counts, n_max, d_entry, d_exit, seeds, out_index, out_seed, n);
+  const cudaError_t err = cudaGetLastError();
+  if (err != cudaSuccess)
+    return set_error(VDI_ELAUNCH, "find_first launch: %s", cudaGetErrorString(err));
+  return VDI_OK;
+}
+
+}  // namespace vdi

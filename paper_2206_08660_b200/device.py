@@ -1,0 +1,135 @@
+"""Device plumbing: torch owns device memory and streams; the compute is in
+libvdi_b200.so. Host<->device traffic goes through pinned staging buffers.
+"""
+
+from __future__ import annotations
+
+import weakref
+
+import numpy as np
+
+from . import _capi
+
+_torch = None
+
+
+def torch():
+    global _torch
+    if _torch is None:
+        import torch as t
+        _torch = t
+    return _torch
+
+
+def require_cuda():
+    t = torch()
+    if not t.cuda.is_available():
+        raise _capi.VdiError("paper_2206_08660_b200 needs a CUDA device (B200); "
+                             "there is no CPU fallback")
+    _capi.load()
+    return t
+
+
+def stream_handle():
+    return torch().cuda.current_stream().cuda_stream
+
+
+def ptr(t) -> int:
+    return 0 if t is None else int(t.data_ptr())
+
+
+def pinned_empty(shape, dtype):
+    t = torch()
+    return t.empty(shape, dtype=dtype, pin_memory=True)
+
+
+def to_device(arr: np.ndarray, dtype=None):
+    """H2D copy; pinned arrays (see pinned_numpy) copy asynchronously."""
+    t = torch()
+    a = np.ascontiguousarray(arr if dtype is None else arr.astype(dtype, copy=False))
+    return t.from_numpy(a).to("cuda", non_blocking=True)
+
+
+def pinned_numpy(shape, np_dtype) -> np.ndarray:
+    """A numpy array backed by pinned host memory."""
+    t = torch()
+    if not _TORCH_OF:
+        _init_dtypes()
+    tt = t.empty(tuple(shape), dtype=_TORCH_OF[np.dtype(np_dtype)], pin_memory=True)
+    return tt.numpy()
+
+
+def to_host(dev_tensor, sync: bool = True) -> np.ndarray:
+    """D2H through a pinned staging buffer."""
+    host = torch().empty(dev_tensor.shape, dtype=dev_tensor.dtype, pin_memory=True)
+    host.copy_(dev_tensor, non_blocking=True)
+    if sync:
+        torch().cuda.current_stream().synchronize()
+    return host.numpy()
+
+
+_TORCH_OF = {}
+
+
+def _init_dtypes():
+    t = torch()
+    _TORCH_OF.update({np.dtype(np.uint8): t.uint8, np.dtype(np.int16): t.int16,
+                      np.dtype(np.uint16): t.uint16, np.dtype(np.int32): t.int32,
+                      np.dtype(np.uint32): t.uint32, np.dtype(np.int64): t.int64,
+                      np.dtype(np.float32): t.float32, np.dtype(np.float64): t.float64})
+
+
+class _ArrayCache:
+    """Device copies of immutable host arrays (Volume.data, TF LUTs), keyed by
+    identity and validated through a weak reference."""
+
+    def __init__(self, capacity: int = 4):
+        self.capacity = capacity
+        self.items = []  # (weakref, key, tensor)
+
+    def get(self, arr: np.ndarray, dtype=None):
+        key = (arr.ctypes.data, arr.shape, arr.dtype.str)
+        for i, (ref, k, tens) in enumerate(self.items):
+            if k == key and ref() is arr:
+                self.items.append(self.items.pop(i))
+                return tens
+        tens = to_device(arr, dtype)
+        self.items.append((weakref.ref(arr), key, tens))
+        while len(self.items) > self.capacity:
+            self.items.pop(0)
+        return tens
+
+    def clear(self):
+        self.items.clear()
+
+
+volume_cache = _ArrayCache(2)
+lut_cache = _ArrayCache(8)
+
+
+def volume_array(vol):
+    """(host array, voxel type) the device samples for `vol`.
+
+    Our Volume with a derived `normalized` uploads the raw u8/u16 brick
+    (normalised on the fly, bit-identical to volume.py:48-50); anything else
+    (a reference vdikit.Volume, or a user-supplied `normalized`) uploads the
+    f32 array the reference samples."""
+    derived = getattr(vol, "normalized_is_derived", False)
+    vt = getattr(vol, "voxel_type", "u8")
+    if derived and vt in ("u8", "u16", "f32"):
+        return vol.data, vt
+    return np.ascontiguousarray(vol.normalized, dtype=np.float32), "f32"
+
+
+def upload_volume(vol, cache: bool = True):
+    arr, vt = volume_array(vol)
+    if arr.ndim != 3:
+        nx, ny, nz = vol.dims
+        arr = arr.reshape(nz, ny, nx)
+    if cache:
+        return volume_cache.get(arr), vt
+    return to_device(arr), vt
+
+
+def upload_lut(lut: np.ndarray):
+    return lut_cache.get(np.ascontiguousarray(lut, dtype=np.float32))

@@ -1,0 +1,183 @@
+"""VDI generation: drop-in for `vdikit.generate_vdi` (generate.py:444-479).
+
+Same signature and return types; the per-ray bisection (Alg. 1 as the
+reference implements it, generate.py:219-273), the front-to-back passes
+(89-216) and the AccelGrid build (322-346) run as sm_100a kernels through
+`vdi_gen_launch` / `vdi_grid_launch` (include/vdi_b200.h).
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _capi
+from . import device as dv
+from .vdi import AccelGrid, DeviceVdi, Vdi, default_grid_dims
+
+SQRT3 = 1.7320508075688772
+
+
+@dataclass(frozen=True)
+class GenParams:
+    """generate.py:28-50."""
+    n_sg: int = 12
+    delta: int | None = None
+    epsilon: float = 1e-6
+    gamma_init: float = 1e-5
+    step: float | None = None
+    ref_step: float | None = None
+    alpha_early: float = 0.999
+
+    def resolve(self, vol) -> tuple:
+        step = self.step if self.step is not None else 0.5 * min(vol.spacing)
+        lref = self.ref_step if self.ref_step is not None else step
+        delta = max(1, int(0.15 * self.n_sg)) if self.delta is None else self.delta
+        delta = min(delta, self.n_sg - 1)
+        if not (0 < self.epsilon < 1):
+            raise ValueError("epsilon must be in (0, 1)")
+        if self.n_sg < 1:
+            raise ValueError("n_sg must be >= 1")
+        return delta, step, lref
+
+
+@dataclass(frozen=True)
+class GenStats:
+    """generate.py:428-441, plus the executed-sample count per ray."""
+    gammas: np.ndarray
+    passes: np.ndarray
+    wall_time_s: float
+    samples: np.ndarray | None = None
+
+    @property
+    def max_passes(self) -> int:
+        return int(self.passes.max())
+
+    @property
+    def mean_passes(self) -> float:
+        active = self.passes[self.passes > 0]
+        return float(active.mean()) if active.size else 0.0
+
+
+def depth_consts(near: float, far: float) -> tuple:
+    """generate.py:349-354."""
+    return (far + near) / (far - near), 2.0 * far * near / (far - near)
+
+
+def _mat(m) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(m, dtype=np.float64).reshape(16))
+
+
+@dataclass
+class GenBuffers:
+    counts: object
+    segs: object
+    gammas: object
+    passes: object
+    samples: object
+    workspace: object
+    grid: object
+
+
+def alloc_gen(width, rows, n_sg, grid_dims, stats=True):
+    t = dv.torch()
+    gx, gy, gz = grid_dims
+    return GenBuffers(
+        counts=t.empty((rows, width), dtype=t.int32, device="cuda"),
+        segs=t.empty((rows * width, n_sg * 6), dtype=t.float32, device="cuda"),
+        gammas=t.empty((rows, width), dtype=t.float64, device="cuda") if stats else None,
+        passes=t.empty((rows, width), dtype=t.int32, device="cuda") if stats else None,
+        samples=t.empty((rows, width), dtype=t.int32, device="cuda") if stats else None,
+        workspace=t.empty(256, dtype=t.uint8, device="cuda"),
+        grid=t.empty((gz, gy, gx), dtype=t.int32, device="cuda"))
+
+
+def gen_args(vol_dev, voxel_type, dims, lut_dev, cam, aabb, params_resolved, n_sg, eps,
+             gamma_init, bufs: GenBuffers, band=(16, 1, 0)) -> _capi.VdiGenArgs:
+    delta, step, lref = params_resolved
+    width, height = cam.viewport
+    a = _capi.VdiGenArgs()
+    a.volume, a.lut = dv.ptr(vol_dev), dv.ptr(lut_dev)
+    a.counts, a.segs = dv.ptr(bufs.counts), dv.ptr(bufs.segs)
+    a.gammas, a.passes, a.samples = dv.ptr(bufs.gammas), dv.ptr(bufs.passes), dv.ptr(bufs.samples)
+    a.workspace = dv.ptr(bufs.workspace)
+    _capi.fill(a.pv, _mat(cam.proj_view()))
+    _capi.fill(a.inv_pv, _mat(cam.inv_proj_view()))
+    _capi.fill(a.eye, np.asarray(cam.position, dtype=np.float64))
+    _capi.fill(a.aabb, np.asarray(aabb, dtype=np.float64).reshape(6))
+    a.eps, a.gamma_init, a.step, a.lref = float(eps), float(gamma_init), float(step), float(lref)
+    a.voxel_type = _capi.VOXEL[voxel_type]
+    a.nx, a.ny, a.nz = (int(v) for v in dims)
+    a.lut_n = int(lut_dev.shape[0])
+    a.width, a.height = int(width), int(height)
+    a.n_sg, a.delta = int(n_sg), int(delta)
+    a.band_rows, a.band_stride, a.band_offset = (int(v) for v in band)
+    return a
+
+
+def grid_args(bufs: GenBuffers, cam, width, height, n_sg, grid_dims, band=(16, 1, 0),
+              clear=True) -> _capi.VdiGridArgs:
+    pa, pb = depth_consts(cam.near, cam.far)
+    g = _capi.VdiGridArgs()
+    g.segs, g.counts, g.grid = dv.ptr(bufs.segs), dv.ptr(bufs.counts), dv.ptr(bufs.grid)
+    g.near, g.far, g.proj_a, g.proj_b = float(cam.near), float(cam.far), pa, pb
+    g.width, g.height, g.n_sg = int(width), int(height), int(n_sg)
+    g.gx, g.gy, g.gz = (int(v) for v in grid_dims)
+    g.band_rows, g.band_stride, g.band_offset = (int(v) for v in band)
+    g.clear = int(clear)
+    return g
+
+
+def launch_generate(vol_dev, voxel_type, dims, lut_dev, cam, aabb, params, resolved,
+                    bufs: GenBuffers, grid_dims, band=(16, 1, 0), stream=None,
+                    split_events=None):
+    """Enqueue generation + grid on the current stream (no sync, no alloc).
+    split_events: optional CUDA events; [1] and [2] bracket the generation
+    kernel (timing only)."""
+    L = _capi.load()
+    s = dv.stream_handle() if stream is None else stream
+    a = gen_args(vol_dev, voxel_type, dims, lut_dev, cam, aabb, resolved, params.n_sg,
+                 params.epsilon, params.gamma_init, bufs, band)
+    if split_events:
+        split_events[1].record()
+    _capi.check(L.vdi_gen_launch(a, s))
+    if split_events:
+        split_events[2].record()
+    w, h = cam.viewport
+    g = grid_args(bufs, cam, w, h, params.n_sg, grid_dims, band)
+    _capi.check(L.vdi_grid_launch(g, s))
+
+
+def generate_vdi(vol, tf, cam, params: GenParams | None = None, grid_dims=None,
+                 with_stats: bool = False, *, cache_volume: bool = True):
+    """Generate a Vdi + AccelGrid from camera `cam` (one ray per viewport pixel).
+
+    Mirrors generate.py:444-479. The returned Vdi / AccelGrid are device
+    resident and materialise their numpy arrays on first access."""
+    params = params or GenParams()
+    resolved = params.resolve(vol)
+    t = dv.require_cuda()
+    width, height = cam.viewport
+    if grid_dims is None:
+        grid_dims = default_grid_dims(width, height)
+    aabb = np.asarray(vol.aabb, dtype=np.float64)
+    t_start = time.perf_counter()
+    vol_dev, vt = dv.upload_volume(vol, cache=cache_volume)
+    lut_dev = dv.upload_lut(tf.lut)
+    bufs = alloc_gen(width, height, params.n_sg, grid_dims, stats=with_stats)
+    launch_generate(vol_dev, vt, vol.dims, lut_dev, cam, aabb, params, resolved, bufs,
+                    grid_dims)
+    dev = DeviceVdi(counts=bufs.counts, segs=bufs.segs)
+    vdi = Vdi(width=width, height=height, n_sg=params.n_sg, counts=None, segs=None,
+              gen_camera=cam, volume_aabb=aabb, _device=dev)
+    grid = AccelGrid(dims=grid_dims, counts=None, near=cam.near, far=cam.far,
+                     _device=bufs.grid)
+    if not with_stats:
+        return vdi, grid
+    t.cuda.current_stream().synchronize()
+    wall = time.perf_counter() - t_start
+    stats = GenStats(gammas=dv.to_host(bufs.gammas), passes=dv.to_host(bufs.passes),
+                     wall_time_s=wall, samples=dv.to_host(bufs.samples))
+    return vdi, grid, stats

@@ -1,0 +1,158 @@
+"""Novel-view VDI rendering: drop-in for `vdikit.render_vdi` (raycast.py:459-491).
+
+The per-pixel NDC DDA, ESS test, Alg. 2 seeded search and Eq. 2 compositing
+(raycast.py:275-456) run in `vdi_render_launch` (include/vdi_b200.h).
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _capi
+from . import device as dv
+from .generate import depth_consts, _mat
+from .image import Image
+
+
+@dataclass(frozen=True)
+class RenderOptions:
+    """raycast.py:28-36."""
+    use_ess: bool = True
+    early_term_alpha: float = 0.999
+    background: tuple = (0.0, 0.0, 0.0, 1.0)
+
+    def __post_init__(self):
+        if not (0.0 < self.early_term_alpha <= 1.0):
+            raise ValueError("early_term_alpha must be in (0, 1]")
+
+
+@dataclass(frozen=True)
+class RenderStats:
+    """raycast.py:39-43 (+ lists searched, a counter the reference lacks)."""
+    lists_visited: int
+    supersegments_intersected: int
+    frame_ms: float
+    lists_searched: int = -1
+
+
+def opacity_correct(alpha: float, l: float) -> float:
+    """raycast.py:46-48."""
+    return 1.0 - (1.0 - alpha) ** l
+
+
+def render_args(dvdi, n_sg, vdi_w, vdi_h, gen_cam, aabb, grid_dev, grid_dims, grid_near,
+                grid_far, cam_new, opts, image, per_pixel=None, stat_sums=None,
+                band=(16, 1, 0)) -> _capi.VdiRenderArgs:
+    a = _capi.VdiRenderArgs()
+    a.segs, a.counts, a.grid, a.image = (dv.ptr(dvdi.segs), dv.ptr(dvdi.counts),
+                                         dv.ptr(grid_dev), dv.ptr(image))
+    if per_pixel is not None:
+        a.lists_visited, a.segs_intersected, a.lists_searched = (dv.ptr(x) for x in per_pixel)
+    a.stat_sums = dv.ptr(stat_sums)
+    _capi.fill(a.gen_pv, _mat(gen_cam.proj_view()))
+    _capi.fill(a.gen_inv_pv, _mat(gen_cam.inv_proj_view()))
+    _capi.fill(a.new_inv_pv, _mat(cam_new.inv_proj_view()))
+    _capi.fill(a.eye, np.asarray(cam_new.position, dtype=np.float64))
+    _capi.fill(a.aabb, np.asarray(aabb, dtype=np.float64).reshape(6))
+    _capi.fill(a.bg, np.asarray(opts.background, dtype=np.float64))
+    pa, pb = depth_consts(gen_cam.near, gen_cam.far)
+    a.near, a.far, a.proj_a, a.proj_b = float(grid_near), float(grid_far), pa, pb
+    a.early_term = float(opts.early_term_alpha)
+    a.vdi_w, a.vdi_h, a.n_sg = int(vdi_w), int(vdi_h), int(n_sg)
+    a.gx, a.gy, a.gz = (int(v) for v in grid_dims)
+    a.out_w, a.out_h = (int(v) for v in cam_new.viewport)
+    a.use_ess = int(bool(opts.use_ess))
+    a.vdi_band_rows, a.vdi_band_world = int(dvdi.band_rows), int(dvdi.world)
+    a.vdi_rows_per_rank = int(dvdi.rows_per_rank)
+    a.band_rows, a.band_stride, a.band_offset = (int(v) for v in band)
+    return a
+
+
+def launch_render(vdi, grid, cam_new, opts, image, per_pixel=None, stat_sums=None,
+                  band=(16, 1, 0), stream=None):
+    """Enqueue one render on the current stream (no sync, no alloc)."""
+    a = render_args(vdi.device(), vdi.n_sg, vdi.width, vdi.height, vdi.gen_camera,
+                    vdi.volume_aabb, grid.device(), grid.dims, grid.near, grid.far, cam_new,
+                    opts, image, per_pixel, stat_sums, band)
+    _capi.check(_capi.load().vdi_render_launch(a, dv.stream_handle() if stream is None
+                                               else stream))
+
+
+def _as_device_vdi(vdi):
+    """Accept our Vdi or any object with the reference Vdi's attributes."""
+    if hasattr(vdi, "device"):
+        return vdi
+    from .vdi import Vdi
+    cached = getattr(vdi, "__b200_vdi", None)
+    if cached is None:
+        cached = Vdi(vdi.width, vdi.height, vdi.n_sg, vdi.counts, vdi.segs, vdi.gen_camera,
+                     vdi.volume_aabb)
+        try:
+            object.__setattr__(vdi, "__b200_vdi", cached)
+        except Exception:
+            pass
+    return cached
+
+
+def _as_device_grid(grid):
+    if hasattr(grid, "device"):
+        return grid
+    from .vdi import AccelGrid
+    return AccelGrid(grid.dims, grid.counts, grid.near, grid.far)
+
+
+def render_vdi(vdi, grid, cam_new, opts: RenderOptions | None = None,
+               with_stats: bool = False):
+    """Render a VDI from a novel viewpoint; returns Image (and RenderStats)."""
+    opts = opts or RenderOptions()
+    t = dv.require_cuda()
+    vdi = _as_device_vdi(vdi)
+    grid = _as_device_grid(grid)
+    out_w, out_h = cam_new.viewport
+    image = t.empty((out_h, out_w, 4), dtype=t.float64, device="cuda")
+    sums = t.zeros(3, dtype=t.int64, device="cuda") if with_stats else None
+    t_start = time.perf_counter()
+    ev0 = ev1 = None
+    if with_stats:
+        ev0, ev1 = t.cuda.Event(enable_timing=True), t.cuda.Event(enable_timing=True)
+        ev0.record()
+    launch_render(vdi, grid, cam_new, opts, image, stat_sums=sums)
+    if with_stats:
+        ev1.record()
+    img = Image.from_array(dv.to_host(image))
+    if not with_stats:
+        return img
+    s = dv.to_host(sums)
+    ms = ev0.elapsed_time(ev1) if ev0 is not None else (time.perf_counter() - t_start) * 1e3
+    return img, RenderStats(lists_visited=int(s[0]), supersegments_intersected=int(s[1]),
+                            frame_ms=float(ms), lists_searched=int(s[2]))
+
+
+def find_first_supersegment(seg_list, d_entry: float, d_exit: float, p: int = -1):
+    """raycast.py:144-156 on the device (batch of one query)."""
+    res = find_first_batch(np.asarray(seg_list, np.float32).reshape(1, -1, 6),
+                           [len(np.asarray(seg_list).reshape(-1, 6))], [d_entry], [d_exit], [p])
+    idx, seed = int(res[0][0]), int(res[1][0])
+    return (None if idx < 0 else idx), seed
+
+
+def find_first_batch(lists, counts, d_entry, d_exit, seeds):
+    """Alg. 2 search for many independent queries: lists (n, n_max, 6) f32."""
+    t = dv.require_cuda()
+    lists = np.asarray(lists, np.float32)
+    n, n_max = lists.shape[0], lists.shape[1]
+    fr = dv.to_device(np.ascontiguousarray(lists[..., 0]))
+    bk = dv.to_device(np.ascontiguousarray(lists[..., 1]))
+    cnt = dv.to_device(np.asarray(counts, np.int32))
+    de = dv.to_device(np.asarray(d_entry, np.float64))
+    dx = dv.to_device(np.asarray(d_exit, np.float64))
+    sd = dv.to_device(np.asarray(seeds, np.int32))
+    oi = t.empty(n, dtype=t.int32, device="cuda")
+    osd = t.empty(n, dtype=t.int32, device="cuda")
+    _capi.check(_capi.load().vdi_find_first_batch(
+        dv.ptr(fr), dv.ptr(bk), dv.ptr(cnt), int(n_max), dv.ptr(de), dv.ptr(dx), dv.ptr(sd),
+        dv.ptr(oi), dv.ptr(osd), int(n), dv.stream_handle()))
+    return dv.to_host(oi), dv.to_host(osd)

@@ -1,0 +1,210 @@
+"""Ray-band sharding of generate -> render across the GPUs of one box.
+
+Both passes are independent per ray (generate.py:281 / raycast.py:283
+`prange`), so each rank takes the interleaved 16-row bands b with
+b % world == rank of the generation viewport and of the output viewport
+(interleaving balances empty borders and 1- vs 22-pass rays). The only
+exchange is between the passes: the render rays of any rank can traverse any
+list, so the AccelGrid partials are all-reduced (sum) and the VDI tiles are
+all-gathered (NCCL over NVLink); the gathered VDI is read in its
+band-interleaved storage order through the band map (include/vdi_b200.h), so
+no permutation copy is made. The image rows are all-gathered at the end.
+
+The collectives go through torch.distributed, so the same host logic runs
+with NCCL on B200s and with gloo on CPU tensors in the tests.
+"""
+
+from __future__ import annotations
+
+import time
+
+import numpy as np
+
+from . import _capi
+from . import device as dv
+from .generate import alloc_gen, launch_generate
+from .raycast import RenderOptions, render_args
+from .vdi import AccelGrid, DeviceVdi, Vdi, default_grid_dims
+
+BAND_ROWS = 16
+
+
+def band_rows(height: int, world: int, rank: int, band: int = BAND_ROWS) -> np.ndarray:
+    """Image rows owned by `rank` (same rule as band_global_row in the kernels)."""
+    rows = np.arange(height)
+    return rows[(rows // band) % world == rank]
+
+
+def local_rows(height: int, world: int, rank: int, band: int = BAND_ROWS) -> int:
+    return int(len(band_rows(height, world, rank, band)))
+
+
+def rows_per_rank(height: int, world: int, band: int = BAND_ROWS) -> int:
+    """Padded per-rank row count (rank 0 owns the most rows)."""
+    return local_rows(height, world, 0, band)
+
+
+def storage_rows(height: int, world: int, band: int = BAND_ROWS) -> np.ndarray:
+    """Storage row of each image row after an all-gather of padded shards
+    (vdi_storage_row in the kernels)."""
+    if world <= 1:
+        return np.arange(height)
+    r = np.arange(height)
+    b = r // band
+    return (b % world) * rows_per_rank(height, world, band) + (b // world) * band + r % band
+
+
+def gather_rows(dist, local, world: int, padded_rows: int):
+    """All-gather equal-size (padded) row shards: [world * padded_rows, ...]."""
+    if local.shape[0] != padded_rows:
+        raise ValueError("shard must be padded to rows_per_rank rows")
+    out = local.new_empty((world * padded_rows, *local.shape[1:]))
+    dist.all_gather_into_tensor(out, local.contiguous())
+    return out
+
+
+class Pipeline:
+    """generate -> (all-reduce grid, all-gather VDI) -> render -> all-gather
+    image, device-resident, for one rank."""
+
+    def __init__(self, vol, tf, gcam, rcam, params, world=1, rank=0, opts=None):
+        t = dv.require_cuda()
+        self.t = t
+        self.vol, self.tf, self.gcam, self.rcam, self.params = vol, tf, gcam, rcam, params
+        self.world, self.rank = world, rank
+        self.opts = opts or RenderOptions()
+        self.resolved = params.resolve(vol)
+        w, h = gcam.viewport
+        self.w, self.h = w, h
+        self.grid_dims = default_grid_dims(w, h)
+        self.vol_dev, self.vt = dv.upload_volume(vol)
+        self.lut_dev = dv.upload_lut(tf.lut)
+        self.aabb = np.asarray(vol.aabb, np.float64)
+        self.band = (BAND_ROWS, world, rank)
+        self.gen_rows = rows_per_rank(h, world)
+        self.local_gen_rays = local_rows(h, world, rank) * w
+        self.bufs = alloc_gen(w, self.gen_rows, params.n_sg, self.grid_dims, stats=True)
+        self.bufs.counts.zero_()  # padding rows stay empty
+        ow, oh = rcam.viewport
+        self.ow, self.oh = ow, oh
+        self.out_rows = rows_per_rank(oh, world)
+        self.local_render_pixels = local_rows(oh, world, rank) * ow
+        self.image = t.zeros((self.out_rows, ow, 4), dtype=t.float64, device="cuda")
+        self.sums = t.zeros(3, dtype=t.int64, device="cuda")
+        self.launches_per_step = 3  # vdi_gen, vdi_grid, vdi_render
+        if world > 1:
+            import torch.distributed as tdist
+            self.dist = tdist
+            self.g_counts = t.empty((world * self.gen_rows, w), dtype=t.int32, device="cuda")
+            self.g_segs = t.empty((world * self.gen_rows * w, params.n_sg * 6),
+                                  dtype=t.float32, device="cuda")
+            self.g_image = t.empty((world * self.out_rows, ow, 4), dtype=t.float64,
+                                   device="cuda")
+            self.dvdi = DeviceVdi(self.g_counts, self.g_segs, BAND_ROWS, world, self.gen_rows)
+        else:
+            self.dist = None
+            self.dvdi = DeviceVdi(self.bufs.counts, self.bufs.segs)
+        self._rargs = render_args(self.dvdi, params.n_sg, w, h, gcam, self.aabb, self.bufs.grid,
+                                  self.grid_dims, gcam.near, gcam.far, rcam, self.opts,
+                                  self.image, stat_sums=self.sums, band=self.band)
+
+    def step(self, timed: bool = False):
+        t = self.t
+        L = _capi.load()
+        ev = [t.cuda.Event(enable_timing=True) for _ in range(6)] if timed else None
+        if timed:
+            ev[0].record()
+        self.sums.zero_()
+        launch_generate(self.vol_dev, self.vt, self.vol.dims, self.lut_dev, self.gcam,
+                        self.aabb, self.params, self.resolved, self.bufs, self.grid_dims,
+                        band=self.band, split_events=ev)
+        if timed:
+            ev[3].record()
+        if self.world > 1:
+            self.dist.all_reduce(self.bufs.grid)
+            self.dist.all_gather_into_tensor(self.g_counts, self.bufs.counts)
+            self.dist.all_gather_into_tensor(self.g_segs, self.bufs.segs)
+        if timed:
+            ev[4].record()
+        _capi.check(L.vdi_render_launch(self._rargs, dv.stream_handle()))
+        if timed:
+            ev[5].record()
+        if self.world > 1:
+            self.dist.all_gather_into_tensor(self.g_image, self.image)
+        if not timed:
+            return None
+        end = t.cuda.Event(enable_timing=True)
+        end.record()
+        end.synchronize()
+        return {"step": ev[0].elapsed_time(end), "gen": ev[1].elapsed_time(ev[2]),
+                "grid": ev[2].elapsed_time(ev[3]),
+                "collective": ev[3].elapsed_time(ev[4]) + ev[5].elapsed_time(end),
+                "render": ev[4].elapsed_time(ev[5])}
+
+    def samples_executed(self) -> int:
+        return int(self.bufs.samples.to(self.t.int64).sum().item())
+
+    def render_stats(self):
+        s = self.sums.cpu().numpy()
+        return int(s[0]), int(s[1]), int(s[2])
+
+    def host_vdi(self):
+        """(counts, segs AoS, grid) on the host, natural row order (N=1)."""
+        vdi = Vdi(self.w, self.h, self.params.n_sg, None, None, self.gcam, self.aabb,
+                  _device=self.dvdi)
+        return vdi.counts, vdi.segs, dv.to_host(self.bufs.grid).view(np.uint32)
+
+    def e2e(self, steps: int):
+        """End to end through host buffers: pinned volume H2D every step, the
+        public generate_vdi / render_vdi (N=1) or the sharded pipeline (N>1),
+        and the step's results read back to pinned host memory."""
+        t = self.t
+        vol = self.vol
+        host = dv.pinned_numpy(vol.data.shape, vol.data.dtype)
+        host[...] = vol.data
+        from .volume import Volume
+        pvol = Volume(dims=vol.dims, voxel_type=vol.voxel_type, spacing=vol.spacing,
+                      data=host, value_range=vol.value_range)
+        times, h2d, d2h = [], 0, 0
+        for _ in range(steps):
+            t.cuda.synchronize()
+            t0 = time.perf_counter()
+            if self.world == 1:
+                from .generate import generate_vdi
+                from .raycast import render_vdi
+                vdi, grid = generate_vdi(pvol, self.tf, self.gcam, self.params,
+                                         cache_volume=False)
+                c, s, g = vdi.counts, vdi.segs, grid.counts
+                img = render_vdi(vdi, grid, self.rcam, self.opts)
+                d2h = c.nbytes + s.nbytes + g.nbytes + img.data.nbytes
+            else:
+                self.vol_dev = dv.to_device(host)
+                self.step()
+                n_sg = self.params.n_sg
+                aos = t.empty((self.gen_rows * self.w, n_sg * 6), dtype=t.float32,
+                              device="cuda")
+                _capi.check(_capi.load().vdi_segs_to_aos(
+                    dv.ptr(self.bufs.segs), dv.ptr(aos), self.gen_rows * self.w, n_sg,
+                    dv.stream_handle()))
+                c = dv.to_host(self.bufs.counts, sync=False)
+                s = dv.to_host(aos, sync=False)
+                img = dv.to_host(self.image, sync=True)
+                d2h = c.nbytes + s.nbytes + img.nbytes
+            t.cuda.synchronize()
+            times.append(time.perf_counter() - t0)
+            h2d = host.nbytes + self.tf.lut.nbytes
+        dt = float(np.mean(times))
+        if self.world > 1:
+            x = t.tensor([dt], dtype=t.float64, device="cuda")
+            self.dist.all_reduce(x, op=self.dist.ReduceOp.MAX)
+            dt = float(x.item())
+        self.vol_dev, _ = dv.upload_volume(self.vol)
+        return {"value": 2 * self.w * self.h / dt / 1e6, "unit": "Mrays/s",
+                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                "ms_per_step": dt * 1e3, "steps": steps}
+
+
+def unshard_image(g_image, out_h: int, world: int):
+    """Gathered band-interleaved image rows -> natural order (host numpy)."""
+    idx = storage_rows(out_h, world)
+    return np.asarray(g_image)[idx]

@@ -56,7 +56,8 @@ class Volume:
         # `normalized` is materialised lazily: the device path uploads the raw
         # brick, so building a 4 B/voxel host copy of a 3 GiB volume up front
         # would only cost host RAM.
-        object.__setattr__(self, "_norm_derived", self.normalized is None)
+        object.__setattr__(self, "_norm_derived",
+                           object.__getattribute__(self, "normalized") is None)
 
     def __getattribute__(self, name):
         if name == "normalized":
