@@ -26,10 +26,11 @@
  *   - return 0 on success, < 0 on bad arguments (VDI_EINVAL) or a launch
  *     error (VDI_ELAUNCH); vdi_last_error() gives a thread-local message.
  *
- * Device segment layout (VDI_LAYOUT_LIST_SOA): each list owns n_sg*6 floats
- *   [front[0..n_sg) | back[0..n_sg) | rgba[0..n_sg) as float4]
+ * Device segment layout (VDI_LAYOUT_LIST_SOA): each list owns
+ * vdi_list_stride(n_sg) = round_up(6*n_sg, 4) floats
+ *   [rgba[0..n_sg) as float4 | front[0..n_sg) | back[0..n_sg) | pad]
  * so the Alg. 2 search touches only the contiguous `back` run and each
- * supersegment's colour is one 16-byte load. VDI_LAYOUT_AOS is the
+ * supersegment's colour is one aligned 16-byte load. VDI_LAYOUT_AOS is the
  * reference's [front, back, r, g, b, a] per supersegment.
  *
  * Row sharding: a "band map" (band_rows, band_stride, band_offset) selects
@@ -62,6 +63,9 @@ extern "C" {
 
 typedef void* vdi_stream_t; /* cudaStream_t */
 
+/* Floats per list in VDI_LAYOUT_LIST_SOA (16-byte aligned lists). */
+static inline int32_t vdi_list_stride(int32_t n_sg) { return (6 * n_sg + 3) & ~3; }
+
 /* Generation: one ray per viewport pixel, per-ray gamma bisection (Alg. 1 as
  * implemented in generate.py:219-273), supersegments written in
  * VDI_LAYOUT_LIST_SOA. Outputs are indexed by local row (band map). */
@@ -69,11 +73,13 @@ typedef struct VdiGenArgs {
   const void* volume;   /* (nz, ny, nx) x-fastest, voxel_type elements */
   const float* lut;     /* (lut_n, 4) f32, TransferFunction.lut */
   int32_t* counts;      /* OUT (local_h, width) */
-  float* segs;          /* OUT (local_h, width, n_sg*6) list-SoA */
+  float* segs;          /* OUT (local_h, width, vdi_list_stride(n_sg)) list-SoA */
   double* gammas;       /* OUT (local_h, width), may be NULL */
   int32_t* passes;      /* OUT (local_h, width), may be NULL */
   int32_t* samples;     /* OUT executed samples per ray (R's loop semantics), may be NULL */
-  void* workspace;      /* vdi_gen_workspace_bytes() bytes, any content */
+  void* workspace;      /* >= vdi_gen_workspace_bytes(args) bytes, any content:
+                           ray counter, 1/n table, per-lane sample cache */
+  size_t workspace_bytes;
   double pv[16];        /* generation proj*view */
   double inv_pv[16];
   double eye[3];

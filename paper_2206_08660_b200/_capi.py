@@ -21,7 +21,7 @@ _I = ctypes.c_int32
 class VdiGenArgs(ctypes.Structure):
     _fields_ = [
         ("volume", _P), ("lut", _P), ("counts", _P), ("segs", _P), ("gammas", _P),
-        ("passes", _P), ("samples", _P), ("workspace", _P),
+        ("passes", _P), ("samples", _P), ("workspace", _P), ("workspace_bytes", ctypes.c_size_t),
         ("pv", _D * 16), ("inv_pv", _D * 16), ("eye", _D * 3), ("aabb", _D * 6),
         ("eps", _D), ("gamma_init", _D), ("step", _D), ("lref", _D),
         ("voxel_type", _I), ("nx", _I), ("ny", _I), ("nz", _I), ("lut_n", _I),

@@ -28,7 +28,10 @@ const char* vdi_last_error(void) { return vdi::g_err; }
 
 int vdi_abi_version(void) { return VDI_ABI_VERSION; }
 
-size_t vdi_gen_workspace_bytes(const VdiGenArgs*) { return 256; }
+size_t vdi_gen_workspace_bytes(const VdiGenArgs* a) {
+  if (!a || !(a->step > 0)) return 0;
+  return vdi::gen_workspace_bytes(a);
+}
 
 int vdi_gen_launch(const VdiGenArgs* a, vdi_stream_t stream) {
   if (!a) return set_error(VDI_EINVAL, "null args");
@@ -43,8 +46,8 @@ int vdi_gen_launch(const VdiGenArgs* a, vdi_stream_t stream) {
   if (!(a->step > 0) || !(a->lref > 0)) return set_error(VDI_EINVAL, "step must be > 0");
   if (a->band_stride > 1 && (a->band_offset < 0 || a->band_offset >= a->band_stride))
     return set_error(VDI_EINVAL, "band_offset out of range");
-  if (reinterpret_cast<uintptr_t>(a->segs) % 16 != 0 || (a->n_sg * 6 * 4) % 16 != 0)
-    return set_error(VDI_EINVAL, "segs must be 16-byte aligned per list");
+  if (reinterpret_cast<uintptr_t>(a->segs) % 16 != 0)
+    return set_error(VDI_EINVAL, "segs must be 16-byte aligned");
   return vdi::gen_launch(a, static_cast<cudaStream_t>(stream));
 }
 
@@ -64,8 +67,8 @@ int vdi_render_launch(const VdiRenderArgs* a, vdi_stream_t stream) {
   if (a->vdi_w < 1 || a->vdi_h < 1 || a->n_sg < 1 || a->out_w < 1 || a->out_h < 1)
     return set_error(VDI_EINVAL, "bad sizes");
   if (a->gx < 1 || a->gy < 1 || a->gz < 1) return set_error(VDI_EINVAL, "bad grid dims");
-  if (reinterpret_cast<uintptr_t>(a->segs) % 16 != 0 || (a->n_sg * 6 * 4) % 16 != 0)
-    return set_error(VDI_EINVAL, "segs must be 16-byte aligned per list");
+  if (reinterpret_cast<uintptr_t>(a->segs) % 16 != 0)
+    return set_error(VDI_EINVAL, "segs must be 16-byte aligned");
   return vdi::render_launch(a, static_cast<cudaStream_t>(stream));
 }
 

@@ -96,6 +96,11 @@ __device__ __forceinline__ bool clip_frustum(const double* __restrict__ m, const
   return true;
 }
 
+// List-SoA offsets (include/vdi_b200.h): [rgba float4 | front | back | pad].
+__host__ __device__ __forceinline__ int list_stride(int n_sg) { return (6 * n_sg + 3) & ~3; }
+__host__ __device__ __forceinline__ int front_off(int n_sg) { return 4 * n_sg; }
+__host__ __device__ __forceinline__ int back_off(int n_sg) { return 5 * n_sg; }
+
 __device__ __forceinline__ double dmax(double a, double b) { return b > a ? b : a; }
 __device__ __forceinline__ double dmin(double a, double b) { return b < a ? b : a; }
 

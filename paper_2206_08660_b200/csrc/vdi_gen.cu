@@ -17,6 +17,22 @@
 // pass; the only case whose result is not the last pass's output (the
 // epsilon exit returning the cached high-gamma segments after a later
 // low-gamma pass) replays the high pass, which is deterministic.
+//
+// Sample cache: every bisection pass walks the same samples with a different
+// gamma, so each lane keeps the classified RGBA (f32, exactly what
+// _lut_classify returned) of its ray in an HBM scratch row; passes 2..k replay
+// it instead of re-sampling the volume (16 B per replayed sample instead of 8
+// voxel gathers + ~100 f64 ops). Transparent runs are stored run-length coded
+// (head entry holds the run length), so replay crosses empty space in O(1).
+// Replay is bit-identical by construction: the same f32 values enter the same
+// f64 expressions.
+//
+// Exact shortcuts (same bits as the reference, fewer instructions):
+//   * dist >= gamma  <=>  d2 >= thr(gamma), with thr the smallest double whose
+//     correctly rounded sqrt is >= gamma (sqrt_rn is monotone), computed once
+//     per pass;
+//   * 1.0 / nsamp is read from a table of host-identical IEEE quotients;
+//   * x / extent is x * (1 / extent) when the extent is a power of two.
 #include <cstdio>
 
 #include "vdi_common.cuh"
@@ -38,6 +54,10 @@ struct GenConst {
   int local_h;
   long long n_slots;  // tiles * 32
   unsigned long long* counter;
+  const double* inv_tab;  // inv_tab[n] == 1.0 / n, bit-exact (host IEEE division)
+  int inv_n;
+  int max_steps;          // per-lane sample-cache capacity
+  float4* cache;          // [lanes][max_steps] classified samples
 };
 
 template <int VT>
@@ -114,16 +134,32 @@ struct RayState {
   // ray geometry
   double o[3], d[3], t0, t1;
   int nsteps, k;
-  float* seg;  // this list's n_sg*6 floats (list-SoA)
+  float* seg;  // this list's list-SoA block
   long long list;
   // current pass (generate.py:97-106)
-  double gamma, fr_t, bk_t, mr, mg, mb, acc_r, acc_g, acc_b, acc_a, last_fr_t;
+  double gamma, thr, fr_t, bk_t, mr, mg, mb, acc_r, acc_g, acc_b, acc_a, last_fr_t;
   float prev_back;
   int count, nsamp, active, mode;
   // bisection (generate.py:230-236)
   double low, high, bis_gamma;
   int first, last_n, high_n, passes, buf_is_high, samples;
+  // sample cache frontier and the open transparent run at the frontier
+  int cached, run_head;
 };
+
+// Smallest double s >= 0 with sqrt_rn(s) >= g, so that sqrt_rn(d2) >= g <=>
+// d2 >= s for every d2 >= 0 (sqrt_rn is monotone non-decreasing).
+__device__ double split_threshold(double g) {
+  if (!(g > 0.0)) return -INFINITY;
+  double s = g * g;
+  while (sqrt(s) < g) s = nextafter(s, INFINITY);
+  while (true) {
+    const double p = nextafter(s, 0.0);
+    if (sqrt(p) >= g) s = p;
+    else break;
+  }
+  return s;
+}
 
 // generate.py:53-86 _emit into the list-SoA slot `count`.
 __device__ __forceinline__ void emit(const GenConst& c, RayState& s) {
@@ -143,9 +179,9 @@ __device__ __forceinline__ void emit(const GenConst& c, RayState& s) {
   if (g32 > a32) g32 = a32;
   if (b32 > a32) b32 = a32;
   const int n_sg = c.a.n_sg;
-  s.seg[s.count] = f;
-  s.seg[n_sg + s.count] = b;
-  reinterpret_cast<float4*>(s.seg + 2 * n_sg)[s.count] = make_float4(r32, g32, b32, a32);
+  s.seg[front_off(n_sg) + s.count] = f;
+  s.seg[back_off(n_sg) + s.count] = b;
+  reinterpret_cast<float4*>(s.seg)[s.count] = make_float4(r32, g32, b32, a32);
   s.prev_back = b;
   s.last_fr_t = s.fr_t;
   s.count += 1;
@@ -153,6 +189,7 @@ __device__ __forceinline__ void emit(const GenConst& c, RayState& s) {
 
 __device__ __forceinline__ void start_pass(RayState& s, double g, int mode) {
   s.gamma = g;
+  s.thr = split_threshold(g);
   s.mode = mode;
   s.k = 0;
   s.count = 0;
@@ -168,9 +205,9 @@ __device__ __forceinline__ void start_pass(RayState& s, double g, int mode) {
 __device__ void finish_ray(const GenConst& c, RayState& s, double g, int n) {
   const int n_sg = c.a.n_sg;
   for (int i = n; i < n_sg; ++i) {
-    s.seg[i] = 0.0f;
-    s.seg[n_sg + i] = 0.0f;
-    reinterpret_cast<float4*>(s.seg + 2 * n_sg)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    s.seg[front_off(n_sg) + i] = 0.0f;
+    s.seg[back_off(n_sg) + i] = 0.0f;
+    reinterpret_cast<float4*>(s.seg)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
   }
   c.a.counts[s.list] = n;
   if (c.a.gammas) c.a.gammas[s.list] = g;
@@ -263,6 +300,8 @@ __device__ bool setup_ray(const GenConst& c, RayState& s, int lx, int gy) {
   s.passes = 0;
   s.buf_is_high = 0;
   s.samples = 0;
+  s.cached = 0;
+  s.run_head = -1;
   start_pass(s, s.bis_gamma, kCount);
   return true;
 }
@@ -280,6 +319,9 @@ __global__ void __launch_bounds__(kGenThreads) gen_kernel(const GenConst c) {
   const int lane = threadIdx.x & 31;
   const int n_sg = c.a.n_sg;
   const double step = c.a.step;
+  const int max_steps = c.max_steps;
+  float4* const cache =
+      c.cache + ((long long)blockIdx.x * blockDim.x + threadIdx.x) * (long long)max_steps;
   // Warp-uniform ray pool: `pool` is the first index of the current 32-ray
   // chunk, `used` how many of it were handed out.
   long long pool = 0;
@@ -310,7 +352,7 @@ __global__ void __launch_bounds__(kGenThreads) gen_kernel(const GenConst c) {
           const int ly = (int)(tile / c.tiles_x) * kTileH + (w >> 3);
           if (lx < c.a.width && ly < c.local_h) {
             s.list = (long long)ly * c.a.width + lx;
-            s.seg = c.a.segs + s.list * (long long)(n_sg * 6);
+            s.seg = c.a.segs + s.list * (long long)list_stride(n_sg);
             const int gy = band_global_row(ly, c.a.band_rows, c.a.band_stride, c.a.band_offset);
             have = setup_ray(c, s, lx, gy);
             if (!have) {
@@ -331,8 +373,7 @@ __global__ void __launch_bounds__(kGenThreads) gen_kernel(const GenConst c) {
     if (__all_sync(0xffffffffu, done)) break;
     if (!have) continue;
 
-    // ---------------------------------------------------- one sample step
-    // (generate.py:111-212)
+    // ------------------------------------- one sample (generate.py:111-212)
     int ended = -1;  // >= 0: pass result
     const double ta = s.t0 + (double)s.k * step;
     double tb = ta + step;
@@ -340,25 +381,51 @@ __global__ void __launch_bounds__(kGenThreads) gen_kernel(const GenConst c) {
     if (tb <= ta) {
       ended = 0;
     } else {
-      if (s.mode != kRedo) s.samples += 1;
-      const double tm = 0.5 * (ta + tb);
-      double q[3];
+      float4 rgba;
+      int run = 1;
+      if (s.k < s.cached) {
+        rgba = cache[s.k];  // replay
+        if (rgba.w <= 0.0f) {
+          run = __float_as_int(rgba.x);
+          if (run < 1) run = 1;
+          if (run > s.cached - s.k) run = s.cached - s.k;
+        }
+      } else {
+        const double tm = 0.5 * (ta + tb);
+        double q[3];
 #pragma unroll
-      for (int a = 0; a < 3; ++a) {
-        const double num = s.o[a] + tm * s.d[a] - c.a.aabb[a];
-        double v = c.ext_pow2[a] ? num * c.inv_ext[a] : num / (c.a.aabb[3 + a] - c.a.aabb[a]);
-        if (v < 0.0) v = 0.0;
-        else if (v > 1.0) v = 1.0;
-        q[a] = v;
+        for (int a = 0; a < 3; ++a) {
+          const double num = s.o[a] + tm * s.d[a] - c.a.aabb[a];
+          double v = c.ext_pow2[a] ? num * c.inv_ext[a] : num / (c.a.aabb[3 + a] - c.a.aabb[a]);
+          if (v < 0.0) v = 0.0;
+          else if (v > 1.0) v = 1.0;
+          q[a] = v;
+        }
+        rgba = classify(s_lut, lut_n, trilinear<VT>(c, s_u8, q[0], q[1], q[2]));
+        if (s.k < max_steps) {
+          if (rgba.w <= 0.0f) {
+            cache[s.k] = make_float4(__int_as_float(1), 0.f, 0.f, 0.f);
+            if (s.run_head < 0) s.run_head = s.k;
+          } else {
+            cache[s.k] = rgba;
+            if (s.run_head >= 0) {  // close the transparent run
+              cache[s.run_head].x = __int_as_float(s.k - s.run_head);
+              s.run_head = -1;
+            }
+          }
+          s.cached = s.k + 1;
+        }
       }
-      const float4 rgba = classify(s_lut, lut_n, trilinear<VT>(c, s_u8, q[0], q[1], q[2]));
-      const double a = (double)rgba.w;
-      if (a <= 0.0) {
+      if (s.mode != kRedo) s.samples += run;
+      if (rgba.w <= 0.0f) {
+        // fully transparent: closes the open supersegment (generate.py:135-142)
         if (s.active) {
           emit(c, s);
           s.active = 0;
         }
+        s.k += run;
       } else {
+        const double a = (double)rgba.w;
         const double dt = tb - ta;
         const double e = c.lref_pow2 ? dt * c.inv_lref : dt / c.a.lref;
         const double om = 1.0 - a;
@@ -375,12 +442,12 @@ __global__ void __launch_bounds__(kGenThreads) gen_kernel(const GenConst c) {
               // reopen the last supersegment (generate.py:151-165)
               s.count -= 1;
               s.fr_t = s.last_fr_t;
-              const float4 l = reinterpret_cast<const float4*>(s.seg + 2 * n_sg)[s.count];
+              const float4 l = reinterpret_cast<const float4*>(s.seg)[s.count];
               s.acc_r = l.x;
               s.acc_g = l.y;
               s.acc_b = l.z;
               s.acc_a = l.w;
-              s.prev_back = s.count > 0 ? s.seg[n_sg + s.count - 1] : 0.0f;
+              s.prev_back = s.count > 0 ? s.seg[back_off(n_sg) + s.count - 1] : 0.0f;
               s.acc_r += (1.0 - s.acc_a) * sr;
               s.acc_g += (1.0 - s.acc_a) * sg;
               s.acc_b += (1.0 - s.acc_a) * sb;
@@ -398,8 +465,7 @@ __global__ void __launch_bounds__(kGenThreads) gen_kernel(const GenConst c) {
           }
         } else {
           const double dr = s.mr - sr, dg = s.mg - sg, db = s.mb - sb;
-          const double dist = sqrt(dr * dr + dg * dg + db * db);
-          if (dist >= s.gamma) {
+          if (dr * dr + dg * dg + db * db >= s.thr) {  // == sqrt(...) >= gamma
             if (s.count + 1 >= n_sg) {
               if (s.mode != kCapped) ended = n_sg + 1;
               else merge = true;
@@ -429,16 +495,15 @@ __global__ void __launch_bounds__(kGenThreads) gen_kernel(const GenConst c) {
           s.acc_a += (1.0 - s.acc_a) * a_adj;
           s.bk_t = tb;
           s.nsamp += 1;
-          const double inv = 1.0 / (double)s.nsamp;
+          const double inv =
+              s.nsamp < c.inv_n ? __ldg(c.inv_tab + s.nsamp) : 1.0 / (double)s.nsamp;
           s.mr += (sr - s.mr) * inv;
           s.mg += (sg - s.mg) * inv;
           s.mb += (sb - s.mb) * inv;
         }
+        if (ended < 0) s.k += 1;
       }
-      if (ended < 0) {
-        s.k += 1;
-        if (s.k >= s.nsteps) ended = 0;
-      }
+      if (ended < 0 && s.k >= s.nsteps) ended = 0;
     }
     if (ended >= 0) {
       int n = ended;
@@ -446,9 +511,61 @@ __global__ void __launch_bounds__(kGenThreads) gen_kernel(const GenConst c) {
         if (s.active) emit(c, s);
         n = s.count;
       }
+      // publish the open run's current length before any replay
+      if (s.run_head >= 0) cache[s.run_head].x = __int_as_float(s.cached - s.run_head);
       have = pass_done(c, s, n);
     }
   }
+}
+
+__global__ void fill_inv_kernel(double* tab, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) tab[i] = i > 0 ? 1.0 / (double)i : 0.0;
+}
+
+struct GenPlan {
+  void (*kern)(const GenConst);
+  long long blocks;
+  int max_steps, inv_n;
+  size_t off_inv, off_cache, total;
+  size_t smem;
+};
+
+static int plan_gen(const VdiGenArgs* a, GenPlan& p, long long n_slots) {
+  switch (a->voxel_type) {
+    case VDI_VOXEL_U8: p.kern = gen_kernel<VDI_VOXEL_U8>; break;
+    case VDI_VOXEL_U16: p.kern = gen_kernel<VDI_VOXEL_U16>; break;
+    case VDI_VOXEL_F32: p.kern = gen_kernel<VDI_VOXEL_F32>; break;
+    default: return set_error(VDI_EINVAL, "bad voxel_type %d", a->voxel_type);
+  }
+  int dev = 0, sms = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  p.smem = sizeof(float4) * a->lut_n;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, p.kern, kGenThreads, p.smem);
+  if (per_sm < 1) per_sm = 1;
+  // persistent grid: every resident slot, but no more warps than 32-ray chunks
+  p.blocks = (long long)sms * per_sm;
+  const long long need = (n_slots / 32 + (kGenThreads / 32) - 1) / (kGenThreads / 32);
+  if (n_slots >= 0 && p.blocks > need) p.blocks = need;
+  if (p.blocks < 1) p.blocks = 1;
+  // no ray has more samples than the box diagonal allows
+  const double ex = a->aabb[3] - a->aabb[0], ey = a->aabb[4] - a->aabb[1],
+               ez = a->aabb[5] - a->aabb[2];
+  const double diag = sqrt(ex * ex + ey * ey + ez * ez);
+  const double ms = ceil(diag / a->step) + 4.0;
+  p.max_steps = ms > 1e7 ? 10000000 : (int)ms;
+  p.inv_n = p.max_steps + 2;
+  p.off_inv = 256;
+  p.off_cache = (p.off_inv + sizeof(double) * p.inv_n + 255) & ~(size_t)255;
+  p.total = p.off_cache + sizeof(float4) * (size_t)p.max_steps * (size_t)p.blocks * kGenThreads;
+  return VDI_OK;
+}
+
+size_t gen_workspace_bytes(const VdiGenArgs* a) {
+  GenPlan p;
+  if (plan_gen(a, p, -1) != VDI_OK) return 0;
+  return p.total;
 }
 
 int gen_launch(const VdiGenArgs* a, cudaStream_t stream) {
@@ -473,31 +590,24 @@ int gen_launch(const VdiGenArgs* a, cudaStream_t stream) {
   c.tiles_x = (a->width + kTileW - 1) / kTileW;
   const long long tiles_y = (c.local_h + kTileH - 1) / kTileH;
   c.n_slots = (long long)c.tiles_x * tiles_y * 32;
-  c.counter = reinterpret_cast<unsigned long long*>(a->workspace);
   if (c.local_h <= 0) return VDI_OK;
+  GenPlan p;
+  int rc = plan_gen(a, p, c.n_slots);
+  if (rc != VDI_OK) return rc;
+  if (a->workspace_bytes < p.total)
+    return set_error(VDI_EINVAL, "workspace too small: %zu < %zu bytes", a->workspace_bytes,
+                     p.total);
+  char* ws = reinterpret_cast<char*>(a->workspace);
+  c.counter = reinterpret_cast<unsigned long long*>(ws);
+  c.inv_tab = reinterpret_cast<const double*>(ws + p.off_inv);
+  c.inv_n = p.inv_n;
+  c.max_steps = p.max_steps;
+  c.cache = reinterpret_cast<float4*>(ws + p.off_cache);
   cudaError_t err = cudaMemsetAsync(c.counter, 0, sizeof(unsigned long long), stream);
   if (err != cudaSuccess) return set_error(VDI_ELAUNCH, "gen memset: %s", cudaGetErrorString(err));
-
-  int dev = 0, sms = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const size_t smem = sizeof(float4) * a->lut_n;
-  int per_sm = 0;
-  void (*kern)(const GenConst) = nullptr;
-  switch (a->voxel_type) {
-    case VDI_VOXEL_U8: kern = gen_kernel<VDI_VOXEL_U8>; break;
-    case VDI_VOXEL_U16: kern = gen_kernel<VDI_VOXEL_U16>; break;
-    case VDI_VOXEL_F32: kern = gen_kernel<VDI_VOXEL_F32>; break;
-    default: return set_error(VDI_EINVAL, "bad voxel_type %d", a->voxel_type);
-  }
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kGenThreads, smem);
-  if (per_sm < 1) per_sm = 1;
-  // persistent grid: every resident slot, but no more warps than 32-ray chunks
-  long long blocks = (long long)sms * per_sm;
-  const long long need = (c.n_slots / 32 + (kGenThreads / 32) - 1) / (kGenThreads / 32);
-  if (blocks > need) blocks = need;
-  if (blocks < 1) blocks = 1;
-  kern<<<(unsigned)blocks, kGenThreads, smem, stream>>>(c);
+  fill_inv_kernel<<<(p.inv_n + 255) / 256, 256, 0, stream>>>(
+      reinterpret_cast<double*>(ws + p.off_inv), p.inv_n);
+  p.kern<<<(unsigned)p.blocks, kGenThreads, p.smem, stream>>>(c);
   err = cudaGetLastError();
   if (err != cudaSuccess) return set_error(VDI_ELAUNCH, "gen launch: %s", cudaGetErrorString(err));
   return VDI_OK;

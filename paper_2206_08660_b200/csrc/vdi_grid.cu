@@ -28,8 +28,9 @@ __global__ void grid_kernel(const GridConst c) {
   const int cy1 = (int)(((ly + 1) * a.gy - 1) / a.height);
   const int cx0 = (int)(((long long)lx * a.gx) / a.width);
   const int cx1 = (int)((((long long)lx + 1) * a.gx - 1) / a.width);
-  const float* fronts = a.segs + list * (long long)(a.n_sg * 6);
-  const float* backs = fronts + a.n_sg;
+  const float* ls = a.segs + list * (long long)list_stride(a.n_sg);
+  const float* fronts = ls + front_off(a.n_sg);
+  const float* backs = ls + back_off(a.n_sg);
   const double fn = a.far - a.near;
   for (int k = 0; k < n; ++k) {
     const double zf = fronts[k], zb = backs[k];
@@ -74,11 +75,11 @@ __global__ void soa_to_aos_kernel(const float* __restrict__ soa, float* __restri
   if (i >= n) return;
   const long long list = i / n_sg;
   const int k = (int)(i - list * n_sg);
-  const float* s = soa + list * n_sg * 6;
-  const float4 c = reinterpret_cast<const float4*>(s + 2 * n_sg)[k];
+  const float* s = soa + list * list_stride(n_sg);
+  const float4 c = reinterpret_cast<const float4*>(s)[k];
   float* o = aos + i * 6;
-  o[0] = s[k];
-  o[1] = s[n_sg + k];
+  o[0] = s[front_off(n_sg) + k];
+  o[1] = s[back_off(n_sg) + k];
   o[2] = c.x;
   o[3] = c.y;
   o[4] = c.z;
@@ -92,10 +93,12 @@ __global__ void aos_to_soa_kernel(const float* __restrict__ aos, float* __restri
   const long long list = i / n_sg;
   const int k = (int)(i - list * n_sg);
   const float* in = aos + i * 6;
-  float* s = soa + list * n_sg * 6;
-  s[k] = in[0];
-  s[n_sg + k] = in[1];
-  reinterpret_cast<float4*>(s + 2 * n_sg)[k] = make_float4(in[2], in[3], in[4], in[5]);
+  float* s = soa + list * list_stride(n_sg);
+  s[front_off(n_sg) + k] = in[0];
+  s[back_off(n_sg) + k] = in[1];
+  reinterpret_cast<float4*>(s)[k] = make_float4(in[2], in[3], in[4], in[5]);
+  if (k == 0)  // zero the alignment pad so the buffer is fully defined
+    for (int p = 6 * n_sg; p < list_stride(n_sg); ++p) s[p] = 0.0f;
 }
 
 int segs_convert(const float* src, float* dst, int64_t n_lists, int32_t n_sg, bool to_aos,

@@ -11,7 +11,7 @@
 //
 // Layout: lists are list-SoA (include/vdi_b200.h), so the search reads only
 // the contiguous back[] run of a list and a supersegment's colour is one
-// float4. A warp owns an 8x4 pixel tile; neighbouring pixels walk
+// aligned float4. A warp owns an 8x4 pixel tile; neighbouring pixels walk
 // neighbouring lists, which keeps the count/back/rgba loads L1-coherent.
 #include "vdi_common.cuh"
 #include "vdi_internal.h"
@@ -208,10 +208,10 @@ __global__ void __launch_bounds__(kRenderThreads) render_kernel(const RenderCons
           }
           if (search) {
             nsearch += 1;
-            const float* ls = a.segs + lidx * (long long)(n_sg * 6);
-            const float* fronts = ls;
-            const float* backs = ls + n_sg;
-            const float4* rgba = reinterpret_cast<const float4*>(ls + 2 * n_sg);
+            const float* ls = a.segs + lidx * (long long)list_stride(n_sg);
+            const float* fronts = ls + front_off(n_sg);
+            const float* backs = ls + back_off(n_sg);
+            const float4* rgba = reinterpret_cast<const float4*>(ls);
             int seed;
             const int j = find_first(fronts, backs, count, d_entry, d_exit, p, seed);
             p = seed;

@@ -20,6 +20,11 @@ from .vdi import AccelGrid, DeviceVdi, Vdi, default_grid_dims
 SQRT3 = 1.7320508075688772
 
 
+def list_stride(n_sg: int) -> int:
+    """Floats per list in the device list-SoA layout (vdi_list_stride)."""
+    return (6 * n_sg + 3) & ~3
+
+
 @dataclass(frozen=True)
 class GenParams:
     """generate.py:28-50."""
@@ -86,11 +91,11 @@ def alloc_gen(width, rows, n_sg, grid_dims, stats=True):
     gx, gy, gz = grid_dims
     return GenBuffers(
         counts=t.empty((rows, width), dtype=t.int32, device="cuda"),
-        segs=t.empty((rows * width, n_sg * 6), dtype=t.float32, device="cuda"),
+        segs=t.empty((rows * width, list_stride(n_sg)), dtype=t.float32, device="cuda"),
         gammas=t.empty((rows, width), dtype=t.float64, device="cuda") if stats else None,
         passes=t.empty((rows, width), dtype=t.int32, device="cuda") if stats else None,
         samples=t.empty((rows, width), dtype=t.int32, device="cuda") if stats else None,
-        workspace=t.empty(256, dtype=t.uint8, device="cuda"),
+        workspace=None,  # sized by vdi_gen_workspace_bytes at launch
         grid=t.empty((gz, gy, gx), dtype=t.int32, device="cuda"))
 
 
@@ -102,7 +107,6 @@ def gen_args(vol_dev, voxel_type, dims, lut_dev, cam, aabb, params_resolved, n_s
     a.volume, a.lut = dv.ptr(vol_dev), dv.ptr(lut_dev)
     a.counts, a.segs = dv.ptr(bufs.counts), dv.ptr(bufs.segs)
     a.gammas, a.passes, a.samples = dv.ptr(bufs.gammas), dv.ptr(bufs.passes), dv.ptr(bufs.samples)
-    a.workspace = dv.ptr(bufs.workspace)
     _capi.fill(a.pv, _mat(cam.proj_view()))
     _capi.fill(a.inv_pv, _mat(cam.inv_proj_view()))
     _capi.fill(a.eye, np.asarray(cam.position, dtype=np.float64))
@@ -140,6 +144,10 @@ def launch_generate(vol_dev, voxel_type, dims, lut_dev, cam, aabb, params, resol
     s = dv.stream_handle() if stream is None else stream
     a = gen_args(vol_dev, voxel_type, dims, lut_dev, cam, aabb, resolved, params.n_sg,
                  params.epsilon, params.gamma_init, bufs, band)
+    need = int(L.vdi_gen_workspace_bytes(a))
+    if bufs.workspace is None or bufs.workspace.numel() < need:
+        bufs.workspace = dv.torch().empty(need, dtype=dv.torch().uint8, device="cuda")
+    a.workspace, a.workspace_bytes = dv.ptr(bufs.workspace), int(bufs.workspace.numel())
     if split_events:
         split_events[1].record()
     _capi.check(L.vdi_gen_launch(a, s))

@@ -96,7 +96,7 @@ class Pipeline:
             import torch.distributed as tdist
             self.dist = tdist
             self.g_counts = t.empty((world * self.gen_rows, w), dtype=t.int32, device="cuda")
-            self.g_segs = t.empty((world * self.gen_rows * w, params.n_sg * 6),
+            self.g_segs = t.empty((world * self.gen_rows * w, self.bufs.segs.shape[1]),
                                   dtype=t.float32, device="cuda")
             self.g_image = t.empty((world * self.out_rows, ow, 4), dtype=t.float64,
                                    device="cuda")

@@ -100,7 +100,7 @@ class Vdi:
             h, w, n = self.height, self.width, self.n_sg
             counts = dv.to_device(np.ascontiguousarray(self._counts, np.int32))
             aos = dv.to_device(np.ascontiguousarray(self._segs, np.float32).reshape(h * w, n * 6))
-            soa = t.empty_like(aos)
+            soa = t.empty((h * w, (6 * n + 3) & ~3), dtype=t.float32, device="cuda")
             _capi.check(_capi.load().vdi_segs_from_aos(dv.ptr(aos), dv.ptr(soa), h * w, n,
                                                        dv.stream_handle()))
             self._device = DeviceVdi(counts=counts.view(h, w), segs=soa)
