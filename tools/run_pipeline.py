@@ -1,0 +1,24 @@
+"""Run generate (+ render) of a config a few times: the target command for ncu
+captures (`ncu ... python tools/run_pipeline.py --config C3 --reps 2`)."""
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
+
+from paper_2206_08660_b200 import shard, synth  # noqa: E402
+from paper_2206_08660_b200.generate import GenParams  # noqa: E402
+
+p = argparse.ArgumentParser()
+p.add_argument("--config", default="C3")
+p.add_argument("--reps", type=int, default=2)
+a = p.parse_args()
+vol, tf, gcam, rcam, n_sg = synth.config(a.config)
+pipe = shard.Pipeline(vol, tf, gcam, rcam, GenParams(n_sg=n_sg))
+for _ in range(a.reps):
+    ev = pipe.step(timed=True)
+    print({k: round(v, 3) for k, v in ev.items()}, flush=True)
+torch.cuda.synchronize()
+print("samples", pipe.samples_executed(), "render stats", pipe.render_stats())
