@@ -77,8 +77,11 @@ typedef struct VdiGenArgs {
   double* gammas;       /* OUT (local_h, width), may be NULL */
   int32_t* passes;      /* OUT (local_h, width), may be NULL */
   int32_t* samples;     /* OUT executed samples per ray (R's loop semantics), may be NULL */
-  void* workspace;      /* >= vdi_gen_workspace_bytes(args) bytes, any content:
-                           ray counter, 1/n table, per-lane sample cache */
+  void* workspace;      /* scratch, any content: queues, 1/n table, sample
+                           cache. vdi_gen_workspace_bytes() is the recommended
+                           size; less still works (rays that do not fit the
+                           cache take more rounds / the fused fallback) down
+                           to a minimum the launch checks (VDI_EINVAL). */
   size_t workspace_bytes;
   double pv[16];        /* generation proj*view */
   double inv_pv[16];
@@ -142,7 +145,9 @@ typedef struct VdiRenderArgs {
 const char* vdi_last_error(void);
 int vdi_abi_version(void);
 
+/* Recommended / minimum workspace bytes for `args` on the current device. */
 size_t vdi_gen_workspace_bytes(const VdiGenArgs* args);
+size_t vdi_gen_workspace_min_bytes(const VdiGenArgs* args);
 int vdi_gen_launch(const VdiGenArgs* args, vdi_stream_t stream);
 int vdi_grid_launch(const VdiGridArgs* args, vdi_stream_t stream);
 int vdi_render_launch(const VdiRenderArgs* args, vdi_stream_t stream);

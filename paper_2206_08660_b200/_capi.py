@@ -54,7 +54,8 @@ class VdiRenderArgs(ctypes.Structure):
     ]
 
 
-EXPORTS = ["vdi_last_error", "vdi_abi_version", "vdi_gen_workspace_bytes", "vdi_gen_launch",
+EXPORTS = ["vdi_last_error", "vdi_abi_version", "vdi_gen_workspace_bytes",
+           "vdi_gen_workspace_min_bytes", "vdi_gen_launch",
            "vdi_grid_launch", "vdi_render_launch", "vdi_find_first_batch",
            "vdi_segs_to_aos", "vdi_segs_from_aos"]
 
@@ -78,6 +79,8 @@ def load():
     L.vdi_abi_version.restype = ctypes.c_int
     L.vdi_gen_workspace_bytes.restype = ctypes.c_size_t
     L.vdi_gen_workspace_bytes.argtypes = [ctypes.POINTER(VdiGenArgs)]
+    L.vdi_gen_workspace_min_bytes.restype = ctypes.c_size_t
+    L.vdi_gen_workspace_min_bytes.argtypes = [ctypes.POINTER(VdiGenArgs)]
     L.vdi_gen_launch.argtypes = [ctypes.POINTER(VdiGenArgs), _P]
     L.vdi_grid_launch.argtypes = [ctypes.POINTER(VdiGridArgs), _P]
     L.vdi_render_launch.argtypes = [ctypes.POINTER(VdiRenderArgs), _P]

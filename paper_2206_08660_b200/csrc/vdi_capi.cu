@@ -30,7 +30,12 @@ int vdi_abi_version(void) { return VDI_ABI_VERSION; }
 
 size_t vdi_gen_workspace_bytes(const VdiGenArgs* a) {
   if (!a || !(a->step > 0)) return 0;
-  return vdi::gen_workspace_bytes(a);
+  return vdi::gen_workspace_bytes(a, 1);
+}
+
+size_t vdi_gen_workspace_min_bytes(const VdiGenArgs* a) {
+  if (!a || !(a->step > 0)) return 0;
+  return vdi::gen_workspace_bytes(a, 0);
 }
 
 int vdi_gen_launch(const VdiGenArgs* a, vdi_stream_t stream) {

@@ -7,32 +7,40 @@
 // f64 in the reference's order (no FMA: built with -fmad=false), f32 rounding
 // at the LUT output and at the segment store, exactly as numba does.
 //
-// B200 structure: the reference's two nested loops (passes x samples) are
-// flattened into a per-lane state machine whose every iteration is ONE sample.
-// A lane whose ray finishes refills from a warp-uniform pool of ray indices
-// (one atomicAdd per 32 rays), so the warp stays converged on the hot sample
-// body even though passes per ray are bimodal (1 vs 5-22).
-// Ray indices map to 8x4 pixel tiles so a warp's rays start spatially
-// coherent. Segments are written straight into the output list during every
-// pass; the only case whose result is not the last pass's output (the
-// epsilon exit returning the cached high-gamma segments after a later
-// low-gamma pass) replays the high pass, which is deterministic.
+// B200 structure. Every bisection pass walks the same samples with a new
+// gamma, so the work splits into (a) sampling the volume once per sample and
+// (b) replaying the per-sample segment logic per pass. Mixing both in one warp
+// serialises them (profiles/r01_gen_v1_fused_cache.md: 16.7 of 32 lanes
+// active), so generation runs in mode-coherent phases:
 //
-// Sample cache: every bisection pass walks the same samples with a different
-// gamma, so each lane keeps the classified RGBA (f32, exactly what
-// _lut_classify returned) of its ray in an HBM scratch row; passes 2..k replay
-// it instead of re-sampling the volume (16 B per replayed sample instead of 8
-// voxel gathers + ~100 f64 ops). Transparent runs are stored run-length coded
-// (head entry holds the run length), so replay crosses empty space in O(1).
+//   sample phase   one lane per ray (8x4 pixel tiles, lanes refill from a
+//                  warp-uniform ray pool): sample + classify every step and run
+//                  pass 1 (gamma_init) on the fly. Most rays finish here
+//                  (pass 1 not exceeding n_sg ends the bisection). A ray whose
+//                  pass 1 overflows gets an exact-size slot from a bump
+//                  allocator and re-walks its samples in fill mode, storing
+//                  the classified f32 RGBA (16 B) per sample; transparent runs
+//                  are stored run-length coded. It is then queued.
+//   bisect phase   replay-only lanes pull queued rays and run passes 2.. of the
+//                  bisection on the stored samples: 16 B per sample and ~35 f64
+//                  ops instead of 8 voxel gathers and ~120 f64 ops; transparent
+//                  runs cost O(1).
+//
+// The cache capacity is whatever workspace the caller provides; rays that do
+// not fit are deferred to the next round (up to kRounds), and anything left
+// after that runs in the fused fallback kernel (sampling and replay in one
+// lane, per-lane cache slot) -- same results, just slower.
+//
 // Replay is bit-identical by construction: the same f32 values enter the same
-// f64 expressions.
-//
-// Exact shortcuts (same bits as the reference, fewer instructions):
-//   * dist >= gamma  <=>  d2 >= thr(gamma), with thr the smallest double whose
-//     correctly rounded sqrt is >= gamma (sqrt_rn is monotone), computed once
-//     per pass;
-//   * 1.0 / nsamp is read from a table of host-identical IEEE quotients;
+// f64 expressions. Exact shortcuts (same bits, fewer instructions):
+//   * dist >= gamma  <=>  d2 >= thr(gamma), thr the smallest double whose
+//     correctly rounded sqrt is >= gamma (sqrt_rn is monotone); per pass;
+//   * 1.0 / nsamp comes from a table of host-identical IEEE quotients;
 //   * x / extent is x * (1 / extent) when the extent is a power of two.
+// Segments are written straight into the output list during every pass; the
+// only result that is not the last pass's output (the epsilon exit returning
+// the cached high-gamma segments after a later low-gamma pass) replays the
+// high pass, which is deterministic.
 #include <cstdio>
 
 #include "vdi_common.cuh"
@@ -41,8 +49,30 @@
 namespace vdi {
 
 constexpr int kGenThreads = 128;
+constexpr int kRounds = 3;
 
 enum PassMode : int { kCount = 0, kCapped = 1, kRedo = 2 };
+
+// A ray whose pass 1 overflowed, handed from the sample to the bisect phase.
+struct RayRec {
+  double d[3];
+  double t0, t1;
+  long long slot;  // first float4 of its cache run
+  int list;        // local list index (row * width + col)
+  int nsteps;      // samples stored
+  int samples1;    // samples executed by pass 1 (R semantics)
+  int pad;
+};
+
+// Per-round queues/counters (all zeroed at launch).
+struct RoundCtl {
+  unsigned long long fetch;     // sample-phase ray pool
+  unsigned long long bump;      // cache allocator (float4 units)
+  unsigned long long nrec;      // rays queued for the bisect phase
+  unsigned long long rfetch;    // bisect-phase pool
+  unsigned long long ndefer;    // rays deferred to the next round
+  unsigned long long pad[3];
+};
 
 struct GenConst {
   VdiGenArgs a;
@@ -53,11 +83,17 @@ struct GenConst {
   int tiles_x;
   int local_h;
   long long n_slots;  // tiles * 32
-  unsigned long long* counter;
   const double* inv_tab;  // inv_tab[n] == 1.0 / n, bit-exact (host IEEE division)
   int inv_n;
-  int max_steps;          // per-lane sample-cache capacity
-  float4* cache;          // [lanes][max_steps] classified samples
+  int max_steps;
+  float4* cache;
+  unsigned long long cache_cap;  // float4 entries
+  RayRec* recs;
+  int* defer_in;   // ray source of rounds >= 1 (local list indices)
+  int* defer_out;
+  RoundCtl* ctl;   // this round
+  RoundCtl* prev;  // previous round (its ndefer sizes defer_in)
+  int round;
 };
 
 template <int VT>
@@ -135,7 +171,7 @@ struct RayState {
   double o[3], d[3], t0, t1;
   int nsteps, k;
   float* seg;  // this list's list-SoA block
-  long long list;
+  int list;
   // current pass (generate.py:97-106)
   double gamma, thr, fr_t, bk_t, mr, mg, mb, acc_r, acc_g, acc_b, acc_a, last_fr_t;
   float prev_back;
@@ -143,8 +179,6 @@ struct RayState {
   // bisection (generate.py:230-236)
   double low, high, bis_gamma;
   int first, last_n, high_n, passes, buf_is_high, samples;
-  // sample cache frontier and the open transparent run at the frontier
-  int cached, run_head;
 };
 
 // Smallest double s >= 0 with sqrt_rn(s) >= g, so that sqrt_rn(d2) >= g <=>
@@ -159,6 +193,24 @@ __device__ double split_threshold(double g) {
     else break;
   }
   return s;
+}
+
+// Sample position -> classified RGBA (generate.py:118-134 + volume.py).
+template <int VT>
+__device__ __forceinline__ float4 sample_at(const GenConst& c, const float4* lut,
+                                            const float* tab, const RayState& s, double ta,
+                                            double tb) {
+  const double tm = 0.5 * (ta + tb);
+  double q[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const double num = s.o[a] + tm * s.d[a] - c.a.aabb[a];
+    double v = c.ext_pow2[a] ? num * c.inv_ext[a] : num / (c.a.aabb[3 + a] - c.a.aabb[a]);
+    if (v < 0.0) v = 0.0;
+    else if (v > 1.0) v = 1.0;
+    q[a] = v;
+  }
+  return classify(lut, c.a.lut_n, trilinear<VT>(c, tab, q[0], q[1], q[2]));
 }
 
 // generate.py:53-86 _emit into the list-SoA slot `count`.
@@ -198,6 +250,106 @@ __device__ __forceinline__ void start_pass(RayState& s, double g, int mode) {
   s.fr_t = s.bk_t = 0.0;
   s.mr = s.mg = s.mb = 0.0;
   s.acc_r = s.acc_g = s.acc_b = s.acc_a = 0.0;
+}
+
+// One sample of _gen_list_pass after classification (generate.py:135-212).
+// `run` >= 1 transparent samples are consumed at once (they only close the
+// open segment). Returns -1 to continue, else the pass result (0 = reached
+// the end: close with close_pass; n_sg + 1 = aborted counting pass);
+// advances s.k.
+__device__ __forceinline__ int segment_step(const GenConst& c, RayState& s, float4 rgba,
+                                            double ta, double tb, int run) {
+  const int n_sg = c.a.n_sg;
+  if (s.mode != kRedo) s.samples += run;
+  if (rgba.w <= 0.0f) {
+    // fully transparent: closes the open supersegment (generate.py:135-142)
+    if (s.active) {
+      emit(c, s);
+      s.active = 0;
+    }
+    s.k += run;
+    return s.k >= s.nsteps ? 0 : -1;
+  }
+  const double a = (double)rgba.w;
+  const double dt = tb - ta;
+  const double e = c.lref_pow2 ? dt * c.inv_lref : dt / c.a.lref;
+  const double om = 1.0 - a;
+  const double a_adj = 1.0 - (e == 1.0 ? om : pow(om, e));
+  const double sr = (double)rgba.x * a_adj;
+  const double sg = (double)rgba.y * a_adj;
+  const double sb = (double)rgba.z * a_adj;
+  bool merge = false, fresh = false;
+  if (!s.active) {
+    if (s.count >= n_sg) {
+      if (s.mode != kCapped) return n_sg + 1;
+      // reopen the last supersegment (generate.py:151-165)
+      s.count -= 1;
+      s.fr_t = s.last_fr_t;
+      const float4 l = reinterpret_cast<const float4*>(s.seg)[s.count];
+      s.acc_r = l.x;
+      s.acc_g = l.y;
+      s.acc_b = l.z;
+      s.acc_a = l.w;
+      s.prev_back = s.count > 0 ? s.seg[back_off(n_sg) + s.count - 1] : 0.0f;
+      s.acc_r += (1.0 - s.acc_a) * sr;
+      s.acc_g += (1.0 - s.acc_a) * sg;
+      s.acc_b += (1.0 - s.acc_a) * sb;
+      s.acc_a += (1.0 - s.acc_a) * a_adj;
+      s.bk_t = tb;
+      s.mr = sr;
+      s.mg = sg;
+      s.mb = sb;
+      s.nsamp = 1;
+      s.active = 1;
+    } else {
+      s.active = 1;
+      fresh = true;
+    }
+  } else {
+    const double dr = s.mr - sr, dg = s.mg - sg, db = s.mb - sb;
+    if (dr * dr + dg * dg + db * db >= s.thr) {  // == sqrt(...) >= gamma
+      if (s.count + 1 >= n_sg) {
+        if (s.mode != kCapped) return n_sg + 1;
+        merge = true;
+      } else {
+        emit(c, s);
+        fresh = true;
+      }
+    } else {
+      merge = true;
+    }
+  }
+  if (fresh) {
+    s.fr_t = ta;
+    s.bk_t = tb;
+    s.mr = sr;
+    s.mg = sg;
+    s.mb = sb;
+    s.nsamp = 1;
+    s.acc_r = sr;
+    s.acc_g = sg;
+    s.acc_b = sb;
+    s.acc_a = a_adj;
+  } else if (merge) {
+    s.acc_r += (1.0 - s.acc_a) * sr;
+    s.acc_g += (1.0 - s.acc_a) * sg;
+    s.acc_b += (1.0 - s.acc_a) * sb;
+    s.acc_a += (1.0 - s.acc_a) * a_adj;
+    s.bk_t = tb;
+    s.nsamp += 1;
+    const double inv = s.nsamp < c.inv_n ? __ldg(c.inv_tab + s.nsamp) : 1.0 / (double)s.nsamp;
+    s.mr += (sr - s.mr) * inv;
+    s.mg += (sg - s.mg) * inv;
+    s.mb += (sb - s.mb) * inv;
+  }
+  s.k += 1;
+  return s.k >= s.nsteps ? 0 : -1;
+}
+
+// Natural end (or the tb <= ta break, generate.py:113-117, 213-216).
+__device__ __forceinline__ int close_pass(const GenConst& c, RayState& s) {
+  if (s.active) emit(c, s);
+  return s.count;
 }
 
 // Zero-fill the unused tail and publish the per-ray outputs
@@ -277,20 +429,7 @@ __device__ bool pass_done(const GenConst& c, RayState& s, int n) {
   return bisect_next(c, s);
 }
 
-// Ray setup (generate.py:282-309). Returns false on a miss.
-__device__ bool setup_ray(const GenConst& c, RayState& s, int lx, int gy) {
-  pixel_ray(c.a.inv_pv, c.a.eye, lx, gy, c.a.width, c.a.height, s.d);
-  s.o[0] = c.a.eye[0];
-  s.o[1] = c.a.eye[1];
-  s.o[2] = c.a.eye[2];
-  double ta, tb, fa, fb;
-  if (!clip_aabb(s.o, s.d, c.a.aabb, ta, tb)) return false;
-  if (!clip_frustum(c.a.pv, s.o, s.d, fa, fb)) return false;
-  const double t0 = dmax(dmax(ta, fa), 0.0), t1 = dmin(tb, fb);
-  if (t1 <= t0) return false;
-  s.t0 = t0;
-  s.t1 = t1;
-  s.nsteps = (int)ceil((t1 - t0) / c.a.step);
+__device__ __forceinline__ void init_bisection(const GenConst& c, RayState& s) {
   s.low = 0.0;
   s.high = kSqrt3;
   s.bis_gamma = c.a.gamma_init;
@@ -300,81 +439,309 @@ __device__ bool setup_ray(const GenConst& c, RayState& s, int lx, int gy) {
   s.passes = 0;
   s.buf_is_high = 0;
   s.samples = 0;
-  s.cached = 0;
-  s.run_head = -1;
+}
+
+// Ray setup (generate.py:282-309) for local list `list`. Returns false on a
+// miss (the list is then published empty).
+__device__ bool setup_ray(const GenConst& c, RayState& s, int list) {
+  const int lx = list % c.a.width, ly = list / c.a.width;
+  const int gy = band_global_row(ly, c.a.band_rows, c.a.band_stride, c.a.band_offset);
+  s.list = list;
+  s.seg = c.a.segs + (long long)list * list_stride(c.a.n_sg);
+  pixel_ray(c.a.inv_pv, c.a.eye, lx, gy, c.a.width, c.a.height, s.d);
+  s.o[0] = c.a.eye[0];
+  s.o[1] = c.a.eye[1];
+  s.o[2] = c.a.eye[2];
+  double ta, tb, fa, fb;
+  bool hit = clip_aabb(s.o, s.d, c.a.aabb, ta, tb) && clip_frustum(c.a.pv, s.o, s.d, fa, fb);
+  double t0 = 0.0, t1 = 0.0;
+  if (hit) {
+    t0 = dmax(dmax(ta, fa), 0.0);
+    t1 = dmin(tb, fb);
+    hit = t1 > t0;
+  }
+  init_bisection(c, s);
+  if (!hit) {
+    finish_ray(c, s, 0.0, 0);
+    return false;
+  }
+  s.t0 = t0;
+  s.t1 = t1;
+  s.nsteps = (int)ceil((t1 - t0) / c.a.step);
   start_pass(s, s.bis_gamma, kCount);
   return true;
 }
 
-template <int VT>
-__global__ void __launch_bounds__(kGenThreads) gen_kernel(const GenConst c) {
-  extern __shared__ float4 s_lut[];
-  __shared__ float s_u8[256];
-  const int lut_n = c.a.lut_n;
-  for (int i = threadIdx.x; i < lut_n; i += blockDim.x)
+// Warp-uniform pool of work indices: one atomicAdd per 32 items. Lanes in
+// `need` receive consecutive indices. Must be called warp-converged.
+struct WarpPool {
+  long long base = 0;
+  int used = 32;
+  __device__ __forceinline__ long long take(unsigned need, int lane,
+                                            unsigned long long* counter) {
+    const int n = __popc(need);
+    const int rank = __popc(need & ((1u << lane) - 1u));
+    const int avail = 32 - used;
+    long long fresh = 0;
+    if (n > avail) {
+      if (lane == 0) fresh = (long long)atomicAdd(counter, 32ull);
+      fresh = __shfl_sync(0xffffffffu, fresh, 0);
+    }
+    const long long idx = rank < avail ? base + used + rank : fresh + (rank - avail);
+    if (n > avail) {
+      base = fresh;
+      used = n - avail;
+    } else {
+      used += n;
+    }
+    return idx;
+  }
+};
+
+// Round 0 enumerates 8x4 pixel tiles; later rounds the deferred list.
+// Returns a local list index, -1 for an empty slot, -2 when exhausted.
+__device__ __forceinline__ int source_list(const GenConst& c, long long slot) {
+  if (c.round == 0) {
+    if (slot >= c.n_slots) return -2;
+    const long long tile = slot >> 5;
+    const int w = (int)(slot & 31);
+    const int lx = (int)(tile % c.tiles_x) * kTileW + (w & 7);
+    const int ly = (int)(tile / c.tiles_x) * kTileH + (w >> 3);
+    return (lx < c.a.width && ly < c.local_h) ? ly * c.a.width + lx : -1;
+  }
+  if (slot >= (long long)c.prev->ndefer) return -2;
+  return c.defer_in[slot];
+}
+
+__device__ __forceinline__ void load_lut(const GenConst& c, float4* s_lut, float* s_u8) {
+  for (int i = threadIdx.x; i < c.a.lut_n; i += blockDim.x)
     s_lut[i] = reinterpret_cast<const float4*>(c.a.lut)[i];
   for (int i = threadIdx.x; i < 256; i += blockDim.x) s_u8[i] = __fdiv_rn((float)i, 255.0f);
   __syncthreads();
+}
 
+// ------------------------------------------------------------ sample phase
+template <int VT>
+__global__ void __launch_bounds__(kGenThreads) gen_sample_kernel(const GenConst c) {
+  extern __shared__ float4 s_lut[];
+  __shared__ float s_u8[256];
+  load_lut(c, s_lut, s_u8);
   const int lane = threadIdx.x & 31;
-  const int n_sg = c.a.n_sg;
   const double step = c.a.step;
-  const int max_steps = c.max_steps;
-  float4* const cache =
-      c.cache + ((long long)blockIdx.x * blockDim.x + threadIdx.x) * (long long)max_steps;
-  // Warp-uniform ray pool: `pool` is the first index of the current 32-ray
-  // chunk, `used` how many of it were handed out.
-  long long pool = 0;
-  int used = 32;
-  bool have = false, done = false;
+  WarpPool pool;
+  bool have = false, done = false, fill = false;
+  int run_head = -1, samples1 = 0;
+  long long slot0 = 0;
   RayState s;
 
   while (true) {
     const unsigned need = __ballot_sync(0xffffffffu, !have && !done);
     if (need) {
-      const int n = __popc(need);
-      const int rank = __popc(need & ((1u << lane) - 1u));
-      const int avail = 32 - used;
-      long long fresh = 0;
-      if (n > avail) {
-        if (lane == 0) fresh = (long long)atomicAdd(c.counter, 32ull);
-        fresh = __shfl_sync(0xffffffffu, fresh, 0);
-      }
+      const long long idx = pool.take(need, lane, &c.ctl->fetch);
       if ((need >> lane) & 1u) {
-        const long long slot = rank < avail ? pool + used + rank : fresh + (rank - avail);
-        if (slot >= c.n_slots) {
+        const int list = source_list(c, idx);
+        if (list == -2) {
           done = true;
-        } else {
-          // 8x4 pixel tiles in row-major tile order
-          const long long tile = slot >> 5;
-          const int w = (int)(slot & 31);
-          const int lx = (int)(tile % c.tiles_x) * kTileW + (w & 7);
-          const int ly = (int)(tile / c.tiles_x) * kTileH + (w >> 3);
-          if (lx < c.a.width && ly < c.local_h) {
-            s.list = (long long)ly * c.a.width + lx;
-            s.seg = c.a.segs + s.list * (long long)list_stride(n_sg);
-            const int gy = band_global_row(ly, c.a.band_rows, c.a.band_stride, c.a.band_offset);
-            have = setup_ray(c, s, lx, gy);
-            if (!have) {
-              s.passes = 0;
-              s.samples = 0;
-              finish_ray(c, s, 0.0, 0);
-            }
-          }
+        } else if (list >= 0) {
+          have = setup_ray(c, s, list);
+          fill = false;
         }
-      }
-      if (n > avail) {
-        pool = fresh;
-        used = n - avail;
-      } else {
-        used += n;
       }
     }
     if (__all_sync(0xffffffffu, done)) break;
     if (!have) continue;
 
-    // ------------------------------------- one sample (generate.py:111-212)
-    int ended = -1;  // >= 0: pass result
+    const double ta = s.t0 + (double)s.k * step;
+    double tb = ta + step;
+    if (tb > s.t1) tb = s.t1;
+    if (!fill) {
+      // pass 1 on the fly (gamma_init, counting mode)
+      int ended = 0;
+      if (tb > ta) {
+        const float4 rgba = sample_at<VT>(c, s_lut, s_u8, s, ta, tb);
+        ended = segment_step(c, s, rgba, ta, tb, 1);
+      }
+      if (ended < 0) continue;
+      if (ended == 0) ended = close_pass(c, s);
+      if (ended <= c.a.n_sg) {  // pass 1 fits: the bisection ends here
+        s.passes = 1;
+        finish_ray(c, s, s.bis_gamma, ended);
+        have = false;
+        continue;
+      }
+      // overflow: needs the bisection -> store its samples
+      samples1 = s.samples;
+      const unsigned long long at = atomicAdd(&c.ctl->bump, (unsigned long long)s.nsteps);
+      if (at + (unsigned long long)s.nsteps > c.cache_cap) {
+        const unsigned long long j = atomicAdd(&c.ctl->ndefer, 1ull);
+        c.defer_out[j] = s.list;
+        have = false;
+        continue;
+      }
+      slot0 = (long long)at;
+      fill = true;
+      run_head = -1;
+      s.k = 0;
+      continue;
+    }
+    // fill mode: classify step k and store it (transparent runs RLE-coded)
+    float4* cache = c.cache + slot0;
+    bool end = tb <= ta;
+    if (!end) {
+      const float4 rgba = sample_at<VT>(c, s_lut, s_u8, s, ta, tb);
+      if (rgba.w <= 0.0f) {
+        cache[s.k] = make_float4(__int_as_float(1), 0.f, 0.f, 0.f);
+        if (run_head < 0) run_head = s.k;
+      } else {
+        cache[s.k] = rgba;
+        if (run_head >= 0) {
+          cache[run_head].x = __int_as_float(s.k - run_head);
+          run_head = -1;
+        }
+      }
+      s.k += 1;
+      end = s.k >= s.nsteps;
+    }
+    if (end) {
+      if (run_head >= 0) cache[run_head].x = __int_as_float(s.k - run_head);
+      const unsigned long long j = atomicAdd(&c.ctl->nrec, 1ull);
+      RayRec r;
+      r.d[0] = s.d[0];
+      r.d[1] = s.d[1];
+      r.d[2] = s.d[2];
+      r.t0 = s.t0;
+      r.t1 = s.t1;
+      r.slot = slot0;
+      r.list = s.list;
+      r.nsteps = s.k;  // == samples stored (a tb <= ta break stops earlier)
+      r.samples1 = samples1;
+      r.pad = 0;
+      c.recs[j] = r;
+      have = false;
+    }
+  }
+}
+
+// ------------------------------------------------------------ bisect phase
+// Passes 2.. of rays queued by the sample phase, replayed from the cache.
+__global__ void __launch_bounds__(kGenThreads) gen_bisect_kernel(const GenConst c) {
+  const int lane = threadIdx.x & 31;
+  const double step = c.a.step;
+  const long long nrec = (long long)c.ctl->nrec;
+  WarpPool pool;
+  bool have = false, done = false;
+  const float4* cache = nullptr;
+  int stored = 0;
+  float4 next = make_float4(0.f, 0.f, 0.f, 0.f);  // prefetched entry next_k
+  int next_k = -1;
+  RayState s;
+
+  while (true) {
+    const unsigned need = __ballot_sync(0xffffffffu, !have && !done);
+    if (need) {
+      const long long idx = pool.take(need, lane, &c.ctl->rfetch);
+      if ((need >> lane) & 1u) {
+        if (idx >= nrec) {
+          done = true;
+        } else {
+          const RayRec r = c.recs[idx];
+          s.list = r.list;
+          s.seg = c.a.segs + (long long)r.list * list_stride(c.a.n_sg);
+          s.o[0] = c.a.eye[0];
+          s.o[1] = c.a.eye[1];
+          s.o[2] = c.a.eye[2];
+          s.d[0] = r.d[0];
+          s.d[1] = r.d[1];
+          s.d[2] = r.d[2];
+          s.t0 = r.t0;
+          s.t1 = r.t1;
+          s.nsteps = (int)ceil((r.t1 - r.t0) / c.a.step);
+          stored = r.nsteps;
+          cache = c.cache + r.slot;
+          // state after the overflowing pass 1 (generate.py:253-273)
+          init_bisection(c, s);
+          s.first = 0;
+          s.passes = 1;
+          s.last_n = c.a.n_sg + 1;
+          s.samples = r.samples1;
+          s.low = c.a.gamma_init;
+          s.bis_gamma = 0.5 * (s.low + s.high);
+          have = bisect_next(c, s);
+          next_k = -1;
+        }
+      }
+    }
+    if (__all_sync(0xffffffffu, done)) break;
+    if (!have) continue;
+
+    int ended;
+    if (s.k >= stored) {
+      ended = 0;  // the reference loop broke here (tb <= ta)
+    } else {
+      const float4 rgba = next_k == s.k ? next : cache[s.k];
+      const double ta = s.t0 + (double)s.k * step;
+      double tb = ta + step;
+      if (tb > s.t1) tb = s.t1;
+      int run = 1;
+      if (rgba.w <= 0.0f) {
+        run = __float_as_int(rgba.x);
+        if (run < 1) run = 1;
+        if (run > stored - s.k) run = stored - s.k;
+      }
+      // prefetch the entry after this one
+      const int nk = s.k + run;
+      if (nk < stored) {
+        next = cache[nk];
+        next_k = nk;
+      }
+      ended = segment_step(c, s, rgba, ta, tb, run);
+      if (ended < 0 && s.k >= stored) ended = 0;
+    }
+    if (ended >= 0) {
+      if (ended == 0) ended = close_pass(c, s);
+      have = pass_done(c, s, ended);
+      next_k = -1;
+    }
+  }
+}
+
+// ---------------------------------------------------------- fused fallback
+// Rays left over after kRounds (cache exhausted): sampling and replay in one
+// lane with a private cache slot of max_steps entries.
+template <int VT>
+__global__ void __launch_bounds__(kGenThreads) gen_fused_kernel(const GenConst c) {
+  extern __shared__ float4 s_lut[];
+  __shared__ float s_u8[256];
+  load_lut(c, s_lut, s_u8);
+  const int lane = threadIdx.x & 31;
+  const double step = c.a.step;
+  const int max_steps = c.max_steps;
+  float4* const cache =
+      c.cache + ((long long)blockIdx.x * blockDim.x + threadIdx.x) * (long long)max_steps;
+  WarpPool pool;
+  bool have = false, done = false;
+  int cached = 0, run_head = -1;
+  RayState s;
+
+  while (true) {
+    const unsigned need = __ballot_sync(0xffffffffu, !have && !done);
+    if (need) {
+      const long long idx = pool.take(need, lane, &c.ctl->fetch);
+      if ((need >> lane) & 1u) {
+        const int list = source_list(c, idx);
+        if (list == -2) {
+          done = true;
+        } else if (list >= 0) {
+          have = setup_ray(c, s, list);
+          cached = 0;
+          run_head = -1;
+        }
+      }
+    }
+    if (__all_sync(0xffffffffu, done)) break;
+    if (!have) continue;
+
+    int ended;
     const double ta = s.t0 + (double)s.k * step;
     double tb = ta + step;
     if (tb > s.t1) tb = s.t1;
@@ -383,137 +750,35 @@ __global__ void __launch_bounds__(kGenThreads) gen_kernel(const GenConst c) {
     } else {
       float4 rgba;
       int run = 1;
-      if (s.k < s.cached) {
-        rgba = cache[s.k];  // replay
+      if (s.k < cached) {
+        rgba = cache[s.k];
         if (rgba.w <= 0.0f) {
           run = __float_as_int(rgba.x);
           if (run < 1) run = 1;
-          if (run > s.cached - s.k) run = s.cached - s.k;
+          if (run > cached - s.k) run = cached - s.k;
         }
       } else {
-        const double tm = 0.5 * (ta + tb);
-        double q[3];
-#pragma unroll
-        for (int a = 0; a < 3; ++a) {
-          const double num = s.o[a] + tm * s.d[a] - c.a.aabb[a];
-          double v = c.ext_pow2[a] ? num * c.inv_ext[a] : num / (c.a.aabb[3 + a] - c.a.aabb[a]);
-          if (v < 0.0) v = 0.0;
-          else if (v > 1.0) v = 1.0;
-          q[a] = v;
-        }
-        rgba = classify(s_lut, lut_n, trilinear<VT>(c, s_u8, q[0], q[1], q[2]));
+        rgba = sample_at<VT>(c, s_lut, s_u8, s, ta, tb);
         if (s.k < max_steps) {
           if (rgba.w <= 0.0f) {
             cache[s.k] = make_float4(__int_as_float(1), 0.f, 0.f, 0.f);
-            if (s.run_head < 0) s.run_head = s.k;
+            if (run_head < 0) run_head = s.k;
           } else {
             cache[s.k] = rgba;
-            if (s.run_head >= 0) {  // close the transparent run
-              cache[s.run_head].x = __int_as_float(s.k - s.run_head);
-              s.run_head = -1;
+            if (run_head >= 0) {
+              cache[run_head].x = __int_as_float(s.k - run_head);
+              run_head = -1;
             }
           }
-          s.cached = s.k + 1;
+          cached = s.k + 1;
         }
       }
-      if (s.mode != kRedo) s.samples += run;
-      if (rgba.w <= 0.0f) {
-        // fully transparent: closes the open supersegment (generate.py:135-142)
-        if (s.active) {
-          emit(c, s);
-          s.active = 0;
-        }
-        s.k += run;
-      } else {
-        const double a = (double)rgba.w;
-        const double dt = tb - ta;
-        const double e = c.lref_pow2 ? dt * c.inv_lref : dt / c.a.lref;
-        const double om = 1.0 - a;
-        const double a_adj = 1.0 - (e == 1.0 ? om : pow(om, e));
-        const double sr = (double)rgba.x * a_adj;
-        const double sg = (double)rgba.y * a_adj;
-        const double sb = (double)rgba.z * a_adj;
-        bool merge = false, fresh_seg = false;
-        if (!s.active) {
-          if (s.count >= n_sg) {
-            if (s.mode != kCapped) {
-              ended = n_sg + 1;
-            } else {
-              // reopen the last supersegment (generate.py:151-165)
-              s.count -= 1;
-              s.fr_t = s.last_fr_t;
-              const float4 l = reinterpret_cast<const float4*>(s.seg)[s.count];
-              s.acc_r = l.x;
-              s.acc_g = l.y;
-              s.acc_b = l.z;
-              s.acc_a = l.w;
-              s.prev_back = s.count > 0 ? s.seg[back_off(n_sg) + s.count - 1] : 0.0f;
-              s.acc_r += (1.0 - s.acc_a) * sr;
-              s.acc_g += (1.0 - s.acc_a) * sg;
-              s.acc_b += (1.0 - s.acc_a) * sb;
-              s.acc_a += (1.0 - s.acc_a) * a_adj;
-              s.bk_t = tb;
-              s.mr = sr;
-              s.mg = sg;
-              s.mb = sb;
-              s.nsamp = 1;
-              s.active = 1;
-            }
-          } else {
-            s.active = 1;
-            fresh_seg = true;
-          }
-        } else {
-          const double dr = s.mr - sr, dg = s.mg - sg, db = s.mb - sb;
-          if (dr * dr + dg * dg + db * db >= s.thr) {  // == sqrt(...) >= gamma
-            if (s.count + 1 >= n_sg) {
-              if (s.mode != kCapped) ended = n_sg + 1;
-              else merge = true;
-            } else {
-              emit(c, s);
-              fresh_seg = true;
-            }
-          } else {
-            merge = true;
-          }
-        }
-        if (fresh_seg) {
-          s.fr_t = ta;
-          s.bk_t = tb;
-          s.mr = sr;
-          s.mg = sg;
-          s.mb = sb;
-          s.nsamp = 1;
-          s.acc_r = sr;
-          s.acc_g = sg;
-          s.acc_b = sb;
-          s.acc_a = a_adj;
-        } else if (merge) {
-          s.acc_r += (1.0 - s.acc_a) * sr;
-          s.acc_g += (1.0 - s.acc_a) * sg;
-          s.acc_b += (1.0 - s.acc_a) * sb;
-          s.acc_a += (1.0 - s.acc_a) * a_adj;
-          s.bk_t = tb;
-          s.nsamp += 1;
-          const double inv =
-              s.nsamp < c.inv_n ? __ldg(c.inv_tab + s.nsamp) : 1.0 / (double)s.nsamp;
-          s.mr += (sr - s.mr) * inv;
-          s.mg += (sg - s.mg) * inv;
-          s.mb += (sb - s.mb) * inv;
-        }
-        if (ended < 0) s.k += 1;
-      }
-      if (ended < 0 && s.k >= s.nsteps) ended = 0;
+      ended = segment_step(c, s, rgba, ta, tb, run);
     }
     if (ended >= 0) {
-      int n = ended;
-      if (n == 0) {  // natural end or tb <= ta break (generate.py:213-216)
-        if (s.active) emit(c, s);
-        n = s.count;
-      }
-      // publish the open run's current length before any replay
-      if (s.run_head >= 0) cache[s.run_head].x = __int_as_float(s.cached - s.run_head);
-      have = pass_done(c, s, n);
+      if (ended == 0) ended = close_pass(c, s);
+      if (run_head >= 0) cache[run_head].x = __int_as_float(cached - run_head);
+      have = pass_done(c, s, ended);
     }
   }
 }
@@ -523,32 +788,46 @@ __global__ void fill_inv_kernel(double* tab, int n) {
   if (i < n) tab[i] = i > 0 ? 1.0 / (double)i : 0.0;
 }
 
+// ------------------------------------------------------------------- host
+
 struct GenPlan {
-  void (*kern)(const GenConst);
-  long long blocks;
+  void (*sample)(const GenConst);
+  void (*fused)(const GenConst);
+  int sms, per_sm_sample, per_sm_bisect, per_sm_fused;
   int max_steps, inv_n;
-  size_t off_inv, off_cache, total;
+  long long n_rays;
+  size_t off_ctl, off_inv, off_recs, off_defer0, off_defer1, off_cache;
   size_t smem;
 };
 
-static int plan_gen(const VdiGenArgs* a, GenPlan& p, long long n_slots) {
+static int plan_gen(const VdiGenArgs* a, GenPlan& p) {
   switch (a->voxel_type) {
-    case VDI_VOXEL_U8: p.kern = gen_kernel<VDI_VOXEL_U8>; break;
-    case VDI_VOXEL_U16: p.kern = gen_kernel<VDI_VOXEL_U16>; break;
-    case VDI_VOXEL_F32: p.kern = gen_kernel<VDI_VOXEL_F32>; break;
-    default: return set_error(VDI_EINVAL, "bad voxel_type %d", a->voxel_type);
+    case VDI_VOXEL_U8:
+      p.sample = gen_sample_kernel<VDI_VOXEL_U8>;
+      p.fused = gen_fused_kernel<VDI_VOXEL_U8>;
+      break;
+    case VDI_VOXEL_U16:
+      p.sample = gen_sample_kernel<VDI_VOXEL_U16>;
+      p.fused = gen_fused_kernel<VDI_VOXEL_U16>;
+      break;
+    case VDI_VOXEL_F32:
+      p.sample = gen_sample_kernel<VDI_VOXEL_F32>;
+      p.fused = gen_fused_kernel<VDI_VOXEL_F32>;
+      break;
+    default:
+      return set_error(VDI_EINVAL, "bad voxel_type %d", a->voxel_type);
   }
-  int dev = 0, sms = 0, per_sm = 0;
+  int dev = 0;
   cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaDeviceGetAttribute(&p.sms, cudaDevAttrMultiProcessorCount, dev);
   p.smem = sizeof(float4) * a->lut_n;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, p.kern, kGenThreads, p.smem);
-  if (per_sm < 1) per_sm = 1;
-  // persistent grid: every resident slot, but no more warps than 32-ray chunks
-  p.blocks = (long long)sms * per_sm;
-  const long long need = (n_slots / 32 + (kGenThreads / 32) - 1) / (kGenThreads / 32);
-  if (n_slots >= 0 && p.blocks > need) p.blocks = need;
-  if (p.blocks < 1) p.blocks = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p.per_sm_sample, p.sample, kGenThreads, p.smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p.per_sm_bisect, gen_bisect_kernel, kGenThreads,
+                                                0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p.per_sm_fused, p.fused, kGenThreads, p.smem);
+  if (p.per_sm_sample < 1) p.per_sm_sample = 1;
+  if (p.per_sm_bisect < 1) p.per_sm_bisect = 1;
+  if (p.per_sm_fused < 1) p.per_sm_fused = 1;
   // no ray has more samples than the box diagonal allows
   const double ex = a->aabb[3] - a->aabb[0], ey = a->aabb[4] - a->aabb[1],
                ez = a->aabb[5] - a->aabb[2];
@@ -556,16 +835,35 @@ static int plan_gen(const VdiGenArgs* a, GenPlan& p, long long n_slots) {
   const double ms = ceil(diag / a->step) + 4.0;
   p.max_steps = ms > 1e7 ? 10000000 : (int)ms;
   p.inv_n = p.max_steps + 2;
-  p.off_inv = 256;
-  p.off_cache = (p.off_inv + sizeof(double) * p.inv_n + 255) & ~(size_t)255;
-  p.total = p.off_cache + sizeof(float4) * (size_t)p.max_steps * (size_t)p.blocks * kGenThreads;
+  const int bands = a->band_rows > 0 ? a->band_rows : 16;
+  p.n_rays = (long long)a->width *
+             local_rows(a->height, bands, a->band_stride > 0 ? a->band_stride : 1,
+                        a->band_offset);
+  auto up = [](size_t x) { return (x + 255) & ~(size_t)255; };
+  p.off_ctl = 0;
+  p.off_inv = up(sizeof(RoundCtl) * (kRounds + 1));
+  p.off_recs = up(p.off_inv + sizeof(double) * p.inv_n);
+  p.off_defer0 = up(p.off_recs + sizeof(RayRec) * (size_t)p.n_rays);
+  p.off_defer1 = up(p.off_defer0 + sizeof(int) * (size_t)p.n_rays);
+  p.off_cache = up(p.off_defer1 + sizeof(int) * (size_t)p.n_rays);
   return VDI_OK;
 }
 
-size_t gen_workspace_bytes(const VdiGenArgs* a) {
+// Minimum: room for one fused-fallback block of per-lane slots. Recommended:
+// enough cache that one round holds every overflowing ray of typical scenes
+// (~30% of rays x the longest chord), capped at 24 GiB.
+size_t gen_workspace_bytes(const VdiGenArgs* a, int recommended) {
   GenPlan p;
-  if (plan_gen(a, p, -1) != VDI_OK) return 0;
-  return p.total;
+  if (plan_gen(a, p) != VDI_OK) return 0;
+  const size_t min_cache = sizeof(float4) * (size_t)kGenThreads * (size_t)p.max_steps;
+  size_t rec = (size_t)(0.30 * (double)p.n_rays * (double)p.max_steps) * sizeof(float4);
+  const size_t fused_all = sizeof(float4) * (size_t)p.sms * p.per_sm_fused * kGenThreads *
+                           (size_t)p.max_steps;
+  if (rec < fused_all) rec = fused_all;
+  const size_t cap = (size_t)24 << 30;
+  if (rec > cap) rec = cap;
+  if (rec < min_cache) rec = min_cache;
+  return p.off_cache + (recommended ? rec : min_cache);
 }
 
 int gen_launch(const VdiGenArgs* a, cudaStream_t stream) {
@@ -592,22 +890,57 @@ int gen_launch(const VdiGenArgs* a, cudaStream_t stream) {
   c.n_slots = (long long)c.tiles_x * tiles_y * 32;
   if (c.local_h <= 0) return VDI_OK;
   GenPlan p;
-  int rc = plan_gen(a, p, c.n_slots);
+  int rc = plan_gen(&c.a, p);
   if (rc != VDI_OK) return rc;
-  if (a->workspace_bytes < p.total)
+  const size_t need = gen_workspace_bytes(&c.a, 0);
+  if (a->workspace_bytes < need)
     return set_error(VDI_EINVAL, "workspace too small: %zu < %zu bytes", a->workspace_bytes,
-                     p.total);
+                     need);
   char* ws = reinterpret_cast<char*>(a->workspace);
-  c.counter = reinterpret_cast<unsigned long long*>(ws);
+  RoundCtl* ctl = reinterpret_cast<RoundCtl*>(ws + p.off_ctl);
   c.inv_tab = reinterpret_cast<const double*>(ws + p.off_inv);
   c.inv_n = p.inv_n;
   c.max_steps = p.max_steps;
+  c.recs = reinterpret_cast<RayRec*>(ws + p.off_recs);
   c.cache = reinterpret_cast<float4*>(ws + p.off_cache);
-  cudaError_t err = cudaMemsetAsync(c.counter, 0, sizeof(unsigned long long), stream);
+  c.cache_cap = (a->workspace_bytes - p.off_cache) / sizeof(float4);
+  int* defer[2] = {reinterpret_cast<int*>(ws + p.off_defer0),
+                   reinterpret_cast<int*>(ws + p.off_defer1)};
+
+  cudaError_t err = cudaMemsetAsync(ctl, 0, sizeof(RoundCtl) * (kRounds + 1), stream);
   if (err != cudaSuccess) return set_error(VDI_ELAUNCH, "gen memset: %s", cudaGetErrorString(err));
   fill_inv_kernel<<<(p.inv_n + 255) / 256, 256, 0, stream>>>(
       reinterpret_cast<double*>(ws + p.off_inv), p.inv_n);
-  p.kern<<<(unsigned)p.blocks, kGenThreads, p.smem, stream>>>(c);
+
+  const long long chunks = c.n_slots / 32;
+  auto grid_for = [&](int per_sm, long long items) {
+    long long b = (long long)p.sms * per_sm;
+    const long long need_b = (items + (kGenThreads / 32) - 1) / (kGenThreads / 32);
+    if (items >= 0 && b > need_b) b = need_b;
+    return (unsigned)(b < 1 ? 1 : b);
+  };
+  for (int r = 0; r < kRounds; ++r) {
+    c.round = r;
+    c.ctl = ctl + r;
+    c.prev = r > 0 ? ctl + r - 1 : ctl;
+    c.defer_in = defer[(r + 1) & 1];
+    c.defer_out = defer[r & 1];
+    p.sample<<<grid_for(p.per_sm_sample, r == 0 ? chunks : -1), kGenThreads, p.smem, stream>>>(c);
+    gen_bisect_kernel<<<grid_for(p.per_sm_bisect, -1), kGenThreads, 0, stream>>>(c);
+  }
+  // leftovers: the fused kernel over the last round's deferred rays
+  c.round = kRounds;
+  c.ctl = ctl + kRounds;
+  c.prev = ctl + kRounds - 1;
+  c.defer_in = defer[(kRounds - 1) & 1];
+  c.defer_out = defer[kRounds & 1];
+  {
+    long long blocks = (long long)(c.cache_cap / (unsigned long long)p.max_steps) / kGenThreads;
+    const long long full = (long long)p.sms * p.per_sm_fused;
+    if (blocks > full) blocks = full;
+    if (blocks < 1) return set_error(VDI_EINVAL, "workspace cannot hold one fallback block");
+    p.fused<<<(unsigned)blocks, kGenThreads, p.smem, stream>>>(c);
+  }
   err = cudaGetLastError();
   if (err != cudaSuccess) return set_error(VDI_ELAUNCH, "gen launch: %s", cudaGetErrorString(err));
   return VDI_OK;

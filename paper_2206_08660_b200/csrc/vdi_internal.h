@@ -21,7 +21,7 @@ inline int local_rows(int h, int band_rows, int stride, int offset) {
 }
 
 int gen_launch(const VdiGenArgs* a, cudaStream_t stream);
-size_t gen_workspace_bytes(const VdiGenArgs* a);
+size_t gen_workspace_bytes(const VdiGenArgs* a, int recommended);
 int grid_launch(const VdiGridArgs* a, cudaStream_t stream);
 int render_launch(const VdiRenderArgs* a, cudaStream_t stream);
 int find_first_batch(const float* fronts, const float* backs, const int32_t* counts,

@@ -136,15 +136,21 @@ def grid_args(bufs: GenBuffers, cam, width, height, n_sg, grid_dims, band=(16, 1
 
 def launch_generate(vol_dev, voxel_type, dims, lut_dev, cam, aabb, params, resolved,
                     bufs: GenBuffers, grid_dims, band=(16, 1, 0), stream=None,
-                    split_events=None):
+                    split_events=None, workspace_bytes=None):
     """Enqueue generation + grid on the current stream (no sync, no alloc).
     split_events: optional CUDA events; [1] and [2] bracket the generation
-    kernel (timing only)."""
+    kernel (timing only). workspace_bytes overrides the recommended scratch
+    size ("min" = the smallest accepted, which forces deferral rounds)."""
     L = _capi.load()
     s = dv.stream_handle() if stream is None else stream
     a = gen_args(vol_dev, voxel_type, dims, lut_dev, cam, aabb, resolved, params.n_sg,
                  params.epsilon, params.gamma_init, bufs, band)
-    need = int(L.vdi_gen_workspace_bytes(a))
+    if workspace_bytes == "min":
+        need = int(L.vdi_gen_workspace_min_bytes(a))
+    elif workspace_bytes is not None:
+        need = int(workspace_bytes)
+    else:
+        need = int(L.vdi_gen_workspace_bytes(a))
     if bufs.workspace is None or bufs.workspace.numel() < need:
         bufs.workspace = dv.torch().empty(need, dtype=dv.torch().uint8, device="cuda")
     a.workspace, a.workspace_bytes = dv.ptr(bufs.workspace), int(bufs.workspace.numel())

@@ -176,3 +176,28 @@ def test_c3_full_size_properties_and_row_sample():
     img, rs = vb.render_vdi(vdi, grid, rcam, with_stats=True)
     assert rs.lists_visited > 0 and rs.supersegments_intersected > 0
     assert np.all(np.isfinite(img.data)) and img.data[..., 3].max() <= 1 + 1e-9
+
+
+@pytest.mark.parametrize("case", ["c1_blobs64", "bands64_u16_nsg4"])
+def test_generate_with_minimal_workspace_defers_but_matches(case):
+    """A cache too small for the overflowing rays forces the deferral rounds
+    and the fused fallback kernel; results must not change."""
+    from paper_2206_08660_b200 import device as dv
+    from paper_2206_08660_b200.generate import alloc_gen, launch_generate
+    g = gio.load(case)
+    vol, tf = _volume(g), _tf(g)
+    cam = gio.camera(g, "gen")
+    params = vb.GenParams(n_sg=int(g["n_sg"]), delta=int(g["delta"]), epsilon=float(g["eps"]))
+    w, h = cam.viewport
+    dims = tuple(int(v) for v in g["grid_dims"])
+    bufs = alloc_gen(w, h, params.n_sg, dims, stats=True)
+    vd, vt = dv.upload_volume(vol)
+    launch_generate(vd, vt, vol.dims, dv.upload_lut(tf.lut), cam, vol.aabb, params,
+                    params.resolve(vol), bufs, dims, workspace_bytes="min")
+    d = vb.vdi.DeviceVdi(bufs.counts, bufs.segs)
+    vdi = vb.Vdi(w, h, params.n_sg, None, None, cam, vol.aabb, _device=d)
+    assert np.array_equal(vdi.counts, g["counts"])
+    assert np.array_equal(vdi.segs.view(np.uint32), gio.expected_segs(g).view(np.uint32))
+    assert np.array_equal(dv.to_host(bufs.passes), g["passes"])
+    assert np.array_equal(dv.to_host(bufs.samples), g["samples"])
+    assert np.array_equal(dv.to_host(bufs.gammas).view(np.uint64), g["gammas"].view(np.uint64))
