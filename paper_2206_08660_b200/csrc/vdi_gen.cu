@@ -53,16 +53,25 @@ constexpr int kRounds = 3;
 
 enum PassMode : int { kCount = 0, kCapped = 1, kRedo = 2 };
 
-// A ray whose pass 1 overflowed, handed from the sample to the bisect phase.
+// A ray whose pass 1 overflowed, handed from the sample phase to the bisect
+// phase, and from there (with the deciding gamma) to the emit phase.
 struct RayRec {
   double d[3];
   double t0, t1;
-  long long slot;  // first float4 of its cache run
-  int list;        // local list index (row * width + col)
-  int nsteps;      // samples stored
-  int samples1;    // samples executed by pass 1 (R semantics)
+  double g_final;   // gamma of the pass whose segments are the result
+  long long slot;   // first float4 of its cache run
+  int list;         // local list index (row * width + col)
+  int nsteps;       // samples stored
+  int samples;      // samples executed so far (R semantics)
+  int passes;       // passes so far (R semantics)
+  int mode_final;   // kCount (window hit / cached high) or kCapped
   int pad;
 };
+
+// Cache entry of a non-transparent sample: the classified f32 RGBA, with the
+// sign bit of r (r >= 0 always) set when the step's opacity exponent
+// (tb - ta) / lref is not exactly 1, i.e. when the replay needs pow().
+__device__ __forceinline__ bool entry_needs_pow(float4 e) { return signbit(e.x); }
 
 // Per-round queues/counters (all zeroed at launch).
 struct RoundCtl {
@@ -71,7 +80,8 @@ struct RoundCtl {
   unsigned long long nrec;      // rays queued for the bisect phase
   unsigned long long rfetch;    // bisect-phase pool
   unsigned long long ndefer;    // rays deferred to the next round
-  unsigned long long pad[3];
+  unsigned long long efetch;    // emit-phase pool
+  unsigned long long pad[2];
 };
 
 struct GenConst {
@@ -593,7 +603,11 @@ __global__ void __launch_bounds__(kGenThreads) gen_sample_kernel(const GenConst 
         cache[s.k] = make_float4(__int_as_float(1), 0.f, 0.f, 0.f);
         if (run_head < 0) run_head = s.k;
       } else {
-        cache[s.k] = rgba;
+        const double dt = tb - ta;
+        const double e = c.lref_pow2 ? dt * c.inv_lref : dt / c.a.lref;
+        float4 st = rgba;
+        if (e != 1.0) st.x = __int_as_float(__float_as_int(st.x) | 0x80000000);
+        cache[s.k] = st;
         if (run_head >= 0) {
           cache[run_head].x = __int_as_float(s.k - run_head);
           run_head = -1;
@@ -614,7 +628,10 @@ __global__ void __launch_bounds__(kGenThreads) gen_sample_kernel(const GenConst 
       r.slot = slot0;
       r.list = s.list;
       r.nsteps = s.k;  // == samples stored (a tb <= ta break stops earlier)
-      r.samples1 = samples1;
+      r.samples = samples1;
+      r.passes = 1;
+      r.g_final = 0.0;
+      r.mode_final = kCount;
       r.pad = 0;
       c.recs[j] = r;
       have = false;
@@ -623,8 +640,181 @@ __global__ void __launch_bounds__(kGenThreads) gen_sample_kernel(const GenConst 
 }
 
 // ------------------------------------------------------------ bisect phase
-// Passes 2.. of rays queued by the sample phase, replayed from the cache.
+// Passes 2.. of the bisection (generate.py:237-273) for the queued rays, as
+// COUNT-ONLY replays: a counting pass's decisions (split, abort, transparent
+// close) depend only on the running mean of premultiplied samples, never on
+// the accumulated colour or the stored segments, so n(gamma) needs 8 state
+// registers and no writes. The deciding (gamma, mode) is handed to the emit
+// phase, which re-runs that one pass with full logic.
+struct CountPass {
+  double mr, mg, mb, thr;
+  int count, nsamp, k;
+  bool active;
+};
+
 __global__ void __launch_bounds__(kGenThreads) gen_bisect_kernel(const GenConst c) {
+  const int lane = threadIdx.x & 31;
+  const long long nrec = (long long)c.ctl->nrec;
+  const int n_sg = c.a.n_sg;
+  WarpPool pool;
+  bool have = false, done = false;
+  const float4* cache = nullptr;
+  RayRec* rec = nullptr;
+  int stored = 0;
+  // bisection state (generate.py:230-236)
+  double low = 0.0, high = 0.0, gamma = 0.0;
+  int last_n = 0, high_n = 0, passes = 0, samples = 0;
+  CountPass p;
+
+  while (true) {
+    const unsigned need = __ballot_sync(0xffffffffu, !have && !done);
+    if (need) {
+      const long long idx = pool.take(need, lane, &c.ctl->rfetch);
+      if ((need >> lane) & 1u) {
+        if (idx >= nrec) {
+          done = true;
+        } else {
+          rec = c.recs + idx;
+          cache = c.cache + rec->slot;
+          stored = rec->nsteps;
+          // state after the overflowing pass 1 (generate.py:253-273)
+          low = c.a.gamma_init;
+          high = kSqrt3;
+          gamma = 0.5 * (low + high);
+          last_n = n_sg + 1;
+          high_n = -1;
+          passes = rec->passes;
+          samples = rec->samples;
+          have = true;
+          p.k = -1;  // -> top of the bisection loop
+        }
+      }
+    }
+    if (__all_sync(0xffffffffu, done)) break;
+    if (!have) continue;
+
+    int n = -1;
+    if (p.k < 0) {
+      // top of the bisection loop: epsilon exit or a new counting pass
+      if (fabs(high - low) < c.a.eps) {
+        if (last_n == 0) {
+          rec->g_final = low;
+          rec->mode_final = kCapped;
+          passes += 1;
+        } else if (high_n >= 0) {
+          rec->g_final = high;  // the cached high-gamma segments
+          rec->mode_final = kCount;
+        } else {
+          rec->g_final = high;
+          rec->mode_final = kCapped;
+          passes += 1;
+        }
+        rec->passes = passes;
+        rec->samples = samples;
+        have = false;
+        continue;
+      }
+      p.thr = split_threshold(gamma);
+      p.count = 0;
+      p.nsamp = 0;
+      p.k = 0;
+      p.active = false;
+      p.mr = p.mg = p.mb = 0.0;
+    }
+    if (p.k >= stored) {
+      n = p.count + (p.active ? 1 : 0);  // natural end (or the tb <= ta break)
+      samples += stored;
+    } else {
+      const float4 e = cache[p.k];
+      if (e.w <= 0.0f) {
+        int run = __float_as_int(e.x);
+        if (run < 1) run = 1;
+        if (run > stored - p.k) run = stored - p.k;
+        if (p.active) {
+          p.count += 1;  // the transparent sample closes the segment
+          p.active = false;
+        }
+        p.k += run;
+      } else {
+        const double a = (double)e.w;
+        double a_adj;
+        if (entry_needs_pow(e)) {
+          const double ta = rec->t0 + (double)p.k * c.a.step;
+          double tb = ta + c.a.step;
+          if (tb > rec->t1) tb = rec->t1;
+          const double dt = tb - ta;
+          const double ex = c.lref_pow2 ? dt * c.inv_lref : dt / c.a.lref;
+          a_adj = 1.0 - pow(1.0 - a, ex);
+        } else {
+          a_adj = 1.0 - (1.0 - a);
+        }
+        const double sr = (double)fabsf(e.x) * a_adj;
+        const double sg = (double)e.y * a_adj;
+        const double sb = (double)e.z * a_adj;
+        bool fresh;
+        if (!p.active) {
+          if (p.count >= n_sg) {
+            n = n_sg + 1;
+          }
+          fresh = true;
+        } else {
+          const double dr = p.mr - sr, dg = p.mg - sg, db = p.mb - sb;
+          if (dr * dr + dg * dg + db * db >= p.thr) {
+            if (p.count + 1 >= n_sg) n = n_sg + 1;
+            else p.count += 1;
+            fresh = true;
+          } else {
+            fresh = false;
+          }
+        }
+        if (n < 0) {
+          if (fresh) {
+            p.active = true;
+            p.mr = sr;
+            p.mg = sg;
+            p.mb = sb;
+            p.nsamp = 1;
+          } else {
+            p.nsamp += 1;
+            const double inv =
+                p.nsamp < c.inv_n ? __ldg(c.inv_tab + p.nsamp) : 1.0 / (double)p.nsamp;
+            p.mr += (sr - p.mr) * inv;
+            p.mg += (sg - p.mg) * inv;
+            p.mb += (sb - p.mb) * inv;
+          }
+          p.k += 1;
+        } else {
+          samples += p.k + 1;  // aborted at sample k
+        }
+      }
+    }
+    if (n >= 0) {
+      // end of a counting pass (generate.py:258-273)
+      passes += 1;
+      last_n = n;
+      if (n > n_sg) {
+        low = gamma;
+      } else if (n < n_sg - c.a.delta) {
+        high = gamma;
+        high_n = n;
+      } else {
+        rec->g_final = gamma;  // window hit: this pass's segments
+        rec->mode_final = kCount;
+        rec->passes = passes;
+        rec->samples = samples;
+        have = false;
+        continue;
+      }
+      gamma = 0.5 * (low + high);
+      p.k = -1;
+    }
+  }
+}
+
+// -------------------------------------------------------------- emit phase
+// The deciding pass of every queued ray, replayed with the full
+// _gen_list_pass logic: segments, counts, gammas, passes, samples.
+__global__ void __launch_bounds__(kGenThreads) gen_emit_kernel(const GenConst c) {
   const int lane = threadIdx.x & 31;
   const double step = c.a.step;
   const long long nrec = (long long)c.ctl->nrec;
@@ -632,14 +822,13 @@ __global__ void __launch_bounds__(kGenThreads) gen_bisect_kernel(const GenConst 
   bool have = false, done = false;
   const float4* cache = nullptr;
   int stored = 0;
-  float4 next = make_float4(0.f, 0.f, 0.f, 0.f);  // prefetched entry next_k
-  int next_k = -1;
+  double g = 0.0;
   RayState s;
 
   while (true) {
     const unsigned need = __ballot_sync(0xffffffffu, !have && !done);
     if (need) {
-      const long long idx = pool.take(need, lane, &c.ctl->rfetch);
+      const long long idx = pool.take(need, lane, &c.ctl->efetch);
       if ((need >> lane) & 1u) {
         if (idx >= nrec) {
           done = true;
@@ -655,19 +844,17 @@ __global__ void __launch_bounds__(kGenThreads) gen_bisect_kernel(const GenConst 
           s.d[2] = r.d[2];
           s.t0 = r.t0;
           s.t1 = r.t1;
-          s.nsteps = (int)ceil((r.t1 - r.t0) / c.a.step);
+          s.nsteps = r.nsteps;
           stored = r.nsteps;
           cache = c.cache + r.slot;
-          // state after the overflowing pass 1 (generate.py:253-273)
           init_bisection(c, s);
-          s.first = 0;
-          s.passes = 1;
-          s.last_n = c.a.n_sg + 1;
-          s.samples = r.samples1;
-          s.low = c.a.gamma_init;
-          s.bis_gamma = 0.5 * (s.low + s.high);
-          have = bisect_next(c, s);
-          next_k = -1;
+          s.passes = r.passes;
+          s.samples = r.samples;
+          g = r.g_final;
+          // window hit / cached high: a counting pass that R does not count
+          // again (kRedo); capped: R's final capped pass (counted)
+          start_pass(s, g, r.mode_final == kCapped ? kCapped : kRedo);
+          have = true;
         }
       }
     }
@@ -676,9 +863,9 @@ __global__ void __launch_bounds__(kGenThreads) gen_bisect_kernel(const GenConst 
 
     int ended;
     if (s.k >= stored) {
-      ended = 0;  // the reference loop broke here (tb <= ta)
+      ended = 0;
     } else {
-      const float4 rgba = next_k == s.k ? next : cache[s.k];
+      float4 rgba = cache[s.k];
       const double ta = s.t0 + (double)s.k * step;
       double tb = ta + step;
       if (tb > s.t1) tb = s.t1;
@@ -687,20 +874,15 @@ __global__ void __launch_bounds__(kGenThreads) gen_bisect_kernel(const GenConst 
         run = __float_as_int(rgba.x);
         if (run < 1) run = 1;
         if (run > stored - s.k) run = stored - s.k;
-      }
-      // prefetch the entry after this one
-      const int nk = s.k + run;
-      if (nk < stored) {
-        next = cache[nk];
-        next_k = nk;
+      } else {
+        rgba.x = fabsf(rgba.x);  // drop the pow flag
       }
       ended = segment_step(c, s, rgba, ta, tb, run);
-      if (ended < 0 && s.k >= stored) ended = 0;
     }
     if (ended >= 0) {
-      if (ended == 0) ended = close_pass(c, s);
-      have = pass_done(c, s, ended);
-      next_k = -1;
+      const int n = ended == 0 ? close_pass(c, s) : ended;
+      finish_ray(c, s, g, n);
+      have = false;
     }
   }
 }
@@ -793,7 +975,7 @@ __global__ void fill_inv_kernel(double* tab, int n) {
 struct GenPlan {
   void (*sample)(const GenConst);
   void (*fused)(const GenConst);
-  int sms, per_sm_sample, per_sm_bisect, per_sm_fused;
+  int sms, per_sm_sample, per_sm_bisect, per_sm_emit, per_sm_fused;
   int max_steps, inv_n;
   long long n_rays;
   size_t off_ctl, off_inv, off_recs, off_defer0, off_defer1, off_cache;
@@ -827,6 +1009,8 @@ static int plan_gen(const VdiGenArgs* a, GenPlan& p) {
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p.per_sm_fused, p.fused, kGenThreads, p.smem);
   if (p.per_sm_sample < 1) p.per_sm_sample = 1;
   if (p.per_sm_bisect < 1) p.per_sm_bisect = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p.per_sm_emit, gen_emit_kernel, kGenThreads, 0);
+  if (p.per_sm_emit < 1) p.per_sm_emit = 1;
   if (p.per_sm_fused < 1) p.per_sm_fused = 1;
   // no ray has more samples than the box diagonal allows
   const double ex = a->aabb[3] - a->aabb[0], ey = a->aabb[4] - a->aabb[1],
@@ -927,6 +1111,7 @@ int gen_launch(const VdiGenArgs* a, cudaStream_t stream) {
     c.defer_out = defer[r & 1];
     p.sample<<<grid_for(p.per_sm_sample, r == 0 ? chunks : -1), kGenThreads, p.smem, stream>>>(c);
     gen_bisect_kernel<<<grid_for(p.per_sm_bisect, -1), kGenThreads, 0, stream>>>(c);
+    gen_emit_kernel<<<grid_for(p.per_sm_emit, -1), kGenThreads, 0, stream>>>(c);
   }
   // leftovers: the fused kernel over the last round's deferred rays
   c.round = kRounds;
