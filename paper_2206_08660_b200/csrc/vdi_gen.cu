@@ -643,28 +643,91 @@ __global__ void __launch_bounds__(kGenThreads) gen_sample_kernel(const GenConst 
 // Passes 2.. of the bisection (generate.py:237-273) for the queued rays, as
 // COUNT-ONLY replays: a counting pass's decisions (split, abort, transparent
 // close) depend only on the running mean of premultiplied samples, never on
-// the accumulated colour or the stored segments, so n(gamma) needs 8 state
+// the accumulated colour or the stored segments, so n(gamma) needs a few
 // registers and no writes. The deciding (gamma, mode) is handed to the emit
 // phase, which re-runs that one pass with full logic.
-struct CountPass {
-  double mr, mg, mb, thr;
-  int count, nsamp, k;
+//
+// Speculation: one replay evaluates the next kLevels levels of the bisection
+// tree at once -- G = 2^kLevels - 1 gammas in heap order, node i's children
+// being (gamma_i, high_i) [n > n_sg] at 2i+1 and (low_i, gamma_i) [n < n_sg -
+// delta] at 2i+2, each gamma = 0.5 * (low + high) exactly as the reference
+// forms it. The G count states are independent (ILP against FP64 latency) and
+// share each loaded sample; R's control flow (epsilon tests included) is then
+// replayed over the counts, so results and the reported passes/samples are
+// exactly the reference's.
+constexpr int kLevels = 2;
+constexpr int kG = (1 << kLevels) - 1;
+
+struct CountState {
+  double mr, mg, mb, thr, inv_next;
+  int count, nsamp, kend, n;  // n >= 0 once resolved
   bool active;
 };
+
+__device__ __forceinline__ void count_reset(CountState& q, double gamma) {
+  q.thr = split_threshold(gamma);
+  q.mr = q.mg = q.mb = 0.0;
+  q.inv_next = 0.5;
+  q.count = 0;
+  q.nsamp = 0;
+  q.kend = 0;
+  q.n = -1;
+  q.active = false;
+}
+
+// One non-transparent sample for one count state (generate.py:166-212 minus
+// the colour accumulation).
+__device__ __forceinline__ void count_sample(const GenConst& c, CountState& q, double sr,
+                                             double sg, double sb, int k, int n_sg) {
+  if (q.n >= 0) return;
+  if (!q.active) {
+    if (q.count >= n_sg) {
+      q.n = n_sg + 1;
+      q.kend = k + 1;
+      return;
+    }
+    q.active = true;
+  } else {
+    const double dr = q.mr - sr, dg = q.mg - sg, db = q.mb - sb;
+    if (!(dr * dr + dg * dg + db * db >= q.thr)) {
+      q.nsamp += 1;
+      const double inv = q.inv_next;
+      q.inv_next = q.nsamp + 1 < c.inv_n ? __ldg(c.inv_tab + q.nsamp + 1)
+                                         : 1.0 / (double)(q.nsamp + 1);
+      q.mr += (sr - q.mr) * inv;
+      q.mg += (sg - q.mg) * inv;
+      q.mb += (sb - q.mb) * inv;
+      return;
+    }
+    if (q.count + 1 >= n_sg) {
+      q.n = n_sg + 1;
+      q.kend = k + 1;
+      return;
+    }
+    q.count += 1;
+  }
+  q.mr = sr;
+  q.mg = sg;
+  q.mb = sb;
+  q.nsamp = 1;
+  q.inv_next = 0.5;
+}
 
 __global__ void __launch_bounds__(kGenThreads) gen_bisect_kernel(const GenConst c) {
   const int lane = threadIdx.x & 31;
   const long long nrec = (long long)c.ctl->nrec;
   const int n_sg = c.a.n_sg;
   WarpPool pool;
-  bool have = false, done = false;
+  bool have = false, done = false, top = false;
   const float4* cache = nullptr;
   RayRec* rec = nullptr;
-  int stored = 0;
+  int stored = 0, k = 0;
+  float4 b0 = make_float4(0.f, 0.f, 0.f, 0.f), b1 = b0;  // entries k, k+1 (in flight)
   // bisection state (generate.py:230-236)
-  double low = 0.0, high = 0.0, gamma = 0.0;
+  double low = 0.0, high = 0.0;
   int last_n = 0, high_n = 0, passes = 0, samples = 0;
-  CountPass p;
+  CountState q[kG];
+  double gam[kG];
 
   while (true) {
     const unsigned need = __ballot_sync(0xffffffffu, !have && !done);
@@ -680,22 +743,22 @@ __global__ void __launch_bounds__(kGenThreads) gen_bisect_kernel(const GenConst 
           // state after the overflowing pass 1 (generate.py:253-273)
           low = c.a.gamma_init;
           high = kSqrt3;
-          gamma = 0.5 * (low + high);
           last_n = n_sg + 1;
           high_n = -1;
           passes = rec->passes;
           samples = rec->samples;
           have = true;
-          p.k = -1;  // -> top of the bisection loop
+          top = true;
         }
       }
     }
     if (__all_sync(0xffffffffu, done)) break;
     if (!have) continue;
 
-    int n = -1;
-    if (p.k < 0) {
-      // top of the bisection loop: epsilon exit or a new counting pass
+    if (top) {
+      // top of the bisection loop: epsilon exit, or a replay of the next
+      // kLevels levels
+      top = false;
       if (fabs(high - low) < c.a.eps) {
         if (last_n == 0) {
           rec->g_final = low;
@@ -714,32 +777,52 @@ __global__ void __launch_bounds__(kGenThreads) gen_bisect_kernel(const GenConst 
         have = false;
         continue;
       }
-      p.thr = split_threshold(gamma);
-      p.count = 0;
-      p.nsamp = 0;
-      p.k = 0;
-      p.active = false;
-      p.mr = p.mg = p.mb = 0.0;
-    }
-    if (p.k >= stored) {
-      n = p.count + (p.active ? 1 : 0);  // natural end (or the tb <= ta break)
-      samples += stored;
-    } else {
-      const float4 e = cache[p.k];
-      if (e.w <= 0.0f) {
-        int run = __float_as_int(e.x);
-        if (run < 1) run = 1;
-        if (run > stored - p.k) run = stored - p.k;
-        if (p.active) {
-          p.count += 1;  // the transparent sample closes the segment
-          p.active = false;
+      double lo[kG], hi[kG];
+      lo[0] = low;
+      hi[0] = high;
+#pragma unroll
+      for (int i = 0; i < kG; ++i) {
+        gam[i] = 0.5 * (lo[i] + hi[i]);
+        if (2 * i + 2 < kG) {
+          lo[2 * i + 1] = gam[i];
+          hi[2 * i + 1] = hi[i];
+          lo[2 * i + 2] = lo[i];
+          hi[2 * i + 2] = gam[i];
         }
-        p.k += run;
+        count_reset(q[i], gam[i]);
+      }
+      k = 0;
+      b0 = cache[0];
+      if (stored > 1) b1 = cache[1];
+    }
+
+    bool resolved = true;
+    if (k >= stored) {
+      // natural end (or the tb <= ta break)
+#pragma unroll
+      for (int i = 0; i < kG; ++i)
+        if (q[i].n < 0) {
+          q[i].n = q[i].count + (q[i].active ? 1 : 0);
+          q[i].kend = stored;
+        }
+    } else {
+      const float4 e = b0;
+      int run = 1;
+      if (e.w <= 0.0f) {
+        run = __float_as_int(e.x);
+        if (run < 1) run = 1;
+        if (run > stored - k) run = stored - k;
+#pragma unroll
+        for (int i = 0; i < kG; ++i)
+          if (q[i].n < 0 && q[i].active) {
+            q[i].count += 1;  // the transparent sample closes the segment
+            q[i].active = false;
+          }
       } else {
         const double a = (double)e.w;
         double a_adj;
         if (entry_needs_pow(e)) {
-          const double ta = rec->t0 + (double)p.k * c.a.step;
+          const double ta = rec->t0 + (double)k * c.a.step;
           double tb = ta + c.a.step;
           if (tb > rec->t1) tb = rec->t1;
           const double dt = tb - ta;
@@ -751,63 +834,62 @@ __global__ void __launch_bounds__(kGenThreads) gen_bisect_kernel(const GenConst 
         const double sr = (double)fabsf(e.x) * a_adj;
         const double sg = (double)e.y * a_adj;
         const double sb = (double)e.z * a_adj;
-        bool fresh;
-        if (!p.active) {
-          if (p.count >= n_sg) {
-            n = n_sg + 1;
-          }
-          fresh = true;
-        } else {
-          const double dr = p.mr - sr, dg = p.mg - sg, db = p.mb - sb;
-          if (dr * dr + dg * dg + db * db >= p.thr) {
-            if (p.count + 1 >= n_sg) n = n_sg + 1;
-            else p.count += 1;
-            fresh = true;
-          } else {
-            fresh = false;
-          }
-        }
-        if (n < 0) {
-          if (fresh) {
-            p.active = true;
-            p.mr = sr;
-            p.mg = sg;
-            p.mb = sb;
-            p.nsamp = 1;
-          } else {
-            p.nsamp += 1;
-            const double inv =
-                p.nsamp < c.inv_n ? __ldg(c.inv_tab + p.nsamp) : 1.0 / (double)p.nsamp;
-            p.mr += (sr - p.mr) * inv;
-            p.mg += (sg - p.mg) * inv;
-            p.mb += (sb - p.mb) * inv;
-          }
-          p.k += 1;
-        } else {
-          samples += p.k + 1;  // aborted at sample k
-        }
+#pragma unroll
+        for (int i = 0; i < kG; ++i) count_sample(c, q[i], sr, sg, sb, k, n_sg);
       }
+      k += run;
+      // keep two entries in flight
+      if (run == 1) {
+        b0 = b1;
+        if (k + 1 < stored) b1 = cache[k + 1];
+      } else {
+        if (k < stored) b0 = cache[k];
+        if (k + 1 < stored) b1 = cache[k + 1];
+      }
+#pragma unroll
+      for (int i = 0; i < kG; ++i) resolved = resolved && q[i].n >= 0;
     }
-    if (n >= 0) {
-      // end of a counting pass (generate.py:258-273)
+    if (!resolved) continue;
+
+    // replay R's control flow over the speculated counts (generate.py:237-273)
+    int node = 0;
+    bool fin = false;
+    for (int lvl = 0; lvl < kLevels; ++lvl) {
+      if (lvl > 0 && fabs(high - low) < c.a.eps) break;  // handled at the top
+      // static selection keeps q[] / gam[] in registers
+      int n = 0, kend = 0;
+      double g = 0.0;
+#pragma unroll
+      for (int i = 0; i < kG; ++i)
+        if (i == node) {
+          n = q[i].n;
+          kend = q[i].kend;
+          g = gam[i];
+        }
       passes += 1;
+      samples += kend;
       last_n = n;
       if (n > n_sg) {
-        low = gamma;
+        low = g;
+        node = 2 * node + 1;
       } else if (n < n_sg - c.a.delta) {
-        high = gamma;
+        high = g;
         high_n = n;
+        node = 2 * node + 2;
       } else {
-        rec->g_final = gamma;  // window hit: this pass's segments
+        rec->g_final = g;  // window hit: this pass's segments
         rec->mode_final = kCount;
         rec->passes = passes;
         rec->samples = samples;
-        have = false;
-        continue;
+        fin = true;
+        break;
       }
-      gamma = 0.5 * (low + high);
-      p.k = -1;
     }
+    if (fin) {
+      have = false;
+      continue;
+    }
+    top = true;
   }
 }
 
