@@ -42,6 +42,7 @@
 // the cached high-gamma segments after a later low-gamma pass) replays the
 // high pass, which is deterministic.
 #include <cstdio>
+#include <cstdlib>
 
 #include "vdi_common.cuh"
 #include "vdi_internal.h"
@@ -655,11 +656,15 @@ __global__ void __launch_bounds__(kGenThreads) gen_sample_kernel(const GenConst 
 // share each loaded sample; R's control flow (epsilon tests included) is then
 // replayed over the counts, so results and the reported passes/samples are
 // exactly the reference's.
-constexpr int kLevels = 2;
-constexpr int kG = (1 << kLevels) - 1;
+
+// Cache rows are read sequentially by one lane; a 128 B line holds 8 entries.
+constexpr int kPrefetchAhead = 16;
+__device__ __forceinline__ void prefetch_l1(const void* p) {
+  asm volatile("prefetch.global.L1 [%0];\n" ::"l"(p));
+}
 
 struct CountState {
-  double mr, mg, mb, thr, inv_next;
+  double mr, mg, mb, thr;
   int count, nsamp, kend, n;  // n >= 0 once resolved
   bool active;
 };
@@ -667,7 +672,6 @@ struct CountState {
 __device__ __forceinline__ void count_reset(CountState& q, double gamma) {
   q.thr = split_threshold(gamma);
   q.mr = q.mg = q.mb = 0.0;
-  q.inv_next = 0.5;
   q.count = 0;
   q.nsamp = 0;
   q.kend = 0;
@@ -676,44 +680,40 @@ __device__ __forceinline__ void count_reset(CountState& q, double gamma) {
 }
 
 // One non-transparent sample for one count state (generate.py:166-212 minus
-// the colour accumulation).
-__device__ __forceinline__ void count_sample(const GenConst& c, CountState& q, double sr,
-                                             double sg, double sb, int k, int n_sg) {
-  if (q.n >= 0) return;
-  if (!q.active) {
-    if (q.count >= n_sg) {
-      q.n = n_sg + 1;
-      q.kend = k + 1;
-      return;
-    }
-    q.active = true;
-  } else {
-    const double dr = q.mr - sr, dg = q.mg - sg, db = q.mb - sb;
-    if (!(dr * dr + dg * dg + db * db >= q.thr)) {
-      q.nsamp += 1;
-      const double inv = q.inv_next;
-      q.inv_next = q.nsamp + 1 < c.inv_n ? __ldg(c.inv_tab + q.nsamp + 1)
-                                         : 1.0 / (double)(q.nsamp + 1);
-      q.mr += (sr - q.mr) * inv;
-      q.mg += (sg - q.mg) * inv;
-      q.mb += (sb - q.mb) * inv;
-      return;
-    }
-    if (q.count + 1 >= n_sg) {
-      q.n = n_sg + 1;
-      q.kend = k + 1;
-      return;
-    }
-    q.count += 1;
+// the colour accumulation), branch-free: both outcomes are computed and
+// selected so the G states of a lane run as straight-line FP64 code.
+//  * t = s - m is exactly -(m - s), so t*t reproduces R's dr*dr bit for bit and
+//    m + t*inv is R's `m += (s - m) * inv`;
+//  * __drcp_rn(n) is the IEEE round-to-nearest reciprocal, i.e. exactly the
+//    host's 1.0 / n.
+__device__ __forceinline__ void count_sample(CountState& q, double sr, double sg, double sb,
+                                             int k, int n_sg) {
+  const double tr = sr - q.mr, tg = sg - q.mg, tb = sb - q.mb;
+  const bool far = tr * tr + tg * tg + tb * tb >= q.thr;
+  const bool live = q.n < 0;
+  const bool merge = q.active && !far;
+  const bool split = q.active && far;
+  const bool abort = (!q.active && q.count >= n_sg) || (split && q.count + 1 >= n_sg);
+  const int ns = q.nsamp + 1;
+  const double inv = __drcp_rn((double)ns);
+  const double nr = q.mr + tr * inv, ng = q.mg + tg * inv, nb = q.mb + tb * inv;
+  if (live && abort) {
+    q.n = n_sg + 1;
+    q.kend = k + 1;
   }
-  q.mr = sr;
-  q.mg = sg;
-  q.mb = sb;
-  q.nsamp = 1;
-  q.inv_next = 0.5;
+  if (live && !abort) {
+    q.count += split ? 1 : 0;
+    q.mr = merge ? nr : sr;
+    q.mg = merge ? ng : sg;
+    q.mb = merge ? nb : sb;
+    q.nsamp = merge ? ns : 1;
+    q.active = true;
+  }
 }
 
+template <int kLevels>
 __global__ void __launch_bounds__(kGenThreads) gen_bisect_kernel(const GenConst c) {
+  constexpr int kG = (1 << kLevels) - 1;
   const int lane = threadIdx.x & 31;
   const long long nrec = (long long)c.ctl->nrec;
   const int n_sg = c.a.n_sg;
@@ -794,10 +794,13 @@ __global__ void __launch_bounds__(kGenThreads) gen_bisect_kernel(const GenConst 
       k = 0;
       b0 = cache[0];
       if (stored > 1) b1 = cache[1];
+      if (stored > 8) prefetch_l1(cache + 8);
+      if (stored > kPrefetchAhead) prefetch_l1(cache + kPrefetchAhead);
     }
 
-    bool resolved = true;
-    if (k >= stored) {
+    bool resolved = false;
+    for (int it = 0; it < 16 && !resolved; ++it) {
+     if (k >= stored) {
       // natural end (or the tb <= ta break)
 #pragma unroll
       for (int i = 0; i < kG; ++i)
@@ -805,7 +808,8 @@ __global__ void __launch_bounds__(kGenThreads) gen_bisect_kernel(const GenConst 
           q[i].n = q[i].count + (q[i].active ? 1 : 0);
           q[i].kend = stored;
         }
-    } else {
+      resolved = true;
+     } else {
       const float4 e = b0;
       int run = 1;
       if (e.w <= 0.0f) {
@@ -835,10 +839,11 @@ __global__ void __launch_bounds__(kGenThreads) gen_bisect_kernel(const GenConst 
         const double sg = (double)e.y * a_adj;
         const double sb = (double)e.z * a_adj;
 #pragma unroll
-        for (int i = 0; i < kG; ++i) count_sample(c, q[i], sr, sg, sb, k, n_sg);
+        for (int i = 0; i < kG; ++i) count_sample(q[i], sr, sg, sb, k, n_sg);
       }
+      const int kold = k;
       k += run;
-      // keep two entries in flight
+      // keep two entries in registers and the row two 128 B lines ahead in L1
       if (run == 1) {
         b0 = b1;
         if (k + 1 < stored) b1 = cache[k + 1];
@@ -846,8 +851,13 @@ __global__ void __launch_bounds__(kGenThreads) gen_bisect_kernel(const GenConst 
         if (k < stored) b0 = cache[k];
         if (k + 1 < stored) b1 = cache[k + 1];
       }
+      if ((((kold + kPrefetchAhead) ^ (k + kPrefetchAhead)) & ~7) != 0 &&
+          k + kPrefetchAhead < stored)
+        prefetch_l1(cache + k + kPrefetchAhead);
+      resolved = true;
 #pragma unroll
       for (int i = 0; i < kG; ++i) resolved = resolved && q[i].n >= 0;
+     }
     }
     if (!resolved) continue;
 
@@ -1057,6 +1067,7 @@ __global__ void fill_inv_kernel(double* tab, int n) {
 struct GenPlan {
   void (*sample)(const GenConst);
   void (*fused)(const GenConst);
+  void (*bisect)(const GenConst);
   int sms, per_sm_sample, per_sm_bisect, per_sm_emit, per_sm_fused;
   int max_steps, inv_n;
   long long n_rays;
@@ -1086,8 +1097,13 @@ static int plan_gen(const VdiGenArgs* a, GenPlan& p) {
   cudaDeviceGetAttribute(&p.sms, cudaDevAttrMultiProcessorCount, dev);
   p.smem = sizeof(float4) * a->lut_n;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p.per_sm_sample, p.sample, kGenThreads, p.smem);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p.per_sm_bisect, gen_bisect_kernel, kGenThreads,
-                                                0);
+  {
+    const char* env = getenv("VDI_BISECT_LEVELS");
+    const int lv = env ? atoi(env) : 2;
+    p.bisect = lv <= 1 ? gen_bisect_kernel<1> : (lv == 2 ? gen_bisect_kernel<2>
+                                                          : gen_bisect_kernel<3>);
+  }
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p.per_sm_bisect, p.bisect, kGenThreads, 0);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p.per_sm_fused, p.fused, kGenThreads, p.smem);
   if (p.per_sm_sample < 1) p.per_sm_sample = 1;
   if (p.per_sm_bisect < 1) p.per_sm_bisect = 1;
@@ -1192,7 +1208,7 @@ int gen_launch(const VdiGenArgs* a, cudaStream_t stream) {
     c.defer_in = defer[(r + 1) & 1];
     c.defer_out = defer[r & 1];
     p.sample<<<grid_for(p.per_sm_sample, r == 0 ? chunks : -1), kGenThreads, p.smem, stream>>>(c);
-    gen_bisect_kernel<<<grid_for(p.per_sm_bisect, -1), kGenThreads, 0, stream>>>(c);
+    p.bisect<<<grid_for(p.per_sm_bisect, -1), kGenThreads, 0, stream>>>(c);
     gen_emit_kernel<<<grid_for(p.per_sm_emit, -1), kGenThreads, 0, stream>>>(c);
   }
   // leftovers: the fused kernel over the last round's deferred rays
