@@ -72,6 +72,7 @@ static inline int32_t vdi_list_stride(int32_t n_sg) { return (6 * n_sg + 3) & ~3
 typedef struct VdiGenArgs {
   const void* volume;   /* (nz, ny, nx) x-fastest, voxel_type elements */
   const float* lut;     /* (lut_n, 4) f32, TransferFunction.lut */
+  const void* brick_max;/* vdi_volume_brick_max() of `volume`, or NULL (no skipping) */
   int32_t* counts;      /* OUT (local_h, width) */
   float* segs;          /* OUT (local_h, width, vdi_list_stride(n_sg)) list-SoA */
   double* gammas;       /* OUT (local_h, width), may be NULL */
@@ -91,12 +92,15 @@ typedef struct VdiGenArgs {
   double gamma_init;
   double step;          /* resolved step (generate.py:38-50) */
   double lref;
+  double ess_max;       /* normalised brick maximum at or below which every sample
+                           classifies to alpha 0 exactly; < 0 disables skipping */
   int32_t voxel_type;
   int32_t nx, ny, nz;
   int32_t lut_n;
   int32_t width, height;
   int32_t n_sg, delta;
   int32_t band_rows, band_stride, band_offset;
+  int32_t brick_log2;   /* brick edge 2^brick_log2 voxels */
 } VdiGenArgs;
 
 /* AccelGrid: per-cell supersegment counts (generate.py:322-346). `grid` is
@@ -161,6 +165,12 @@ int vdi_find_first_batch(const float* fronts, const float* backs,
                          const int32_t* seeds, int32_t* out_index,
                          int32_t* out_seed, int64_t n_queries,
                          vdi_stream_t stream);
+
+/* Per-brick maximum of the raw voxels (edge 2^brick_log2, +1 trilinear halo):
+ * out is (ceil(nz/B), ceil(ny/B), ceil(nx/B)) of the volume's voxel type.
+ * Used for exact empty-space skipping in vdi_gen_launch. */
+int vdi_volume_brick_max(const void* volume, int32_t voxel_type, int32_t nx, int32_t ny,
+                         int32_t nz, int32_t brick_log2, void* out, vdi_stream_t stream);
 
 /* Layout conversion for n_lists lists of n_sg supersegments. */
 int vdi_segs_to_aos(const float* soa, float* aos, int64_t n_lists,

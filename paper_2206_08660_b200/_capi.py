@@ -20,13 +20,13 @@ _I = ctypes.c_int32
 
 class VdiGenArgs(ctypes.Structure):
     _fields_ = [
-        ("volume", _P), ("lut", _P), ("counts", _P), ("segs", _P), ("gammas", _P),
+        ("volume", _P), ("lut", _P), ("brick_max", _P), ("counts", _P), ("segs", _P), ("gammas", _P),
         ("passes", _P), ("samples", _P), ("workspace", _P), ("workspace_bytes", ctypes.c_size_t),
         ("pv", _D * 16), ("inv_pv", _D * 16), ("eye", _D * 3), ("aabb", _D * 6),
-        ("eps", _D), ("gamma_init", _D), ("step", _D), ("lref", _D),
+        ("eps", _D), ("gamma_init", _D), ("step", _D), ("lref", _D), ("ess_max", _D),
         ("voxel_type", _I), ("nx", _I), ("ny", _I), ("nz", _I), ("lut_n", _I),
         ("width", _I), ("height", _I), ("n_sg", _I), ("delta", _I),
-        ("band_rows", _I), ("band_stride", _I), ("band_offset", _I),
+        ("band_rows", _I), ("band_stride", _I), ("band_offset", _I), ("brick_log2", _I),
     ]
 
 
@@ -57,7 +57,7 @@ class VdiRenderArgs(ctypes.Structure):
 EXPORTS = ["vdi_last_error", "vdi_abi_version", "vdi_gen_workspace_bytes",
            "vdi_gen_workspace_min_bytes", "vdi_gen_launch",
            "vdi_grid_launch", "vdi_render_launch", "vdi_find_first_batch",
-           "vdi_segs_to_aos", "vdi_segs_from_aos"]
+           "vdi_volume_brick_max", "vdi_segs_to_aos", "vdi_segs_from_aos"]
 
 _lib = None
 
@@ -85,6 +85,8 @@ def load():
     L.vdi_grid_launch.argtypes = [ctypes.POINTER(VdiGridArgs), _P]
     L.vdi_render_launch.argtypes = [ctypes.POINTER(VdiRenderArgs), _P]
     L.vdi_find_first_batch.argtypes = [_P, _P, _P, _I, _P, _P, _P, _P, _P, ctypes.c_int64, _P]
+    L.vdi_volume_brick_max.argtypes = [_P, _I, _I, _I, _I, _I, _P, _P]
+    L.vdi_volume_brick_max.restype = ctypes.c_int
     L.vdi_segs_to_aos.argtypes = [_P, _P, ctypes.c_int64, _I, _P]
     L.vdi_segs_from_aos.argtypes = [_P, _P, ctypes.c_int64, _I, _P]
     for name in ("vdi_gen_launch", "vdi_grid_launch", "vdi_render_launch",

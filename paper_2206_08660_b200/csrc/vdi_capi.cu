@@ -86,6 +86,15 @@ int vdi_find_first_batch(const float* fronts, const float* backs, const int32_t*
                                out_seed, n_queries, static_cast<cudaStream_t>(stream));
 }
 
+int vdi_volume_brick_max(const void* volume, int32_t voxel_type, int32_t nx, int32_t ny,
+                         int32_t nz, int32_t brick_log2, void* out, vdi_stream_t stream) {
+  if (!volume || !out) return set_error(VDI_EINVAL, "null device pointer");
+  if (nx < 2 || ny < 2 || nz < 2 || brick_log2 < 1 || brick_log2 > 8)
+    return set_error(VDI_EINVAL, "bad sizes");
+  return vdi::brick_max(volume, voxel_type, nx, ny, nz, brick_log2, out,
+                        static_cast<cudaStream_t>(stream));
+}
+
 int vdi_segs_to_aos(const float* soa, float* aos, int64_t n_lists, int32_t n_sg,
                     vdi_stream_t stream) {
   if (n_lists < 0 || n_sg < 1) return set_error(VDI_EINVAL, "bad sizes");

@@ -105,6 +105,8 @@ struct GenConst {
   RoundCtl* ctl;   // this round
   RoundCtl* prev;  // previous round (its ndefer sizes defer_in)
   int round;
+  int ess;         // empty-space skipping enabled
+  int bnx, bny;    // brick grid x / y extent
 };
 
 template <int VT>
@@ -143,6 +145,16 @@ __device__ __forceinline__ double trilinear(const GenConst& c, const float* tab,
   if (ix > nx - 2) ix = nx - 2;
   if (iy > ny - 2) iy = ny - 2;
   if (iz > nz - 2) iz = nz - 2;
+  if (c.ess) {
+    // Exact empty-space skip: every voxel this sample can read lies in the
+    // brick (+1 halo), whose maximum classifies at or below the last row of
+    // the LUT's leading alpha == 0 run with margin, and a trilinear mix never
+    // exceeds its largest input by more than a few ulps. -1 classifies to LUT
+    // row 0, whose alpha is 0: the sample is transparent, as in the reference.
+    const int lb = c.a.brick_log2;
+    const long long bi = ((long long)(iz >> lb) * c.bny + (iy >> lb)) * c.bnx + (ix >> lb);
+    if (Voxel<VT>::get(c.a.brick_max, bi, tab) <= c.a.ess_max) return -1.0;
+  }
   const double fx = gx - ix, fy = gy - iy, fz = gz - iz;
   const long long sy = nx, sz = (long long)nx * ny;
   const long long b = iz * sz + iy * sy + ix;
@@ -1170,6 +1182,14 @@ int gen_launch(const VdiGenArgs* a, cudaStream_t stream) {
   c.tiles_x = (a->width + kTileW - 1) / kTileW;
   const long long tiles_y = (c.local_h + kTileH - 1) / kTileH;
   c.n_slots = (long long)c.tiles_x * tiles_y * 32;
+  c.ess = a->brick_max != nullptr && a->ess_max >= 0.0 && a->brick_log2 >= 1;
+  if (c.ess) {
+    const int B = 1 << a->brick_log2;
+    c.bnx = (a->nx + B - 1) / B;
+    c.bny = (a->ny + B - 1) / B;
+  } else {
+    c.bnx = c.bny = 0;
+  }
   if (c.local_h <= 0) return VDI_OK;
   GenPlan p;
   int rc = plan_gen(&c.a, p);

@@ -131,5 +131,47 @@ def upload_volume(vol, cache: bool = True):
     return to_device(arr), vt
 
 
+BRICK_LOG2 = 3
+_bricks = {}
+
+
+def volume_bricks(vol_dev, voxel_type: str, dims, log2: int = BRICK_LOG2):
+    """Per-brick voxel maxima of a device volume (vdi_volume_brick_max), cached
+    for as long as the device volume lives."""
+    key = (vol_dev.data_ptr(), tuple(dims), voxel_type, log2)
+    hit = _bricks.get(key)
+    if hit is not None and hit[0]() is vol_dev:
+        return hit[1]
+    nx, ny, nz = (int(v) for v in dims)
+    b = 1 << log2
+    out = torch().empty(((nz + b - 1) // b, (ny + b - 1) // b, (nx + b - 1) // b),
+                        dtype=vol_dev.dtype, device=vol_dev.device)
+    _capi.check(_capi.load().vdi_volume_brick_max(ptr(vol_dev), _capi.VOXEL[voxel_type], nx, ny,
+                                                   nz, log2, ptr(out), stream_handle()))
+    for k in [k for k, v in _bricks.items() if v[0]() is None]:
+        del _bricks[k]
+    _bricks[key] = (weakref.ref(vol_dev), out)
+    return out
+
+
+def ess_threshold(lut: np.ndarray) -> float:
+    """Largest normalised brick maximum that guarantees alpha == 0.
+
+    _lut_classify (volume.py:164-177) lerps rows i = floor(x), i + 1 with
+    x = s (n - 1); if rows 0..K all have alpha 0, every s with x <= K
+    classifies to alpha 0 exactly (x == K gives f == 0). A 1e-6 margin in x
+    covers the few-ulp overshoot of a trilinear mix over its inputs. Returns
+    -1 (no skipping) when row 0 is already visible."""
+    a = np.asarray(lut, dtype=np.float32)[:, 3]
+    n = len(a)
+    nz = np.nonzero(a > 0)[0]
+    if len(nz) == 0:
+        return float("inf")
+    k = int(nz[0]) - 1
+    if k < 0:
+        return -1.0
+    return (k - 1e-6) / (n - 1)
+
+
 def upload_lut(lut: np.ndarray):
     return lut_cache.get(np.ascontiguousarray(lut, dtype=np.float32))

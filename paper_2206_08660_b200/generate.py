@@ -100,11 +100,15 @@ def alloc_gen(width, rows, n_sg, grid_dims, stats=True):
 
 
 def gen_args(vol_dev, voxel_type, dims, lut_dev, cam, aabb, params_resolved, n_sg, eps,
-             gamma_init, bufs: GenBuffers, band=(16, 1, 0)) -> _capi.VdiGenArgs:
+             gamma_init, bufs: GenBuffers, band=(16, 1, 0), bricks=None,
+             ess_max=-1.0) -> _capi.VdiGenArgs:
     delta, step, lref = params_resolved
     width, height = cam.viewport
     a = _capi.VdiGenArgs()
     a.volume, a.lut = dv.ptr(vol_dev), dv.ptr(lut_dev)
+    a.brick_max = dv.ptr(bricks)
+    a.ess_max = float(ess_max) if bricks is not None else -1.0
+    a.brick_log2 = dv.BRICK_LOG2
     a.counts, a.segs = dv.ptr(bufs.counts), dv.ptr(bufs.segs)
     a.gammas, a.passes, a.samples = dv.ptr(bufs.gammas), dv.ptr(bufs.passes), dv.ptr(bufs.samples)
     _capi.fill(a.pv, _mat(cam.proj_view()))
@@ -136,7 +140,7 @@ def grid_args(bufs: GenBuffers, cam, width, height, n_sg, grid_dims, band=(16, 1
 
 def launch_generate(vol_dev, voxel_type, dims, lut_dev, cam, aabb, params, resolved,
                     bufs: GenBuffers, grid_dims, band=(16, 1, 0), stream=None,
-                    split_events=None, workspace_bytes=None):
+                    split_events=None, workspace_bytes=None, bricks=None, ess_max=-1.0):
     """Enqueue generation + grid on the current stream (no sync, no alloc).
     split_events: optional CUDA events; [1] and [2] bracket the generation
     kernel (timing only). workspace_bytes overrides the recommended scratch
@@ -144,7 +148,7 @@ def launch_generate(vol_dev, voxel_type, dims, lut_dev, cam, aabb, params, resol
     L = _capi.load()
     s = dv.stream_handle() if stream is None else stream
     a = gen_args(vol_dev, voxel_type, dims, lut_dev, cam, aabb, resolved, params.n_sg,
-                 params.epsilon, params.gamma_init, bufs, band)
+                 params.epsilon, params.gamma_init, bufs, band, bricks, ess_max)
     if workspace_bytes == "min":
         need = int(L.vdi_gen_workspace_min_bytes(a))
     elif workspace_bytes is not None:
@@ -181,8 +185,9 @@ def generate_vdi(vol, tf, cam, params: GenParams | None = None, grid_dims=None,
     vol_dev, vt = dv.upload_volume(vol, cache=cache_volume)
     lut_dev = dv.upload_lut(tf.lut)
     bufs = alloc_gen(width, height, params.n_sg, grid_dims, stats=with_stats)
+    bricks = dv.volume_bricks(vol_dev, vt, vol.dims)
     launch_generate(vol_dev, vt, vol.dims, lut_dev, cam, aabb, params, resolved, bufs,
-                    grid_dims)
+                    grid_dims, bricks=bricks, ess_max=dv.ess_threshold(tf.lut))
     dev = DeviceVdi(counts=bufs.counts, segs=bufs.segs)
     vdi = Vdi(width=width, height=height, n_sg=params.n_sg, counts=None, segs=None,
               gen_camera=cam, volume_aabb=aabb, _device=dev)

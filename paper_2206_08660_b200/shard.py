@@ -79,6 +79,8 @@ class Pipeline:
         self.grid_dims = default_grid_dims(w, h)
         self.vol_dev, self.vt = dv.upload_volume(vol)
         self.lut_dev = dv.upload_lut(tf.lut)
+        self.bricks = dv.volume_bricks(self.vol_dev, self.vt, vol.dims)
+        self.ess_max = dv.ess_threshold(tf.lut)
         self.aabb = np.asarray(vol.aabb, np.float64)
         self.band = (BAND_ROWS, world, rank)
         self.gen_rows = rows_per_rank(h, world)
@@ -117,7 +119,8 @@ class Pipeline:
         self.sums.zero_()
         launch_generate(self.vol_dev, self.vt, self.vol.dims, self.lut_dev, self.gcam,
                         self.aabb, self.params, self.resolved, self.bufs, self.grid_dims,
-                        band=self.band, split_events=ev)
+                        band=self.band, split_events=ev, bricks=self.bricks,
+                        ess_max=self.ess_max)
         if timed:
             ev[3].record()
         if self.world > 1:
@@ -179,6 +182,7 @@ class Pipeline:
                 d2h = c.nbytes + s.nbytes + g.nbytes + img.data.nbytes
             else:
                 self.vol_dev = dv.to_device(host)
+                self.bricks = dv.volume_bricks(self.vol_dev, self.vt, vol.dims)
                 self.step()
                 n_sg = self.params.n_sg
                 aos = t.empty((self.gen_rows * self.w, n_sg * 6), dtype=t.float32,
@@ -199,6 +203,7 @@ class Pipeline:
             self.dist.all_reduce(x, op=self.dist.ReduceOp.MAX)
             dt = float(x.item())
         self.vol_dev, _ = dv.upload_volume(self.vol)
+        self.bricks = dv.volume_bricks(self.vol_dev, self.vt, self.vol.dims)
         return {"value": 2 * self.w * self.h / dt / 1e6, "unit": "Mrays/s",
                 "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                 "ms_per_step": dt * 1e3, "steps": steps}
