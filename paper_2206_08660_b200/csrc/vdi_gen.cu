@@ -87,7 +87,7 @@ struct RoundCtl {
 
 struct GenConst {
   VdiGenArgs a;
-  double inv_ext[3];  // 1/extent where the extent is a power of two
+  double inv_ext[3];  // RN(1/extent): exact scale (power of two) or Markstein reciprocal
   int ext_pow2[3];
   double inv_lref;
   int lref_pow2;
@@ -113,12 +113,14 @@ template <int VT>
 struct Voxel;
 template <>
 struct Voxel<VDI_VOXEL_F32> {
+  using type = float;
   static __device__ __forceinline__ double get(const void* p, long long i, const float*) {
     return (double)__ldg(reinterpret_cast<const float*>(p) + i);
   }
 };
 template <>
 struct Voxel<VDI_VOXEL_U8> {
+  using type = unsigned char;
   // volume.py:48-50 normalises with an f32 division by 255; the 256 exact
   // quotients live in shared memory.
   static __device__ __forceinline__ double get(const void* p, long long i, const float* tab) {
@@ -127,6 +129,7 @@ struct Voxel<VDI_VOXEL_U8> {
 };
 template <>
 struct Voxel<VDI_VOXEL_U16> {
+  using type = unsigned short;
   static __device__ __forceinline__ double get(const void* p, long long i, const float*) {
     return (double)__fdiv_rn((float)__ldg(reinterpret_cast<const unsigned short*>(p) + i),
                              65535.0f);
@@ -156,14 +159,17 @@ __device__ __forceinline__ double trilinear(const GenConst& c, const float* tab,
     if (Voxel<VT>::get(c.a.brick_max, bi, tab) <= c.a.ess_max) return -1.0;
   }
   const double fx = gx - ix, fy = gy - iy, fz = gz - iz;
-  const long long sy = nx, sz = (long long)nx * ny;
-  const long long b = iz * sz + iy * sy + ix;
-  const void* v = c.a.volume;
-  const double v000 = Voxel<VT>::get(v, b, tab), v001 = Voxel<VT>::get(v, b + 1, tab);
-  const double v010 = Voxel<VT>::get(v, b + sy, tab), v011 = Voxel<VT>::get(v, b + sy + 1, tab);
-  const double v100 = Voxel<VT>::get(v, b + sz, tab), v101 = Voxel<VT>::get(v, b + sz + 1, tab);
-  const double v110 = Voxel<VT>::get(v, b + sz + sy, tab);
-  const double v111 = Voxel<VT>::get(v, b + sz + sy + 1, tab);
+  // four row pointers, then [ptr + 0/1] gathers (no per-voxel 64-bit math)
+  using T = typename Voxel<VT>::type;
+  const T* r00 = static_cast<const T*>(c.a.volume) +
+                 ((long long)iz * ny + iy) * (long long)nx + ix;
+  const T* r01 = r00 + nx;
+  const T* r10 = r00 + (long long)nx * ny;
+  const T* r11 = r10 + nx;
+  const double v000 = Voxel<VT>::get(r00, 0, tab), v001 = Voxel<VT>::get(r00, 1, tab);
+  const double v010 = Voxel<VT>::get(r01, 0, tab), v011 = Voxel<VT>::get(r01, 1, tab);
+  const double v100 = Voxel<VT>::get(r10, 0, tab), v101 = Voxel<VT>::get(r10, 1, tab);
+  const double v110 = Voxel<VT>::get(r11, 0, tab), v111 = Voxel<VT>::get(r11, 1, tab);
   const double c00 = v000 * (1 - fx) + v001 * fx;
   const double c10 = v010 * (1 - fx) + v011 * fx;
   const double c01 = v100 * (1 - fx) + v101 * fx;
@@ -228,7 +234,8 @@ __device__ __forceinline__ float4 sample_at(const GenConst& c, const float4* lut
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
     const double num = s.o[a] + tm * s.d[a] - c.a.aabb[a];
-    double v = c.ext_pow2[a] ? num * c.inv_ext[a] : num / (c.a.aabb[3 + a] - c.a.aabb[a]);
+    double v = c.ext_pow2[a] ? num * c.inv_ext[a]
+                             : div_by(num, c.a.aabb[3 + a] - c.a.aabb[a], c.inv_ext[a]);
     if (v < 0.0) v = 0.0;
     else if (v > 1.0) v = 1.0;
     q[a] = v;
