@@ -63,6 +63,15 @@ def gather_rows(dist, local, world: int, padded_rows: int):
     return out
 
 
+def exchange_vdi(dist, counts, segs, grid, g_counts, g_segs):
+    """The one exchange between generation and rendering: sum the partial
+    AccelGrids in place and all-gather the padded VDI shards (counts
+    [rows, W], segs [rows * W, stride]) into band-interleaved storage."""
+    dist.all_reduce(grid)
+    dist.all_gather_into_tensor(g_counts, counts)
+    dist.all_gather_into_tensor(g_segs, segs)
+
+
 class Pipeline:
     """generate -> (all-reduce grid, all-gather VDI) -> render -> all-gather
     image, device-resident, for one rank."""
@@ -124,9 +133,8 @@ class Pipeline:
         if timed:
             ev[3].record()
         if self.world > 1:
-            self.dist.all_reduce(self.bufs.grid)
-            self.dist.all_gather_into_tensor(self.g_counts, self.bufs.counts)
-            self.dist.all_gather_into_tensor(self.g_segs, self.bufs.segs)
+            exchange_vdi(self.dist, self.bufs.counts, self.bufs.segs, self.bufs.grid,
+                         self.g_counts, self.g_segs)
         if timed:
             ev[4].record()
         _capi.check(L.vdi_render_launch(self._rargs, dv.stream_handle()))
