@@ -1,0 +1,8 @@
+mkdir -p gpurun_out
+nvidia-smi --query-gpu=name,driver_version,clocks.sm,clocks.max.sm,power.limit --format=csv > gpurun_out/gpu_info.txt
+nproc > gpurun_out/nproc.txt; lscpu | grep -E "Model name|^CPU\(s\)" >> gpurun_out/nproc.txt
+timeout 900 python bench.py > gpurun_out/bench_full.log 2>&1; echo "bench rc=$?"
+timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.log 2>&1; echo "ref rc=$?"
+B="python bench.py --steps 2 --warmup 1 --no-cpu-baseline --e2e-steps 1"
+$B > gpurun_out/plain.log 2>&1 && ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/bench_launches.csv $B > gpurun_out/ncu_bench.log 2>&1; echo "ncu rc=$?"
+tail -1 gpurun_out/bench_full.log | cut -c1-3000; tail -1 gpurun_out/bench_ref.log
