@@ -114,7 +114,7 @@ struct Voxel;
 template <>
 struct Voxel<VDI_VOXEL_F32> {
   using type = float;
-  static __device__ __forceinline__ double get(const void* p, long long i, const float*) {
+  static __device__ __forceinline__ double get(const void* p, long long i, const double*) {
     return (double)__ldg(reinterpret_cast<const float*>(p) + i);
   }
 };
@@ -122,15 +122,15 @@ template <>
 struct Voxel<VDI_VOXEL_U8> {
   using type = unsigned char;
   // volume.py:48-50 normalises with an f32 division by 255; the 256 exact
-  // quotients live in shared memory.
-  static __device__ __forceinline__ double get(const void* p, long long i, const float* tab) {
-    return (double)tab[__ldg(reinterpret_cast<const unsigned char*>(p) + i)];
+  // quotients live in shared memory, already widened to f64.
+  static __device__ __forceinline__ double get(const void* p, long long i, const double* tab) {
+    return tab[__ldg(reinterpret_cast<const unsigned char*>(p) + i)];
   }
 };
 template <>
 struct Voxel<VDI_VOXEL_U16> {
   using type = unsigned short;
-  static __device__ __forceinline__ double get(const void* p, long long i, const float*) {
+  static __device__ __forceinline__ double get(const void* p, long long i, const double*) {
     return (double)__fdiv_rn((float)__ldg(reinterpret_cast<const unsigned short*>(p) + i),
                              65535.0f);
   }
@@ -138,7 +138,7 @@ struct Voxel<VDI_VOXEL_U16> {
 
 // volume.py:180-205 _trilinear.
 template <int VT>
-__device__ __forceinline__ double trilinear(const GenConst& c, const float* tab, double px,
+__device__ __forceinline__ double trilinear(const GenConst& c, const double* tab, double px,
                                             double py, double pz) {
   const int nx = c.a.nx, ny = c.a.ny, nz = c.a.nz;
   const double gx = px * (double)(nx - 1);
@@ -180,18 +180,21 @@ __device__ __forceinline__ double trilinear(const GenConst& c, const float* tab,
 }
 
 // volume.py:164-177 _lut_classify: f64 lerp rounded to f32.
-__device__ __forceinline__ float4 classify(const float4* lut, int n, double s) {
+__device__ __forceinline__ float4 narrow(const double4 v) {
+  return make_float4((float)v.x, (float)v.y, (float)v.z, (float)v.w);
+}
+__device__ __forceinline__ float4 classify(const double4* lut, int n, double s) {
   const double x = s * (double)(n - 1);
-  if (x <= 0.0) return lut[0];
-  if (x >= (double)(n - 1)) return lut[n - 1];
+  if (x <= 0.0) return narrow(lut[0]);
+  if (x >= (double)(n - 1)) return narrow(lut[n - 1]);
   const int i = (int)x;
   const double f = x - i;
-  const float4 l0 = lut[i], l1 = lut[i + 1];
+  const double4 l0 = lut[i], l1 = lut[i + 1];
   float4 o;
-  o.x = (float)((double)l0.x * (1.0 - f) + (double)l1.x * f);
-  o.y = (float)((double)l0.y * (1.0 - f) + (double)l1.y * f);
-  o.z = (float)((double)l0.z * (1.0 - f) + (double)l1.z * f);
-  o.w = (float)((double)l0.w * (1.0 - f) + (double)l1.w * f);
+  o.x = (float)(l0.x * (1.0 - f) + l1.x * f);
+  o.y = (float)(l0.y * (1.0 - f) + l1.y * f);
+  o.z = (float)(l0.z * (1.0 - f) + l1.z * f);
+  o.w = (float)(l0.w * (1.0 - f) + l1.w * f);
   return o;
 }
 
@@ -226,8 +229,8 @@ __device__ double split_threshold(double g) {
 
 // Sample position -> classified RGBA (generate.py:118-134 + volume.py).
 template <int VT>
-__device__ __forceinline__ float4 sample_at(const GenConst& c, const float4* lut,
-                                            const float* tab, const RayState& s, double ta,
+__device__ __forceinline__ float4 sample_at(const GenConst& c, const double4* lut,
+                                            const double* tab, const RayState& s, double ta,
                                             double tb) {
   const double tm = 0.5 * (ta + tb);
   double q[3];
@@ -543,18 +546,21 @@ __device__ __forceinline__ int source_list(const GenConst& c, long long slot) {
   return c.defer_in[slot];
 }
 
-__device__ __forceinline__ void load_lut(const GenConst& c, float4* s_lut, float* s_u8) {
-  for (int i = threadIdx.x; i < c.a.lut_n; i += blockDim.x)
-    s_lut[i] = reinterpret_cast<const float4*>(c.a.lut)[i];
-  for (int i = threadIdx.x; i < 256; i += blockDim.x) s_u8[i] = __fdiv_rn((float)i, 255.0f);
+__device__ __forceinline__ void load_lut(const GenConst& c, double4* s_lut, double* s_u8) {
+  for (int i = threadIdx.x; i < c.a.lut_n; i += blockDim.x) {
+    const float4 l = reinterpret_cast<const float4*>(c.a.lut)[i];
+    s_lut[i] = make_double4(l.x, l.y, l.z, l.w);
+  }
+  for (int i = threadIdx.x; i < 256; i += blockDim.x)
+    s_u8[i] = (double)__fdiv_rn((float)i, 255.0f);
   __syncthreads();
 }
 
 // ------------------------------------------------------------ sample phase
 template <int VT>
 __global__ void __launch_bounds__(kGenThreads) gen_sample_kernel(const GenConst c) {
-  extern __shared__ float4 s_lut[];
-  __shared__ float s_u8[256];
+  extern __shared__ double4 s_lut[];
+  __shared__ double s_u8[256];
   load_lut(c, s_lut, s_u8);
   const int lane = threadIdx.x & 31;
   const double step = c.a.step;
@@ -681,6 +687,47 @@ constexpr int kPrefetchAhead = 16;
 __device__ __forceinline__ void prefetch_l1(const void* p) {
   asm volatile("prefetch.global.L1 [%0];\n" ::"l"(p));
 }
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p));
+}
+
+// A lane's stream of cache entries: b[i] holds entry k + i (loads in flight),
+// plus a cache-level prefetch kPrefetchAhead entries ahead at line crossings
+// (PF: 0 none, 1 into L1, 2 into L2).
+template <int D, int PF>
+struct EntryPipe {
+  float4 b[D];
+  __device__ __forceinline__ void prefetch(const float4* row, int at, int stored) {
+    if (at < stored) {
+      if (PF == 1) prefetch_l1(row + at);
+      if (PF == 2) prefetch_l2(row + at);
+    }
+  }
+  __device__ __forceinline__ void start(const float4* row, int k, int stored) {
+#pragma unroll
+    for (int i = 0; i < D; ++i)
+      if (k + i < stored) b[i] = row[k + i];
+    if (PF) {
+      prefetch(row, (k & ~7) + 8, stored);
+      prefetch(row, (k & ~7) + kPrefetchAhead, stored);
+    }
+  }
+  __device__ __forceinline__ void advance(const float4* row, int kold, int k, int stored) {
+    if (k == kold + 1) {
+#pragma unroll
+      for (int i = 0; i + 1 < D; ++i) b[i] = b[i + 1];
+      if (k + D - 1 < stored) b[D - 1] = row[k + D - 1];
+    } else {
+#pragma unroll
+      for (int i = 0; i < D; ++i)
+        if (k + i < stored) b[i] = row[k + i];
+    }
+    if (PF && (((kold + kPrefetchAhead) ^ (k + kPrefetchAhead)) & ~7) != 0)
+      prefetch(row, k + kPrefetchAhead, stored);
+  }
+};
+
+constexpr int kInvSmem = 4096;  // 32 KiB of 1/n per block; larger n use __drcp_rn
 
 struct CountState {
   double mr, mg, mb, thr;
@@ -706,7 +753,7 @@ __device__ __forceinline__ void count_reset(CountState& q, double gamma) {
 //  * __drcp_rn(n) is the IEEE round-to-nearest reciprocal, i.e. exactly the
 //    host's 1.0 / n.
 __device__ __forceinline__ void count_sample(CountState& q, double sr, double sg, double sb,
-                                             int k, int n_sg) {
+                                             int k, int n_sg, const double* s_inv, int inv_n) {
   const double tr = sr - q.mr, tg = sg - q.mg, tb = sb - q.mb;
   const bool far = tr * tr + tg * tg + tb * tb >= q.thr;
   const bool live = q.n < 0;
@@ -714,7 +761,7 @@ __device__ __forceinline__ void count_sample(CountState& q, double sr, double sg
   const bool split = q.active && far;
   const bool abort = (!q.active && q.count >= n_sg) || (split && q.count + 1 >= n_sg);
   const int ns = q.nsamp + 1;
-  const double inv = __drcp_rn((double)ns);
+  const double inv = ns < inv_n ? s_inv[ns] : __drcp_rn((double)ns);
   const double nr = q.mr + tr * inv, ng = q.mg + tg * inv, nb = q.mb + tb * inv;
   if (live && abort) {
     q.n = n_sg + 1;
@@ -730,9 +777,14 @@ __device__ __forceinline__ void count_sample(CountState& q, double sr, double sg
   }
 }
 
-template <int kLevels>
-__global__ void __launch_bounds__(kGenThreads) gen_bisect_kernel(const GenConst c) {
+template <int kLevels, int kDepth, int kPF, int kMinB = 1>
+__global__ void __launch_bounds__(kGenThreads, kMinB) gen_bisect_kernel(const GenConst c) {
   constexpr int kG = (1 << kLevels) - 1;
+  // 1/n for the running means: host-identical IEEE quotients in shared memory
+  extern __shared__ double s_inv[];
+  const int inv_n = c.inv_n < kInvSmem ? c.inv_n : kInvSmem;
+  for (int i = threadIdx.x; i < inv_n; i += blockDim.x) s_inv[i] = c.inv_tab[i];
+  __syncthreads();
   const int lane = threadIdx.x & 31;
   const long long nrec = (long long)c.ctl->nrec;
   const int n_sg = c.a.n_sg;
@@ -741,7 +793,7 @@ __global__ void __launch_bounds__(kGenThreads) gen_bisect_kernel(const GenConst 
   const float4* cache = nullptr;
   RayRec* rec = nullptr;
   int stored = 0, k = 0;
-  float4 b0 = make_float4(0.f, 0.f, 0.f, 0.f), b1 = b0;  // entries k, k+1 (in flight)
+  EntryPipe<kDepth, kPF> pipe;
   // bisection state (generate.py:230-236)
   double low = 0.0, high = 0.0;
   int last_n = 0, high_n = 0, passes = 0, samples = 0;
@@ -811,10 +863,7 @@ __global__ void __launch_bounds__(kGenThreads) gen_bisect_kernel(const GenConst 
         count_reset(q[i], gam[i]);
       }
       k = 0;
-      b0 = cache[0];
-      if (stored > 1) b1 = cache[1];
-      if (stored > 8) prefetch_l1(cache + 8);
-      if (stored > kPrefetchAhead) prefetch_l1(cache + kPrefetchAhead);
+      pipe.start(cache, 0, stored);
     }
 
     bool resolved = false;
@@ -829,7 +878,7 @@ __global__ void __launch_bounds__(kGenThreads) gen_bisect_kernel(const GenConst 
         }
       resolved = true;
      } else {
-      const float4 e = b0;
+      const float4 e = pipe.b[0];
       int run = 1;
       if (e.w <= 0.0f) {
         run = __float_as_int(e.x);
@@ -858,21 +907,11 @@ __global__ void __launch_bounds__(kGenThreads) gen_bisect_kernel(const GenConst 
         const double sg = (double)e.y * a_adj;
         const double sb = (double)e.z * a_adj;
 #pragma unroll
-        for (int i = 0; i < kG; ++i) count_sample(q[i], sr, sg, sb, k, n_sg);
+        for (int i = 0; i < kG; ++i) count_sample(q[i], sr, sg, sb, k, n_sg, s_inv, inv_n);
       }
       const int kold = k;
       k += run;
-      // keep two entries in registers and the row two 128 B lines ahead in L1
-      if (run == 1) {
-        b0 = b1;
-        if (k + 1 < stored) b1 = cache[k + 1];
-      } else {
-        if (k < stored) b0 = cache[k];
-        if (k + 1 < stored) b1 = cache[k + 1];
-      }
-      if ((((kold + kPrefetchAhead) ^ (k + kPrefetchAhead)) & ~7) != 0 &&
-          k + kPrefetchAhead < stored)
-        prefetch_l1(cache + k + kPrefetchAhead);
+      pipe.advance(cache, kold, k, stored);
       resolved = true;
 #pragma unroll
       for (int i = 0; i < kG; ++i) resolved = resolved && q[i].n >= 0;
@@ -1003,8 +1042,8 @@ __global__ void __launch_bounds__(kGenThreads) gen_emit_kernel(const GenConst c)
 // lane with a private cache slot of max_steps entries.
 template <int VT>
 __global__ void __launch_bounds__(kGenThreads) gen_fused_kernel(const GenConst c) {
-  extern __shared__ float4 s_lut[];
-  __shared__ float s_u8[256];
+  extern __shared__ double4 s_lut[];
+  __shared__ double s_u8[256];
   load_lut(c, s_lut, s_u8);
   const int lane = threadIdx.x & 31;
   const double step = c.a.step;
@@ -1091,7 +1130,7 @@ struct GenPlan {
   int max_steps, inv_n;
   long long n_rays;
   size_t off_ctl, off_inv, off_recs, off_defer0, off_defer1, off_cache;
-  size_t smem;
+  size_t smem, smem_inv;
 };
 
 static int plan_gen(const VdiGenArgs* a, GenPlan& p) {
@@ -1111,24 +1150,6 @@ static int plan_gen(const VdiGenArgs* a, GenPlan& p) {
     default:
       return set_error(VDI_EINVAL, "bad voxel_type %d", a->voxel_type);
   }
-  int dev = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&p.sms, cudaDevAttrMultiProcessorCount, dev);
-  p.smem = sizeof(float4) * a->lut_n;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p.per_sm_sample, p.sample, kGenThreads, p.smem);
-  {
-    const char* env = getenv("VDI_BISECT_LEVELS");
-    const int lv = env ? atoi(env) : 2;
-    p.bisect = lv <= 1 ? gen_bisect_kernel<1> : (lv == 2 ? gen_bisect_kernel<2>
-                                                          : gen_bisect_kernel<3>);
-  }
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p.per_sm_bisect, p.bisect, kGenThreads, 0);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p.per_sm_fused, p.fused, kGenThreads, p.smem);
-  if (p.per_sm_sample < 1) p.per_sm_sample = 1;
-  if (p.per_sm_bisect < 1) p.per_sm_bisect = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p.per_sm_emit, gen_emit_kernel, kGenThreads, 0);
-  if (p.per_sm_emit < 1) p.per_sm_emit = 1;
-  if (p.per_sm_fused < 1) p.per_sm_fused = 1;
   // no ray has more samples than the box diagonal allows
   const double ex = a->aabb[3] - a->aabb[0], ey = a->aabb[4] - a->aabb[1],
                ez = a->aabb[5] - a->aabb[2];
@@ -1136,6 +1157,46 @@ static int plan_gen(const VdiGenArgs* a, GenPlan& p) {
   const double ms = ceil(diag / a->step) + 4.0;
   p.max_steps = ms > 1e7 ? 10000000 : (int)ms;
   p.inv_n = p.max_steps + 2;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&p.sms, cudaDevAttrMultiProcessorCount, dev);
+  p.smem = sizeof(double4) * a->lut_n;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p.per_sm_sample, p.sample, kGenThreads, p.smem);
+  {
+    // VDI_BISECT_VARIANT = "levels,depth,prefetch" (tuning switch; default 2,2,1)
+    const char* env = getenv("VDI_BISECT_VARIANT");
+    int lv = 2, dp = 2, pf = 1, mb = 0;
+    if (env) sscanf(env, "%d,%d,%d,%d", &lv, &dp, &pf, &mb);
+    const int key = mb ? lv * 1000 + dp * 100 + pf * 10 + mb : lv * 100 + dp * 10 + pf;
+    switch (key) {
+      case 120: p.bisect = gen_bisect_kernel<1, 2, 0>; break;
+      case 141: p.bisect = gen_bisect_kernel<1, 4, 1>; break;
+      case 142: p.bisect = gen_bisect_kernel<1, 4, 2>; break;
+      case 220: p.bisect = gen_bisect_kernel<2, 2, 0>; break;
+      case 222: p.bisect = gen_bisect_kernel<2, 2, 2>; break;
+      case 241: p.bisect = gen_bisect_kernel<2, 4, 1>; break;
+      case 242: p.bisect = gen_bisect_kernel<2, 4, 2>; break;
+      case 282: p.bisect = gen_bisect_kernel<2, 8, 2>; break;
+      case 342: p.bisect = gen_bisect_kernel<3, 4, 2>; break;
+      case 2215: p.bisect = gen_bisect_kernel<2, 2, 1, 5>; break;
+      case 2216: p.bisect = gen_bisect_kernel<2, 2, 1, 6>; break;
+      case 2218: p.bisect = gen_bisect_kernel<2, 2, 1, 8>; break;
+      case 1216: p.bisect = gen_bisect_kernel<1, 2, 1, 6>; break;
+      case 1218: p.bisect = gen_bisect_kernel<1, 2, 1, 8>; break;
+      default: p.bisect = gen_bisect_kernel<2, 2, 1>; break;
+    }
+  }
+  // the emit kernel uses no shared memory: give the unified L1 everything
+  cudaFuncSetAttribute(gen_emit_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
+  p.smem_inv = sizeof(double) * (p.inv_n < kInvSmem ? p.inv_n : kInvSmem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p.per_sm_bisect, p.bisect, kGenThreads,
+                                                p.smem_inv);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p.per_sm_fused, p.fused, kGenThreads, p.smem);
+  if (p.per_sm_sample < 1) p.per_sm_sample = 1;
+  if (p.per_sm_bisect < 1) p.per_sm_bisect = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p.per_sm_emit, gen_emit_kernel, kGenThreads, 0);
+  if (p.per_sm_emit < 1) p.per_sm_emit = 1;
+  if (p.per_sm_fused < 1) p.per_sm_fused = 1;
   const int bands = a->band_rows > 0 ? a->band_rows : 16;
   p.n_rays = (long long)a->width *
              local_rows(a->height, bands, a->band_stride > 0 ? a->band_stride : 1,
@@ -1235,7 +1296,7 @@ int gen_launch(const VdiGenArgs* a, cudaStream_t stream) {
     c.defer_in = defer[(r + 1) & 1];
     c.defer_out = defer[r & 1];
     p.sample<<<grid_for(p.per_sm_sample, r == 0 ? chunks : -1), kGenThreads, p.smem, stream>>>(c);
-    p.bisect<<<grid_for(p.per_sm_bisect, -1), kGenThreads, 0, stream>>>(c);
+    p.bisect<<<grid_for(p.per_sm_bisect, -1), kGenThreads, p.smem_inv, stream>>>(c);
     gen_emit_kernel<<<grid_for(p.per_sm_emit, -1), kGenThreads, 0, stream>>>(c);
   }
   // leftovers: the fused kernel over the last round's deferred rays
