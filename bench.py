@@ -120,6 +120,18 @@ class ClockSampler:
 
 # ---------------------------------------------------------------- workload
 
+def gen_traffic(config):
+    """DRAM bytes (read + write) of one generation launch from the committed ncu
+    capture of the same workload (profiles/*_gen_traffic.json), or None."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", f"*_{config.lower()}_gen_traffic.json")))
+    if not files:
+        return None, None
+    with open(files[-1]) as f:
+        d = json.load(f)
+    return float(d["gen_dram_bytes_per_launch"]), os.path.relpath(files[-1], ROOT)
+
+
 def workload(name):
     from paper_2206_08660_b200 import synth
     vol, tf, gcam, rcam, n_sg = synth.config(name)
@@ -284,8 +296,10 @@ def run_b200(args):
     ren_gbs = b_ren / (r_ms * 1e-3) / 1e9
     dominant = "vdi_gen" if g_ms >= r_ms else "vdi_render"
     ach = gen_gbs if dominant == "vdi_gen" else ren_gbs
+    traffic, traffic_src = gen_traffic(args.config) if dominant == "vdi_gen" else (None, None)
     roof = {"kernel": dominant, "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
-            "frac": ach / peak, "peak_kind": peak_kind, "traffic": None,
+            "frac": ach / peak, "peak_kind": peak_kind, "traffic": traffic,
+            "traffic_source": traffic_src,
             "algorithmic_bytes": b_gen if dominant == "vdi_gen" else b_ren,
             "gen": {"ms": g_ms, "bytes": b_gen, "GBps": gen_gbs, "frac": gen_gbs / peak,
                     "samples": S, "Gsamples_per_s": S / (g_ms * 1e-3) / 1e9},
