@@ -43,6 +43,7 @@
 // high pass, which is deterministic.
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 
 #include "vdi_common.cuh"
 #include "vdi_internal.h"
