@@ -89,6 +89,43 @@ def kingsnake(dims=(1024, 1024, 795), seed: int = 1) -> Volume:
     return make_volume(data, "u8")
 
 
+def rt_like(n: int = 1024, seed: int = 2) -> Volume:
+    """Rayleigh-Taylor-shaped f32 volume: a perturbed
+    heavy/light interface z = h(x, y) = 0.5 + sum_m A_m sin(2 pi k_m . (x, y) +
+    phi_m) (16 integer wave vectors, |k| in [2, 16], A ~ 1/|k|, sum A = 0.12),
+    density rho = 0.5 - 0.5 tanh((z - h) / 0.02), plus 3-octave separable
+    sinusoidal noise of amplitude 0.05 within |z - h| < 0.1, clipped to [0, 1]."""
+    rng = np.random.default_rng(seed)
+    ks = []
+    while len(ks) < 16:
+        k = rng.integers(-16, 17, size=2)
+        if 2 <= np.hypot(*k) <= 16:
+            ks.append(k)
+    ks = np.array(ks, dtype=np.float64)
+    amp = 1.0 / np.hypot(ks[:, 0], ks[:, 1])
+    amp *= 0.12 / amp.sum()
+    phi = rng.uniform(0, 2 * np.pi, 16)
+    u = (np.arange(n, dtype=np.float64) + 0.5) / n
+    X, Y = np.meshgrid(u, u, indexing="xy")  # (ny, nx)
+    h = 0.5 + sum(amp[m] * np.sin(2 * np.pi * (ks[m, 0] * X + ks[m, 1] * Y) + phi[m])
+                  for m in range(16))
+    octs = [(4.0 * 2 ** o, 0.05 / 2 ** o, rng.uniform(0, 2 * np.pi, 3)) for o in range(3)]
+    sx = [np.sin(2 * np.pi * f * u + p[0])[None, :] for f, _, p in octs]
+    sy = [np.sin(2 * np.pi * f * u + p[1])[:, None] for f, _, p in octs]
+    sxy = [(a * sx[i] * sy[i]).astype(np.float32) for i, (f, a, p) in enumerate(octs)]
+    h32 = h.astype(np.float32)
+    data = np.empty((n, n, n), dtype=np.float32)
+    for iz in range(n):
+        z = np.float32(u[iz])
+        dz = z - h32
+        rho = np.float32(0.5) - np.float32(0.5) * np.tanh(dz / np.float32(0.02))
+        noise = sum(sxy[i] * np.float32(np.sin(2 * np.pi * f * u[iz] + p[2]))
+                    for i, (f, a, p) in enumerate(octs))
+        rho = np.where(np.abs(dz) < np.float32(0.1), rho + noise, rho)
+        data[iz] = np.clip(rho, 0.0, 1.0)
+    return make_volume(data, "f32")
+
+
 def preset_volume(preset: str, dims: int = 128) -> Volume:
     """The reference's sphere / bands presets (synth.py:25-58), u8."""
     c1 = np.arange(dims, dtype=np.float64) + 0.5
@@ -131,6 +168,7 @@ CONFIGS = {
     "C1": (lambda: blobs(64), "blobs", (128, 128), 20, 2.8, 15.0),
     "C2": (lambda: blobs(256), "blobs", (512, 512), 20, 2.8, 15.0),
     "C3": (lambda: kingsnake(), "kingsnake", (1920, 1080), 20, 1.6, 15.0),
+    "C4": (lambda: rt_like(), "rt", (1920, 1080), 30, 1.6, 15.0),
 }
 
 
