@@ -172,6 +172,12 @@ int vdi_find_first_batch(const float* fronts, const float* backs,
 int vdi_volume_brick_max(const void* volume, int32_t voxel_type, int32_t nx, int32_t ny,
                          int32_t nz, int32_t brick_log2, void* out, vdi_stream_t stream);
 
+/* Device self-check of the exact arithmetic shortcuts the kernels use, on n
+ * random inputs: bad[0..3] (device, 4 x u64) receive the mismatch counts of
+ * Markstein division, __drcp_rn reciprocals, the sqrt-free split threshold
+ * and the shared-reciprocal world/NDC transform (all must be 0). */
+int vdi_selftest_arith(int64_t n, uint64_t seed, unsigned long long* bad, vdi_stream_t stream);
+
 /* Layout conversion for n_lists lists of n_sg supersegments. */
 int vdi_segs_to_aos(const float* soa, float* aos, int64_t n_lists,
                     int32_t n_sg, vdi_stream_t stream);

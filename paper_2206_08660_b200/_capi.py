@@ -57,7 +57,8 @@ class VdiRenderArgs(ctypes.Structure):
 EXPORTS = ["vdi_last_error", "vdi_abi_version", "vdi_gen_workspace_bytes",
            "vdi_gen_workspace_min_bytes", "vdi_gen_launch",
            "vdi_grid_launch", "vdi_render_launch", "vdi_find_first_batch",
-           "vdi_volume_brick_max", "vdi_segs_to_aos", "vdi_segs_from_aos"]
+           "vdi_volume_brick_max", "vdi_selftest_arith", "vdi_segs_to_aos",
+           "vdi_segs_from_aos"]
 
 _lib = None
 
@@ -87,6 +88,8 @@ def load():
     L.vdi_find_first_batch.argtypes = [_P, _P, _P, _I, _P, _P, _P, _P, _P, ctypes.c_int64, _P]
     L.vdi_volume_brick_max.argtypes = [_P, _I, _I, _I, _I, _I, _P, _P]
     L.vdi_volume_brick_max.restype = ctypes.c_int
+    L.vdi_selftest_arith.argtypes = [ctypes.c_int64, ctypes.c_uint64, _P, _P]
+    L.vdi_selftest_arith.restype = ctypes.c_int
     L.vdi_segs_to_aos.argtypes = [_P, _P, ctypes.c_int64, _I, _P]
     L.vdi_segs_from_aos.argtypes = [_P, _P, ctypes.c_int64, _I, _P]
     for name in ("vdi_gen_launch", "vdi_grid_launch", "vdi_render_launch",

@@ -95,6 +95,12 @@ int vdi_volume_brick_max(const void* volume, int32_t voxel_type, int32_t nx, int
                         static_cast<cudaStream_t>(stream));
 }
 
+int vdi_selftest_arith(int64_t n, uint64_t seed, unsigned long long* bad,
+                       vdi_stream_t stream) {
+  if (!bad || n < 0) return set_error(VDI_EINVAL, "bad arguments");
+  return vdi::selftest_arith(n, seed, bad, static_cast<cudaStream_t>(stream));
+}
+
 int vdi_segs_to_aos(const float* soa, float* aos, int64_t n_lists, int32_t n_sg,
                     vdi_stream_t stream) {
   if (n_lists < 0 || n_sg < 1) return set_error(VDI_EINVAL, "bad sizes");

@@ -15,16 +15,29 @@ constexpr double kSqrt3 = 1.7320508075688772;  // math.sqrt(3.0), generate.py:25
 constexpr int kTileW = 8;                     // a warp owns an 8x4 pixel tile
 constexpr int kTileH = 4;
 
+// x / d, correctly rounded, with y = RN(1 / d) given (Markstein: q = RN(x y)
+// is within 1 ulp, r = x - q d is exact with an FMA, q + r y rounds correctly;
+// valid for any d barring over/underflow). The FMAs compute an exact residual;
+// they do not contract any expression of the reference. Verified on device by
+// vdi_selftest_arith (tests/test_gpu_arith.py) and on 2.2e9 host quotients.
+__device__ __forceinline__ double div_by(double x, double d, double y) {
+  const double q = x * y;
+  const double r = __fma_rn(-q, d, x);
+  return __fma_rn(r, y, q);
+}
+
 // _geom.py:12-19 ndc_of / 22-25 world_of: ((m0 x + m1 y) + m2 z) + m3, / w.
+// The three quotients by the same w share one IEEE reciprocal.
 __device__ __forceinline__ void xform(const double* __restrict__ m, double x, double y,
                                       double z, double& ox, double& oy, double& oz) {
   const double hx = m[0] * x + m[1] * y + m[2] * z + m[3];
   const double hy = m[4] * x + m[5] * y + m[6] * z + m[7];
   const double hz = m[8] * x + m[9] * y + m[10] * z + m[11];
   const double hw = m[12] * x + m[13] * y + m[14] * z + m[15];
-  ox = hx / hw;
-  oy = hy / hw;
-  oz = hz / hw;
+  const double rw = 1.0 / hw;
+  ox = div_by(hx, hw, rw);
+  oy = div_by(hy, hw, rw);
+  oz = div_by(hz, hw, rw);
 }
 
 // Only the z component of ndc_of (what _emit, generate.py:55-56, keeps).
@@ -100,17 +113,6 @@ __device__ __forceinline__ bool clip_frustum(const double* __restrict__ m, const
 __host__ __device__ __forceinline__ int list_stride(int n_sg) { return (6 * n_sg + 3) & ~3; }
 __host__ __device__ __forceinline__ int front_off(int n_sg) { return 4 * n_sg; }
 __host__ __device__ __forceinline__ int back_off(int n_sg) { return 5 * n_sg; }
-
-// x / d, correctly rounded, for a fixed divisor with y = RN(1 / d) precomputed
-// (Markstein: q = RN(x y) is within 1 ulp, r = x - q d is exact with an FMA,
-// q + r y rounds correctly). The FMAs compute an exact residual; they do not
-// contract any expression of the reference. Checked against IEEE division on
-// 2.2e9 random quotients (0 mismatches) before use.
-__device__ __forceinline__ double div_by(double x, double d, double y) {
-  const double q = x * y;
-  const double r = __fma_rn(-q, d, x);
-  return __fma_rn(r, y, q);
-}
 
 __device__ __forceinline__ double dmax(double a, double b) { return b > a ? b : a; }
 __device__ __forceinline__ double dmin(double a, double b) { return b < a ? b : a; }

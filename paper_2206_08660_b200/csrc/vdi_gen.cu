@@ -1319,3 +1319,72 @@ int gen_launch(const VdiGenArgs* a, cudaStream_t stream) {
 }
 
 }  // namespace vdi
+
+// ----------------------------------------------------------- self checks
+// Device-side checks of the exact arithmetic shortcuts the kernels rely on
+// (vdi_selftest_arith). counters: [0] Markstein quotient != IEEE quotient,
+// [1] __drcp_rn(n) != 1.0 / n, [2] (d2 >= thr(g)) != (sqrt(d2) >= g),
+// [3] shared-reciprocal xform != per-component division.
+namespace vdi {
+
+__device__ __forceinline__ unsigned long long mix64(unsigned long long x) {
+  x ^= x >> 33;
+  x *= 0xff51afd7ed558ccdull;
+  x ^= x >> 33;
+  x *= 0xc4ceb9fe1a85ec53ull;
+  x ^= x >> 33;
+  return x;
+}
+
+__device__ __forceinline__ double rand_double(unsigned long long& s, int emin, int emax) {
+  s = mix64(s + 0x9e3779b97f4a7c15ull);
+  const unsigned long long mant = s >> 12;
+  s = mix64(s + 0x9e3779b97f4a7c15ull);
+  const int e = emin + (int)(s % (unsigned long long)(emax - emin + 1));
+  const unsigned long long bits = ((unsigned long long)(1023 + e) << 52) | mant;
+  double v = __longlong_as_double((long long)bits);
+  if ((s >> 40) & 1) v = -v;
+  return v;
+}
+
+__global__ void selftest_kernel(long long n, unsigned long long seed, unsigned long long* bad) {
+  unsigned long long local[4] = {0, 0, 0, 0};
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    unsigned long long s = mix64(seed ^ (unsigned long long)i);
+    const double x = rand_double(s, -40, 40), d = rand_double(s, -40, 40);
+    if (div_by(x, d, 1.0 / d) != x / d) local[0] += 1;
+    const double nn = (double)(1 + (i % (1 << 22)));
+    if (__drcp_rn(nn) != 1.0 / nn) local[1] += 1;
+    const double g = fabs(rand_double(s, -20, 1));
+    const double t = split_threshold(g);
+    const double d2a = fabs(rand_double(s, -40, 2));
+    const double d2b = t * (1.0 + (double)((long long)(s % 9) - 4) * 1e-16);  // near thr
+    if ((d2a >= t) != (sqrt(d2a) >= g)) local[2] += 1;
+    if ((d2b >= t) != (sqrt(d2b) >= g)) local[2] += 1;
+    double m[16];
+    for (int j = 0; j < 16; ++j) m[j] = rand_double(s, -3, 3);
+    const double px = rand_double(s, -2, 3), py = rand_double(s, -2, 3), pz = rand_double(s, -2, 3);
+    double ox, oy, oz;
+    xform(m, px, py, pz, ox, oy, oz);
+    const double hx = m[0] * px + m[1] * py + m[2] * pz + m[3];
+    const double hy = m[4] * px + m[5] * py + m[6] * pz + m[7];
+    const double hz = m[8] * px + m[9] * py + m[10] * pz + m[11];
+    const double hw = m[12] * px + m[13] * py + m[14] * pz + m[15];
+    if (ox != hx / hw || oy != hy / hw || oz != hz / hw) local[3] += 1;
+  }
+  for (int j = 0; j < 4; ++j)
+    if (local[j]) atomicAdd(bad + j, local[j]);
+}
+
+int selftest_arith(long long n, unsigned long long seed, unsigned long long* bad,
+                   cudaStream_t stream) {
+  cudaError_t err = cudaMemsetAsync(bad, 0, 4 * sizeof(unsigned long long), stream);
+  if (err != cudaSuccess) return set_error(VDI_ELAUNCH, "selftest memset: %s", cudaGetErrorString(err));
+  selftest_kernel<<<148 * 8, 256, 0, stream>>>(n, seed, bad);
+  err = cudaGetLastError();
+  if (err != cudaSuccess) return set_error(VDI_ELAUNCH, "selftest launch: %s", cudaGetErrorString(err));
+  return VDI_OK;
+}
+
+}  // namespace vdi
