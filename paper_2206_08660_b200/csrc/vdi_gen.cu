@@ -728,7 +728,16 @@ struct EntryPipe {
   }
 };
 
-constexpr int kInvSmem = 4096;  // 32 KiB of 1/n per block; larger n use __drcp_rn
+constexpr int kInvSmem = 4096;  // 32 KiB of 1/n per block; larger n read the global table
+// The table is read through a 32-bit shared address computed once per thread
+// (ld.shared): plain C++ accesses made the compiler rebuild the CTA's shared
+// window base (S2R SR_CgaCtaId + LEA) at every read in the hot loop.
+__shared__ double g_s_inv[kInvSmem];
+__device__ __forceinline__ double lds_f64(unsigned addr) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];\n" : "=d"(v) : "r"(addr));
+  return v;
+}
 
 struct CountState {
   double mr, mg, mb, thr;
@@ -751,10 +760,10 @@ __device__ __forceinline__ void count_reset(CountState& q, double gamma) {
 // selected so the G states of a lane run as straight-line FP64 code.
 //  * t = s - m is exactly -(m - s), so t*t reproduces R's dr*dr bit for bit and
 //    m + t*inv is R's `m += (s - m) * inv`;
-//  * __drcp_rn(n) is the IEEE round-to-nearest reciprocal, i.e. exactly the
-//    host's 1.0 / n.
+//  * 1/n comes from the table of host-identical IEEE quotients.
 __device__ __forceinline__ void count_sample(CountState& q, double sr, double sg, double sb,
-                                             int k, int n_sg, const double* s_inv, int inv_n) {
+                                             int k, int n_sg, int inv_n, const double* g_inv,
+                                             unsigned s_inv) {
   const double tr = sr - q.mr, tg = sg - q.mg, tb = sb - q.mb;
   const bool far = tr * tr + tg * tg + tb * tb >= q.thr;
   const bool live = q.n < 0;
@@ -762,7 +771,10 @@ __device__ __forceinline__ void count_sample(CountState& q, double sr, double sg
   const bool split = q.active && far;
   const bool abort = (!q.active && q.count >= n_sg) || (split && q.count + 1 >= n_sg);
   const int ns = q.nsamp + 1;
-  const double inv = ns < inv_n ? s_inv[ns] : __drcp_rn((double)ns);
+  // nsamp <= max_steps, which the global table always covers; the shared copy
+  // holds the first inv_n entries (selecting between two loads, never a
+  // reciprocal sequence)
+  const double inv = ns < inv_n ? lds_f64(s_inv + 8u * (unsigned)ns) : __ldg(g_inv + ns);
   const double nr = q.mr + tr * inv, ng = q.mg + tg * inv, nb = q.mb + tb * inv;
   if (live && abort) {
     q.n = n_sg + 1;
@@ -782,9 +794,12 @@ template <int kLevels, int kDepth, int kPF, int kMinB = 1>
 __global__ void __launch_bounds__(kGenThreads, kMinB) gen_bisect_kernel(const GenConst c) {
   constexpr int kG = (1 << kLevels) - 1;
   // 1/n for the running means: host-identical IEEE quotients in shared memory
-  extern __shared__ double s_inv[];
   const int inv_n = c.inv_n < kInvSmem ? c.inv_n : kInvSmem;
-  for (int i = threadIdx.x; i < inv_n; i += blockDim.x) s_inv[i] = c.inv_tab[i];
+  for (int i = threadIdx.x; i < inv_n; i += blockDim.x) g_s_inv[i] = c.inv_tab[i];
+  // opaque copy: keeps the address in a register instead of letting ptxas
+  // rematerialise it from SR_CgaCtaId at every use
+  unsigned s_inv;
+  asm volatile("mov.u32 %0, %1;\n" : "=r"(s_inv) : "r"((unsigned)__cvta_generic_to_shared(g_s_inv)));
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const long long nrec = (long long)c.ctl->nrec;
@@ -908,7 +923,8 @@ __global__ void __launch_bounds__(kGenThreads, kMinB) gen_bisect_kernel(const Ge
         const double sg = (double)e.y * a_adj;
         const double sb = (double)e.z * a_adj;
 #pragma unroll
-        for (int i = 0; i < kG; ++i) count_sample(q[i], sr, sg, sb, k, n_sg, s_inv, inv_n);
+        for (int i = 0; i < kG; ++i)
+          count_sample(q[i], sr, sg, sb, k, n_sg, inv_n, c.inv_tab, s_inv);
       }
       const int kold = k;
       k += run;
@@ -1189,7 +1205,7 @@ static int plan_gen(const VdiGenArgs* a, GenPlan& p) {
   }
   // the emit kernel uses no shared memory: give the unified L1 everything
   cudaFuncSetAttribute(gen_emit_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
-  p.smem_inv = sizeof(double) * (p.inv_n < kInvSmem ? p.inv_n : kInvSmem);
+  p.smem_inv = 0;  // static shared table (g_s_inv)
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p.per_sm_bisect, p.bisect, kGenThreads,
                                                 p.smem_inv);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p.per_sm_fused, p.fused, kGenThreads, p.smem);
