@@ -1180,26 +1180,16 @@ static int plan_gen(const VdiGenArgs* a, GenPlan& p) {
   p.smem = sizeof(double4) * a->lut_n;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p.per_sm_sample, p.sample, kGenThreads, p.smem);
   {
-    // VDI_BISECT_VARIANT = "levels,depth,prefetch" (tuning switch; default 2,2,1)
+    // VDI_BISECT_VARIANT = "levels,depth,prefetch[,minblocks]" (tuning switch for
+    // A/B runs; default 2,2,1: 2 speculated levels, 2-entry register pipe, L1
+    // line prefetch). See profiles/ for the variants measured this round.
     const char* env = getenv("VDI_BISECT_VARIANT");
     int lv = 2, dp = 2, pf = 1, mb = 0;
     if (env) sscanf(env, "%d,%d,%d,%d", &lv, &dp, &pf, &mb);
     const int key = mb ? lv * 1000 + dp * 100 + pf * 10 + mb : lv * 100 + dp * 10 + pf;
     switch (key) {
-      case 120: p.bisect = gen_bisect_kernel<1, 2, 0>; break;
-      case 141: p.bisect = gen_bisect_kernel<1, 4, 1>; break;
-      case 142: p.bisect = gen_bisect_kernel<1, 4, 2>; break;
-      case 220: p.bisect = gen_bisect_kernel<2, 2, 0>; break;
-      case 222: p.bisect = gen_bisect_kernel<2, 2, 2>; break;
-      case 241: p.bisect = gen_bisect_kernel<2, 4, 1>; break;
-      case 242: p.bisect = gen_bisect_kernel<2, 4, 2>; break;
-      case 282: p.bisect = gen_bisect_kernel<2, 8, 2>; break;
-      case 342: p.bisect = gen_bisect_kernel<3, 4, 2>; break;
-      case 2215: p.bisect = gen_bisect_kernel<2, 2, 1, 5>; break;
-      case 2216: p.bisect = gen_bisect_kernel<2, 2, 1, 6>; break;
-      case 2218: p.bisect = gen_bisect_kernel<2, 2, 1, 8>; break;
-      case 1216: p.bisect = gen_bisect_kernel<1, 2, 1, 6>; break;
-      case 1218: p.bisect = gen_bisect_kernel<1, 2, 1, 8>; break;
+      case 120: p.bisect = gen_bisect_kernel<1, 2, 0>; break;  // one gamma per replay
+      case 242: p.bisect = gen_bisect_kernel<2, 4, 2>; break;  // deeper entry pipe, L2 hint
       default: p.bisect = gen_bisect_kernel<2, 2, 1>; break;
     }
   }
