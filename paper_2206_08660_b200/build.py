@@ -26,7 +26,7 @@ NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-fmad=false", "-std=c++17",
     "-Xcompiler", "-fPIC", "-Xptxas", "-v", "--expt-relaxed-constexpr",
-]
+] + os.environ.get("VDI_NVCC_EXTRA", "").split()  # tuning experiments only
 
 
 def nvcc() -> str:

@@ -51,6 +51,9 @@
 namespace vdi {
 
 constexpr int kGenThreads = 128;
+#ifndef VDI_SAMPLE_MINB
+#define VDI_SAMPLE_MINB 1
+#endif
 constexpr int kRounds = 3;
 
 enum PassMode : int { kCount = 0, kCapped = 1, kRedo = 2 };
@@ -559,7 +562,7 @@ __device__ __forceinline__ void load_lut(const GenConst& c, double4* s_lut, doub
 
 // ------------------------------------------------------------ sample phase
 template <int VT>
-__global__ void __launch_bounds__(kGenThreads) gen_sample_kernel(const GenConst c) {
+__global__ void __launch_bounds__(kGenThreads, VDI_SAMPLE_MINB) gen_sample_kernel(const GenConst c) {
   extern __shared__ double4 s_lut[];
   __shared__ double s_u8[256];
   load_lut(c, s_lut, s_u8);
