@@ -237,9 +237,17 @@ def run_b200(args):
     import torch.distributed as tdist
 
     world, rank, local = dist_env()
-    torch.cuda.set_device(local)
+    # one process per GPU; VDI_DIST_BACKEND=gloo with more ranks than GPUs is a
+    # plumbing check of the multi-rank path on one device (collectives on the
+    # host, no kernel waits on another rank), never a measurement
+    dev = local % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(dev)
+    backend = os.environ.get("VDI_DIST_BACKEND", "nccl")
     if world > 1:
-        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            tdist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            tdist.init_process_group(backend)
     from paper_2206_08660_b200 import device as dv
     from paper_2206_08660_b200 import shard
     from paper_2206_08660_b200.generate import GenParams
@@ -260,7 +268,7 @@ def run_b200(args):
     S = pipe.samples_executed()            # this rank's executed samples (R semantics)
     stats = pipe.render_stats()            # this rank's (L, K, L_s)
 
-    clocks = ClockSampler(local)
+    clocks = ClockSampler(dev)
     step_ms, gen_ms, grid_ms, coll_ms, ren_ms = [], [], [], [], []
     clocks.start()
     for _ in range(args.steps):
@@ -296,7 +304,9 @@ def run_b200(args):
     ren_gbs = b_ren / (r_ms * 1e-3) / 1e9
     dominant = "vdi_gen" if g_ms >= r_ms else "vdi_render"
     ach = gen_gbs if dominant == "vdi_gen" else ren_gbs
-    traffic, traffic_src = gen_traffic(args.config) if dominant == "vdi_gen" else (None, None)
+    # the committed ncu capture is of the full-frame (N=1) generation
+    traffic, traffic_src = (gen_traffic(args.config) if dominant == "vdi_gen" and world == 1
+                            else (None, None))
     roof = {"kernel": dominant, "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
             "frac": ach / peak, "peak_kind": peak_kind, "traffic": traffic,
             "traffic_source": traffic_src,
