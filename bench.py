@@ -218,13 +218,21 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+DESCRIBE = {
+    "C1": "64^3 f32 Gaussian blobs",
+    "C2": "256^3 f32 Gaussian blobs",
+    "C3": "Kingsnake-shaped 1024x1024x795 u8",
+    "C4": "Rayleigh-Taylor-shaped 1024^3 f32",
+}
+
+
 def config_dict(args, gcam, n_sg, note=None):
     w, h = gcam.viewport
-    d = {"workload": f"{args.config}: Kingsnake-shaped 1024x1024x795 u8, {w}x{h}, "
+    d = {"workload": f"{args.config}: {DESCRIBE.get(args.config, args.config)}, {w}x{h}, "
                      f"n_sg {n_sg}, generate @0deg + render @15deg",
          "rays_per_step": 2 * w * h, "viewport": [w, h], "n_sg": n_sg,
          "parallelism": f"ray-band shard x{args.gpus}",
-         "l2": "256 MiB L2-flush write between timed steps; volume (795 MiB) > L2"}
+         "l2": "256 MiB L2-flush write between timed steps"}
     if note:
         d["note"] = note
     return d
