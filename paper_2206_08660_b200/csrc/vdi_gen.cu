@@ -86,7 +86,8 @@ struct RoundCtl {
   unsigned long long rfetch;    // bisect-phase pool
   unsigned long long ndefer;    // rays deferred to the next round
   unsigned long long efetch;    // emit-phase pool
-  unsigned long long pad[2];
+  unsigned long long ffetch;    // fill-phase pool (one ray per warp)
+  unsigned long long pad[1];
 };
 
 struct GenConst {
@@ -569,9 +570,7 @@ __global__ void __launch_bounds__(kGenThreads, VDI_SAMPLE_MINB) gen_sample_kerne
   const int lane = threadIdx.x & 31;
   const double step = c.a.step;
   WarpPool pool;
-  bool have = false, done = false, fill = false;
-  int run_head = -1, samples1 = 0;
-  long long slot0 = 0;
+  bool have = false, done = false;
   RayState s;
 
   while (true) {
@@ -584,7 +583,6 @@ __global__ void __launch_bounds__(kGenThreads, VDI_SAMPLE_MINB) gen_sample_kerne
           done = true;
         } else if (list >= 0) {
           have = setup_ray(c, s, list);
-          fill = false;
         }
       }
     }
@@ -594,7 +592,7 @@ __global__ void __launch_bounds__(kGenThreads, VDI_SAMPLE_MINB) gen_sample_kerne
     const double ta = s.t0 + (double)s.k * step;
     double tb = ta + step;
     if (tb > s.t1) tb = s.t1;
-    if (!fill) {
+    {
       // pass 1 on the fly (gamma_init, counting mode)
       int ended = 0;
       if (tb > ta) {
@@ -609,8 +607,7 @@ __global__ void __launch_bounds__(kGenThreads, VDI_SAMPLE_MINB) gen_sample_kerne
         have = false;
         continue;
       }
-      // overflow: needs the bisection -> store its samples
-      samples1 = s.samples;
+      // overflow: needs the bisection -> reserve its cache run
       const unsigned long long at = atomicAdd(&c.ctl->bump, (unsigned long long)s.nsteps);
       if (at + (unsigned long long)s.nsteps > c.cache_cap) {
         const unsigned long long j = atomicAdd(&c.ctl->ndefer, 1ull);
@@ -618,36 +615,7 @@ __global__ void __launch_bounds__(kGenThreads, VDI_SAMPLE_MINB) gen_sample_kerne
         have = false;
         continue;
       }
-      slot0 = (long long)at;
-      fill = true;
-      run_head = -1;
-      s.k = 0;
-      continue;
-    }
-    // fill mode: classify step k and store it (transparent runs RLE-coded)
-    float4* cache = c.cache + slot0;
-    bool end = tb <= ta;
-    if (!end) {
-      const float4 rgba = sample_at<VT>(c, s_lut, s_u8, s, ta, tb);
-      if (rgba.w <= 0.0f) {
-        cache[s.k] = make_float4(__int_as_float(1), 0.f, 0.f, 0.f);
-        if (run_head < 0) run_head = s.k;
-      } else {
-        const double dt = tb - ta;
-        const double e = c.lref_pow2 ? dt * c.inv_lref : dt / c.a.lref;
-        float4 st = rgba;
-        if (e != 1.0) st.x = __int_as_float(__float_as_int(st.x) | 0x80000000);
-        cache[s.k] = st;
-        if (run_head >= 0) {
-          cache[run_head].x = __int_as_float(s.k - run_head);
-          run_head = -1;
-        }
-      }
-      s.k += 1;
-      end = s.k >= s.nsteps;
-    }
-    if (end) {
-      if (run_head >= 0) cache[run_head].x = __int_as_float(s.k - run_head);
+      // queue it; gen_fill_kernel stores its samples one warp per ray
       const unsigned long long j = atomicAdd(&c.ctl->nrec, 1ull);
       RayRec r;
       r.d[0] = s.d[0];
@@ -655,10 +623,10 @@ __global__ void __launch_bounds__(kGenThreads, VDI_SAMPLE_MINB) gen_sample_kerne
       r.d[2] = s.d[2];
       r.t0 = s.t0;
       r.t1 = s.t1;
-      r.slot = slot0;
+      r.slot = (long long)at;
       r.list = s.list;
-      r.nsteps = s.k;  // == samples stored (a tb <= ta break stops earlier)
-      r.samples = samples1;
+      r.nsteps = s.nsteps;
+      r.samples = s.samples;
       r.passes = 1;
       r.g_final = 0.0;
       r.mode_final = kCount;
@@ -666,6 +634,102 @@ __global__ void __launch_bounds__(kGenThreads, VDI_SAMPLE_MINB) gen_sample_kerne
       c.recs[j] = r;
       have = false;
     }
+  }
+}
+
+// -------------------------------------------------------------- fill phase
+// One warp per queued ray: lane j classifies sample kb + j of 32-sample chunks
+// and stores it in the ray's cache run (coalesced 512 B per chunk, coherent
+// gathers, no lane idles on another ray). Transparent runs are run-length
+// coded with ballot masks: a run's head entry holds the distance to the next
+// visible sample (or to the end of the row); the open run of a chunk is
+// carried to the next. The non-transparent entries carry the pow flag (sign
+// of r) exactly as the lane-per-ray fill did. Sets rec->nsteps to the number
+// of samples stored (the tb <= ta break, generate.py:113-117, stops earlier).
+template <int VT>
+__global__ void __launch_bounds__(kGenThreads) gen_fill_kernel(const GenConst c) {
+  extern __shared__ double4 s_lut[];
+  __shared__ double s_u8[256];
+  load_lut(c, s_lut, s_u8);
+  const int lane = threadIdx.x & 31;
+  const long long nrec = (long long)c.ctl->nrec;
+  const double step = c.a.step;
+  RayState s;
+  s.o[0] = c.a.eye[0];
+  s.o[1] = c.a.eye[1];
+  s.o[2] = c.a.eye[2];
+  while (true) {
+    long long idx = 0;
+    if (lane == 0) idx = (long long)atomicAdd(&c.ctl->ffetch, 1ull);
+    idx = __shfl_sync(0xffffffffu, idx, 0);
+    if (idx >= nrec) break;
+    RayRec* rec = c.recs + idx;
+    s.d[0] = rec->d[0];
+    s.d[1] = rec->d[1];
+    s.d[2] = rec->d[2];
+    s.t0 = rec->t0;
+    s.t1 = rec->t1;
+    const int nsteps = rec->nsteps;
+    float4* cache = c.cache + rec->slot;
+    int open_head = -1;  // warp-uniform
+    int stored = nsteps;
+    for (int kb = 0; kb < stored; kb += 32) {
+      const int k = kb + lane;
+      bool valid = k < stored;
+      double ta = 0.0, tb = 0.0;
+      if (valid) {
+        ta = s.t0 + (double)k * step;
+        tb = ta + step;
+        if (tb > s.t1) tb = s.t1;
+        valid = tb > ta;
+      }
+      // the reference loop breaks at the first k with tb <= ta
+      const unsigned broke = __ballot_sync(0xffffffffu, k < stored && !valid);
+      if (broke) stored = kb + __ffs(broke) - 1;
+      valid = k < stored;
+      float4 rgba = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (valid) rgba = sample_at<VT>(c, s_lut, s_u8, s, ta, tb);
+      const bool transp = valid && rgba.w <= 0.0f;
+      const unsigned tm = __ballot_sync(0xffffffffu, transp);
+      const unsigned vm = __ballot_sync(0xffffffffu, valid);
+      const unsigned nt = vm & ~tm;  // visible samples of the chunk
+      // a transparent lane 0 continues the run carried from the previous chunk
+      const unsigned prev_t = (tm << 1) | (open_head >= 0 ? 1u : 0u);
+      const unsigned heads = tm & ~prev_t;
+      // close the carried run at the chunk's first visible sample
+      if (open_head >= 0 && nt) {
+        if (lane == 0)
+          cache[open_head].x = __int_as_float(kb + __ffs(nt) - 1 - open_head);
+        open_head = -1;
+      }
+      if (valid) {
+        float4 st;
+        if (transp) {
+          int len = 1;
+          if ((heads >> lane) & 1u) {
+            const unsigned after = nt & ~((2u << lane) - 1u);
+            len = after ? __ffs(after) - 1 - lane : 1;  // open runs are patched later
+          }
+          st = make_float4(__int_as_float(len), 0.f, 0.f, 0.f);
+        } else {
+          const double dt = tb - ta;
+          const double e = c.lref_pow2 ? dt * c.inv_lref : dt / c.a.lref;
+          st = rgba;
+          if (e != 1.0) st.x = __int_as_float(__float_as_int(st.x) | 0x80000000);
+        }
+        cache[k] = st;
+      }
+      // the last head without a visible sample after it stays open
+      if (heads) {
+        const int last = 31 - __clz(heads);
+        const unsigned after = nt & ~((2u << last) - 1u);
+        if (!after) open_head = kb + last;
+      }
+      __syncwarp();
+    }
+    if (open_head >= 0 && lane == 0) cache[open_head].x = __int_as_float(stored - open_head);
+    if (lane == 0) rec->nsteps = stored;
+    __syncwarp();
   }
 }
 
@@ -1145,8 +1209,9 @@ __global__ void fill_inv_kernel(double* tab, int n) {
 struct GenPlan {
   void (*sample)(const GenConst);
   void (*fused)(const GenConst);
+  void (*fill)(const GenConst);
   void (*bisect)(const GenConst);
-  int sms, per_sm_sample, per_sm_bisect, per_sm_emit, per_sm_fused;
+  int sms, per_sm_sample, per_sm_fill, per_sm_bisect, per_sm_emit, per_sm_fused;
   int max_steps, inv_n;
   long long n_rays;
   size_t off_ctl, off_inv, off_recs, off_defer0, off_defer1, off_cache;
@@ -1157,14 +1222,17 @@ static int plan_gen(const VdiGenArgs* a, GenPlan& p) {
   switch (a->voxel_type) {
     case VDI_VOXEL_U8:
       p.sample = gen_sample_kernel<VDI_VOXEL_U8>;
+      p.fill = gen_fill_kernel<VDI_VOXEL_U8>;
       p.fused = gen_fused_kernel<VDI_VOXEL_U8>;
       break;
     case VDI_VOXEL_U16:
       p.sample = gen_sample_kernel<VDI_VOXEL_U16>;
+      p.fill = gen_fill_kernel<VDI_VOXEL_U16>;
       p.fused = gen_fused_kernel<VDI_VOXEL_U16>;
       break;
     case VDI_VOXEL_F32:
       p.sample = gen_sample_kernel<VDI_VOXEL_F32>;
+      p.fill = gen_fill_kernel<VDI_VOXEL_F32>;
       p.fused = gen_fused_kernel<VDI_VOXEL_F32>;
       break;
     default:
@@ -1182,6 +1250,8 @@ static int plan_gen(const VdiGenArgs* a, GenPlan& p) {
   cudaDeviceGetAttribute(&p.sms, cudaDevAttrMultiProcessorCount, dev);
   p.smem = sizeof(double4) * a->lut_n;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p.per_sm_sample, p.sample, kGenThreads, p.smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p.per_sm_fill, p.fill, kGenThreads, p.smem);
+  if (p.per_sm_fill < 1) p.per_sm_fill = 1;
   {
     // VDI_BISECT_VARIANT = "levels,depth,prefetch[,minblocks]" (tuning switch for
     // A/B runs; default 2,2,1: 2 speculated levels, 2-entry register pipe, L1
@@ -1306,6 +1376,7 @@ int gen_launch(const VdiGenArgs* a, cudaStream_t stream) {
     c.defer_in = defer[(r + 1) & 1];
     c.defer_out = defer[r & 1];
     p.sample<<<grid_for(p.per_sm_sample, r == 0 ? chunks : -1), kGenThreads, p.smem, stream>>>(c);
+    p.fill<<<grid_for(p.per_sm_fill, -1), kGenThreads, p.smem, stream>>>(c);
     p.bisect<<<grid_for(p.per_sm_bisect, -1), kGenThreads, p.smem_inv, stream>>>(c);
     gen_emit_kernel<<<grid_for(p.per_sm_emit, -1), kGenThreads, 0, stream>>>(c);
   }
