@@ -1257,13 +1257,14 @@ static int plan_gen(const VdiGenArgs* a, GenPlan& p) {
     // A/B runs; default 2,2,1: 2 speculated levels, 2-entry register pipe, L1
     // line prefetch). See profiles/ for the variants measured this round.
     const char* env = getenv("VDI_BISECT_VARIANT");
-    int lv = 2, dp = 2, pf = 1, mb = 0;
+    int lv = 2, dp = 2, pf = 1, mb = 5;
     if (env) sscanf(env, "%d,%d,%d,%d", &lv, &dp, &pf, &mb);
     const int key = mb ? lv * 1000 + dp * 100 + pf * 10 + mb : lv * 100 + dp * 10 + pf;
     switch (key) {
       case 120: p.bisect = gen_bisect_kernel<1, 2, 0>; break;  // one gamma per replay
       case 242: p.bisect = gen_bisect_kernel<2, 4, 2>; break;  // deeper entry pipe, L2 hint
-      default: p.bisect = gen_bisect_kernel<2, 2, 1>; break;
+      case 221: p.bisect = gen_bisect_kernel<2, 2, 1>; break;  // unconstrained registers
+      default: p.bisect = gen_bisect_kernel<2, 2, 1, 5>; break;  // <= 102 regs, 5 blocks/SM
     }
   }
   // the emit kernel uses no shared memory: give the unified L1 everything
