@@ -44,6 +44,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <type_traits>
 
 #include "vdi_common.cuh"
 #include "vdi_internal.h"
@@ -104,6 +105,7 @@ struct GenConst {
   long long n_slots;  // tiles * 32
   const double* inv_tab;  // inv_tab[n] == 1.0 / n, bit-exact (host IEEE division)
   int inv_n;
+  int inv_smem;       // leading inv_tab entries the bisect phase stages in shared memory
   int max_steps;
   float4* cache;
   unsigned long long cache_cap;  // float4 entries
@@ -754,24 +756,37 @@ __global__ void __launch_bounds__(kGenThreads) gen_fill_kernel(const GenConst c)
 // exactly the reference's.
 
 // Cache rows are read sequentially by one lane; a 128 B line holds 8 entries.
-constexpr int kPrefetchAhead = 16;
 __device__ __forceinline__ void prefetch_l1(const void* p) {
   asm volatile("prefetch.global.L1 [%0];\n" ::"l"(p));
 }
 __device__ __forceinline__ void prefetch_l2(const void* p) {
   asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p));
 }
+// TMA bulk prefetch of `bytes` (multiple of 16, 16-B aligned) into L2
+__device__ __forceinline__ void prefetch_l2_bulk(const void* p, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(p), "r"(bytes) : "memory");
+}
+constexpr int kBulkEntries = 32;  // 512 B of cache row per bulk prefetch
 
 // A lane's stream of cache entries: b[i] holds entry k + i (loads in flight),
-// plus a cache-level prefetch kPrefetchAhead entries ahead at line crossings
-// (PF: 0 none, 1 into L1, 2 into L2).
-template <int D, int PF>
+// plus a cache-level prefetch kAhead entries ahead at line crossings
+// (PF: 0 none, 1 into L1, 2 into L2, 3 = 1 plus a bulk L2 prefetch of the next
+// kBulkEntries-entry chunk whenever the lane enters a chunk).
+template <int D, int PF, int kAhead = 16>
 struct EntryPipe {
   float4 b[D];
+  __device__ __forceinline__ float4 cur() const { return b[0]; }
   __device__ __forceinline__ void prefetch(const float4* row, int at, int stored) {
     if (at < stored) {
-      if (PF == 1) prefetch_l1(row + at);
+      if (PF == 1 || PF == 3) prefetch_l1(row + at);
       if (PF == 2) prefetch_l2(row + at);
+    }
+  }
+  __device__ __forceinline__ void bulk(const float4* row, int chunk, int stored) {
+    const int at = chunk * kBulkEntries;
+    if (at < stored) {
+      const int n = stored - at < kBulkEntries ? stored - at : kBulkEntries;
+      prefetch_l2_bulk(row + at, 16u * (unsigned)n);
     }
   }
   __device__ __forceinline__ void start(const float4* row, int k, int stored) {
@@ -780,7 +795,11 @@ struct EntryPipe {
       if (k + i < stored) b[i] = row[k + i];
     if (PF) {
       prefetch(row, (k & ~7) + 8, stored);
-      prefetch(row, (k & ~7) + kPrefetchAhead, stored);
+      if (kAhead > 8) prefetch(row, (k & ~7) + kAhead, stored);
+    }
+    if (PF == 3) {
+      bulk(row, k / kBulkEntries, stored);
+      bulk(row, k / kBulkEntries + 1, stored);
     }
   }
   __device__ __forceinline__ void advance(const float4* row, int kold, int k, int stored) {
@@ -793,16 +812,72 @@ struct EntryPipe {
       for (int i = 0; i < D; ++i)
         if (k + i < stored) b[i] = row[k + i];
     }
-    if (PF && (((kold + kPrefetchAhead) ^ (k + kPrefetchAhead)) & ~7) != 0)
-      prefetch(row, k + kPrefetchAhead, stored);
+    if (PF && (((kold + kAhead) ^ (k + kAhead)) & ~7) != 0)
+      prefetch(row, k + kAhead, stored);
+    if (PF == 3 && kold / kBulkEntries != k / kBulkEntries)
+      bulk(row, k / kBulkEntries + 1, stored);
   }
 };
 
-constexpr int kInvSmem = 4096;  // 32 KiB of 1/n per block; larger n read the global table
-// The table is read through a 32-bit shared address computed once per thread
-// (ld.shared): plain C++ accesses made the compiler rebuild the CTA's shared
-// window base (S2R SR_CgaCtaId + LEA) at every read in the hot loop.
-__shared__ double g_s_inv[kInvSmem];
+// Two-slot ring with a parity bit: the entry after the current one is loaded
+// straight into the slot just consumed, so no register shuffle follows the
+// load (EntryPipe's b[0] = b[1] shift made ptxas load into a temporary and
+// move it into place right after the LDG -- a stall on every sample).
+// predicated 16-B load into the registers of `v` itself (left unchanged when
+// !pred): written in PTX so the compiler cannot load into a temporary and
+// select afterwards
+__device__ __forceinline__ void ld_pred(float4& v, const float4* p, bool pred) {
+  asm volatile(
+      "{\n .reg .pred q;\n setp.ne.b32 q, %5, 0;\n"
+      " @q ld.global.nc.v4.f32 {%0, %1, %2, %3}, [%4];\n}\n"
+      : "+f"(v.x), "+f"(v.y), "+f"(v.z), "+f"(v.w)
+      : "l"(p), "r"((int)pred));
+}
+
+template <int PF, int kAhead = 16>
+struct EntryRing {
+  float4 b0, b1;
+  bool par;  // current entry in b1
+  __device__ __forceinline__ float4 cur() const {
+    float4 e;
+    e.x = par ? b1.x : b0.x;
+    e.y = par ? b1.y : b0.y;
+    e.z = par ? b1.z : b0.z;
+    e.w = par ? b1.w : b0.w;
+    return e;
+  }
+  __device__ __forceinline__ void prefetch(const float4* row, int at, int stored) {
+    if (PF == 1 && at < stored) prefetch_l1(row + at);
+  }
+  __device__ __forceinline__ void start(const float4* row, int k, int stored) {
+    par = false;
+    if (k < stored) b0 = row[k];
+    if (k + 1 < stored) b1 = row[k + 1];
+    if (PF) {
+      prefetch(row, (k & ~7) + 8, stored);
+      if (kAhead > 8) prefetch(row, (k & ~7) + kAhead, stored);
+    }
+  }
+  __device__ __forceinline__ void advance(const float4* row, int kold, int k, int stored) {
+    if (k == kold + 1) {
+      const bool more = k + 1 < stored;
+      ld_pred(b1, row + k + 1, more && par);
+      ld_pred(b0, row + k + 1, more && !par);
+      par = !par;
+    } else {
+      start(row, k, stored);
+      return;
+    }
+    if (PF && (((kold + kAhead) ^ (k + kAhead)) & ~7) != 0)
+      prefetch(row, k + kAhead, stored);
+  }
+};
+
+// The leading c.inv_smem entries of the 1/n table live in dynamic shared
+// memory (larger n read the global table). The table is read through a 32-bit
+// shared address computed once per thread (ld.shared): plain C++ accesses made
+// the compiler rebuild the CTA's shared window base (S2R SR_CgaCtaId + LEA) at
+// every read in the hot loop.
 __device__ __forceinline__ double lds_f64(unsigned addr) {
   double v;
   asm volatile("ld.shared.f64 %0, [%1];\n" : "=d"(v) : "r"(addr));
@@ -860,11 +935,13 @@ __device__ __forceinline__ void count_sample(CountState& q, double sr, double sg
   }
 }
 
-template <int kLevels, int kDepth, int kPF, int kMinB = 1>
-__global__ void __launch_bounds__(kGenThreads, kMinB) gen_bisect_kernel(const GenConst c) {
+template <int kLevels, int kDepth, int kPF, int kMinB = 1, int kThreads = kGenThreads,
+          int kAhead = 16, bool kRing = false>
+__global__ void __launch_bounds__(kThreads, kMinB) gen_bisect_kernel(const GenConst c) {
   constexpr int kG = (1 << kLevels) - 1;
+  extern __shared__ double g_s_inv[];
   // 1/n for the running means: host-identical IEEE quotients in shared memory
-  const int inv_n = c.inv_n < kInvSmem ? c.inv_n : kInvSmem;
+  const int inv_n = c.inv_n < c.inv_smem ? c.inv_n : c.inv_smem;
   for (int i = threadIdx.x; i < inv_n; i += blockDim.x) g_s_inv[i] = c.inv_tab[i];
   // opaque copy: keeps the address in a register instead of letting ptxas
   // rematerialise it from SR_CgaCtaId at every use
@@ -879,7 +956,8 @@ __global__ void __launch_bounds__(kGenThreads, kMinB) gen_bisect_kernel(const Ge
   const float4* cache = nullptr;
   RayRec* rec = nullptr;
   int stored = 0, k = 0;
-  EntryPipe<kDepth, kPF> pipe;
+  typename std::conditional<kRing, EntryRing<kPF, kAhead>, EntryPipe<kDepth, kPF, kAhead>>::type
+      pipe;
   // bisection state (generate.py:230-236)
   double low = 0.0, high = 0.0;
   int last_n = 0, high_n = 0, passes = 0, samples = 0;
@@ -964,7 +1042,7 @@ __global__ void __launch_bounds__(kGenThreads, kMinB) gen_bisect_kernel(const Ge
         }
       resolved = true;
      } else {
-      const float4 e = pipe.b[0];
+      const float4 e = pipe.cur();
       int run = 1;
       if (e.w <= 0.0f) {
         run = __float_as_int(e.x);
@@ -1051,6 +1129,8 @@ __global__ void __launch_bounds__(kGenThreads, kMinB) gen_bisect_kernel(const Ge
 // -------------------------------------------------------------- emit phase
 // The deciding pass of every queued ray, replayed with the full
 // _gen_list_pass logic: segments, counts, gammas, passes, samples.
+// kRing: entries through the two-slot EntryRing (next load in flight)
+template <bool kRing>
 __global__ void __launch_bounds__(kGenThreads, VDI_EMIT_MINB) gen_emit_kernel(const GenConst c) {
   const int lane = threadIdx.x & 31;
   const double step = c.a.step;
@@ -1061,6 +1141,7 @@ __global__ void __launch_bounds__(kGenThreads, VDI_EMIT_MINB) gen_emit_kernel(co
   int stored = 0;
   double g = 0.0;
   RayState s;
+  EntryRing<1> ring;
 
   while (true) {
     const unsigned need = __ballot_sync(0xffffffffu, !have && !done);
@@ -1091,6 +1172,7 @@ __global__ void __launch_bounds__(kGenThreads, VDI_EMIT_MINB) gen_emit_kernel(co
           // window hit / cached high: a counting pass that R does not count
           // again (kRedo); capped: R's final capped pass (counted)
           start_pass(s, g, r.mode_final == kCapped ? kCapped : kRedo);
+          if (kRing) ring.start(cache, 0, stored);
           have = true;
         }
       }
@@ -1102,7 +1184,8 @@ __global__ void __launch_bounds__(kGenThreads, VDI_EMIT_MINB) gen_emit_kernel(co
     if (s.k >= stored) {
       ended = 0;
     } else {
-      float4 rgba = cache[s.k];
+      float4 rgba = kRing ? ring.cur() : cache[s.k];
+      const int kold = s.k;
       const double ta = s.t0 + (double)s.k * step;
       double tb = ta + step;
       if (tb > s.t1) tb = s.t1;
@@ -1115,6 +1198,7 @@ __global__ void __launch_bounds__(kGenThreads, VDI_EMIT_MINB) gen_emit_kernel(co
         rgba.x = fabsf(rgba.x);  // drop the pow flag
       }
       ended = segment_step(c, s, rgba, ta, tb, run);
+      if (kRing && ended < 0) ring.advance(cache, kold, s.k, stored);
     }
     if (ended >= 0) {
       const int n = ended == 0 ? close_pass(c, s) : ended;
@@ -1214,7 +1298,9 @@ struct GenPlan {
   void (*fused)(const GenConst);
   void (*fill)(const GenConst);
   void (*bisect)(const GenConst);
+  void (*emit)(const GenConst);
   int sms, per_sm_sample, per_sm_fill, per_sm_bisect, per_sm_emit, per_sm_fused;
+  int bisect_threads, inv_smem;
   int max_steps, inv_n;
   long long n_rays;
   size_t off_ctl, off_inv, off_recs, off_defer0, off_defer1, off_cache;
@@ -1256,29 +1342,44 @@ static int plan_gen(const VdiGenArgs* a, GenPlan& p) {
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p.per_sm_fill, p.fill, kGenThreads, p.smem);
   if (p.per_sm_fill < 1) p.per_sm_fill = 1;
   {
-    // VDI_BISECT_VARIANT = "levels,depth,prefetch[,minblocks]" (tuning switch for
-    // A/B runs; default 2,2,1: 2 speculated levels, 2-entry register pipe, L1
-    // line prefetch). See profiles/ for the variants measured this round.
+    // VDI_BISECT_VARIANT = "levels,depth,prefetch,minblocks,threads,inv,ahead"
+    // (tuning switch for A/B runs). Default 2,9,1,5,128,4096,16: 2 speculated
+    // levels, the two-slot entry ring, L1 line prefetch 16 entries ahead, 5
+    // blocks of 128 per SM (<= 102 registers), 4096 shared 1/n entries.
+    // See profiles/ for the variants measured this round.
     const char* env = getenv("VDI_BISECT_VARIANT");
-    int lv = 2, dp = 2, pf = 1, mb = 5;
-    if (env) sscanf(env, "%d,%d,%d,%d", &lv, &dp, &pf, &mb);
-    const int key = mb ? lv * 1000 + dp * 100 + pf * 10 + mb : lv * 100 + dp * 10 + pf;
+    int lv = 2, dp = 9, pf = 1, mb = 5, th = 128, inv = 4096, ah = 16;
+    if (env) sscanf(env, "%d,%d,%d,%d,%d,%d,%d", &lv, &dp, &pf, &mb, &th, &inv, &ah);
+    const long long key = (((lv * 10LL + dp) * 10 + pf) * 10 + mb) * 10000LL + th * 10LL +
+                          (ah == 8 ? 1 : ah == 32 ? 2 : 0);
+    p.bisect_threads = kGenThreads;
     switch (key) {
-      case 120: p.bisect = gen_bisect_kernel<1, 2, 0>; break;  // one gamma per replay
-      case 242: p.bisect = gen_bisect_kernel<2, 4, 2>; break;  // deeper entry pipe, L2 hint
-      case 221: p.bisect = gen_bisect_kernel<2, 2, 1>; break;  // unconstrained registers
-      default: p.bisect = gen_bisect_kernel<2, 2, 1, 5>; break;  // <= 102 regs, 5 blocks/SM
+      case 1200 * 10000LL + 1280: p.bisect = gen_bisect_kernel<1, 2, 0>; break;
+      case 2225 * 10000LL + 1280: p.bisect = gen_bisect_kernel<2, 2, 1, 5>; break;  // shift pipe
+      case 2914 * 10000LL + 1280: p.bisect = gen_bisect_kernel<2, 2, 1, 4, 128, 16, true>; break;
+      case 2915 * 10000LL + 1282: p.bisect = gen_bisect_kernel<2, 2, 1, 5, 128, 32, true>; break;
+      case 2905 * 10000LL + 1280: p.bisect = gen_bisect_kernel<2, 2, 0, 5, 128, 16, true>; break;
+      default:  // depth "9": the two-slot ring, 5 blocks/SM
+        p.bisect = gen_bisect_kernel<2, 2, 1, 5, 128, 16, true>;
+        break;
     }
+    p.inv_smem = inv < 0 ? 0 : inv;
   }
   // the emit kernel uses no shared memory: give the unified L1 everything
-  cudaFuncSetAttribute(gen_emit_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
-  p.smem_inv = 0;  // static shared table (g_s_inv)
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p.per_sm_bisect, p.bisect, kGenThreads,
+  {
+    const char* env = getenv("VDI_EMIT_RING");  // A/B switch; default: ring
+    p.emit = env && env[0] == '0' ? gen_emit_kernel<false> : gen_emit_kernel<true>;
+  }
+  cudaFuncSetAttribute(p.emit, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
+  p.smem_inv = sizeof(double) * (size_t)(p.inv_smem < p.inv_n ? p.inv_smem : p.inv_n);
+  if (p.smem_inv > 48 * 1024)
+    cudaFuncSetAttribute(p.bisect, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem_inv);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p.per_sm_bisect, p.bisect, p.bisect_threads,
                                                 p.smem_inv);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p.per_sm_fused, p.fused, kGenThreads, p.smem);
   if (p.per_sm_sample < 1) p.per_sm_sample = 1;
   if (p.per_sm_bisect < 1) p.per_sm_bisect = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p.per_sm_emit, gen_emit_kernel, kGenThreads, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p.per_sm_emit, p.emit, kGenThreads, 0);
   if (p.per_sm_emit < 1) p.per_sm_emit = 1;
   if (p.per_sm_fused < 1) p.per_sm_fused = 1;
   const int bands = a->band_rows > 0 ? a->band_rows : 16;
@@ -1354,6 +1455,7 @@ int gen_launch(const VdiGenArgs* a, cudaStream_t stream) {
   RoundCtl* ctl = reinterpret_cast<RoundCtl*>(ws + p.off_ctl);
   c.inv_tab = reinterpret_cast<const double*>(ws + p.off_inv);
   c.inv_n = p.inv_n;
+  c.inv_smem = (int)(p.smem_inv / sizeof(double));
   c.max_steps = p.max_steps;
   c.recs = reinterpret_cast<RayRec*>(ws + p.off_recs);
   c.cache = reinterpret_cast<float4*>(ws + p.off_cache);
@@ -1381,8 +1483,8 @@ int gen_launch(const VdiGenArgs* a, cudaStream_t stream) {
     c.defer_out = defer[r & 1];
     p.sample<<<grid_for(p.per_sm_sample, r == 0 ? chunks : -1), kGenThreads, p.smem, stream>>>(c);
     p.fill<<<grid_for(p.per_sm_fill, -1), kGenThreads, p.smem, stream>>>(c);
-    p.bisect<<<grid_for(p.per_sm_bisect, -1), kGenThreads, p.smem_inv, stream>>>(c);
-    gen_emit_kernel<<<grid_for(p.per_sm_emit, -1), kGenThreads, 0, stream>>>(c);
+    p.bisect<<<grid_for(p.per_sm_bisect, -1), p.bisect_threads, p.smem_inv, stream>>>(c);
+    p.emit<<<grid_for(p.per_sm_emit, -1), kGenThreads, 0, stream>>>(c);
   }
   // leftovers: the fused kernel over the last round's deferred rays
   c.round = kRounds;
