@@ -277,7 +277,7 @@ def run_b200(args):
     stats = pipe.render_stats()            # this rank's (L, K, L_s)
 
     clocks = ClockSampler(dev)
-    step_ms, gen_ms, grid_ms, coll_ms, ren_ms = [], [], [], [], []
+    step_ms, prep_ms, gen_ms, grid_ms, coll_ms, ren_ms = [], [], [], [], [], []
     clocks.start()
     for _ in range(args.steps):
         flush.fill_(1)
@@ -287,6 +287,7 @@ def run_b200(args):
         torch.cuda.synchronize()
         barrier()
         step_ms.append(ev["step"])
+        prep_ms.append(ev["prep"])
         gen_ms.append(ev["gen"])
         grid_ms.append(ev["grid"])
         coll_ms.append(ev["collective"])
@@ -335,7 +336,7 @@ def run_b200(args):
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic", "config": config_dict(args, gcam, n_sg),
             "fps": 1.0 / t_step,
-            "phases_ms": {"gen": g_ms, "grid": float(np.mean(grid_ms)),
+            "phases_ms": {"prep": float(np.mean(prep_ms)), "gen": g_ms, "grid": float(np.mean(grid_ms)),
                           "collective": float(np.mean(coll_ms)), "render": r_ms},
             "gen_mrays_s": w * h / (g_ms * 1e-3) / 1e6,
             "render_mrays_s": w * h / (r_ms * 1e-3) / 1e6,

@@ -57,6 +57,9 @@ extern "C" {
 #define VDI_VOXEL_U8 0
 #define VDI_VOXEL_U16 1
 #define VDI_VOXEL_F32 2
+/* Flag on VdiGenArgs.voxel_type: `volume` holds vdi_volume_cells() corner
+ * records of the base type instead of the plain voxel grid. */
+#define VDI_VOXEL_CELLS 16
 
 #define VDI_LAYOUT_LIST_SOA 0
 #define VDI_LAYOUT_AOS 1
@@ -70,7 +73,8 @@ static inline int32_t vdi_list_stride(int32_t n_sg) { return (6 * n_sg + 3) & ~3
  * implemented in generate.py:219-273), supersegments written in
  * VDI_LAYOUT_LIST_SOA. Outputs are indexed by local row (band map). */
 typedef struct VdiGenArgs {
-  const void* volume;   /* (nz, ny, nx) x-fastest, voxel_type elements */
+  const void* volume;   /* (nz, ny, nx) x-fastest, voxel_type elements; with
+                           VDI_VOXEL_CELLS, vdi_volume_cells() records */
   const float* lut;     /* (lut_n, 4) f32, TransferFunction.lut */
   const void* brick_max;/* vdi_volume_brick_max() of `volume`, or NULL (no skipping) */
   int32_t* counts;      /* OUT (local_h, width) */
@@ -171,6 +175,19 @@ int vdi_find_first_batch(const float* fronts, const float* backs,
  * Used for exact empty-space skipping in vdi_gen_launch. */
 int vdi_volume_brick_max(const void* volume, int32_t voxel_type, int32_t nx, int32_t ny,
                          int32_t nz, int32_t brick_log2, void* out, vdi_stream_t stream);
+
+/* Corner records for generation: cell (x, y, z) of the (nz, ny, nx) grid
+ * becomes the 8 voxels of its trilinear cube, [v(x,y,z), v(x+1,y,z),
+ * v(x,y+1,z), v(x+1,y+1,z), v(x,y,z+1), v(x+1,y,z+1), v(x,y+1,z+1),
+ * v(x+1,y+1,z+1)] (indices clamped to the grid), stored contiguously: one
+ * aligned 8 x sizeof(voxel) load per sample instead of 8 gathers. The same
+ * voxel values, so generation results are unchanged. `out` must hold
+ * vdi_volume_cells_bytes() bytes, 32-byte aligned. Replaces nothing in the
+ * reference: it is this library's HBM layout of Volume.normalized
+ * (volume.py:48-50, read by _trilinear, volume.py:180-205). */
+size_t vdi_volume_cells_bytes(int32_t voxel_type, int32_t nx, int32_t ny, int32_t nz);
+int vdi_volume_cells(const void* volume, int32_t voxel_type, int32_t nx, int32_t ny, int32_t nz,
+                     void* out, vdi_stream_t stream);
 
 /* Device self-check of the exact arithmetic shortcuts the kernels use, on n
  * random inputs: bad[0..3] (device, 4 x u64) receive the mismatch counts of

@@ -13,6 +13,7 @@ _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_PKG, "lib", "libvdi_b200.so")
 
 VOXEL = {"u8": 0, "u16": 1, "f32": 2}
+VOXEL_CELLS = 16  # flag: VdiGenArgs.volume holds vdi_volume_cells() records
 _P = ctypes.c_void_p
 _D = ctypes.c_double
 _I = ctypes.c_int32
@@ -58,7 +59,7 @@ EXPORTS = ["vdi_last_error", "vdi_abi_version", "vdi_gen_workspace_bytes",
            "vdi_gen_workspace_min_bytes", "vdi_gen_launch",
            "vdi_grid_launch", "vdi_render_launch", "vdi_find_first_batch",
            "vdi_volume_brick_max", "vdi_selftest_arith", "vdi_segs_to_aos",
-           "vdi_segs_from_aos"]
+           "vdi_segs_from_aos", "vdi_volume_cells_bytes", "vdi_volume_cells"]
 
 _lib = None
 
@@ -88,6 +89,10 @@ def load():
     L.vdi_find_first_batch.argtypes = [_P, _P, _P, _I, _P, _P, _P, _P, _P, ctypes.c_int64, _P]
     L.vdi_volume_brick_max.argtypes = [_P, _I, _I, _I, _I, _I, _P, _P]
     L.vdi_volume_brick_max.restype = ctypes.c_int
+    L.vdi_volume_cells_bytes.argtypes = [_I, _I, _I, _I]
+    L.vdi_volume_cells_bytes.restype = ctypes.c_size_t
+    L.vdi_volume_cells.argtypes = [_P, _I, _I, _I, _I, _P, _P]
+    L.vdi_volume_cells.restype = ctypes.c_int
     L.vdi_selftest_arith.argtypes = [ctypes.c_int64, ctypes.c_uint64, _P, _P]
     L.vdi_selftest_arith.restype = ctypes.c_int
     L.vdi_segs_to_aos.argtypes = [_P, _P, ctypes.c_int64, _I, _P]

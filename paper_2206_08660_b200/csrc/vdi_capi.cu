@@ -95,6 +95,21 @@ int vdi_volume_brick_max(const void* volume, int32_t voxel_type, int32_t nx, int
                         static_cast<cudaStream_t>(stream));
 }
 
+size_t vdi_volume_cells_bytes(int32_t voxel_type, int32_t nx, int32_t ny, int32_t nz) {
+  const size_t e = voxel_type == VDI_VOXEL_U8 ? 1 : voxel_type == VDI_VOXEL_U16 ? 2
+                   : voxel_type == VDI_VOXEL_F32 ? 4 : 0;
+  if (nx < 1 || ny < 1 || nz < 1) return 0;
+  return 8 * e * (size_t)nx * (size_t)ny * (size_t)nz;
+}
+
+int vdi_volume_cells(const void* volume, int32_t voxel_type, int32_t nx, int32_t ny, int32_t nz,
+                     void* out, vdi_stream_t stream) {
+  if (!volume || !out) return set_error(VDI_EINVAL, "null device pointer");
+  if (nx < 2 || ny < 2 || nz < 2) return set_error(VDI_EINVAL, "bad sizes");
+  if (reinterpret_cast<uintptr_t>(out) & 31) return set_error(VDI_EINVAL, "cells not 32-byte aligned");
+  return vdi::volume_cells(volume, voxel_type, nx, ny, nz, out, static_cast<cudaStream_t>(stream));
+}
+
 int vdi_selftest_arith(int64_t n, uint64_t seed, unsigned long long* bad,
                        vdi_stream_t stream) {
   if (!bad || n < 0) return set_error(VDI_EINVAL, "bad arguments");

@@ -146,7 +146,47 @@ struct Voxel<VDI_VOXEL_U16> {
   }
 };
 
-// volume.py:180-205 _trilinear.
+// Corner records (vdi_volume_cells): the 8 voxels of cell i in one load.
+template <int BT>
+struct Cell;
+template <>
+struct Cell<VDI_VOXEL_U8> {
+  static __device__ __forceinline__ void get(const void* cells, long long i, const double* tab,
+                                             double v[8]) {
+    const uint2 r = __ldg(reinterpret_cast<const uint2*>(cells) + i);
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      v[b] = tab[(r.x >> (8 * b)) & 0xffu];
+      v[4 + b] = tab[(r.y >> (8 * b)) & 0xffu];
+    }
+  }
+};
+template <>
+struct Cell<VDI_VOXEL_U16> {
+  static __device__ __forceinline__ void get(const void* cells, long long i, const double*,
+                                             double v[8]) {
+    const uint4 r = __ldg(reinterpret_cast<const uint4*>(cells) + i);
+    const unsigned w[4] = {r.x, r.y, r.z, r.w};
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      v[2 * b] = (double)__fdiv_rn((float)(w[b] & 0xffffu), 65535.0f);
+      v[2 * b + 1] = (double)__fdiv_rn((float)(w[b] >> 16), 65535.0f);
+    }
+  }
+};
+template <>
+struct Cell<VDI_VOXEL_F32> {
+  static __device__ __forceinline__ void get(const void* cells, long long i, const double*,
+                                             double v[8]) {
+    const float4 a = __ldg(reinterpret_cast<const float4*>(cells) + 2 * i);
+    const float4 b = __ldg(reinterpret_cast<const float4*>(cells) + 2 * i + 1);
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+    v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+  }
+};
+
+// volume.py:180-205 _trilinear. VT is a VDI_VOXEL_* type, optionally with the
+// VDI_VOXEL_CELLS flag (c.a.volume then holds corner records).
 template <int VT>
 __device__ __forceinline__ double trilinear(const GenConst& c, const double* tab, double px,
                                             double py, double pz) {
@@ -166,20 +206,32 @@ __device__ __forceinline__ double trilinear(const GenConst& c, const double* tab
     // row 0, whose alpha is 0: the sample is transparent, as in the reference.
     const int lb = c.a.brick_log2;
     const long long bi = ((long long)(iz >> lb) * c.bny + (iy >> lb)) * c.bnx + (ix >> lb);
-    if (Voxel<VT>::get(c.a.brick_max, bi, tab) <= c.a.ess_max) return -1.0;
+    if (Voxel<(VT & 15)>::get(c.a.brick_max, bi, tab) <= c.a.ess_max) return -1.0;
   }
   const double fx = gx - ix, fy = gy - iy, fz = gz - iz;
+  if (VT & VDI_VOXEL_CELLS) {
+    double v[8];
+    Cell<(VT & 15)>::get(c.a.volume, ((long long)iz * ny + iy) * (long long)nx + ix, tab, v);
+    const double c00 = v[0] * (1 - fx) + v[1] * fx;
+    const double c10 = v[2] * (1 - fx) + v[3] * fx;
+    const double c01 = v[4] * (1 - fx) + v[5] * fx;
+    const double c11 = v[6] * (1 - fx) + v[7] * fx;
+    const double c0 = c00 * (1 - fy) + c10 * fy;
+    const double c1 = c01 * (1 - fy) + c11 * fy;
+    return c0 * (1 - fz) + c1 * fz;
+  }
   // four row pointers, then [ptr + 0/1] gathers (no per-voxel 64-bit math)
-  using T = typename Voxel<VT>::type;
+  using T = typename Voxel<(VT & 15)>::type;
   const T* r00 = static_cast<const T*>(c.a.volume) +
                  ((long long)iz * ny + iy) * (long long)nx + ix;
   const T* r01 = r00 + nx;
   const T* r10 = r00 + (long long)nx * ny;
   const T* r11 = r10 + nx;
-  const double v000 = Voxel<VT>::get(r00, 0, tab), v001 = Voxel<VT>::get(r00, 1, tab);
-  const double v010 = Voxel<VT>::get(r01, 0, tab), v011 = Voxel<VT>::get(r01, 1, tab);
-  const double v100 = Voxel<VT>::get(r10, 0, tab), v101 = Voxel<VT>::get(r10, 1, tab);
-  const double v110 = Voxel<VT>::get(r11, 0, tab), v111 = Voxel<VT>::get(r11, 1, tab);
+  using V = Voxel<(VT & 15)>;
+  const double v000 = V::get(r00, 0, tab), v001 = V::get(r00, 1, tab);
+  const double v010 = V::get(r01, 0, tab), v011 = V::get(r01, 1, tab);
+  const double v100 = V::get(r10, 0, tab), v101 = V::get(r10, 1, tab);
+  const double v110 = V::get(r11, 0, tab), v111 = V::get(r11, 1, tab);
   const double c00 = v000 * (1 - fx) + v001 * fx;
   const double c10 = v010 * (1 - fx) + v011 * fx;
   const double c01 = v100 * (1 - fx) + v101 * fx;
@@ -1308,7 +1360,20 @@ struct GenPlan {
 };
 
 static int plan_gen(const VdiGenArgs* a, GenPlan& p) {
+#define VDI_GEN_KERNELS(VT)               \
+  p.sample = gen_sample_kernel<VT>;       \
+  p.fill = gen_fill_kernel<VT>;           \
+  p.fused = gen_fused_kernel<VT>;
   switch (a->voxel_type) {
+    case VDI_VOXEL_U8 | VDI_VOXEL_CELLS:
+      VDI_GEN_KERNELS(VDI_VOXEL_U8 | VDI_VOXEL_CELLS)
+      break;
+    case VDI_VOXEL_U16 | VDI_VOXEL_CELLS:
+      VDI_GEN_KERNELS(VDI_VOXEL_U16 | VDI_VOXEL_CELLS)
+      break;
+    case VDI_VOXEL_F32 | VDI_VOXEL_CELLS:
+      VDI_GEN_KERNELS(VDI_VOXEL_F32 | VDI_VOXEL_CELLS)
+      break;
     case VDI_VOXEL_U8:
       p.sample = gen_sample_kernel<VDI_VOXEL_U8>;
       p.fill = gen_fill_kernel<VDI_VOXEL_U8>;

@@ -66,4 +66,142 @@ int brick_max(const void* volume, int voxel_type, int nx, int ny, int nz, int lo
   return VDI_OK;
 }
 
+// Corner records (include/vdi_b200.h vdi_volume_cells): one thread per cell,
+// x fastest, so the 8 corner reads coalesce across a warp (rows x and x+1 of
+// four (y, z) rows) and the record stores are contiguous.
+template <typename T>
+struct CellRecord;
+template <>
+struct CellRecord<uint8_t> {
+  static __device__ __forceinline__ void store(void* out, long long i, const uint8_t v[8]) {
+    uint2 r;
+    r.x = v[0] | (v[1] << 8) | (v[2] << 16) | ((unsigned)v[3] << 24);
+    r.y = v[4] | (v[5] << 8) | (v[6] << 16) | ((unsigned)v[7] << 24);
+    reinterpret_cast<uint2*>(out)[i] = r;
+  }
+};
+template <>
+struct CellRecord<uint16_t> {
+  static __device__ __forceinline__ void store(void* out, long long i, const uint16_t v[8]) {
+    uint4 r;
+    r.x = v[0] | ((unsigned)v[1] << 16);
+    r.y = v[2] | ((unsigned)v[3] << 16);
+    r.z = v[4] | ((unsigned)v[5] << 16);
+    r.w = v[6] | ((unsigned)v[7] << 16);
+    reinterpret_cast<uint4*>(out)[i] = r;
+  }
+};
+template <>
+struct CellRecord<float> {
+  static __device__ __forceinline__ void store(void* out, long long i, const float v[8]) {
+    float4* o = reinterpret_cast<float4*>(out) + 2 * i;
+    o[0] = make_float4(v[0], v[1], v[2], v[3]);
+    o[1] = make_float4(v[4], v[5], v[6], v[7]);
+  }
+};
+
+template <typename T>
+__global__ void cells_kernel(const T* __restrict__ vol, void* __restrict__ out, int nx, int ny,
+                             int nz) {
+  const long long n = (long long)nx * ny * nz;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int x = (int)(i % nx);
+    const long long yz = i / nx;
+    const int y = (int)(yz % ny), z = (int)(yz / ny);
+    const int dx = x + 1 < nx ? 1 : 0;
+    const long long dy = y + 1 < ny ? nx : 0;
+    const long long dz = z + 1 < nz ? (long long)nx * ny : 0;
+    const T* p = vol + i;
+    T v[8];
+    v[0] = __ldg(p);
+    v[1] = __ldg(p + dx);
+    v[2] = __ldg(p + dy);
+    v[3] = __ldg(p + dy + dx);
+    v[4] = __ldg(p + dz);
+    v[5] = __ldg(p + dz + dx);
+    v[6] = __ldg(p + dz + dy);
+    v[7] = __ldg(p + dz + dy + dx);
+    CellRecord<T>::store(out, i, v);
+  }
+}
+
+// u8 fast path (nx % 4 == 0): a thread builds the records of 4 cells along x
+// from one aligned 32-bit word plus the next byte of each of the 4 (y, z)
+// rows, and stores them as two 16-byte writes.
+__global__ void cells_u8x4_kernel(const uint8_t* __restrict__ vol, uint4* __restrict__ out,
+                                  int nx, int ny, int nz) {
+  const int qx = nx >> 2;
+  const long long n = (long long)qx * ny * nz;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int x = (int)(i % qx) * 4;
+    const long long yz = i / qx;
+    const int y = (int)(yz % ny), z = (int)(yz / ny);
+    const long long base = yz * nx + x;
+    const long long dy = y + 1 < ny ? nx : 0;
+    const long long dz = z + 1 < nz ? (long long)nx * ny : 0;
+    const bool last = x + 4 >= nx;
+    unsigned w[4], e[4];  // rows (y,z), (y+1,z), (y,z+1), (y+1,z+1)
+    const long long off[4] = {0, dy, dz, dy + dz};
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      w[r] = __ldg(reinterpret_cast<const unsigned*>(vol + base + off[r]));
+      // voxel x+4 (clamped to x+3 at the row end: the last cell repeats it)
+      e[r] = last ? (w[r] >> 24) : (unsigned)__ldg(vol + base + off[r] + 4);
+    }
+    unsigned rec[8];  // cell j: rec[2j] = (v000 v001 v010 v011), rec[2j+1] = z+1 row pair
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      // bytes j and j+1 of each row (byte 4 = e[r])
+      unsigned p[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const unsigned lo = (w[r] >> (8 * j)) & 0xffu;
+        const unsigned hi = j < 3 ? (w[r] >> (8 * (j + 1))) & 0xffu : e[r];
+        p[r] = lo | (hi << 8);
+      }
+      rec[2 * j] = p[0] | (p[1] << 16);
+      rec[2 * j + 1] = p[2] | (p[3] << 16);
+    }
+    uint4* o = out + 2 * i;
+    o[0] = make_uint4(rec[0], rec[1], rec[2], rec[3]);
+    o[1] = make_uint4(rec[4], rec[5], rec[6], rec[7]);
+  }
+}
+
+int volume_cells(const void* volume, int voxel_type, int nx, int ny, int nz, void* out,
+                 cudaStream_t stream) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const long long n = (long long)nx * ny * nz;
+  long long blocks = (n + 255) / 256;
+  if (blocks > (long long)sms * 64) blocks = (long long)sms * 64;
+  switch (voxel_type) {
+    case VDI_VOXEL_U8:
+      if (nx % 4 == 0)
+        cells_u8x4_kernel<<<(unsigned)((blocks + 3) / 4), 256, 0, stream>>>(
+            static_cast<const uint8_t*>(volume), static_cast<uint4*>(out), nx, ny, nz);
+      else
+        cells_kernel<<<(unsigned)blocks, 256, 0, stream>>>(static_cast<const uint8_t*>(volume),
+                                                           out, nx, ny, nz);
+      break;
+    case VDI_VOXEL_U16:
+      cells_kernel<<<(unsigned)blocks, 256, 0, stream>>>(static_cast<const uint16_t*>(volume),
+                                                         out, nx, ny, nz);
+      break;
+    case VDI_VOXEL_F32:
+      cells_kernel<<<(unsigned)blocks, 256, 0, stream>>>(static_cast<const float*>(volume), out,
+                                                         nx, ny, nz);
+      break;
+    default:
+      return set_error(VDI_EINVAL, "bad voxel_type %d", voxel_type);
+  }
+  const cudaError_t err = cudaGetLastError();
+  if (err != cudaSuccess)
+    return set_error(VDI_ELAUNCH, "volume_cells launch: %s", cudaGetErrorString(err));
+  return VDI_OK;
+}
+
 }  // namespace vdi

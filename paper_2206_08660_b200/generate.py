@@ -101,11 +101,12 @@ def alloc_gen(width, rows, n_sg, grid_dims, stats=True):
 
 def gen_args(vol_dev, voxel_type, dims, lut_dev, cam, aabb, params_resolved, n_sg, eps,
              gamma_init, bufs: GenBuffers, band=(16, 1, 0), bricks=None,
-             ess_max=-1.0) -> _capi.VdiGenArgs:
+             ess_max=-1.0, cells=None) -> _capi.VdiGenArgs:
     delta, step, lref = params_resolved
     width, height = cam.viewport
     a = _capi.VdiGenArgs()
-    a.volume, a.lut = dv.ptr(vol_dev), dv.ptr(lut_dev)
+    a.volume = dv.ptr(cells if cells is not None else vol_dev)
+    a.lut = dv.ptr(lut_dev)
     a.brick_max = dv.ptr(bricks)
     a.ess_max = float(ess_max) if bricks is not None else -1.0
     a.brick_log2 = dv.BRICK_LOG2
@@ -116,7 +117,7 @@ def gen_args(vol_dev, voxel_type, dims, lut_dev, cam, aabb, params_resolved, n_s
     _capi.fill(a.eye, np.asarray(cam.position, dtype=np.float64))
     _capi.fill(a.aabb, np.asarray(aabb, dtype=np.float64).reshape(6))
     a.eps, a.gamma_init, a.step, a.lref = float(eps), float(gamma_init), float(step), float(lref)
-    a.voxel_type = _capi.VOXEL[voxel_type]
+    a.voxel_type = _capi.VOXEL[voxel_type] | (_capi.VOXEL_CELLS if cells is not None else 0)
     a.nx, a.ny, a.nz = (int(v) for v in dims)
     a.lut_n = int(lut_dev.shape[0])
     a.width, a.height = int(width), int(height)
@@ -140,15 +141,17 @@ def grid_args(bufs: GenBuffers, cam, width, height, n_sg, grid_dims, band=(16, 1
 
 def launch_generate(vol_dev, voxel_type, dims, lut_dev, cam, aabb, params, resolved,
                     bufs: GenBuffers, grid_dims, band=(16, 1, 0), stream=None,
-                    split_events=None, workspace_bytes=None, bricks=None, ess_max=-1.0):
+                    split_events=None, workspace_bytes=None, bricks=None, ess_max=-1.0,
+                    cells=None):
     """Enqueue generation + grid on the current stream (no sync, no alloc).
     split_events: optional CUDA events; [1] and [2] bracket the generation
     kernel (timing only). workspace_bytes overrides the recommended scratch
-    size ("min" = the smallest accepted, which forces deferral rounds)."""
+    size ("min" = the smallest accepted, which forces deferral rounds).
+    cells: vdi_volume_cells() records of vol_dev to sample from (or None)."""
     L = _capi.load()
     s = dv.stream_handle() if stream is None else stream
     a = gen_args(vol_dev, voxel_type, dims, lut_dev, cam, aabb, resolved, params.n_sg,
-                 params.epsilon, params.gamma_init, bufs, band, bricks, ess_max)
+                 params.epsilon, params.gamma_init, bufs, band, bricks, ess_max, cells)
     if workspace_bytes == "min":
         need = int(L.vdi_gen_workspace_min_bytes(a))
     elif workspace_bytes is not None:
@@ -186,8 +189,9 @@ def generate_vdi(vol, tf, cam, params: GenParams | None = None, grid_dims=None,
     lut_dev = dv.upload_lut(tf.lut)
     bufs = alloc_gen(width, height, params.n_sg, grid_dims, stats=with_stats)
     bricks = dv.volume_bricks(vol_dev, vt, vol.dims)
+    cells = dv.volume_cells(vol_dev, vt, vol.dims) if dv.use_cells(vt, vol.dims) else None
     launch_generate(vol_dev, vt, vol.dims, lut_dev, cam, aabb, params, resolved, bufs,
-                    grid_dims, bricks=bricks, ess_max=dv.ess_threshold(tf.lut))
+                    grid_dims, bricks=bricks, ess_max=dv.ess_threshold(tf.lut), cells=cells)
     dev = DeviceVdi(counts=bufs.counts, segs=bufs.segs)
     vdi = Vdi(width=width, height=height, n_sg=params.n_sg, counts=None, segs=None,
               gen_camera=cam, volume_aabb=aabb, _device=dev)

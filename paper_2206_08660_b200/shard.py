@@ -88,7 +88,11 @@ class Pipeline:
         self.grid_dims = default_grid_dims(w, h)
         self.vol_dev, self.vt = dv.upload_volume(vol)
         self.lut_dev = dv.upload_lut(tf.lut)
-        self.bricks = dv.volume_bricks(self.vol_dev, self.vt, vol.dims)
+        # per-volume acceleration data, rebuilt from the volume inside every
+        # step (a new timestep's volume needs new ones): brick maxima for
+        # empty-space skipping and, when they fit, the corner records
+        self.bricks = dv.alloc_bricks(self.vol_dev, vol.dims)
+        self.cells = dv.alloc_cells(self.vt, vol.dims) if dv.use_cells(self.vt, vol.dims) else None
         self.ess_max = dv.ess_threshold(tf.lut)
         self.aabb = np.asarray(vol.aabb, np.float64)
         self.band = (BAND_ROWS, world, rank)
@@ -102,9 +106,10 @@ class Pipeline:
         self.local_render_pixels = local_rows(oh, world, rank) * ow
         self.image = t.zeros((self.out_rows, ow, 4), dtype=t.float64, device="cuda")
         self.sums = t.zeros(3, dtype=t.int64, device="cuda")
-        # vdi_gen_launch = fill_inv + 3 rounds x (sample, bisect, emit) + fused
-        # fallback; then vdi_grid_launch and vdi_render_launch
-        self.launches_per_step = 1 + 3 * 3 + 1 + 1 + 1
+        # brick maxima (+ corner records); vdi_gen_launch = fill_inv + 3 rounds
+        # x (sample, fill, bisect, emit) + fused fallback; then
+        # vdi_grid_launch and vdi_render_launch
+        self.launches_per_step = (1 + (self.cells is not None) + 1 + 3 * 4 + 1 + 1 + 1)
         if world > 1:
             import torch.distributed as tdist
             self.dist = tdist
@@ -128,10 +133,13 @@ class Pipeline:
         if timed:
             ev[0].record()
         self.sums.zero_()
+        dv.launch_bricks(self.vol_dev, self.vt, self.vol.dims, self.bricks)
+        if self.cells is not None:
+            dv.launch_cells(self.vol_dev, self.vt, self.vol.dims, self.cells)
         launch_generate(self.vol_dev, self.vt, self.vol.dims, self.lut_dev, self.gcam,
                         self.aabb, self.params, self.resolved, self.bufs, self.grid_dims,
                         band=self.band, split_events=ev, bricks=self.bricks,
-                        ess_max=self.ess_max)
+                        ess_max=self.ess_max, cells=self.cells)
         if timed:
             ev[3].record()
         if self.world > 1:
@@ -149,7 +157,8 @@ class Pipeline:
         end = t.cuda.Event(enable_timing=True)
         end.record()
         end.synchronize()
-        return {"step": ev[0].elapsed_time(end), "gen": ev[1].elapsed_time(ev[2]),
+        return {"step": ev[0].elapsed_time(end), "prep": ev[0].elapsed_time(ev[1]),
+                "gen": ev[1].elapsed_time(ev[2]),
                 "grid": ev[2].elapsed_time(ev[3]),
                 "collective": ev[3].elapsed_time(ev[4]) + ev[5].elapsed_time(end),
                 "render": ev[4].elapsed_time(ev[5])}
@@ -195,7 +204,6 @@ class Pipeline:
                 d2h = c.nbytes + s.nbytes + g.nbytes + img.data.nbytes
             else:
                 self.vol_dev = dv.to_device(host)
-                self.bricks = dv.volume_bricks(self.vol_dev, self.vt, vol.dims)
                 self.step()
                 n_sg = self.params.n_sg
                 aos = t.empty((self.gen_rows * self.w, n_sg * 6), dtype=t.float32,
@@ -217,7 +225,6 @@ class Pipeline:
             self.dist.all_reduce(x, op=self.dist.ReduceOp.MAX)
             dt = float(x.item())
         self.vol_dev, _ = dv.upload_volume(self.vol)
-        self.bricks = dv.volume_bricks(self.vol_dev, self.vt, self.vol.dims)
         return {"value": 2 * self.w * self.h / dt / 1e6, "unit": "Mrays/s",
                 "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                 "ms_per_step": dt * 1e3, "steps": steps}
