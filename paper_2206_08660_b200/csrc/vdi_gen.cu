@@ -987,8 +987,14 @@ __device__ __forceinline__ void count_sample(CountState& q, double sr, double sg
   }
 }
 
+// kMode: how a lane streams its cache row -- 0 EntryPipe (register shift),
+// 1 EntryRing (two slots, parity select), 2 A/B: the sample loop unrolled by
+// two with static slot roles (step A reads only b0, step B only b1), so the
+// load of an entry has a full A+B iteration to land and no instruction reads
+// a slot whose load is in flight (scoreboards are per warp: EntryRing's
+// select reads both slots and waits for both).
 template <int kLevels, int kDepth, int kPF, int kMinB = 1, int kThreads = kGenThreads,
-          int kAhead = 16, bool kRing = false>
+          int kAhead = 16, int kMode = 0>
 __global__ void __launch_bounds__(kThreads, kMinB) gen_bisect_kernel(const GenConst c) {
   constexpr int kG = (1 << kLevels) - 1;
   extern __shared__ double g_s_inv[];
@@ -1008,8 +1014,9 @@ __global__ void __launch_bounds__(kThreads, kMinB) gen_bisect_kernel(const GenCo
   const float4* cache = nullptr;
   RayRec* rec = nullptr;
   int stored = 0, k = 0;
-  typename std::conditional<kRing, EntryRing<kPF, kAhead>, EntryPipe<kDepth, kPF, kAhead>>::type
-      pipe;
+  typename std::conditional<kMode == 1, EntryRing<kPF, kAhead>,
+                            EntryPipe<kDepth, kPF, kAhead>>::type pipe;
+  float4 b0, b1;  // kMode 2: entries k and k+1 at the top of the unrolled loop
   // bisection state (generate.py:230-236)
   double low = 0.0, high = 0.0;
   int last_n = 0, high_n = 0, passes = 0, samples = 0;
@@ -1079,11 +1086,110 @@ __global__ void __launch_bounds__(kThreads, kMinB) gen_bisect_kernel(const GenCo
         count_reset(q[i], gam[i]);
       }
       k = 0;
-      pipe.start(cache, 0, stored);
+      if (kMode == 2) {
+        ld_pred(b0, cache, 0 < stored);
+        ld_pred(b1, cache + 1, 1 < stored);
+        if (kPF) prefetch_l1(cache + 8);
+      } else {
+        pipe.start(cache, 0, stored);
+      }
     }
 
     bool resolved = false;
-    for (int it = 0; it < 16 && !resolved; ++it) {
+    // one sample (or a transparent run) for all kG count states; returns the
+    // entries consumed
+    auto consume = [&](const float4 e) -> int {
+      int run = 1;
+      if (e.w <= 0.0f) {
+        run = __float_as_int(e.x);
+        if (run < 1) run = 1;
+        if (run > stored - k) run = stored - k;
+#pragma unroll
+        for (int i = 0; i < kG; ++i)
+          if (q[i].n < 0 && q[i].active) {
+            q[i].count += 1;  // the transparent sample closes the segment
+            q[i].active = false;
+          }
+      } else {
+        const double a = (double)e.w;
+        double a_adj;
+        if (entry_needs_pow(e)) {
+          const double ta = rec->t0 + (double)k * c.a.step;
+          double tb = ta + c.a.step;
+          if (tb > rec->t1) tb = rec->t1;
+          const double dt = tb - ta;
+          const double ex = c.lref_pow2 ? dt * c.inv_lref : dt / c.a.lref;
+          a_adj = 1.0 - pow(1.0 - a, ex);
+        } else {
+          a_adj = 1.0 - (1.0 - a);
+        }
+        const double sr = (double)fabsf(e.x) * a_adj;
+        const double sg = (double)e.y * a_adj;
+        const double sb = (double)e.z * a_adj;
+#pragma unroll
+        for (int i = 0; i < kG; ++i)
+          count_sample(q[i], sr, sg, sb, k, n_sg, inv_n, c.inv_tab, s_inv);
+      }
+      return run;
+    };
+    auto all_resolved = [&]() {
+      bool r = true;
+#pragma unroll
+      for (int i = 0; i < kG; ++i) r = r && q[i].n >= 0;
+      return r;
+    };
+    auto natural_end = [&]() {
+      // natural end (or the tb <= ta break)
+#pragma unroll
+      for (int i = 0; i < kG; ++i)
+        if (q[i].n < 0) {
+          q[i].n = q[i].count + (q[i].active ? 1 : 0);
+          q[i].kend = stored;
+        }
+    };
+    if (kMode == 2) {
+      for (int it = 0; it < 8; ++it) {
+        if (k >= stored) {
+          natural_end();
+          resolved = true;
+          break;
+        }
+        // step A: b0 = entry k, b1 = entry k + 1
+        int kold = k;
+        k += consume(b0);
+        if (all_resolved()) {
+          resolved = true;
+          break;
+        }
+        if (k != kold + 1) {  // skipped a transparent run: refill both slots
+          ld_pred(b0, cache + k, k < stored);
+          ld_pred(b1, cache + k + 1, k + 1 < stored);
+          if (kPF) prefetch_l1(cache + (k & ~7) + 8);
+          continue;
+        }
+        ld_pred(b0, cache + k + 1, k + 1 < stored);
+        if (kPF && (((kold + kAhead) ^ (k + kAhead)) & ~7) != 0 && k + kAhead < stored)
+          prefetch_l1(cache + k + kAhead);
+        if (k >= stored) continue;
+        // step B: b1 = entry k, b0 = entry k + 1
+        kold = k;
+        k += consume(b1);
+        if (all_resolved()) {
+          resolved = true;
+          break;
+        }
+        if (k != kold + 1) {
+          ld_pred(b0, cache + k, k < stored);
+          ld_pred(b1, cache + k + 1, k + 1 < stored);
+          if (kPF) prefetch_l1(cache + (k & ~7) + 8);
+          continue;
+        }
+        ld_pred(b1, cache + k + 1, k + 1 < stored);
+        if (kPF && (((kold + kAhead) ^ (k + kAhead)) & ~7) != 0 && k + kAhead < stored)
+          prefetch_l1(cache + k + kAhead);
+      }
+    }
+    for (int it = 0; kMode != 2 && it < 16 && !resolved; ++it) {
      if (k >= stored) {
       // natural end (or the tb <= ta break)
 #pragma unroll
@@ -1181,7 +1287,8 @@ __global__ void __launch_bounds__(kThreads, kMinB) gen_bisect_kernel(const GenCo
 // -------------------------------------------------------------- emit phase
 // The deciding pass of every queued ray, replayed with the full
 // _gen_list_pass logic: segments, counts, gammas, passes, samples.
-// kRing: entries through the two-slot EntryRing (next load in flight)
+// kRing: entries k, k + 1 in two register slots read by an A/B-unrolled loop
+// (see gen_bisect_kernel kMode 2); otherwise one load per sample.
 template <bool kRing>
 __global__ void __launch_bounds__(kGenThreads, VDI_EMIT_MINB) gen_emit_kernel(const GenConst c) {
   const int lane = threadIdx.x & 31;
@@ -1193,7 +1300,7 @@ __global__ void __launch_bounds__(kGenThreads, VDI_EMIT_MINB) gen_emit_kernel(co
   int stored = 0;
   double g = 0.0;
   RayState s;
-  EntryRing<1> ring;
+  float4 b0, b1;
 
   while (true) {
     const unsigned need = __ballot_sync(0xffffffffu, !have && !done);
@@ -1224,7 +1331,10 @@ __global__ void __launch_bounds__(kGenThreads, VDI_EMIT_MINB) gen_emit_kernel(co
           // window hit / cached high: a counting pass that R does not count
           // again (kRedo); capped: R's final capped pass (counted)
           start_pass(s, g, r.mode_final == kCapped ? kCapped : kRedo);
-          if (kRing) ring.start(cache, 0, stored);
+          if (kRing) {
+            ld_pred(b0, cache, 0 < stored);
+            ld_pred(b1, cache + 1, 1 < stored);
+          }
           have = true;
         }
       }
@@ -1232,12 +1342,8 @@ __global__ void __launch_bounds__(kGenThreads, VDI_EMIT_MINB) gen_emit_kernel(co
     if (__all_sync(0xffffffffu, done)) break;
     if (!have) continue;
 
-    int ended;
-    if (s.k >= stored) {
-      ended = 0;
-    } else {
-      float4 rgba = kRing ? ring.cur() : cache[s.k];
-      const int kold = s.k;
+    // one cache entry through segment_step: >= 0 when the pass ended
+    auto entry_step = [&](float4 rgba) -> int {
       const double ta = s.t0 + (double)s.k * step;
       double tb = ta + step;
       if (tb > s.t1) tb = s.t1;
@@ -1249,8 +1355,38 @@ __global__ void __launch_bounds__(kGenThreads, VDI_EMIT_MINB) gen_emit_kernel(co
       } else {
         rgba.x = fabsf(rgba.x);  // drop the pow flag
       }
-      ended = segment_step(c, s, rgba, ta, tb, run);
-      if (kRing && ended < 0) ring.advance(cache, kold, s.k, stored);
+      return segment_step(c, s, rgba, ta, tb, run);
+    };
+    int ended = -1;
+    if (!kRing) {
+      ended = s.k >= stored ? 0 : entry_step(cache[s.k]);
+    } else {
+      for (int it = 0; it < 4; ++it) {
+        if (s.k >= stored) {
+          ended = 0;
+          break;
+        }
+        // step A: b0 = entry k, b1 = entry k + 1
+        int kold = s.k;
+        ended = entry_step(b0);
+        if (ended >= 0) break;
+        if (s.k != kold + 1) {
+          ld_pred(b0, cache + s.k, s.k < stored);
+          ld_pred(b1, cache + s.k + 1, s.k + 1 < stored);
+          continue;
+        }
+        ld_pred(b0, cache + s.k + 1, s.k + 1 < stored);
+        // step B: b1 = entry k, b0 = entry k + 1 (s.k < stored: the pass goes on)
+        kold = s.k;
+        ended = entry_step(b1);
+        if (ended >= 0) break;
+        if (s.k != kold + 1) {
+          ld_pred(b0, cache + s.k, s.k < stored);
+          ld_pred(b1, cache + s.k + 1, s.k + 1 < stored);
+          continue;
+        }
+        ld_pred(b1, cache + s.k + 1, s.k + 1 < stored);
+      }
     }
     if (ended >= 0) {
       const int n = ended == 0 ? close_pass(c, s) : ended;
@@ -1408,12 +1544,12 @@ static int plan_gen(const VdiGenArgs* a, GenPlan& p) {
   if (p.per_sm_fill < 1) p.per_sm_fill = 1;
   {
     // VDI_BISECT_VARIANT = "levels,depth,prefetch,minblocks,threads,inv,ahead"
-    // (tuning switch for A/B runs). Default 2,9,1,5,128,4096,16: 2 speculated
-    // levels, the two-slot entry ring, L1 line prefetch 16 entries ahead, 5
+    // (tuning switch for A/B runs). Default 2,8,1,5,128,4096,16: 2 speculated
+    // levels, the A/B-unrolled entry loop, L1 line prefetch 16 entries ahead, 5
     // blocks of 128 per SM (<= 102 registers), 4096 shared 1/n entries.
     // See profiles/ for the variants measured this round.
     const char* env = getenv("VDI_BISECT_VARIANT");
-    int lv = 2, dp = 9, pf = 1, mb = 5, th = 128, inv = 4096, ah = 16;
+    int lv = 2, dp = 8, pf = 1, mb = 5, th = 128, inv = 4096, ah = 16;
     if (env) sscanf(env, "%d,%d,%d,%d,%d,%d,%d", &lv, &dp, &pf, &mb, &th, &inv, &ah);
     const long long key = (((lv * 10LL + dp) * 10 + pf) * 10 + mb) * 10000LL + th * 10LL +
                           (ah == 8 ? 1 : ah == 32 ? 2 : 0);
@@ -1421,11 +1557,15 @@ static int plan_gen(const VdiGenArgs* a, GenPlan& p) {
     switch (key) {
       case 1200 * 10000LL + 1280: p.bisect = gen_bisect_kernel<1, 2, 0>; break;
       case 2225 * 10000LL + 1280: p.bisect = gen_bisect_kernel<2, 2, 1, 5>; break;  // shift pipe
-      case 2914 * 10000LL + 1280: p.bisect = gen_bisect_kernel<2, 2, 1, 4, 128, 16, true>; break;
-      case 2915 * 10000LL + 1282: p.bisect = gen_bisect_kernel<2, 2, 1, 5, 128, 32, true>; break;
-      case 2905 * 10000LL + 1280: p.bisect = gen_bisect_kernel<2, 2, 0, 5, 128, 16, true>; break;
-      default:  // depth "9": the two-slot ring, 5 blocks/SM
-        p.bisect = gen_bisect_kernel<2, 2, 1, 5, 128, 16, true>;
+      case 2914 * 10000LL + 1280: p.bisect = gen_bisect_kernel<2, 2, 1, 4, 128, 16, 1>; break;
+      case 2915 * 10000LL + 1282: p.bisect = gen_bisect_kernel<2, 2, 1, 5, 128, 32, 1>; break;
+      case 2905 * 10000LL + 1280: p.bisect = gen_bisect_kernel<2, 2, 0, 5, 128, 16, 1>; break;
+      case 2915 * 10000LL + 1280:  // depth "9": the two-slot ring, 5 blocks/SM
+        p.bisect = gen_bisect_kernel<2, 2, 1, 5, 128, 16, 1>;
+        break;
+      case 2814 * 10000LL + 1280: p.bisect = gen_bisect_kernel<2, 2, 1, 4, 128, 16, 2>; break;
+      default:  // depth "8": the A/B-unrolled loop, 5 blocks/SM
+        p.bisect = gen_bisect_kernel<2, 2, 1, 5, 128, 16, 2>;
         break;
     }
     p.inv_smem = inv < 0 ? 0 : inv;
