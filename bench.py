@@ -44,7 +44,7 @@ def parse():
     p.add_argument("--cpu-seconds", type=float, default=12.0,
                    help="target CPU time of the bounded cpu_baseline sample")
     p.add_argument("--no-cpu-baseline", action="store_true")
-    p.add_argument("--e2e-steps", type=int, default=3)
+    p.add_argument("--e2e-steps", type=int, default=8)
     return p.parse_args()
 
 
@@ -326,7 +326,8 @@ def run_b200(args):
                        "lists_visited": L, "segs_intersected": K, "lists_searched": Ls}}
 
     # ---- end to end through the public API with host buffers
-    e2e = pipe.e2e(args.e2e_steps)
+    e2e = pipe.e2e_stream(args.e2e_steps)
+    e2e["serial"] = pipe.e2e(min(args.e2e_steps, 3))
 
     line = None
     if rank == 0:

@@ -126,17 +126,21 @@ class Pipeline:
                                   self.grid_dims, gcam.near, gcam.far, rcam, self.opts,
                                   self.image, stat_sums=self.sums, band=self.band)
 
-    def step(self, timed: bool = False):
+    def step(self, timed: bool = False, vol_dev=None):
+        """One frame on the current stream: volume prep, generation, grid,
+        (exchange,) render. vol_dev: the frame's device volume (default: the
+        pipeline's own copy)."""
         t = self.t
+        vol_dev = self.vol_dev if vol_dev is None else vol_dev
         L = _capi.load()
         ev = [t.cuda.Event(enable_timing=True) for _ in range(6)] if timed else None
         if timed:
             ev[0].record()
         self.sums.zero_()
-        dv.launch_bricks(self.vol_dev, self.vt, self.vol.dims, self.bricks)
+        dv.launch_bricks(vol_dev, self.vt, self.vol.dims, self.bricks)
         if self.cells is not None:
-            dv.launch_cells(self.vol_dev, self.vt, self.vol.dims, self.cells)
-        launch_generate(self.vol_dev, self.vt, self.vol.dims, self.lut_dev, self.gcam,
+            dv.launch_cells(vol_dev, self.vt, self.vol.dims, self.cells)
+        launch_generate(vol_dev, self.vt, self.vol.dims, self.lut_dev, self.gcam,
                         self.aabb, self.params, self.resolved, self.bufs, self.grid_dims,
                         band=self.band, split_events=ev, bricks=self.bricks,
                         ess_max=self.ess_max, cells=self.cells)
@@ -176,10 +180,46 @@ class Pipeline:
                   _device=self.dvdi)
         return vdi.counts, vdi.segs, dv.to_host(self.bufs.grid).view(np.uint32)
 
+    def e2e_stream(self, steps: int, warmup: int = 2):
+        """End to end through the public FrameStream API: every frame uploads
+        its volume from pinned host memory and reads its results (counts, AoS
+        segs, AccelGrid, image) back to pinned host memory, overlapped with
+        the neighbouring frames' kernels (stream.py). Time per frame over
+        `steps` frames after `warmup` frames, max over ranks."""
+        from .stream import FrameStream
+        t = self.t
+        host = dv.pinned_numpy(self.vol.data.shape, self.vol.data.dtype)
+        host[...] = self.vol.data
+        fs = FrameStream(self)
+        fs.run([host] * warmup)
+        t.cuda.synchronize()
+        if self.world > 1:
+            self.dist.barrier()
+        t0 = time.perf_counter()
+        fs.run([host] * steps)
+        t.cuda.synchronize()
+        dt = (time.perf_counter() - t0) / steps
+        if self.world > 1:
+            x = t.tensor([dt], dtype=t.float64, device="cuda")
+            self.dist.all_reduce(x, op=self.dist.ReduceOp.MAX)
+            dt = float(x.item())
+        del fs
+        return {"value": 2 * self.w * self.h / dt / 1e6, "unit": "Mrays/s",
+                "h2d_bytes_per_step": int(fs_h2d(host, self.tf)),
+                "d2h_bytes_per_step": int(self._d2h_bytes()),
+                "ms_per_step": dt * 1e3, "steps": steps,
+                "mode": "FrameStream: H2D(i+1) | kernels(i) | D2H(i-1) overlapped"}
+
+    def _d2h_bytes(self) -> int:
+        n_sg = self.params.n_sg
+        return (self.gen_rows * self.w * (4 + 24 * n_sg) + self.bufs.grid.numel() * 4
+                + self.image.numel() * 8)
+
     def e2e(self, steps: int):
-        """End to end through host buffers: pinned volume H2D every step, the
-        public generate_vdi / render_vdi (N=1) or the sharded pipeline (N>1),
-        and the step's results read back to pinned host memory."""
+        """End to end through host buffers, one frame at a time: pinned volume
+        H2D every step, the public generate_vdi / render_vdi (N=1) or the
+        sharded pipeline (N>1), and the step's results read back to pinned
+        host memory."""
         t = self.t
         vol = self.vol
         host = dv.pinned_numpy(vol.data.shape, vol.data.dtype)
@@ -228,6 +268,11 @@ class Pipeline:
         return {"value": 2 * self.w * self.h / dt / 1e6, "unit": "Mrays/s",
                 "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                 "ms_per_step": dt * 1e3, "steps": steps}
+
+
+def fs_h2d(host, tf) -> int:
+    """Input bytes a frame uploads: the volume (the LUT is uploaded once)."""
+    return host.nbytes
 
 
 def unshard_image(g_image, out_h: int, world: int):

@@ -1,0 +1,53 @@
+"""FrameStream (overlapped H2D / kernels / D2H over a stream of volumes) gives,
+frame by frame, exactly what the one-frame public API gives for that frame's
+volume -- with alternating volumes, so a slot mix-up cannot go unnoticed."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2206_08660_b200 as vb  # noqa: E402
+from paper_2206_08660_b200 import device as dv  # noqa: E402
+from paper_2206_08660_b200 import shard, synth  # noqa: E402
+from paper_2206_08660_b200.stream import FrameStream  # noqa: E402
+from paper_2206_08660_b200.volume import make_volume  # noqa: E402
+
+
+@pytest.mark.parametrize("name", ["C1", "C2"])
+def test_stream_frames_match_single_frame_api(name):
+    vol, tf, gcam, rcam, n_sg = synth.config(name)
+    other = make_volume(np.ascontiguousarray(vol.data[::-1]), vol.voxel_type)  # same dims
+    params = vb.GenParams(n_sg=n_sg)
+    refs = []
+    for v in (vol, other):
+        vdi, grid = vb.generate_vdi(v, tf, gcam, params)
+        img = vb.render_vdi(vdi, grid, rcam)
+        refs.append((vdi.counts, vdi.segs, grid.counts, img.data))
+    pipe = shard.Pipeline(vol, tf, gcam, rcam, params)
+    fs = FrameStream(pipe)
+    hosts = []
+    for v in (vol, other):
+        h = dv.pinned_numpy(v.data.shape, v.data.dtype)
+        h[...] = v.data
+        hosts.append(h)
+    order = [0, 1, 0, 1, 1, 0]
+    seen = []
+
+    def check(r):
+        c, s, g, im = refs[order[r.index]]
+        h, w = c.shape
+        assert np.array_equal(r.counts[:h], c)
+        assert np.array_equal(r.segs[:h], s)
+        assert np.array_equal(r.grid, g)
+        oh = im.shape[0]
+        assert np.array_equal(r.image[:oh], im)
+        seen.append(r.index)
+
+    n = fs.run([hosts[i] for i in order], on_result=check)
+    assert n == len(order) and seen == list(range(len(order)))
+    assert fs.h2d_bytes == vol.data.nbytes and fs.d2h_bytes > 0
