@@ -20,6 +20,7 @@ _LAZY = {
     "find_first_supersegment": "raycast",
     "Vdi": "vdi", "AccelGrid": "vdi", "default_grid_dims": "vdi",
     "validate_vdi": "vdi",
+    "FrameStream": "stream", "FrameResult": "stream",
 }
 
 

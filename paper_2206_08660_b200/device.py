@@ -159,11 +159,14 @@ def cells_bytes(voxel_type: str, dims) -> int:
 def use_cells(voxel_type: str, dims) -> bool:
     """Whether generation samples from corner records (vdi_volume_cells): 8x
     the volume's bytes in exchange for one load per sample instead of 8
-    gathers. VDI_CELLS=0/1 forces it; by default it is used while the records
-    fit in a quarter of the device's memory."""
+    gathers. VDI_CELLS=0/1 forces it. By default only u8 volumes use them
+    (C3: build 1.8 ms, generation -2.5 ms; for f32, C4: build 9.6 ms for
+    -3 ms), and only while the records fit in a quarter of device memory."""
     env = os.environ.get("VDI_CELLS")
     if env is not None:
         return env not in ("0", "", "false")
+    if voxel_type != "u8":
+        return False
     total = torch().cuda.get_device_properties(torch().cuda.current_device()).total_memory
     return cells_bytes(voxel_type, dims) <= total // 4
 
