@@ -14,6 +14,8 @@
  *   vdi_render_launch  replaces raycast.py:275-456   _render_kernel
  *                      (with _find_first raycast.py:79-141, _bins raycast.py:51-62)
  *   vdi_find_first_batch  batch form of raycast.py:144-156 find_first_supersegment
+ *   vdi_dvr_launch     replaces dvr.py:21-89      _dvr_kernel (render_dvr's
+ *                      ground-truth emission-absorption raycast)
  *   vdi_segs_to_aos / vdi_segs_from_aos  device layout <-> the reference's
  *                      (H, W, n_sg, 6) f32 array (vdi.py:3-7, 23-24)
  *
@@ -150,6 +152,35 @@ typedef struct VdiRenderArgs {
   int32_t band_rows, band_stride, band_offset;  /* output-row sharding */
 } VdiRenderArgs;
 
+/* Ground-truth direct volume rendering (dvr.py:21-89): the generation ray,
+ * clip and sampler, composited front to back with early termination.
+ * Outputs are indexed by local row (band map). */
+typedef struct VdiDvrArgs {
+  const void* volume;           /* as VdiGenArgs.volume (VDI_VOXEL_CELLS allowed) */
+  const float* lut;             /* (lut_n, 4) f32 */
+  const void* brick_max;        /* vdi_volume_brick_max() of the volume, or NULL */
+  double* image;                /* OUT (local_h, width, 4) f64 premultiplied, 16 B aligned */
+  int32_t* samples;             /* OUT executed samples per pixel, may be NULL */
+  unsigned long long* stat_sums;/* OUT [1] += executed samples, may be NULL */
+  void* workspace;              /* >= VDI_DVR_WORKSPACE_BYTES device bytes, any content */
+  double pv[16];
+  double inv_pv[16];
+  double eye[3];
+  double aabb[6];
+  double bg[4];                 /* straight RGBA background */
+  double step, lref;            /* render_dvr step / ref_step (resolved) */
+  double early_term;            /* early_term_alpha */
+  double ess_max;               /* as VdiGenArgs.ess_max */
+  int32_t voxel_type;
+  int32_t nx, ny, nz;
+  int32_t lut_n;
+  int32_t width, height;
+  int32_t band_rows, band_stride, band_offset;
+  int32_t brick_log2;
+} VdiDvrArgs;
+
+#define VDI_DVR_WORKSPACE_BYTES 256
+
 const char* vdi_last_error(void);
 int vdi_abi_version(void);
 
@@ -159,6 +190,7 @@ size_t vdi_gen_workspace_min_bytes(const VdiGenArgs* args);
 int vdi_gen_launch(const VdiGenArgs* args, vdi_stream_t stream);
 int vdi_grid_launch(const VdiGridArgs* args, vdi_stream_t stream);
 int vdi_render_launch(const VdiRenderArgs* args, vdi_stream_t stream);
+int vdi_dvr_launch(const VdiDvrArgs* args, vdi_stream_t stream);
 
 /* Alg. 2 search over a batch of independent queries (raycast.py:79-156).
  * fronts/backs: (n_queries, n_max) f32, counts: (n_queries,), d_entry /

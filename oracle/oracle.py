@@ -59,6 +59,9 @@ def lib():
                                       ctypes.c_int64,
                                       ctypes.POINTER(ctypes.c_int64)]
         L.vdio_find_first.restype = ctypes.c_int64
+        L.vdio_dvr.argtypes = [
+            _f32, _int, _int, _int, _f32, _int, _f64, _f64, _f64, _f64,
+            _int, _int, _dbl, _dbl, _dbl, _f64, _vp, _int, _int, _f64, _vp]
         L.vdio_max_threads.restype = _int
         _lib = L
     return _lib
@@ -149,3 +152,20 @@ def find_first(fronts, backs, count, d_entry, d_exit, p):
     idx = lib().vdio_find_first(fr, bk, int(count), float(d_entry),
                                 float(d_exit), int(p), ctypes.byref(seed))
     return int(idx), int(seed.value)
+
+
+def dvr(vol_norm, lut, pv, inv_pv, eye, aabb, width, height, step, lref,
+        early_term=0.999, bg=(0.0, 0.0, 0.0, 1.0), rows=None, threads=0,
+        with_samples=False):
+    """_dvr_kernel (dvr.py:21-89): image (h, w, 4) f64 [, executed samples]."""
+    vol = np.ascontiguousarray(vol_norm, dtype=np.float32)
+    nz, ny, nx = vol.shape
+    lut = np.ascontiguousarray(lut, dtype=np.float32)
+    img = np.zeros((height, width, 4), np.float64)
+    smp = np.zeros((height, width), np.int64) if with_samples else None
+    rp, nr, _keep = _rows(rows)
+    lib().vdio_dvr(vol, nx, ny, nz, lut, lut.shape[0], _m(pv), _m(inv_pv), _m(eye),
+                   _m(aabb), width, height, float(step), float(lref), float(early_term),
+                   _m(bg), rp, nr, threads, img,
+                   None if smp is None else smp.ctypes.data_as(ctypes.c_void_p))
+    return (img, smp) if with_samples else img

@@ -772,6 +772,83 @@ int vdio_render(const float* segs, const int32_t* counts, int vdi_w, int vdi_h,
   return 0;
 }
 
+/* ------------------------------------------------------------------- DVR */
+
+/* One pixel of dvr.py:21-89 _dvr_kernel: the generation ray and sampler
+ * (same clip, midpoint sample, opacity length normalisation), composited
+ * front to back with early termination. */
+static void dvr_pixel(const float* vol, int nx, int ny, int nz, const float* lut,
+                      int lut_n, const double* pv, const double* inv_pv,
+                      const double* eye, const double* bb, int width, int height,
+                      double step, double lref, double early_term, const double* bg,
+                      int64_t idx, double* img, int64_t* samples) {
+  const int row = (int)(idx / width), col = (int)(idx % width);
+  const double ex = bb[3] - bb[0], ey = bb[4] - bb[1], ez = bb[5] - bb[2];
+  double d[3];
+  pixel_ray(inv_pv, eye, col, row, width, height, d); /* dvr.py:28-40 */
+  double acc_r = 0.0, acc_g = 0.0, acc_b = 0.0, acc_a = 0.0;
+  int64_t nexec = 0;
+  double ta, tb, fa, fb;
+  if (clip_aabb(eye[0], eye[1], eye[2], d[0], d[1], d[2], bb, &ta, &tb) &&
+      clip_frustum(pv, eye[0], eye[1], eye[2], d[0], d[1], d[2], &fa, &fb)) {
+    const double t0 = dmax(dmax(ta, fa), 0.0), t1 = dmin(tb, fb); /* 47-48 */
+    if (t1 > t0) {
+      const int64_t nsteps = (int64_t)ceil((t1 - t0) / step);
+      for (int64_t k = 0; k < nsteps; ++k) { /* dvr.py:51-83 */
+        const double sa = t0 + (double)k * step;
+        double sb = sa + step;
+        if (sb > t1) sb = t1;
+        if (sb <= sa) break;
+        ++nexec;
+        const double tm = 0.5 * (sa + sb);
+        double qx = (eye[0] + tm * d[0] - bb[0]) / ex;
+        double qy = (eye[1] + tm * d[1] - bb[1]) / ey;
+        double qz = (eye[2] + tm * d[2] - bb[2]) / ez;
+        qx = dmin(dmax(qx, 0.0), 1.0);
+        qy = dmin(dmax(qy, 0.0), 1.0);
+        qz = dmin(dmax(qz, 0.0), 1.0);
+        float rgba[4];
+        lut_classify(lut, lut_n, trilinear(vol, nx, ny, nz, qx, qy, qz), rgba);
+        const double a = (double)rgba[3];
+        if (a <= 0.0) continue;
+        const double a_adj = 1.0 - pow(1.0 - a, (sb - sa) / lref);
+        const double w = 1.0 - acc_a;
+        acc_r += w * (double)rgba[0] * a_adj;
+        acc_g += w * (double)rgba[1] * a_adj;
+        acc_b += w * (double)rgba[2] * a_adj;
+        acc_a += w * a_adj;
+        if (acc_a >= early_term) break;
+      }
+    }
+  }
+  const double w = 1.0 - acc_a; /* dvr.py:84-89 */
+  double* o = img + idx * 4;
+  o[0] = acc_r + w * bg[0] * bg[3];
+  o[1] = acc_g + w * bg[1] * bg[3];
+  o[2] = acc_b + w * bg[2] * bg[3];
+  o[3] = acc_a + w * bg[3];
+  if (samples) samples[idx] = nexec;
+}
+
+/* dvr.py:21-89 over all pixels, or only over the listed rows. */
+int vdio_dvr(const float* vol, int nx, int ny, int nz, const float* lut, int lut_n,
+             const double* pv, const double* inv_pv, const double* eye,
+             const double* bb, int width, int height, double step, double lref,
+             double early_term, const double* bg, const int32_t* rows, int n_rows,
+             int nthreads, double* img, int64_t* samples) {
+  int64_t total = rows ? (int64_t)n_rows * width : (int64_t)width * height;
+#ifdef _OPENMP
+  if (nthreads > 0) omp_set_num_threads(nthreads);
+#endif
+#pragma omp parallel for schedule(dynamic, 64)
+  for (int64_t j = 0; j < total; ++j) {
+    int64_t idx = rows ? (int64_t)rows[j / width] * width + j % width : j;
+    dvr_pixel(vol, nx, ny, nz, lut, lut_n, pv, inv_pv, eye, bb, width, height, step,
+              lref, early_term, bg, idx, img, samples);
+  }
+  return 0;
+}
+
 int vdio_max_threads(void) {
 #ifdef _OPENMP
   return omp_get_max_threads();

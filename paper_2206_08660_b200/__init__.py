@@ -21,6 +21,7 @@ _LAZY = {
     "Vdi": "vdi", "AccelGrid": "vdi", "default_grid_dims": "vdi",
     "validate_vdi": "vdi",
     "FrameStream": "stream", "FrameResult": "stream",
+    "render_dvr": "dvr",
 }
 
 

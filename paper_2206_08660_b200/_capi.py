@@ -55,9 +55,23 @@ class VdiRenderArgs(ctypes.Structure):
     ]
 
 
+class VdiDvrArgs(ctypes.Structure):
+    _fields_ = [
+        ("volume", _P), ("lut", _P), ("brick_max", _P), ("image", _P), ("samples", _P),
+        ("stat_sums", _P), ("workspace", _P),
+        ("pv", _D * 16), ("inv_pv", _D * 16), ("eye", _D * 3), ("aabb", _D * 6), ("bg", _D * 4),
+        ("step", _D), ("lref", _D), ("early_term", _D), ("ess_max", _D),
+        ("voxel_type", _I), ("nx", _I), ("ny", _I), ("nz", _I), ("lut_n", _I),
+        ("width", _I), ("height", _I), ("band_rows", _I), ("band_stride", _I),
+        ("band_offset", _I), ("brick_log2", _I),
+    ]
+
+
+DVR_WORKSPACE_BYTES = 256
+
 EXPORTS = ["vdi_last_error", "vdi_abi_version", "vdi_gen_workspace_bytes",
            "vdi_gen_workspace_min_bytes", "vdi_gen_launch",
-           "vdi_grid_launch", "vdi_render_launch", "vdi_find_first_batch",
+           "vdi_grid_launch", "vdi_render_launch", "vdi_dvr_launch", "vdi_find_first_batch",
            "vdi_volume_brick_max", "vdi_selftest_arith", "vdi_segs_to_aos",
            "vdi_segs_from_aos", "vdi_volume_cells_bytes", "vdi_volume_cells"]
 
@@ -86,6 +100,7 @@ def load():
     L.vdi_gen_launch.argtypes = [ctypes.POINTER(VdiGenArgs), _P]
     L.vdi_grid_launch.argtypes = [ctypes.POINTER(VdiGridArgs), _P]
     L.vdi_render_launch.argtypes = [ctypes.POINTER(VdiRenderArgs), _P]
+    L.vdi_dvr_launch.argtypes = [ctypes.POINTER(VdiDvrArgs), _P]
     L.vdi_find_first_batch.argtypes = [_P, _P, _P, _I, _P, _P, _P, _P, _P, ctypes.c_int64, _P]
     L.vdi_volume_brick_max.argtypes = [_P, _I, _I, _I, _I, _I, _P, _P]
     L.vdi_volume_brick_max.restype = ctypes.c_int
@@ -97,7 +112,7 @@ def load():
     L.vdi_selftest_arith.restype = ctypes.c_int
     L.vdi_segs_to_aos.argtypes = [_P, _P, ctypes.c_int64, _I, _P]
     L.vdi_segs_from_aos.argtypes = [_P, _P, ctypes.c_int64, _I, _P]
-    for name in ("vdi_gen_launch", "vdi_grid_launch", "vdi_render_launch",
+    for name in ("vdi_gen_launch", "vdi_grid_launch", "vdi_render_launch", "vdi_dvr_launch", "vdi_dvr_launch",
                  "vdi_find_first_batch", "vdi_segs_to_aos", "vdi_segs_from_aos"):
         getattr(L, name).restype = ctypes.c_int
     if L.vdi_abi_version() != 1:

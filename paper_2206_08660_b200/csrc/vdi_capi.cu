@@ -77,6 +77,22 @@ int vdi_render_launch(const VdiRenderArgs* a, vdi_stream_t stream) {
   return vdi::render_launch(a, static_cast<cudaStream_t>(stream));
 }
 
+int vdi_dvr_launch(const VdiDvrArgs* a, vdi_stream_t stream) {
+  if (!a) return set_error(VDI_EINVAL, "null args");
+  if (!a->volume || !a->lut || !a->image || !a->workspace)
+    return set_error(VDI_EINVAL, "null device pointer");
+  if (a->nx < 2 || a->ny < 2 || a->nz < 2)
+    return set_error(VDI_EINVAL, "dims components must be >= 2 for trilinear sampling");
+  if (a->lut_n < 2 || a->lut_n > 4096) return set_error(VDI_EINVAL, "lut_n out of range");
+  if (a->width < 1 || a->height < 1) return set_error(VDI_EINVAL, "empty viewport");
+  if (!(a->step > 0) || !(a->lref > 0)) return set_error(VDI_EINVAL, "step must be > 0");
+  if (a->band_stride > 1 && (a->band_offset < 0 || a->band_offset >= a->band_stride))
+    return set_error(VDI_EINVAL, "band_offset out of range");
+  if (reinterpret_cast<uintptr_t>(a->image) % 16 != 0)
+    return set_error(VDI_EINVAL, "image must be 16-byte aligned");
+  return vdi::dvr_launch(a, static_cast<cudaStream_t>(stream));
+}
+
 int vdi_find_first_batch(const float* fronts, const float* backs, const int32_t* counts,
                          int32_t n_max, const double* d_entry, const double* d_exit,
                          const int32_t* seeds, int32_t* out_index, int32_t* out_seed,

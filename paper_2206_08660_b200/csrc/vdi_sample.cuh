@@ -1,0 +1,156 @@
+// vdi_sample.cuh -- the volume sampler shared by generation (vdi_gen.cu) and
+// the direct volume renderer (vdi_dvr.cu): trilinear interpolation
+// (volume.py:180-205 _trilinear) and transfer-function classification
+// (volume.py:164-177 _lut_classify), f64 in the reference's order.
+//
+// trilinear<VT>(c, ...) reads, from any constant block `c`: c.a.volume,
+// c.a.nx/ny/nz, c.a.brick_max, c.a.brick_log2, c.a.ess_max, c.ess, c.bnx,
+// c.bny (the generation and DVR argument blocks share these names).
+#pragma once
+
+#include "vdi_common.cuh"
+
+namespace vdi {
+
+template <int VT>
+struct Voxel;
+template <>
+struct Voxel<VDI_VOXEL_F32> {
+  using type = float;
+  static __device__ __forceinline__ double get(const void* p, long long i, const double*) {
+    return (double)__ldg(reinterpret_cast<const float*>(p) + i);
+  }
+};
+template <>
+struct Voxel<VDI_VOXEL_U8> {
+  using type = unsigned char;
+  // volume.py:48-50 normalises with an f32 division by 255; the 256 exact
+  // quotients live in shared memory, already widened to f64.
+  static __device__ __forceinline__ double get(const void* p, long long i, const double* tab) {
+    return tab[__ldg(reinterpret_cast<const unsigned char*>(p) + i)];
+  }
+};
+template <>
+struct Voxel<VDI_VOXEL_U16> {
+  using type = unsigned short;
+  static __device__ __forceinline__ double get(const void* p, long long i, const double*) {
+    return (double)__fdiv_rn((float)__ldg(reinterpret_cast<const unsigned short*>(p) + i),
+                             65535.0f);
+  }
+};
+
+// Corner records (vdi_volume_cells): the 8 voxels of cell i in one load.
+template <int BT>
+struct Cell;
+template <>
+struct Cell<VDI_VOXEL_U8> {
+  static __device__ __forceinline__ void get(const void* cells, long long i, const double* tab,
+                                             double v[8]) {
+    const uint2 r = __ldg(reinterpret_cast<const uint2*>(cells) + i);
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      v[b] = tab[(r.x >> (8 * b)) & 0xffu];
+      v[4 + b] = tab[(r.y >> (8 * b)) & 0xffu];
+    }
+  }
+};
+template <>
+struct Cell<VDI_VOXEL_U16> {
+  static __device__ __forceinline__ void get(const void* cells, long long i, const double*,
+                                             double v[8]) {
+    const uint4 r = __ldg(reinterpret_cast<const uint4*>(cells) + i);
+    const unsigned w[4] = {r.x, r.y, r.z, r.w};
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      v[2 * b] = (double)__fdiv_rn((float)(w[b] & 0xffffu), 65535.0f);
+      v[2 * b + 1] = (double)__fdiv_rn((float)(w[b] >> 16), 65535.0f);
+    }
+  }
+};
+template <>
+struct Cell<VDI_VOXEL_F32> {
+  static __device__ __forceinline__ void get(const void* cells, long long i, const double*,
+                                             double v[8]) {
+    const float4 a = __ldg(reinterpret_cast<const float4*>(cells) + 2 * i);
+    const float4 b = __ldg(reinterpret_cast<const float4*>(cells) + 2 * i + 1);
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+    v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+  }
+};
+
+// volume.py:180-205 _trilinear. VT is a VDI_VOXEL_* type, optionally with the
+// VDI_VOXEL_CELLS flag (c.a.volume then holds corner records).
+template <int VT, class C>
+__device__ __forceinline__ double trilinear(const C& c, const double* tab, double px,
+                                            double py, double pz) {
+  const int nx = c.a.nx, ny = c.a.ny, nz = c.a.nz;
+  const double gx = px * (double)(nx - 1);
+  const double gy = py * (double)(ny - 1);
+  const double gz = pz * (double)(nz - 1);
+  int ix = (int)gx, iy = (int)gy, iz = (int)gz;
+  if (ix > nx - 2) ix = nx - 2;
+  if (iy > ny - 2) iy = ny - 2;
+  if (iz > nz - 2) iz = nz - 2;
+  if (c.ess) {
+    // Exact empty-space skip: every voxel this sample can read lies in the
+    // brick (+1 halo), whose maximum classifies at or below the last row of
+    // the LUT's leading alpha == 0 run with margin, and a trilinear mix never
+    // exceeds its largest input by more than a few ulps. -1 classifies to LUT
+    // row 0, whose alpha is 0: the sample is transparent, as in the reference.
+    const int lb = c.a.brick_log2;
+    const long long bi = ((long long)(iz >> lb) * c.bny + (iy >> lb)) * c.bnx + (ix >> lb);
+    if (Voxel<(VT & 15)>::get(c.a.brick_max, bi, tab) <= c.a.ess_max) return -1.0;
+  }
+  const double fx = gx - ix, fy = gy - iy, fz = gz - iz;
+  if (VT & VDI_VOXEL_CELLS) {
+    double v[8];
+    Cell<(VT & 15)>::get(c.a.volume, ((long long)iz * ny + iy) * (long long)nx + ix, tab, v);
+    const double c00 = v[0] * (1 - fx) + v[1] * fx;
+    const double c10 = v[2] * (1 - fx) + v[3] * fx;
+    const double c01 = v[4] * (1 - fx) + v[5] * fx;
+    const double c11 = v[6] * (1 - fx) + v[7] * fx;
+    const double c0 = c00 * (1 - fy) + c10 * fy;
+    const double c1 = c01 * (1 - fy) + c11 * fy;
+    return c0 * (1 - fz) + c1 * fz;
+  }
+  // four row pointers, then [ptr + 0/1] gathers (no per-voxel 64-bit math)
+  using T = typename Voxel<(VT & 15)>::type;
+  const T* r00 = static_cast<const T*>(c.a.volume) +
+                 ((long long)iz * ny + iy) * (long long)nx + ix;
+  const T* r01 = r00 + nx;
+  const T* r10 = r00 + (long long)nx * ny;
+  const T* r11 = r10 + nx;
+  using V = Voxel<(VT & 15)>;
+  const double v000 = V::get(r00, 0, tab), v001 = V::get(r00, 1, tab);
+  const double v010 = V::get(r01, 0, tab), v011 = V::get(r01, 1, tab);
+  const double v100 = V::get(r10, 0, tab), v101 = V::get(r10, 1, tab);
+  const double v110 = V::get(r11, 0, tab), v111 = V::get(r11, 1, tab);
+  const double c00 = v000 * (1 - fx) + v001 * fx;
+  const double c10 = v010 * (1 - fx) + v011 * fx;
+  const double c01 = v100 * (1 - fx) + v101 * fx;
+  const double c11 = v110 * (1 - fx) + v111 * fx;
+  const double c0 = c00 * (1 - fy) + c10 * fy;
+  const double c1 = c01 * (1 - fy) + c11 * fy;
+  return c0 * (1 - fz) + c1 * fz;
+}
+
+// volume.py:164-177 _lut_classify: f64 lerp rounded to f32.
+__device__ __forceinline__ float4 narrow(const double4 v) {
+  return make_float4((float)v.x, (float)v.y, (float)v.z, (float)v.w);
+}
+__device__ __forceinline__ float4 classify(const double4* lut, int n, double s) {
+  const double x = s * (double)(n - 1);
+  if (x <= 0.0) return narrow(lut[0]);
+  if (x >= (double)(n - 1)) return narrow(lut[n - 1]);
+  const int i = (int)x;
+  const double f = x - i;
+  const double4 l0 = lut[i], l1 = lut[i + 1];
+  float4 o;
+  o.x = (float)(l0.x * (1.0 - f) + l1.x * f);
+  o.y = (float)(l0.y * (1.0 - f) + l1.y * f);
+  o.z = (float)(l0.z * (1.0 - f) + l1.z * f);
+  o.w = (float)(l0.w * (1.0 - f) + l1.w * f);
+  return o;
+}
+
+}  // namespace vdi

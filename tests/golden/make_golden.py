@@ -288,7 +288,53 @@ def search_case(name, n_cases=20000):
                     seeds=pp, index=oi, seed_out=os_))
 
 
+def dvr_case(name, specs):
+    """render_dvr (dvr.py:92-103) on the volumes of the generation fixtures.
+    specs: (tag, volume fixture, our Volume, TF, camera, step, ref_step,
+    early_term_alpha, background)."""
+    rec = {"tags": np.array([s[0] for s in specs])}
+    for tag, vfrom, vol, tf, cam, step, ref_step, et, bg in specs:
+        rvol, rtf, rc = r_volume(vol), vk.TransferFunction(tf.control_points), r_camera(cam)
+        img = vk.render_dvr(rvol, rtf, rc, step=step, ref_step=ref_step,
+                            early_term_alpha=et, background=bg)
+        rec.update(cam_record(tag, rc))
+        rec[f"{tag}_volume_from"] = np.array(vfrom)
+        rec[f"{tag}_lut"] = rtf.lut
+        rec[f"{tag}_params"] = np.array([np.nan if step is None else step,
+                                         np.nan if ref_step is None else ref_step, et,
+                                         *bg], np.float64)
+        rec[f"{tag}_image"] = img.data
+        print(f"{name}/{tag}: alpha mean {img.data[..., 3].mean():.4f}")
+    save(name, rec)
+
+
+def dvr_main():
+    vol, tf, gcam, rcam, _ = synth.config("C1")
+    sph = synth.preset_volume("sphere", 64)
+    stf = synth.preset_tf("sphere")
+    scam = synth.sweep_camera(sph, 25.0, (96, 80), elevation_deg=10.0)
+    bands = synth.preset_volume("bands", 64)
+    bu16 = synth.make_volume(bands.data.astype(np.uint16) * 257 + 3, "u16")
+    bview = synth.sweep_camera(bands, 50.0, (64, 64), elevation_deg=-20.0)
+    z = np.arange(32)[:, None, None]
+    stripes = np.broadcast_to(np.where(z % 6 < 3, 200, 0), (32, 32, 32)).astype(np.uint8)
+    svol = synth.make_volume(stripes, "u8")
+    stcam = synth.sweep_camera(svol, 30.0, (24, 24), elevation_deg=60.0)
+    bg0 = (0.0, 0.0, 0.0, 1.0)
+    dvr_case("dvr", [
+        ("d0", "c1_blobs64", vol, tf, rcam, None, None, 0.999, bg0),
+        ("d1", "c1_blobs64", vol, tf, gcam, 0.37, 0.5, 0.999, (0.2, 0.3, 0.4, 0.7)),
+        ("d2", "sphere64_u8", sph, stf, scam, None, None, 0.5, bg0),
+        ("d3", "bands64_u16_nsg4", bu16, synth.preset_tf("bands"), bview, 0.8, 0.6, 0.999,
+         bg0),
+        ("d4", "stripes32_capped", svol, stf, stcam, None, None, 1.0, (1.0, 1.0, 1.0, 0.5)),
+    ])
+
+
 def main():
+    if "--only-dvr" in sys.argv:
+        dvr_main()
+        return
     deg = math.radians
     RO = vk.RenderOptions
     # C1: the BASELINE config the CPU reference runs (blobs 64^3 f32, 128^2, n_sg 20)
@@ -342,6 +388,7 @@ def main():
 
     random_vdi_case("random_vdi", [0, 1, 2, 3, 4, 5])
     search_case("search_fuzz")
+    dvr_main()
 
 
 if __name__ == "__main__":

@@ -74,3 +74,24 @@ def render_specs(g):
                         viewport=tuple(int(v) for v in g[f"{t}_viewport"]),
                         use_ess=bool(o[0]), early_term=float(o[1]), bg=o[2:6]))
     return out
+
+
+def dvr_specs():
+    """The render_dvr cases of dvr.npz (dvr.py:92-103), with the volume they
+    ran on and step / ref_step resolved as render_dvr does."""
+    g = load("dvr")
+    out = []
+    for t in (str(x) for x in g["tags"]):
+        vg = load(str(g[f"{t}_volume_from"]))
+        p = g[f"{t}_params"]
+        step = 0.5 * float(np.min(vg["spacing"])) if np.isnan(p[0]) else float(p[0])
+        lref = step if np.isnan(p[1]) else float(p[1])
+        vp = g[f"{t}_viewport"]
+        out.append(dict(tag=t, vg=vg, lut=g[f"{t}_lut"], pv=g[f"{t}_pv"],
+                        inv_pv=g[f"{t}_inv_pv"], eye=g[f"{t}_pose"][:3],
+                        aabb=vg["aabb"], width=int(vp[0]), height=int(vp[1]),
+                        step=step, lref=lref, early_term=float(p[2]), bg=p[3:7],
+                        image=g[f"{t}_image"],
+                        step_arg=None if np.isnan(p[0]) else float(p[0]),
+                        ref_step_arg=None if np.isnan(p[1]) else float(p[1])))
+    return out

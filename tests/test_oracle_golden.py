@@ -89,3 +89,12 @@ def test_camera_matrices_bit_exact():
             assert np.array_equal(cam.proj_view().view(np.uint64), g[f"{t}_pv"].view(np.uint64))
             assert np.array_equal(cam.inv_proj_view().view(np.uint64),
                                   g[f"{t}_inv_pv"].view(np.uint64))
+
+
+def test_dvr_bit_exact():
+    """render_dvr (dvr.py:21-103): the oracle reproduces R's image bits."""
+    for s in gio.dvr_specs():
+        img = oracle.dvr(gio.normalized(s["vg"]), s["lut"], s["pv"], s["inv_pv"], s["eye"],
+                         s["aabb"], s["width"], s["height"], s["step"], s["lref"],
+                         s["early_term"], s["bg"])
+        assert np.array_equal(img.view(np.uint64), s["image"].view(np.uint64)), s["tag"]
