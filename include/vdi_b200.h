@@ -16,6 +16,9 @@
  *   vdi_find_first_batch  batch form of raycast.py:144-156 find_first_supersegment
  *   vdi_dvr_launch     replaces dvr.py:21-89      _dvr_kernel (render_dvr's
  *                      ground-truth emission-absorption raycast)
+ *   vdi_preview_launch replaces preview.py:49-205  _preview_kernel (point-sampled
+ *                      preview through the AccelGrid)
+ *   vdi_bilinear_upsample  replaces preview.py:208-223 bilinear_upsample
  *   vdi_segs_to_aos / vdi_segs_from_aos  device layout <-> the reference's
  *                      (H, W, n_sg, 6) f32 array (vdi.py:3-7, 23-24)
  *
@@ -181,6 +184,33 @@ typedef struct VdiDvrArgs {
 
 #define VDI_DVR_WORKSPACE_BYTES 256
 
+/* Preview rendering with dynamic subsampling (preview.py:49-205) at the
+ * low-res viewport out_w x out_h; upsample with vdi_bilinear_upsample. */
+typedef struct VdiPreviewArgs {
+  const float* segs;            /* list-SoA */
+  const int32_t* counts;
+  const uint32_t* grid;         /* (gz, gy, gx) */
+  double* image;                /* OUT (out_h, out_w, 4) f64 premultiplied, 16 B aligned */
+  unsigned long long* cell_samples; /* OUT (gz, gy, gx) planned samples, zeroed by the
+                                   launch; may be NULL */
+  unsigned long long* stat_sums;/* OUT [1] += total samples, may be NULL */
+  void* workspace;              /* >= VDI_PREVIEW_WORKSPACE_BYTES device bytes */
+  double gen_pv[16];
+  double gen_inv_pv[16];
+  double new_inv_pv[16];        /* low-res camera */
+  double eye[3];
+  double aabb[6];               /* Vdi.volume_aabb */
+  double bg[4];
+  double near, far, proj_a, proj_b;  /* grid near/far, generation depth constants */
+  double d_r, early_term;
+  int32_t vdi_w, vdi_h, n_sg;
+  int32_t gx, gy, gz;
+  int32_t out_w, out_h;
+  int32_t vdi_band_rows, vdi_band_world, vdi_rows_per_rank;  /* as VdiRenderArgs */
+} VdiPreviewArgs;
+
+#define VDI_PREVIEW_WORKSPACE_BYTES 256
+
 const char* vdi_last_error(void);
 int vdi_abi_version(void);
 
@@ -191,6 +221,12 @@ int vdi_gen_launch(const VdiGenArgs* args, vdi_stream_t stream);
 int vdi_grid_launch(const VdiGridArgs* args, vdi_stream_t stream);
 int vdi_render_launch(const VdiRenderArgs* args, vdi_stream_t stream);
 int vdi_dvr_launch(const VdiDvrArgs* args, vdi_stream_t stream);
+int vdi_preview_launch(const VdiPreviewArgs* args, vdi_stream_t stream);
+/* (h, w, channels) f64 -> (out_h, out_w, channels), preview.py:208-223
+ * (the caller handles the identity case, where R returns its input). */
+int vdi_bilinear_upsample(const double* src, int32_t w, int32_t h, double* dst,
+                          int32_t out_w, int32_t out_h, int32_t channels,
+                          vdi_stream_t stream);
 
 /* Alg. 2 search over a batch of independent queries (raycast.py:79-156).
  * fronts/backs: (n_queries, n_max) f32, counts: (n_queries,), d_entry /

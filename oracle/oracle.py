@@ -62,6 +62,16 @@ def lib():
         L.vdio_dvr.argtypes = [
             _f32, _int, _int, _int, _f32, _int, _f64, _f64, _f64, _f64,
             _int, _int, _dbl, _dbl, _dbl, _f64, _vp, _int, _int, _f64, _vp]
+        L.vdio_preview.argtypes = [
+            _f32, _i32, _int, _int, _int, _f64, _f64, _f64, _f64, _f64,
+            _int, _int, _u32, _int, _int, _int, _dbl, _dbl, _dbl, _dbl,
+            _dbl, _dbl, _f64, _int, _f64, _i64]
+        L.vdio_preview.restype = ctypes.c_int64
+        _u8 = np.ctypeslib.ndpointer(np.uint8, flags="C_CONTIGUOUS")
+        L.vdio_lz4_compress.argtypes = [_u8, ctypes.c_int64, _u8]
+        L.vdio_lz4_compress.restype = ctypes.c_int64
+        L.vdio_lz4_decompress.argtypes = [_u8, ctypes.c_int64, _u8, ctypes.c_int64]
+        L.vdio_lz4_decompress.restype = ctypes.c_int64
         L.vdio_max_threads.restype = _int
         _lib = L
     return _lib
@@ -169,3 +179,81 @@ def dvr(vol_norm, lut, pv, inv_pv, eye, aabb, width, height, step, lref,
                    _m(bg), rp, nr, threads, img,
                    None if smp is None else smp.ctypes.data_as(ctypes.c_void_p))
     return (img, smp) if with_samples else img
+
+
+def preview_lowres(segs, counts, gen_pv, gen_inv_pv, aabb, new_inv_pv, eye, out_w, out_h,
+                   grid, near, far, d_r, early_term=0.999, bg=(0.0, 0.0, 0.0, 1.0),
+                   threads=0):
+    """_preview_kernel (preview.py:49-205): low-res image, total samples,
+    per-cell samples (gz, gy, gx) i64."""
+    segs = np.ascontiguousarray(segs, np.float32)
+    vdi_h, vdi_w, n_sg, _ = segs.shape
+    grid = np.ascontiguousarray(grid, np.uint32)
+    gz, gy, gx = grid.shape
+    pa, pb = depth_consts(near, far)
+    img = np.zeros((out_h, out_w, 4), np.float64)
+    cells = np.zeros((gz, gy, gx), np.int64)
+    total = lib().vdio_preview(segs, np.ascontiguousarray(counts, np.int32), vdi_w, vdi_h,
+                               n_sg, _m(gen_pv), _m(gen_inv_pv), _m(aabb), _m(new_inv_pv),
+                               _m(eye), out_w, out_h, grid, gx, gy, gz, float(near),
+                               float(far), pa, pb, float(d_r), float(early_term), _m(bg),
+                               threads, img, cells)
+    return img, int(total), cells
+
+
+def bilinear_upsample(arr, out_w, out_h):
+    """preview.py:208-223, restated with the same numpy expressions."""
+    h, w = arr.shape[:2]
+    if (w, h) == (out_w, out_h):
+        return arr
+    xs = (np.arange(out_w) + 0.5) * w / out_w - 0.5
+    ys = (np.arange(out_h) + 0.5) * h / out_h - 0.5
+    x0 = np.clip(np.floor(xs).astype(np.int64), 0, w - 1)
+    y0 = np.clip(np.floor(ys).astype(np.int64), 0, h - 1)
+    x1 = np.minimum(x0 + 1, w - 1)
+    y1 = np.minimum(y0 + 1, h - 1)
+    fx = np.clip(xs - x0, 0.0, 1.0)[None, :, None]
+    fy = np.clip(ys - y0, 0.0, 1.0)[:, None, None]
+    top = arr[y0[:, None], x0[None, :]] * (1 - fx) + arr[y0[:, None], x1[None, :]] * fx
+    bot = arr[y1[:, None], x0[None, :]] * (1 - fx) + arr[y1[:, None], x1[None, :]] * fx
+    return top * (1 - fy) + bot * fy
+
+
+def lz4_compress(data: bytes) -> bytes:
+    """lz4.py:51-114 + 171-175 compress()."""
+    src = np.frombuffer(data, dtype=np.uint8).copy()
+    dst = np.empty(len(data) + len(data) // 255 + 16, dtype=np.uint8)
+    n = lib().vdio_lz4_compress(src, len(src), dst)
+    return dst[:n].tobytes()
+
+
+def lz4_decompress(data: bytes, uncompressed_len: int) -> bytes:
+    """lz4.py:117-168 + 178-189 decompress(); raises ValueError like
+    DecompressFailure."""
+    if uncompressed_len == 0:
+        if len(data) != 0 and data != b"\x00":
+            raise ValueError("nonempty block for empty payload")
+        return b""
+    src = np.frombuffer(data, dtype=np.uint8).copy()
+    dst = np.empty(uncompressed_len, dtype=np.uint8)
+    n = lib().vdio_lz4_decompress(src, len(src), dst, uncompressed_len)
+    if n != uncompressed_len:
+        raise ValueError(f"decoded {n} bytes, expected {uncompressed_len}")
+    return dst.tobytes()
+
+
+def encode_vdi(width, height, n_sg, counts, segs, cam_vals, aabb, grid):
+    """vdi.py:141-159 encode_vdi: the VDI1 little-endian byte layout.
+    cam_vals = (pos3, quat4, fov_y, near, far); segs (H, W, n_sg, 6) AoS;
+    grid (gz, gy, gx)."""
+    import struct
+    gz, gy, gx = grid.shape
+    parts = [struct.pack("<4sIIII", b"VDI1", 1, width, height, n_sg),
+             struct.pack("<10d", *cam_vals),
+             struct.pack("<6d", *np.asarray(aabb, np.float64).reshape(6)),
+             struct.pack("<3I", gx, gy, gz),
+             np.asarray(counts).astype("<u2").tobytes()]
+    mask = np.arange(n_sg)[None, None, :] < np.asarray(counts)[:, :, None]
+    parts.append(np.asarray(segs, np.float32)[mask].astype("<f4").tobytes())
+    parts.append(np.asarray(grid).astype("<u4").tobytes())
+    return b"".join(parts)

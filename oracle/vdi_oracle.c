@@ -849,6 +849,294 @@ int vdio_dvr(const float* vol, int nx, int ny, int nz, const float* lut, int lut
   return 0;
 }
 
+/* --------------------------------------------------------------- preview */
+
+static int cmp_double(const void* a, const void* b) {
+  const double x = *(const double*)a, y = *(const double*)b;
+  return (x > y) - (x < y);
+}
+
+static inline double sq(double x) { return x * x; } /* numba x ** 2 == x * x */
+
+/* One pixel of preview.py:49-213 _preview_kernel: chord breakpoints at grid
+ * cell boundaries (sorted, as np.sort), round(d_r * len * count) point
+ * samples per non-empty cell, each taking the colour of the supersegment
+ * containing it (R's _find_first with d_entry == d_exit) with opacity from
+ * the distance to the previous sample. `brks` is caller scratch of
+ * gx + gy + gz + 2 doubles. Returns the samples planned for this pixel. */
+static int64_t preview_pixel(const float* segs, const int32_t* counts, int vdi_w,
+                             int vdi_h, int n_sg, const double* gen_pv,
+                             const double* gen_inv_pv, const double* bb,
+                             const double* new_inv_pv, const double* eye, int out_w,
+                             int out_h, const uint32_t* gcounts, int gx, int gy, int gz,
+                             double near, double far, double proj_a, double proj_b,
+                             double d_r, double early_term, const double* bg,
+                             int64_t idx, double* img, int64_t* cell_samples,
+                             double* brks) {
+  const int row = (int)(idx / out_w), col = (int)(idx % out_w);
+  double acc_r = 0.0, acc_g = 0.0, acc_b = 0.0, acc_a = 0.0;
+  int64_t total = 0;
+  double d[3];
+  pixel_ray(new_inv_pv, eye, col, row, out_w, out_h, d); /* 60-69 */
+  double ta, tb, fa, fb, t0 = 0.0, t1 = 0.0;
+  int ok = 0;
+  if (clip_aabb(eye[0], eye[1], eye[2], d[0], d[1], d[2], bb, &ta, &tb) &&
+      clip_frustum(gen_pv, eye[0], eye[1], eye[2], d[0], d[1], d[2], &fa, &fb)) {
+    t0 = dmax(dmax(ta, fa), 0.0);
+    t1 = dmin(tb, fb);
+    ok = t1 > t0;
+  }
+  if (ok) {
+    double a0x, a0y, a0z, a1x, a1y, a1z;
+    xform(gen_pv, eye[0] + t0 * d[0], eye[1] + t0 * d[1], eye[2] + t0 * d[2], &a0x, &a0y, &a0z);
+    xform(gen_pv, eye[0] + t1 * d[0], eye[1] + t1 * d[1], eye[2] + t1 * d[2], &a1x, &a1y, &a1z);
+    const double cdx = a1x - a0x, cdy = a1y - a0y, cdz = a1z - a0z;
+    int nb = 0; /* 94-121 */
+    brks[nb++] = 0.0;
+    brks[nb++] = 1.0;
+    if (fabs(cdx) > 1e-14)
+      for (int i = 1; i < gx; ++i) {
+        const double s = (-1.0 + 2.0 * i / gx - a0x) / cdx;
+        if (0.0 < s && s < 1.0) brks[nb++] = s;
+      }
+    if (fabs(cdy) > 1e-14)
+      for (int i = 1; i < gy; ++i) {
+        const double s = (-1.0 + 2.0 * i / gy - a0y) / cdy;
+        if (0.0 < s && s < 1.0) brks[nb++] = s;
+      }
+    if (fabs(cdz) > 1e-14)
+      for (int i = 1; i < gz; ++i) {
+        const double dep = near + (far - near) * i / gz;
+        const double zb = proj_a - proj_b / dep;
+        const double s = (zb - a0z) / cdz;
+        if (0.0 < s && s < 1.0) brks[nb++] = s;
+      }
+    qsort(brks, (size_t)nb, sizeof(double), cmp_double); /* 122 */
+    double prev_x, prev_y, prev_z;
+    xform(gen_inv_pv, a0x, a0y, a0z, &prev_x, &prev_y, &prev_z); /* 125 */
+    int64_t p = -1;
+    int done = 0;
+    for (int bi = 0; bi < nb - 1 && !done; ++bi) { /* 128-210 */
+      const double s_a = brks[bi], s_b = brks[bi + 1];
+      if (s_b - s_a < 1e-15) continue;
+      const double sm = 0.5 * (s_a + s_b);
+      const double mx = a0x + sm * cdx, my = a0y + sm * cdy, mz = a0z + sm * cdz;
+      const int64_t cgx = clampi(floor_i((mx + 1.0) * gx / 2.0), 0, gx - 1);
+      const int64_t cgy = clampi(floor_i((my + 1.0) * gy / 2.0), 0, gy - 1);
+      const double mdep = proj_b / (proj_a - mz);
+      const int64_t cgz = clampi(floor_i((mdep - near) / (far - near) * gz), 0, gz - 1);
+      const int64_t cell = (cgz * gy + cgy) * gx + cgx;
+      const uint32_t cnt = gcounts[cell];
+      if (cnt == 0) continue;
+      double w0x, w0y, w0z, w1x, w1y, w1z;
+      xform(gen_inv_pv, a0x + s_a * cdx, a0y + s_a * cdy, a0z + s_a * cdz, &w0x, &w0y, &w0z);
+      xform(gen_inv_pv, a0x + s_b * cdx, a0y + s_b * cdy, a0z + s_b * cdz, &w1x, &w1y, &w1z);
+      const double seg_len = sqrt(sq(w1x - w0x) + sq(w1y - w0y) + sq(w1z - w0z));
+      const int64_t n = (int64_t)floor(d_r * seg_len * (double)cnt + 0.5);
+      if (n <= 0) continue;
+      if (cell_samples) {
+#pragma omp atomic
+        cell_samples[cell] += n;
+      }
+      total += n;
+      for (int64_t i = 0; i < n; ++i) {
+        const double sf = s_a + ((double)i + 0.5) / (double)n * (s_b - s_a);
+        const double sx = a0x + sf * cdx, sy = a0y + sf * cdy, sz = a0z + sf * cdz;
+        double swx, swy, swz;
+        xform(gen_inv_pv, sx, sy, sz, &swx, &swy, &swz);
+        const double dist = sqrt(sq(swx - prev_x) + sq(swy - prev_y) + sq(swz - prev_z));
+        prev_x = swx;
+        prev_y = swy;
+        prev_z = swz;
+        const int64_t lx = clampi(floor_i((sx + 1.0) * vdi_w / 2.0), 0, vdi_w - 1);
+        const int64_t ly = clampi(floor_i((sy + 1.0) * vdi_h / 2.0), 0, vdi_h - 1);
+        const int64_t lc = counts[ly * vdi_w + lx];
+        if (lc == 0) continue;
+        const float* ls = segs + (ly * vdi_w + lx) * (int64_t)n_sg * 6;
+        int64_t seed;
+        const int64_t j = find_first(ls, ls + 1, 6, lc, sz, sz, p, &seed);
+        p = seed;
+        if (j < 0) continue;
+        const float alpha = ls[j * 6 + 5];
+        if (alpha <= 0.0f) continue;
+        const double xc = -1.0 + 2.0 * (lx + 0.5) / vdi_w;
+        const double yc = -1.0 + 2.0 * (ly + 0.5) / vdi_h;
+        double wfx, wfy, wfz, wbx, wby, wbz;
+        xform(gen_inv_pv, xc, yc, (double)ls[j * 6], &wfx, &wfy, &wfz);
+        xform(gen_inv_pv, xc, yc, (double)ls[j * 6 + 1], &wbx, &wby, &wbz);
+        const double thick = sqrt(sq(wbx - wfx) + sq(wby - wfy) + sq(wbz - wfz));
+        if (thick <= 0.0) continue;
+        const double a_t = 1.0 - pow(1.0 - (double)alpha, dist / thick);
+        const double scale = a_t / (double)alpha;
+        const double w = 1.0 - acc_a;
+        acc_r += w * (double)ls[j * 6 + 2] * scale;
+        acc_g += w * (double)ls[j * 6 + 3] * scale;
+        acc_b += w * (double)ls[j * 6 + 4] * scale;
+        acc_a += w * a_t;
+        if (acc_a >= early_term) {
+          done = 1;
+          break;
+        }
+      }
+    }
+  }
+  const double w = 1.0 - acc_a; /* 207-211 */
+  double* o = img + idx * 4;
+  o[0] = acc_r + w * bg[0] * bg[3];
+  o[1] = acc_g + w * bg[1] * bg[3];
+  o[2] = acc_b + w * bg[2] * bg[3];
+  o[3] = acc_a + w * bg[3];
+  return total;
+}
+
+/* preview.py:49-213 over all pixels (R runs it serially; pixels are
+ * independent and cell_samples is an integer sum, so the order is free).
+ * Returns the total planned samples. */
+int64_t vdio_preview(const float* segs, const int32_t* counts, int vdi_w, int vdi_h,
+                     int n_sg, const double* gen_pv, const double* gen_inv_pv,
+                     const double* bb, const double* new_inv_pv, const double* eye,
+                     int out_w, int out_h, const uint32_t* gcounts, int gx, int gy,
+                     int gz, double near, double far, double proj_a, double proj_b,
+                     double d_r, double early_term, const double* bg, int nthreads,
+                     double* img, int64_t* cell_samples) {
+  int64_t total = 0;
+#ifdef _OPENMP
+  if (nthreads > 0) omp_set_num_threads(nthreads);
+#endif
+#pragma omp parallel reduction(+ : total)
+  {
+    double* brks = (double*)malloc(sizeof(double) * (size_t)(gx + gy + gz + 2));
+#pragma omp for schedule(dynamic, 16)
+    for (int64_t j = 0; j < (int64_t)out_w * out_h; ++j)
+      total += preview_pixel(segs, counts, vdi_w, vdi_h, n_sg, gen_pv, gen_inv_pv, bb,
+                             new_inv_pv, eye, out_w, out_h, gcounts, gx, gy, gz, near, far,
+                             proj_a, proj_b, d_r, early_term, bg, j, img, cell_samples, brks);
+    free(brks);
+  }
+  return total;
+}
+
+/* ------------------------------------------------------------------- LZ4 */
+
+/* lz4.py:13-17 */
+#define LZ4_HASH_LOG 16
+#define LZ4_MIN_MATCH 4
+#define LZ4_LAST_LITERALS 5
+#define LZ4_MFLIMIT 12
+
+static inline uint32_t lz4_read32(const uint8_t* s, int64_t i) { /* lz4.py:34-38 */
+  return (uint32_t)s[i] | ((uint32_t)s[i + 1] << 8) | ((uint32_t)s[i + 2] << 16) |
+         ((uint32_t)s[i + 3] << 24);
+}
+
+static inline uint32_t lz4_hash32(uint32_t v) { /* lz4.py:28-31 */
+  return ((v * 2654435761u) >> (32 - LZ4_HASH_LOG)) & ((1u << LZ4_HASH_LOG) - 1u);
+}
+
+static inline int64_t lz4_write_length(uint8_t* dst, int64_t o, int64_t len) { /* 41-48 */
+  while (len >= 255) {
+    dst[o++] = 255;
+    len -= 255;
+  }
+  dst[o++] = (uint8_t)len;
+  return o;
+}
+
+/* lz4.py:51-114 _compress_kernel: the reference's greedy single-probe
+ * parse. dst must hold n + n / 255 + 16 bytes. Returns the block length. */
+int64_t vdio_lz4_compress(const uint8_t* src, int64_t n, uint8_t* dst) {
+  if (n == 0) return 0;
+  int64_t* table = (int64_t*)malloc(sizeof(int64_t) << LZ4_HASH_LOG);
+  for (int64_t k = 0; k < (1 << LZ4_HASH_LOG); ++k) table[k] = -1;
+  int64_t o = 0, anchor = 0, i = 0;
+  const int64_t limit = n - LZ4_MFLIMIT;
+  while (i < limit) {
+    const uint32_t h = lz4_hash32(lz4_read32(src, i));
+    const int64_t cand = table[h];
+    table[h] = i;
+    if (cand >= 0 && i - cand <= 65535 && lz4_read32(src, cand) == lz4_read32(src, i)) {
+      int64_t mlen = LZ4_MIN_MATCH;
+      const int64_t mmax = n - LZ4_LAST_LITERALS - i;
+      while (mlen < mmax && src[cand + mlen] == src[i + mlen]) ++mlen;
+      const int64_t lit = i - anchor;
+      const int64_t tok = o++;
+      const int64_t lcode = lit >= 15 ? 15 : lit;
+      if (lit >= 15) o = lz4_write_length(dst, o, lit - 15);
+      memcpy(dst + o, src + anchor, (size_t)lit);
+      o += lit;
+      const int64_t off = i - cand;
+      dst[o] = (uint8_t)(off & 0xFF);
+      dst[o + 1] = (uint8_t)((off >> 8) & 0xFF);
+      o += 2;
+      const int64_t mcode = mlen - LZ4_MIN_MATCH;
+      if (mcode >= 15) {
+        dst[tok] = (uint8_t)((lcode << 4) | 15);
+        o = lz4_write_length(dst, o, mcode - 15);
+      } else {
+        dst[tok] = (uint8_t)((lcode << 4) | mcode);
+      }
+      i += mlen;
+      anchor = i;
+      if (i < limit) table[lz4_hash32(lz4_read32(src, i - 2))] = i - 2;
+    } else {
+      ++i;
+    }
+  }
+  const int64_t lit = n - anchor; /* final literal run (102-113) */
+  const int64_t tok = o++;
+  if (lit >= 15) {
+    dst[tok] = 15 << 4;
+    o = lz4_write_length(dst, o, lit - 15);
+  } else {
+    dst[tok] = (uint8_t)(lit << 4);
+  }
+  memcpy(dst + o, src + anchor, (size_t)lit);
+  o += lit;
+  free(table);
+  return o;
+}
+
+/* lz4.py:117-168 _decompress_kernel: bytes written, or -1 on malformed input. */
+int64_t vdio_lz4_decompress(const uint8_t* src, int64_t n, uint8_t* dst, int64_t out_n) {
+  int64_t si = 0, di = 0;
+  while (si < n) {
+    const int token = src[si++];
+    int64_t lit = token >> 4;
+    if (lit == 15) {
+      for (;;) {
+        if (si >= n) return -1;
+        const int b = src[si++];
+        lit += b;
+        if (b != 255) break;
+      }
+    }
+    if (si + lit > n || di + lit > out_n) return -1;
+    memcpy(dst + di, src + si, (size_t)lit);
+    si += lit;
+    di += lit;
+    if (si >= n) break; /* last sequence has no match part */
+    if (si + 2 > n) return -1;
+    const int64_t off = (int64_t)src[si] | ((int64_t)src[si + 1] << 8);
+    si += 2;
+    if (off == 0 || off > di) return -1;
+    int64_t mlen = token & 15;
+    if (mlen == 15) {
+      for (;;) {
+        if (si >= n) return -1;
+        const int b = src[si++];
+        mlen += b;
+        if (b != 255) break;
+      }
+    }
+    mlen += LZ4_MIN_MATCH;
+    if (di + mlen > out_n) return -1;
+    const int64_t mp = di - off;
+    for (int64_t k = 0; k < mlen; ++k) dst[di + k] = dst[mp + k]; /* overlapping copy */
+    di += mlen;
+  }
+  return di;
+}
+
 int vdio_max_threads(void) {
 #ifdef _OPENMP
   return omp_get_max_threads();

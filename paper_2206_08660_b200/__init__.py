@@ -22,6 +22,9 @@ _LAZY = {
     "validate_vdi": "vdi",
     "FrameStream": "stream", "FrameResult": "stream",
     "render_dvr": "dvr",
+    "render_preview": "preview", "PreviewParams": "preview", "PreviewStats": "preview",
+    "PiController": "preview", "pi_update": "preview", "samples_in_cell": "preview",
+    "bilinear_upsample": "preview",
 }
 
 

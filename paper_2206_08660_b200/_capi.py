@@ -69,9 +69,27 @@ class VdiDvrArgs(ctypes.Structure):
 
 DVR_WORKSPACE_BYTES = 256
 
+
+class VdiPreviewArgs(ctypes.Structure):
+    _fields_ = [
+        ("segs", _P), ("counts", _P), ("grid", _P), ("image", _P), ("cell_samples", _P),
+        ("stat_sums", _P), ("workspace", _P),
+        ("gen_pv", _D * 16), ("gen_inv_pv", _D * 16), ("new_inv_pv", _D * 16),
+        ("eye", _D * 3), ("aabb", _D * 6), ("bg", _D * 4),
+        ("near", _D), ("far", _D), ("proj_a", _D), ("proj_b", _D), ("d_r", _D),
+        ("early_term", _D),
+        ("vdi_w", _I), ("vdi_h", _I), ("n_sg", _I), ("gx", _I), ("gy", _I), ("gz", _I),
+        ("out_w", _I), ("out_h", _I),
+        ("vdi_band_rows", _I), ("vdi_band_world", _I), ("vdi_rows_per_rank", _I),
+    ]
+
+
+PREVIEW_WORKSPACE_BYTES = 256
+
 EXPORTS = ["vdi_last_error", "vdi_abi_version", "vdi_gen_workspace_bytes",
            "vdi_gen_workspace_min_bytes", "vdi_gen_launch",
-           "vdi_grid_launch", "vdi_render_launch", "vdi_dvr_launch", "vdi_find_first_batch",
+           "vdi_grid_launch", "vdi_render_launch", "vdi_dvr_launch",
+           "vdi_preview_launch", "vdi_bilinear_upsample", "vdi_find_first_batch",
            "vdi_volume_brick_max", "vdi_selftest_arith", "vdi_segs_to_aos",
            "vdi_segs_from_aos", "vdi_volume_cells_bytes", "vdi_volume_cells"]
 
@@ -101,6 +119,8 @@ def load():
     L.vdi_grid_launch.argtypes = [ctypes.POINTER(VdiGridArgs), _P]
     L.vdi_render_launch.argtypes = [ctypes.POINTER(VdiRenderArgs), _P]
     L.vdi_dvr_launch.argtypes = [ctypes.POINTER(VdiDvrArgs), _P]
+    L.vdi_preview_launch.argtypes = [ctypes.POINTER(VdiPreviewArgs), _P]
+    L.vdi_bilinear_upsample.argtypes = [_P, _I, _I, _P, _I, _I, _I, _P]
     L.vdi_find_first_batch.argtypes = [_P, _P, _P, _I, _P, _P, _P, _P, _P, ctypes.c_int64, _P]
     L.vdi_volume_brick_max.argtypes = [_P, _I, _I, _I, _I, _I, _P, _P]
     L.vdi_volume_brick_max.restype = ctypes.c_int
@@ -112,7 +132,9 @@ def load():
     L.vdi_selftest_arith.restype = ctypes.c_int
     L.vdi_segs_to_aos.argtypes = [_P, _P, ctypes.c_int64, _I, _P]
     L.vdi_segs_from_aos.argtypes = [_P, _P, ctypes.c_int64, _I, _P]
-    for name in ("vdi_gen_launch", "vdi_grid_launch", "vdi_render_launch", "vdi_dvr_launch", "vdi_dvr_launch",
+    for name in ("vdi_gen_launch", "vdi_grid_launch", "vdi_render_launch", "vdi_dvr_launch",
+                 "vdi_preview_launch", "vdi_bilinear_upsample",
+           "vdi_preview_launch", "vdi_bilinear_upsample", "vdi_dvr_launch",
                  "vdi_find_first_batch", "vdi_segs_to_aos", "vdi_segs_from_aos"):
         getattr(L, name).restype = ctypes.c_int
     if L.vdi_abi_version() != 1:

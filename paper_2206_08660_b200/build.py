@@ -20,8 +20,8 @@ CSRC = os.path.join(PKG, "csrc")
 LIBDIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIBDIR, "libvdi_b200.so")
 SOURCES = ["vdi_capi.cu", "vdi_gen.cu", "vdi_grid.cu", "vdi_render.cu", "vdi_volume.cu",
-           "vdi_dvr.cu"]
-HEADERS = ["vdi_common.cuh", "vdi_sample.cuh", "vdi_internal.h", "../../include/vdi_b200.h"]
+           "vdi_dvr.cu", "vdi_preview.cu"]
+HEADERS = ["vdi_common.cuh", "vdi_sample.cuh", "vdi_search.cuh", "vdi_internal.h", "../../include/vdi_b200.h"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

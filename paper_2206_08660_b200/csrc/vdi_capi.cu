@@ -93,6 +93,31 @@ int vdi_dvr_launch(const VdiDvrArgs* a, vdi_stream_t stream) {
   return vdi::dvr_launch(a, static_cast<cudaStream_t>(stream));
 }
 
+int vdi_preview_launch(const VdiPreviewArgs* a, vdi_stream_t stream) {
+  if (!a) return set_error(VDI_EINVAL, "null args");
+  if (!a->segs || !a->counts || !a->grid || !a->image || !a->workspace)
+    return set_error(VDI_EINVAL, "null device pointer");
+  if (!(a->d_r > 0.0 && a->d_r <= 1.0)) return set_error(VDI_EINVAL, "d_r must be in (0, 1]");
+  if (!(a->early_term > 0.0 && a->early_term <= 1.0))
+    return set_error(VDI_EINVAL, "early_term must be in (0, 1]");
+  if (a->vdi_w < 1 || a->vdi_h < 1 || a->n_sg < 1 || a->out_w < 1 || a->out_h < 1)
+    return set_error(VDI_EINVAL, "bad sizes");
+  if (a->gx < 1 || a->gy < 1 || a->gz < 1) return set_error(VDI_EINVAL, "bad grid dims");
+  if (reinterpret_cast<uintptr_t>(a->segs) % 16 != 0 ||
+      reinterpret_cast<uintptr_t>(a->image) % 16 != 0)
+    return set_error(VDI_EINVAL, "segs and image must be 16-byte aligned");
+  return vdi::preview_launch(a, static_cast<cudaStream_t>(stream));
+}
+
+int vdi_bilinear_upsample(const double* src, int32_t w, int32_t h, double* dst, int32_t out_w,
+                          int32_t out_h, int32_t channels, vdi_stream_t stream) {
+  if (!src || !dst) return set_error(VDI_EINVAL, "null device pointer");
+  if (w < 1 || h < 1 || out_w < 1 || out_h < 1 || channels < 1)
+    return set_error(VDI_EINVAL, "bad sizes");
+  return vdi::bilinear_upsample(src, w, h, dst, out_w, out_h, channels,
+                                static_cast<cudaStream_t>(stream));
+}
+
 int vdi_find_first_batch(const float* fronts, const float* backs, const int32_t* counts,
                          int32_t n_max, const double* d_entry, const double* d_exit,
                          const int32_t* seeds, int32_t* out_index, int32_t* out_seed,

@@ -25,6 +25,9 @@ size_t gen_workspace_bytes(const VdiGenArgs* a, int recommended);
 int grid_launch(const VdiGridArgs* a, cudaStream_t stream);
 int render_launch(const VdiRenderArgs* a, cudaStream_t stream);
 int dvr_launch(const VdiDvrArgs* a, cudaStream_t stream);
+int preview_launch(const VdiPreviewArgs* a, cudaStream_t stream);
+int bilinear_upsample(const double* src, int w, int h, double* dst, int out_w, int out_h,
+                      int channels, cudaStream_t stream);
 int find_first_batch(const float* fronts, const float* backs, const int32_t* counts,
                      int32_t n_max, const double* d_entry, const double* d_exit,
                      const int32_t* seeds, int32_t* out_index, int32_t* out_seed,

@@ -331,9 +331,123 @@ def dvr_main():
     ])
 
 
+def fixture_vdi(src):
+    """A reference Vdi + AccelGrid rebuilt from a committed fixture:
+    "<volume case>" or "random_vdi:<seed>"."""
+    from golden_io import load, unpack_segs
+    if src.startswith("random_vdi:"):
+        g = load("random_vdi")
+        t = "s" + src.split(":")[1]
+        pose = g[f"{t}_gen_pose"]
+        vp = g[f"{t}_gen_viewport"]
+        counts, segs, aabb, grid = (g[f"{t}_counts"], g[f"{t}_segs"], g[f"{t}_aabb"],
+                                    g[f"{t}_grid"])
+    else:
+        g = load(src)
+        pose, vp = g["gen_pose"], g["gen_viewport"]
+        counts, aabb, grid = g["counts"], g["aabb"], g["grid"]
+        segs = unpack_segs(counts, g["segs_packed"], int(g["n_sg"]))
+    cam = vk.Camera(position=tuple(pose[0:3]), orientation=tuple(pose[3:7]),
+                    fov_y=float(pose[7]), near=float(pose[8]), far=float(pose[9]),
+                    viewport=(int(vp[0]), int(vp[1])))
+    h, w, n_sg, _ = segs.shape
+    vdi = vk.Vdi(w, h, n_sg, counts, segs, cam, aabb)
+    gz, gy, gx = grid.shape
+    return vdi, vk.AccelGrid((gx, gy, gz), grid, cam.near, cam.far)
+
+
+def preview_main():
+    """render_preview (preview.py:233-268) on committed VDIs: low-res
+    image, upsampled image, total and per-cell samples."""
+    from vdikit.preview import PreviewParams, render_preview
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    vol, tf, gcam, rcam, _ = synth.config("C1")
+    sph = synth.preset_volume("sphere", 64)
+    sc = synth.sweep_camera(sph, 25.0, (128, 128), elevation_deg=10.0)
+    bands = synth.preset_volume("bands", 64)
+    bview = synth.sweep_camera(bands, 50.0, (64, 64), elevation_deg=-20.0)
+    from vdikit import orbit_camera as r_orbit
+    rv_cam = r_orbit((0.0, 0.0, 2.5), 4.0, 30.0, 20.0, fov_y=0.8, near=0.3, far=25.0,
+                     viewport=(32, 32))
+    specs = [
+        ("p0", "c1_blobs64", r_camera(rcam), 1.0, 1.0, (128, 128), (0.0, 0.0, 0.0, 1.0)),
+        ("p1", "c1_blobs64", r_camera(gcam), 0.5, 0.8, (128, 128), (0.2, 0.3, 0.4, 0.7)),
+        ("p2", "sphere64_u8", r_camera(sc), 0.3, 0.5, (96, 64), (0.0, 0.0, 0.0, 1.0)),
+        ("p3", "bands64_u16_nsg4", r_camera(bview), 0.7, 1.0, (64, 64), (1.0, 1.0, 1.0, 0.5)),
+        ("p4", "random_vdi:0", rv_cam, 1.0, 0.25, (32, 32), (0.0, 0.0, 0.0, 1.0)),
+        ("p5", "sphere64_u8", r_camera(sc), 1.0, 0.25, (128, 128), (0.0, 0.0, 0.0, 1.0)),
+    ]
+    rec = {"tags": np.array([s[0] for s in specs])}
+    for tag, src, cam, d_i, d_r, disp, bg in specs:
+        vdi, grid = fixture_vdi(src)
+        params = PreviewParams(d_i=d_i, d_r=d_r, display=disp)
+        img, st = render_preview(vdi, grid, cam, params, background=bg, with_stats=True)
+        rec.update(cam_record(tag, cam))
+        rec[f"{tag}_vdi_from"] = np.array(src)
+        rec[f"{tag}_params"] = np.array([d_i, d_r, disp[0], disp[1], *bg], np.float64)
+        rec[f"{tag}_image"] = img.data
+        rec[f"{tag}_total_samples"] = np.array(st.total_samples, np.int64)
+        rec[f"{tag}_cell_samples"] = st.cell_samples
+        print(f"preview/{tag}: {st.total_samples} samples, image {img.data.shape}")
+    save("preview", rec)
+
+
+def lz4_inputs():
+    """Byte strings for the LZ4 vectors: edge sizes around the 12-byte match
+    limit and 5-byte literal tail, runs, periodic data, long literal runs,
+    long matches (255-run length extensions) and random data."""
+    rng = np.random.default_rng(11)
+    out = [b"", b"a", b"abcdefghijkl", b"abcdefghijklm", b"\x00" * 13, b"\x00" * 1000,
+           bytes(range(256)) * 40, rng.integers(0, 256, 5000, dtype=np.uint8).tobytes(),
+           (b"VDI1" + bytes(rng.integers(0, 4, 3000, dtype=np.uint8))) * 3,
+           rng.integers(0, 256, 300, dtype=np.uint8).tobytes() + b"\x07" * 70000 +
+           rng.integers(0, 256, 17, dtype=np.uint8).tobytes()]
+    words = [rng.integers(0, 256, int(k), dtype=np.uint8).tobytes()
+             for k in rng.integers(3, 40, 60)]
+    out.append(b"".join(words[int(i)] for i in rng.integers(0, 60, 4000)))
+    return out
+
+
+def codec_main():
+    """encode_vdi (vdi.py:141-159) and lz4.compress (lz4.py:51-114, 171-175)
+    on committed VDIs and byte vectors."""
+    import hashlib
+    from vdikit import lz4 as rlz4
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    rec = {}
+    vdis = ["c1_blobs64", "sphere64_u8", "bands64_u16_nsg4", "blobs64_nsg3",
+            "stripes32_capped", "random_vdi:0", "random_vdi:3"]
+    rec["vdi_tags"] = np.array(vdis)
+    for k, src in enumerate(vdis):
+        vdi, grid = fixture_vdi(src)
+        raw = vk.encode_vdi(vdi, grid)
+        comp = rlz4.compress(raw)
+        assert rlz4.decompress(comp, len(raw)) == raw
+        v2, g2 = vk.decode_vdi(raw)
+        assert vk.encode_vdi(v2, g2) == raw
+        rec[f"v{k}_raw_sha256"] = np.array(hashlib.sha256(raw).hexdigest())
+        rec[f"v{k}_raw_len"] = np.array(len(raw), np.int64)
+        rec[f"v{k}_lz4"] = np.frombuffer(comp, np.uint8)
+        print(f"codec/{src}: raw {len(raw)} B, lz4 {len(comp)} B")
+    ins = lz4_inputs()
+    rec["n_bytes_cases"] = np.array(len(ins))
+    for k, b in enumerate(ins):
+        comp = rlz4.compress(b)
+        assert rlz4.decompress(comp, len(b)) == b
+        rec[f"b{k}_in"] = np.frombuffer(b, np.uint8)
+        rec[f"b{k}_lz4"] = np.frombuffer(comp, np.uint8)
+    save("codec", rec)
+
+
 def main():
+    if "--only-codec" in sys.argv:
+        codec_main()
+        return
     if "--only-dvr" in sys.argv:
         dvr_main()
+        return
+    if "--only-preview" in sys.argv:
+        preview_main()
         return
     deg = math.radians
     RO = vk.RenderOptions
@@ -389,6 +503,8 @@ def main():
     random_vdi_case("random_vdi", [0, 1, 2, 3, 4, 5])
     search_case("search_fuzz")
     dvr_main()
+    preview_main()
+    codec_main()
 
 
 if __name__ == "__main__":

@@ -95,3 +95,31 @@ def dvr_specs():
                         step_arg=None if np.isnan(p[0]) else float(p[0]),
                         ref_step_arg=None if np.isnan(p[1]) else float(p[1])))
     return out
+
+
+def fixture_vdi(src):
+    """(counts, segs AoS, grid, gen prefix record, aabb) of a committed VDI:
+    "<volume case>" or "random_vdi:<seed>"."""
+    if src.startswith("random_vdi:"):
+        g = load("random_vdi")
+        t = "s" + src.split(":")[1]
+        rec = {k[len(t) + 1:]: v for k, v in g.items() if k.startswith(f"{t}_gen_")}
+        return g[f"{t}_counts"], g[f"{t}_segs"], g[f"{t}_grid"], rec, g[f"{t}_aabb"]
+    g = load(src)
+    rec = {k: v for k, v in g.items() if k.startswith("gen_")}
+    return g["counts"], expected_segs(g), g["grid"], rec, g["aabb"]
+
+
+def preview_specs():
+    """The render_preview cases of preview.npz (preview.py:233-268)."""
+    g = load("preview")
+    out = []
+    for t in (str(x) for x in g["tags"]):
+        p = g[f"{t}_params"]
+        counts, segs, grid, gen, aabb = fixture_vdi(str(g[f"{t}_vdi_from"]))
+        out.append(dict(tag=t, counts=counts, segs=segs, grid=grid, gen=gen, aabb=aabb,
+                        d_i=float(p[0]), d_r=float(p[1]), display=(int(p[2]), int(p[3])),
+                        bg=p[4:8], pose=g[f"{t}_pose"], viewport=g[f"{t}_viewport"],
+                        image=g[f"{t}_image"], total=int(g[f"{t}_total_samples"]),
+                        cells=g[f"{t}_cell_samples"]))
+    return out

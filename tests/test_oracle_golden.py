@@ -98,3 +98,70 @@ def test_dvr_bit_exact():
                          s["aabb"], s["width"], s["height"], s["step"], s["lref"],
                          s["early_term"], s["bg"])
         assert np.array_equal(img.view(np.uint64), s["image"].view(np.uint64)), s["tag"]
+
+
+def _low_camera(s):
+    from paper_2206_08660_b200.camera import Camera
+    p = s["pose"]
+    w, h = s["display"]
+    low = (max(1, round(w * s["d_i"])), max(1, round(h * s["d_i"])))
+    return Camera(position=tuple(p[0:3]), orientation=tuple(p[3:7]), fov_y=float(p[7]),
+                  near=float(p[8]), far=float(p[9]), viewport=low)
+
+
+@pytest.mark.parametrize("spec", gio.preview_specs(), ids=lambda s: s["tag"])
+def test_preview_bit_exact(spec):
+    """render_preview (preview.py:49-268): low-res point-sampled render +
+    bilinear upsample; image bits, total and per-cell samples."""
+    s = spec
+    cam = _low_camera(s)
+    gen = s["gen"]
+    img, total, cells = oracle.preview_lowres(
+        s["segs"], s["counts"], gen["gen_pv"], gen["gen_inv_pv"], s["aabb"],
+        cam.inv_proj_view(), np.asarray(cam.position), *cam.viewport, s["grid"],
+        float(gen["gen_pose"][8]), float(gen["gen_pose"][9]), s["d_r"], 0.999, s["bg"])
+    up = oracle.bilinear_upsample(img, *s["display"])
+    assert total == s["total"]
+    assert np.array_equal(cells, s["cells"])
+    assert np.array_equal(up.view(np.uint64), s["image"].view(np.uint64))
+
+
+def _cam_vals(gen):
+    p = gen["gen_pose"]
+    return tuple(float(v) for v in p[:10])
+
+
+def test_encode_vdi_bytes_match_reference():
+    """vdi.py:141-159: the oracle's VDI1 bytes hash to the reference's."""
+    import hashlib
+    g = gio.load("codec")
+    for k, src in enumerate(str(t) for t in g["vdi_tags"]):
+        counts, segs, grid, gen, aabb = gio.fixture_vdi(src)
+        h, w, n_sg, _ = segs.shape
+        raw = oracle.encode_vdi(w, h, n_sg, counts, segs, _cam_vals(gen), aabb, grid)
+        assert len(raw) == int(g[f"v{k}_raw_len"]), src
+        assert hashlib.sha256(raw).hexdigest() == str(g[f"v{k}_raw_sha256"]), src
+        assert oracle.lz4_compress(raw) == g[f"v{k}_lz4"].tobytes(), src
+        assert oracle.lz4_decompress(g[f"v{k}_lz4"].tobytes(), len(raw)) == raw, src
+
+
+def test_lz4_bit_exact():
+    """lz4.py:51-168: compress is the reference's block bit for bit and
+    decompress inverts it."""
+    g = gio.load("codec")
+    for k in range(int(g["n_bytes_cases"])):
+        src = g[f"b{k}_in"].tobytes()
+        exp = g[f"b{k}_lz4"].tobytes()
+        assert oracle.lz4_compress(src) == exp, k
+        assert oracle.lz4_decompress(exp, len(src)) == src, k
+
+
+def test_lz4_decompress_rejects_malformed():
+    """lz4.py:139-166 failure paths."""
+    raw = bytes(range(200)) * 5
+    comp = oracle.lz4_compress(raw)
+    for bad in (comp[:-1], comp + b"\x00", b"\x1f\x00\x00", b"\x10a\x00\x00"):
+        with pytest.raises(ValueError):
+            oracle.lz4_decompress(bad, len(raw))
+    with pytest.raises(ValueError):
+        oracle.lz4_decompress(b"\x01", 0)
