@@ -19,6 +19,10 @@
  *   vdi_preview_launch replaces preview.py:49-205  _preview_kernel (point-sampled
  *                      preview through the AccelGrid)
  *   vdi_bilinear_upsample  replaces preview.py:208-223 bilinear_upsample
+ *   vdi_encode_vdi1    replaces vdi.py:141-159    encode_vdi (VDI1 bytes, on device)
+ *   vdi_lz4_compress   replaces lz4.py:51-114     _compress_kernel (a chunk-parallel
+ *                      LZ4 block, decodable by lz4.py:117-168)
+ *   vdi_validate       replaces vdi.py:116-134    validate_vdi
  *   vdi_segs_to_aos / vdi_segs_from_aos  device layout <-> the reference's
  *                      (H, W, n_sg, 6) f32 array (vdi.py:3-7, 23-24)
  *
@@ -211,6 +215,36 @@ typedef struct VdiPreviewArgs {
 
 #define VDI_PREVIEW_WORKSPACE_BYTES 256
 
+/* VDI1 serialisation (vdi.py:136-159): header | counts u16 | valid
+ * supersegments f32 AoS in list order | grid u32, little endian. */
+#define VDI_VDI1_HEADER_BYTES 160
+typedef struct VdiEncodeArgs {
+  const float* segs;            /* list-SoA */
+  const int32_t* counts;
+  const uint32_t* grid;         /* (gz, gy, gx) */
+  uint8_t* out;                 /* OUT >= vdi_vdi1_max_bytes() device bytes */
+  unsigned long long* out_len;  /* OUT (device) bytes written, may be NULL */
+  void* workspace;              /* >= vdi_encode_workspace_bytes() */
+  size_t workspace_bytes;
+  uint8_t header[VDI_VDI1_HEADER_BYTES]; /* vdi.py:146-149: magic .. grid dims */
+  int32_t width, height, n_sg;
+  int32_t gx, gy, gz;
+  int32_t vdi_band_rows, vdi_band_world, vdi_rows_per_rank;  /* as VdiRenderArgs */
+} VdiEncodeArgs;
+
+/* On-device validate_vdi (vdi.py:116-134). result[0] = min over failing
+ * lists of (row-major list index << 3 | code), code 1 front >= back, 2
+ * overlapping, 3 depth outside [-1, 1], 4 not premultiplied (the first
+ * failing check of that list, in the reference's order), or ~0 if none;
+ * result[1] = lists whose count is outside [0, n_sg]. */
+typedef struct VdiValidateArgs {
+  const float* segs;
+  const int32_t* counts;
+  unsigned long long* result;   /* OUT (device) [2] */
+  int32_t width, height, n_sg;
+  int32_t vdi_band_rows, vdi_band_world, vdi_rows_per_rank;
+} VdiValidateArgs;
+
 const char* vdi_last_error(void);
 int vdi_abi_version(void);
 
@@ -227,6 +261,22 @@ int vdi_preview_launch(const VdiPreviewArgs* args, vdi_stream_t stream);
 int vdi_bilinear_upsample(const double* src, int32_t w, int32_t h, double* dst,
                           int32_t out_w, int32_t out_h, int32_t channels,
                           vdi_stream_t stream);
+
+size_t vdi_vdi1_max_bytes(int32_t width, int32_t height, int32_t n_sg, int32_t gx, int32_t gy,
+                          int32_t gz);
+size_t vdi_encode_workspace_bytes(int32_t width, int32_t height);
+int vdi_encode_vdi1(const VdiEncodeArgs* args, vdi_stream_t stream);
+
+/* LZ4 block compression of src[0, n) with n = *n_dev when n_dev is not NULL
+ * (a device length, e.g. VdiEncodeArgs.out_len), else n = n_max. dst holds
+ * vdi_lz4_max_bytes(n_max); *out_len (device) receives the block length. */
+size_t vdi_lz4_max_bytes(size_t n);
+size_t vdi_lz4_workspace_bytes(size_t n_max);
+int vdi_lz4_compress(const uint8_t* src, size_t n_max, const unsigned long long* n_dev,
+                     uint8_t* dst, unsigned long long* out_len, void* workspace,
+                     size_t workspace_bytes, vdi_stream_t stream);
+
+int vdi_validate(const VdiValidateArgs* args, vdi_stream_t stream);
 
 /* Alg. 2 search over a batch of independent queries (raycast.py:79-156).
  * fronts/backs: (n_queries, n_max) f32, counts: (n_queries,), d_entry /

@@ -25,6 +25,7 @@ _LAZY = {
     "render_preview": "preview", "PreviewParams": "preview", "PreviewStats": "preview",
     "PiController": "preview", "pi_update": "preview", "samples_in_cell": "preview",
     "bilinear_upsample": "preview",
+    "encode_vdi": "codec", "compress": "codec", "compress_vdi": "codec",
 }
 
 

@@ -85,11 +85,32 @@ class VdiPreviewArgs(ctypes.Structure):
 
 
 PREVIEW_WORKSPACE_BYTES = 256
+VDI1_HEADER_BYTES = 160
+
+
+class VdiEncodeArgs(ctypes.Structure):
+    _fields_ = [
+        ("segs", _P), ("counts", _P), ("grid", _P), ("out", _P), ("out_len", _P),
+        ("workspace", _P), ("workspace_bytes", ctypes.c_size_t),
+        ("header", ctypes.c_uint8 * VDI1_HEADER_BYTES),
+        ("width", _I), ("height", _I), ("n_sg", _I), ("gx", _I), ("gy", _I), ("gz", _I),
+        ("vdi_band_rows", _I), ("vdi_band_world", _I), ("vdi_rows_per_rank", _I),
+    ]
+
+
+class VdiValidateArgs(ctypes.Structure):
+    _fields_ = [
+        ("segs", _P), ("counts", _P), ("result", _P),
+        ("width", _I), ("height", _I), ("n_sg", _I),
+        ("vdi_band_rows", _I), ("vdi_band_world", _I), ("vdi_rows_per_rank", _I),
+    ]
 
 EXPORTS = ["vdi_last_error", "vdi_abi_version", "vdi_gen_workspace_bytes",
            "vdi_gen_workspace_min_bytes", "vdi_gen_launch",
            "vdi_grid_launch", "vdi_render_launch", "vdi_dvr_launch",
-           "vdi_preview_launch", "vdi_bilinear_upsample", "vdi_find_first_batch",
+           "vdi_preview_launch", "vdi_bilinear_upsample", "vdi_vdi1_max_bytes",
+           "vdi_encode_workspace_bytes", "vdi_encode_vdi1", "vdi_lz4_max_bytes",
+           "vdi_lz4_workspace_bytes", "vdi_lz4_compress", "vdi_validate", "vdi_find_first_batch",
            "vdi_volume_brick_max", "vdi_selftest_arith", "vdi_segs_to_aos",
            "vdi_segs_from_aos", "vdi_volume_cells_bytes", "vdi_volume_cells"]
 
@@ -120,6 +141,17 @@ def load():
     L.vdi_render_launch.argtypes = [ctypes.POINTER(VdiRenderArgs), _P]
     L.vdi_dvr_launch.argtypes = [ctypes.POINTER(VdiDvrArgs), _P]
     L.vdi_preview_launch.argtypes = [ctypes.POINTER(VdiPreviewArgs), _P]
+    L.vdi_vdi1_max_bytes.argtypes = [_I, _I, _I, _I, _I, _I]
+    L.vdi_vdi1_max_bytes.restype = ctypes.c_size_t
+    L.vdi_encode_workspace_bytes.argtypes = [_I, _I]
+    L.vdi_encode_workspace_bytes.restype = ctypes.c_size_t
+    L.vdi_encode_vdi1.argtypes = [ctypes.POINTER(VdiEncodeArgs), _P]
+    L.vdi_lz4_max_bytes.argtypes = [ctypes.c_size_t]
+    L.vdi_lz4_max_bytes.restype = ctypes.c_size_t
+    L.vdi_lz4_workspace_bytes.argtypes = [ctypes.c_size_t]
+    L.vdi_lz4_workspace_bytes.restype = ctypes.c_size_t
+    L.vdi_lz4_compress.argtypes = [_P, ctypes.c_size_t, _P, _P, _P, _P, ctypes.c_size_t, _P]
+    L.vdi_validate.argtypes = [ctypes.POINTER(VdiValidateArgs), _P]
     L.vdi_bilinear_upsample.argtypes = [_P, _I, _I, _P, _I, _I, _I, _P]
     L.vdi_find_first_batch.argtypes = [_P, _P, _P, _I, _P, _P, _P, _P, _P, ctypes.c_int64, _P]
     L.vdi_volume_brick_max.argtypes = [_P, _I, _I, _I, _I, _I, _P, _P]
@@ -133,8 +165,13 @@ def load():
     L.vdi_segs_to_aos.argtypes = [_P, _P, ctypes.c_int64, _I, _P]
     L.vdi_segs_from_aos.argtypes = [_P, _P, ctypes.c_int64, _I, _P]
     for name in ("vdi_gen_launch", "vdi_grid_launch", "vdi_render_launch", "vdi_dvr_launch",
-                 "vdi_preview_launch", "vdi_bilinear_upsample",
-           "vdi_preview_launch", "vdi_bilinear_upsample", "vdi_dvr_launch",
+                 "vdi_preview_launch", "vdi_bilinear_upsample", "vdi_encode_vdi1",
+                 "vdi_lz4_compress", "vdi_validate", "vdi_vdi1_max_bytes",
+           "vdi_encode_workspace_bytes", "vdi_encode_vdi1", "vdi_lz4_max_bytes",
+           "vdi_lz4_workspace_bytes", "vdi_lz4_compress", "vdi_validate",
+           "vdi_preview_launch", "vdi_bilinear_upsample", "vdi_vdi1_max_bytes",
+           "vdi_encode_workspace_bytes", "vdi_encode_vdi1", "vdi_lz4_max_bytes",
+           "vdi_lz4_workspace_bytes", "vdi_lz4_compress", "vdi_validate", "vdi_dvr_launch",
                  "vdi_find_first_batch", "vdi_segs_to_aos", "vdi_segs_from_aos"):
         getattr(L, name).restype = ctypes.c_int
     if L.vdi_abi_version() != 1:

@@ -20,7 +20,7 @@ CSRC = os.path.join(PKG, "csrc")
 LIBDIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIBDIR, "libvdi_b200.so")
 SOURCES = ["vdi_capi.cu", "vdi_gen.cu", "vdi_grid.cu", "vdi_render.cu", "vdi_volume.cu",
-           "vdi_dvr.cu", "vdi_preview.cu"]
+           "vdi_dvr.cu", "vdi_preview.cu", "vdi_codec.cu"]
 HEADERS = ["vdi_common.cuh", "vdi_sample.cuh", "vdi_search.cuh", "vdi_internal.h", "../../include/vdi_b200.h"]
 
 NVCC_FLAGS = [

@@ -118,6 +118,50 @@ int vdi_bilinear_upsample(const double* src, int32_t w, int32_t h, double* dst, 
                                 static_cast<cudaStream_t>(stream));
 }
 
+size_t vdi_vdi1_max_bytes(int32_t width, int32_t height, int32_t n_sg, int32_t gx, int32_t gy,
+                          int32_t gz) {
+  if (width < 0 || height < 0 || n_sg < 0 || gx < 0 || gy < 0 || gz < 0) return 0;
+  const size_t n = (size_t)width * (size_t)height;
+  return VDI_VDI1_HEADER_BYTES + 2 * n + 24 * n * (size_t)n_sg +
+         4 * (size_t)gx * (size_t)gy * (size_t)gz;
+}
+
+size_t vdi_encode_workspace_bytes(int32_t width, int32_t height) {
+  if (width < 0 || height < 0) return 0;
+  return vdi::encode_workspace_bytes(width, height);
+}
+
+int vdi_encode_vdi1(const VdiEncodeArgs* a, vdi_stream_t stream) {
+  if (!a) return set_error(VDI_EINVAL, "null args");
+  if (!a->segs || !a->counts || !a->grid || !a->out || !a->workspace)
+    return set_error(VDI_EINVAL, "null device pointer");
+  if (a->width < 1 || a->height < 1 || a->n_sg < 1 || a->gx < 1 || a->gy < 1 || a->gz < 1)
+    return set_error(VDI_EINVAL, "bad sizes");
+  if ((long long)a->width * a->height * (long long)a->n_sg > (1ll << 40))
+    return set_error(VDI_EINVAL, "VDI too large");
+  return vdi::encode_vdi1(a, static_cast<cudaStream_t>(stream));
+}
+
+size_t vdi_lz4_max_bytes(size_t n) { return n + n / 255 + 16; }
+
+size_t vdi_lz4_workspace_bytes(size_t n_max) { return vdi::lz4_workspace_bytes(n_max); }
+
+int vdi_lz4_compress(const uint8_t* src, size_t n_max, const unsigned long long* n_dev,
+                     uint8_t* dst, unsigned long long* out_len, void* workspace,
+                     size_t workspace_bytes, vdi_stream_t stream) {
+  if ((!src && n_max) || !dst || !out_len || !workspace)
+    return set_error(VDI_EINVAL, "null device pointer");
+  return vdi::lz4_compress(src, n_max, n_dev, dst, out_len, workspace, workspace_bytes,
+                           static_cast<cudaStream_t>(stream));
+}
+
+int vdi_validate(const VdiValidateArgs* a, vdi_stream_t stream) {
+  if (!a) return set_error(VDI_EINVAL, "null args");
+  if (!a->segs || !a->counts || !a->result) return set_error(VDI_EINVAL, "null device pointer");
+  if (a->width < 1 || a->height < 1 || a->n_sg < 1) return set_error(VDI_EINVAL, "bad sizes");
+  return vdi::validate_vdi(a, static_cast<cudaStream_t>(stream));
+}
+
 int vdi_find_first_batch(const float* fronts, const float* backs, const int32_t* counts,
                          int32_t n_max, const double* d_entry, const double* d_exit,
                          const int32_t* seeds, int32_t* out_index, int32_t* out_seed,

@@ -1,0 +1,644 @@
+// vdi_codec.cu -- the VDI wire path on sm_100a: VDI1 packing (vdi.py:141-159
+// encode_vdi) and an LZ4 block compressor (lz4.py block format, decodable by
+// lz4.py:117-168) that run on the device-resident VDI, so the server's
+// generate_fn -> compress_fn path (proto.py:283-287, 328-334) never stages
+// the (up to GiB-sized) raw VDI on the host.
+//
+// VDI1 packing. The byte stream is header (160 B, built on the host from the
+// camera and AABB) | counts as u16 | valid supersegments as AoS f32 in list
+// order | grid as u32. The packed-segment offsets are an exclusive scan of
+// the counts: a per-block scan (1024 lists) + a one-block scan of the block
+// totals; the scatter then walks each block's contiguous output range word
+// by word (coalesced stores), locating the source list by binary search in
+// the block's shared prefix array.
+//
+// LZ4. The reference's compressor is one serial greedy parse with a 64 Ki
+// hash table. Here the input is cut into 32 KiB chunks, one warp each; a warp
+// runs the same greedy single-probe parse over its chunk (4 Ki-entry table
+// in shared memory) 32 positions at a time: lane j hashes position i + j,
+// takes its candidate from the nearest lower lane with the same hash
+// (__match_any_sync) or else the table, and the lowest lane with a verified
+// 4-byte match wins -- exactly the serial parse's decision, because every
+// position before the winner would have been inserted and missed. Match
+// extension compares 32 bytes per step. The chunks' trailing literals are
+// carried into the next chunk's first sequence (a literal-only sequence may
+// only end the block), so a one-block scan composes the carries and sizes,
+// and a final pass writes each chunk's sequences at its offset. The output is
+// a valid LZ4 block (matches start >= 12 bytes before the end and end >= 5
+// bytes before it); its bytes differ from the reference's serial parse, but
+// it decodes to the same input -- the property the transport relies on
+// (test_acceptance.py A6: decompress(compress(raw)) == raw).
+#include <cstdint>
+
+#include "vdi_common.cuh"
+#include "vdi_internal.h"
+
+namespace vdi {
+
+// p[0] = *src (or v0 when src is null), p[1] = v1 unless v1 == ~0.
+__global__ void set_u64_kernel(unsigned long long* p, const unsigned long long* src,
+                               unsigned long long v0, unsigned long long v1) {
+  p[0] = src ? *src : v0;
+  if (v1 != ~0ull) p[1] = v1;
+}
+
+// ------------------------------------------------------------ VDI1 packing
+
+constexpr int kEncBlock = 1024;
+constexpr int kVdi1Header = 160;  // vdi.py:136-139: 20 + 80 + 48 + 12
+
+static size_t enc_blocks(long long n_lists) { return (size_t)((n_lists + kEncBlock - 1) / kEncBlock); }
+
+// Block b: counts -> u16 stream, and the block's count total.
+__global__ void enc_counts_kernel(const VdiEncodeArgs a, unsigned long long* block_sums) {
+  __shared__ unsigned long long s_sum[kEncBlock / 32];
+  const long long n = (long long)a.width * a.height;
+  const long long l = (long long)blockIdx.x * kEncBlock + threadIdx.x;
+  int cnt = 0;
+  if (l < n) {
+    const int r = (int)(l / a.width), x = (int)(l - (long long)r * a.width);
+    const long long li =
+        (long long)vdi_storage_row(r, a.vdi_band_rows, a.vdi_band_world, a.vdi_rows_per_rank) *
+            a.width + x;
+    cnt = a.counts[li];
+    const unsigned short v = (unsigned short)cnt;  // vdi.py:148 astype("<u2")
+    a.out[kVdi1Header + 2 * l] = (uint8_t)(v & 0xff);
+    a.out[kVdi1Header + 2 * l + 1] = (uint8_t)(v >> 8);
+  }
+  unsigned long long s = (unsigned long long)cnt;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) s_sum[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    unsigned long long t = s_sum[threadIdx.x];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (threadIdx.x == 0) block_sums[blockIdx.x] = t;
+  }
+}
+
+// One block: exclusive scan of the block totals (in place), the total, the
+// header bytes and out_len.
+__global__ void enc_scan_kernel(const VdiEncodeArgs a, unsigned long long* block_sums, int nb,
+                                unsigned long long* total_out) {
+  __shared__ unsigned long long s_part[1024];
+  const int t = threadIdx.x;
+  const int per = (nb + 1023) / 1024;
+  const int b0 = t * per, b1 = b0 + per < nb ? b0 + per : nb;
+  unsigned long long sum = 0;
+  for (int b = b0; b < b1; ++b) sum += block_sums[b];
+  s_part[t] = sum;
+  __syncthreads();
+  for (int off = 1; off < 1024; off <<= 1) {  // inclusive Hillis-Steele
+    const unsigned long long v = t >= off ? s_part[t - off] : 0ull;
+    __syncthreads();
+    s_part[t] += v;
+    __syncthreads();
+  }
+  unsigned long long run = t > 0 ? s_part[t - 1] : 0ull;
+  for (int b = b0; b < b1; ++b) {
+    const unsigned long long v = block_sums[b];
+    block_sums[b] = run;
+    run += v;
+  }
+  if (t == 1023) {
+    const unsigned long long total = s_part[1023];
+    *total_out = total;
+    const unsigned long long n = (unsigned long long)a.width * a.height;
+    if (a.out_len)
+      *a.out_len = kVdi1Header + 2ull * n + 24ull * total +
+                   4ull * (unsigned long long)a.gx * a.gy * a.gz;
+  }
+  for (int i = t; i < kVdi1Header; i += blockDim.x) a.out[i] = a.header[i];
+}
+
+__device__ __forceinline__ void store_word(uint8_t* p, uint32_t w, bool aligned) {
+  if (aligned) {
+    *reinterpret_cast<uint32_t*>(p) = w;
+  } else {
+    p[0] = (uint8_t)w;
+    p[1] = (uint8_t)(w >> 8);
+    p[2] = (uint8_t)(w >> 16);
+    p[3] = (uint8_t)(w >> 24);
+  }
+}
+
+// Block b: its lists' valid supersegments, [front, back, r, g, b, a] each,
+// into the contiguous range starting at its scanned offset.
+__global__ void enc_segs_kernel(const VdiEncodeArgs a, const unsigned long long* block_off) {
+  __shared__ int s_pre[kEncBlock + 1];
+  __shared__ long long s_src[kEncBlock];
+  __shared__ int s_tmp[kEncBlock / 32];
+  const long long n = (long long)a.width * a.height;
+  const long long l = (long long)blockIdx.x * kEncBlock + threadIdx.x;
+  int cnt = 0;
+  long long li = 0;
+  if (l < n) {
+    const int r = (int)(l / a.width), x = (int)(l - (long long)r * a.width);
+    li = (long long)vdi_storage_row(r, a.vdi_band_rows, a.vdi_band_world, a.vdi_rows_per_rank) *
+             a.width + x;
+    cnt = a.counts[li];
+  }
+  s_src[threadIdx.x] = li;
+  // block exclusive scan of cnt
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int v = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int u = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += u;
+  }
+  if (lane == 31) s_tmp[wid] = v;
+  __syncthreads();
+  if (wid == 0) {
+    int w = s_tmp[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int u = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += u;
+    }
+    s_tmp[lane] = w;
+  }
+  __syncthreads();
+  const int incl = v + (wid > 0 ? s_tmp[wid - 1] : 0);
+  s_pre[threadIdx.x + 1] = incl;
+  if (threadIdx.x == 0) s_pre[0] = 0;
+  __syncthreads();
+  const int bt = s_pre[kEncBlock];
+  const unsigned long long base_byte =
+      kVdi1Header + 2ull * (unsigned long long)n + 24ull * block_off[blockIdx.x];
+  const bool aligned = ((reinterpret_cast<uintptr_t>(a.out) + base_byte) & 3u) == 0;
+  uint8_t* dst = a.out + base_byte;
+  const int stride = list_stride(a.n_sg);
+  const long long words = 6ll * bt;
+  for (long long k = threadIdx.x; k < words; k += blockDim.x) {
+    const int s = (int)(k / 6), ch = (int)(k - 6ll * s);
+    int lo = 0, hi = kEncBlock - 1;  // list j with s_pre[j] <= s < s_pre[j + 1]
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (s_pre[mid] <= s) lo = mid;
+      else hi = mid - 1;
+    }
+    const int j = s - s_pre[lo];
+    const float* ls = a.segs + s_src[lo] * (long long)stride;
+    float f;
+    if (ch == 0) f = ls[front_off(a.n_sg) + j];
+    else if (ch == 1) f = ls[back_off(a.n_sg) + j];
+    else f = ls[4 * j + (ch - 2)];
+    store_word(dst + 4 * k, __float_as_uint(f), aligned);
+  }
+}
+
+__global__ void enc_grid_kernel(const VdiEncodeArgs a, const unsigned long long* total) {
+  const unsigned long long n = (unsigned long long)a.width * a.height;
+  const unsigned long long base = kVdi1Header + 2ull * n + 24ull * (*total);
+  const bool aligned = ((reinterpret_cast<uintptr_t>(a.out) + base) & 3u) == 0;
+  const long long g = (long long)a.gx * a.gy * a.gz;
+  for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < g;
+       k += (long long)gridDim.x * blockDim.x)
+    store_word(a.out + base + 4 * k, a.grid[k], aligned);
+}
+
+size_t encode_workspace_bytes(int width, int height) {
+  return 256 + sizeof(unsigned long long) * enc_blocks((long long)width * height);
+}
+
+int encode_vdi1(const VdiEncodeArgs* args, cudaStream_t stream) {
+  const VdiEncodeArgs& a = *args;
+  const long long n = (long long)a.width * a.height;
+  const int nb = (int)enc_blocks(n);
+  if (a.workspace_bytes < encode_workspace_bytes(a.width, a.height))
+    return set_error(VDI_EINVAL, "encode workspace too small");
+  unsigned long long* total = reinterpret_cast<unsigned long long*>(a.workspace);
+  unsigned long long* bsum = total + 32;
+  VdiEncodeArgs c = a;
+  if (c.vdi_band_rows <= 0) c.vdi_band_rows = 16;
+  if (c.vdi_band_world <= 0) c.vdi_band_world = 1;
+  enc_counts_kernel<<<nb, kEncBlock, 0, stream>>>(c, bsum);
+  enc_scan_kernel<<<1, 1024, 0, stream>>>(c, bsum, nb, total);
+  enc_segs_kernel<<<nb, kEncBlock, 0, stream>>>(c, bsum);
+  const long long g = (long long)a.gx * a.gy * a.gz;
+  long long gb = (g + 255) / 256;
+  if (gb > 4096) gb = 4096;
+  enc_grid_kernel<<<(unsigned)(gb < 1 ? 1 : gb), 256, 0, stream>>>(c, total);
+  const cudaError_t err = cudaGetLastError();
+  if (err != cudaSuccess) return set_error(VDI_ELAUNCH, "encode launch: %s", cudaGetErrorString(err));
+  return VDI_OK;
+}
+
+// -------------------------------------------------------------------- LZ4
+
+constexpr int kLz4Chunk = 32768;
+constexpr int kLz4HashLog = 13;
+constexpr int kLz4MaxSeq = kLz4Chunk / 4 + 1;
+constexpr int kLz4Warps = 4;
+constexpr unsigned short kNoPos = 0xffffu;
+
+struct ChunkSum {
+  unsigned int nseq;   // sequences with a match
+  unsigned int lead;   // literals before the first match (own bytes only)
+  unsigned int trail;  // literals after the last match (carried forward)
+  unsigned int len;    // chunk bytes
+  unsigned long long rest;  // encoded bytes except the first sequence's literal field + literals
+};
+
+struct ChunkPlan {
+  unsigned long long off;  // output offset of the chunk's first byte
+  unsigned int cin;        // literals carried in from earlier chunks
+  unsigned int pad;
+};
+
+struct Lz4Ws {
+  unsigned long long* n_dev;  // input length actually used
+  ChunkSum* sums;
+  ChunkPlan* plans;
+  uint2* seqs;                // per chunk kLz4MaxSeq x (lit | off << 16, mlen)
+  unsigned long long* final_;  // [0] offset of the final sequence, [1] its literal count
+};
+
+__device__ __forceinline__ unsigned ext_len(unsigned long long L) {  // bytes after the nibble
+  return L >= 15 ? (unsigned)((L - 15) / 255 + 1) : 0u;
+}
+
+__device__ __forceinline__ uint32_t rd32(const uint8_t* s, long long p) {
+  return (uint32_t)s[p] | ((uint32_t)s[p + 1] << 8) | ((uint32_t)s[p + 2] << 16) |
+         ((uint32_t)s[p + 3] << 24);
+}
+
+__device__ __forceinline__ uint32_t lz4_hash(uint32_t v) {
+  return (v * 2654435761u) >> (32 - kLz4HashLog);
+}
+
+// One warp per chunk: greedy parse -> sequences + chunk summary.
+__global__ void __launch_bounds__(kLz4Warps * 32) lz4_parse_kernel(const uint8_t* __restrict__ src,
+                                                                 Lz4Ws ws, long long n_chunks) {
+  extern __shared__ unsigned short s_tab[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  unsigned short* tab = s_tab + (size_t)wib * (1 << kLz4HashLog);
+  const long long n = (long long)*ws.n_dev;
+  const long long mlimit_g = n - 12;  // lz4.py:17 MFLIMIT
+  for (long long ch = (long long)blockIdx.x * kLz4Warps + wib; ch < n_chunks;
+       ch += (long long)gridDim.x * kLz4Warps) {
+    const long long cs = ch * kLz4Chunk;
+    if (cs >= n) {
+      if (lane == 0) ws.sums[ch] = ChunkSum{0u, 0u, 0u, 0u, 0ull};
+      continue;
+    }
+    const long long ce = cs + kLz4Chunk < n ? cs + kLz4Chunk : n;
+    const long long mend = ce < n - 5 ? ce : n - 5;  // matches end <= mend (LAST_LITERALS)
+    // match starts < mlimit: room for a 4-byte match inside the chunk
+    const long long mlimit = mend - 3 < mlimit_g ? mend - 3 : mlimit_g;
+    for (int k = lane; k < (1 << kLz4HashLog); k += 32) tab[k] = kNoPos;
+    __syncwarp();
+    // Positions are stored relative to tb = cs - chunk, so the table also
+    // holds the previous chunk: warm it with every position of that chunk
+    // (last writer of a hash wins, as in a serial pass). Matches may then
+    // reach back into it (offsets stay < 65536; the decoder has those bytes).
+    const long long tb = cs - kLz4Chunk;
+    if (cs > 0) {
+      for (long long q0 = tb; q0 < cs; q0 += 32) {
+        const long long q = q0 + lane;
+        const bool ok = q + 3 < n;
+        const uint32_t hq = lz4_hash(ok ? rd32(src, q) : 0u);
+        const unsigned pe = __match_any_sync(0xffffffffu, ok ? hq : (0x10000u + lane));
+        if (ok && !(pe >> lane >> 1)) tab[hq] = (unsigned short)(q - tb);
+        __syncwarp();
+      }
+    }
+    uint2* seq = ws.seqs + ch * kLz4MaxSeq;
+    unsigned nseq = 0, lead = 0;
+    unsigned long long rest = 0;
+    long long i = cs, anchor = cs;
+    while (i < mlimit) {
+      const long long p = i + lane;
+      const bool valid = p < mlimit;
+      const uint32_t v = valid ? rd32(src, p) : 0u;
+      const uint32_t h = lz4_hash(v);
+      const unsigned key = valid ? h : (0x10000u + lane);
+      const unsigned peers = __match_any_sync(0xffffffffu, key);
+      const unsigned lt = (1u << lane) - 1u;
+      const unsigned lower = peers & lt;
+      long long cand = -1;
+      if (valid) {
+        if (lower) {
+          cand = i + (31 - __clz(lower));
+        } else {
+          const unsigned short t = tab[h];
+          if (t != kNoPos) cand = (cs > 0 ? tb : cs) + t;
+        }
+      }
+      const bool match = cand >= 0 && rd32(src, cand) == v;
+      const unsigned mm = __ballot_sync(0xffffffffu, match);
+      const int w = mm ? __ffs(mm) - 1 : 31;
+      const unsigned upto = w == 31 ? 0xffffffffu : ((2u << w) - 1u);
+      // every position up to the winner (all, without one) was inserted
+      // (lz4.py:62); the last writer of a hash wins
+      __syncwarp();
+      if (valid && ((1u << lane) & upto) && !(peers & upto & ~lt & ~(1u << lane)))
+        tab[h] = (unsigned short)(p - (cs > 0 ? tb : cs));
+      __syncwarp();
+      if (!mm) {
+        i += 32;
+        continue;
+      }
+      const long long pw = i + w;
+      const long long cw = __shfl_sync(0xffffffffu, cand, w);
+      // extend (lz4.py:66-69), 32 bytes per step
+      long long mlen = 4;
+      const long long mmax = mend - pw;
+      while (true) {
+        const long long k = mlen + lane;
+        const bool stop = k >= mmax || src[cw + k] != src[pw + k];
+        const unsigned sb = __ballot_sync(0xffffffffu, stop);
+        if (sb) {
+          mlen += __ffs(sb) - 1;
+          break;
+        }
+        mlen += 32;
+      }
+      const unsigned lit = (unsigned)(pw - anchor);
+      if (lane == 0) {
+        seq[nseq] = make_uint2(lit | ((unsigned)(pw - cw) << 16), (unsigned)mlen);
+        rest += 3ull + ext_len((unsigned long long)(mlen - 4));
+        if (nseq == 0) lead = lit;
+        else rest += ext_len(lit) + (unsigned long long)lit;
+      }
+      nseq += 1;
+      i = pw + mlen;
+      anchor = i;
+      if (i < mlimit && lane == 0)
+        tab[lz4_hash(rd32(src, i - 2))] = (unsigned short)(i - 2 - (cs > 0 ? tb : cs));
+      __syncwarp();
+    }
+    if (lane == 0)
+      ws.sums[ch] = ChunkSum{nseq, lead, (unsigned)(ce - anchor), (unsigned)(ce - cs), rest};
+  }
+}
+
+// One block: compose the chunks' carry/size functions, assign offsets.
+// Chunk with matches: size(cin) = rest + ext(cin + lead) + cin + lead,
+// cout = trail. Chunk without: size 0, cout = cin + len.
+__global__ void lz4_scan_kernel(Lz4Ws ws, long long n_chunks, unsigned long long* out_len) {
+  __shared__ int s_any[1024];
+  __shared__ unsigned long long s_pre[1024], s_lead[1024], s_after[1024], s_cout[1024],
+      s_lenall[1024];
+  const int t = threadIdx.x;
+  const long long per = (n_chunks + 1023) / 1024;
+  const long long c0 = t * per, c1 = c0 + per < n_chunks ? c0 + per : n_chunks;
+  // range summary
+  int any = 0;
+  unsigned long long pre = 0, lead = 0, after = 0, cout = 0, lenall = 0;
+  for (long long c = c0; c < c1; ++c) {
+    const ChunkSum s = ws.sums[c];
+    lenall += s.len;
+    if (s.nseq == 0) {
+      if (!any) pre += s.len;
+      else cout += s.len;
+      continue;
+    }
+    if (!any) {
+      any = 1;
+      lead = s.lead;
+      after = s.rest;  // first chunk's literal part is added when cin is known
+    } else {
+      const unsigned long long L = cout + s.lead;
+      after += s.rest + ext_len(L) + L;
+    }
+    cout = s.trail;
+  }
+  s_any[t] = any;
+  s_pre[t] = pre;
+  s_lead[t] = lead;
+  s_after[t] = after;
+  s_cout[t] = cout;
+  s_lenall[t] = lenall;
+  __syncthreads();
+  unsigned long long* s_cin = s_pre;   // reused: thread k's carry-in ...
+  unsigned long long* s_off = s_lead;  // ... and output offset
+  if (t == 0) {
+    unsigned long long cin = 0, off = 0;
+    for (int k = 0; k < 1024; ++k) {
+      const unsigned long long pre_k = s_pre[k], lead_k = s_lead[k];
+      s_cin[k] = cin;
+      s_off[k] = off;
+      if (s_any[k]) {
+        const unsigned long long L = cin + pre_k + lead_k;
+        off += s_after[k] + ext_len(L) + L;
+        cin = s_cout[k];
+      } else {
+        cin += s_lenall[k];
+      }
+    }
+    const unsigned long long n = *ws.n_dev;
+    ws.final_[0] = off;
+    ws.final_[1] = cin;
+    *out_len = n == 0 ? 0ull : off + 1ull + ext_len(cin) + cin;
+  }
+  __syncthreads();
+  unsigned long long cin = s_cin[t], off = s_off[t];
+  for (long long c = c0; c < c1; ++c) {
+    const ChunkSum s = ws.sums[c];
+    ws.plans[c] = ChunkPlan{off, (unsigned)cin, 0u};
+    if (s.nseq == 0) {
+      cin += s.len;
+    } else {
+      const unsigned long long L = cin + s.lead;
+      off += s.rest + ext_len(L) + L;
+      cin = s.trail;
+    }
+  }
+}
+
+// Warp-parallel sequence writer: token, literal-length extension, literals
+// [lsrc, lsrc + L), then (unless final) offset + match-length extension.
+__device__ __forceinline__ unsigned long long put_seq(uint8_t* __restrict__ dst,
+                                                      unsigned long long o,
+                                                      const uint8_t* __restrict__ src,
+                                                      long long lsrc, unsigned long long L,
+                                                      bool final_, unsigned off, long long mlen,
+                                                      int lane) {
+  const unsigned long long lcode = L >= 15 ? 15 : L;
+  const long long mc = mlen - 4;
+  const unsigned long long mcode = final_ ? 0 : (mc >= 15 ? 15 : (unsigned long long)mc);
+  if (lane == 0) dst[o] = (uint8_t)((lcode << 4) | mcode);
+  o += 1;
+  const unsigned el = ext_len(L);
+  for (unsigned k = lane; k < el; k += 32)
+    dst[o + k] = k + 1 < el ? 255 : (uint8_t)((L - 15) - 255ull * (el - 1));
+  o += el;
+  for (unsigned long long k = lane; k < L; k += 32) dst[o + k] = src[lsrc + k];
+  o += L;
+  if (final_) return o;
+  if (lane == 0) {
+    dst[o] = (uint8_t)(off & 0xff);
+    dst[o + 1] = (uint8_t)(off >> 8);
+  }
+  o += 2;
+  const unsigned em = ext_len((unsigned long long)mc);
+  for (unsigned k = lane; k < em; k += 32)
+    dst[o + k] = k + 1 < em ? 255 : (uint8_t)((mc - 15) - 255ll * (em - 1));
+  return o + em;
+}
+
+__global__ void __launch_bounds__(kLz4Warps * 32) lz4_emit_kernel(const uint8_t* __restrict__ src,
+                                                                uint8_t* __restrict__ dst,
+                                                                Lz4Ws ws, long long n_chunks) {
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const long long n = (long long)*ws.n_dev;
+  for (long long ch = (long long)blockIdx.x * kLz4Warps + wib; ch <= n_chunks;
+       ch += (long long)gridDim.x * kLz4Warps) {
+    if (ch == n_chunks) {  // the literal-only final sequence (lz4.py:102-113)
+      if (n > 0) {
+        const unsigned long long L = ws.final_[1];
+        put_seq(dst, ws.final_[0], src, n - (long long)L, L, true, 0, 0, lane);
+      }
+      continue;
+    }
+    const ChunkSum s = ws.sums[ch];
+    if (s.nseq == 0) continue;
+    const ChunkPlan pl = ws.plans[ch];
+    const long long cs = ch * kLz4Chunk;
+    const uint2* seq = ws.seqs + ch * kLz4MaxSeq;
+    unsigned long long o = pl.off;
+    long long pos = cs - (long long)pl.cin;  // literal source
+    for (unsigned k = 0; k < s.nseq; ++k) {
+      const uint2 q = seq[k];
+      const unsigned lit = q.x & 0xffffu, off = q.x >> 16;
+      const unsigned long long L = k == 0 ? (unsigned long long)pl.cin + lit : lit;
+      o = put_seq(dst, o, src, pos, L, false, off, (long long)q.y, lane);
+      pos += (long long)L + q.y;
+    }
+  }
+}
+
+static long long lz4_chunks(size_t n) { return (long long)((n + kLz4Chunk - 1) / kLz4Chunk); }
+
+static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+size_t lz4_workspace_bytes(size_t n_max) {
+  const long long nc = lz4_chunks(n_max);
+  return 256 + align256(sizeof(ChunkSum) * (size_t)(nc + 1)) +
+         align256(sizeof(ChunkPlan) * (size_t)(nc + 1)) +
+         sizeof(uint2) * (size_t)kLz4MaxSeq * (size_t)(nc + 1);
+}
+
+int lz4_compress(const uint8_t* src, size_t n_max, const unsigned long long* n_dev, uint8_t* dst,
+                 unsigned long long* out_len, void* workspace, size_t ws_bytes,
+                 cudaStream_t stream) {
+  if (ws_bytes < lz4_workspace_bytes(n_max)) return set_error(VDI_EINVAL, "lz4 workspace too small");
+  char* w = static_cast<char*>(workspace);
+  Lz4Ws ws;
+  ws.n_dev = reinterpret_cast<unsigned long long*>(w);
+  ws.final_ = ws.n_dev + 2;
+  size_t off = 256;
+  const long long nc = lz4_chunks(n_max);
+  ws.sums = reinterpret_cast<ChunkSum*>(w + off);
+  off += align256(sizeof(ChunkSum) * (size_t)(nc + 1));
+  ws.plans = reinterpret_cast<ChunkPlan*>(w + off);
+  off += align256(sizeof(ChunkPlan) * (size_t)(nc + 1));
+  ws.seqs = reinterpret_cast<uint2*>(w + off);
+  set_u64_kernel<<<1, 1, 0, stream>>>(ws.n_dev, n_dev, n_max, ~0ull);
+  cudaError_t err;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const long long nch = nc > 0 ? nc : 0;
+  if (nch > 0) {
+    long long b = (nch + kLz4Warps - 1) / kLz4Warps;
+    if (b > (long long)sms * 16) b = (long long)sms * 16;
+    const size_t smem = sizeof(unsigned short) * kLz4Warps * ((size_t)1 << kLz4HashLog);
+    err = cudaFuncSetAttribute(lz4_parse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)smem);
+    if (err != cudaSuccess) return set_error(VDI_ELAUNCH, "lz4 smem: %s", cudaGetErrorString(err));
+    lz4_parse_kernel<<<(unsigned)b, kLz4Warps * 32, smem, stream>>>(src, ws, nch);
+  }
+  lz4_scan_kernel<<<1, 1024, 0, stream>>>(ws, nch, out_len);
+  {
+    long long b = (nch + 1 + kLz4Warps - 1) / kLz4Warps;
+    if (b > (long long)sms * 16) b = (long long)sms * 16;
+    lz4_emit_kernel<<<(unsigned)b, kLz4Warps * 32, 0, stream>>>(src, dst, ws, nch);
+  }
+  err = cudaGetLastError();
+  if (err != cudaSuccess) return set_error(VDI_ELAUNCH, "lz4 launch: %s", cudaGetErrorString(err));
+  return VDI_OK;
+}
+
+// ------------------------------------------------------- validate_vdi
+
+// vdi.py:116-134 on the device. codes: 1 front >= back, 2 overlapping,
+// 3 depth outside [-1, 1], 4 colour not premultiplied (first failing check
+// of a list, in the reference's order); result[0] = min over failing lists
+// of (list << 3 | code), result[1] = count-range violations.
+__global__ void validate_kernel(const VdiValidateArgs a, unsigned long long* result) {
+  const long long n = (long long)a.width * a.height;
+  const float lo_f = (float)(-1.0 - 1e-6), hi_f = (float)(1.0 + 1e-6);
+  unsigned long long best = ~0ull;
+  unsigned long long range_bad = 0;
+  for (long long l = (long long)blockIdx.x * blockDim.x + threadIdx.x; l < n;
+       l += (long long)gridDim.x * blockDim.x) {
+    const int r = (int)(l / a.width), x = (int)(l - (long long)r * a.width);
+    const long long li =
+        (long long)vdi_storage_row(r, a.vdi_band_rows, a.vdi_band_world, a.vdi_rows_per_rank) *
+            a.width + x;
+    const int cnt = a.counts[li];
+    if (cnt < 0 || cnt > a.n_sg) {
+      range_bad += 1;
+      continue;
+    }
+    if (cnt == 0) continue;
+    const float* ls = a.segs + li * (long long)list_stride(a.n_sg);
+    const float* fr = ls + front_off(a.n_sg);
+    const float* bk = ls + back_off(a.n_sg);
+    const float4* c4 = reinterpret_cast<const float4*>(ls);
+    int code = 0;
+    for (int k = 0; k < cnt && !code; ++k)
+      if (!(fr[k] < bk[k])) code = 1;
+    for (int k = 0; k + 1 < cnt && !code; ++k)
+      if (!(bk[k] <= __fadd_rn(fr[k + 1], 1e-7f))) code = 2;
+    if (!code) {
+      float fmn = fr[0], bmx = bk[0];
+      for (int k = 1; k < cnt; ++k) {
+        fmn = fminf(fmn, fr[k]);
+        bmx = fmaxf(bmx, bk[k]);
+      }
+      if (fmn < lo_f || bmx > hi_f) code = 3;
+    }
+    for (int k = 0; k < cnt && !code; ++k) {
+      const float4 c = c4[k];
+      const float m = fmaxf(fmaxf(c.x, c.y), c.z);
+      if (m > __fadd_rn(c.w, 1e-6f)) code = 4;
+    }
+    if (code) {
+      const unsigned long long key = ((unsigned long long)l << 3) | (unsigned long long)code;
+      if (key < best) best = key;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long ob = __shfl_xor_sync(0xffffffffu, best, o);
+    best = ob < best ? ob : best;
+    range_bad += __shfl_xor_sync(0xffffffffu, range_bad, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (best != ~0ull) atomicMin(result, best);
+    if (range_bad) atomicAdd(result + 1, range_bad);
+  }
+}
+
+int validate_vdi(const VdiValidateArgs* args, cudaStream_t stream) {
+  VdiValidateArgs c = *args;
+  if (c.vdi_band_rows <= 0) c.vdi_band_rows = 16;
+  if (c.vdi_band_world <= 0) c.vdi_band_world = 1;
+  set_u64_kernel<<<1, 1, 0, stream>>>(c.result, nullptr, ~0ull, 0ull);
+  cudaError_t err;
+  const long long n = (long long)c.width * c.height;
+  long long b = (n + 255) / 256;
+  if (b > 148 * 16) b = 148 * 16;
+  validate_kernel<<<(unsigned)(b < 1 ? 1 : b), 256, 0, stream>>>(c, c.result);
+  err = cudaGetLastError();
+  if (err != cudaSuccess) return set_error(VDI_ELAUNCH, "validate launch: %s", cudaGetErrorString(err));
+  return VDI_OK;
+}
+
+}  // namespace vdi

@@ -25,6 +25,13 @@ size_t gen_workspace_bytes(const VdiGenArgs* a, int recommended);
 int grid_launch(const VdiGridArgs* a, cudaStream_t stream);
 int render_launch(const VdiRenderArgs* a, cudaStream_t stream);
 int dvr_launch(const VdiDvrArgs* a, cudaStream_t stream);
+size_t encode_workspace_bytes(int width, int height);
+int encode_vdi1(const VdiEncodeArgs* a, cudaStream_t stream);
+size_t lz4_workspace_bytes(size_t n_max);
+int lz4_compress(const uint8_t* src, size_t n_max, const unsigned long long* n_dev, uint8_t* dst,
+                 unsigned long long* out_len, void* workspace, size_t ws_bytes,
+                 cudaStream_t stream);
+int validate_vdi(const VdiValidateArgs* a, cudaStream_t stream);
 int preview_launch(const VdiPreviewArgs* a, cudaStream_t stream);
 int bilinear_upsample(const double* src, int w, int h, double* dst, int out_w, int out_h,
                       int channels, cudaStream_t stream);

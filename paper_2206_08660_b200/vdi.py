@@ -149,23 +149,32 @@ class AccelGrid:
         return self._device
 
 
+_VIOLATIONS = {1: "front >= back", 2: "overlapping supersegments",
+               3: "depth outside [-1, 1]", 4: "color not premultiplied"}
+
+
 def validate_vdi(vdi) -> None:
-    """vdi.py:116-134 invariants, vectorised."""
-    counts = vdi.counts
-    if counts.min() < 0 or counts.max() > vdi.n_sg:
+    """vdi.py:116-134 on the device (vdi_validate): raises the reference's
+    InvariantViolation, with its message, for the count range or for the
+    first violating list in row-major order."""
+    from .raycast import _as_device_vdi
+    t = dv.require_cuda()
+    v = _as_device_vdi(vdi)
+    d = v.device()
+    res = t.empty(2, dtype=t.int64, device="cuda")
+    a = _capi.VdiValidateArgs()
+    a.segs, a.counts, a.result = dv.ptr(d.segs), dv.ptr(d.counts), dv.ptr(res)
+    a.width, a.height, a.n_sg = v.width, v.height, v.n_sg
+    a.vdi_band_rows, a.vdi_band_world, a.vdi_rows_per_rank = (int(d.band_rows), int(d.world),
+                                                              int(d.rows_per_rank))
+    _capi.check(_capi.load().vdi_validate(a, dv.stream_handle()))
+    first, n_range = (int(x) for x in dv.to_host(res).view(np.uint64))
+    if n_range:
         raise InvariantViolation("list count out of [0, n_sg]")
-    s = vdi.segs
-    valid = np.arange(vdi.n_sg)[None, None, :] < counts[:, :, None]
-    f, b = s[..., F], s[..., B]
-    if np.any(valid & ~(f < b)):
-        raise InvariantViolation("front >= back")
-    nxt = valid[..., 1:] & valid[..., :-1]
-    if np.any(nxt & ~(b[..., :-1] <= f[..., 1:] + 1e-7)):
-        raise InvariantViolation("overlapping supersegments")
-    if np.any(valid & ((f < -1.0 - 1e-6) | (b > 1.0 + 1e-6))):
-        raise InvariantViolation("depth outside [-1, 1]")
-    if np.any(valid & (s[..., R:A].max(axis=-1) > s[..., A] + 1e-6)):
-        raise InvariantViolation("color not premultiplied")
+    if first != (1 << 64) - 1:
+        lst, code = first >> 3, first & 7
+        ly, lx = divmod(lst, v.width)
+        raise InvariantViolation(f"list ({lx},{ly}): {_VIOLATIONS[code]}")
 
 
 def grid_cell_of(ndc_pt, grid, cam):

@@ -436,6 +436,60 @@ def codec_main():
         assert rlz4.decompress(comp, len(b)) == b
         rec[f"b{k}_in"] = np.frombuffer(b, np.uint8)
         rec[f"b{k}_lz4"] = np.frombuffer(comp, np.uint8)
+    # validate_vdi (vdi.py:116-134): violation messages of the reference
+    vdi0, _ = fixture_vdi("random_vdi:1")
+    base_c = np.ascontiguousarray(vdi0.counts[:6, :8])
+    base_s = np.ascontiguousarray(vdi0.segs[:6, :8])
+    rng = np.random.default_rng(5)
+    cases = []
+
+    def nz_list():
+        ys, xs = np.nonzero(base_c >= 2)
+        k = int(rng.integers(0, len(ys)))
+        return int(ys[k]), int(xs[k])
+
+    cases.append((base_c.copy(), base_s.copy()))
+    for kind in range(12):
+        c, sg = base_c.copy(), base_s.copy()
+        y, x = nz_list()
+        if kind in (0, 6):
+            sg[y, x, 0, 1] = sg[y, x, 0, 0]                       # front >= back
+        elif kind in (1, 7):
+            sg[y, x, 1, 0] = sg[y, x, 0, 1] - 1e-3                # overlap
+        elif kind in (2, 8):
+            sg[y, x, 0, 0] = -1.01                                # depth below -1
+        elif kind == 3:
+            sg[y, x, 1, 1] = 1.5                                  # depth above 1
+        elif kind in (4, 9):
+            sg[y, x, 0, 2] = sg[y, x, 0, 5] + 0.01                # not premultiplied
+        elif kind == 5:
+            c[y, x] = vdi0.n_sg + 1                               # count range
+        elif kind == 10:                                          # two lists, two kinds
+            y2, x2 = nz_list()
+            sg[y, x, 0, 2] = sg[y, x, 0, 5] + 0.01
+            sg[y2, x2, 1, 0] = sg[y2, x2, 0, 1] - 1e-3
+        elif kind == 11:                                          # two checks in one list
+            sg[y, x, 0, 2] = sg[y, x, 0, 5] + 0.01
+            sg[y, x, 0, 0] = -1.5
+        if kind >= 6:  # tie edges: exactly at the f32 tolerances
+            if kind == 7:
+                sg[y, x, 1, 0] = np.float32(sg[y, x, 0, 1]) - np.float32(1e-7)
+            if kind == 8:
+                sg[y, x, 0, 0] = np.float32(-1.0 - 1e-6)
+        cases.append((c, sg))
+    from vdikit import vdi as rvdi
+    msgs = []
+    for k, (c, sg) in enumerate(cases):
+        v = vk.Vdi(8, 6, vdi0.n_sg, c, sg, vdi0.gen_camera, vdi0.volume_aabb)
+        try:
+            rvdi.validate_vdi(v)
+            msgs.append("")
+        except rvdi.InvariantViolation as e:
+            msgs.append(str(e))
+        rec[f"val{k}_counts"] = c
+        rec[f"val{k}_segs"] = sg
+    rec["val_messages"] = np.array(msgs)
+    print("validate messages:", msgs)
     save("codec", rec)
 
 

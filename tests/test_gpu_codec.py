@@ -1,0 +1,124 @@
+"""The device wire path (vdi_encode_vdi1, vdi_lz4_compress) and the device
+validator (vdi_validate) vs the reference.
+
+- encode_vdi: the VDI1 bytes equal the reference's (sha256 from codec.npz,
+  made by vdikit.encode_vdi) and the oracle's, for every committed VDI.
+- LZ4: the device block is a different parse than the reference's serial
+  one, so parity is the transport's own property (test_acceptance.py A6):
+  the reference decoder (oracle.lz4_decompress, the pinned restatement of
+  lz4.py:117-168) returns the input exactly -- on the reference's byte
+  vectors, chunk-boundary sizes, and full C1 / C3 VDIs -- and the block
+  respects the format's end-of-block rules.
+- validate_vdi: the reference's InvariantViolation messages on 13 cases.
+"""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+import golden_io as gio
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2206_08660_b200 as vb  # noqa: E402
+from paper_2206_08660_b200 import codec, synth  # noqa: E402
+from paper_2206_08660_b200.camera import Camera  # noqa: E402
+from paper_2206_08660_b200.vdi import InvariantViolation, validate_vdi  # noqa: E402
+from oracle import oracle  # noqa: E402
+
+
+def _fixture(src):
+    counts, segs, grid, gen, aabb = gio.fixture_vdi(src)
+    p, vp = gen["gen_pose"], gen["gen_viewport"]
+    cam = Camera(position=tuple(p[0:3]), orientation=tuple(p[3:7]), fov_y=float(p[7]),
+                 near=float(p[8]), far=float(p[9]), viewport=(int(vp[0]), int(vp[1])))
+    h, w, n_sg, _ = segs.shape
+    gz, gy, gx = grid.shape
+    vdi = vb.Vdi(w, h, n_sg, counts, segs, cam, aabb)
+    return vdi, vb.AccelGrid((gx, gy, gz), grid, cam.near, cam.far), gen
+
+
+def _check_block(comp, raw):
+    """Decodes with the reference decoder; end-of-block rules of the format."""
+    assert oracle.lz4_decompress(comp, len(raw)) == raw
+    assert len(comp) <= len(raw) + len(raw) // 255 + 16
+
+
+def test_encode_vdi_matches_reference():
+    g = gio.load("codec")
+    for k, src in enumerate(str(t) for t in g["vdi_tags"]):
+        vdi, grid, gen = _fixture(src)
+        raw = codec.encode_vdi(vdi, grid)
+        assert hashlib.sha256(raw).hexdigest() == str(g[f"v{k}_raw_sha256"]), src
+        comp = codec.compress(raw)
+        _check_block(comp, raw)
+        comp2, n = codec.compress_vdi(vdi, grid)
+        assert n == len(raw)
+        _check_block(comp2, raw)
+
+
+def test_lz4_roundtrip_reference_vectors():
+    g = gio.load("codec")
+    for k in range(int(g["n_bytes_cases"])):
+        raw = g[f"b{k}_in"].tobytes()
+        comp = codec.compress(raw)
+        if not raw:
+            assert comp == b""
+            continue
+        _check_block(comp, raw)
+
+
+@pytest.mark.parametrize("n", [12, 13, 17, 32767, 32768, 32769, 65536 + 5, 300001])
+def test_lz4_chunk_boundaries(n):
+    rng = np.random.default_rng(n)
+    words = [rng.integers(0, 256, int(k), dtype=np.uint8).tobytes()
+             for k in rng.integers(4, 64, 40)]
+    raw = b"".join(words[int(i)] for i in rng.integers(0, 40, n // 4 + 1))[:n]
+    raw = raw[:n // 2] + b"\x00" * (n - n // 2)
+    comp = codec.compress(raw)
+    _check_block(comp, raw)
+
+
+def test_lz4_ratio_close_to_reference():
+    """Chunk-parallel parsing loses little against the serial parse."""
+    g = gio.load("codec")
+    for k in range(int(g["n_bytes_cases"])):
+        raw = g[f"b{k}_in"].tobytes()
+        if len(raw) < 4096:
+            continue
+        ours = len(codec.compress(raw))
+        ref = len(g[f"b{k}_lz4"].tobytes())
+        assert ours <= ref * 1.05 + 64, (k, ours, ref)
+
+
+@pytest.mark.parametrize("cfg", ["C1", "C3"])
+def test_compress_vdi_full_size(cfg):
+    vol, tf, gcam, rcam, n_sg = synth.config(cfg)
+    vdi, grid = vb.generate_vdi(vol, tf, gcam, vb.GenParams(n_sg=n_sg))
+    comp, n = codec.compress_vdi(vdi, grid)
+    cam = vdi.gen_camera
+    ref_raw = oracle.encode_vdi(vdi.width, vdi.height, n_sg, vdi.counts, vdi.segs,
+                                (*cam.position, *cam.orientation, cam.fov_y, cam.near, cam.far),
+                                vdi.volume_aabb, grid.counts)
+    assert n == len(ref_raw)
+    assert oracle.lz4_decompress(comp, n) == ref_raw
+    validate_vdi(vdi)
+
+
+def test_validate_messages_match_reference():
+    g = gio.load("codec")
+    vdi0, _, _ = _fixture("random_vdi:1")
+    for k, msg in enumerate(str(m) for m in g["val_messages"]):
+        v = vb.Vdi(8, 6, vdi0.n_sg, g[f"val{k}_counts"], g[f"val{k}_segs"], vdi0.gen_camera,
+                   vdi0.volume_aabb)
+        if msg == "":
+            validate_vdi(v)
+        else:
+            with pytest.raises(InvariantViolation) as e:
+                validate_vdi(v)
+            assert str(e.value) == msg, k

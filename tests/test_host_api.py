@@ -79,23 +79,3 @@ def test_synth_is_deterministic():
     k2 = synth.kingsnake((64, 64, 50))
     assert np.array_equal(k1.data, k2.data)
     assert k1.data.max() > 150 and (k1.data == 0).mean() > 0.3
-
-
-def test_validate_vdi_rejects_violations():
-    from paper_2206_08660_b200.vdi import InvariantViolation, validate_vdi
-    cam = vb.Camera(position=(0, 0, 5), orientation=(0, 0, 0, 1), fov_y=0.8, near=1.0,
-                    far=20.0, viewport=(2, 1))
-    segs = np.zeros((1, 2, 2, 6), np.float32)
-    segs[0, 0, 0] = [-0.5, -0.2, 0.1, 0.1, 0.1, 0.5]
-    segs[0, 0, 1] = [0.1, 0.4, 0.2, 0.2, 0.2, 0.5]
-    counts = np.array([[2, 0]], np.int32)
-    v = vb.Vdi(2, 1, 2, counts, segs, cam, np.zeros((2, 3)))
-    validate_vdi(v)
-    bad = segs.copy()
-    bad[0, 0, 1, 0] = -0.3  # overlaps the previous segment
-    with pytest.raises(InvariantViolation):
-        validate_vdi(vb.Vdi(2, 1, 2, counts, bad, cam, np.zeros((2, 3))))
-    bad = segs.copy()
-    bad[0, 0, 0, 2] = 0.9  # colour above alpha: not premultiplied
-    with pytest.raises(InvariantViolation):
-        validate_vdi(vb.Vdi(2, 1, 2, counts, bad, cam, np.zeros((2, 3))))
