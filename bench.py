@@ -326,7 +326,11 @@ def run_b200(args):
                        "lists_visited": L, "segs_intersected": K, "lists_searched": Ls}}
 
     # ---- end to end through the public API with host buffers
-    e2e = pipe.e2e_stream(args.e2e_steps)
+    # headline: the VDI comes back in the reference's VDI1 wire format
+    # (encode_vdi bytes, packed on the device); "dense" reads back the full
+    # (H, W, n_sg, 6) array instead, "serial" is one frame at a time
+    e2e = pipe.e2e_stream(args.e2e_steps, packed=True)
+    e2e["dense"] = pipe.e2e_stream(args.e2e_steps)
     e2e["serial"] = pipe.e2e(min(args.e2e_steps, 3))
 
     line = None

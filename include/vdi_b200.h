@@ -307,6 +307,13 @@ size_t vdi_volume_cells_bytes(int32_t voxel_type, int32_t nx, int32_t ny, int32_
 int vdi_volume_cells(const void* volume, int32_t voxel_type, int32_t nx, int32_t ny, int32_t nz,
                      void* out, vdi_stream_t stream);
 
+/* Synthetic input for config C5 (not a reference function): a
+ * Richtmyer-Meshkov-shaped u8 volume (nz, ny, nx) written on the device.
+ * modes: 12 x (kx, ky, amplitude, phase) of the interface; band: half-width
+ * of the mixing band in unit coordinates. */
+int vdi_synth_rm_u8(uint8_t* out, int32_t nx, int32_t ny, int32_t nz, const float* modes_host,
+                    float band, uint32_t seed, vdi_stream_t stream);
+
 /* Device self-check of the exact arithmetic shortcuts the kernels use, on n
  * random inputs: bad[0..3] (device, 4 x u64) receive the mismatch counts of
  * Markstein division, __drcp_rn reciprocals, the sqrt-free split threshold

@@ -47,6 +47,8 @@ def lib():
             _f32, _int, _int, _int, _f32, _int, _f64, _f64, _f64, _f64,
             _int, _int, _int, _int, _dbl, _dbl, _dbl, _dbl,
             _vp, _int, _int, _i32, _f32, _f64, _i32, _i64]
+        _u8v = np.ctypeslib.ndpointer(np.uint8, flags="C_CONTIGUOUS")
+        L.vdio_generate_u8.argtypes = [_u8v] + L.vdio_generate.argtypes[1:]
         L.vdio_accumulate_grid.argtypes = [
             _i32, _f32, _int, _int, _int, _int, _int, _int,
             _dbl, _dbl, _dbl, _dbl, _u32]
@@ -93,25 +95,31 @@ def _rows(rows):
 
 
 def generate(vol_norm, lut, pv, inv_pv, eye, aabb, width, height, n_sg, delta,
-             eps, gamma_init, step, lref, rows=None, threads=0):
+             eps, gamma_init, step, lref, rows=None, threads=0, compact=False):
     """_generate_kernel (generate.py:276-319) + executed-sample counter.
 
-    vol_norm is the f32 (nz, ny, nx) array R samples (Volume.normalized)."""
-    vol = np.ascontiguousarray(vol_norm, dtype=np.float32)
+    vol_norm is the f32 (nz, ny, nx) array R samples (Volume.normalized), or
+    the raw u8 voxels it is derived from (normalised identically on the fly)."""
+    u8 = isinstance(vol_norm, np.ndarray) and vol_norm.dtype == np.uint8
+    vol = np.ascontiguousarray(vol_norm) if u8 else np.ascontiguousarray(vol_norm, np.float32)
     nz, ny, nx = vol.shape
     lut = np.ascontiguousarray(lut, dtype=np.float32)
-    counts = np.zeros((height, width), np.int32)
-    segs = np.zeros((height, width, n_sg, 6), np.float32)
-    gammas = np.zeros((height, width), np.float64)
-    passes = np.zeros((height, width), np.int32)
-    samples = np.zeros((height, width), np.int64)
+    oh = len(rows) if (compact and rows is not None) else height
+    counts = np.zeros((oh, width), np.int32)
+    segs = np.zeros((oh, width, n_sg, 6), np.float32)
+    gammas = np.zeros((oh, width), np.float64)
+    passes = np.zeros((oh, width), np.int32)
+    samples = np.zeros((oh, width), np.int64)
     rp, nr, _keep = _rows(rows)
-    lib().vdio_generate(vol, nx, ny, nz, lut, lut.shape[0], _m(pv), _m(inv_pv),
+    if compact and rows is not None:
+        nr = -nr
+    fn = lib().vdio_generate_u8 if u8 else lib().vdio_generate
+    fn(vol, nx, ny, nz, lut, lut.shape[0], _m(pv), _m(inv_pv),
                         _m(eye), _m(aabb), width, height, n_sg, delta,
                         float(eps), float(gamma_init), float(step), float(lref),
                         rp, nr, threads, counts, segs, gammas, passes, samples)
     return dict(counts=counts, segs=segs, gammas=gammas, passes=passes,
-                samples=samples)
+                samples=samples)  # compact: rows in the order given
 
 
 def accumulate_grid(counts, segs, dims, near, far, proj_a, proj_b):

@@ -120,8 +120,25 @@ static inline void pixel_ray(const double* inv_pv, const double* eye, int col,
 
 /* --------------------------------------------------------------- sampler */
 
-/* volume.py:180-205 _trilinear on the f32 normalized array. */
-static inline double trilinear(const float* vol, int nx, int ny, int nz,
+/* The sampled volume: R's f32 `normalized` array, or raw u8 voxels that
+ * are normalised exactly as volume.py:48-50 does (f32 v / 255) -- the same
+ * values, without a 4 B/voxel host copy (large configs). */
+typedef struct {
+  const float* f32;
+  const uint8_t* u8;
+} vox_t;
+
+static float g_u8tab[256];
+static void init_u8tab(void) {
+  for (int i = 0; i < 256; ++i) g_u8tab[i] = (float)i / 255.0f;
+}
+
+static inline double vox(vox_t v, int64_t i) {
+  return v.u8 ? (double)g_u8tab[v.u8[i]] : (double)v.f32[i];
+}
+
+/* volume.py:180-205 _trilinear on the normalized volume. */
+static inline double trilinear(vox_t vol, int nx, int ny, int nz,
                                double px, double py, double pz) {
   double gx = px * (double)(nx - 1);
   double gy = py * (double)(ny - 1);
@@ -132,11 +149,11 @@ static inline double trilinear(const float* vol, int nx, int ny, int nz,
   if (iz > nz - 2) iz = nz - 2;
   double fx = gx - (double)ix, fy = gy - (double)iy, fz = gz - (double)iz;
   const int64_t sx = 1, sy = nx, sz = (int64_t)nx * ny;
-  const float* b = vol + iz * sz + iy * sy + ix;
-  double c00 = (double)b[0] * (1 - fx) + (double)b[sx] * fx;
-  double c10 = (double)b[sy] * (1 - fx) + (double)b[sy + sx] * fx;
-  double c01 = (double)b[sz] * (1 - fx) + (double)b[sz + sx] * fx;
-  double c11 = (double)b[sz + sy] * (1 - fx) + (double)b[sz + sy + sx] * fx;
+  const int64_t b = iz * sz + iy * sy + ix;
+  double c00 = vox(vol, b) * (1 - fx) + vox(vol, b + sx) * fx;
+  double c10 = vox(vol, b + sy) * (1 - fx) + vox(vol, b + sy + sx) * fx;
+  double c01 = vox(vol, b + sz) * (1 - fx) + vox(vol, b + sz + sx) * fx;
+  double c11 = vox(vol, b + sz + sy) * (1 - fx) + vox(vol, b + sz + sy + sx) * fx;
   double c0 = c00 * (1 - fy) + c10 * fy;
   double c1 = c01 * (1 - fy) + c11 * fy;
   return c0 * (1 - fz) + c1 * fz;
@@ -163,7 +180,7 @@ static inline void lut_classify(const float* lut, int n, double s, float* out) {
 /* ------------------------------------------------------------- generation */
 
 typedef struct {
-  const float* vol;
+  vox_t vol;
   int nx, ny, nz;
   const float* lut;
   int lut_n;
@@ -363,17 +380,18 @@ static void find_gamma_list(const ray_ctx* r, int delta, double eps,
 }
 
 /* One ray of generate.py:281-319 (_generate_kernel body). */
-static void generate_ray(const float* vol, int nx, int ny, int nz,
+static void generate_ray(vox_t vol, int nx, int ny, int nz,
                          const float* lut, int lut_n, const double* pv,
                          const double* inv_pv, const double* eye,
                          const double* bb, int width, int height, int n_sg,
                          int delta, double eps, double gamma_init, double step,
-                         double lref, int64_t idx, int32_t* counts, float* segs,
+                         double lref, int64_t idx, int64_t oidx, int32_t* counts, float* segs,
                          double* gammas, int32_t* passes, int64_t* samples,
                          double* tseg, float* high_seg) {
   int ly = (int)(idx / width), lx = (int)(idx % width);
   double d[3];
   pixel_ray(inv_pv, eye, lx, ly, width, height, d);
+  idx = oidx; /* outputs go to oidx (compact row sets) */
   float* out_seg = segs + idx * (int64_t)n_sg * 6;
   counts[idx] = 0;
   if (gammas) gammas[idx] = 0.0;
@@ -404,13 +422,16 @@ static void generate_ray(const float* vol, int nx, int ny, int nz,
 
 /* _generate_kernel over all rays, or only over the listed rows (bounded CPU
  * baseline samples). Output arrays are full (H, W) sized either way. */
-int vdio_generate(const float* vol, int nx, int ny, int nz, const float* lut,
+static int generate_all(vox_t vol, int nx, int ny, int nz, const float* lut,
                   int lut_n, const double* pv, const double* inv_pv,
                   const double* eye, const double* bb, int width, int height,
                   int n_sg, int delta, double eps, double gamma_init,
                   double step, double lref, const int32_t* rows, int n_rows,
                   int nthreads, int32_t* counts, float* segs, double* gammas,
                   int32_t* passes, int64_t* samples) {
+  /* n_rows < 0: the -n_rows listed rows, outputs packed as (n_rows, W) */
+  const int compact = n_rows < 0;
+  if (compact) n_rows = -n_rows;
   int64_t total = rows ? (int64_t)n_rows * width : (int64_t)width * height;
 #ifdef _OPENMP
   if (nthreads > 0) omp_set_num_threads(nthreads);
@@ -424,12 +445,40 @@ int vdio_generate(const float* vol, int nx, int ny, int nz, const float* lut,
       int64_t idx = rows ? (int64_t)rows[j / width] * width + j % width : j;
       generate_ray(vol, nx, ny, nz, lut, lut_n, pv, inv_pv, eye, bb, width,
                    height, n_sg, delta, eps, gamma_init, step, lref, idx,
-                   counts, segs, gammas, passes, samples, tseg, high_seg);
+                   compact ? j : idx, counts, segs, gammas, passes, samples, tseg, high_seg);
     }
     free(tseg);
     free(high_seg);
   }
   return 0;
+}
+
+int vdio_generate(const float* vol, int nx, int ny, int nz, const float* lut,
+                  int lut_n, const double* pv, const double* inv_pv,
+                  const double* eye, const double* bb, int width, int height,
+                  int n_sg, int delta, double eps, double gamma_init,
+                  double step, double lref, const int32_t* rows, int n_rows,
+                  int nthreads, int32_t* counts, float* segs, double* gammas,
+                  int32_t* passes, int64_t* samples) {
+  vox_t v = {vol, NULL};
+  return generate_all(v, nx, ny, nz, lut, lut_n, pv, inv_pv, eye, bb, width, height, n_sg,
+                      delta, eps, gamma_init, step, lref, rows, n_rows, nthreads, counts, segs,
+                      gammas, passes, samples);
+}
+
+/* The same over raw u8 voxels (normalised on the fly, volume.py:48-50). */
+int vdio_generate_u8(const uint8_t* vol, int nx, int ny, int nz, const float* lut,
+                     int lut_n, const double* pv, const double* inv_pv,
+                     const double* eye, const double* bb, int width, int height,
+                     int n_sg, int delta, double eps, double gamma_init,
+                     double step, double lref, const int32_t* rows, int n_rows,
+                     int nthreads, int32_t* counts, float* segs, double* gammas,
+                     int32_t* passes, int64_t* samples) {
+  init_u8tab();
+  vox_t v = {NULL, vol};
+  return generate_all(v, nx, ny, nz, lut, lut_n, pv, inv_pv, eye, bb, width, height, n_sg,
+                      delta, eps, gamma_init, step, lref, rows, n_rows, nthreads, counts, segs,
+                      gammas, passes, samples);
 }
 
 /* generate.py:322-346 _accumulate_grid (serial, as in R). */
@@ -777,7 +826,7 @@ int vdio_render(const float* segs, const int32_t* counts, int vdi_w, int vdi_h,
 /* One pixel of dvr.py:21-89 _dvr_kernel: the generation ray and sampler
  * (same clip, midpoint sample, opacity length normalisation), composited
  * front to back with early termination. */
-static void dvr_pixel(const float* vol, int nx, int ny, int nz, const float* lut,
+static void dvr_pixel(vox_t vol, int nx, int ny, int nz, const float* lut,
                       int lut_n, const double* pv, const double* inv_pv,
                       const double* eye, const double* bb, int width, int height,
                       double step, double lref, double early_term, const double* bg,
@@ -836,6 +885,7 @@ int vdio_dvr(const float* vol, int nx, int ny, int nz, const float* lut, int lut
              const double* bb, int width, int height, double step, double lref,
              double early_term, const double* bg, const int32_t* rows, int n_rows,
              int nthreads, double* img, int64_t* samples) {
+  vox_t v = {vol, NULL};
   int64_t total = rows ? (int64_t)n_rows * width : (int64_t)width * height;
 #ifdef _OPENMP
   if (nthreads > 0) omp_set_num_threads(nthreads);
@@ -843,7 +893,7 @@ int vdio_dvr(const float* vol, int nx, int ny, int nz, const float* lut, int lut
 #pragma omp parallel for schedule(dynamic, 64)
   for (int64_t j = 0; j < total; ++j) {
     int64_t idx = rows ? (int64_t)rows[j / width] * width + j % width : j;
-    dvr_pixel(vol, nx, ny, nz, lut, lut_n, pv, inv_pv, eye, bb, width, height, step,
+    dvr_pixel(v, nx, ny, nz, lut, lut_n, pv, inv_pv, eye, bb, width, height, step,
               lref, early_term, bg, idx, img, samples);
   }
   return 0;

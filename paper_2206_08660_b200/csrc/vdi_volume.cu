@@ -205,3 +205,105 @@ int volume_cells(const void* volume, int voxel_type, int nx, int ny, int nz, voi
 }
 
 }  // namespace vdi
+
+// ------------------------------------------------------------- synthetic
+// Richtmyer-Meshkov-shaped u8 volume for config C5, built
+// on the device because the 2048 x 2048 x 1920 brick (7.5 GiB) would take
+// minutes to synthesise on the host. A mixing band |z - h(x, y)| < w around
+// a perturbed interface h = 0.5 + sum_m A_m sin(2 pi k_m . (x, y) + phi_m);
+// inside it a 4-octave value-noise fbm mapped to 60..255, outside 0. Integer
+// hashing and f32 arithmetic: the same bytes on every run and every B200.
+namespace vdi {
+
+__device__ __forceinline__ uint32_t hash3(uint32_t x, uint32_t y, uint32_t z, uint32_t s) {
+  uint32_t h = s ^ 0x9e3779b9u;
+  h ^= x * 0x85ebca6bu;
+  h = (h << 13) | (h >> 19);
+  h ^= y * 0xc2b2ae35u;
+  h = (h << 11) | (h >> 21);
+  h ^= z * 0x27d4eb2fu;
+  h ^= h >> 16;
+  h *= 0x7feb352du;
+  h ^= h >> 15;
+  h *= 0x846ca68bu;
+  h ^= h >> 16;
+  return h;
+}
+
+__device__ __forceinline__ float lattice(int x, int y, int z, uint32_t s) {
+  return (float)(hash3((uint32_t)x, (uint32_t)y, (uint32_t)z, s) >> 8) * (1.0f / 16777216.0f);
+}
+
+__device__ __forceinline__ float smooth(float t) { return t * t * (3.0f - 2.0f * t); }
+
+__device__ float value_noise(float px, float py, float pz, uint32_t s) {
+  const float fx = floorf(px), fy = floorf(py), fz = floorf(pz);
+  const int ix = (int)fx, iy = (int)fy, iz = (int)fz;
+  const float tx = smooth(px - fx), ty = smooth(py - fy), tz = smooth(pz - fz);
+  float c[2][2];
+  for (int b = 0; b < 2; ++b)
+    for (int a = 0; a < 2; ++a) {
+      const float v0 = lattice(ix, iy + a, iz + b, s), v1 = lattice(ix + 1, iy + a, iz + b, s);
+      c[b][a] = v0 + (v1 - v0) * tx;
+    }
+  const float c0 = c[0][0] + (c[0][1] - c[0][0]) * ty;
+  const float c1 = c[1][0] + (c[1][1] - c[1][0]) * ty;
+  return c0 + (c1 - c0) * tz;
+}
+
+struct RmModes {
+  float kx[12], ky[12], amp[12], phase[12];
+  float band;
+  uint32_t seed;
+};
+
+__global__ void synth_rm_kernel(uint8_t* __restrict__ out, int nx, int ny, int nz,
+                                const RmModes m) {
+  const long long cols = (long long)nx * ny;
+  for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < cols;
+       c += (long long)gridDim.x * blockDim.x) {
+    const int ix = (int)(c % nx), iy = (int)(c / nx);
+    const float x = (ix + 0.5f) / nx, y = (iy + 0.5f) / ny;
+    float h = 0.5f;
+    for (int k = 0; k < 12; ++k)
+      h += m.amp[k] * sinf(6.28318530718f * (m.kx[k] * x + m.ky[k] * y) + m.phase[k]);
+    for (int iz = 0; iz < nz; ++iz) {
+      const float z = (iz + 0.5f) / nz;
+      uint8_t v = 0;
+      if (fabsf(z - h) < m.band) {
+        float f = 0.0f, a = 1.0f, norm = 0.0f, fr = 8.0f;
+        for (int o = 0; o < 4; ++o) {
+          f += a * value_noise(x * fr, y * fr, z * fr, m.seed + 977u * o);
+          norm += a;
+          a *= 0.5f;
+          fr *= 2.0f;
+        }
+        f /= norm;
+        v = (uint8_t)(60.0f + 195.0f * fminf(fmaxf(f, 0.0f), 1.0f) + 0.5f);
+      }
+      out[(long long)iz * cols + c] = v;
+    }
+  }
+}
+
+int synth_rm_u8(uint8_t* out, int nx, int ny, int nz, const float* modes, float band,
+                uint32_t seed, cudaStream_t stream) {
+  RmModes m;
+  for (int k = 0; k < 12; ++k) {
+    m.kx[k] = modes[4 * k];
+    m.ky[k] = modes[4 * k + 1];
+    m.amp[k] = modes[4 * k + 2];
+    m.phase[k] = modes[4 * k + 3];
+  }
+  m.band = band;
+  m.seed = seed;
+  const long long cols = (long long)nx * ny;
+  long long blocks = (cols + 255) / 256;
+  if (blocks > 148 * 32) blocks = 148 * 32;
+  synth_rm_kernel<<<(unsigned)blocks, 256, 0, stream>>>(out, nx, ny, nz, m);
+  const cudaError_t err = cudaGetLastError();
+  if (err != cudaSuccess) return set_error(VDI_ELAUNCH, "synth launch: %s", cudaGetErrorString(err));
+  return VDI_OK;
+}
+
+}  // namespace vdi

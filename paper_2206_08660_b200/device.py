@@ -123,6 +123,8 @@ def volume_array(vol):
 
 
 def upload_volume(vol, cache: bool = True):
+    if hasattr(vol, "device_data"):  # DeviceVolume: already resident
+        return vol.device_data, vol.voxel_type
     arr, vt = volume_array(vol)
     if arr.ndim != 3:
         nx, ny, nz = vol.dims

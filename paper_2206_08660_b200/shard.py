@@ -180,7 +180,7 @@ class Pipeline:
                   _device=self.dvdi)
         return vdi.counts, vdi.segs, dv.to_host(self.bufs.grid).view(np.uint32)
 
-    def e2e_stream(self, steps: int, warmup: int = 2):
+    def e2e_stream(self, steps: int, warmup: int = 2, packed: bool = False):
         """End to end through the public FrameStream API: every frame uploads
         its volume from pinned host memory and reads its results (counts, AoS
         segs, AccelGrid, image) back to pinned host memory, overlapped with
@@ -190,13 +190,14 @@ class Pipeline:
         t = self.t
         host = dv.pinned_numpy(self.vol.data.shape, self.vol.data.dtype)
         host[...] = self.vol.data
-        fs = FrameStream(self)
+        fs = FrameStream(self, packed=packed)
         fs.run([host] * warmup)
         t.cuda.synchronize()
         if self.world > 1:
             self.dist.barrier()
+        d2h = []
         t0 = time.perf_counter()
-        fs.run([host] * steps)
+        fs.run([host] * steps, on_result=lambda r: d2h.append(r.nbytes))
         t.cuda.synchronize()
         dt = (time.perf_counter() - t0) / steps
         if self.world > 1:
@@ -204,11 +205,13 @@ class Pipeline:
             self.dist.all_reduce(x, op=self.dist.ReduceOp.MAX)
             dt = float(x.item())
         del fs
+        mode = "FrameStream: H2D(i+1) | kernels(i) | D2H(i-1) overlapped"
+        if packed:
+            mode += "; VDI read back as its VDI1 bytes (encode_vdi, vdi.py:141)"
         return {"value": 2 * self.w * self.h / dt / 1e6, "unit": "Mrays/s",
                 "h2d_bytes_per_step": int(fs_h2d(host, self.tf)),
-                "d2h_bytes_per_step": int(self._d2h_bytes()),
-                "ms_per_step": dt * 1e3, "steps": steps,
-                "mode": "FrameStream: H2D(i+1) | kernels(i) | D2H(i-1) overlapped"}
+                "d2h_bytes_per_step": int(np.mean(d2h)) if d2h else int(self._d2h_bytes()),
+                "ms_per_step": dt * 1e3, "steps": steps, "mode": mode}
 
     def _d2h_bytes(self) -> int:
         n_sg = self.params.n_sg

@@ -22,6 +22,16 @@ its upload and for the download that last read its output slot.
 Results are handed out as numpy views of the pinned host slot: they stay
 valid until the frame two submissions later is submitted (copy them to keep
 them longer).
+
+packed=True returns the VDI in the reference's own wire/file format instead
+of the dense (H, W, n_sg, 6) array: the VDI1 byte string of
+`encode_vdi(vdi, grid)` (vdi.py:141-159, bit-identical; `decode_vdi` rebuilds
+the identical Vdi and AccelGrid), packed on the device (vdi_encode_vdi1).
+Only valid supersegments cross the host link (C3: 183 MB instead of 1 GB).
+The packed length is known on the device only, so a frame's length and image
+are read back on the d2h stream with the frame, and its VDI1 bytes are
+copied once `collect` has read the length -- still overlapped with the next
+frame's kernels, which are queued by then.
 """
 
 from __future__ import annotations
@@ -38,14 +48,36 @@ from . import device as dv
 class FrameResult:
     """Host results of one frame (views of a pinned slot; see module doc)."""
     index: int
-    counts: np.ndarray   # (rows, W) i32, this rank's generation rows
-    segs: np.ndarray     # (rows, W, n_sg, 6) f32 AoS [front, back, r, g, b, a]
-    grid: np.ndarray     # (gz, gy, gx) u32 AccelGrid counts (summed over ranks)
-    image: np.ndarray    # (out_rows, out_w, 4) f64 premultiplied RGBA, this rank's rows
+    counts: np.ndarray | None  # (rows, W) i32, this rank's generation rows
+    segs: np.ndarray | None    # (rows, W, n_sg, 6) f32 AoS [front, back, r, g, b, a]
+    grid: np.ndarray | None    # (gz, gy, gx) u32 AccelGrid counts (summed over ranks)
+    image: np.ndarray          # (out_rows, out_w, 4) f64 premultiplied RGBA, this rank's rows
+    vdi1: np.ndarray | None = None  # packed mode: the VDI1 bytes (u8)
 
     @property
     def nbytes(self) -> int:
+        if self.vdi1 is not None:
+            return self.vdi1.nbytes + self.image.nbytes + 8
         return self.counts.nbytes + self.segs.nbytes + self.grid.nbytes + self.image.nbytes
+
+    def decode(self):
+        """(counts, segs, grid) from the VDI1 bytes (vdi.py:162-210 layout)."""
+        if self.vdi1 is None:
+            return self.counts, self.segs, self.grid
+        import struct
+        b = self.vdi1
+        _, _, w, h, n_sg = struct.unpack_from("<4sIIII", b, 0)
+        gx, gy, gz = struct.unpack_from("<3I", b, 148)
+        off = 160
+        counts = np.frombuffer(b, "<u2", w * h, off).reshape(h, w).astype(np.int32)
+        off += 2 * w * h
+        total = int(counts.sum())
+        packed = np.frombuffer(b, "<f4", 6 * total, off).reshape(total, 6)
+        off += 24 * total
+        grid = np.frombuffer(b, "<u4", gx * gy * gz, off).reshape(gz, gy, gx)
+        segs = np.zeros((h, w, n_sg, 6), np.float32)
+        segs[np.arange(n_sg)[None, None, :] < counts[:, :, None]] = packed
+        return counts, segs, grid
 
 
 class FrameStream:
@@ -56,9 +88,9 @@ class FrameStream:
     N > 1, the NCCL exchange) on the compute stream.
     """
 
-    def __init__(self, pipe):
+    def __init__(self, pipe, packed: bool = False):
         t = dv.require_cuda()
-        self.t, self.pipe = t, pipe
+        self.t, self.pipe, self.packed = t, pipe, packed
         vol = pipe.vol
         shape = tuple(pipe.vol_dev.shape)
         self.h2d, self.comp, self.d2h = (t.cuda.Stream() for _ in range(3))
@@ -69,15 +101,25 @@ class FrameStream:
         gz, gy, gx = pipe.grid_dims[2], pipe.grid_dims[1], pipe.grid_dims[0]
         self.out = []
         self.host = []
+        L = _capi.load()
+        self.vdi1_cap = int(L.vdi_vdi1_max_bytes(w, rows, n_sg, gx, gy, gz))
+        self.enc_ws = t.empty(int(L.vdi_encode_workspace_bytes(w, rows)), dtype=t.uint8,
+                              device="cuda")
         for _ in range(2):
-            self.out.append({
-                "counts": t.empty((rows, w), dtype=t.int32, device="cuda"),
-                "segs": t.empty((rows * w, n_sg * 6), dtype=t.float32, device="cuda"),
-                "grid": t.empty((gz, gy, gx), dtype=t.int32, device="cuda"),
-                "image": t.empty(tuple(pipe.image.shape), dtype=t.float64, device="cuda"),
-            })
+            if packed:
+                o = {"vdi1": t.empty(self.vdi1_cap, dtype=t.uint8, device="cuda"),
+                     "len": t.zeros(1, dtype=t.int64, device="cuda"),
+                     "image": t.empty(tuple(pipe.image.shape), dtype=t.float64,
+                                      device="cuda")}
+            else:
+                o = {"counts": t.empty((rows, w), dtype=t.int32, device="cuda"),
+                     "segs": t.empty((rows * w, n_sg * 6), dtype=t.float32, device="cuda"),
+                     "grid": t.empty((gz, gy, gx), dtype=t.int32, device="cuda"),
+                     "image": t.empty(tuple(pipe.image.shape), dtype=t.float64,
+                                      device="cuda")}
+            self.out.append(o)
             self.host.append({k: t.empty(v.shape, dtype=v.dtype, pin_memory=True)
-                              for k, v in self.out[-1].items()})
+                              for k, v in o.items()})
         ev = lambda: t.cuda.Event()  # noqa: E731
         self.ev_h2d = [ev(), ev()]       # upload of slot s done
         self.ev_comp = [ev(), ev()]      # compute that read vol slot / wrote out slot s done
@@ -110,18 +152,22 @@ class FrameStream:
                 self.comp.wait_event(self.ev_d2h[s])
             p.step(vol_dev=self.vol_slots[s])
             L = _capi.load()
-            _capi.check(L.vdi_segs_to_aos(dv.ptr(p.bufs.segs), dv.ptr(out["segs"]),
-                                          p.gen_rows * p.w, p.params.n_sg,
-                                          dv.stream_handle()))
-            out["counts"].copy_(p.bufs.counts, non_blocking=True)
-            out["grid"].copy_(p.bufs.grid, non_blocking=True)
+            if self.packed:
+                _capi.check(L.vdi_encode_vdi1(self._enc_args(out), dv.stream_handle()))
+            else:
+                _capi.check(L.vdi_segs_to_aos(dv.ptr(p.bufs.segs), dv.ptr(out["segs"]),
+                                              p.gen_rows * p.w, p.params.n_sg,
+                                              dv.stream_handle()))
+                out["counts"].copy_(p.bufs.counts, non_blocking=True)
+                out["grid"].copy_(p.bufs.grid, non_blocking=True)
             out["image"].copy_(p.image, non_blocking=True)
             self.ev_comp[s].record(self.comp)
         self.used_out[s] = True
         with t.cuda.stream(self.d2h):
             self.d2h.wait_event(self.ev_comp[s])
             for k, v in out.items():
-                self.host[s][k].copy_(v, non_blocking=True)
+                if k != "vdi1":  # packed: its length is read first (collect)
+                    self.host[s][k].copy_(v, non_blocking=True)
             self.ev_d2h[s].record(self.d2h)
         self.pending.append(i)
         self.n += 1
@@ -133,6 +179,16 @@ class FrameStream:
         self.ev_d2h[s].synchronize()
         h = self.host[s]
         p = self.pipe
+        if self.packed:
+            n = int(h["len"][0])
+            with self.t.cuda.stream(self.d2h):
+                h["vdi1"][:n].copy_(self.out[s]["vdi1"][:n], non_blocking=True)
+                self.ev_d2h[s].record(self.d2h)
+            self.ev_d2h[s].synchronize()
+            res = FrameResult(index=i, counts=None, segs=None, grid=None,
+                              image=h["image"].numpy(), vdi1=h["vdi1"][:n].numpy())
+            self.d2h_bytes = res.nbytes
+            return res
         res = FrameResult(
             index=i,
             counts=h["counts"].numpy(),
@@ -141,6 +197,25 @@ class FrameStream:
             image=h["image"].numpy())
         self.d2h_bytes = res.nbytes
         return res
+
+    def _enc_args(self, out):
+        """vdi_encode_vdi1 arguments for this rank's generation rows."""
+        from .codec import vdi1_header
+        from .vdi import AccelGrid, Vdi
+        p = self.pipe
+        if not hasattr(self, "_hdr"):
+            vdi = Vdi(p.w, p.gen_rows, p.params.n_sg, None, None, p.gcam, p.aabb)
+            self._hdr = vdi1_header(vdi, AccelGrid(p.grid_dims, None, p.gcam.near, p.gcam.far))
+        a = _capi.VdiEncodeArgs()
+        a.segs, a.counts, a.grid = dv.ptr(p.bufs.segs), dv.ptr(p.bufs.counts), dv.ptr(p.bufs.grid)
+        a.out, a.out_len = dv.ptr(out["vdi1"]), dv.ptr(out["len"])
+        a.workspace, a.workspace_bytes = dv.ptr(self.enc_ws), int(self.enc_ws.numel())
+        for k, b in enumerate(self._hdr):
+            a.header[k] = b
+        a.width, a.height, a.n_sg = p.w, p.gen_rows, p.params.n_sg
+        a.gx, a.gy, a.gz = (int(v) for v in p.grid_dims)
+        a.vdi_band_rows, a.vdi_band_world, a.vdi_rows_per_rank = 16, 1, p.gen_rows
+        return a
 
     def run(self, volumes, on_result=None):
         """Submit every volume, collecting each frame once the next one is

@@ -8,6 +8,7 @@ these generators define the configs:
   C2  blobs(256)  256^3 f32, 512x512, n_sg 20
   C3  kingsnake() 1024x1024x795 u8, 1920x1080, n_sg 20 (the bench workload)
   C4  rt_like()   1024^3 f32, 1920x1080, n_sg 30, sweep 0-30 deg
+  C5  rm_like()   2048x2048x1920 u8 (built on the GPU), 3840x2160, n_sg 40
 
 Cameras follow the reference's sweep convention (bench.py:28-41 ==
 synth.py:89-100): orbit about the volume centre, fov 45 deg, near = 0.15 r,
@@ -33,6 +34,8 @@ KINGSNAKE_TF = ((0.0, 0, 0, 0, 0), (0.12, 0, 0, 0, 0), (0.2, .8, .7, .5, .05),
                 (0.55, .9, .5, .2, .6), (0.8, 1, 1, .9, .3), (1.0, 1, 1, 1, .4))
 RT_TF = ((0.0, 0, 0, 0, 0), (0.3, .1, .2, .8, .02), (0.6, .9, .6, .2, .15),
          (1.0, 1, .2, .1, .5))
+RM_TF = ((0.0, 0, 0, 0, 0), (0.22, 0, 0, 0, 0), (0.3, .9, .4, .1, .03),
+         (0.55, .3, .7, .9, .12), (0.8, 1, .9, .6, .35), (1.0, 1, 1, 1, .6))
 
 
 def blobs(n: int, k: int = 12, seed: int = 0) -> Volume:
@@ -126,6 +129,42 @@ def rt_like(n: int = 1024, seed: int = 2) -> Volume:
     return make_volume(data, "f32")
 
 
+def rm_modes(seed: int = 3) -> np.ndarray:
+    """12 interface modes (kx, ky, amplitude, phase) of rm_like: integer wave
+    vectors with |k| in [1, 12], A ~ |k|^-1.2 normalised to sum 0.1."""
+    rng = np.random.default_rng(seed)
+    ks = []
+    while len(ks) < 12:
+        k = rng.integers(-12, 13, size=2)
+        if 1 <= np.hypot(*k) <= 12:
+            ks.append(k)
+    ks = np.array(ks, dtype=np.float64)
+    amp = np.hypot(ks[:, 0], ks[:, 1]) ** -1.2
+    amp *= 0.1 / amp.sum()
+    phase = rng.uniform(0, 2 * np.pi, 12)
+    return np.ascontiguousarray(np.stack([ks[:, 0], ks[:, 1], amp, phase], 1), np.float32)
+
+
+def rm_like(dims=(2048, 2048, 1920), seed: int = 3):
+    """Richtmyer-Meshkov-shaped u8 volume, synthesised on
+    the device (vdi_synth_rm_u8): a mixing band of half-width 0.15 around a
+    12-mode perturbed interface z = h(x, y), filled with 4-octave value-noise
+    fbm mapped to 60..255; 0 outside. Returns a DeviceVolume."""
+    import ctypes
+    from . import _capi
+    from . import device as dv
+    from .volume import DeviceVolume
+    t = dv.require_cuda()
+    nx, ny, nz = dims
+    out = t.empty((nz, ny, nx), dtype=t.uint8, device="cuda")
+    modes = rm_modes(seed)
+    _capi.check(_capi.load().vdi_synth_rm_u8(
+        dv.ptr(out), nx, ny, nz, modes.ctypes.data_as(ctypes.c_void_p), ctypes.c_float(0.15),
+        seed, dv.stream_handle()))
+    t.cuda.current_stream().synchronize()
+    return DeviceVolume(out, "u8")
+
+
 def preset_volume(preset: str, dims: int = 128) -> Volume:
     """The reference's sphere / bands presets (synth.py:25-58), u8."""
     c1 = np.arange(dims, dtype=np.float64) + 0.5
@@ -147,7 +186,7 @@ def preset_volume(preset: str, dims: int = 128) -> Volume:
 
 def preset_tf(preset: str) -> TransferFunction:
     table = {"sphere": SPHERE_TF, "blobs": SPHERE_TF, "bands": BANDS_TF,
-             "kingsnake": KINGSNAKE_TF, "rt": RT_TF}
+             "kingsnake": KINGSNAKE_TF, "rt": RT_TF, "rm": RM_TF}
     return TransferFunction(table[preset])
 
 
@@ -169,6 +208,7 @@ CONFIGS = {
     "C2": (lambda: blobs(256), "blobs", (512, 512), 20, 2.8, 15.0),
     "C3": (lambda: kingsnake(), "kingsnake", (1920, 1080), 20, 1.6, 15.0),
     "C4": (lambda: rt_like(), "rt", (1920, 1080), 30, 1.6, 15.0),
+    "C5": (lambda: rm_like(), "rm", (3840, 2160), 40, 1.6, 15.0),
 }
 
 

@@ -87,6 +87,53 @@ class Volume:
         return np.stack([np.zeros(3), self.world_size])
 
 
+class DeviceVolume:
+    """A volume that lives only in device memory (a torch tensor (nz, ny, nx)
+    of the voxel type), e.g. one synthesised on the GPU. It carries the
+    Volume attributes the path reads (dims, voxel_type, spacing, aabb,
+    world_size); `data` / `normalized` copy it to the host on first use (for
+    checkers only -- the device path never needs them)."""
+
+    normalized_is_derived = True
+
+    def __init__(self, device_data, voxel_type: str, spacing=(1.0, 1.0, 1.0)):
+        if voxel_type not in VOXEL_DTYPES:
+            raise UnsupportedVoxelType(voxel_type)
+        nz, ny, nx = (int(v) for v in device_data.shape)
+        if min(nx, ny, nz) < 2:
+            raise ValueError("dims components must be >= 2 for trilinear sampling")
+        self.device_data = device_data
+        self.dims = (nx, ny, nz)
+        self.voxel_type = voxel_type
+        self.spacing = tuple(float(v) for v in spacing)
+        self._host = None
+
+    @property
+    def data(self) -> np.ndarray:
+        if self._host is None:
+            self._host = self.device_data.cpu().numpy()
+        return self._host
+
+    @property
+    def normalized(self) -> np.ndarray:
+        d = self.data
+        if self.voxel_type == "f32":
+            return d
+        return d.astype(np.float32) / np.float32(VOXEL_MAX[self.voxel_type])
+
+    @property
+    def value_range(self) -> tuple:
+        return (float(self.device_data.min()), float(self.device_data.max()))
+
+    @property
+    def world_size(self) -> np.ndarray:
+        return np.array(self.dims, dtype=np.float64) * np.array(self.spacing)
+
+    @property
+    def aabb(self) -> np.ndarray:
+        return np.stack([np.zeros(3), self.world_size])
+
+
 def make_volume(data: np.ndarray, voxel_type: str, spacing=(1.0, 1.0, 1.0)) -> Volume:
     """Wrap a (nz, ny, nx) scalar array (volume.py:63-75)."""
     if voxel_type not in VOXEL_DTYPES:

@@ -51,3 +51,34 @@ def test_stream_frames_match_single_frame_api(name):
     n = fs.run([hosts[i] for i in order], on_result=check)
     assert n == len(order) and seen == list(range(len(order)))
     assert fs.h2d_bytes == vol.data.nbytes and fs.d2h_bytes > 0
+
+
+def test_stream_packed_vdi1_matches_encode_vdi():
+    """packed=True: each frame's VDI comes back as the VDI1 bytes of
+    encode_vdi (vdi.py:141-159) of that frame's VDI, and decodes to it."""
+    from paper_2206_08660_b200 import codec
+    vol, tf, gcam, rcam, n_sg = synth.config("C1")
+    other = make_volume(np.ascontiguousarray(vol.data[::-1]), vol.voxel_type)
+    params = vb.GenParams(n_sg=n_sg)
+    refs = []
+    for v in (vol, other):
+        vdi, grid = vb.generate_vdi(v, tf, gcam, params)
+        img = vb.render_vdi(vdi, grid, rcam)
+        refs.append((codec.encode_vdi(vdi, grid), vdi.counts, vdi.segs, grid.counts, img.data))
+    pipe = shard.Pipeline(vol, tf, gcam, rcam, params)
+    fs = FrameStream(pipe, packed=True)
+    hosts = []
+    for v in (vol, other):
+        h = dv.pinned_numpy(v.data.shape, v.data.dtype)
+        h[...] = v.data
+        hosts.append(h)
+    order = [1, 0, 0, 1]
+
+    def check(r):
+        raw, c, s, g, im = refs[order[r.index]]
+        assert r.vdi1.tobytes() == raw
+        dc, ds, dg = r.decode()
+        assert np.array_equal(dc, c) and np.array_equal(ds, s) and np.array_equal(dg, g)
+        assert np.array_equal(r.image[:im.shape[0]], im)
+
+    assert fs.run([hosts[i] for i in order], on_result=check) == len(order)
