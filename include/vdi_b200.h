@@ -57,7 +57,7 @@
 extern "C" {
 #endif
 
-#define VDI_ABI_VERSION 1
+#define VDI_ABI_VERSION 2
 
 #define VDI_OK 0
 #define VDI_EINVAL (-1)
@@ -114,6 +114,16 @@ typedef struct VdiGenArgs {
   int32_t n_sg, delta;
   int32_t band_rows, band_stride, band_offset;
   int32_t brick_log2;   /* brick edge 2^brick_log2 voxels */
+  /* Resident box (volume bricked across GPUs): when sub_dims[0] > 0,
+   * `volume` (and brick_max / corner records) hold only the voxels
+   * [sub_origin, sub_origin + sub_dims) of the nx x ny x nz grid, stored
+   * (sub_dims[2], sub_dims[1], sub_dims[0]) x-fastest; sub_origin must be a
+   * multiple of the brick edge. Sample positions are unchanged, so results
+   * equal the full-volume run when the box holds every cell the rays touch;
+   * a touched cell outside it sets *sub_oob (device, may be NULL). */
+  int32_t sub_origin[3];
+  int32_t sub_dims[3];
+  uint32_t* sub_oob;
 } VdiGenArgs;
 
 /* AccelGrid: per-cell supersegment counts (generate.py:322-346). `grid` is
@@ -310,9 +320,10 @@ int vdi_volume_cells(const void* volume, int32_t voxel_type, int32_t nx, int32_t
 /* Synthetic input for config C5 (not a reference function): a
  * Richtmyer-Meshkov-shaped u8 volume (nz, ny, nx) written on the device.
  * modes: 12 x (kx, ky, amplitude, phase) of the interface; band: half-width
- * of the mixing band in unit coordinates. */
-int vdi_synth_rm_u8(uint8_t* out, int32_t nx, int32_t ny, int32_t nz, const float* modes_host,
-                    float band, uint32_t seed, vdi_stream_t stream);
+ * of the mixing band in unit coordinates. box_host (or NULL = everything):
+ * [ox, oy, oz, sx, sy, sz], write only that box, stored (sz, sy, sx). */
+int vdi_synth_rm_u8(uint8_t* out, int32_t nx, int32_t ny, int32_t nz, const int32_t* box_host,
+                    const float* modes_host, float band, uint32_t seed, vdi_stream_t stream);
 
 /* Device self-check of the exact arithmetic shortcuts the kernels use, on n
  * random inputs: bad[0..3] (device, 4 x u64) receive the mismatch counts of

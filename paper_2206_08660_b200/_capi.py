@@ -28,6 +28,7 @@ class VdiGenArgs(ctypes.Structure):
         ("voxel_type", _I), ("nx", _I), ("ny", _I), ("nz", _I), ("lut_n", _I),
         ("width", _I), ("height", _I), ("n_sg", _I), ("delta", _I),
         ("band_rows", _I), ("band_stride", _I), ("band_offset", _I), ("brick_log2", _I),
+        ("sub_origin", _I * 3), ("sub_dims", _I * 3), ("sub_oob", _P),
     ]
 
 
@@ -152,7 +153,7 @@ def load():
     L.vdi_lz4_workspace_bytes.restype = ctypes.c_size_t
     L.vdi_lz4_compress.argtypes = [_P, ctypes.c_size_t, _P, _P, _P, _P, ctypes.c_size_t, _P]
     L.vdi_validate.argtypes = [ctypes.POINTER(VdiValidateArgs), _P]
-    L.vdi_synth_rm_u8.argtypes = [_P, _I, _I, _I, _P, ctypes.c_float, ctypes.c_uint32, _P]
+    L.vdi_synth_rm_u8.argtypes = [_P, _I, _I, _I, _P, _P, ctypes.c_float, ctypes.c_uint32, _P]
     L.vdi_bilinear_upsample.argtypes = [_P, _I, _I, _P, _I, _I, _I, _P]
     L.vdi_find_first_batch.argtypes = [_P, _P, _P, _I, _P, _P, _P, _P, _P, ctypes.c_int64, _P]
     L.vdi_volume_brick_max.argtypes = [_P, _I, _I, _I, _I, _I, _P, _P]
@@ -175,7 +176,7 @@ def load():
            "vdi_lz4_workspace_bytes", "vdi_lz4_compress", "vdi_validate", "vdi_synth_rm_u8", "vdi_dvr_launch",
                  "vdi_find_first_batch", "vdi_segs_to_aos", "vdi_segs_from_aos"):
         getattr(L, name).restype = ctypes.c_int
-    if L.vdi_abi_version() != 1:
+    if L.vdi_abi_version() != 2:
         raise VdiError("libvdi_b200.so ABI mismatch")
     _lib = L
     return L

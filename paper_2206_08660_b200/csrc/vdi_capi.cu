@@ -162,11 +162,11 @@ int vdi_validate(const VdiValidateArgs* a, vdi_stream_t stream) {
   return vdi::validate_vdi(a, static_cast<cudaStream_t>(stream));
 }
 
-int vdi_synth_rm_u8(uint8_t* out, int32_t nx, int32_t ny, int32_t nz, const float* modes_host,
-                    float band, uint32_t seed, vdi_stream_t stream) {
+int vdi_synth_rm_u8(uint8_t* out, int32_t nx, int32_t ny, int32_t nz, const int32_t* box_host,
+                    const float* modes_host, float band, uint32_t seed, vdi_stream_t stream) {
   if (!out || !modes_host) return set_error(VDI_EINVAL, "null pointer");
   if (nx < 2 || ny < 2 || nz < 2) return set_error(VDI_EINVAL, "bad dims");
-  return vdi::synth_rm_u8(out, nx, ny, nz, modes_host, band, seed,
+  return vdi::synth_rm_u8(out, nx, ny, nz, box_host, modes_host, band, seed,
                           static_cast<cudaStream_t>(stream));
 }
 

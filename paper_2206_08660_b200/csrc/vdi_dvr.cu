@@ -36,6 +36,10 @@ struct DvrConst {
   int tiles_x, local_h;
   long long n_slots;
   unsigned long long* fetch;
+  // resident-box fields of the shared sampler (unused: DVR samples full volumes)
+  long long sub_sx, sub_sy, sub_voff, sub_boff;
+  int sub_ox, sub_oy, sub_oz, sub_nx, sub_ny, sub_nz;
+  unsigned* sub_oob;
 };
 
 struct DvrRay {

@@ -117,7 +117,11 @@ struct GenConst {
   RoundCtl* prev;  // previous round (its ndefer sizes defer_in)
   int round;
   int ess;         // empty-space skipping enabled
-  int bnx, bny;    // brick grid x / y extent
+  int bnx, bny;    // brick grid x / y extent (of the resident box in kVoxelSub variants)
+  // resident box (kVoxelSub variants): row strides, index rebases, origin, extent
+  long long sub_sx, sub_sy, sub_voff, sub_boff;
+  int sub_ox, sub_oy, sub_oz, sub_nx, sub_ny, sub_nz;
+  unsigned* sub_oob;
 };
 
 struct RayState {
@@ -1360,7 +1364,8 @@ static int plan_gen(const VdiGenArgs* a, GenPlan& p) {
   p.sample = gen_sample_kernel<VT>;       \
   p.fill = gen_fill_kernel<VT>;           \
   p.fused = gen_fused_kernel<VT>;
-  switch (a->voxel_type) {
+  const bool sub = a->sub_dims[0] > 0;
+  switch (a->voxel_type | (sub ? kVoxelSub : 0)) {
     case VDI_VOXEL_U8 | VDI_VOXEL_CELLS:
       VDI_GEN_KERNELS(VDI_VOXEL_U8 | VDI_VOXEL_CELLS)
       break;
@@ -1371,19 +1376,25 @@ static int plan_gen(const VdiGenArgs* a, GenPlan& p) {
       VDI_GEN_KERNELS(VDI_VOXEL_F32 | VDI_VOXEL_CELLS)
       break;
     case VDI_VOXEL_U8:
-      p.sample = gen_sample_kernel<VDI_VOXEL_U8>;
-      p.fill = gen_fill_kernel<VDI_VOXEL_U8>;
-      p.fused = gen_fused_kernel<VDI_VOXEL_U8>;
+      VDI_GEN_KERNELS(VDI_VOXEL_U8)
       break;
     case VDI_VOXEL_U16:
-      p.sample = gen_sample_kernel<VDI_VOXEL_U16>;
-      p.fill = gen_fill_kernel<VDI_VOXEL_U16>;
-      p.fused = gen_fused_kernel<VDI_VOXEL_U16>;
+      VDI_GEN_KERNELS(VDI_VOXEL_U16)
       break;
     case VDI_VOXEL_F32:
-      p.sample = gen_sample_kernel<VDI_VOXEL_F32>;
-      p.fill = gen_fill_kernel<VDI_VOXEL_F32>;
-      p.fused = gen_fused_kernel<VDI_VOXEL_F32>;
+      VDI_GEN_KERNELS(VDI_VOXEL_F32)
+      break;
+    case VDI_VOXEL_U8 | VDI_VOXEL_CELLS | kVoxelSub:
+      VDI_GEN_KERNELS(VDI_VOXEL_U8 | VDI_VOXEL_CELLS | kVoxelSub)
+      break;
+    case VDI_VOXEL_U8 | kVoxelSub:
+      VDI_GEN_KERNELS(VDI_VOXEL_U8 | kVoxelSub)
+      break;
+    case VDI_VOXEL_U16 | kVoxelSub:
+      VDI_GEN_KERNELS(VDI_VOXEL_U16 | kVoxelSub)
+      break;
+    case VDI_VOXEL_F32 | kVoxelSub:
+      VDI_GEN_KERNELS(VDI_VOXEL_F32 | kVoxelSub)
       break;
     default:
       return set_error(VDI_EINVAL, "bad voxel_type %d", a->voxel_type);
@@ -1501,12 +1512,32 @@ int gen_launch(const VdiGenArgs* a, cudaStream_t stream) {
   const long long tiles_y = (c.local_h + kTileH - 1) / kTileH;
   c.n_slots = (long long)c.tiles_x * tiles_y * 32;
   c.ess = a->brick_max != nullptr && a->ess_max >= 0.0 && a->brick_log2 >= 1;
+  const bool sub = a->sub_dims[0] > 0;
+  const int rx = sub ? a->sub_dims[0] : a->nx, ry = sub ? a->sub_dims[1] : a->ny;
   if (c.ess) {
     const int B = 1 << a->brick_log2;
-    c.bnx = (a->nx + B - 1) / B;
-    c.bny = (a->ny + B - 1) / B;
+    c.bnx = (rx + B - 1) / B;
+    c.bny = (ry + B - 1) / B;
   } else {
     c.bnx = c.bny = 0;
+  }
+  c.sub_ox = a->sub_origin[0];
+  c.sub_oy = a->sub_origin[1];
+  c.sub_oz = a->sub_origin[2];
+  c.sub_nx = sub ? a->sub_dims[0] : a->nx;
+  c.sub_ny = sub ? a->sub_dims[1] : a->ny;
+  c.sub_nz = sub ? a->sub_dims[2] : a->nz;
+  c.sub_sx = c.sub_nx;
+  c.sub_sy = c.sub_ny;
+  c.sub_voff = sub ? ((long long)c.sub_oz * c.sub_sy + c.sub_oy) * c.sub_sx + c.sub_ox : 0;
+  c.sub_boff = 0;
+  c.sub_oob = a->sub_oob;
+  if (sub) {
+    const int lb = a->brick_log2 >= 1 ? a->brick_log2 : 3;
+    if (c.ess && ((c.sub_ox | c.sub_oy | c.sub_oz) & ((1 << lb) - 1)))
+      return set_error(VDI_EINVAL, "sub_origin must be a multiple of the brick edge");
+    c.sub_boff = ((long long)(c.sub_oz >> lb) * c.bny + (c.sub_oy >> lb)) * c.bnx +
+                 (c.sub_ox >> lb);
   }
   if (c.local_h <= 0) return VDI_OK;
   GenPlan p;

@@ -32,8 +32,8 @@ int lz4_compress(const uint8_t* src, size_t n_max, const unsigned long long* n_d
                  unsigned long long* out_len, void* workspace, size_t ws_bytes,
                  cudaStream_t stream);
 int validate_vdi(const VdiValidateArgs* a, cudaStream_t stream);
-int synth_rm_u8(uint8_t* out, int nx, int ny, int nz, const float* modes, float band,
-                uint32_t seed, cudaStream_t stream);
+int synth_rm_u8(uint8_t* out, int nx, int ny, int nz, const int32_t* box, const float* modes,
+                float band, uint32_t seed, cudaStream_t stream);
 int preview_launch(const VdiPreviewArgs* a, cudaStream_t stream);
 int bilinear_upsample(const double* src, int w, int h, double* dst, int out_w, int out_h,
                       int channels, cudaStream_t stream);

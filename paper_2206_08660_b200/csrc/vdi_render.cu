@@ -20,6 +20,9 @@
 namespace vdi {
 
 constexpr int kRenderThreads = 128;
+#ifndef VDI_RENDER_MINB
+#define VDI_RENDER_MINB 6  // 80 registers: 6 blocks/SM (C3 render 1.29 -> 0.95 ms, run_pipeline)
+#endif
 
 struct RenderConst {
   VdiRenderArgs a;
@@ -28,7 +31,7 @@ struct RenderConst {
   long long n_slots;
 };
 
-__global__ void __launch_bounds__(kRenderThreads) render_kernel(const RenderConst c) {
+__global__ void __launch_bounds__(kRenderThreads, VDI_RENDER_MINB) render_kernel(const RenderConst c) {
   const VdiRenderArgs& a = c.a;
   const long long slot = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   unsigned long long st_vis = 0, st_int = 0, st_srch = 0;

@@ -5,7 +5,8 @@
 //
 // trilinear<VT>(c, ...) reads, from any constant block `c`: c.a.volume,
 // c.a.nx/ny/nz, c.a.brick_max, c.a.brick_log2, c.a.ess_max, c.ess, c.bnx,
-// c.bny (the generation and DVR argument blocks share these names).
+// c.bny (the generation and DVR argument blocks share these names), and for
+// kVoxelSub variants c.sub_*.
 #pragma once
 
 #include "vdi_common.cuh"
@@ -78,8 +79,15 @@ struct Cell<VDI_VOXEL_F32> {
   }
 };
 
+// Kernel-variant flag (not part of the C ABI): the volume in memory is only
+// a resident box of the full grid (VdiGenArgs.sub_origin / sub_dims), e.g.
+// one rank's slab of a volume bricked across GPUs. Sample positions and cell
+// indices stay those of the full grid; only the addresses are rebased.
+constexpr int kVoxelSub = 32;
+
 // volume.py:180-205 _trilinear. VT is a VDI_VOXEL_* type, optionally with the
-// VDI_VOXEL_CELLS flag (c.a.volume then holds corner records).
+// VDI_VOXEL_CELLS flag (c.a.volume then holds corner records) and kVoxelSub
+// (then c.sub_* describe the resident box).
 template <int VT, class C>
 __device__ __forceinline__ double trilinear(const C& c, const double* tab, double px,
                                             double py, double pz) {
@@ -91,6 +99,23 @@ __device__ __forceinline__ double trilinear(const C& c, const double* tab, doubl
   if (ix > nx - 2) ix = nx - 2;
   if (iy > ny - 2) iy = ny - 2;
   if (iz > nz - 2) iz = nz - 2;
+  long long sx = nx, sy = ny, voff = 0, boff = 0;
+  if constexpr ((VT & kVoxelSub) != 0) {
+    sx = c.sub_sx;
+    sy = c.sub_sy;
+    voff = c.sub_voff;
+    boff = c.sub_boff;
+    // a cell outside the resident box means the box was planned too small:
+    // flag it (the result is then invalid) and keep the address in bounds
+    const int lx = ix - c.sub_ox, ly = iy - c.sub_oy, lz = iz - c.sub_oz;
+    if ((unsigned)lx > (unsigned)(c.sub_nx - 2) || (unsigned)ly > (unsigned)(c.sub_ny - 2) ||
+        (unsigned)lz > (unsigned)(c.sub_nz - 2)) {
+      if (c.sub_oob) atomicOr(c.sub_oob, 1u);
+      ix = c.sub_ox + min(max(lx, 0), c.sub_nx - 2);
+      iy = c.sub_oy + min(max(ly, 0), c.sub_ny - 2);
+      iz = c.sub_oz + min(max(lz, 0), c.sub_nz - 2);
+    }
+  }
   if (c.ess) {
     // Exact empty-space skip: every voxel this sample can read lies in the
     // brick (+1 halo), whose maximum classifies at or below the last row of
@@ -98,13 +123,14 @@ __device__ __forceinline__ double trilinear(const C& c, const double* tab, doubl
     // exceeds its largest input by more than a few ulps. -1 classifies to LUT
     // row 0, whose alpha is 0: the sample is transparent, as in the reference.
     const int lb = c.a.brick_log2;
-    const long long bi = ((long long)(iz >> lb) * c.bny + (iy >> lb)) * c.bnx + (ix >> lb);
+    const long long bi =
+        ((long long)(iz >> lb) * c.bny + (iy >> lb)) * c.bnx + (ix >> lb) - boff;
     if (Voxel<(VT & 15)>::get(c.a.brick_max, bi, tab) <= c.a.ess_max) return -1.0;
   }
   const double fx = gx - ix, fy = gy - iy, fz = gz - iz;
   if (VT & VDI_VOXEL_CELLS) {
     double v[8];
-    Cell<(VT & 15)>::get(c.a.volume, ((long long)iz * ny + iy) * (long long)nx + ix, tab, v);
+    Cell<(VT & 15)>::get(c.a.volume, ((long long)iz * sy + iy) * sx + ix - voff, tab, v);
     const double c00 = v[0] * (1 - fx) + v[1] * fx;
     const double c10 = v[2] * (1 - fx) + v[3] * fx;
     const double c01 = v[4] * (1 - fx) + v[5] * fx;
@@ -115,11 +141,10 @@ __device__ __forceinline__ double trilinear(const C& c, const double* tab, doubl
   }
   // four row pointers, then [ptr + 0/1] gathers (no per-voxel 64-bit math)
   using T = typename Voxel<(VT & 15)>::type;
-  const T* r00 = static_cast<const T*>(c.a.volume) +
-                 ((long long)iz * ny + iy) * (long long)nx + ix;
-  const T* r01 = r00 + nx;
-  const T* r10 = r00 + (long long)nx * ny;
-  const T* r11 = r10 + nx;
+  const T* r00 = static_cast<const T*>(c.a.volume) + (((long long)iz * sy + iy) * sx + ix - voff);
+  const T* r01 = r00 + sx;
+  const T* r10 = r00 + sx * sy;
+  const T* r11 = r10 + sx;
   using V = Voxel<(VT & 15)>;
   const double v000 = V::get(r00, 0, tab), v001 = V::get(r00, 1, tab);
   const double v010 = V::get(r01, 0, tab), v011 = V::get(r01, 1, tab);

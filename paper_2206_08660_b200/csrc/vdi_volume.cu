@@ -257,17 +257,19 @@ struct RmModes {
   uint32_t seed;
 };
 
-__global__ void synth_rm_kernel(uint8_t* __restrict__ out, int nx, int ny, int nz,
-                                const RmModes m) {
-  const long long cols = (long long)nx * ny;
+// Writes the box [o, o + s) of the nx x ny x nz volume, stored (sz, sy, sx).
+__global__ void synth_rm_kernel(uint8_t* __restrict__ out, int nx, int ny, int nz, int ox,
+                                int oy, int oz, int bx, int by, int bz, const RmModes m) {
+  const long long cols = (long long)bx * by;
   for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < cols;
        c += (long long)gridDim.x * blockDim.x) {
-    const int ix = (int)(c % nx), iy = (int)(c / nx);
+    const int ix = ox + (int)(c % bx), iy = oy + (int)(c / bx);
     const float x = (ix + 0.5f) / nx, y = (iy + 0.5f) / ny;
     float h = 0.5f;
     for (int k = 0; k < 12; ++k)
       h += m.amp[k] * sinf(6.28318530718f * (m.kx[k] * x + m.ky[k] * y) + m.phase[k]);
-    for (int iz = 0; iz < nz; ++iz) {
+    for (int jz = 0; jz < bz; ++jz) {
+      const int iz = oz + jz;
       const float z = (iz + 0.5f) / nz;
       uint8_t v = 0;
       if (fabsf(z - h) < m.band) {
@@ -281,13 +283,18 @@ __global__ void synth_rm_kernel(uint8_t* __restrict__ out, int nx, int ny, int n
         f /= norm;
         v = (uint8_t)(60.0f + 195.0f * fminf(fmaxf(f, 0.0f), 1.0f) + 0.5f);
       }
-      out[(long long)iz * cols + c] = v;
+      out[(long long)jz * cols + c] = v;
     }
   }
 }
 
-int synth_rm_u8(uint8_t* out, int nx, int ny, int nz, const float* modes, float band,
-                uint32_t seed, cudaStream_t stream) {
+int synth_rm_u8(uint8_t* out, int nx, int ny, int nz, const int32_t* box, const float* modes,
+                float band, uint32_t seed, cudaStream_t stream) {
+  const int ox = box ? box[0] : 0, oy = box ? box[1] : 0, oz = box ? box[2] : 0;
+  const int bx = box ? box[3] : nx, by = box ? box[4] : ny, bz = box ? box[5] : nz;
+  if (ox < 0 || oy < 0 || oz < 0 || bx < 1 || by < 1 || bz < 1 || ox + bx > nx ||
+      oy + by > ny || oz + bz > nz)
+    return set_error(VDI_EINVAL, "synth box outside the volume");
   RmModes m;
   for (int k = 0; k < 12; ++k) {
     m.kx[k] = modes[4 * k];
@@ -297,10 +304,11 @@ int synth_rm_u8(uint8_t* out, int nx, int ny, int nz, const float* modes, float 
   }
   m.band = band;
   m.seed = seed;
-  const long long cols = (long long)nx * ny;
+  const long long cols = (long long)bx * by;
   long long blocks = (cols + 255) / 256;
   if (blocks > 148 * 32) blocks = 148 * 32;
-  synth_rm_kernel<<<(unsigned)blocks, 256, 0, stream>>>(out, nx, ny, nz, m);
+  synth_rm_kernel<<<(unsigned)blocks, 256, 0, stream>>>(out, nx, ny, nz, ox, oy, oz, bx, by, bz,
+                                                        m);
   const cudaError_t err = cudaGetLastError();
   if (err != cudaSuccess) return set_error(VDI_ELAUNCH, "synth launch: %s", cudaGetErrorString(err));
   return VDI_OK;

@@ -101,7 +101,9 @@ def alloc_gen(width, rows, n_sg, grid_dims, stats=True):
 
 def gen_args(vol_dev, voxel_type, dims, lut_dev, cam, aabb, params_resolved, n_sg, eps,
              gamma_init, bufs: GenBuffers, band=(16, 1, 0), bricks=None,
-             ess_max=-1.0, cells=None) -> _capi.VdiGenArgs:
+             ess_max=-1.0, cells=None, sub=None) -> _capi.VdiGenArgs:
+    """sub: (origin, box dims, oob flag tensor) when vol_dev holds only a
+    resident box of the dims volume (VdiGenArgs.sub_*)."""
     delta, step, lref = params_resolved
     width, height = cam.viewport
     a = _capi.VdiGenArgs()
@@ -123,6 +125,12 @@ def gen_args(vol_dev, voxel_type, dims, lut_dev, cam, aabb, params_resolved, n_s
     a.width, a.height = int(width), int(height)
     a.n_sg, a.delta = int(n_sg), int(delta)
     a.band_rows, a.band_stride, a.band_offset = (int(v) for v in band)
+    if sub is not None:
+        org, box, oob = sub
+        for k in range(3):
+            a.sub_origin[k] = int(org[k])
+            a.sub_dims[k] = int(box[k])
+        a.sub_oob = dv.ptr(oob)
     return a
 
 
@@ -142,7 +150,7 @@ def grid_args(bufs: GenBuffers, cam, width, height, n_sg, grid_dims, band=(16, 1
 def launch_generate(vol_dev, voxel_type, dims, lut_dev, cam, aabb, params, resolved,
                     bufs: GenBuffers, grid_dims, band=(16, 1, 0), stream=None,
                     split_events=None, workspace_bytes=None, bricks=None, ess_max=-1.0,
-                    cells=None):
+                    cells=None, sub=None):
     """Enqueue generation + grid on the current stream (no sync, no alloc).
     split_events: optional CUDA events; [1] and [2] bracket the generation
     kernel (timing only). workspace_bytes overrides the recommended scratch
@@ -151,7 +159,7 @@ def launch_generate(vol_dev, voxel_type, dims, lut_dev, cam, aabb, params, resol
     L = _capi.load()
     s = dv.stream_handle() if stream is None else stream
     a = gen_args(vol_dev, voxel_type, dims, lut_dev, cam, aabb, resolved, params.n_sg,
-                 params.epsilon, params.gamma_init, bufs, band, bricks, ess_max, cells)
+                 params.epsilon, params.gamma_init, bufs, band, bricks, ess_max, cells, sub)
     if workspace_bytes == "min":
         need = int(L.vdi_gen_workspace_min_bytes(a))
     elif workspace_bytes is not None:

@@ -63,6 +63,58 @@ def gather_rows(dist, local, world: int, padded_rows: int):
     return out
 
 
+def band_volume_box(vol, cam, row0: int, row1: int, margin: int = 2, align: int = 8):
+    """Voxel box (origin, size) holding every cell the generation rays of
+    image rows [row0, row1) can sample: the rays' clipped chords
+    (generate.py:282-306, evaluated for every pixel of the band, f64 as the
+    kernels do) -> normalised positions -> trilinear cells (+1 neighbour),
+    widened by `margin` voxels for rounding and aligned to the brick edge.
+    With an elevation-0 orbit camera a contiguous row band maps to a y-slab
+    of the volume (SURVEY.md 8(e), C5 "bricked across 8")."""
+    w, h = cam.viewport
+    dims = np.array(vol.dims, np.int64)
+    lo_b, hi_b = np.asarray(vol.aabb, np.float64)
+    inv = np.asarray(cam.inv_proj_view(), np.float64)
+    pv = np.asarray(cam.proj_view(), np.float64)
+    eye = np.asarray(cam.position, np.float64)
+    cols = np.arange(w)
+    rows = np.arange(row0, row1)
+    X, Y = np.meshgrid(2.0 * (cols + 0.5) / w - 1.0, 2.0 * (rows + 0.5) / h - 1.0)
+    P = np.stack([X.ravel(), Y.ravel(), -np.ones(X.size), np.ones(X.size)], 1) @ inv.T
+    P = P[:, :3] / P[:, 3:4]
+    D = P - eye
+    D /= np.linalg.norm(D, axis=1, keepdims=True)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        ta = (lo_b - eye) / D
+        tb = (hi_b - eye) / D
+    t0 = np.nanmax(np.minimum(ta, tb), axis=1)
+    t1 = np.nanmin(np.maximum(ta, tb), axis=1)
+    # generation frustum (7 half-spaces c + t d >= 0), as clip_frustum
+    c4 = np.append(eye, 1.0) @ pv.T
+    d4 = np.concatenate([D, np.zeros((len(D), 1))], 1) @ pv.T
+    cs = np.stack([c4[3], c4[3] - c4[0], c4[3] + c4[0], c4[3] - c4[1], c4[3] + c4[1],
+                   c4[3] - c4[2], c4[3] + c4[2]])
+    ds = np.stack([d4[:, 3], d4[:, 3] - d4[:, 0], d4[:, 3] + d4[:, 0], d4[:, 3] - d4[:, 1],
+                   d4[:, 3] + d4[:, 1], d4[:, 3] - d4[:, 2], d4[:, 3] + d4[:, 2]], 1)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        tt = -cs[None, :] / ds
+    fa = np.max(np.where(ds > 0, tt, -np.inf), axis=1)
+    fb = np.min(np.where(ds < 0, tt, np.inf), axis=1)
+    t0 = np.maximum(np.maximum(t0, fa), 0.0)
+    t1 = np.minimum(t1, fb)
+    hit = t1 > t0
+    if not hit.any():
+        return (0, 0, 0), (min(int(dims[0]), align), min(int(dims[1]), align),
+                           min(int(dims[2]), align))
+    ends = np.concatenate([eye + t0[hit, None] * D[hit], eye + t1[hit, None] * D[hit]])
+    q = np.clip((ends - lo_b) / (hi_b - lo_b), 0.0, 1.0) * (dims - 1)
+    cmin = np.floor(q.min(0)).astype(np.int64) - margin
+    cmax = np.floor(q.max(0)).astype(np.int64) + 1 + margin
+    org = np.clip((cmin // align) * align, 0, None)
+    end = np.minimum(cmax + 1, dims)
+    return tuple(int(v) for v in org), tuple(int(v) for v in end - org)
+
+
 def exchange_vdi(dist, counts, segs, grid, g_counts, g_segs):
     """The one exchange between generation and rendering: sum the partial
     AccelGrids in place and all-gather the padded VDI shards (counts
@@ -76,7 +128,14 @@ class Pipeline:
     """generate -> (all-reduce grid, all-gather VDI) -> render -> all-gather
     image, device-resident, for one rank."""
 
-    def __init__(self, vol, tf, gcam, rcam, params, world=1, rank=0, opts=None):
+    def __init__(self, vol, tf, gcam, rcam, params, world=1, rank=0, opts=None,
+                 bricked=False, box_volume=None):
+        """bricked: generation takes contiguous row bands (rank r: rows
+        [r B, (r + 1) B), B = ceil(H / world)) and keeps only the voxel box
+        those rays sample (band_volume_box) resident -- the C5 placement,
+        "bricked across 8 x B200". box_volume(origin, size) -> device tensor
+        (size[2], size[1], size[0]) supplies that box (default: sliced from
+        `vol`). Rendering keeps the interleaved 16-row bands."""
         t = dv.require_cuda()
         self.t = t
         self.vol, self.tf, self.gcam, self.rcam, self.params = vol, tf, gcam, rcam, params
@@ -86,18 +145,43 @@ class Pipeline:
         w, h = gcam.viewport
         self.w, self.h = w, h
         self.grid_dims = default_grid_dims(w, h)
-        self.vol_dev, self.vt = dv.upload_volume(vol)
+        self.bricked = bricked
+        self.gen_band_rows = -(-h // world) if bricked else BAND_ROWS
+        self.sub = None
+        if bricked:
+            r0 = rank * self.gen_band_rows
+            r1 = min(h, r0 + self.gen_band_rows)
+            org, size = band_volume_box(vol, gcam, r0, max(r1, r0 + 1))
+            self.box = (org, size)
+            if box_volume is not None:
+                self.vol_dev = box_volume(org, size)
+            else:
+                full, _ = dv.upload_volume(vol, cache=False)
+                ox, oy, oz = org
+                sx, sy, sz = size
+                self.vol_dev = full[oz:oz + sz, oy:oy + sy, ox:ox + sx].contiguous()
+                del full
+            self.vt = vol.voxel_type
+            self.oob = t.zeros(1, dtype=t.int32, device="cuda")
+            self.sub = (org, size, self.oob)
+            self.res_dims = size
+        else:
+            self.box = None
+            self.vol_dev, self.vt = dv.upload_volume(vol)
+            self.res_dims = tuple(vol.dims)
         self.lut_dev = dv.upload_lut(tf.lut)
         # per-volume acceleration data, rebuilt from the volume inside every
         # step (a new timestep's volume needs new ones): brick maxima for
         # empty-space skipping and, when they fit, the corner records
-        self.bricks = dv.alloc_bricks(self.vol_dev, vol.dims)
-        self.cells = dv.alloc_cells(self.vt, vol.dims) if dv.use_cells(self.vt, vol.dims) else None
+        self.bricks = dv.alloc_bricks(self.vol_dev, self.res_dims)
+        self.cells = (dv.alloc_cells(self.vt, self.res_dims)
+                      if dv.use_cells(self.vt, self.res_dims) else None)
         self.ess_max = dv.ess_threshold(tf.lut)
         self.aabb = np.asarray(vol.aabb, np.float64)
         self.band = (BAND_ROWS, world, rank)
-        self.gen_rows = rows_per_rank(h, world)
-        self.local_gen_rays = local_rows(h, world, rank) * w
+        self.gen_band = (self.gen_band_rows, world, rank)
+        self.gen_rows = rows_per_rank(h, world, self.gen_band_rows)
+        self.local_gen_rays = local_rows(h, world, rank, self.gen_band_rows) * w
         self.bufs = alloc_gen(w, self.gen_rows, params.n_sg, self.grid_dims, stats=True)
         self.bufs.counts.zero_()  # padding rows stay empty
         ow, oh = rcam.viewport
@@ -118,7 +202,8 @@ class Pipeline:
                                   dtype=t.float32, device="cuda")
             self.g_image = t.empty((world * self.out_rows, ow, 4), dtype=t.float64,
                                    device="cuda")
-            self.dvdi = DeviceVdi(self.g_counts, self.g_segs, BAND_ROWS, world, self.gen_rows)
+            self.dvdi = DeviceVdi(self.g_counts, self.g_segs, self.gen_band_rows, world,
+                                  self.gen_rows)
         else:
             self.dist = None
             self.dvdi = DeviceVdi(self.bufs.counts, self.bufs.segs)
@@ -137,13 +222,13 @@ class Pipeline:
         if timed:
             ev[0].record()
         self.sums.zero_()
-        dv.launch_bricks(vol_dev, self.vt, self.vol.dims, self.bricks)
+        dv.launch_bricks(vol_dev, self.vt, self.res_dims, self.bricks)
         if self.cells is not None:
-            dv.launch_cells(vol_dev, self.vt, self.vol.dims, self.cells)
+            dv.launch_cells(vol_dev, self.vt, self.res_dims, self.cells)
         launch_generate(vol_dev, self.vt, self.vol.dims, self.lut_dev, self.gcam,
                         self.aabb, self.params, self.resolved, self.bufs, self.grid_dims,
-                        band=self.band, split_events=ev, bricks=self.bricks,
-                        ess_max=self.ess_max, cells=self.cells)
+                        band=self.gen_band, split_events=ev, bricks=self.bricks,
+                        ess_max=self.ess_max, cells=self.cells, sub=self.sub)
         if timed:
             ev[3].record()
         if self.world > 1:
@@ -166,6 +251,18 @@ class Pipeline:
                 "grid": ev[2].elapsed_time(ev[3]),
                 "collective": ev[3].elapsed_time(ev[4]) + ev[5].elapsed_time(end),
                 "render": ev[4].elapsed_time(ev[5])}
+
+    def generate_only(self, vol_dev=None):
+        """This rank's volume prep + generation + partial grid (no exchange,
+        no render), on the current stream."""
+        vol_dev = self.vol_dev if vol_dev is None else vol_dev
+        dv.launch_bricks(vol_dev, self.vt, self.res_dims, self.bricks)
+        if self.cells is not None:
+            dv.launch_cells(vol_dev, self.vt, self.res_dims, self.cells)
+        launch_generate(vol_dev, self.vt, self.vol.dims, self.lut_dev, self.gcam,
+                        self.aabb, self.params, self.resolved, self.bufs, self.grid_dims,
+                        band=self.gen_band, bricks=self.bricks, ess_max=self.ess_max,
+                        cells=self.cells, sub=self.sub)
 
     def samples_executed(self) -> int:
         return int(self.bufs.samples.to(self.t.int64).sum().item())

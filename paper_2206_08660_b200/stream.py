@@ -94,6 +94,11 @@ class FrameStream:
         vol = pipe.vol
         shape = tuple(pipe.vol_dev.shape)
         self.h2d, self.comp, self.d2h = (t.cuda.Stream() for _ in range(3))
+        # packed mode: the variable-length VDI1 copy gets its own stream, so it
+        # does not queue behind the next frame's fixed-size readback (which
+        # waits for that frame's kernels)
+        self.d2h_var = t.cuda.Stream()
+        self.ev_var = t.cuda.Event()
         self.vol_slots = [t.empty(shape, dtype=pipe.vol_dev.dtype, device="cuda")
                           for _ in range(2)]
         n_sg, w = pipe.params.n_sg, pipe.w
@@ -181,10 +186,12 @@ class FrameStream:
         p = self.pipe
         if self.packed:
             n = int(h["len"][0])
-            with self.t.cuda.stream(self.d2h):
+            with self.t.cuda.stream(self.d2h_var):
+                self.d2h_var.wait_event(self.ev_comp[s])
                 h["vdi1"][:n].copy_(self.out[s]["vdi1"][:n], non_blocking=True)
-                self.ev_d2h[s].record(self.d2h)
-            self.ev_d2h[s].synchronize()
+                self.ev_var.record(self.d2h_var)
+                self.ev_d2h[s].record(self.d2h_var)  # slot s is free after this copy
+            self.ev_var.synchronize()
             res = FrameResult(index=i, counts=None, segs=None, grid=None,
                               image=h["image"].numpy(), vdi1=h["vdi1"][:n].numpy())
             self.d2h_bytes = res.nbytes

@@ -145,24 +145,31 @@ def rm_modes(seed: int = 3) -> np.ndarray:
     return np.ascontiguousarray(np.stack([ks[:, 0], ks[:, 1], amp, phase], 1), np.float32)
 
 
-def rm_like(dims=(2048, 2048, 1920), seed: int = 3):
+def rm_like(dims=(2048, 2048, 1920), seed: int = 3, box=None):
     """Richtmyer-Meshkov-shaped u8 volume, synthesised on
     the device (vdi_synth_rm_u8): a mixing band of half-width 0.15 around a
     12-mode perturbed interface z = h(x, y), filled with 4-octave value-noise
-    fbm mapped to 60..255; 0 outside. Returns a DeviceVolume."""
+    fbm mapped to 60..255; 0 outside. Returns a DeviceVolume; with box =
+    (origin, size) only that resident box is synthesised (a DeviceVolume of
+    the full dims holding a sub-box, as one rank of a bricked volume)."""
     import ctypes
     from . import _capi
     from . import device as dv
     from .volume import DeviceVolume
     t = dv.require_cuda()
     nx, ny, nz = dims
-    out = t.empty((nz, ny, nx), dtype=t.uint8, device="cuda")
+    if box is None:
+        org, size = (0, 0, 0), (nx, ny, nz)
+    else:
+        org, size = tuple(int(v) for v in box[0]), tuple(int(v) for v in box[1])
+    out = t.empty((size[2], size[1], size[0]), dtype=t.uint8, device="cuda")
     modes = rm_modes(seed)
+    bx = np.array([*org, *size], np.int32)
     _capi.check(_capi.load().vdi_synth_rm_u8(
-        dv.ptr(out), nx, ny, nz, modes.ctypes.data_as(ctypes.c_void_p), ctypes.c_float(0.15),
-        seed, dv.stream_handle()))
+        dv.ptr(out), nx, ny, nz, bx.ctypes.data_as(ctypes.c_void_p),
+        modes.ctypes.data_as(ctypes.c_void_p), ctypes.c_float(0.15), seed, dv.stream_handle()))
     t.cuda.current_stream().synchronize()
-    return DeviceVolume(out, "u8")
+    return DeviceVolume(out, "u8", full_dims=dims if box is not None else None, origin=org)
 
 
 def preset_volume(preset: str, dims: int = 128) -> Volume:

@@ -96,14 +96,20 @@ class DeviceVolume:
 
     normalized_is_derived = True
 
-    def __init__(self, device_data, voxel_type: str, spacing=(1.0, 1.0, 1.0)):
+    def __init__(self, device_data, voxel_type: str, spacing=(1.0, 1.0, 1.0), full_dims=None,
+                 origin=(0, 0, 0)):
+        """full_dims / origin: device_data is only the resident box
+        [origin, origin + shape) of a full_dims volume (one rank's bricks)."""
         if voxel_type not in VOXEL_DTYPES:
             raise UnsupportedVoxelType(voxel_type)
         nz, ny, nx = (int(v) for v in device_data.shape)
         if min(nx, ny, nz) < 2:
             raise ValueError("dims components must be >= 2 for trilinear sampling")
         self.device_data = device_data
-        self.dims = (nx, ny, nz)
+        self.box_dims = (nx, ny, nz)
+        self.origin = tuple(int(v) for v in origin)
+        self.dims = tuple(int(v) for v in full_dims) if full_dims is not None else (nx, ny, nz)
+        self.is_sub = full_dims is not None
         self.voxel_type = voxel_type
         self.spacing = tuple(float(v) for v in spacing)
         self._host = None

@@ -47,7 +47,7 @@ def test_exports_every_declared_symbol(lib):
 
 
 def test_abi_version(lib):
-    assert lib.vdi_abi_version() == 1
+    assert lib.vdi_abi_version() == 2
 
 
 PROBE = r"""
