@@ -1,11 +1,16 @@
 """Multi-rank host path on CPU (gloo, world size 2).
 
-Each rank computes its interleaved 16-row bands of the generation and of the
-render viewport (here with the CPU oracle standing in for the kernels, which
-cannot run without a GPU), then the ranks exchange through the very functions
-the NCCL pipeline uses (shard.exchange_vdi / shard.gather_rows). The gathered,
-band-interleaved VDI, the all-reduced AccelGrid and the gathered image must
-equal a single-process run bit for bit.
+Each rank computes its bands of the generation and of the render viewport
+(here with the CPU oracle standing in for the kernels, which cannot run
+without a GPU), then the ranks exchange through the very functions the NCCL
+pipeline uses (shard.exchange_vdi / shard.gather_rows). The gathered VDI,
+the all-reduced AccelGrid and the gathered image must equal a single-process
+run bit for bit.
+
+Layouts: "interleaved" (16-row bands, rank b % world) and "bricked"
+(contiguous generation bands, each rank sampling a volume in which every
+voxel outside its planned resident box, shard.band_volume_box, is poisoned:
+any ray that reached outside the box would change the result).
 """
 
 import os
@@ -64,7 +69,17 @@ def render(counts, segs, vol, gcam, rcam, grid, rows=None):
                          gcam.near, gcam.far, rows=rows)
 
 
-def rank_main(rank, world, port, out):
+def poisoned(vol, box):
+    """vol with every voxel outside box = (origin, size) set to 1.0."""
+    from paper_2206_08660_b200.volume import make_volume
+    (ox, oy, oz), (sx, sy, sz) = box
+    data = np.ones_like(vol.normalized)
+    data[oz:oz + sz, oy:oy + sy, ox:ox + sx] = vol.normalized[oz:oz + sz, oy:oy + sy,
+                                                             ox:ox + sx]
+    return make_volume(data, "f32")
+
+
+def rank_main(rank, world, port, out, layout="interleaved"):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -73,9 +88,15 @@ def rank_main(rank, world, port, out):
         w, h = gcam.viewport
         dims = default_grid_dims(w, h)
         pa, pb = oracle.depth_consts(gcam.near, gcam.far)
-        mine = shard.band_rows(h, world, rank)
-        per = shard.rows_per_rank(h, world)
-        local = gen(vol, tf, gcam, n_sg, res, params, rows=mine)
+        band = -(-h // world) if layout == "bricked" else shard.BAND_ROWS
+        mine = shard.band_rows(h, world, rank, band)
+        per = shard.rows_per_rank(h, world, band)
+        gvol = vol
+        if layout == "bricked":
+            box = shard.band_volume_box(vol, gcam, int(mine[0]), int(mine[-1]) + 1)
+            assert box[1][1] < vol.dims[1]  # a real slab, not the whole volume
+            gvol = poisoned(vol, box)
+        local = gen(gvol, tf, gcam, n_sg, res, params, rows=mine)
         # local shard, padded to rows_per_rank rows (what the gen kernel writes)
         counts = np.zeros((per, w), np.int32)
         counts[: len(mine)] = local["counts"][mine]
@@ -89,7 +110,7 @@ def rank_main(rank, world, port, out):
         g_segs = torch.empty((world * per * w, segs.shape[1]), dtype=torch.float32)
         shard.exchange_vdi(dist, t_counts, t_segs, t_grid, g_counts, g_segs)
         # band-interleaved storage -> natural rows
-        st = shard.storage_rows(h, world)
+        st = shard.storage_rows(h, world, band)
         full_counts = g_counts.numpy()[st]
         full_segs = from_list_soa(g_segs.numpy().reshape(world * per, w, -1)[st].reshape(h * w, -1),
                                   n_sg).reshape(h, w, n_sg, 6)
@@ -115,10 +136,10 @@ def free_port():
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("world", [2])
-def test_sharded_generate_render_equals_single_process(tmp_path, world):
+@pytest.mark.parametrize("world,layout", [(2, "interleaved"), (2, "bricked")])
+def test_sharded_generate_render_equals_single_process(tmp_path, world, layout):
     out = str(tmp_path / "rank0.npz")
-    mp.start_processes(rank_main, args=(world, free_port(), out), nprocs=world,
+    mp.start_processes(rank_main, args=(world, free_port(), out, layout), nprocs=world,
                        start_method="spawn", join=True)
     got = np.load(out)
     vol, tf, gcam, rcam, n_sg, res, params = scene()
