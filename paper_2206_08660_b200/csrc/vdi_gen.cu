@@ -1483,7 +1483,9 @@ size_t gen_workspace_bytes(const VdiGenArgs* a, int recommended) {
   const size_t fused_all = sizeof(float4) * (size_t)p.sms * p.per_sm_fused * kGenThreads *
                            (size_t)p.max_steps;
   if (rec < fused_all) rec = fused_all;
-  const size_t cap = (size_t)24 << 30;
+  // cache cap: 24 GiB unless VDI_GEN_WS_GB says otherwise (A/B switch)
+  size_t cap = (size_t)24 << 30;
+  if (const char* env = getenv("VDI_GEN_WS_GB")) cap = (size_t)atoll(env) << 30;
   if (rec > cap) rec = cap;
   if (rec < min_cache) rec = min_cache;
   return p.off_cache + (recommended ? rec : min_cache);
