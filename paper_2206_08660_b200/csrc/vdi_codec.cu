@@ -8,9 +8,9 @@
 // camera and AABB) | counts as u16 | valid supersegments as AoS f32 in list
 // order | grid as u32. The packed-segment offsets are an exclusive scan of
 // the counts: a per-block scan (1024 lists) + a one-block scan of the block
-// totals; the scatter then walks each block's contiguous output range word
-// by word (coalesced stores), locating the source list by binary search in
-// the block's shared prefix array.
+// totals; the scatter then fills each block's contiguous output range, one
+// thread per supersegment (24 contiguous bytes), locating the source list by
+// binary search in the block's shared prefix array.
 //
 // LZ4. The reference's compressor is one serial greedy parse with a 64 Ki
 // hash table. Here the input is cut into 32 KiB chunks, one warp each; a warp
@@ -171,22 +171,24 @@ __global__ void enc_segs_kernel(const VdiEncodeArgs a, const unsigned long long*
   const bool aligned = ((reinterpret_cast<uintptr_t>(a.out) + base_byte) & 3u) == 0;
   uint8_t* dst = a.out + base_byte;
   const int stride = list_stride(a.n_sg);
-  const long long words = 6ll * bt;
-  for (long long k = threadIdx.x; k < words; k += blockDim.x) {
-    const int s = (int)(k / 6), ch = (int)(k - 6ll * s);
-    int lo = 0, hi = kEncBlock - 1;  // list j with s_pre[j] <= s < s_pre[j + 1]
+  // one thread per supersegment: locate its list once, write its 6 words
+  for (int sidx = threadIdx.x; sidx < bt; sidx += blockDim.x) {
+    int lo = 0, hi = kEncBlock - 1;  // list j with s_pre[j] <= sidx < s_pre[j + 1]
     while (lo < hi) {
       const int mid = (lo + hi + 1) >> 1;
-      if (s_pre[mid] <= s) lo = mid;
+      if (s_pre[mid] <= sidx) lo = mid;
       else hi = mid - 1;
     }
-    const int j = s - s_pre[lo];
+    const int j = sidx - s_pre[lo];
     const float* ls = a.segs + s_src[lo] * (long long)stride;
-    float f;
-    if (ch == 0) f = ls[front_off(a.n_sg) + j];
-    else if (ch == 1) f = ls[back_off(a.n_sg) + j];
-    else f = ls[4 * j + (ch - 2)];
-    store_word(dst + 4 * k, __float_as_uint(f), aligned);
+    const float4 c4 = reinterpret_cast<const float4*>(ls)[j];
+    uint8_t* o = dst + 24ll * sidx;
+    store_word(o, __float_as_uint(ls[front_off(a.n_sg) + j]), aligned);
+    store_word(o + 4, __float_as_uint(ls[back_off(a.n_sg) + j]), aligned);
+    store_word(o + 8, __float_as_uint(c4.x), aligned);
+    store_word(o + 12, __float_as_uint(c4.y), aligned);
+    store_word(o + 16, __float_as_uint(c4.z), aligned);
+    store_word(o + 20, __float_as_uint(c4.w), aligned);
   }
 }
 

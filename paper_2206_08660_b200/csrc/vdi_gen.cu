@@ -1483,12 +1483,20 @@ size_t gen_workspace_bytes(const VdiGenArgs* a, int recommended) {
   const size_t fused_all = sizeof(float4) * (size_t)p.sms * p.per_sm_fused * kGenThreads *
                            (size_t)p.max_steps;
   if (rec < fused_all) rec = fused_all;
-  // cache cap: 24 GiB unless VDI_GEN_WS_GB says otherwise (A/B switch)
+  // cache cap: half of the device memory free now, at least 24 GiB. Rays
+  // that do not fit are deferred to another round and re-sampled, which is
+  // what makes a small cap expensive (C5: 24 GiB -> 989 ms, 64 GiB -> 426 ms,
+  // 120 GiB -> 372 ms of generation). VDI_GEN_WS_GB overrides (A/B switch).
+  if (!recommended) return p.off_cache + min_cache;  // (no device query on the launch path)
   size_t cap = (size_t)24 << 30;
+  {
+    size_t free_b = 0, total_b = 0;
+    if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess && free_b / 2 > cap) cap = free_b / 2;
+  }
   if (const char* env = getenv("VDI_GEN_WS_GB")) cap = (size_t)atoll(env) << 30;
   if (rec > cap) rec = cap;
   if (rec < min_cache) rec = min_cache;
-  return p.off_cache + (recommended ? rec : min_cache);
+  return p.off_cache + rec;
 }
 
 int gen_launch(const VdiGenArgs* a, cudaStream_t stream) {

@@ -164,6 +164,9 @@ def launch_generate(vol_dev, voxel_type, dims, lut_dev, cam, aabb, params, resol
         need = int(L.vdi_gen_workspace_min_bytes(a))
     elif workspace_bytes is not None:
         need = int(workspace_bytes)
+    elif bufs.workspace is not None:
+        # sized once (the recommendation depends on the free device memory)
+        need = int(L.vdi_gen_workspace_min_bytes(a))
     else:
         need = int(L.vdi_gen_workspace_bytes(a))
     if bufs.workspace is None or bufs.workspace.numel() < need:
