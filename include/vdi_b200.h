@@ -316,6 +316,13 @@ int vdi_volume_brick_max(const void* volume, int32_t voxel_type, int32_t nx, int
 size_t vdi_volume_cells_bytes(int32_t voxel_type, int32_t nx, int32_t ny, int32_t nz);
 int vdi_volume_cells(const void* volume, int32_t voxel_type, int32_t nx, int32_t ny, int32_t nz,
                      void* out, vdi_stream_t stream);
+/* The same, skipping the cells of bricks whose vdi_volume_brick_max()
+ * value normalises to <= ess_max: the samplers' empty-space test skips those
+ * samples before any corner-record load, so their records are never read
+ * (and are left with any content). */
+int vdi_volume_cells_masked(const void* volume, int32_t voxel_type, int32_t nx, int32_t ny,
+                            int32_t nz, const void* brick_max, int32_t brick_log2, double ess_max,
+                            void* out, vdi_stream_t stream);
 
 /* Synthetic input for config C5 (not a reference function): a
  * Richtmyer-Meshkov-shaped u8 volume (nz, ny, nx) written on the device.

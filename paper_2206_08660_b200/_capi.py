@@ -113,7 +113,7 @@ EXPORTS = ["vdi_last_error", "vdi_abi_version", "vdi_gen_workspace_bytes",
            "vdi_encode_workspace_bytes", "vdi_encode_vdi1", "vdi_lz4_max_bytes",
            "vdi_lz4_workspace_bytes", "vdi_lz4_compress", "vdi_validate", "vdi_synth_rm_u8", "vdi_find_first_batch",
            "vdi_volume_brick_max", "vdi_selftest_arith", "vdi_segs_to_aos",
-           "vdi_segs_from_aos", "vdi_volume_cells_bytes", "vdi_volume_cells"]
+           "vdi_segs_from_aos", "vdi_volume_cells_bytes", "vdi_volume_cells", "vdi_volume_cells_masked"]
 
 _lib = None
 
@@ -162,6 +162,8 @@ def load():
     L.vdi_volume_cells_bytes.restype = ctypes.c_size_t
     L.vdi_volume_cells.argtypes = [_P, _I, _I, _I, _I, _P, _P]
     L.vdi_volume_cells.restype = ctypes.c_int
+    L.vdi_volume_cells_masked.argtypes = [_P, _I, _I, _I, _I, _P, _I, _D, _P, _P]
+    L.vdi_volume_cells_masked.restype = ctypes.c_int
     L.vdi_selftest_arith.argtypes = [ctypes.c_int64, ctypes.c_uint64, _P, _P]
     L.vdi_selftest_arith.restype = ctypes.c_int
     L.vdi_segs_to_aos.argtypes = [_P, _P, ctypes.c_int64, _I, _P]

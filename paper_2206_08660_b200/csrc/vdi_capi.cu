@@ -203,6 +203,17 @@ int vdi_volume_cells(const void* volume, int32_t voxel_type, int32_t nx, int32_t
   return vdi::volume_cells(volume, voxel_type, nx, ny, nz, out, static_cast<cudaStream_t>(stream));
 }
 
+int vdi_volume_cells_masked(const void* volume, int32_t voxel_type, int32_t nx, int32_t ny,
+                            int32_t nz, const void* brick_max, int32_t brick_log2, double ess_max,
+                            void* out, vdi_stream_t stream) {
+  if (!volume || !out || !brick_max) return set_error(VDI_EINVAL, "null device pointer");
+  if (nx < 2 || ny < 2 || nz < 2) return set_error(VDI_EINVAL, "bad sizes");
+  if (brick_log2 < 2 || brick_log2 > 10) return set_error(VDI_EINVAL, "bad brick_log2");
+  if (reinterpret_cast<uintptr_t>(out) & 31) return set_error(VDI_EINVAL, "cells not 32-byte aligned");
+  return vdi::volume_cells(volume, voxel_type, nx, ny, nz, out, static_cast<cudaStream_t>(stream),
+                           brick_max, brick_log2, ess_max);
+}
+
 int vdi_selftest_arith(int64_t n, uint64_t seed, unsigned long long* bad,
                        vdi_stream_t stream) {
   if (!bad || n < 0) return set_error(VDI_EINVAL, "bad arguments");

@@ -122,6 +122,7 @@ struct GenConst {
   long long sub_sx, sub_sy, sub_voff, sub_boff;
   int sub_ox, sub_oy, sub_oz, sub_nx, sub_ny, sub_nz;
   unsigned* sub_oob;
+  int chain_levels;  // bisect replays starting below this level use the down-chain shape
 };
 
 struct RayState {
@@ -884,6 +885,7 @@ __global__ void __launch_bounds__(kThreads, kMinB) gen_bisect_kernel(const GenCo
   // bisection state (generate.py:230-236)
   double low = 0.0, high = 0.0;
   int last_n = 0, high_n = 0, passes = 0, samples = 0;
+  bool chain = false;  // this replay's speculation shape (see the top of the loop)
   CountState q[kG];
   double gam[kG];
 
@@ -935,13 +937,23 @@ __global__ void __launch_bounds__(kThreads, kMinB) gen_bisect_kernel(const GenCo
         have = false;
         continue;
       }
+      // speculation shape: the tree (node, both children) or, while the
+      // bisection is in its first levels, where it goes down almost always
+      // (tools/bisect_paths.py), the chain node -> down -> down, which covers
+      // kG levels instead of kLevels when the prediction holds
+      chain = kLevels == 2 && (passes - 1) < c.chain_levels;
       double lo[kG], hi[kG];
       lo[0] = low;
       hi[0] = high;
 #pragma unroll
       for (int i = 0; i < kG; ++i) {
         gam[i] = 0.5 * (lo[i] + hi[i]);
-        if (2 * i + 2 < kG) {
+        if (chain) {
+          if (i + 1 < kG) {
+            lo[i + 1] = lo[i];
+            hi[i + 1] = gam[i];
+          }
+        } else if (2 * i + 2 < kG) {
           lo[2 * i + 1] = gam[i];
           hi[2 * i + 1] = hi[i];
           lo[2 * i + 2] = lo[i];
@@ -1109,7 +1121,7 @@ __global__ void __launch_bounds__(kThreads, kMinB) gen_bisect_kernel(const GenCo
     // replay R's control flow over the speculated counts (generate.py:237-273)
     int node = 0;
     bool fin = false;
-    for (int lvl = 0; lvl < kLevels; ++lvl) {
+    for (int lvl = 0; lvl < kG && node >= 0; ++lvl) {
       if (lvl > 0 && fabs(high - low) < c.a.eps) break;  // handled at the top
       // static selection keeps q[] / gam[] in registers
       int n = 0, kend = 0;
@@ -1126,11 +1138,11 @@ __global__ void __launch_bounds__(kThreads, kMinB) gen_bisect_kernel(const GenCo
       last_n = n;
       if (n > n_sg) {
         low = g;
-        node = 2 * node + 1;
+        node = chain ? -1 : (2 * node + 1 < kG ? 2 * node + 1 : -1);
       } else if (n < n_sg - c.a.delta) {
         high = g;
         high_n = n;
-        node = 2 * node + 2;
+        node = chain ? (node + 1 < kG ? node + 1 : -1) : (2 * node + 2 < kG ? 2 * node + 2 : -1);
       } else {
         rec->g_final = g;  // window hit: this pass's segments
         rec->mode_final = kCount;
@@ -1542,6 +1554,8 @@ int gen_launch(const VdiGenArgs* a, cudaStream_t stream) {
   c.sub_voff = sub ? ((long long)c.sub_oz * c.sub_sy + c.sub_oy) * c.sub_sx + c.sub_ox : 0;
   c.sub_boff = 0;
   c.sub_oob = a->sub_oob;
+  c.chain_levels = 0;
+  if (const char* env = getenv("VDI_CHAIN_LEVELS")) c.chain_levels = atoi(env);
   if (sub) {
     const int lb = a->brick_log2 >= 1 ? a->brick_log2 : 3;
     if (c.ess && ((c.sub_ox | c.sub_oy | c.sub_oz) & ((1 << lb) - 1)))

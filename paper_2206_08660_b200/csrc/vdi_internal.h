@@ -44,7 +44,8 @@ int find_first_batch(const float* fronts, const float* backs, const int32_t* cou
 int brick_max(const void* volume, int voxel_type, int nx, int ny, int nz, int log2b, void* out,
               cudaStream_t stream);
 int volume_cells(const void* volume, int voxel_type, int nx, int ny, int nz, void* out,
-                 cudaStream_t stream);
+                 cudaStream_t stream, const void* brick_max = nullptr, int brick_log2 = 0,
+                 double ess_max = -1.0);
 int selftest_arith(long long n, unsigned long long seed, unsigned long long* bad,
                    cudaStream_t stream);
 int segs_convert(const float* src, float* dst, int64_t n_lists, int32_t n_sg, bool to_aos,

@@ -9,6 +9,7 @@
 // vdi_gen.cu). The reduction is integer/float max, so it is exact.
 #include "vdi_common.cuh"
 #include "vdi_internal.h"
+#include <type_traits>
 
 namespace vdi {
 
@@ -100,15 +101,35 @@ struct CellRecord<float> {
   }
 };
 
+// Brick mask for the corner records: a brick whose maximum classifies to
+// alpha 0 (the generation / DVR empty-space test, vdi_sample.cuh) is never
+// sampled, so its cells need no record. bmax == nullptr: write every cell.
+template <typename T>
+struct CellMask {
+  const T* bmax;
+  int lb, bnx, bny;
+  double ess_max;
+  __device__ __forceinline__ bool skip(int x, int y, int z) const {
+    if (!bmax) return false;
+    const T v = __ldg(bmax + ((long long)(z >> lb) * bny + (y >> lb)) * bnx + (x >> lb));
+    double d;
+    if (sizeof(T) == 1) d = (double)__fdiv_rn((float)v, 255.0f);
+    else if (sizeof(T) == 2) d = (double)__fdiv_rn((float)v, 65535.0f);
+    else d = (double)v;
+    return d <= ess_max;
+  }
+};
+
 template <typename T>
 __global__ void cells_kernel(const T* __restrict__ vol, void* __restrict__ out, int nx, int ny,
-                             int nz) {
+                             int nz, const CellMask<T> mask) {
   const long long n = (long long)nx * ny * nz;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x) {
     const int x = (int)(i % nx);
     const long long yz = i / nx;
     const int y = (int)(yz % ny), z = (int)(yz / ny);
+    if (mask.skip(x, y, z)) continue;
     const int dx = x + 1 < nx ? 1 : 0;
     const long long dy = y + 1 < ny ? nx : 0;
     const long long dz = z + 1 < nz ? (long long)nx * ny : 0;
@@ -130,7 +151,7 @@ __global__ void cells_kernel(const T* __restrict__ vol, void* __restrict__ out, 
 // from one aligned 32-bit word plus the next byte of each of the 4 (y, z)
 // rows, and stores them as two 16-byte writes.
 __global__ void cells_u8x4_kernel(const uint8_t* __restrict__ vol, uint4* __restrict__ out,
-                                  int nx, int ny, int nz) {
+                                  int nx, int ny, int nz, const CellMask<uint8_t> mask) {
   const int qx = nx >> 2;
   const long long n = (long long)qx * ny * nz;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
@@ -138,6 +159,7 @@ __global__ void cells_u8x4_kernel(const uint8_t* __restrict__ vol, uint4* __rest
     const int x = (int)(i % qx) * 4;
     const long long yz = i / qx;
     const int y = (int)(yz % ny), z = (int)(yz / ny);
+    if (mask.skip(x, y, z)) continue;  // the 4 cells share a brick (x % 4 == 0, edge >= 4)
     const long long base = yz * nx + x;
     const long long dy = y + 1 < ny ? nx : 0;
     const long long dz = z + 1 < nz ? (long long)nx * ny : 0;
@@ -171,7 +193,15 @@ __global__ void cells_u8x4_kernel(const uint8_t* __restrict__ vol, uint4* __rest
 }
 
 int volume_cells(const void* volume, int voxel_type, int nx, int ny, int nz, void* out,
-                 cudaStream_t stream) {
+                 cudaStream_t stream, const void* brick_max, int brick_log2, double ess_max) {
+  const bool masked = brick_max != nullptr && ess_max >= 0.0 && brick_log2 >= 2;
+  const int B = 1 << (brick_log2 > 0 ? brick_log2 : 3);
+  const int bnx = (nx + B - 1) / B, bny = (ny + B - 1) / B;
+  auto mk = [&](auto* tag) {
+    using T = std::remove_pointer_t<decltype(tag)>;
+    return CellMask<T>{masked ? static_cast<const T*>(brick_max) : nullptr, brick_log2, bnx, bny,
+                       ess_max};
+  };
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -182,18 +212,19 @@ int volume_cells(const void* volume, int voxel_type, int nx, int ny, int nz, voi
     case VDI_VOXEL_U8:
       if (nx % 4 == 0)
         cells_u8x4_kernel<<<(unsigned)((blocks + 3) / 4), 256, 0, stream>>>(
-            static_cast<const uint8_t*>(volume), static_cast<uint4*>(out), nx, ny, nz);
+            static_cast<const uint8_t*>(volume), static_cast<uint4*>(out), nx, ny, nz,
+            mk((uint8_t*)nullptr));
       else
         cells_kernel<<<(unsigned)blocks, 256, 0, stream>>>(static_cast<const uint8_t*>(volume),
-                                                           out, nx, ny, nz);
+                                                           out, nx, ny, nz, mk((uint8_t*)nullptr));
       break;
     case VDI_VOXEL_U16:
       cells_kernel<<<(unsigned)blocks, 256, 0, stream>>>(static_cast<const uint16_t*>(volume),
-                                                         out, nx, ny, nz);
+                                                         out, nx, ny, nz, mk((uint16_t*)nullptr));
       break;
     case VDI_VOXEL_F32:
       cells_kernel<<<(unsigned)blocks, 256, 0, stream>>>(static_cast<const float*>(volume), out,
-                                                         nx, ny, nz);
+                                                         nx, ny, nz, mk((float*)nullptr));
       break;
     default:
       return set_error(VDI_EINVAL, "bad voxel_type %d", voxel_type);

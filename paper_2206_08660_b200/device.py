@@ -177,8 +177,15 @@ def alloc_cells(voxel_type: str, dims):
     return torch().empty(cells_bytes(voxel_type, dims), dtype=torch().uint8, device="cuda")
 
 
-def launch_cells(vol_dev, voxel_type: str, dims, out) -> None:
+def launch_cells(vol_dev, voxel_type: str, dims, out, bricks=None, ess_max=-1.0) -> None:
+    """Corner records; with brick maxima and an ESS threshold, the records of
+    bricks the samplers always skip are not written (vdi_volume_cells_masked)."""
     nx, ny, nz = (int(v) for v in dims)
+    if bricks is not None and ess_max >= 0.0:
+        _capi.check(_capi.load().vdi_volume_cells_masked(
+            ptr(vol_dev), _capi.VOXEL[voxel_type], nx, ny, nz, ptr(bricks), BRICK_LOG2,
+            float(ess_max), ptr(out), stream_handle()))
+        return
     _capi.check(_capi.load().vdi_volume_cells(ptr(vol_dev), _capi.VOXEL[voxel_type], nx, ny, nz,
                                               ptr(out), stream_handle()))
 
@@ -200,16 +207,19 @@ _cells = {}
 
 
 def volume_cells(vol_dev, voxel_type: str, dims):
-    """Corner records of a device volume, cached for as long as it lives."""
-    key = (vol_dev.data_ptr(), tuple(dims), voxel_type)
+    """Corner records of a device volume, cached for as long as it lives. A
+    new volume of the same shape (a new timestep, or an uncached upload)
+    rebuilds into the previous buffer instead of allocating another
+    8 x volume-sized block."""
+    key = (tuple(dims), voxel_type)
     hit = _cells.get(key)
-    if hit is not None and hit[0]() is vol_dev:
+    if hit is not None and hit[0]() is vol_dev and hit[2] == vol_dev.data_ptr():
         return hit[1]
-    for k in [k for k, v in _cells.items() if v[0]() is None]:
+    out = hit[1] if hit is not None else alloc_cells(voxel_type, dims)
+    for k in [k for k in _cells if k != key]:
         del _cells[k]
-    out = alloc_cells(voxel_type, dims)
     launch_cells(vol_dev, voxel_type, dims, out)
-    _cells[key] = (weakref.ref(vol_dev), out)
+    _cells[key] = (weakref.ref(vol_dev), out, vol_dev.data_ptr())
     return out
 
 

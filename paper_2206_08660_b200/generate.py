@@ -182,6 +182,29 @@ def launch_generate(vol_dev, voxel_type, dims, lut_dev, cam, aabb, params, resol
     _capi.check(L.vdi_grid_launch(g, s))
 
 
+_shared_ws = {}
+
+
+def shared_workspace(nbytes: int):
+    """One generation scratch buffer per device, reused by every
+    generate_vdi call (in stream order) and grown when a call needs more:
+    the recommended size can be tens of GB, and allocating it per call
+    thrashes the caching allocator."""
+    t = dv.torch()
+    dev = t.cuda.current_device()
+    ws = _shared_ws.get(dev)
+    if ws is None or ws.numel() < nbytes:
+        _shared_ws.pop(dev, None)
+        ws = t.empty(nbytes, dtype=t.uint8, device="cuda")
+        _shared_ws[dev] = ws
+    return ws
+
+
+def release_workspace() -> None:
+    """Drop the shared generation scratch (returns it to torch's cache)."""
+    _shared_ws.clear()
+
+
 def generate_vdi(vol, tf, cam, params: GenParams | None = None, grid_dims=None,
                  with_stats: bool = False, *, cache_volume: bool = True):
     """Generate a Vdi + AccelGrid from camera `cam` (one ray per viewport pixel).
@@ -199,6 +222,9 @@ def generate_vdi(vol, tf, cam, params: GenParams | None = None, grid_dims=None,
     vol_dev, vt = dv.upload_volume(vol, cache=cache_volume)
     lut_dev = dv.upload_lut(tf.lut)
     bufs = alloc_gen(width, height, params.n_sg, grid_dims, stats=with_stats)
+    a = gen_args(vol_dev, vt, vol.dims, lut_dev, cam, aabb, resolved, params.n_sg,
+                 params.epsilon, params.gamma_init, bufs)
+    bufs.workspace = shared_workspace(int(_capi.load().vdi_gen_workspace_bytes(a)))
     bricks = dv.volume_bricks(vol_dev, vt, vol.dims)
     cells = dv.volume_cells(vol_dev, vt, vol.dims) if dv.use_cells(vt, vol.dims) else None
     launch_generate(vol_dev, vt, vol.dims, lut_dev, cam, aabb, params, resolved, bufs,

@@ -224,7 +224,7 @@ class Pipeline:
         self.sums.zero_()
         dv.launch_bricks(vol_dev, self.vt, self.res_dims, self.bricks)
         if self.cells is not None:
-            dv.launch_cells(vol_dev, self.vt, self.res_dims, self.cells)
+            dv.launch_cells(vol_dev, self.vt, self.res_dims, self.cells, self.bricks, self.ess_max)
         launch_generate(vol_dev, self.vt, self.vol.dims, self.lut_dev, self.gcam,
                         self.aabb, self.params, self.resolved, self.bufs, self.grid_dims,
                         band=self.gen_band, split_events=ev, bricks=self.bricks,
@@ -258,7 +258,7 @@ class Pipeline:
         vol_dev = self.vol_dev if vol_dev is None else vol_dev
         dv.launch_bricks(vol_dev, self.vt, self.res_dims, self.bricks)
         if self.cells is not None:
-            dv.launch_cells(vol_dev, self.vt, self.res_dims, self.cells)
+            dv.launch_cells(vol_dev, self.vt, self.res_dims, self.cells, self.bricks, self.ess_max)
         launch_generate(vol_dev, self.vt, self.vol.dims, self.lut_dev, self.gcam,
                         self.aabb, self.params, self.resolved, self.bufs, self.grid_dims,
                         band=self.gen_band, bricks=self.bricks, ess_max=self.ess_max,

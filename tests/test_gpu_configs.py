@@ -70,3 +70,20 @@ def test_c4_render_sweep(c4, deg):
     assert np.array_equal(lv[ROWS], ref["lists_visited"][ROWS])
     assert np.array_equal(si[ROWS], ref["segs_intersected"][ROWS])
     assert np.array_equal(ls[ROWS], ref["lists_searched"][ROWS])
+
+
+def test_c3_pipeline_masked_cells_match_public_api():
+    """The bench pipeline builds corner records only for bricks the
+    empty-space test can sample (vdi_volume_cells_masked); its VDI must equal
+    the public generate_vdi's (full corner records) bit for bit."""
+    from paper_2206_08660_b200 import shard
+    vol, tf, gcam, rcam, n_sg = synth.config("C3")
+    params = vb.GenParams(n_sg=n_sg)
+    vdi, grid = vb.generate_vdi(vol, tf, gcam, params)
+    pipe = shard.Pipeline(vol, tf, gcam, rcam, params)
+    assert pipe.cells is not None
+    pipe.step()
+    d = vdi.device()
+    assert torch.equal(pipe.bufs.counts, d.counts)
+    assert torch.equal(pipe.bufs.segs, d.segs)
+    assert torch.equal(pipe.bufs.grid, grid.device())
