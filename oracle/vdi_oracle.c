@@ -329,6 +329,18 @@ static int gen_list_pass(const ray_ctx* r, double gamma, int capped,
   return count;
 }
 
+/* Analysis hook (tools/bisect_predict.py): when set, every counting pass of
+ * ray oidx appends (gamma, n) at g_trace[oidx * 48 + 2 * pass]. */
+static double* g_trace = NULL;
+static _Thread_local int64_t g_trace_ray = -1;
+
+static inline void trace_pass(int pass, double gamma, int n) {
+  if (g_trace && g_trace_ray >= 0 && pass < 24) {
+    g_trace[g_trace_ray * 48 + 2 * pass] = gamma;
+    g_trace[g_trace_ray * 48 + 2 * pass + 1] = (double)n;
+  }
+}
+
 /* generate.py:219-273 _find_gamma_list (Alg. 1 as R implements it). */
 static void find_gamma_list(const ray_ctx* r, int delta, double eps,
                             double gamma_init, float* out_seg, double* tseg,
@@ -356,6 +368,7 @@ static void find_gamma_list(const ray_ctx* r, int delta, double eps,
       return;
     }
     int n = gen_list_pass(r, gamma, 0, out_seg, tseg);
+    trace_pass(passes, gamma, n);
     passes += 1;
     last_n = n;
     if (first) {
@@ -392,6 +405,7 @@ static void generate_ray(vox_t vol, int nx, int ny, int nz,
   double d[3];
   pixel_ray(inv_pv, eye, lx, ly, width, height, d);
   idx = oidx; /* outputs go to oidx (compact row sets) */
+  g_trace_ray = oidx;
   float* out_seg = segs + idx * (int64_t)n_sg * 6;
   counts[idx] = 0;
   if (gammas) gammas[idx] = 0.0;
@@ -464,6 +478,25 @@ int vdio_generate(const float* vol, int nx, int ny, int nz, const float* lut,
   return generate_all(v, nx, ny, nz, lut, lut_n, pv, inv_pv, eye, bb, width, height, n_sg,
                       delta, eps, gamma_init, step, lref, rows, n_rows, nthreads, counts, segs,
                       gammas, passes, samples);
+}
+
+/* vdio_generate with the (gamma, n) trace of every counting pass recorded
+ * into trace[(ray) * 48 + 2 * pass] (analysis only, not thread-safe across
+ * concurrent calls). */
+int vdio_generate_trace(const float* vol, int nx, int ny, int nz, const float* lut,
+                        int lut_n, const double* pv, const double* inv_pv,
+                        const double* eye, const double* bb, int width, int height,
+                        int n_sg, int delta, double eps, double gamma_init,
+                        double step, double lref, const int32_t* rows, int n_rows,
+                        int nthreads, int32_t* counts, float* segs, double* gammas,
+                        int32_t* passes, int64_t* samples, double* trace) {
+  g_trace = trace;
+  vox_t v = {vol, NULL};
+  const int rc = generate_all(v, nx, ny, nz, lut, lut_n, pv, inv_pv, eye, bb, width, height,
+                              n_sg, delta, eps, gamma_init, step, lref, rows, n_rows, nthreads,
+                              counts, segs, gammas, passes, samples);
+  g_trace = NULL;
+  return rc;
 }
 
 /* The same over raw u8 voxels (normalised on the fly, volume.py:48-50). */
