@@ -150,6 +150,14 @@ __global__ void __launch_bounds__(kDvrThreads, VDI_DVR_MINB) dvr_kernel(const Dv
         q[ax] = dmin(dmax(v, 0.0), 1.0);
       }
       const float4 rgba = classify(s_lut, c.a.lut_n, trilinear<VT>(c, s_u8, q[0], q[1], q[2]));
+      if (rgba.w <= 0.0f && c.ess) {
+        // a run of samples in an empty brick: all transparent (dvr.py:64-65)
+        int run = empty_run<VT>(c, s_u8, c.a.eye, s.d, tm, step, s.nsteps - 1 - s.k);
+        if (run > 1) {
+          s.samples += run - 1;
+          s.k += run - 1;
+        }
+      }
       if (rgba.w > 0.0f) {
         const double a = (double)rgba.w;
         const double dt = sb - sa;

@@ -519,7 +519,14 @@ __global__ void __launch_bounds__(kGenThreads, VDI_SAMPLE_MINB) gen_sample_kerne
       int ended = 0;
       if (tb > ta) {
         const float4 rgba = sample_at<VT>(c, s_lut, s_u8, s, ta, tb);
-        ended = segment_step(c, s, rgba, ta, tb, 1);
+        int run = 1;
+        if (c.ess && rgba.w <= 0.0f) {
+          // a run of samples in an empty brick: transparent, counted, not
+          // sampled (never the last sample, whose tb is clipped to t1)
+          run = empty_run<VT>(c, s_u8, s.o, s.d, 0.5 * (ta + tb), step, s.nsteps - 1 - s.k);
+          if (run < 1) run = 1;
+        }
+        ended = segment_step(c, s, rgba, ta, tb, run);
       }
       if (ended < 0) continue;
       if (ended == 0) ended = close_pass(c, s);

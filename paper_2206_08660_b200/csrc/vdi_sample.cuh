@@ -159,6 +159,58 @@ __device__ __forceinline__ double trilinear(const C& c, const double* tab, doubl
   return c0 * (1 - fz) + c1 * fz;
 }
 
+// Empty-brick runs, an exact shortcut over per-sample empty-space skipping.
+// When the sample at parameter tm lies in a brick whose maximum classifies
+// to alpha 0, every later sample whose cell stays in that brick is
+// transparent too. The cell coordinate g_a = q_a (n_a - 1) of sample k is
+// affine in k (tm = t0 + (k + 0.5) step up to rounding), so the samples that
+// stay inside the brick with a margin of 1e-6 cells -- far above the few-ulp
+// rounding of the sampler's own evaluation of g -- need not be sampled.
+// Returns how many samples from this one on (>= 1, <= max_run) are known to
+// be transparent, or 0 when this sample's brick is not an empty one.
+// inv_ext / ext_pow2 / c.a.aabb as in the sampler; only with c.ess.
+template <int VT, class C>
+__device__ __forceinline__ int empty_run(const C& c, const double* tab, const double o[3],
+                                         const double d[3], double tm, double step,
+                                         int max_run) {
+  const int n[3] = {c.a.nx, c.a.ny, c.a.nz};
+  double g[3];
+  int cell[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const double num = o[a] + tm * d[a] - c.a.aabb[a];
+    const double v = c.ext_pow2[a] ? num * c.inv_ext[a]
+                                   : div_by(num, c.a.aabb[3 + a] - c.a.aabb[a], c.inv_ext[a]);
+    if (!(v >= 0.0 && v <= 1.0)) return 0;  // clamped sample: no run
+    g[a] = v * (double)(n[a] - 1);
+    int ic = (int)g[a];
+    if (ic > n[a] - 2) ic = n[a] - 2;
+    cell[a] = ic;
+  }
+  const int lb = c.a.brick_log2;
+  long long boff = 0;
+  if constexpr ((VT & kVoxelSub) != 0) boff = c.sub_boff;
+  const long long bi = ((long long)(cell[2] >> lb) * c.bny + (cell[1] >> lb)) * c.bnx +
+                       (cell[0] >> lb) - boff;
+  if (!(Voxel<(VT & 15)>::get(c.a.brick_max, bi, tab) <= c.a.ess_max)) return 0;
+  const int B = 1 << lb;
+  long long m = max_run - 1;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const int b0 = (cell[a] >> lb) << lb;
+    // the brick's g interval; the clamps make the outer bricks open-ended
+    const double lo = b0 == 0 ? -INFINITY : (double)b0;
+    const double hi = b0 + B - 1 >= n[a] - 2 ? INFINITY : (double)(b0 + B);
+    const double dg = d[a] * step * (double)(n[a] - 1) * c.inv_ext[a];
+    double lim = INFINITY;
+    if (dg > 0.0) lim = (hi - 1e-6 - g[a]) / dg;
+    else if (dg < 0.0) lim = (g[a] - lo - 1e-6) / -dg;
+    if (!(lim >= 0.0)) return 1;  // within the margin of the brick's edge
+    if (lim < (double)m) m = (long long)lim;
+  }
+  return 1 + (int)m;
+}
+
 // volume.py:164-177 _lut_classify: f64 lerp rounded to f32.
 __device__ __forceinline__ float4 narrow(const double4 v) {
   return make_float4((float)v.x, (float)v.y, (float)v.z, (float)v.w);
