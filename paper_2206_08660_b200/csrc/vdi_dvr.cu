@@ -149,8 +149,9 @@ __global__ void __launch_bounds__(kDvrThreads, VDI_DVR_MINB) dvr_kernel(const Dv
                                   : div_by(num, c.a.aabb[3 + ax] - c.a.aabb[ax], c.inv_ext[ax]);
         q[ax] = dmin(dmax(v, 0.0), 1.0);
       }
-      const float4 rgba = classify(s_lut, c.a.lut_n, trilinear<VT>(c, s_u8, q[0], q[1], q[2]));
-      if (rgba.w <= 0.0f && c.ess) {
+      const double val = trilinear<VT>(c, s_u8, q[0], q[1], q[2]);
+      const float4 rgba = classify(s_lut, c.a.lut_n, val);
+      if (val == -1.0 && c.ess) {  // the empty-brick sentinel (or a genuine -1 sample)
         // a run of samples in an empty brick: all transparent (dvr.py:64-65)
         int run = empty_run<VT>(c, s_u8, c.a.eye, s.d, tm, step, s.nsteps - 1 - s.k);
         if (run > 1) {

@@ -158,7 +158,7 @@ __device__ double split_threshold(double g) {
 template <int VT>
 __device__ __forceinline__ float4 sample_at(const GenConst& c, const double4* lut,
                                             const double* tab, const RayState& s, double ta,
-                                            double tb) {
+                                            double tb, bool* ess_hit = nullptr) {
   const double tm = 0.5 * (ta + tb);
   double q[3];
 #pragma unroll
@@ -170,7 +170,9 @@ __device__ __forceinline__ float4 sample_at(const GenConst& c, const double4* lu
     else if (v > 1.0) v = 1.0;
     q[a] = v;
   }
-  return classify(lut, c.a.lut_n, trilinear<VT>(c, tab, q[0], q[1], q[2]));
+  const double v = trilinear<VT>(c, tab, q[0], q[1], q[2]);
+  if (ess_hit) *ess_hit = v == -1.0;  // the empty-brick sentinel (or a genuine -1 sample)
+  return classify(lut, c.a.lut_n, v);
 }
 
 // generate.py:53-86 _emit into the list-SoA slot `count`.
@@ -518,9 +520,10 @@ __global__ void __launch_bounds__(kGenThreads, VDI_SAMPLE_MINB) gen_sample_kerne
       // pass 1 on the fly (gamma_init, counting mode)
       int ended = 0;
       if (tb > ta) {
-        const float4 rgba = sample_at<VT>(c, s_lut, s_u8, s, ta, tb);
+        bool ess_hit = false;
+        const float4 rgba = sample_at<VT>(c, s_lut, s_u8, s, ta, tb, &ess_hit);
         int run = 1;
-        if (c.ess && rgba.w <= 0.0f) {
+        if (ess_hit) {
           // a run of samples in an empty brick: transparent, counted, not
           // sampled (never the last sample, whose tb is clipped to t1)
           run = empty_run<VT>(c, s_u8, s.o, s.d, 0.5 * (ta + tb), step, s.nsteps - 1 - s.k);
