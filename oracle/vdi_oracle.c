@@ -480,6 +480,71 @@ int vdio_generate(const float* vol, int nx, int ny, int nz, const float* lut,
                       gammas, passes, samples);
 }
 
+/* Analysis hook: the no-split trajectory of one ray (a counting pass with
+ * gamma = +inf): the number of visible runs V and max over samples of the
+ * d^2 the split test compares, so that every gamma with sqrt(d2max) < gamma
+ * has no split and n(gamma) = V (or the abort at run n_sg + 1). */
+static void nosplit_ray(const ray_ctx* r, int64_t* v_out, double* d2_out) {
+  int active = 0, nsamp = 0;
+  int64_t runs = 0;
+  double mr = 0, mg = 0, mb = 0, d2max = 0.0;
+  const double ex = r->bb[3] - r->bb[0], ey = r->bb[4] - r->bb[1], ez = r->bb[5] - r->bb[2];
+  const int64_t nsteps = (int64_t)ceil((r->t1 - r->t0) / r->step);
+  for (int64_t k = 0; k < nsteps; ++k) {
+    double ta = r->t0 + (double)k * r->step;
+    double tb = ta + r->step;
+    if (tb > r->t1) tb = r->t1;
+    if (tb <= ta) break;
+    double tm = 0.5 * (ta + tb);
+    double qx = (r->ox + tm * r->dx - r->bb[0]) / ex;
+    double qy = (r->oy + tm * r->dy - r->bb[1]) / ey;
+    double qz = (r->oz + tm * r->dz - r->bb[2]) / ez;
+    if (qx < 0.0) qx = 0.0; else if (qx > 1.0) qx = 1.0;
+    if (qy < 0.0) qy = 0.0; else if (qy > 1.0) qy = 1.0;
+    if (qz < 0.0) qz = 0.0; else if (qz > 1.0) qz = 1.0;
+    float rgba[4];
+    lut_classify(r->lut, r->lut_n, trilinear(r->vol, r->nx, r->ny, r->nz, qx, qy, qz), rgba);
+    double a = (double)rgba[3];
+    if (a <= 0.0) { active = 0; continue; }
+    double a_adj = 1.0 - pow(1.0 - a, (tb - ta) / r->lref);
+    double sr = (double)rgba[0] * a_adj, sg = (double)rgba[1] * a_adj, sb = (double)rgba[2] * a_adj;
+    if (!active) { active = 1; runs += 1; mr = sr; mg = sg; mb = sb; nsamp = 1; continue; }
+    double dr = mr - sr, dg = mg - sg, db = mb - sb;
+    double d2 = dr * dr + dg * dg + db * db;
+    if (d2 > d2max) d2max = d2;
+    nsamp += 1;
+    double inv = 1.0 / (double)nsamp;
+    mr += (sr - mr) * inv; mg += (sg - mg) * inv; mb += (sb - mb) * inv;
+  }
+  *v_out = runs;
+  *d2_out = d2max;
+}
+
+int vdio_nosplit(const float* vol, int nx, int ny, int nz, const float* lut, int lut_n,
+                 const double* pv, const double* inv_pv, const double* eye, const double* bb,
+                 int width, int height, double step, double lref, const int32_t* rows,
+                 int n_rows, int64_t* v_out, double* d2_out) {
+  int64_t total = (int64_t)n_rows * width;
+#pragma omp parallel for schedule(dynamic, 64)
+  for (int64_t j = 0; j < total; ++j) {
+    int64_t idx = (int64_t)rows[j / width] * width + j % width;
+    int ly = (int)(idx / width), lx = (int)(idx % width);
+    double d[3];
+    pixel_ray(inv_pv, eye, lx, ly, width, height, d);
+    v_out[j] = -1; d2_out[j] = -1.0;
+    double ta, tb, fa, fb;
+    if (!(clip_aabb(eye[0], eye[1], eye[2], d[0], d[1], d[2], bb, &ta, &tb) &&
+          clip_frustum(pv, eye[0], eye[1], eye[2], d[0], d[1], d[2], &fa, &fb))) continue;
+    double t0 = dmax(dmax(ta, fa), 0.0), t1 = dmin(tb, fb);
+    if (!(t1 > t0)) continue;
+    vox_t v = {vol, NULL};
+    ray_ctx r = {v, nx, ny, nz, lut, lut_n, pv, eye[0], eye[1], eye[2], d[0], d[1], d[2], bb,
+                 t0, t1, step, lref, 0, NULL};
+    nosplit_ray(&r, v_out + j, d2_out + j);
+  }
+  return 0;
+}
+
 /* vdio_generate with the (gamma, n) trace of every counting pass recorded
  * into trace[(ray) * 48 + 2 * pass] (analysis only, not thread-safe across
  * concurrent calls). */

@@ -139,3 +139,45 @@ def main():
 
 if __name__ == "__main__":
     main()
+
+
+def nosplit_study(cfg, nrows):
+    """How many bisection passes have gamma above the ray's no-split bound
+    D* = sqrt(max d^2 along the gamma = inf trajectory): those passes' counts
+    are the visible-run count V without running them."""
+    import ctypes
+    from oracle import oracle
+    from paper_2206_08660_b200 import synth
+    from paper_2206_08660_b200.generate import GenParams
+    tr, passes, n_sg, delta = traces(cfg, nrows)
+    vol, tf, gcam, rcam, _ = synth.config(cfg)
+    p = GenParams(n_sg=n_sg)
+    _, step, lref = p.resolve(vol)
+    w, h = gcam.viewport
+    rows = np.unique(np.linspace(0, h - 1, nrows).round().astype(np.int32))
+    L = oracle.lib()
+    i64 = np.ctypeslib.ndpointer(np.int64, flags="C_CONTIGUOUS")
+    f64 = np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS")
+    f32 = np.ctypeslib.ndpointer(np.float32, flags="C_CONTIGUOUS")
+    L.vdio_nosplit.argtypes = [f32, ctypes.c_int, ctypes.c_int, ctypes.c_int, f32, ctypes.c_int,
+                               f64, f64, f64, f64, ctypes.c_int, ctypes.c_int, ctypes.c_double,
+                               ctypes.c_double, ctypes.c_void_p, ctypes.c_int, i64, f64]
+    V = np.zeros(len(rows) * w, np.int64)
+    D2 = np.zeros(len(rows) * w)
+    m = lambda a: np.ascontiguousarray(np.asarray(a, np.float64).reshape(-1))  # noqa: E731
+    L.vdio_nosplit(np.ascontiguousarray(vol.normalized, np.float32), *vol.dims,
+                   np.ascontiguousarray(tf.lut, np.float32), tf.lut.shape[0], m(gcam.proj_view()),
+                   m(gcam.inv_proj_view()), m(gcam.position), m(vol.aabb), w, h, step, lref,
+                   rows.ctypes.data_as(ctypes.c_void_p), len(rows), V, D2)
+    tot = saved = 0
+    for t, np_, v, d2 in zip(tr, passes, V, D2):
+        if np_ < 2:
+            continue
+        k = int(np.sum(~np.isnan(t[:, 0])))
+        for gam, n in t[1:k]:
+            tot += 1
+            if math.sqrt(d2) < gam:
+                saved += 1
+                assert n == min(v, n_sg + 1) or n == v, (gam, n, v)
+    print(cfg, f"bisection passes {tot}, resolved by the no-split bound {saved} "
+               f"({100 * saved / max(tot, 1):.1f} %)")
