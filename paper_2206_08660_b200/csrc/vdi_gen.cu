@@ -833,14 +833,22 @@ __device__ __forceinline__ void count_reset(CountState& q, double gamma) {
 //  * t = s - m is exactly -(m - s), so t*t reproduces R's dr*dr bit for bit and
 //    m + t*inv is R's `m += (s - m) * inv`;
 //  * 1/n comes from the table of host-identical IEEE quotients.
+template <bool kTrack = false>
 __device__ __forceinline__ void count_sample(CountState& q, double sr, double sg, double sb,
                                              int k, int n_sg, int inv_n, const double* g_inv,
-                                             unsigned s_inv) {
+                                             unsigned s_inv, double* d2max = nullptr,
+                                             bool* split_seen = nullptr) {
   const double tr = sr - q.mr, tg = sg - q.mg, tb = sb - q.mb;
-  const bool far = tr * tr + tg * tg + tb * tb >= q.thr;
+  const double d2 = tr * tr + tg * tg + tb * tb;
+  const bool far = d2 >= q.thr;
   const bool live = q.n < 0;
   const bool merge = q.active && !far;
   const bool split = q.active && far;
+  if (kTrack) {
+    // the split test's d^2 along this state's trajectory (see gen_bisect_kernel)
+    if (live && q.active && d2 > *d2max) *d2max = d2;
+    if (live && split) *split_seen = true;
+  }
   const bool abort = (!q.active && q.count >= n_sg) || (split && q.count + 1 >= n_sg);
   const int ns = q.nsamp + 1;
   // nsamp <= max_steps, which the global table always covers; the shared copy
@@ -896,6 +904,13 @@ __global__ void __launch_bounds__(kThreads, kMinB) gen_bisect_kernel(const GenCo
   double low = 0.0, high = 0.0;
   int last_n = 0, high_n = 0, passes = 0, samples = 0;
   bool chain = false;  // this replay's speculation shape (see the top of the loop)
+  // No-split certificate: state 0 (this replay's largest gamma) records the
+  // largest d^2 its split test saw and whether it split. With no split, its
+  // trajectory is the gamma = inf one, so every gamma' with sqrt(d2max0) <
+  // gamma' has no split either and the same count -- such levels need no
+  // replay (their pass runs to the natural end: samples += stored).
+  double d2max0 = 0.0;
+  bool split0 = false;
   CountState q[kG];
   double gam[kG];
 
@@ -971,6 +986,8 @@ __global__ void __launch_bounds__(kThreads, kMinB) gen_bisect_kernel(const GenCo
         }
         count_reset(q[i], gam[i]);
       }
+      d2max0 = 0.0;
+      split0 = false;
       k = 0;
       if (kMode == 2) {
         ld_pred(b0, cache, 0 < stored);
@@ -1012,8 +1029,9 @@ __global__ void __launch_bounds__(kThreads, kMinB) gen_bisect_kernel(const GenCo
         const double sr = (double)fabsf(e.x) * a_adj;
         const double sg = (double)e.y * a_adj;
         const double sb = (double)e.z * a_adj;
+        count_sample<true>(q[0], sr, sg, sb, k, n_sg, inv_n, c.inv_tab, s_inv, &d2max0, &split0);
 #pragma unroll
-        for (int i = 0; i < kG; ++i)
+        for (int i = 1; i < kG; ++i)
           count_sample(q[i], sr, sg, sb, k, n_sg, inv_n, c.inv_tab, s_inv);
       }
       return run;
@@ -1114,8 +1132,9 @@ __global__ void __launch_bounds__(kThreads, kMinB) gen_bisect_kernel(const GenCo
         const double sr = (double)fabsf(e.x) * a_adj;
         const double sg = (double)e.y * a_adj;
         const double sb = (double)e.z * a_adj;
+        count_sample<true>(q[0], sr, sg, sb, k, n_sg, inv_n, c.inv_tab, s_inv, &d2max0, &split0);
 #pragma unroll
-        for (int i = 0; i < kG; ++i)
+        for (int i = 1; i < kG; ++i)
           count_sample(q[i], sr, sg, sb, k, n_sg, inv_n, c.inv_tab, s_inv);
       }
       const int kold = k;
@@ -1160,6 +1179,32 @@ __global__ void __launch_bounds__(kThreads, kMinB) gen_bisect_kernel(const GenCo
         rec->samples = samples;
         fin = true;
         break;
+      }
+    }
+    if (!fin && !split0 && q[0].n >= 0 && q[0].n <= n_sg && q[0].kend == stored) {
+      // levels whose gamma is above the certified no-split bound: n = q[0].n,
+      // a full pass each (generate.py:237-273 with the known count)
+      const double dstar = sqrt(d2max0);
+      const int nv = q[0].n;
+      while (fabs(high - low) >= c.a.eps) {
+        const double g = 0.5 * (low + high);
+        if (!(dstar < g)) break;
+        passes += 1;
+        samples += stored;
+        last_n = nv;
+        if (nv > n_sg) {  // (not reached: nv <= n_sg)
+          low = g;
+        } else if (nv < n_sg - c.a.delta) {
+          high = g;
+          high_n = nv;
+        } else {
+          rec->g_final = g;
+          rec->mode_final = kCount;
+          rec->passes = passes;
+          rec->samples = samples;
+          fin = true;
+          break;
+        }
       }
     }
     if (fin) {
