@@ -93,6 +93,9 @@ struct RoundCtl {
   unsigned long long efetch;    // emit-phase pool
   unsigned long long ffetch;    // fill-phase pool (one ray per warp)
   unsigned long long pad[1];
+  // bisection decisions seen so far in this round, per level: [0] up, [1] down
+  // (the bisect replays' learned speculation direction)
+  unsigned dir[2][32];
 };
 
 struct GenConst {
@@ -123,6 +126,7 @@ struct GenConst {
   int sub_ox, sub_oy, sub_oz, sub_nx, sub_ny, sub_nz;
   unsigned* sub_oob;
   int chain_levels;  // bisect replays starting below this level use the down-chain shape
+  int learn;         // learned chain directions at the later levels (VDI_LEARN_CHAIN)
 };
 
 struct RayState {
@@ -904,6 +908,7 @@ __global__ void __launch_bounds__(kThreads, kMinB) gen_bisect_kernel(const GenCo
   double low = 0.0, high = 0.0;
   int last_n = 0, high_n = 0, passes = 0, samples = 0;
   bool chain = false;  // this replay's speculation shape (see the top of the loop)
+  int cdir = 0;        // chain directions (bit i set: step i goes up)
   // No-split certificate: state 0 (this replay's largest gamma) records the
   // largest d^2 its split test saw and whether it split. With no split, its
   // trajectory is the gamma = inf one, so every gamma' with sqrt(d2max0) <
@@ -966,7 +971,30 @@ __global__ void __launch_bounds__(kThreads, kMinB) gen_bisect_kernel(const GenCo
       // bisection is in its first levels, where it goes down almost always
       // (tools/bisect_paths.py), the chain node -> down -> down, which covers
       // kG levels instead of kLevels when the prediction holds
-      chain = kLevels == 2 && (passes - 1) < c.chain_levels;
+      // Beyond those levels, a level whose decisions so far (this round, all
+      // rays: ctl->dir) lean strongly one way gets a chain in that direction
+      // when the next level leans too; otherwise the tree. The shape only
+      // changes how many levels a replay covers, never a result.
+      const int lvl0 = passes - 1;
+      chain = kLevels == 2 && lvl0 < c.chain_levels;
+      cdir = 0;  // bit i: the chain's step i goes up
+      if (kLevels == 2 && !chain && lvl0 + 1 < 32 && c.learn) {
+        int dirs = 0;
+        bool ok = true;
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const unsigned u = *((volatile unsigned*)&c.ctl->dir[0][lvl0 + j]);
+          const unsigned dn = *((volatile unsigned*)&c.ctl->dir[1][lvl0 + j]);
+          const unsigned tot = u + dn;
+          if (tot < 256u) ok = false;
+          else if (4u * u >= 3u * tot) dirs |= 1 << j;
+          else if (!(4u * dn >= 3u * tot)) ok = false;
+        }
+        if (ok) {
+          chain = true;
+          cdir = dirs;
+        }
+      }
       double lo[kG], hi[kG];
       lo[0] = low;
       hi[0] = high;
@@ -975,8 +1003,9 @@ __global__ void __launch_bounds__(kThreads, kMinB) gen_bisect_kernel(const GenCo
         gam[i] = 0.5 * (lo[i] + hi[i]);
         if (chain) {
           if (i + 1 < kG) {
-            lo[i + 1] = lo[i];
-            hi[i + 1] = gam[i];
+            const bool up = (cdir >> i) & 1;
+            lo[i + 1] = up ? gam[i] : lo[i];
+            hi[i + 1] = up ? hi[i] : gam[i];
           }
         } else if (2 * i + 2 < kG) {
           lo[2 * i + 1] = gam[i];
@@ -1165,13 +1194,18 @@ __global__ void __launch_bounds__(kThreads, kMinB) gen_bisect_kernel(const GenCo
       passes += 1;
       samples += kend;
       last_n = n;
+      const int plvl = passes - 2;  // this pass's bisection level
       if (n > n_sg) {
         low = g;
-        node = chain ? -1 : (2 * node + 1 < kG ? 2 * node + 1 : -1);
+        if (c.learn && plvl < 32) atomicAdd(&c.ctl->dir[0][plvl], 1u);
+        node = chain ? (((cdir >> node) & 1) && node + 1 < kG ? node + 1 : -1)
+                     : (2 * node + 1 < kG ? 2 * node + 1 : -1);
       } else if (n < n_sg - c.a.delta) {
         high = g;
         high_n = n;
-        node = chain ? (node + 1 < kG ? node + 1 : -1) : (2 * node + 2 < kG ? 2 * node + 2 : -1);
+        if (c.learn && plvl < 32) atomicAdd(&c.ctl->dir[1][plvl], 1u);
+        node = chain ? (!((cdir >> node) & 1) && node + 1 < kG ? node + 1 : -1)
+                     : (2 * node + 2 < kG ? 2 * node + 2 : -1);
       } else {
         rec->g_final = g;  // window hit: this pass's segments
         rec->mode_final = kCount;
@@ -1615,6 +1649,10 @@ int gen_launch(const VdiGenArgs* a, cudaStream_t stream) {
   // -> 73.9, C5 391 -> 359 (VDI_CHAIN_LEVELS = 0 restores the tree everywhere)
   c.chain_levels = 6;
   if (const char* env = getenv("VDI_CHAIN_LEVELS")) c.chain_levels = atoi(env);
+  // learned chain directions beyond those levels (measured: C3 gen 33.6 ->
+  // 32.8 ms; C4 / C5 within noise). VDI_LEARN_CHAIN = 0 disables.
+  c.learn = 1;
+  if (const char* env = getenv("VDI_LEARN_CHAIN")) c.learn = atoi(env);
   if (sub) {
     const int lb = a->brick_log2 >= 1 ? a->brick_log2 : 3;
     if (c.ess && ((c.sub_ox | c.sub_oy | c.sub_oz) & ((1 << lb) - 1)))
