@@ -23,6 +23,11 @@
  *   vdi_lz4_compress   replaces lz4.py:51-114     _compress_kernel (a chunk-parallel
  *                      LZ4 block, decodable by lz4.py:117-168)
  *   vdi_validate       replaces vdi.py:116-134    validate_vdi
+ *   vdi_gen_rays       replaces generate.py:371-407 generate_list / find_gamma
+ *                      (single-ray passes / bisections, batched)
+ *   vdi_composite_lists replaces raycast.py:494-518 composite_lists
+ *   vdi_dda_cells      replaces raycast.py:159-234 _dda_cells / dda_traverse (batched)
+ *   vdi_project_rays   replaces raycast.py:237-255 project_ray_to_ndc (batched)
  *   vdi_segs_to_aos / vdi_segs_from_aos  device layout <-> the reference's
  *                      (H, W, n_sg, 6) f32 array (vdi.py:3-7, 23-24)
  *
@@ -287,6 +292,36 @@ int vdi_lz4_compress(const uint8_t* src, size_t n_max, const unsigned long long*
                      size_t workspace_bytes, vdi_stream_t stream);
 
 int vdi_validate(const VdiValidateArgs* args, vdi_stream_t stream);
+
+/* Single-ray generation for n arbitrary rays (rays: (n, 6) f64 origin xyz,
+ * direction xyz), with the volume / LUT / camera / params of `args` (its
+ * width, height, band map, workspace and brick fields are ignored; outputs
+ * are indexed by ray): mode 0 = the full gamma bisection (find_gamma,
+ * generate.py:390-407: counts, segs, gammas, passes, samples); mode 1 / 2 =
+ * one counting / capped pass at gammas_in[i] (generate_list,
+ * generate.py:371-387: counts[i] = n, n_sg + 1 when exceeded). */
+#define VDI_RAYS_BISECT 0
+#define VDI_RAYS_COUNT 1
+#define VDI_RAYS_CAPPED 2
+int vdi_gen_rays(const VdiGenArgs* args, const double* rays, const double* gammas_in,
+                 int64_t n_rays, int32_t mode, vdi_stream_t stream);
+
+/* composite_lists (raycast.py:494-518) of a (h, w) list-SoA VDI into an
+ * (h, w, 4) f64 image; bg: HOST straight RGBA. */
+int vdi_composite_lists(const float* segs, const int32_t* counts, int32_t w, int32_t h,
+                        int32_t n_sg, double early_term, const double* bg_host, double* image,
+                        vdi_stream_t stream);
+
+/* _dda_cells (raycast.py:159-222) for n chords (6 f64: a0 xyz, a1 xyz):
+ * cells (n, cap, 2) i32, zs (n, cap, 4) f64 (z_entry, z_exit, s_entry,
+ * s_exit), counts (n,) i32; cap >= w + h + 4 holds every visit. */
+int vdi_dda_cells(const double* chords, int64_t n, int32_t w, int32_t h, int32_t cap,
+                  int32_t* cells, double* zs, int32_t* counts, vdi_stream_t stream);
+
+/* project_ray_to_ndc (raycast.py:237-255) for n world rays (6 f64): out (n, 6)
+ * NDC chord (a0, a1), hit (n,) 0/1; gen_pv, aabb: HOST f64[16], f64[6]. */
+int vdi_project_rays(const double* rays, int64_t n, const double* gen_pv_host,
+                     const double* aabb_host, double* out, int32_t* hit, vdi_stream_t stream);
 
 /* Alg. 2 search over a batch of independent queries (raycast.py:79-156).
  * fronts/backs: (n_queries, n_max) f32, counts: (n_queries,), d_entry /

@@ -17,7 +17,9 @@ __version__ = "0.1.0"
 _LAZY = {
     "GenParams": "generate", "GenStats": "generate", "generate_vdi": "generate",
     "RenderOptions": "raycast", "RenderStats": "raycast", "render_vdi": "raycast",
-    "find_first_supersegment": "raycast",
+    "find_first_supersegment": "raycast", "composite_lists": "raycast",
+    "dda_traverse": "raycast", "project_ray_to_ndc": "raycast", "opacity_correct": "raycast",
+    "terminate_check": "generate", "generate_list": "generate", "find_gamma": "generate",
     "Vdi": "vdi", "AccelGrid": "vdi", "default_grid_dims": "vdi",
     "validate_vdi": "vdi",
     "FrameStream": "stream", "FrameResult": "stream",

@@ -170,6 +170,46 @@ int vdi_synth_rm_u8(uint8_t* out, int32_t nx, int32_t ny, int32_t nz, const int3
                           static_cast<cudaStream_t>(stream));
 }
 
+int vdi_gen_rays(const VdiGenArgs* a, const double* rays, const double* gammas_in,
+                 int64_t n_rays, int32_t mode, vdi_stream_t stream) {
+  if (!a || (!rays && n_rays > 0)) return set_error(VDI_EINVAL, "null pointer");
+  if (!a->volume || !a->lut || !a->counts || !a->segs)
+    return set_error(VDI_EINVAL, "null device pointer");
+  if (a->nx < 2 || a->ny < 2 || a->nz < 2) return set_error(VDI_EINVAL, "bad dims");
+  if (a->n_sg < 1) return set_error(VDI_EINVAL, "n_sg must be >= 1");
+  if (!(a->eps > 0 && a->eps < 1)) return set_error(VDI_EINVAL, "epsilon must be in (0, 1)");
+  if (!(a->step > 0) || !(a->lref > 0)) return set_error(VDI_EINVAL, "step must be > 0");
+  if (mode < 0 || mode > 2) return set_error(VDI_EINVAL, "bad mode");
+  if ((a->voxel_type & ~15) != 0) return set_error(VDI_EINVAL, "plain voxel grids only");
+  return vdi::gen_rays(a, rays, gammas_in, n_rays, mode, static_cast<cudaStream_t>(stream));
+}
+
+int vdi_composite_lists(const float* segs, const int32_t* counts, int32_t w, int32_t h,
+                        int32_t n_sg, double early_term, const double* bg_host, double* image,
+                        vdi_stream_t stream) {
+  if (!segs || !counts || !bg_host || !image) return set_error(VDI_EINVAL, "null pointer");
+  if (w < 1 || h < 1 || n_sg < 1) return set_error(VDI_EINVAL, "bad sizes");
+  if (!(early_term > 0.0 && early_term <= 1.0))
+    return set_error(VDI_EINVAL, "early_term_alpha must be in (0, 1]");
+  return vdi::composite_lists(segs, counts, w, h, n_sg, early_term, bg_host, image,
+                              static_cast<cudaStream_t>(stream));
+}
+
+int vdi_dda_cells(const double* chords, int64_t n, int32_t w, int32_t h, int32_t cap,
+                  int32_t* cells, double* zs, int32_t* counts, vdi_stream_t stream) {
+  if ((!chords || !cells || !zs || !counts) && n > 0) return set_error(VDI_EINVAL, "null pointer");
+  if (w < 1 || h < 1 || cap < 1) return set_error(VDI_EINVAL, "bad sizes");
+  return vdi::dda_cells(chords, n, w, h, cap, cells, zs, counts, static_cast<cudaStream_t>(stream));
+}
+
+int vdi_project_rays(const double* rays, int64_t n, const double* gen_pv_host,
+                     const double* aabb_host, double* out, int32_t* hit, vdi_stream_t stream) {
+  if ((!rays || !out || !hit) && n > 0) return set_error(VDI_EINVAL, "null pointer");
+  if (!gen_pv_host || !aabb_host) return set_error(VDI_EINVAL, "null host pointer");
+  return vdi::project_rays(rays, n, gen_pv_host, aabb_host, out, hit,
+                           static_cast<cudaStream_t>(stream));
+}
+
 int vdi_find_first_batch(const float* fronts, const float* backs, const int32_t* counts,
                          int32_t n_max, const double* d_entry, const double* d_exit,
                          const int32_t* seeds, int32_t* out_index, int32_t* out_seed,

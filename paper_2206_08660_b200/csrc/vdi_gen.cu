@@ -1600,6 +1600,117 @@ size_t gen_workspace_bytes(const VdiGenArgs* a, int recommended) {
   return p.off_cache + rec;
 }
 
+// ------------------------------------------------------- single rays (G14)
+// generate_list / find_gamma (generate.py:371-407) for a batch of arbitrary
+// rays: one thread per ray, the reference's sequential loop (each pass
+// re-samples, as R does), on the same device helpers as the phased kernels.
+// mode 0: the full bisection (_find_gamma_list); 1: one counting pass at
+// gammas_in[i]; 2: one capped pass at gammas_in[i] (_gen_list_pass).
+template <int VT>
+__global__ void __launch_bounds__(kGenThreads) gen_rays_kernel(const GenConst c,
+                                                              const double* __restrict__ rays,
+                                                              const double* __restrict__ gin,
+                                                              long long n, int mode) {
+  extern __shared__ double4 s_lut[];
+  __shared__ double s_u8[256];
+  load_lut(c, s_lut, s_u8);
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double step = c.a.step;
+  RayState s;
+  s.list = (int)i;
+  s.seg = c.a.segs + i * (long long)list_stride(c.a.n_sg);
+  s.o[0] = rays[6 * i];
+  s.o[1] = rays[6 * i + 1];
+  s.o[2] = rays[6 * i + 2];
+  s.d[0] = rays[6 * i + 3];
+  s.d[1] = rays[6 * i + 4];
+  s.d[2] = rays[6 * i + 5];
+  init_bisection(c, s);
+  // generate.py:414-425 _clip_for_generation
+  double ta, tb, fa, fb;
+  bool hit = clip_aabb(s.o, s.d, c.a.aabb, ta, tb) && clip_frustum(c.a.pv, s.o, s.d, fa, fb);
+  if (hit) {
+    s.t0 = dmax(dmax(ta, fa), 0.0);
+    s.t1 = dmin(tb, fb);
+    hit = s.t1 > s.t0;
+  }
+  if (!hit) {
+    // find_gamma returns (gamma_init, 0, zeros, 0); generate_list (0, zeros, False)
+    finish_ray(c, s, mode == 0 ? c.a.gamma_init : gin[i], 0);
+    return;
+  }
+  s.nsteps = (int)ceil((s.t1 - s.t0) / step);
+  if (mode == 0) {
+    start_pass(s, s.bis_gamma, kCount);
+  } else {
+    start_pass(s, gin[i], mode == 1 ? kCount : kCapped);
+  }
+  while (true) {
+    const double sa = s.t0 + (double)s.k * step;
+    double sb = sa + step;
+    if (sb > s.t1) sb = s.t1;
+    int ended;
+    if (sb <= sa) {
+      ended = 0;
+    } else {
+      const float4 rgba = sample_at<VT>(c, s_lut, s_u8, s, sa, sb);
+      ended = segment_step(c, s, rgba, sa, sb, 1);
+    }
+    if (ended < 0) continue;
+    if (ended == 0) ended = close_pass(c, s);
+    if (mode != 0) {  // one pass: count (n_sg + 1 = exceeded) and the segments it wrote
+      s.passes = 1;
+      c.a.counts[i] = ended;
+      if (c.a.samples) c.a.samples[i] = s.samples;
+      return;
+    }
+    if (!pass_done(c, s, ended)) return;
+  }
+}
+
+int gen_rays(const VdiGenArgs* a, const double* rays, const double* gammas_in, long long n,
+             int mode, cudaStream_t stream) {
+  if (n <= 0) return VDI_OK;
+  if (mode != 0 && !gammas_in) return set_error(VDI_EINVAL, "mode 1/2 needs gammas_in");
+  GenConst c;
+  memset(&c, 0, sizeof(c));
+  c.a = *a;
+  for (int i = 0; i < 3; ++i) {
+    const double ext = a->aabb[3 + i] - a->aabb[i];
+    int e;
+    c.ext_pow2[i] = (frexp(ext, &e) == 0.5);
+    c.inv_ext[i] = 1.0 / ext;
+  }
+  {
+    int e;
+    c.lref_pow2 = (frexp(a->lref, &e) == 0.5);
+    c.inv_lref = 1.0 / a->lref;
+  }
+  c.ess = 0;  // plain per-sample sampling (no brick maxima needed)
+  c.inv_tab = nullptr;
+  c.inv_n = 0;  // 1/n by IEEE division (no table)
+  void (*k)(const GenConst, const double*, const double*, long long, int) = nullptr;
+  switch (a->voxel_type) {
+    case VDI_VOXEL_U8: k = gen_rays_kernel<VDI_VOXEL_U8>; break;
+    case VDI_VOXEL_U16: k = gen_rays_kernel<VDI_VOXEL_U16>; break;
+    case VDI_VOXEL_F32: k = gen_rays_kernel<VDI_VOXEL_F32>; break;
+    default: return set_error(VDI_EINVAL, "bad voxel_type %d", a->voxel_type);
+  }
+  const size_t smem = sizeof(double4) * a->lut_n;
+  if (smem > 48 * 1024) {
+    const cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               (int)smem);
+    if (e != cudaSuccess) return set_error(VDI_ELAUNCH, "rays smem: %s", cudaGetErrorString(e));
+  }
+  k<<<(unsigned)((n + kGenThreads - 1) / kGenThreads), kGenThreads, smem, stream>>>(c, rays,
+                                                                                   gammas_in, n,
+                                                                                   mode);
+  const cudaError_t err = cudaGetLastError();
+  if (err != cudaSuccess) return set_error(VDI_ELAUNCH, "rays launch: %s", cudaGetErrorString(err));
+  return VDI_OK;
+}
+
 int gen_launch(const VdiGenArgs* a, cudaStream_t stream) {
   GenConst c;
   c.a = *a;

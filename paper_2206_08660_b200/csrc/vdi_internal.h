@@ -25,6 +25,14 @@ size_t gen_workspace_bytes(const VdiGenArgs* a, int recommended);
 int grid_launch(const VdiGridArgs* a, cudaStream_t stream);
 int render_launch(const VdiRenderArgs* a, cudaStream_t stream);
 int dvr_launch(const VdiDvrArgs* a, cudaStream_t stream);
+int gen_rays(const VdiGenArgs* a, const double* rays, const double* gammas_in, long long n,
+             int mode, cudaStream_t stream);
+int composite_lists(const float* segs, const int32_t* counts, int w, int h, int n_sg,
+                    double early_term, const double* bg, double* img, cudaStream_t stream);
+int dda_cells(const double* chords, long long nq, int w, int h, int cap, int32_t* cells,
+              double* zs, int32_t* n_out, cudaStream_t stream);
+int project_rays(const double* rays, long long n, const double* gen_pv, const double* aabb,
+                 double* out, int32_t* hit, cudaStream_t stream);
 size_t encode_workspace_bytes(int width, int height);
 int encode_vdi1(const VdiEncodeArgs* a, cudaStream_t stream);
 size_t lz4_workspace_bytes(size_t n_max);

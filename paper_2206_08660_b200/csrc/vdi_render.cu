@@ -13,6 +13,8 @@
 // the contiguous back[] run of a list and a supersegment's colour is one
 // aligned float4. A warp owns an 8x4 pixel tile; neighbouring pixels walk
 // neighbouring lists, which keeps the count/back/rgba loads L1-coherent.
+#include <cstring>
+
 #include "vdi_common.cuh"
 #include "vdi_internal.h"
 #include "vdi_search.cuh"
@@ -243,6 +245,147 @@ int render_launch(const VdiRenderArgs* args, cudaStream_t stream) {
   const cudaError_t err = cudaGetLastError();
   if (err != cudaSuccess)
     return set_error(VDI_ELAUNCH, "render launch: %s", cudaGetErrorString(err));
+  return VDI_OK;
+}
+
+// raycast.py:494-518 composite_lists: the identity-view oracle, per list a
+// front-to-back composite of its stored supersegments (no traversal, no
+// search, no length correction). One thread per list (natural row order).
+__global__ void composite_lists_kernel(const float* __restrict__ segs,
+                                       const int32_t* __restrict__ counts, int w, int h,
+                                       int n_sg, double early_term, double bg0, double bg1,
+                                       double bg2, double bg3, double* __restrict__ img) {
+  const long long l = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (l >= (long long)w * h) return;
+  const float* ls = segs + l * (long long)list_stride(n_sg);
+  const float4* c4 = reinterpret_cast<const float4*>(ls);
+  double r = 0.0, g = 0.0, b = 0.0, a = 0.0;
+  const int n = counts[l];
+  for (int k = 0; k < n; ++k) {
+    const float4 s = c4[k];
+    const double wt = 1.0 - a;
+    r += wt * (double)s.x;
+    g += wt * (double)s.y;
+    b += wt * (double)s.z;
+    a += wt * (double)s.w;
+    if (a >= early_term) break;
+  }
+  const double wt = 1.0 - a;
+  double2* o = reinterpret_cast<double2*>(img + 4 * l);
+  o[0] = make_double2(r + wt * bg0 * bg3, g + wt * bg1 * bg3);
+  o[1] = make_double2(b + wt * bg2 * bg3, a + wt * bg3);
+}
+
+int composite_lists(const float* segs, const int32_t* counts, int w, int h, int n_sg,
+                    double early_term, const double* bg, double* img, cudaStream_t stream) {
+  const long long n = (long long)w * h;
+  if (n <= 0) return VDI_OK;
+  composite_lists_kernel<<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(
+      segs, counts, w, h, n_sg, early_term, bg[0], bg[1], bg[2], bg[3], img);
+  const cudaError_t err = cudaGetLastError();
+  if (err != cudaSuccess) return set_error(VDI_ELAUNCH, "composite launch: %s", cudaGetErrorString(err));
+  return VDI_OK;
+}
+
+// raycast.py:159-222 _dda_cells for a batch of NDC chords (a0, a1: 6 f64 per
+// query): the visited cells (cx, cy) and (z_entry, z_exit, s_entry, s_exit),
+// at most w + h + 4 per query; n_out[q] = cells visited. One thread per chord
+// (the same DDA arithmetic as render_kernel).
+__global__ void dda_kernel(const double* __restrict__ chords, long long nq, int w, int h,
+                           int cap, int32_t* __restrict__ cells, double* __restrict__ zs,
+                           int32_t* __restrict__ n_out) {
+  const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= nq) return;
+  const double x0 = chords[6 * q], y0 = chords[6 * q + 1], z0 = chords[6 * q + 2];
+  const double dx = chords[6 * q + 3] - x0, dy = chords[6 * q + 4] - y0,
+               dz = chords[6 * q + 5] - z0;
+  int cx = clampi(floor_ll((x0 + 1.0) * w / 2.0), 0, w - 1);
+  int cy = clampi(floor_ll((y0 + 1.0) * h / 2.0), 0, h - 1);
+  const int step_x = dx > 0 ? 1 : (dx < 0 ? -1 : 0);
+  const int step_y = dy > 0 ? 1 : (dy < 0 ? -1 : 0);
+  double t_max_x = INFINITY, t_delta_x = INFINITY, t_max_y = INFINITY, t_delta_y = INFINITY;
+  if (step_x != 0) {
+    const double bx = -1.0 + 2.0 * (double)(cx + (step_x > 0 ? 1 : 0)) / w;
+    t_max_x = (bx - x0) / dx;
+    t_delta_x = (2.0 / w) / fabs(dx);
+  }
+  if (step_y != 0) {
+    const double by = -1.0 + 2.0 * (double)(cy + (step_y > 0 ? 1 : 0)) / h;
+    t_max_y = (by - y0) / dy;
+    t_delta_y = (2.0 / h) / fabs(dy);
+  }
+  int n = 0;
+  double s_cur = 0.0;
+  for (int it = 0; it < w + h + 4 && n < cap; ++it) {
+    double s_exit = dmin(dmin(t_max_x, t_max_y), 1.0);
+    if (s_exit < s_cur) s_exit = s_cur;
+    const long long o = q * (long long)cap + n;
+    cells[2 * o] = cx;
+    cells[2 * o + 1] = cy;
+    zs[4 * o] = z0 + s_cur * dz;
+    zs[4 * o + 1] = z0 + s_exit * dz;
+    zs[4 * o + 2] = s_cur;
+    zs[4 * o + 3] = s_exit;
+    n += 1;
+    if (s_exit >= 1.0) break;
+    if (t_max_x <= t_max_y) {
+      cx += step_x;
+      s_cur = t_max_x;
+      t_max_x += t_delta_x;
+    } else {
+      cy += step_y;
+      s_cur = t_max_y;
+      t_max_y += t_delta_y;
+    }
+    if (cx < 0 || cx >= w || cy < 0 || cy >= h) break;
+  }
+  n_out[q] = n;
+}
+
+int dda_cells(const double* chords, long long nq, int w, int h, int cap, int32_t* cells,
+              double* zs, int32_t* n_out, cudaStream_t stream) {
+  if (nq <= 0) return VDI_OK;
+  dda_kernel<<<(unsigned)((nq + 127) / 128), 128, 0, stream>>>(chords, nq, w, h, cap, cells, zs,
+                                                               n_out);
+  const cudaError_t err = cudaGetLastError();
+  if (err != cudaSuccess) return set_error(VDI_ELAUNCH, "dda launch: %s", cudaGetErrorString(err));
+  return VDI_OK;
+}
+
+// raycast.py:237-255 project_ray_to_ndc for a batch of world rays (origin,
+// dir: 6 f64): clip to the volume box and the generation frustum; out (a0,
+// a1: 6 f64) and hit flags.
+__global__ void project_kernel(const double* __restrict__ rays, long long n, const RenderConst c,
+                               double* __restrict__ out, int32_t* __restrict__ hit_out) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double o[3] = {rays[6 * i], rays[6 * i + 1], rays[6 * i + 2]};
+  const double d[3] = {rays[6 * i + 3], rays[6 * i + 4], rays[6 * i + 5]};
+  double ta, tb, fa, fb;
+  int hit = 0;
+  if (clip_aabb(o, d, c.a.aabb, ta, tb) && clip_frustum(c.a.gen_pv, o, d, fa, fb)) {
+    const double t0 = dmax(dmax(ta, fa), 0.0), t1 = dmin(tb, fb);
+    if (t1 > t0) {
+      hit = 1;
+      xform(c.a.gen_pv, o[0] + t0 * d[0], o[1] + t0 * d[1], o[2] + t0 * d[2], out[6 * i],
+            out[6 * i + 1], out[6 * i + 2]);
+      xform(c.a.gen_pv, o[0] + t1 * d[0], o[1] + t1 * d[1], o[2] + t1 * d[2], out[6 * i + 3],
+            out[6 * i + 4], out[6 * i + 5]);
+    }
+  }
+  hit_out[i] = hit;
+}
+
+int project_rays(const double* rays, long long n, const double* gen_pv, const double* aabb,
+                 double* out, int32_t* hit, cudaStream_t stream) {
+  if (n <= 0) return VDI_OK;
+  RenderConst c;
+  memset(&c, 0, sizeof(c));
+  for (int k = 0; k < 16; ++k) c.a.gen_pv[k] = gen_pv[k];
+  for (int k = 0; k < 6; ++k) c.a.aabb[k] = aabb[k];
+  project_kernel<<<(unsigned)((n + 127) / 128), 128, 0, stream>>>(rays, n, c, out, hit);
+  const cudaError_t err = cudaGetLastError();
+  if (err != cudaSuccess) return set_error(VDI_ELAUNCH, "project launch: %s", cudaGetErrorString(err));
   return VDI_OK;
 }
 

@@ -241,3 +241,71 @@ def generate_vdi(vol, tf, cam, params: GenParams | None = None, grid_dims=None,
     stats = GenStats(gammas=dv.to_host(bufs.gammas), passes=dv.to_host(bufs.passes),
                      wall_time_s=wall, samples=dv.to_host(bufs.samples))
     return vdi, grid, stats
+
+
+# ------------------------------------------------------------ single rays (G14)
+
+def terminate_check(seg_color, seg_alpha, sample_rgba, step_len, gamma) -> bool:
+    """generate.py:357-368: True iff a new supersegment must start (a scalar
+    predicate on host values, evaluated with the reference's expressions)."""
+    import math
+    a_adj = 1.0 - (1.0 - float(sample_rgba[3])) ** float(step_len)
+    d = math.sqrt(sum((float(seg_color[c]) - float(sample_rgba[c]) * a_adj) ** 2
+                      for c in range(3)))
+    return d >= gamma
+
+
+def _rays_array(rays) -> np.ndarray:
+    out = np.empty((len(rays), 6), np.float64)
+    for i, r in enumerate(rays):
+        out[i, :3] = np.asarray(r.origin, np.float64)
+        out[i, 3:] = np.asarray(r.dir, np.float64)
+    return out
+
+
+def gen_rays(rays, vol, tf, params: GenParams, cam, mode: int, gammas=None):
+    """Batch of single-ray generations on the device (vdi_gen_rays): mode 0
+    = find_gamma's bisection, 1 / 2 = one counting / capped pass at gammas.
+    Returns host (counts, segs (n, n_sg, 6), gammas, passes, samples)."""
+    t = dv.require_cuda()
+    L = _capi.load()
+    resolved = params.resolve(vol)
+    n = len(rays)
+    arr = _rays_array(rays)
+    vol_dev, vt = dv.upload_volume(vol)
+    lut_dev = dv.upload_lut(tf.lut)
+    n_sg = params.n_sg
+    bufs = GenBuffers(counts=t.zeros(max(n, 1), dtype=t.int32, device="cuda"),
+                      segs=t.zeros((max(n, 1), list_stride(n_sg)), dtype=t.float32,
+                                   device="cuda"),
+                      gammas=t.zeros(max(n, 1), dtype=t.float64, device="cuda"),
+                      passes=t.zeros(max(n, 1), dtype=t.int32, device="cuda"),
+                      samples=t.zeros(max(n, 1), dtype=t.int32, device="cuda"),
+                      workspace=None, grid=None)
+    a = gen_args(vol_dev, vt, vol.dims, lut_dev, cam, np.asarray(vol.aabb, np.float64),
+                 resolved, n_sg, params.epsilon, params.gamma_init, bufs)
+    rays_dev = dv.to_device(arr)
+    g_dev = dv.to_device(np.asarray(gammas, np.float64)) if gammas is not None else None
+    _capi.check(L.vdi_gen_rays(a, dv.ptr(rays_dev), dv.ptr(g_dev), n, int(mode),
+                               dv.stream_handle()))
+    aos = t.empty((max(n, 1), n_sg * 6), dtype=t.float32, device="cuda")
+    _capi.check(L.vdi_segs_to_aos(dv.ptr(bufs.segs), dv.ptr(aos), max(n, 1), n_sg,
+                                  dv.stream_handle()))
+    return (dv.to_host(bufs.counts)[:n], dv.to_host(aos).reshape(-1, n_sg, 6)[:n],
+            dv.to_host(bufs.gammas)[:n], dv.to_host(bufs.passes)[:n],
+            dv.to_host(bufs.samples)[:n])
+
+
+def generate_list(ray, vol, tf, gamma: float, params: GenParams, cam, capped: bool = False):
+    """generate.py:371-387: one generation pass along `ray` at `gamma`;
+    returns (count, segments (n_sg, 6) f32, exceeded)."""
+    c, s, _, _, _ = gen_rays([ray], vol, tf, params, cam, 2 if capped else 1, [float(gamma)])
+    n = int(c[0])
+    return min(n, params.n_sg), s[0], n > params.n_sg
+
+
+def find_gamma(ray, vol, tf, params: GenParams, cam):
+    """generate.py:390-407: the per-ray bisection; returns (gamma, count,
+    segments, passes) (segments past `count` are zero)."""
+    c, s, g, p, _ = gen_rays([ray], vol, tf, params, cam, 0)
+    return float(g[0]), int(c[0]), s[0], int(p[0])

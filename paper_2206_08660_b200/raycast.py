@@ -156,3 +156,61 @@ def find_first_batch(lists, counts, d_entry, d_exit, seeds):
         dv.ptr(fr), dv.ptr(bk), dv.ptr(cnt), int(n_max), dv.ptr(de), dv.ptr(dx), dv.ptr(sd),
         dv.ptr(oi), dv.ptr(osd), int(n), dv.stream_handle()))
     return dv.to_host(oi), dv.to_host(osd)
+
+
+# ------------------------------------------------------- test-facing (R9, R10)
+
+def composite_lists(vdi, opts: RenderOptions | None = None) -> Image:
+    """raycast.py:494-518: the identity-view oracle -- each list's stored
+    supersegments composited front to back, no traversal, no length
+    correction -- on the device (vdi_composite_lists)."""
+    opts = opts or RenderOptions()
+    t = dv.require_cuda()
+    vdi = _as_device_vdi(vdi)
+    d = vdi.device()
+    counts, segs = d.counts, d.segs
+    if d.world > 1:
+        from .vdi import unshard_rows
+        counts, segs = unshard_rows(d, vdi.height, vdi.width)
+    img = t.empty((vdi.height, vdi.width, 4), dtype=t.float64, device="cuda")
+    bg = np.ascontiguousarray(np.asarray(opts.background, np.float64))
+    _capi.check(_capi.load().vdi_composite_lists(
+        dv.ptr(segs), dv.ptr(counts), vdi.width, vdi.height, vdi.n_sg,
+        float(opts.early_term_alpha), bg.ctypes.data, dv.ptr(img), dv.stream_handle()))
+    return Image.from_array(dv.to_host(img))
+
+
+def dda_traverse(a0, a1, width: int, height: int):
+    """raycast.py:225-234: the list cells an NDC chord visits, with the
+    per-cell entry / exit NDC z (vdi_dda_cells)."""
+    t = dv.require_cuda()
+    cap = int(width) + int(height) + 4
+    ch = dv.to_device(np.concatenate([np.asarray(a0, np.float64).reshape(3),
+                                      np.asarray(a1, np.float64).reshape(3)]))
+    cells = t.empty((cap, 2), dtype=t.int32, device="cuda")
+    zs = t.empty((cap, 4), dtype=t.float64, device="cuda")
+    n = t.empty(1, dtype=t.int32, device="cuda")
+    _capi.check(_capi.load().vdi_dda_cells(dv.ptr(ch), 1, int(width), int(height), cap,
+                                           dv.ptr(cells), dv.ptr(zs), dv.ptr(n),
+                                           dv.stream_handle()))
+    k = int(dv.to_host(n)[0])
+    c, z = dv.to_host(cells), dv.to_host(zs)
+    return [((int(c[i, 0]), int(c[i, 1])), float(z[i, 0]), float(z[i, 1])) for i in range(k)]
+
+
+def project_ray_to_ndc(ray, gen_cam, volume_aabb):
+    """raycast.py:237-255: the ray clipped to the volume box and the
+    generation frustum, as an NDC chord (a0, a1), or None."""
+    t = dv.require_cuda()
+    r = dv.to_device(np.concatenate([np.asarray(ray.origin, np.float64).reshape(3),
+                                     np.asarray(ray.dir, np.float64).reshape(3)]))
+    out = t.empty(6, dtype=t.float64, device="cuda")
+    hit = t.empty(1, dtype=t.int32, device="cuda")
+    pv = np.ascontiguousarray(_mat(gen_cam.proj_view()))
+    bb = np.ascontiguousarray(np.asarray(volume_aabb, np.float64).reshape(6))
+    _capi.check(_capi.load().vdi_project_rays(dv.ptr(r), 1, pv.ctypes.data, bb.ctypes.data,
+                                              dv.ptr(out), dv.ptr(hit), dv.stream_handle()))
+    if not int(dv.to_host(hit)[0]):
+        return None
+    o = dv.to_host(out)
+    return o[:3].copy(), o[3:].copy()

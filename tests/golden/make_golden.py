@@ -493,7 +493,96 @@ def codec_main():
     save("codec", rec)
 
 
+def singles_main():
+    """The reference's single-ray / test-facing functions: generate_list and
+    find_gamma (generate.py:371-407) on pixel rays and off-axis rays of the C1
+    scene, terminate_check (357-368), dda_traverse (raycast.py:225-234),
+    project_ray_to_ndc (237-255) and composite_lists (494-518)."""
+    from vdikit import generate as rg, raycast as rr
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    vol, tf, gcam, rcam, n_sg = synth.config("C1")
+    rvol, rtf, rc = r_volume(vol), vk.TransferFunction(tf.control_points), r_camera(gcam)
+    rng = np.random.default_rng(21)
+    rays = []
+    for _ in range(96):
+        px = (int(rng.integers(0, 128)), int(rng.integers(0, 128)))
+        rays.append(vk.generate_ray(rc, px))
+    for _ in range(32):  # off-axis rays from points around the volume
+        o = np.asarray(rc.position) + rng.normal(0, 8, 3)
+        tgt = rng.uniform(8, 56, 3)
+        d = tgt - o
+        rays.append(vk.Ray(origin=o, dir=d / np.linalg.norm(d)))
+    rec = {"ray_o": np.array([r.origin for r in rays]), "ray_d": np.array([r.dir for r in rays])}
+    gams = [1e-5, 0.01, 0.05, 0.2, 1.0]
+    rec["gammas"] = np.array(gams)
+    for pi, params in enumerate((vk.GenParams(n_sg=n_sg), vk.GenParams(n_sg=4, delta=1),
+                                 vk.GenParams(n_sg=6, delta=0, epsilon=0.02))):
+        rec[f"p{pi}"] = np.array([params.n_sg, -1 if params.delta is None else params.delta,
+                                  params.epsilon])
+        for gi, g in enumerate(gams):
+            for cap in (0, 1):
+                cn, sg, ex = [], [], []
+                for r in rays:
+                    c, sgl, e = rg.generate_list(r, rvol, rtf, g, params, rc, capped=bool(cap))
+                    cn.append(c); sg.append(sgl.copy()); ex.append(e)
+                rec[f"p{pi}_g{gi}_c{cap}_count"] = np.array(cn)
+                rec[f"p{pi}_g{gi}_c{cap}_segs"] = np.array(sg)
+                rec[f"p{pi}_g{gi}_c{cap}_exceeded"] = np.array(ex)
+        fg, fn, fs, fp = [], [], [], []
+        for r in rays:
+            g, n, sgl, p = rg.find_gamma(r, rvol, rtf, params, rc)
+            fg.append(g); fn.append(n); fs.append(sgl.copy()); fp.append(p)
+        rec[f"p{pi}_fg_gamma"] = np.array(fg)
+        rec[f"p{pi}_fg_count"] = np.array(fn)
+        rec[f"p{pi}_fg_segs"] = np.array(fs)
+        rec[f"p{pi}_fg_passes"] = np.array(fp)
+    rec.update(cam_record("gen", rc))
+    # terminate_check
+    tc_in = rng.uniform(0, 1, (400, 9))
+    tc_in[:, 7] = rng.uniform(0.2, 2.0, 400)       # step_len
+    tc_in[:, 8] = rng.uniform(0.0, 0.8, 400)       # gamma
+    rec["tc_in"] = tc_in
+    rec["tc_out"] = np.array([rg.terminate_check(x[0:3], x[3], x[3:7], x[7], x[8])
+                              for x in tc_in])
+    # dda_traverse: random chords, axis-parallel and corner-tie chords
+    grid = np.linspace(-1, 1, 9)
+    chords = [rng.uniform(-1.1, 1.1, 6) for _ in range(150)]
+    chords += [np.array([rng.choice(grid), rng.choice(grid), -0.5, rng.choice(grid),
+                         rng.choice(grid), 0.5]) for _ in range(50)]
+    chords += [np.array([0.1, -0.9, 0.0, 0.1, 0.9, 1.0]), np.array([-0.9, 0.3, 0, 0.9, 0.3, 0])]
+    rec["dda_chords"] = np.array(chords)
+    rec["dda_wh"] = np.array([[32, 24], [7, 5]])
+    for wi, (w, h) in enumerate(((32, 24), (7, 5))):
+        cells, zs, ns = [], [], []
+        for ch in chords:
+            out = rr.dda_traverse(ch[:3], ch[3:], w, h)
+            ns.append(len(out))
+            cells += [c for c, _, _ in out]
+            zs += [(a, b) for _, a, b in out]
+        rec[f"dda{wi}_n"] = np.array(ns)
+        rec[f"dda{wi}_cells"] = np.array(cells)
+        rec[f"dda{wi}_z"] = np.array(zs)
+    # project_ray_to_ndc on the rays above, against the C1 generation camera
+    prj, hit = [], []
+    for r in rays:
+        res = rr.project_ray_to_ndc(r, rc, rvol.aabb)
+        hit.append(res is not None)
+        prj.append(np.concatenate(res) if res is not None else np.zeros(6))
+    rec["proj_hit"] = np.array(hit)
+    rec["proj_out"] = np.array(prj)
+    # composite_lists on committed VDIs
+    for src, tag in (("random_vdi:0", "cl0"), ("sphere64_u8", "cl1")):
+        vdi, _ = fixture_vdi(src)
+        rec[f"{tag}_img"] = rr.composite_lists(vdi).data
+        rec[f"{tag}_img_opts"] = rr.composite_lists(
+            vdi, vk.RenderOptions(early_term_alpha=0.5, background=(0.2, 0.3, 0.4, 0.7))).data
+    save("singles", rec)
+
+
 def main():
+    if "--only-singles" in sys.argv:
+        singles_main()
+        return
     if "--only-codec" in sys.argv:
         codec_main()
         return
@@ -559,6 +648,7 @@ def main():
     dvr_main()
     preview_main()
     codec_main()
+    singles_main()
 
 
 if __name__ == "__main__":

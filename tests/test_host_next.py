@@ -99,3 +99,11 @@ def test_band_volume_box_is_a_slab():
     for org, size in boxes:
         ys.update(range(org[1], org[1] + size[1]))
     assert ys >= set(range(full[0][1] + 2, full[0][1] + full[1][1] - 2))
+
+
+def test_terminate_check_matches_reference():
+    """generate.py:357-368 (host predicate) on the reference's 400 cases."""
+    from paper_2206_08660_b200.generate import terminate_check
+    g = gio.load("singles")
+    got = [terminate_check(x[0:3], x[3], x[3:7], x[7], x[8]) for x in g["tc_in"]]
+    assert np.array_equal(np.array(got), g["tc_out"])
