@@ -67,13 +67,16 @@ def test_dvr_full_size_vs_oracle(cfg, rows):
 @pytest.mark.parametrize("preset", ["sphere", "bands"])
 def test_a3_identity_view_fidelity(preset):
     """The reference's A3 (test_acceptance.py:122-129, conftest.py:43-58):
-    render_vdi from the generation view vs render_dvr ground truth, PSNR over
-    all RGBA channels (metrics.py:73-80) >= 45 dB, both on the device."""
+    render_vdi from the generation view equals composite_lists within 1e-5,
+    and vs render_dvr ground truth has PSNR over all RGBA channels
+    (metrics.py:73-80) >= 45 dB -- all on the device."""
     vol = synth.preset_volume(preset, 128)
     tf = synth.preset_tf(preset)
     cam = synth.sweep_camera(vol, 0.0, (256, 256))
     vdi, grid = vb.generate_vdi(vol, tf, cam, vb.GenParams(n_sg=12))
     img = vb.render_vdi(vdi, grid, cam).data
+    oracle_img = vb.composite_lists(vdi).data  # A3's first check: identity-view oracle
+    assert np.abs(img - oracle_img).max() <= 1e-5
     truth = vb.render_dvr(vol, tf, cam).data
     mse = float(np.mean((img - truth) ** 2))
     psnr = np.inf if mse == 0.0 else 10.0 * np.log10(1.0 / mse)
