@@ -917,7 +917,6 @@ __global__ void __launch_bounds__(kThreads, kMinB) gen_bisect_kernel(const GenCo
   double d2max0 = 0.0;
   bool split0 = false;
   CountState q[kG];
-  double gam[kG];
 
   while (true) {
     const unsigned need = __ballot_sync(0xffffffffu, !have && !done);
@@ -995,7 +994,7 @@ __global__ void __launch_bounds__(kThreads, kMinB) gen_bisect_kernel(const GenCo
           cdir = dirs;
         }
       }
-      double lo[kG], hi[kG];
+      double lo[kG], hi[kG], gam[kG];
       lo[0] = low;
       hi[0] = high;
 #pragma unroll
@@ -1181,15 +1180,17 @@ __global__ void __launch_bounds__(kThreads, kMinB) gen_bisect_kernel(const GenCo
     bool fin = false;
     for (int lvl = 0; lvl < kG && node >= 0; ++lvl) {
       if (lvl > 0 && fabs(high - low) < c.a.eps) break;  // handled at the top
-      // static selection keeps q[] / gam[] in registers
+      // static selection keeps q[] in registers. The node's gamma is the
+      // midpoint of the current bracket: every speculated state was formed
+      // that way from the bracket its ancestors' decisions leave, so it need
+      // not stay live through the replay
       int n = 0, kend = 0;
-      double g = 0.0;
+      const double g = 0.5 * (low + high);
 #pragma unroll
       for (int i = 0; i < kG; ++i)
         if (i == node) {
           n = q[i].n;
           kend = q[i].kend;
-          g = gam[i];
         }
       passes += 1;
       samples += kend;
