@@ -282,6 +282,15 @@ size_t vdi_vdi1_max_bytes(int32_t width, int32_t height, int32_t n_sg, int32_t g
 size_t vdi_encode_workspace_bytes(int32_t width, int32_t height);
 int vdi_encode_vdi1(const VdiEncodeArgs* args, vdi_stream_t stream);
 
+/* The lists of a VDI1 stream (counts u16 at byte 160, then the valid
+ * supersegments) -> counts i32 (rows, width) + list-SoA segs with zeroed
+ * tails (decode_vdi's arrays, vdi.py:162-210, on the device). workspace:
+ * vdi_encode_workspace_bytes(width, rows). Used by the multi-GPU exchange,
+ * which all-gathers packed VDI1 shards instead of the padded list-SoA. */
+int vdi_decode_vdi1_lists(const uint8_t* src, int32_t width, int32_t rows, int32_t n_sg,
+                          int32_t* counts, float* segs, void* workspace, size_t workspace_bytes,
+                          vdi_stream_t stream);
+
 /* LZ4 block compression of src[0, n) with n = *n_dev when n_dev is not NULL
  * (a device length, e.g. VdiEncodeArgs.out_len), else n = n_max. dst holds
  * vdi_lz4_max_bytes(n_max); *out_len (device) receives the block length. */

@@ -112,7 +112,8 @@ EXPORTS = ["vdi_last_error", "vdi_abi_version", "vdi_gen_workspace_bytes",
            "vdi_preview_launch", "vdi_bilinear_upsample", "vdi_vdi1_max_bytes",
            "vdi_encode_workspace_bytes", "vdi_encode_vdi1", "vdi_lz4_max_bytes",
            "vdi_lz4_workspace_bytes", "vdi_lz4_compress", "vdi_validate", "vdi_synth_rm_u8",
-           "vdi_gen_rays", "vdi_composite_lists", "vdi_dda_cells", "vdi_project_rays", "vdi_find_first_batch",
+           "vdi_gen_rays", "vdi_composite_lists", "vdi_dda_cells", "vdi_project_rays",
+           "vdi_decode_vdi1_lists", "vdi_find_first_batch",
            "vdi_volume_brick_max", "vdi_selftest_arith", "vdi_segs_to_aos",
            "vdi_segs_from_aos", "vdi_volume_cells_bytes", "vdi_volume_cells", "vdi_volume_cells_masked"]
 
@@ -154,6 +155,7 @@ def load():
     L.vdi_lz4_workspace_bytes.restype = ctypes.c_size_t
     L.vdi_lz4_compress.argtypes = [_P, ctypes.c_size_t, _P, _P, _P, _P, ctypes.c_size_t, _P]
     L.vdi_validate.argtypes = [ctypes.POINTER(VdiValidateArgs), _P]
+    L.vdi_decode_vdi1_lists.argtypes = [_P, _I, _I, _I, _P, _P, _P, ctypes.c_size_t, _P]
     L.vdi_gen_rays.argtypes = [ctypes.POINTER(VdiGenArgs), _P, _P, ctypes.c_int64, _I, _P]
     L.vdi_composite_lists.argtypes = [_P, _P, _I, _I, _I, _D, _P, _P, _P]
     L.vdi_dda_cells.argtypes = [_P, ctypes.c_int64, _I, _I, _I, _P, _P, _P, _P]
@@ -175,15 +177,8 @@ def load():
     L.vdi_segs_from_aos.argtypes = [_P, _P, ctypes.c_int64, _I, _P]
     for name in ("vdi_gen_launch", "vdi_grid_launch", "vdi_render_launch", "vdi_dvr_launch",
                  "vdi_preview_launch", "vdi_bilinear_upsample", "vdi_encode_vdi1",
-                 "vdi_lz4_compress", "vdi_validate", "vdi_synth_rm_u8", "vdi_gen_rays",
-                 "vdi_composite_lists", "vdi_dda_cells", "vdi_project_rays", "vdi_vdi1_max_bytes",
-           "vdi_encode_workspace_bytes", "vdi_encode_vdi1", "vdi_lz4_max_bytes",
-           "vdi_lz4_workspace_bytes", "vdi_lz4_compress", "vdi_validate", "vdi_synth_rm_u8",
-           "vdi_gen_rays", "vdi_composite_lists", "vdi_dda_cells", "vdi_project_rays",
-           "vdi_preview_launch", "vdi_bilinear_upsample", "vdi_vdi1_max_bytes",
-           "vdi_encode_workspace_bytes", "vdi_encode_vdi1", "vdi_lz4_max_bytes",
-           "vdi_lz4_workspace_bytes", "vdi_lz4_compress", "vdi_validate", "vdi_synth_rm_u8",
-           "vdi_gen_rays", "vdi_composite_lists", "vdi_dda_cells", "vdi_project_rays", "vdi_dvr_launch",
+                 "vdi_decode_vdi1_lists", "vdi_lz4_compress", "vdi_validate", "vdi_synth_rm_u8",
+                 "vdi_gen_rays", "vdi_composite_lists", "vdi_dda_cells", "vdi_project_rays",
                  "vdi_find_first_batch", "vdi_segs_to_aos", "vdi_segs_from_aos"):
         getattr(L, name).restype = ctypes.c_int
     if L.vdi_abi_version() != 2:

@@ -142,6 +142,17 @@ int vdi_encode_vdi1(const VdiEncodeArgs* a, vdi_stream_t stream) {
   return vdi::encode_vdi1(a, static_cast<cudaStream_t>(stream));
 }
 
+int vdi_decode_vdi1_lists(const uint8_t* src, int32_t width, int32_t rows, int32_t n_sg,
+                          int32_t* counts, float* segs, void* workspace, size_t workspace_bytes,
+                          vdi_stream_t stream) {
+  if (!src || !counts || !segs || !workspace) return set_error(VDI_EINVAL, "null device pointer");
+  if (width < 1 || rows < 0 || n_sg < 1) return set_error(VDI_EINVAL, "bad sizes");
+  if (reinterpret_cast<uintptr_t>(segs) % 16 != 0)
+    return set_error(VDI_EINVAL, "segs must be 16-byte aligned");
+  return vdi::decode_vdi1_lists(src, width, rows, n_sg, counts, segs, workspace, workspace_bytes,
+                                static_cast<cudaStream_t>(stream));
+}
+
 size_t vdi_lz4_max_bytes(size_t n) { return n + n / 255 + 16; }
 
 size_t vdi_lz4_workspace_bytes(size_t n_max) { return vdi::lz4_workspace_bytes(n_max); }

@@ -229,6 +229,120 @@ int encode_vdi1(const VdiEncodeArgs* args, cudaStream_t stream) {
   return VDI_OK;
 }
 
+// VDI1 lists -> list-SoA (the receiving side of the multi-GPU exchange, and
+// decode_vdi's counts / segs on the device): counts u16 at byte 160, the
+// valid supersegments AoS after them. One thread per list copies its
+// supersegments into its list-SoA slot and zero-fills the tail (the
+// reference's (H, W, n_sg, 6) array is zero past each count).
+__global__ void dec_counts_kernel(const uint8_t* __restrict__ src, long long n,
+                                  int32_t* __restrict__ counts, unsigned long long* block_sums) {
+  __shared__ unsigned long long s_sum[kEncBlock / 32];
+  const long long l = (long long)blockIdx.x * kEncBlock + threadIdx.x;
+  int cnt = 0;
+  if (l < n) {
+    cnt = (int)src[kVdi1Header + 2 * l] | ((int)src[kVdi1Header + 2 * l + 1] << 8);
+    counts[l] = cnt;
+  }
+  unsigned long long sm = (unsigned long long)cnt;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) sm += __shfl_xor_sync(0xffffffffu, sm, o);
+  if ((threadIdx.x & 31) == 0) s_sum[threadIdx.x >> 5] = sm;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    unsigned long long t = s_sum[threadIdx.x];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (threadIdx.x == 0) block_sums[blockIdx.x] = t;
+  }
+}
+
+__global__ void scan_blocks_kernel(unsigned long long* block_sums, int nb) {
+  __shared__ unsigned long long s_part[1024];
+  const int t = threadIdx.x;
+  const int per = (nb + 1023) / 1024;
+  const int b0 = t * per, b1 = b0 + per < nb ? b0 + per : nb;
+  unsigned long long sum = 0;
+  for (int b = b0; b < b1; ++b) sum += block_sums[b];
+  s_part[t] = sum;
+  __syncthreads();
+  for (int off = 1; off < 1024; off <<= 1) {
+    const unsigned long long v = t >= off ? s_part[t - off] : 0ull;
+    __syncthreads();
+    s_part[t] += v;
+    __syncthreads();
+  }
+  unsigned long long run = t > 0 ? s_part[t - 1] : 0ull;
+  for (int b = b0; b < b1; ++b) {
+    const unsigned long long v = block_sums[b];
+    block_sums[b] = run;
+    run += v;
+  }
+}
+
+__global__ void dec_segs_kernel(const uint8_t* __restrict__ src, long long n, int n_sg,
+                                const int32_t* __restrict__ counts,
+                                const unsigned long long* __restrict__ block_off,
+                                float* __restrict__ segs) {
+  __shared__ int s_tmp[kEncBlock / 32];
+  const long long l = (long long)blockIdx.x * kEncBlock + threadIdx.x;
+  const int cnt = l < n ? counts[l] : 0;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int v = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int u = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += u;
+  }
+  if (lane == 31) s_tmp[wid] = v;
+  __syncthreads();
+  if (wid == 0) {
+    int w = s_tmp[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int u = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += u;
+    }
+    s_tmp[lane] = w;
+  }
+  __syncthreads();
+  if (l >= n) return;
+  const long long excl = (long long)block_off[blockIdx.x] + (v - cnt) + (wid > 0 ? s_tmp[wid - 1] : 0);
+  const uint8_t* rec = src + kVdi1Header + 2 * n + 24 * excl;
+  float* ls = segs + l * (long long)list_stride(n_sg);
+  float4* c4 = reinterpret_cast<float4*>(ls);
+  for (int k = 0; k < n_sg; ++k) {
+    float f[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    if (k < cnt) {
+      const uint8_t* r = rec + 24 * k;
+#pragma unroll
+      for (int j = 0; j < 6; ++j) {
+        const unsigned u = (unsigned)r[4 * j] | ((unsigned)r[4 * j + 1] << 8) |
+                           ((unsigned)r[4 * j + 2] << 16) | ((unsigned)r[4 * j + 3] << 24);
+        f[j] = __uint_as_float(u);
+      }
+    }
+    ls[front_off(n_sg) + k] = f[0];
+    ls[back_off(n_sg) + k] = f[1];
+    c4[k] = make_float4(f[2], f[3], f[4], f[5]);
+  }
+}
+
+int decode_vdi1_lists(const uint8_t* src, int width, int rows, int n_sg, int32_t* counts,
+                      float* segs, void* workspace, size_t ws_bytes, cudaStream_t stream) {
+  const long long n = (long long)width * rows;
+  if (n <= 0) return VDI_OK;
+  if (ws_bytes < encode_workspace_bytes(width, rows))
+    return set_error(VDI_EINVAL, "decode workspace too small");
+  const int nb = (int)enc_blocks(n);
+  unsigned long long* bsum = reinterpret_cast<unsigned long long*>(workspace) + 32;
+  dec_counts_kernel<<<nb, kEncBlock, 0, stream>>>(src, n, counts, bsum);
+  scan_blocks_kernel<<<1, 1024, 0, stream>>>(bsum, nb);
+  dec_segs_kernel<<<nb, kEncBlock, 0, stream>>>(src, n, n_sg, counts, bsum, segs);
+  const cudaError_t err = cudaGetLastError();
+  if (err != cudaSuccess) return set_error(VDI_ELAUNCH, "decode launch: %s", cudaGetErrorString(err));
+  return VDI_OK;
+}
+
 // -------------------------------------------------------------------- LZ4
 
 constexpr int kLz4Chunk = 32768;

@@ -35,6 +35,8 @@ int project_rays(const double* rays, long long n, const double* gen_pv, const do
                  double* out, int32_t* hit, cudaStream_t stream);
 size_t encode_workspace_bytes(int width, int height);
 int encode_vdi1(const VdiEncodeArgs* a, cudaStream_t stream);
+int decode_vdi1_lists(const uint8_t* src, int width, int rows, int n_sg, int32_t* counts,
+                      float* segs, void* workspace, size_t ws_bytes, cudaStream_t stream);
 size_t lz4_workspace_bytes(size_t n_max);
 int lz4_compress(const uint8_t* src, size_t n_max, const unsigned long long* n_dev, uint8_t* dst,
                  unsigned long long* out_len, void* workspace, size_t ws_bytes,

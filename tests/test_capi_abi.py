@@ -91,3 +91,15 @@ def test_invalid_args_rejected_without_launch(lib):
     assert lib.vdi_segs_to_aos(None, None, 1, 0, None) == -1
     assert lib.vdi_find_first_batch(None, None, None, 0, None, None, None, None, None, 1,
                                     None) == -1
+
+
+def test_size_queries_are_64_bit(lib):
+    """Byte-count queries return size_t: C5-sized answers exceed 2^32 and
+    must not be truncated by the binding (_capi.load sets the restypes)."""
+    from paper_2206_08660_b200 import _capi
+    L = _capi.load()
+    assert L.vdi_lz4_workspace_bytes(10_000_000_000) > 2 ** 34
+    assert L.vdi_vdi1_max_bytes(3840, 2160, 40, 240, 135, 32) == (
+        160 + 2 * 3840 * 2160 + 24 * 3840 * 2160 * 40 + 4 * 240 * 135 * 32)
+    assert L.vdi_lz4_max_bytes(2 ** 33) == 2 ** 33 + 2 ** 33 // 255 + 16
+    assert L.vdi_volume_cells_bytes(0, 2048, 2048, 1920) == 8 * 2048 * 2048 * 1920
