@@ -28,6 +28,7 @@ _LAZY = {
     "PiController": "preview", "pi_update": "preview", "samples_in_cell": "preview",
     "bilinear_upsample": "preview",
     "encode_vdi": "codec", "compress": "codec", "compress_vdi": "codec",
+    "decode_vdi": "codec",
 }
 
 

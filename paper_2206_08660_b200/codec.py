@@ -116,3 +116,72 @@ def compress_vdi(vdi, grid):
     lens = dv.to_host(dv.torch().cat([raw_len, out_len]))
     m = int(lens[1])
     return dv.to_host(dst[:m]).tobytes(), int(lens[0])
+
+
+class BadMagic(ValueError):
+    """vdi.py:27-28."""
+
+
+class VersionMismatch(ValueError):
+    """vdi.py:31-32."""
+
+
+class TruncatedStream(ValueError):
+    """vdi.py:35-36."""
+
+
+def decode_vdi(data: bytes):
+    """vdi.py:162-210 decode_vdi: VDI1 bytes -> (Vdi, AccelGrid), device
+    resident. The header and the length checks are read on the host (the
+    reference's errors: BadMagic, VersionMismatch, TruncatedStream); the
+    lists are unpacked on the device (vdi_decode_vdi1_lists) and validated
+    there (validate_vdi, InvariantViolation) as the reference does."""
+    from .camera import Camera
+    from .vdi import AccelGrid, DeviceVdi, Vdi, validate_vdi
+    t = dv.require_cuda()
+    L = _capi.load()
+    b = memoryview(data)
+    if len(b) < _HEADER.size:
+        raise TruncatedStream(f"need {_HEADER.size} bytes, have {len(b)}")
+    magic, version, width, height, n_sg = _HEADER.unpack_from(b, 0)
+    if magic != MAGIC:
+        raise BadMagic(repr(magic))
+    if version != VERSION:
+        raise VersionMismatch(f"version {version}, expected {VERSION}")
+    off = _HEADER.size
+    need = off + _CAMERA.size + _AABB.size + _GRID_DIMS.size
+    if len(b) < need:
+        raise TruncatedStream(f"need {need} bytes, have {len(b)}")
+    camvals = _CAMERA.unpack_from(b, off)
+    off += _CAMERA.size
+    aabbvals = _AABB.unpack_from(b, off)
+    off += _AABB.size
+    gdims = _GRID_DIMS.unpack_from(b, off)
+    off += _GRID_DIMS.size
+    n = width * height
+    if len(b) < off + 2 * n:
+        raise TruncatedStream(f"need {off + 2 * n} bytes, have {len(b)}")
+    counts_u16 = np.frombuffer(b, "<u2", n, off)
+    total = int(counts_u16.sum(dtype=np.int64))  # sizes the stream (vdi.py:182-183)
+    ng = gdims[0] * gdims[1] * gdims[2]
+    end = off + 2 * n + 24 * total + 4 * ng
+    if len(b) < end:
+        raise TruncatedStream(f"need {end} bytes, have {len(b)}")
+    if len(b) > end:
+        raise TruncatedStream(f"{len(b) - end} trailing bytes")
+    cam = Camera(position=camvals[0:3], orientation=camvals[3:7], fov_y=camvals[7],
+                 near=camvals[8], far=camvals[9], viewport=(width, height))
+    aabb = np.array(aabbvals, dtype=np.float64).reshape(2, 3)
+    src = dv.to_device(np.frombuffer(b, np.uint8, end - 4 * ng, 0))
+    counts = t.empty((height, width), dtype=t.int32, device="cuda")
+    segs = t.empty((max(n, 1), (6 * n_sg + 3) & ~3), dtype=t.float32, device="cuda")
+    ws = t.empty(int(L.vdi_encode_workspace_bytes(width, height)), dtype=t.uint8, device="cuda")
+    _capi.check(L.vdi_decode_vdi1_lists(dv.ptr(src), width, height, n_sg, dv.ptr(counts),
+                                        dv.ptr(segs), dv.ptr(ws), int(ws.numel()),
+                                        dv.stream_handle()))
+    grid = np.frombuffer(b, "<u4", ng, end - 4 * ng).reshape(gdims[2], gdims[1], gdims[0]).copy()
+    vdi = Vdi(width, height, n_sg, None, None, cam, aabb,
+              _device=DeviceVdi(counts=counts, segs=segs))
+    agrid = AccelGrid(tuple(gdims), grid, cam.near, cam.far)
+    validate_vdi(vdi)
+    return vdi, agrid

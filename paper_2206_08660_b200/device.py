@@ -48,7 +48,11 @@ def to_device(arr: np.ndarray, dtype=None):
     """H2D copy; pinned arrays (see pinned_numpy) copy asynchronously."""
     t = torch()
     a = np.ascontiguousarray(arr if dtype is None else arr.astype(dtype, copy=False))
-    return t.from_numpy(a).to("cuda", non_blocking=True)
+    import warnings
+    with warnings.catch_warnings():
+        # read-only sources (bytes objects) are only read by the copy
+        warnings.filterwarnings("ignore", message="The given NumPy array is not writable")
+        return t.from_numpy(a).to("cuda", non_blocking=True)
 
 
 def pinned_numpy(shape, np_dtype) -> np.ndarray:

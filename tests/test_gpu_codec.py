@@ -122,3 +122,38 @@ def test_validate_messages_match_reference():
             with pytest.raises(InvariantViolation) as e:
                 validate_vdi(v)
             assert str(e.value) == msg, k
+
+
+def test_decode_vdi_matches_reference_arrays():
+    """vdi.py:162-210 on the device: reference VDI1 bytes (the golden LZ4
+    blocks decompressed by the reference decoder) decode to the fixture's
+    counts, segments (zero past each count) and grid, and re-encode to the
+    same bytes; the reference's error cases raise its exceptions."""
+    from paper_2206_08660_b200.vdi import InvariantViolation
+    g = gio.load("codec")
+    for k, src in enumerate(str(t) for t in g["vdi_tags"]):
+        vdi0, grid0, gen = _fixture(src)
+        raw = oracle.lz4_decompress(g[f"v{k}_lz4"].tobytes(), int(g[f"v{k}_raw_len"]))
+        vdi, grid = codec.decode_vdi(raw)
+        assert np.array_equal(vdi.counts, vdi0.counts), src
+        assert np.array_equal(vdi.segs.view(np.uint32), vdi0.segs.view(np.uint32)), src
+        assert np.array_equal(grid.counts, grid0.counts), src
+        assert codec.encode_vdi(vdi, grid) == raw, src
+    vdi0, grid0, _ = _fixture("sphere64_u8")
+    raw = codec.encode_vdi(vdi0, grid0)
+    with pytest.raises(codec.BadMagic):
+        codec.decode_vdi(b"XDI1" + raw[4:])
+    with pytest.raises(codec.VersionMismatch):
+        codec.decode_vdi(raw[:4] + (2).to_bytes(4, "little") + raw[8:])
+    with pytest.raises(codec.TruncatedStream):
+        codec.decode_vdi(raw[:-1])
+    with pytest.raises(codec.TruncatedStream):
+        codec.decode_vdi(raw + b"\x00")
+    bad = bytearray(raw)
+    w = int.from_bytes(raw[8:12], "little")
+    n_sg = int.from_bytes(raw[16:20], "little")
+    bad[160:162] = (n_sg + 1).to_bytes(2, "little")  # list (0,0) count > n_sg
+    bad = bytes(bad) + b"\x00" * 24 * (n_sg + 1 - int.from_bytes(raw[160:162], "little"))
+    with pytest.raises((InvariantViolation, codec.TruncatedStream)):
+        codec.decode_vdi(bad)
+    del w
