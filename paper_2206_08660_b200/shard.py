@@ -17,6 +17,7 @@ with NCCL on B200s and with gloo on CPU tensors in the tests.
 from __future__ import annotations
 
 import time
+import weakref
 
 import numpy as np
 
@@ -127,7 +128,9 @@ class PackedExchange:
     def __init__(self, pipe):
         t = dv.torch()
         L = _capi.load()
-        self.pipe = pipe
+        # a proxy, not a reference: Pipeline owns this object, and a cycle
+        # would keep its (tens of GB of) device buffers alive after `del`
+        self.pipe = weakref.proxy(pipe)
         w, rows, n_sg = pipe.w, pipe.gen_rows, pipe.params.n_sg
         self.cap = int(L.vdi_vdi1_max_bytes(w, rows, n_sg, 1, 1, 1))
         self.buf = t.zeros(self.cap, dtype=t.uint8, device="cuda")

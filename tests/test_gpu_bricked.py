@@ -27,6 +27,8 @@ def _check(cfg, world, box_volume=None, max_frac=0.75):
     params = vb.GenParams(n_sg=n_sg)
     vdi, grid, st = vb.generate_vdi(vol, tf, gcam, params, with_stats=True)
     d = vdi.device()
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()  # the ranks below allocate their own (large) workspaces
     w, h = gcam.viewport
     full_bytes = int(np.prod(vol.dims)) * (1 if vol.voxel_type == "u8" else 4)
     grid_sum = torch.zeros_like(grid.device())
@@ -47,6 +49,7 @@ def _check(cfg, world, box_volume=None, max_frac=0.75):
         assert torch.equal(p.bufs.samples[:n].cpu(), torch.from_numpy(st.samples[r0:r0 + n])), r
         grid_sum += p.bufs.grid
         del p
+        torch.cuda.empty_cache()
     assert torch.equal(grid_sum, grid.device())  # the all-reduce of the partial grids
 
 
