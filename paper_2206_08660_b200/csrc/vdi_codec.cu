@@ -29,6 +29,7 @@
 // it decodes to the same input -- the property the transport relies on
 // (test_acceptance.py A6: decompress(compress(raw)) == raw).
 #include <cstdint>
+#include <cstdlib>
 
 #include "vdi_common.cuh"
 #include "vdi_internal.h"
@@ -346,9 +347,10 @@ int decode_vdi1_lists(const uint8_t* src, int width, int rows, int n_sg, int32_t
 // -------------------------------------------------------------------- LZ4
 
 constexpr int kLz4Chunk = 32768;
-constexpr int kLz4HashLog = 13;
+constexpr int kLz4HashLog = 12;  // default table: 4 Ki entries per warp
 constexpr int kLz4MaxSeq = kLz4Chunk / 4 + 1;
 constexpr int kLz4Warps = 4;
+constexpr int kLz4Group = 1;  // consecutive chunks parsed by one warp (table carried)
 constexpr unsigned short kNoPos = 0xffffu;
 
 struct ChunkSum {
@@ -374,28 +376,58 @@ struct Lz4Ws {
 };
 
 __device__ __forceinline__ unsigned ext_len(unsigned long long L) {  // bytes after the nibble
-  return L >= 15 ? (unsigned)((L - 15) / 255 + 1) : 0u;
+  if (L < 15) return 0u;
+  // 32-bit division whenever it suffices (the 64-bit one is a long subroutine)
+  return L - 15 <= 0xffffffffull ? (unsigned)(L - 15) / 255u + 1u
+                                 : (unsigned)((L - 15) / 255 + 1);
 }
 
+// 4 bytes at s + p, little endian, from the aligned words holding them (a
+// word that holds a byte of the buffer is mapped: allocations are aligned).
 __device__ __forceinline__ uint32_t rd32(const uint8_t* s, long long p) {
-  return (uint32_t)s[p] | ((uint32_t)s[p + 1] << 8) | ((uint32_t)s[p + 2] << 16) |
-         ((uint32_t)s[p + 3] << 24);
+  const uintptr_t a = reinterpret_cast<uintptr_t>(s + p);
+  const uint32_t* w = reinterpret_cast<const uint32_t*>(a & ~(uintptr_t)3);
+  const uint32_t sh = (uint32_t)(a & 3) * 8;
+  const uint32_t lo = __ldg(w);
+  return sh ? __funnelshift_r(lo, __ldg(w + 1), sh) : lo;
 }
 
+// The 4-byte values at positions i + lane (lane 0..31) of one warp, in two
+// steps so the load can be issued an iteration early: each lane loads one
+// aligned word of the 36-byte window (one coalesced load), and the unaligned
+// values are assembled with two shuffles.
+__device__ __forceinline__ uint32_t window_load(const uint8_t* s, long long n, long long i,
+                                                int lane) {
+  const uint32_t* wb =
+      reinterpret_cast<const uint32_t*>(reinterpret_cast<uintptr_t>(s + i) & ~(uintptr_t)3);
+  return reinterpret_cast<const uint8_t*>(wb + lane) < s + n ? __ldg(wb + lane) : 0u;
+}
+__device__ __forceinline__ uint32_t window_value(uint32_t wl, int o, int lane) {
+  const int k = (o + lane) >> 2;
+  const uint32_t lo = __shfl_sync(0xffffffffu, wl, k);
+  const uint32_t hi = __shfl_sync(0xffffffffu, wl, k + 1);
+  return __funnelshift_r(lo, hi, (uint32_t)((o + lane) & 3) * 8);
+}
+
+template <int HL>
 __device__ __forceinline__ uint32_t lz4_hash(uint32_t v) {
-  return (v * 2654435761u) >> (32 - kLz4HashLog);
+  return (v * 2654435761u) >> (32 - HL);
 }
 
 // One warp per chunk: greedy parse -> sequences + chunk summary.
+template <int HL>
 __global__ void __launch_bounds__(kLz4Warps * 32) lz4_parse_kernel(const uint8_t* __restrict__ src,
                                                                  Lz4Ws ws, long long n_chunks) {
   extern __shared__ unsigned short s_tab[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  unsigned short* tab = s_tab + (size_t)wib * (1 << kLz4HashLog);
+  unsigned short* tab = s_tab + (size_t)wib * (1 << HL);
   const long long n = (long long)*ws.n_dev;
   const long long mlimit_g = n - 12;  // lz4.py:17 MFLIMIT
-  for (long long ch = (long long)blockIdx.x * kLz4Warps + wib; ch < n_chunks;
-       ch += (long long)gridDim.x * kLz4Warps) {
+  const int o = (int)(reinterpret_cast<uintptr_t>(src) & 3);  // alignment of src + (4k)
+  const long long n_groups = (n_chunks + kLz4Group - 1) / kLz4Group;
+  for (long long g = (long long)blockIdx.x * kLz4Warps + wib; g < n_groups;
+       g += (long long)gridDim.x * kLz4Warps)
+  for (long long ch = g * kLz4Group; ch < (g + 1) * kLz4Group && ch < n_chunks; ++ch) {
     const long long cs = ch * kLz4Chunk;
     if (cs >= n) {
       if (lane == 0) ws.sums[ch] = ChunkSum{0u, 0u, 0u, 0u, 0ull};
@@ -405,46 +437,75 @@ __global__ void __launch_bounds__(kLz4Warps * 32) lz4_parse_kernel(const uint8_t
     const long long mend = ce < n - 5 ? ce : n - 5;  // matches end <= mend (LAST_LITERALS)
     // match starts < mlimit: room for a 4-byte match inside the chunk
     const long long mlimit = mend - 3 < mlimit_g ? mend - 3 : mlimit_g;
-    for (int k = lane; k < (1 << kLz4HashLog); k += 32) tab[k] = kNoPos;
-    __syncwarp();
     // Positions are stored relative to tb = cs - chunk, so the table also
-    // holds the previous chunk: warm it with every position of that chunk
-    // (last writer of a hash wins, as in a serial pass). Matches may then
-    // reach back into it (offsets stay < 65536; the decoder has those bytes).
+    // holds the previous chunk and matches may reach back into it (offsets
+    // stay < 65536; the decoder has those bytes). The first chunk of a group
+    // warms the table with every position of the previous chunk (the last
+    // writer of a hash wins, as in a serial pass); the next chunks of the
+    // group keep the table of the chunk just parsed, shifted by one chunk.
     const long long tb = cs - kLz4Chunk;
-    if (cs > 0) {
-      for (long long q0 = tb; q0 < cs; q0 += 32) {
-        const long long q = q0 + lane;
-        const bool ok = q + 3 < n;
-        const uint32_t hq = lz4_hash(ok ? rd32(src, q) : 0u);
-        const unsigned pe = __match_any_sync(0xffffffffu, ok ? hq : (0x10000u + lane));
-        if (ok && !(pe >> lane >> 1)) tab[hq] = (unsigned short)(q - tb);
-        __syncwarp();
+    if (ch > g * kLz4Group) {
+      for (int k = lane; k < (1 << HL); k += 32) {
+        const unsigned t = tab[k];
+        tab[k] = t != kNoPos && t >= (unsigned)kLz4Chunk ? (unsigned short)(t - kLz4Chunk)
+                                                         : kNoPos;
+      }
+      __syncwarp();
+    } else {
+      for (int k = lane; k < (1 << HL); k += 32) tab[k] = kNoPos;
+      __syncwarp();
+      if (cs > 0) {
+        // two batches of 32 positions per step (independent until their
+        // stores, which stay in position order)
+        uint32_t wl0 = window_load(src, n, tb, lane), wl1 = window_load(src, n, tb + 32, lane);
+        for (long long q0 = tb; q0 < cs; q0 += 64) {
+          const uint32_t wn0 = window_load(src, n, q0 + 64, lane);
+          const uint32_t wn1 = window_load(src, n, q0 + 96, lane);
+          const long long qa = q0 + lane, qb = qa + 32;
+          const bool oka = qa + 3 < n, okb = qb + 3 < n;
+          const uint32_t ha = lz4_hash<HL>(window_value(wl0, o, lane));
+          const uint32_t hb = lz4_hash<HL>(window_value(wl1, o, lane));
+          wl0 = wn0;
+          wl1 = wn1;
+          const unsigned pa = __match_any_sync(0xffffffffu, oka ? ha : (0x10000u + lane));
+          const unsigned pb = __match_any_sync(0xffffffffu, okb ? hb : (0x10000u + lane));
+          if (oka && !(pa >> lane >> 1)) tab[ha] = (unsigned short)(qa - tb);
+          __syncwarp();
+          if (okb && !(pb >> lane >> 1)) tab[hb] = (unsigned short)(qb - tb);
+          __syncwarp();
+        }
       }
     }
+    // the parse runs in 32-bit offsets from base (the table's origin)
+    const long long base = cs > 0 ? tb : cs;
+    const uint8_t* sb = src + base;
+    const long long nrl = n - base < 3ll * kLz4Chunk ? n - base : 3ll * kLz4Chunk;
+    const int nr = (int)nrl;  // readable bytes from sb (clamped)
+    const int mlim = (int)(mlimit - base), mendr = (int)(mend - base);
     uint2* seq = ws.seqs + ch * kLz4MaxSeq;
     unsigned nseq = 0, lead = 0;
     unsigned long long rest = 0;
-    long long i = cs, anchor = cs;
-    while (i < mlimit) {
-      const long long p = i + lane;
-      const bool valid = p < mlimit;
-      const uint32_t v = valid ? rd32(src, p) : 0u;
-      const uint32_t h = lz4_hash(v);
+    int i = (int)(cs - base), anchor = i;
+    uint32_t wl = window_load(sb, nr, i, lane);
+    while (i < mlim) {
+      const uint32_t wn = window_load(sb, nr, i + 32, lane);  // the no-match successor
+      const int p = i + lane;
+      const bool valid = p < mlim;
+      const uint32_t v = window_value(wl, (o + (i & 3)) & 3, lane);
+      const uint32_t h = lz4_hash<HL>(v);
+      // the table candidate and its bytes are fetched while the warp finds
+      // same-hash lanes; a lower lane's candidate is its own value
+      const unsigned short t = valid ? tab[h] : kNoPos;
+      const int tc = t != kNoPos ? (int)t : -1;
+      const uint32_t tv = tc >= 0 ? rd32(sb, tc) : ~v;
       const unsigned key = valid ? h : (0x10000u + lane);
       const unsigned peers = __match_any_sync(0xffffffffu, key);
       const unsigned lt = (1u << lane) - 1u;
       const unsigned lower = peers & lt;
-      long long cand = -1;
-      if (valid) {
-        if (lower) {
-          cand = i + (31 - __clz(lower));
-        } else {
-          const unsigned short t = tab[h];
-          if (t != kNoPos) cand = (cs > 0 ? tb : cs) + t;
-        }
-      }
-      const bool match = cand >= 0 && rd32(src, cand) == v;
+      const int pl = lower ? 31 - __clz(lower) : lane;
+      const uint32_t pv = __shfl_sync(0xffffffffu, v, pl);
+      const int cand = lower ? i + pl : tc;
+      const bool match = valid && (lower ? pv == v : tv == v);
       const unsigned mm = __ballot_sync(0xffffffffu, match);
       const int w = mm ? __ffs(mm) - 1 : 31;
       const unsigned upto = w == 31 ? 0xffffffffu : ((2u << w) - 1u);
@@ -452,23 +513,24 @@ __global__ void __launch_bounds__(kLz4Warps * 32) lz4_parse_kernel(const uint8_t
       // (lz4.py:62); the last writer of a hash wins
       __syncwarp();
       if (valid && ((1u << lane) & upto) && !(peers & upto & ~lt & ~(1u << lane)))
-        tab[h] = (unsigned short)(p - (cs > 0 ? tb : cs));
+        tab[h] = (unsigned short)p;
       __syncwarp();
       if (!mm) {
         i += 32;
+        wl = wn;
         continue;
       }
-      const long long pw = i + w;
-      const long long cw = __shfl_sync(0xffffffffu, cand, w);
+      const int pw = i + w;
+      const int cw = __shfl_sync(0xffffffffu, cand, w);
       // extend (lz4.py:66-69), 32 bytes per step
-      long long mlen = 4;
-      const long long mmax = mend - pw;
+      int mlen = 4;
+      const int mmax = mendr - pw;
       while (true) {
-        const long long k = mlen + lane;
-        const bool stop = k >= mmax || src[cw + k] != src[pw + k];
-        const unsigned sb = __ballot_sync(0xffffffffu, stop);
-        if (sb) {
-          mlen += __ffs(sb) - 1;
+        const int k = mlen + lane;
+        const bool stop = k >= mmax || sb[cw + k] != sb[pw + k];
+        const unsigned sbits = __ballot_sync(0xffffffffu, stop);
+        if (sbits) {
+          mlen += __ffs(sbits) - 1;
           break;
         }
         mlen += 32;
@@ -483,12 +545,12 @@ __global__ void __launch_bounds__(kLz4Warps * 32) lz4_parse_kernel(const uint8_t
       nseq += 1;
       i = pw + mlen;
       anchor = i;
-      if (i < mlimit && lane == 0)
-        tab[lz4_hash(rd32(src, i - 2))] = (unsigned short)(i - 2 - (cs > 0 ? tb : cs));
+      if (i < mlim && lane == 0) tab[lz4_hash<HL>(rd32(sb, i - 2))] = (unsigned short)(i - 2);
+      wl = window_load(sb, nr, i, lane);
       __syncwarp();
     }
     if (lane == 0)
-      ws.sums[ch] = ChunkSum{nseq, lead, (unsigned)(ce - anchor), (unsigned)(ce - cs), rest};
+      ws.sums[ch] = ChunkSum{nseq, lead, (unsigned)(ce - base - anchor), (unsigned)(ce - cs), rest};
   }
 }
 
@@ -661,13 +723,18 @@ int lz4_compress(const uint8_t* src, size_t n_max, const unsigned long long* n_d
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const long long nch = nc > 0 ? nc : 0;
   if (nch > 0) {
-    long long b = (nch + kLz4Warps - 1) / kLz4Warps;
+    const long long ng = (nch + kLz4Group - 1) / kLz4Group;
+    long long b = (ng + kLz4Warps - 1) / kLz4Warps;
     if (b > (long long)sms * 16) b = (long long)sms * 16;
-    const size_t smem = sizeof(unsigned short) * kLz4Warps * ((size_t)1 << kLz4HashLog);
-    err = cudaFuncSetAttribute(lz4_parse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)smem);
+    // VDI_LZ4_HASHLOG (12 or 13) selects the table size: tuning experiments only
+    const char* hl_env = getenv("VDI_LZ4_HASHLOG");
+    const int hl = hl_env && atoi(hl_env) == 12 ? 12 : (hl_env && atoi(hl_env) == 13 ? 13 : kLz4HashLog);
+    const size_t smem = sizeof(unsigned short) * kLz4Warps * ((size_t)1 << hl);
+    const void* fn = hl == 12 ? (const void*)lz4_parse_kernel<12> : (const void*)lz4_parse_kernel<13>;
+    err = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (err != cudaSuccess) return set_error(VDI_ELAUNCH, "lz4 smem: %s", cudaGetErrorString(err));
-    lz4_parse_kernel<<<(unsigned)b, kLz4Warps * 32, smem, stream>>>(src, ws, nch);
+    if (hl == 12) lz4_parse_kernel<12><<<(unsigned)b, kLz4Warps * 32, smem, stream>>>(src, ws, nch);
+    else lz4_parse_kernel<13><<<(unsigned)b, kLz4Warps * 32, smem, stream>>>(src, ws, nch);
   }
   lz4_scan_kernel<<<1, 1024, 0, stream>>>(ws, nch, out_len);
   {

@@ -27,6 +27,7 @@ if not torch.cuda.is_available():
 
 import paper_2206_08660_b200 as vb  # noqa: E402
 from paper_2206_08660_b200 import codec, synth  # noqa: E402
+from paper_2206_08660_b200 import device as dv  # noqa: E402
 from paper_2206_08660_b200.camera import Camera  # noqa: E402
 from paper_2206_08660_b200.vdi import InvariantViolation, validate_vdi  # noqa: E402
 from oracle import oracle  # noqa: E402
@@ -73,7 +74,7 @@ def test_lz4_roundtrip_reference_vectors():
         _check_block(comp, raw)
 
 
-@pytest.mark.parametrize("n", [12, 13, 17, 32767, 32768, 32769, 65536 + 5, 300001])
+@pytest.mark.parametrize("n", [12, 13, 17, 32767, 32768, 32769, 65536 + 5, 3 * 32768 + 7, 300001])
 def test_lz4_chunk_boundaries(n):
     rng = np.random.default_rng(n)
     words = [rng.integers(0, 256, int(k), dtype=np.uint8).tobytes()
@@ -82,6 +83,21 @@ def test_lz4_chunk_boundaries(n):
     raw = raw[:n // 2] + b"\x00" * (n - n // 2)
     comp = codec.compress(raw)
     _check_block(comp, raw)
+
+
+@pytest.mark.parametrize("shift", [1, 2, 3])
+def test_lz4_unaligned_source(shift):
+    """The C ABI takes any device pointer: windows of an unaligned source are
+    assembled from aligned words (csrc/vdi_codec.cu window_load/value)."""
+    rng = np.random.default_rng(shift)
+    words = [rng.integers(0, 256, int(k), dtype=np.uint8).tobytes()
+             for k in rng.integers(4, 64, 40)]
+    n = 4 * 32768 + 1001
+    raw = b"".join(words[int(i)] for i in rng.integers(0, 40, n // 4 + 1))[:n]
+    buf = dv.to_device(np.frombuffer(b"\x55" * shift + raw + b"\xaa" * 3, dtype=np.uint8))
+    dst, out_len = codec.compress_device(buf[shift:shift + n], n)
+    m = int(dv.to_host(out_len)[0])
+    _check_block(dv.to_host(dst[:m]).tobytes(), raw)
 
 
 def test_lz4_ratio_close_to_reference():
