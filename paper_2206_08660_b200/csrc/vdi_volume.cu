@@ -9,6 +9,7 @@
 // vdi_gen.cu). The reduction is integer/float max, so it is exact.
 #include "vdi_common.cuh"
 #include "vdi_internal.h"
+#include <algorithm>
 #include <type_traits>
 
 namespace vdi {
@@ -36,6 +37,33 @@ __global__ void brick_max_kernel(const T* __restrict__ vol, T* __restrict__ out,
   out[b] = m;
 }
 
+// u8 bricks of 8 (nx % 8 == 0, 8-byte aligned volume): each row of a brick
+// (9 voxels with the +1 overlap) is one aligned 8-byte load plus one byte,
+// reduced with SIMD byte maxima.
+__global__ void brick_max_u8x8_kernel(const uint8_t* __restrict__ vol, uint8_t* __restrict__ out,
+                                      int nx, int ny, int nz, int bx_n, int by_n,
+                                      long long n_bricks) {
+  const long long b = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= n_bricks) return;
+  const int bx = (int)(b % bx_n);
+  const int by = (int)((b / bx_n) % by_n);
+  const int bz = (int)(b / ((long long)bx_n * by_n));
+  const int x0 = bx * 8, y0 = by * 8, z0 = bz * 8;
+  const int y1 = min(y0 + 8, ny - 1), z1 = min(z0 + 8, nz - 1);
+  const bool has_next = x0 + 8 <= nx - 1;  // the overlap voxel x0 + 8 exists
+  unsigned m4 = 0u, me = 0u;
+  for (int z = z0; z <= z1; ++z)
+    for (int y = y0; y <= y1; ++y) {
+      const uint8_t* row = vol + ((long long)z * ny + y) * nx + x0;
+      const uint2 w = __ldg(reinterpret_cast<const uint2*>(row));
+      m4 = __vmaxu4(m4, __vmaxu4(w.x, w.y));
+      if (has_next) me = max(me, (unsigned)__ldg(row + 8));
+    }
+  const unsigned a = max(m4 & 0xffu, (m4 >> 8) & 0xffu);
+  const unsigned c = max((m4 >> 16) & 0xffu, m4 >> 24);
+  out[b] = (uint8_t)max(max(a, c), me);
+}
+
 int brick_max(const void* volume, int voxel_type, int nx, int ny, int nz, int log2b, void* out,
               cudaStream_t stream) {
   const int B = 1 << log2b;
@@ -44,6 +72,12 @@ int brick_max(const void* volume, int voxel_type, int nx, int ny, int nz, int lo
   const unsigned blocks = (unsigned)((n + 127) / 128);
   switch (voxel_type) {
     case VDI_VOXEL_U8:
+      if (log2b == 3 && nx % 8 == 0 && (reinterpret_cast<uintptr_t>(volume) & 7) == 0) {
+        brick_max_u8x8_kernel<<<blocks, 128, 0, stream>>>(static_cast<const uint8_t*>(volume),
+                                                          static_cast<uint8_t*>(out), nx, ny, nz,
+                                                          bx, by, n);
+        break;
+      }
       brick_max_kernel<<<blocks, 128, 0, stream>>>(static_cast<const uint8_t*>(volume),
                                                    static_cast<uint8_t*>(out), nx, ny, nz, log2b,
                                                    bx, by, n);
@@ -152,43 +186,46 @@ __global__ void cells_kernel(const T* __restrict__ vol, void* __restrict__ out, 
 // rows, and stores them as two 16-byte writes.
 __global__ void cells_u8x4_kernel(const uint8_t* __restrict__ vol, uint4* __restrict__ out,
                                   int nx, int ny, int nz, const CellMask<uint8_t> mask) {
+  // one (y, z) row per block iteration: 32-bit row arithmetic, no 64-bit
+  // division per thread
   const int qx = nx >> 2;
-  const long long n = (long long)qx * ny * nz;
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (long long)gridDim.x * blockDim.x) {
-    const int x = (int)(i % qx) * 4;
-    const long long yz = i / qx;
-    const int y = (int)(yz % ny), z = (int)(yz / ny);
-    if (mask.skip(x, y, z)) continue;  // the 4 cells share a brick (x % 4 == 0, edge >= 4)
-    const long long base = yz * nx + x;
+  const int rows = ny * nz;
+  for (int row = blockIdx.x; row < rows; row += gridDim.x) {
+    const int y = row % ny, z = row / ny;
     const long long dy = y + 1 < ny ? nx : 0;
     const long long dz = z + 1 < nz ? (long long)nx * ny : 0;
-    const bool last = x + 4 >= nx;
-    unsigned w[4], e[4];  // rows (y,z), (y+1,z), (y,z+1), (y+1,z+1)
     const long long off[4] = {0, dy, dz, dy + dz};
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      w[r] = __ldg(reinterpret_cast<const unsigned*>(vol + base + off[r]));
-      // voxel x+4 (clamped to x+3 at the row end: the last cell repeats it)
-      e[r] = last ? (w[r] >> 24) : (unsigned)__ldg(vol + base + off[r] + 4);
-    }
-    unsigned rec[8];  // cell j: rec[2j] = (v000 v001 v010 v011), rec[2j+1] = z+1 row pair
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      // bytes j and j+1 of each row (byte 4 = e[r])
-      unsigned p[4];
+    const long long rbase = (long long)row * nx;
+    for (int q = threadIdx.x; q < qx; q += blockDim.x) {
+      const int x = q * 4;
+      if (mask.skip(x, y, z)) continue;  // the 4 cells share a brick (x % 4 == 0, edge >= 4)
+      const long long base = rbase + x;
+      const bool last = x + 4 >= nx;
+      unsigned w[4], e[4];  // rows (y,z), (y+1,z), (y,z+1), (y+1,z+1)
 #pragma unroll
       for (int r = 0; r < 4; ++r) {
-        const unsigned lo = (w[r] >> (8 * j)) & 0xffu;
-        const unsigned hi = j < 3 ? (w[r] >> (8 * (j + 1))) & 0xffu : e[r];
-        p[r] = lo | (hi << 8);
+        w[r] = __ldg(reinterpret_cast<const unsigned*>(vol + base + off[r]));
+        // voxel x+4 (clamped to x+3 at the row end: the last cell repeats it)
+        e[r] = last ? (w[r] >> 24) : (unsigned)__ldg(vol + base + off[r] + 4);
       }
-      rec[2 * j] = p[0] | (p[1] << 16);
-      rec[2 * j + 1] = p[2] | (p[3] << 16);
+      unsigned rec[8];  // cell j: rec[2j] = (v000 v001 v010 v011), rec[2j+1] = z+1 row pair
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        // bytes j and j+1 of each row (byte 4 = e[r])
+        unsigned p[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const unsigned lo = (w[r] >> (8 * j)) & 0xffu;
+          const unsigned hi = j < 3 ? (w[r] >> (8 * (j + 1))) & 0xffu : e[r];
+          p[r] = lo | (hi << 8);
+        }
+        rec[2 * j] = p[0] | (p[1] << 16);
+        rec[2 * j + 1] = p[2] | (p[3] << 16);
+      }
+      uint4* o = out + 2 * (base >> 2);
+      o[0] = make_uint4(rec[0], rec[1], rec[2], rec[3]);
+      o[1] = make_uint4(rec[4], rec[5], rec[6], rec[7]);
     }
-    uint4* o = out + 2 * i;
-    o[0] = make_uint4(rec[0], rec[1], rec[2], rec[3]);
-    o[1] = make_uint4(rec[4], rec[5], rec[6], rec[7]);
   }
 }
 
@@ -211,7 +248,8 @@ int volume_cells(const void* volume, int voxel_type, int nx, int ny, int nz, voi
   switch (voxel_type) {
     case VDI_VOXEL_U8:
       if (nx % 4 == 0)
-        cells_u8x4_kernel<<<(unsigned)((blocks + 3) / 4), 256, 0, stream>>>(
+        cells_u8x4_kernel<<<(unsigned)std::min<long long>((long long)ny * nz, (long long)sms * 32),
+                            256, 0, stream>>>(
             static_cast<const uint8_t*>(volume), static_cast<uint4*>(out), nx, ny, nz,
             mk((uint8_t*)nullptr));
       else
