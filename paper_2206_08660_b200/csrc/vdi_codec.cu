@@ -350,7 +350,7 @@ constexpr int kLz4Chunk = 32768;
 constexpr int kLz4HashLog = 12;  // default table: 4 Ki entries per warp
 constexpr int kLz4MaxSeq = kLz4Chunk / 4 + 1;
 constexpr int kLz4Warps = 4;
-constexpr int kLz4Group = 1;  // consecutive chunks parsed by one warp (table carried)
+constexpr int kLz4Warm = 16384;  // bytes of the previous chunk hashed into a chunk's table
 constexpr unsigned short kNoPos = 0xffffu;
 
 struct ChunkSum {
@@ -424,10 +424,8 @@ __global__ void __launch_bounds__(kLz4Warps * 32) lz4_parse_kernel(const uint8_t
   const long long n = (long long)*ws.n_dev;
   const long long mlimit_g = n - 12;  // lz4.py:17 MFLIMIT
   const int o = (int)(reinterpret_cast<uintptr_t>(src) & 3);  // alignment of src + (4k)
-  const long long n_groups = (n_chunks + kLz4Group - 1) / kLz4Group;
-  for (long long g = (long long)blockIdx.x * kLz4Warps + wib; g < n_groups;
-       g += (long long)gridDim.x * kLz4Warps)
-  for (long long ch = g * kLz4Group; ch < (g + 1) * kLz4Group && ch < n_chunks; ++ch) {
+  for (long long ch = (long long)blockIdx.x * kLz4Warps + wib; ch < n_chunks;
+       ch += (long long)gridDim.x * kLz4Warps) {
     const long long cs = ch * kLz4Chunk;
     if (cs >= n) {
       if (lane == 0) ws.sums[ch] = ChunkSum{0u, 0u, 0u, 0u, 0ull};
@@ -439,26 +437,21 @@ __global__ void __launch_bounds__(kLz4Warps * 32) lz4_parse_kernel(const uint8_t
     const long long mlimit = mend - 3 < mlimit_g ? mend - 3 : mlimit_g;
     // Positions are stored relative to tb = cs - chunk, so the table also
     // holds the previous chunk and matches may reach back into it (offsets
-    // stay < 65536; the decoder has those bytes). The first chunk of a group
-    // warms the table with every position of the previous chunk (the last
-    // writer of a hash wins, as in a serial pass); the next chunks of the
-    // group keep the table of the chunk just parsed, shifted by one chunk.
+    // stay < 65536; the decoder has those bytes). The table is warmed with
+    // every position of the previous chunk's last kLz4Warm bytes (the last
+    // writer of a hash wins, as in a serial pass): with 4 Ki slots, a slot
+    // whose last writer lies further back survives 16 Ki later positions
+    // with probability e^-4, so the older half adds almost nothing.
     const long long tb = cs - kLz4Chunk;
-    if (ch > g * kLz4Group) {
-      for (int k = lane; k < (1 << HL); k += 32) {
-        const unsigned t = tab[k];
-        tab[k] = t != kNoPos && t >= (unsigned)kLz4Chunk ? (unsigned short)(t - kLz4Chunk)
-                                                         : kNoPos;
-      }
-      __syncwarp();
-    } else {
+    {
       for (int k = lane; k < (1 << HL); k += 32) tab[k] = kNoPos;
       __syncwarp();
       if (cs > 0) {
         // two batches of 32 positions per step (independent until their
         // stores, which stay in position order)
-        uint32_t wl0 = window_load(src, n, tb, lane), wl1 = window_load(src, n, tb + 32, lane);
-        for (long long q0 = tb; q0 < cs; q0 += 64) {
+        const long long w0 = cs - kLz4Warm;
+        uint32_t wl0 = window_load(src, n, w0, lane), wl1 = window_load(src, n, w0 + 32, lane);
+        for (long long q0 = w0; q0 < cs; q0 += 64) {
           const uint32_t wn0 = window_load(src, n, q0 + 64, lane);
           const uint32_t wn1 = window_load(src, n, q0 + 96, lane);
           const long long qa = q0 + lane, qb = qa + 32;
@@ -723,8 +716,7 @@ int lz4_compress(const uint8_t* src, size_t n_max, const unsigned long long* n_d
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const long long nch = nc > 0 ? nc : 0;
   if (nch > 0) {
-    const long long ng = (nch + kLz4Group - 1) / kLz4Group;
-    long long b = (ng + kLz4Warps - 1) / kLz4Warps;
+    long long b = (nch + kLz4Warps - 1) / kLz4Warps;
     if (b > (long long)sms * 16) b = (long long)sms * 16;
     // VDI_LZ4_HASHLOG (12 or 13) selects the table size: tuning experiments only
     const char* hl_env = getenv("VDI_LZ4_HASHLOG");
