@@ -547,6 +547,64 @@ __global__ void __launch_bounds__(kLz4Warps * 32) lz4_parse_kernel(const uint8_t
   }
 }
 
+// The effect of a run of chunks on (carried literals cin, output offset
+// off): without a match the run only carries its bytes forward; with one,
+// its first sequence absorbs cin and the run leaves its trailing literals.
+// Composition (then) keeps that form, so runs combine in a warp scan.
+struct Lz4Carry {
+  int any;                        // the run holds a sequence with a match
+  unsigned long long pre;         // bytes before its first match chunk
+  unsigned long long lead;        // that chunk's own leading literals
+  unsigned long long after;       // encoded bytes besides the first literal field
+  unsigned long long cout;        // literals carried out (when any)
+  unsigned long long lenall;      // all bytes of the run
+  __device__ static Lz4Carry identity() { return Lz4Carry{0, 0ull, 0ull, 0ull, 0ull, 0ull}; }
+  __device__ void apply(unsigned long long& cin, unsigned long long& off) const {
+    if (any) {
+      const unsigned long long L = cin + pre + lead;
+      off += after + ext_len(L) + L;
+      cin = cout;
+    } else {
+      cin += lenall;
+    }
+  }
+  __device__ Lz4Carry then(const Lz4Carry& g) const {  // this run, then g
+    Lz4Carry r;
+    r.lenall = lenall + g.lenall;
+    if (!any) {
+      r.any = g.any;
+      r.pre = lenall + g.pre;
+      r.lead = g.lead;
+      r.after = g.after;
+      r.cout = g.cout;
+    } else if (!g.any) {
+      r.any = 1;
+      r.pre = pre;
+      r.lead = lead;
+      r.after = after;
+      r.cout = cout + g.lenall;
+    } else {
+      const unsigned long long L = cout + g.pre + g.lead;
+      r.any = 1;
+      r.pre = pre;
+      r.lead = lead;
+      r.after = after + g.after + ext_len(L) + L;
+      r.cout = g.cout;
+    }
+    return r;
+  }
+  __device__ Lz4Carry shfl_up(int d) const {
+    Lz4Carry r;
+    r.any = __shfl_up_sync(0xffffffffu, any, d);
+    r.pre = __shfl_up_sync(0xffffffffu, pre, d);
+    r.lead = __shfl_up_sync(0xffffffffu, lead, d);
+    r.after = __shfl_up_sync(0xffffffffu, after, d);
+    r.cout = __shfl_up_sync(0xffffffffu, cout, d);
+    r.lenall = __shfl_up_sync(0xffffffffu, lenall, d);
+    return r;
+  }
+};
+
 // One block: compose the chunks' carry/size functions, assign offsets.
 // Chunk with matches: size(cin) = rest + ext(cin + lead) + cin + lead,
 // cout = trail. Chunk without: size 0, cout = cin + len.
@@ -587,24 +645,37 @@ __global__ void lz4_scan_kernel(Lz4Ws ws, long long n_chunks, unsigned long long
   __syncthreads();
   unsigned long long* s_cin = s_pre;   // reused: thread k's carry-in ...
   unsigned long long* s_off = s_lead;  // ... and output offset
-  if (t == 0) {
+  if (t < 32) {
+    // warp 0: lane l composes the summaries of threads [32 l, 32 l + 32),
+    // a warp scan composes the lanes, and each lane then walks its 32 again
+    // assigning carry-ins and offsets (64 serial steps instead of 1024)
+    Lz4Carry acc = Lz4Carry::identity();
+    for (int j = 0; j < 32; ++j) {
+      const int k = 32 * t + j;
+      acc = acc.then(Lz4Carry{s_any[k], s_pre[k], s_lead[k], s_after[k], s_cout[k], s_lenall[k]});
+    }
+    Lz4Carry inc = acc;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const Lz4Carry up = inc.shfl_up(d);
+      if (t >= d) inc = up.then(inc);
+    }
+    const Lz4Carry exc = inc.shfl_up(1);
     unsigned long long cin = 0, off = 0;
-    for (int k = 0; k < 1024; ++k) {
-      const unsigned long long pre_k = s_pre[k], lead_k = s_lead[k];
+    if (t > 0) exc.apply(cin, off);
+    for (int j = 0; j < 32; ++j) {
+      const int k = 32 * t + j;
+      const Lz4Carry f{s_any[k], s_pre[k], s_lead[k], s_after[k], s_cout[k], s_lenall[k]};
       s_cin[k] = cin;
       s_off[k] = off;
-      if (s_any[k]) {
-        const unsigned long long L = cin + pre_k + lead_k;
-        off += s_after[k] + ext_len(L) + L;
-        cin = s_cout[k];
-      } else {
-        cin += s_lenall[k];
-      }
+      f.apply(cin, off);
     }
-    const unsigned long long n = *ws.n_dev;
-    ws.final_[0] = off;
-    ws.final_[1] = cin;
-    *out_len = n == 0 ? 0ull : off + 1ull + ext_len(cin) + cin;
+    if (t == 31) {
+      const unsigned long long n = *ws.n_dev;
+      ws.final_[0] = off;
+      ws.final_[1] = cin;
+      *out_len = n == 0 ? 0ull : off + 1ull + ext_len(cin) + cin;
+    }
   }
   __syncthreads();
   unsigned long long cin = s_cin[t], off = s_off[t];
@@ -671,14 +742,65 @@ __global__ void __launch_bounds__(kLz4Warps * 32) lz4_emit_kernel(const uint8_t*
     const ChunkPlan pl = ws.plans[ch];
     const long long cs = ch * kLz4Chunk;
     const uint2* seq = ws.seqs + ch * kLz4MaxSeq;
-    unsigned long long o = pl.off;
-    long long pos = cs - (long long)pl.cin;  // literal source
-    for (unsigned k = 0; k < s.nseq; ++k) {
-      const uint2 q = seq[k];
-      const unsigned lit = q.x & 0xffffu, off = q.x >> 16;
-      const unsigned long long L = k == 0 ? (unsigned long long)pl.cin + lit : lit;
-      o = put_seq(dst, o, src, pos, L, false, off, (long long)q.y, lane);
-      pos += (long long)L + q.y;
+    unsigned long long o = pl.off;           // output offset of the batch
+    long long pos = cs - (long long)pl.cin;  // literal source of the batch
+    // 32 sequences per step: one coalesced load of their records, warp scans
+    // of their encoded sizes and source spans, headers written by the owning
+    // lane, literals copied by the owning lane (short) or the warp (long)
+    for (unsigned kb = 0; kb < s.nseq; kb += 32) {
+      const unsigned k = kb + lane;
+      const bool v = k < s.nseq;
+      const uint2 q = v ? seq[k] : make_uint2(0u, 4u);
+      const unsigned off = q.x >> 16;
+      const unsigned long long L = (q.x & 0xffffu) + (k == 0 ? (unsigned long long)pl.cin : 0ull);
+      const unsigned mlen = q.y;
+      const unsigned el = ext_len(L), em = ext_len((unsigned long long)(mlen - 4));
+      const unsigned long long size = v ? 3ull + el + L + em : 0ull;
+      const unsigned long long span = v ? L + mlen : 0ull;
+      unsigned long long so = size, sp = span;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const unsigned long long a = __shfl_up_sync(0xffffffffu, so, d);
+        const unsigned long long b = __shfl_up_sync(0xffffffffu, sp, d);
+        if (lane >= d) {
+          so += a;
+          sp += b;
+        }
+      }
+      const unsigned long long mo = o + so - size;            // this sequence's token
+      const long long ms = pos + (long long)(sp - span);      // its literals' source
+      const unsigned long long lo = mo + 1 + el;              // its literals' destination
+      if (v) {
+        const unsigned mc = mlen - 4;
+        dst[mo] = (uint8_t)(((L >= 15 ? 15u : (unsigned)L) << 4) | (mc >= 15 ? 15u : mc));
+        if (el <= 32)
+          for (unsigned j = 0; j < el; ++j)
+            dst[mo + 1 + j] = j + 1 < el ? 255 : (uint8_t)((L - 15) - 255ull * (el - 1));
+        const unsigned long long om = lo + L;
+        dst[om] = (uint8_t)(off & 0xff);
+        dst[om + 1] = (uint8_t)(off >> 8);
+        for (unsigned j = 0; j < em; ++j)
+          dst[om + 2 + j] = j + 1 < em ? 255 : (uint8_t)((mc - 15) - 255u * (em - 1));
+        if (L < 32)
+          for (unsigned j = 0; j < (unsigned)L; ++j) dst[lo + j] = src[ms + j];
+      }
+      // long literal-length extensions (carried literals) and long literal runs
+      unsigned big = __ballot_sync(0xffffffffu, v && (el > 32 || L >= 32));
+      while (big) {
+        const int j = __ffs(big) - 1;
+        big &= big - 1;
+        const unsigned long long jL = __shfl_sync(0xffffffffu, L, j);
+        const unsigned long long jlo = __shfl_sync(0xffffffffu, lo, j);
+        const long long jms = __shfl_sync(0xffffffffu, ms, j);
+        const unsigned jel = __shfl_sync(0xffffffffu, el, j);
+        if (jel > 32)
+          for (unsigned x = lane; x < jel; x += 32)
+            dst[jlo - jel + x] = x + 1 < jel ? 255 : (uint8_t)((jL - 15) - 255ull * (jel - 1));
+        if (jL >= 32)
+          for (unsigned long long x = lane; x < jL; x += 32) dst[jlo + x] = src[jms + x];
+      }
+      o += __shfl_sync(0xffffffffu, so, 31);
+      pos += (long long)__shfl_sync(0xffffffffu, sp, 31);
     }
   }
 }
