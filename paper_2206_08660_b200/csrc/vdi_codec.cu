@@ -392,6 +392,13 @@ __device__ __forceinline__ uint32_t rd32(const uint8_t* s, long long p) {
   return sh ? __funnelshift_r(lo, __ldg(w + 1), sh) : lo;
 }
 
+// rd32 without the alignment branch, for p with p + 7 < n (both words mapped).
+__device__ __forceinline__ uint32_t rd32_inner(const uint8_t* s, long long p) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(s + p);
+  const uint32_t* w = reinterpret_cast<const uint32_t*>(a & ~(uintptr_t)3);
+  return __funnelshift_r(__ldg(w), __ldg(w + 1), (uint32_t)(a & 3) * 8);
+}
+
 // The 4-byte values at positions i + lane (lane 0..31) of one warp, in two
 // steps so the load can be issued an iteration early: each lane loads one
 // aligned word of the 36-byte window (one coalesced load), and the unaligned
@@ -479,9 +486,10 @@ __global__ void __launch_bounds__(kLz4Warps * 32) lz4_parse_kernel(const uint8_t
     unsigned nseq = 0, lead = 0;
     unsigned long long rest = 0;
     int i = (int)(cs - base), anchor = i;
-    uint32_t wl = window_load(sb, nr, i, lane);
+    // windows of the batch and of its no-match successor are loaded ahead
+    uint32_t wl = window_load(sb, nr, i, lane), w1 = window_load(sb, nr, i + 32, lane);
     while (i < mlim) {
-      const uint32_t wn = window_load(sb, nr, i + 32, lane);  // the no-match successor
+      const uint32_t w2 = window_load(sb, nr, i + 64, lane);
       const int p = i + lane;
       const bool valid = p < mlim;
       const uint32_t v = window_value(wl, (o + (i & 3)) & 3, lane);
@@ -490,7 +498,9 @@ __global__ void __launch_bounds__(kLz4Warps * 32) lz4_parse_kernel(const uint8_t
       // same-hash lanes; a lower lane's candidate is its own value
       const unsigned short t = valid ? tab[h] : kNoPos;
       const int tc = t != kNoPos ? (int)t : -1;
-      const uint32_t tv = tc >= 0 ? rd32(sb, tc) : ~v;
+      // (candidates lie >= 12 bytes before the end: both words are mapped)
+      const uint32_t tv0 = rd32_inner(sb, tc >= 0 ? tc : 0);
+      const uint32_t tv = tc >= 0 ? tv0 : ~v;
       const unsigned key = valid ? h : (0x10000u + lane);
       const unsigned peers = __match_any_sync(0xffffffffu, key);
       const unsigned lt = (1u << lane) - 1u;
@@ -510,7 +520,8 @@ __global__ void __launch_bounds__(kLz4Warps * 32) lz4_parse_kernel(const uint8_t
       __syncwarp();
       if (!mm) {
         i += 32;
-        wl = wn;
+        wl = w1;
+        w1 = w2;
         continue;
       }
       const int pw = i + w;
@@ -540,6 +551,7 @@ __global__ void __launch_bounds__(kLz4Warps * 32) lz4_parse_kernel(const uint8_t
       anchor = i;
       if (i < mlim && lane == 0) tab[lz4_hash<HL>(rd32(sb, i - 2))] = (unsigned short)(i - 2);
       wl = window_load(sb, nr, i, lane);
+      w1 = window_load(sb, nr, i + 32, lane);
       __syncwarp();
     }
     if (lane == 0)
