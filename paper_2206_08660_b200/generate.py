@@ -183,7 +183,6 @@ def launch_generate(vol_dev, voxel_type, dims, lut_dev, cam, aabb, params, resol
 
 
 _shared_ws = {}
-SHARED_WS_MAX = 24 << 30
 
 
 def shared_workspace(nbytes: int):
@@ -225,11 +224,7 @@ def generate_vdi(vol, tf, cam, params: GenParams | None = None, grid_dims=None,
     bufs = alloc_gen(width, height, params.n_sg, grid_dims, stats=with_stats)
     a = gen_args(vol_dev, vt, vol.dims, lut_dev, cam, aabb, resolved, params.n_sg,
                  params.epsilon, params.gamma_init, bufs)
-    need = int(_capi.load().vdi_gen_workspace_bytes(a))
-    # small scratch is kept for the next call; a large one (C5: half the free
-    # device memory) is only lent to this call
-    bufs.workspace = (shared_workspace(need) if need <= SHARED_WS_MAX
-                      else t.empty(need, dtype=t.uint8, device="cuda"))
+    bufs.workspace = shared_workspace(int(_capi.load().vdi_gen_workspace_bytes(a)))
     bricks = dv.volume_bricks(vol_dev, vt, vol.dims)
     cells = dv.volume_cells(vol_dev, vt, vol.dims) if dv.use_cells(vt, vol.dims) else None
     launch_generate(vol_dev, vt, vol.dims, lut_dev, cam, aabb, params, resolved, bufs,

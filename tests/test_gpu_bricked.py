@@ -19,6 +19,7 @@ if not torch.cuda.is_available():
     pytest.skip("needs a CUDA device", allow_module_level=True)
 
 import paper_2206_08660_b200 as vb  # noqa: E402
+from paper_2206_08660_b200 import generate as gen  # noqa: E402
 from paper_2206_08660_b200 import shard, synth  # noqa: E402
 
 
@@ -28,7 +29,8 @@ def _check(cfg, world, box_volume=None, max_frac=0.75):
     vdi, grid, st = vb.generate_vdi(vol, tf, gcam, params, with_stats=True)
     d = vdi.device()
     torch.cuda.synchronize()
-    torch.cuda.empty_cache()  # the ranks below allocate their own (large) workspaces
+    gen.release_workspace()  # the ranks below allocate their own (large) workspaces
+    torch.cuda.empty_cache()
     w, h = gcam.viewport
     full_bytes = int(np.prod(vol.dims)) * (1 if vol.voxel_type == "u8" else 4)
     grid_sum = torch.zeros_like(grid.device())
