@@ -185,9 +185,12 @@ __global__ void cells_kernel(const T* __restrict__ vol, void* __restrict__ out, 
 // from one aligned 32-bit word plus the next byte of each of the 4 (y, z)
 // rows, and stores them as two 16-byte writes.
 __global__ void cells_u8x4_kernel(const uint8_t* __restrict__ vol, uint4* __restrict__ out,
-                                  int nx, int ny, int nz, const CellMask<uint8_t> mask) {
-  // one (y, z) row per block iteration: 32-bit row arithmetic, no 64-bit
-  // division per thread
+                                  int nx, int ny, int nz, const uint8_t* __restrict__ bmax,
+                                  int lb, int bnx, int bny, int skip_max) {
+  // one (y, z) row per block iteration: 32-bit row arithmetic, no division
+  // per thread. A 4-cell group is skipped when its brick's maximum is <=
+  // skip_max (the u8 form of CellMask: the largest v with v / 255 <= ess_max;
+  // -1 = no mask).
   const int qx = nx >> 2;
   const int rows = ny * nz;
   for (int row = blockIdx.x; row < rows; row += gridDim.x) {
@@ -196,9 +199,11 @@ __global__ void cells_u8x4_kernel(const uint8_t* __restrict__ vol, uint4* __rest
     const long long dz = z + 1 < nz ? (long long)nx * ny : 0;
     const long long off[4] = {0, dy, dz, dy + dz};
     const long long rbase = (long long)row * nx;
+    const uint8_t* brow = bmax ? bmax + ((long long)(z >> lb) * bny + (y >> lb)) * bnx : nullptr;
     for (int q = threadIdx.x; q < qx; q += blockDim.x) {
       const int x = q * 4;
-      if (mask.skip(x, y, z)) continue;  // the 4 cells share a brick (x % 4 == 0, edge >= 4)
+      // the 4 cells share a brick (x % 4 == 0, edge >= 4)
+      if (brow && (int)__ldg(brow + (x >> lb)) <= skip_max) continue;
       const long long base = rbase + x;
       const bool last = x + 4 >= nx;
       unsigned w[4], e[4];  // rows (y,z), (y+1,z), (y,z+1), (y+1,z+1)
@@ -208,23 +213,18 @@ __global__ void cells_u8x4_kernel(const uint8_t* __restrict__ vol, uint4* __rest
         // voxel x+4 (clamped to x+3 at the row end: the last cell repeats it)
         e[r] = last ? (w[r] >> 24) : (unsigned)__ldg(vol + base + off[r] + 4);
       }
-      unsigned rec[8];  // cell j: rec[2j] = (v000 v001 v010 v011), rec[2j+1] = z+1 row pair
+      // cell j: rec[2j] = (v000 v001 v010 v011) = bytes j, j+1 of rows 0 and 1,
+      // rec[2j+1] the same of rows 2 and 3; byte 4 of a row is e[r]
+      unsigned n[4];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        // bytes j and j+1 of each row (byte 4 = e[r])
-        unsigned p[4];
-#pragma unroll
-        for (int r = 0; r < 4; ++r) {
-          const unsigned lo = (w[r] >> (8 * j)) & 0xffu;
-          const unsigned hi = j < 3 ? (w[r] >> (8 * (j + 1))) & 0xffu : e[r];
-          p[r] = lo | (hi << 8);
-        }
-        rec[2 * j] = p[0] | (p[1] << 16);
-        rec[2 * j + 1] = p[2] | (p[3] << 16);
-      }
+      for (int r = 0; r < 4; ++r) n[r] = __funnelshift_r(w[r], e[r], 8);  // bytes 1..4
+      const uint4 o0 = make_uint4(__byte_perm(w[0], w[1], 0x5410), __byte_perm(w[2], w[3], 0x5410),
+                                  __byte_perm(w[0], w[1], 0x6521), __byte_perm(w[2], w[3], 0x6521));
+      const uint4 o1 = make_uint4(__byte_perm(w[0], w[1], 0x7632), __byte_perm(w[2], w[3], 0x7632),
+                                  __byte_perm(n[0], n[1], 0x7632), __byte_perm(n[2], n[3], 0x7632));
       uint4* o = out + 2 * (base >> 2);
-      o[0] = make_uint4(rec[0], rec[1], rec[2], rec[3]);
-      o[1] = make_uint4(rec[4], rec[5], rec[6], rec[7]);
+      o[0] = o0;
+      o[1] = o1;
     }
   }
 }
@@ -247,11 +247,18 @@ int volume_cells(const void* volume, int voxel_type, int nx, int ny, int nz, voi
   if (blocks > (long long)sms * 64) blocks = (long long)sms * 64;
   switch (voxel_type) {
     case VDI_VOXEL_U8:
-      if (nx % 4 == 0)
+      if (nx % 4 == 0) {
+        // the largest u8 value the samplers classify as always transparent
+        int skip_max = -1;
+        if (masked)
+          for (int v = 0; v < 256; ++v)
+            if ((double)((float)v / 255.0f) <= ess_max) skip_max = v;
         cells_u8x4_kernel<<<(unsigned)std::min<long long>((long long)ny * nz, (long long)sms * 32),
                             256, 0, stream>>>(
             static_cast<const uint8_t*>(volume), static_cast<uint4*>(out), nx, ny, nz,
-            mk((uint8_t*)nullptr));
+            masked ? static_cast<const uint8_t*>(brick_max) : nullptr, brick_log2, bnx, bny,
+            skip_max);
+      }
       else
         cells_kernel<<<(unsigned)blocks, 256, 0, stream>>>(static_cast<const uint8_t*>(volume),
                                                            out, nx, ny, nz, mk((uint8_t*)nullptr));
