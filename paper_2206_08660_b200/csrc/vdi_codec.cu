@@ -350,7 +350,7 @@ constexpr int kLz4Chunk = 32768;
 constexpr int kLz4HashLog = 12;  // default table: 4 Ki entries per warp
 constexpr int kLz4MaxSeq = kLz4Chunk / 4 + 1;
 constexpr int kLz4Warps = 4;
-constexpr int kLz4Warm = 16384;  // bytes of the previous chunk hashed into a chunk's table
+constexpr int kLz4Warm = 8192;   // bytes of the previous chunk hashed into a chunk's table
 constexpr unsigned short kNoPos = 0xffffu;
 
 struct ChunkSum {
@@ -447,8 +447,8 @@ __global__ void __launch_bounds__(kLz4Warps * 32) lz4_parse_kernel(const uint8_t
     // stay < 65536; the decoder has those bytes). The table is warmed with
     // every position of the previous chunk's last kLz4Warm bytes (the last
     // writer of a hash wins, as in a serial pass): with 4 Ki slots, a slot
-    // whose last writer lies further back survives 16 Ki later positions
-    // with probability e^-4, so the older half adds almost nothing.
+    // whose last writer lies further back survives 8 Ki later positions with
+    // probability e^-2, and such old candidates rarely match (C3: +0.01 %).
     const long long tb = cs - kLz4Chunk;
     {
       for (int k = lane; k < (1 << HL); k += 32) tab[k] = kNoPos;
