@@ -291,8 +291,8 @@ int vdi_decode_vdi1_lists(const uint8_t* src, int32_t width, int32_t rows, int32
                           int32_t* counts, float* segs, void* workspace, size_t workspace_bytes,
                           vdi_stream_t stream);
 
-/* LZ4 block compression of src[0, n) with n = *n_dev when n_dev is not NULL
- * (a device length, e.g. VdiEncodeArgs.out_len), else n = n_max. dst holds
+/* LZ4 block compression of src[0, n) with n = min(*n_dev, n_max) when n_dev
+ * is not NULL (a device length, e.g. VdiEncodeArgs.out_len), else n = n_max. dst holds
  * vdi_lz4_max_bytes(n_max); *out_len (device) receives the block length. */
 size_t vdi_lz4_max_bytes(size_t n);
 size_t vdi_lz4_workspace_bytes(size_t n_max);

@@ -36,10 +36,10 @@
 
 namespace vdi {
 
-// p[0] = *src (or v0 when src is null), p[1] = v1 unless v1 == ~0.
+// p[0] = min(*src, v0) (or v0 when src is null), p[1] = v1 unless v1 == ~0.
 __global__ void set_u64_kernel(unsigned long long* p, const unsigned long long* src,
                                unsigned long long v0, unsigned long long v1) {
-  p[0] = src ? *src : v0;
+  p[0] = src && *src < v0 ? *src : v0;
   if (v1 != ~0ull) p[1] = v1;
 }
 

@@ -100,6 +100,19 @@ def test_lz4_unaligned_source(shift):
     _check_block(dv.to_host(dst[:m]).tobytes(), raw)
 
 
+def test_lz4_device_length_clamped_to_capacity():
+    """A device length above n_max compresses the first n_max bytes (the
+    workspace and dst are sized for n_max; include/vdi_b200.h)."""
+    rng = np.random.default_rng(5)
+    raw = (rng.integers(0, 4, 70000, dtype=np.uint8) * 17).tobytes()
+    n_max = 65536 + 77
+    src = dv.to_device(np.frombuffer(raw, dtype=np.uint8))
+    n_dev = torch.tensor([len(raw) + 12345], dtype=torch.int64, device="cuda")
+    dst, out_len = codec.compress_device(src, n_max, n_dev)
+    m = int(dv.to_host(out_len)[0])
+    _check_block(dv.to_host(dst[:m]).tobytes(), raw[:n_max])
+
+
 def test_lz4_ratio_close_to_reference():
     """Chunk-parallel parsing loses little against the serial parse."""
     g = gio.load("codec")
