@@ -62,7 +62,7 @@
 extern "C" {
 #endif
 
-#define VDI_ABI_VERSION 2
+#define VDI_ABI_VERSION 3
 
 #define VDI_OK 0
 #define VDI_EINVAL (-1)
@@ -172,6 +172,11 @@ typedef struct VdiRenderArgs {
   int32_t use_ess;
   int32_t vdi_band_rows, vdi_band_world, vdi_rows_per_rank;
   int32_t band_rows, band_stride, band_offset;  /* output-row sharding */
+  /* optional (may be NULL): occupancy bitmap of 8x8-list tiles
+   * (vdi_list_tiles). A step of the DDA into a list of an empty tile is
+   * counted as a visit without reading the list's count (it is 0), so the
+   * image and every counter are unchanged. */
+  const uint32_t* list_tiles;
 } VdiRenderArgs;
 
 /* Ground-truth direct volume rendering (dvr.py:21-89): the generation ray,
@@ -269,6 +274,14 @@ size_t vdi_gen_workspace_min_bytes(const VdiGenArgs* args);
 int vdi_gen_launch(const VdiGenArgs* args, vdi_stream_t stream);
 int vdi_grid_launch(const VdiGridArgs* args, vdi_stream_t stream);
 int vdi_render_launch(const VdiRenderArgs* args, vdi_stream_t stream);
+
+/* Occupancy of 8x8-list tiles of a (band-sharded) VDI: bit t of the bitmap
+ * (tiles row-major, ceil(vdi_w/8) per row) is set iff a list of tile t has
+ * count > 0. Reads args->counts, vdi_w, vdi_h and the vdi_band_* fields;
+ * writes vdi_list_tiles_words(vdi_w, vdi_h) words to tiles. An accelerator
+ * for vdi_render_launch (VdiRenderArgs.list_tiles), SURVEY 8(f) rank 4. */
+size_t vdi_list_tiles_words(int32_t vdi_w, int32_t vdi_h);
+int vdi_list_tiles(const VdiRenderArgs* args, uint32_t* tiles, vdi_stream_t stream);
 int vdi_dvr_launch(const VdiDvrArgs* args, vdi_stream_t stream);
 int vdi_preview_launch(const VdiPreviewArgs* args, vdi_stream_t stream);
 /* (h, w, channels) f64 -> (out_h, out_w, channels), preview.py:208-223

@@ -53,6 +53,7 @@ class VdiRenderArgs(ctypes.Structure):
         ("out_w", _I), ("out_h", _I), ("use_ess", _I),
         ("vdi_band_rows", _I), ("vdi_band_world", _I), ("vdi_rows_per_rank", _I),
         ("band_rows", _I), ("band_stride", _I), ("band_offset", _I),
+        ("list_tiles", _P),
     ]
 
 
@@ -115,7 +116,8 @@ EXPORTS = ["vdi_last_error", "vdi_abi_version", "vdi_gen_workspace_bytes",
            "vdi_gen_rays", "vdi_composite_lists", "vdi_dda_cells", "vdi_project_rays",
            "vdi_decode_vdi1_lists", "vdi_find_first_batch",
            "vdi_volume_brick_max", "vdi_selftest_arith", "vdi_segs_to_aos",
-           "vdi_segs_from_aos", "vdi_volume_cells_bytes", "vdi_volume_cells", "vdi_volume_cells_masked"]
+           "vdi_segs_from_aos", "vdi_volume_cells_bytes", "vdi_volume_cells", "vdi_volume_cells_masked",
+           "vdi_list_tiles_words", "vdi_list_tiles"]
 
 _lib = None
 
@@ -173,15 +175,19 @@ def load():
     L.vdi_volume_cells_masked.restype = ctypes.c_int
     L.vdi_selftest_arith.argtypes = [ctypes.c_int64, ctypes.c_uint64, _P, _P]
     L.vdi_selftest_arith.restype = ctypes.c_int
+    L.vdi_list_tiles.argtypes = [ctypes.POINTER(VdiRenderArgs), _P, _P]
+    L.vdi_list_tiles_words.argtypes = [_I, _I]
+    L.vdi_list_tiles_words.restype = ctypes.c_size_t
     L.vdi_segs_to_aos.argtypes = [_P, _P, ctypes.c_int64, _I, _P]
     L.vdi_segs_from_aos.argtypes = [_P, _P, ctypes.c_int64, _I, _P]
     for name in ("vdi_gen_launch", "vdi_grid_launch", "vdi_render_launch", "vdi_dvr_launch",
                  "vdi_preview_launch", "vdi_bilinear_upsample", "vdi_encode_vdi1",
                  "vdi_decode_vdi1_lists", "vdi_lz4_compress", "vdi_validate", "vdi_synth_rm_u8",
                  "vdi_gen_rays", "vdi_composite_lists", "vdi_dda_cells", "vdi_project_rays",
-                 "vdi_find_first_batch", "vdi_segs_to_aos", "vdi_segs_from_aos"):
+                 "vdi_find_first_batch", "vdi_segs_to_aos", "vdi_segs_from_aos",
+                 "vdi_list_tiles"):
         getattr(L, name).restype = ctypes.c_int
-    if L.vdi_abi_version() != 2:
+    if L.vdi_abi_version() != 3:
         raise VdiError("libvdi_b200.so ABI mismatch")
     _lib = L
     return L

@@ -77,6 +77,17 @@ int vdi_render_launch(const VdiRenderArgs* a, vdi_stream_t stream) {
   return vdi::render_launch(a, static_cast<cudaStream_t>(stream));
 }
 
+size_t vdi_list_tiles_words(int32_t vdi_w, int32_t vdi_h) {
+  return vdi::list_tiles_words(vdi_w, vdi_h);
+}
+
+int vdi_list_tiles(const VdiRenderArgs* a, uint32_t* tiles, vdi_stream_t stream) {
+  if (!a) return set_error(VDI_EINVAL, "null args");
+  if (!a->counts || !tiles) return set_error(VDI_EINVAL, "null device pointer");
+  if (a->vdi_w < 1 || a->vdi_h < 1) return set_error(VDI_EINVAL, "bad sizes");
+  return vdi::list_tiles(a, tiles, static_cast<cudaStream_t>(stream));
+}
+
 int vdi_dvr_launch(const VdiDvrArgs* a, vdi_stream_t stream) {
   if (!a) return set_error(VDI_EINVAL, "null args");
   if (!a->volume || !a->lut || !a->image || !a->workspace)

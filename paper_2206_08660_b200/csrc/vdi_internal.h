@@ -24,6 +24,8 @@ int gen_launch(const VdiGenArgs* a, cudaStream_t stream);
 size_t gen_workspace_bytes(const VdiGenArgs* a, int recommended);
 int grid_launch(const VdiGridArgs* a, cudaStream_t stream);
 int render_launch(const VdiRenderArgs* a, cudaStream_t stream);
+size_t list_tiles_words(int vdi_w, int vdi_h);
+int list_tiles(const VdiRenderArgs* args, uint32_t* tiles, cudaStream_t stream);
 int dvr_launch(const VdiDvrArgs* a, cudaStream_t stream);
 int gen_rays(const VdiGenArgs* a, const double* rays, const double* gammas_in, long long n,
              int mode, cudaStream_t stream);

@@ -31,10 +31,22 @@ struct RenderConst {
   int tiles_x;
   int local_h;
   long long n_slots;
+  int lt_words;  // words of the list-tile bitmap staged in shared memory (0: none)
+  int lt_wpr;    // its words per tile row
 };
+
+// List-tile occupancy (vdi_list_tiles): 8x8 lists per tile, one bitmap word
+// per 32 horizontally adjacent tiles, rows padded to whole words.
+constexpr int kListTile = 8;
+__host__ __device__ inline int lt_words_per_row(int vdi_w) {
+  return ((vdi_w + kListTile - 1) / kListTile + 31) / 32;
+}
 
 __global__ void __launch_bounds__(kRenderThreads, VDI_RENDER_MINB) render_kernel(const RenderConst c) {
   const VdiRenderArgs& a = c.a;
+  extern __shared__ uint32_t s_tiles[];
+  for (int k = threadIdx.x; k < c.lt_words; k += blockDim.x) s_tiles[k] = __ldg(a.list_tiles + k);
+  __syncthreads();
   const long long slot = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   unsigned long long st_vis = 0, st_int = 0, st_srch = 0;
   if (slot < c.n_slots) {
@@ -97,7 +109,12 @@ __global__ void __launch_bounds__(kRenderThreads, VDI_RENDER_MINB) render_kernel
           const long long lidx =
               (long long)vdi_storage_row(cy, a.vdi_band_rows, a.vdi_band_world,
                                          a.vdi_rows_per_rank) * vdi_w + cx;
-          const int count = __ldg(a.counts + lidx);
+          // a list of an empty tile has count 0: no load (SURVEY 8(f) rank 4,
+          // empty-list skipping with exact lists_visited accounting)
+          int count = 0;
+          if (c.lt_words == 0 ||
+              ((s_tiles[(cy >> 3) * c.lt_wpr + (cx >> 8)] >> ((cx >> 3) & 31)) & 1u))
+            count = __ldg(a.counts + lidx);
           bool search = count > 0;
           if (search && a.use_ess) {
             const double x_a = a0x + s_cur * cdx, y_a = a0y + s_cur * cdy;
@@ -241,10 +258,67 @@ int render_launch(const VdiRenderArgs* args, cudaStream_t stream) {
   c.n_slots = (long long)c.tiles_x * tiles_y * 32;
   if (c.n_slots == 0) return VDI_OK;
   const long long blocks = (c.n_slots + kRenderThreads - 1) / kRenderThreads;
-  render_kernel<<<(unsigned)blocks, kRenderThreads, 0, stream>>>(c);
+  c.lt_wpr = lt_words_per_row(c.a.vdi_w);
+  const long long ltw = (long long)c.lt_wpr * ((c.a.vdi_h + kListTile - 1) / kListTile);
+  // staged when it fits next to the 6 resident blocks' registers (<= 32 KiB)
+  c.lt_words = c.a.list_tiles && ltw <= 8192 ? (int)ltw : 0;
+  const size_t smem = sizeof(uint32_t) * (size_t)c.lt_words;
+  if (smem > 0) {
+    const cudaError_t e = cudaFuncSetAttribute(render_kernel,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               (int)smem);
+    if (e != cudaSuccess) return set_error(VDI_ELAUNCH, "render smem: %s", cudaGetErrorString(e));
+  }
+  render_kernel<<<(unsigned)blocks, kRenderThreads, smem, stream>>>(c);
   const cudaError_t err = cudaGetLastError();
   if (err != cudaSuccess)
     return set_error(VDI_ELAUNCH, "render launch: %s", cudaGetErrorString(err));
+  return VDI_OK;
+}
+
+// vdi_list_tiles: lane j of a warp owns tile (ty, 32 w + j) and scans its
+// 8x8 counts (eight 32-byte row pieces per lane, contiguous across the warp);
+// the warp's ballot is one bitmap word.
+__global__ void list_tiles_kernel(const VdiRenderArgs a, uint32_t* __restrict__ tiles, int wpr,
+                                  int n_words) {
+  const int lane = threadIdx.x & 31;
+  const int word = (int)(((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  if (word >= n_words) return;  // warp-uniform
+  const int ty = word / wpr, txi = (word - ty * wpr) * 32 + lane;
+  const int x0 = txi * kListTile;
+  bool any = false;
+  if (x0 < a.vdi_w) {
+    const int x1 = min(x0 + kListTile, a.vdi_w);
+    const int y1 = min((ty + 1) * kListTile, a.vdi_h);
+    for (int y = ty * kListTile; y < y1 && !any; ++y) {
+      const int32_t* row = a.counts + (long long)vdi_storage_row(y, a.vdi_band_rows,
+                                                                   a.vdi_band_world,
+                                                                   a.vdi_rows_per_rank) *
+                                          a.vdi_w;
+      for (int x = x0; x < x1; ++x) any |= __ldg(row + x) > 0;
+    }
+  }
+  const unsigned b = __ballot_sync(0xffffffffu, any);
+  if (lane == 0) tiles[word] = b;
+}
+
+size_t list_tiles_words(int vdi_w, int vdi_h) {
+  if (vdi_w < 1 || vdi_h < 1) return 0;
+  return (size_t)lt_words_per_row(vdi_w) * (size_t)((vdi_h + kListTile - 1) / kListTile);
+}
+
+int list_tiles(const VdiRenderArgs* args, uint32_t* tiles, cudaStream_t stream) {
+  VdiRenderArgs a = *args;
+  if (a.vdi_band_rows <= 0) a.vdi_band_rows = 16;
+  if (a.vdi_band_world <= 0) a.vdi_band_world = 1;
+  const long long words = (long long)list_tiles_words(a.vdi_w, a.vdi_h);
+  if (words == 0) return VDI_OK;
+  const long long blocks = (words * 32 + 127) / 128;
+  list_tiles_kernel<<<(unsigned)blocks, 128, 0, stream>>>(a, tiles, lt_words_per_row(a.vdi_w),
+                                                         (int)words);
+  const cudaError_t err = cudaGetLastError();
+  if (err != cudaSuccess)
+    return set_error(VDI_ELAUNCH, "list_tiles launch: %s", cudaGetErrorString(err));
   return VDI_OK;
 }
 

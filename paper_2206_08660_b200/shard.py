@@ -24,7 +24,8 @@ import numpy as np
 from . import _capi
 from . import device as dv
 from .generate import alloc_gen, launch_generate
-from .raycast import RenderOptions, render_args
+from .raycast import (RenderOptions, alloc_list_tiles, launch_list_tiles, render_args,
+                      use_list_tiles)
 from .vdi import AccelGrid, DeviceVdi, Vdi, default_grid_dims
 
 BAND_ROWS = 16
@@ -260,7 +261,9 @@ class Pipeline:
         # brick maxima (+ corner records); vdi_gen_launch = fill_inv + 3 rounds
         # x (sample, fill, bisect, emit) + fused fallback; then
         # vdi_grid_launch and vdi_render_launch
-        self.launches_per_step = (1 + (self.cells is not None) + 1 + 3 * 4 + 1 + 1 + 1)
+        self.tiles = (alloc_list_tiles(w, h) if use_list_tiles() else None)
+        self.launches_per_step = (1 + (self.cells is not None) + 1 + 3 * 4 + 1 + 1
+                                  + (self.tiles is not None) + 1)
         if world > 1:
             import torch.distributed as tdist
             self.dist = tdist
@@ -309,6 +312,8 @@ class Pipeline:
                              self.g_counts, self.g_segs)
         if timed:
             ev[4].record()
+        if self.tiles is not None:
+            launch_list_tiles(self._rargs, self.tiles)
         _capi.check(L.vdi_render_launch(self._rargs, dv.stream_handle()))
         if timed:
             ev[5].record()

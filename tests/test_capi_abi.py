@@ -46,8 +46,18 @@ def test_exports_every_declared_symbol(lib):
         assert hasattr(lib, name)
 
 
+def test_every_entry_point_has_a_prototype(lib):
+    """ctypes passes arguments by its declared prototype: an entry point with
+    parameters but no argtypes would pass a struct by value (a crash)."""
+    no_params = {"vdi_last_error", "vdi_abi_version"}
+    for name in _capi.EXPORTS:
+        if name in no_params:
+            continue
+        assert getattr(lib, name).argtypes, name
+
+
 def test_abi_version(lib):
-    assert lib.vdi_abi_version() == 2
+    assert lib.vdi_abi_version() == 3
 
 
 PROBE = r"""

@@ -1,0 +1,62 @@
+"""Empty-list skipping in the render DDA: the
+8x8-list tile bitmap (vdi_list_tiles) lets the render step through lists of
+empty tiles without reading their counts. The image and every per-pixel
+counter (lists visited / searched, supersegments intersected) must equal
+the render without the bitmap bit for bit, and the bitmap must equal the
+tile occupancy of the counts.
+"""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2206_08660_b200 as vb  # noqa: E402
+from paper_2206_08660_b200 import _capi, synth  # noqa: E402
+from paper_2206_08660_b200 import device as dv  # noqa: E402
+from paper_2206_08660_b200.raycast import (alloc_list_tiles, launch_list_tiles,  # noqa: E402
+                                           render_args)
+
+
+def _tiles_ref(counts):
+    h, w = counts.shape
+    ty, tx = -(-h // 8), -(-w // 8)
+    wpr = -(-tx // 32)
+    occ = np.zeros((ty, wpr * 32), bool)
+    for y in range(ty):
+        for x in range(tx):
+            occ[y, x] = (counts[8 * y:8 * y + 8, 8 * x:8 * x + 8] > 0).any()
+    bits = occ.reshape(ty, wpr, 32).astype(np.uint64) << np.arange(32, dtype=np.uint64)
+    return bits.sum(axis=2).astype(np.uint32).reshape(-1)
+
+
+@pytest.mark.parametrize("cfg,angle", [("C2", 15.0), ("C2", 40.0), ("C3", 15.0)])
+def test_tiles_exact(cfg, angle):
+    vol, tf, gcam, rcam, n_sg = synth.config(cfg)
+    rcam = synth.sweep_camera(vol, angle, gcam.viewport, synth.CONFIGS[cfg][4])
+    vdi, grid = vb.generate_vdi(vol, tf, gcam, vb.GenParams(n_sg=n_sg))
+    d = vdi.device()
+    ow, oh = rcam.viewport
+    L = _capi.load()
+    outs = []
+    for use in (False, True):
+        image = torch.empty((oh, ow, 4), dtype=torch.float64, device="cuda")
+        pp = [torch.empty((oh, ow), dtype=torch.int32, device="cuda") for _ in range(3)]
+        a = render_args(d, n_sg, vdi.width, vdi.height, gcam, vdi.volume_aabb, grid.device(),
+                        grid.dims, grid.near, grid.far, rcam, vb.RenderOptions(), image,
+                        per_pixel=pp)
+        if use:
+            tiles = alloc_list_tiles(vdi.width, vdi.height)
+            launch_list_tiles(a, tiles)
+            got = tiles.cpu().numpy().view(np.uint32)
+            np.testing.assert_array_equal(got, _tiles_ref(d.counts.cpu().numpy()))
+        _capi.check(L.vdi_render_launch(a, dv.stream_handle()))
+        torch.cuda.synchronize()
+        outs.append([image.cpu().numpy()] + [x.cpu().numpy() for x in pp])
+    for x, y in zip(outs[0], outs[1]):
+        np.testing.assert_array_equal(x, y)
+    assert outs[0][1].sum() > 0
