@@ -113,3 +113,16 @@ def test_size_queries_are_64_bit(lib):
         160 + 2 * 3840 * 2160 + 24 * 3840 * 2160 * 40 + 4 * 240 * 135 * 32)
     assert L.vdi_lz4_max_bytes(2 ** 33) == 2 ** 33 + 2 ** 33 // 255 + 16
     assert L.vdi_volume_cells_bytes(0, 2048, 2048, 1920) == 8 * 2048 * 2048 * 1920
+
+
+def test_integration_stub_matches_binding():
+    """The ctypes stub INTEGRATION.md hands a maintainer has the binding's
+    VdiGenArgs layout (a stale copy would pass misaligned arguments)."""
+    text = open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                             "INTEGRATION.md")).read()
+    code = text[text.index("import ctypes\n"):text.index('lib = ctypes.CDLL("libvdi_b200.so")')]
+    ns = {}
+    exec(code, ns)
+    stub = ns["VdiGenArgs"]
+    assert [f[0] for f in stub._fields_] == [f[0] for f in _capi.VdiGenArgs._fields_]
+    assert ctypes.sizeof(stub) == ctypes.sizeof(_capi.VdiGenArgs)
