@@ -56,6 +56,14 @@ constexpr int kGenThreads = 128;
 #ifndef VDI_SAMPLE_MINB
 #define VDI_SAMPLE_MINB 5  // 96 registers: 5 blocks/SM (measured: 9.59 -> 9.14 ms at C3)
 #endif
+#ifndef VDI_FILL_MINB
+#define VDI_FILL_MINB 10  // 48 registers, 10 blocks/SM (C3 gen -0.2 ms; 0 = no minimum: 64 registers)
+#endif
+#if VDI_FILL_MINB > 0
+#define VDI_FILL_BOUNDS __launch_bounds__(kGenThreads, VDI_FILL_MINB)
+#else
+#define VDI_FILL_BOUNDS __launch_bounds__(kGenThreads)
+#endif
 #ifndef VDI_EMIT_MINB
 #define VDI_EMIT_MINB 6  // 80 registers: 6 blocks/SM (measured: 6.16 -> 5.64 ms at C3)
 #endif
@@ -583,7 +591,7 @@ __global__ void __launch_bounds__(kGenThreads, VDI_SAMPLE_MINB) gen_sample_kerne
 // of r) exactly as the lane-per-ray fill did. Sets rec->nsteps to the number
 // of samples stored (the tb <= ta break, generate.py:113-117, stops earlier).
 template <int VT>
-__global__ void __launch_bounds__(kGenThreads) gen_fill_kernel(const GenConst c) {
+__global__ void VDI_FILL_BOUNDS gen_fill_kernel(const GenConst c) {
   extern __shared__ double4 s_lut[];
   __shared__ double s_u8[256];
   load_lut(c, s_lut, s_u8);
