@@ -57,7 +57,7 @@ constexpr int kGenThreads = 128;
 #define VDI_SAMPLE_MINB 5  // 96 registers: 5 blocks/SM (measured: 9.59 -> 9.14 ms at C3)
 #endif
 #ifndef VDI_FILL_MINB
-#define VDI_FILL_MINB 10  // 48 registers, 10 blocks/SM (C3 gen -0.2 ms; 0 = no minimum: 64 registers)
+#define VDI_FILL_MINB 0  // no minimum (64 registers): 10 blocks/SM gave C3 -0.2 ms but C4 / C5 +4 ms
 #endif
 #if VDI_FILL_MINB > 0
 #define VDI_FILL_BOUNDS __launch_bounds__(kGenThreads, VDI_FILL_MINB)

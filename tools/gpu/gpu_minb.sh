@@ -5,6 +5,6 @@ for v in $2; do
   grep -A1 "gen_fill_kernelILi16" gpurun_out/build_$v.log | grep -o "Used [0-9]* registers\|[0-9]* bytes spill stores" | head -2 | tr '\n' ' '
   timeout 600 python -m pytest tests/test_gpu_parity.py -q -k "generate" --timeout 500 > gpurun_out/ab_$v.log 2>&1
   echo "$1=$v tests: $(tail -1 gpurun_out/ab_$v.log)"
-  timeout 300 python tools/run_pipeline.py --config C3 --reps 3 2>&1 | grep step | tail -1
+  for c in ${CFGS:-C3}; do echo "$c $(timeout 600 python tools/run_pipeline.py --config $c --reps 3 2>&1 | grep step | tail -1)"; done
 done
 python -m paper_2206_08660_b200.build > /dev/null 2>&1
