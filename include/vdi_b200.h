@@ -62,7 +62,7 @@
 extern "C" {
 #endif
 
-#define VDI_ABI_VERSION 3
+#define VDI_ABI_VERSION 4
 
 #define VDI_OK 0
 #define VDI_EINVAL (-1)
@@ -177,6 +177,12 @@ typedef struct VdiRenderArgs {
    * counted as a visit without reading the list's count (it is 0), so the
    * image and every counter are unchanged. */
   const uint32_t* list_tiles;
+  /* optional (may be NULL; ignored when gz > 64): vdi_grid_zmask() of
+   * `grid`, one 64-bit word per grid column (cgy, cgx) whose bit cz is set
+   * iff grid[cz][cgy][cgx] > 0. The ESS test (raycast.py:352-372) then ORs
+   * the words of its column range and tests its slab range in one compare
+   * instead of reading every cell; the result is the same. */
+  const uint64_t* grid_zmask;
 } VdiRenderArgs;
 
 /* Ground-truth direct volume rendering (dvr.py:21-89): the generation ray,
@@ -282,6 +288,11 @@ int vdi_render_launch(const VdiRenderArgs* args, vdi_stream_t stream);
  * for vdi_render_launch (VdiRenderArgs.list_tiles), SURVEY 8(f) rank 4. */
 size_t vdi_list_tiles_words(int32_t vdi_w, int32_t vdi_h);
 int vdi_list_tiles(const VdiRenderArgs* args, uint32_t* tiles, vdi_stream_t stream);
+/* Per-column slab occupancy of an AccelGrid (gz, gy, gx) u32, gz <= 64:
+ * out[cgy * gx + cgx] bit cz = grid[cz][cgy][cgx] > 0 (gx * gy words). An
+ * accelerator for vdi_render_launch (VdiRenderArgs.grid_zmask). */
+int vdi_grid_zmask(const uint32_t* grid, int32_t gx, int32_t gy, int32_t gz, uint64_t* out,
+                   vdi_stream_t stream);
 int vdi_dvr_launch(const VdiDvrArgs* args, vdi_stream_t stream);
 int vdi_preview_launch(const VdiPreviewArgs* args, vdi_stream_t stream);
 /* (h, w, channels) f64 -> (out_h, out_w, channels), preview.py:208-223

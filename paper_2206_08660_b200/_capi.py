@@ -53,7 +53,7 @@ class VdiRenderArgs(ctypes.Structure):
         ("out_w", _I), ("out_h", _I), ("use_ess", _I),
         ("vdi_band_rows", _I), ("vdi_band_world", _I), ("vdi_rows_per_rank", _I),
         ("band_rows", _I), ("band_stride", _I), ("band_offset", _I),
-        ("list_tiles", _P),
+        ("list_tiles", _P), ("grid_zmask", _P),
     ]
 
 
@@ -117,7 +117,7 @@ EXPORTS = ["vdi_last_error", "vdi_abi_version", "vdi_gen_workspace_bytes",
            "vdi_decode_vdi1_lists", "vdi_find_first_batch",
            "vdi_volume_brick_max", "vdi_selftest_arith", "vdi_segs_to_aos",
            "vdi_segs_from_aos", "vdi_volume_cells_bytes", "vdi_volume_cells", "vdi_volume_cells_masked",
-           "vdi_list_tiles_words", "vdi_list_tiles"]
+           "vdi_list_tiles_words", "vdi_list_tiles", "vdi_grid_zmask"]
 
 _lib = None
 
@@ -178,6 +178,7 @@ def load():
     L.vdi_list_tiles.argtypes = [ctypes.POINTER(VdiRenderArgs), _P, _P]
     L.vdi_list_tiles_words.argtypes = [_I, _I]
     L.vdi_list_tiles_words.restype = ctypes.c_size_t
+    L.vdi_grid_zmask.argtypes = [_P, _I, _I, _I, _P, _P]
     L.vdi_segs_to_aos.argtypes = [_P, _P, ctypes.c_int64, _I, _P]
     L.vdi_segs_from_aos.argtypes = [_P, _P, ctypes.c_int64, _I, _P]
     for name in ("vdi_gen_launch", "vdi_grid_launch", "vdi_render_launch", "vdi_dvr_launch",
@@ -185,9 +186,9 @@ def load():
                  "vdi_decode_vdi1_lists", "vdi_lz4_compress", "vdi_validate", "vdi_synth_rm_u8",
                  "vdi_gen_rays", "vdi_composite_lists", "vdi_dda_cells", "vdi_project_rays",
                  "vdi_find_first_batch", "vdi_segs_to_aos", "vdi_segs_from_aos",
-                 "vdi_list_tiles"):
+                 "vdi_list_tiles", "vdi_grid_zmask"):
         getattr(L, name).restype = ctypes.c_int
-    if L.vdi_abi_version() != 3:
+    if L.vdi_abi_version() != 4:
         raise VdiError("libvdi_b200.so ABI mismatch")
     _lib = L
     return L

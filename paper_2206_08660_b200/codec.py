@@ -137,7 +137,7 @@ def decode_vdi(data: bytes):
     lists are unpacked on the device (vdi_decode_vdi1_lists) and validated
     there (validate_vdi, InvariantViolation) as the reference does."""
     from .camera import Camera
-    from .vdi import AccelGrid, DeviceVdi, Vdi, validate_vdi
+    from .vdi import AccelGrid, DeviceVdi, InvariantViolation, Vdi, validate_vdi
     t = dv.require_cuda()
     L = _capi.load()
     b = memoryview(data)
@@ -169,6 +169,11 @@ def decode_vdi(data: bytes):
         raise TruncatedStream(f"need {end} bytes, have {len(b)}")
     if len(b) > end:
         raise TruncatedStream(f"{len(b) - end} trailing bytes")
+    over = np.flatnonzero(counts_u16 > n_sg)
+    if over.size:  # vdi.py:199-201: the first such list in row-major order
+        ly, lx = divmod(int(over[0]), width)
+        raise InvariantViolation(f"list ({lx},{ly}) count {int(counts_u16[over[0]])} "
+                                 f"> n_sg {n_sg}")
     cam = Camera(position=camvals[0:3], orientation=camvals[3:7], fov_y=camvals[7],
                  near=camvals[8], far=camvals[9], viewport=(width, height))
     aabb = np.array(aabbvals, dtype=np.float64).reshape(2, 3)

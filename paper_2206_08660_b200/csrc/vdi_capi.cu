@@ -88,6 +88,13 @@ int vdi_list_tiles(const VdiRenderArgs* a, uint32_t* tiles, vdi_stream_t stream)
   return vdi::list_tiles(a, tiles, static_cast<cudaStream_t>(stream));
 }
 
+int vdi_grid_zmask(const uint32_t* grid, int32_t gx, int32_t gy, int32_t gz, uint64_t* out,
+                   vdi_stream_t stream) {
+  if (!grid || !out) return set_error(VDI_EINVAL, "null device pointer");
+  if (gx < 1 || gy < 1 || gz < 1 || gz > 64) return set_error(VDI_EINVAL, "bad grid dims");
+  return vdi::grid_zmask(grid, gx, gy, gz, out, static_cast<cudaStream_t>(stream));
+}
+
 int vdi_dvr_launch(const VdiDvrArgs* a, vdi_stream_t stream) {
   if (!a) return set_error(VDI_EINVAL, "null args");
   if (!a->volume || !a->lut || !a->image || !a->workspace)

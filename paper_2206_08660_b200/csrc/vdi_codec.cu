@@ -852,19 +852,13 @@ int lz4_compress(const uint8_t* src, size_t n_max, const unsigned long long* n_d
   if (nch > 0) {
     long long b = (nch + kLz4Warps - 1) / kLz4Warps;
     if (b > (long long)sms * 16) b = (long long)sms * 16;
-    // VDI_LZ4_HASHLOG (11, 12 or 13) selects the table size: tuning experiments only
-    const char* hl_env = getenv("VDI_LZ4_HASHLOG");
-    const int hl_req = hl_env ? atoi(hl_env) : kLz4HashLog;
-    const int hl = hl_req >= 11 && hl_req <= 13 ? hl_req : kLz4HashLog;
-    const size_t smem = sizeof(unsigned short) * kLz4Warps * ((size_t)1 << hl);
-    const void* fn = hl == 11 ? (const void*)lz4_parse_kernel<11>
-                     : hl == 12 ? (const void*)lz4_parse_kernel<12>
-                                : (const void*)lz4_parse_kernel<13>;
-    err = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    // 4 K-entry tables, 24 warps/SM (2 K: faster, larger blocks; 8 K: the
+    // reverse; measured in profiles/r01_bench_codec.jsonl)
+    const size_t smem = sizeof(unsigned short) * kLz4Warps * ((size_t)1 << kLz4HashLog);
+    err = cudaFuncSetAttribute(lz4_parse_kernel<kLz4HashLog>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (err != cudaSuccess) return set_error(VDI_ELAUNCH, "lz4 smem: %s", cudaGetErrorString(err));
-    if (hl == 11) lz4_parse_kernel<11><<<(unsigned)b, kLz4Warps * 32, smem, stream>>>(src, ws, nch);
-    else if (hl == 12) lz4_parse_kernel<12><<<(unsigned)b, kLz4Warps * 32, smem, stream>>>(src, ws, nch);
-    else lz4_parse_kernel<13><<<(unsigned)b, kLz4Warps * 32, smem, stream>>>(src, ws, nch);
+    lz4_parse_kernel<kLz4HashLog><<<(unsigned)b, kLz4Warps * 32, smem, stream>>>(src, ws, nch);
   }
   lz4_scan_kernel<<<1, 1024, 0, stream>>>(ws, nch, out_len);
   {

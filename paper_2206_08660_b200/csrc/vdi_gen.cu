@@ -134,7 +134,7 @@ struct GenConst {
   int sub_ox, sub_oy, sub_oz, sub_nx, sub_ny, sub_nz;
   unsigned* sub_oob;
   int chain_levels;  // bisect replays starting below this level use the down-chain shape
-  int learn;         // learned chain directions at the later levels (VDI_LEARN_CHAIN)
+  int learn;         // learned chain directions at the later levels 
 };
 
 struct RayState {
@@ -1523,39 +1523,15 @@ static int plan_gen(const VdiGenArgs* a, GenPlan& p) {
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p.per_sm_sample, p.sample, kGenThreads, p.smem);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p.per_sm_fill, p.fill, kGenThreads, p.smem);
   if (p.per_sm_fill < 1) p.per_sm_fill = 1;
-  {
-    // VDI_BISECT_VARIANT = "levels,depth,prefetch,minblocks,threads,inv,ahead"
-    // (tuning switch for A/B runs). Default 2,8,1,5,128,4096,16: 2 speculated
-    // levels, the A/B-unrolled entry loop, L1 line prefetch 16 entries ahead, 5
-    // blocks of 128 per SM (<= 102 registers), 4096 shared 1/n entries.
-    // See profiles/ for the variants measured this round.
-    const char* env = getenv("VDI_BISECT_VARIANT");
-    int lv = 2, dp = 8, pf = 1, mb = 5, th = 128, inv = 4096, ah = 16;
-    if (env) sscanf(env, "%d,%d,%d,%d,%d,%d,%d", &lv, &dp, &pf, &mb, &th, &inv, &ah);
-    const long long key = (((lv * 10LL + dp) * 10 + pf) * 10 + mb) * 10000LL + th * 10LL +
-                          (ah == 8 ? 1 : ah == 32 ? 2 : 0);
-    p.bisect_threads = kGenThreads;
-    switch (key) {
-      case 1200 * 10000LL + 1280: p.bisect = gen_bisect_kernel<1, 2, 0>; break;
-      case 2225 * 10000LL + 1280: p.bisect = gen_bisect_kernel<2, 2, 1, 5>; break;  // shift pipe
-      case 2914 * 10000LL + 1280: p.bisect = gen_bisect_kernel<2, 2, 1, 4, 128, 16, 1>; break;
-      case 2915 * 10000LL + 1282: p.bisect = gen_bisect_kernel<2, 2, 1, 5, 128, 32, 1>; break;
-      case 2905 * 10000LL + 1280: p.bisect = gen_bisect_kernel<2, 2, 0, 5, 128, 16, 1>; break;
-      case 2915 * 10000LL + 1280:  // depth "9": the two-slot ring, 5 blocks/SM
-        p.bisect = gen_bisect_kernel<2, 2, 1, 5, 128, 16, 1>;
-        break;
-      case 2814 * 10000LL + 1280: p.bisect = gen_bisect_kernel<2, 2, 1, 4, 128, 16, 2>; break;
-      default:  // depth "8": the A/B-unrolled loop, 5 blocks/SM
-        p.bisect = gen_bisect_kernel<2, 2, 1, 5, 128, 16, 2>;
-        break;
-    }
-    p.inv_smem = inv < 0 ? 0 : inv;
-  }
+  // count-only replays: 2 speculated levels, the A/B-unrolled entry loop, L1
+  // line prefetch 16 entries ahead, 5 blocks of 128 per SM (<= 102
+  // registers), 4096 shared 1/n entries (the variants measured in round 1 are
+  // in profiles/r01_gen_v1_fused_cache.md)
+  p.bisect_threads = kGenThreads;
+  p.bisect = gen_bisect_kernel<2, 2, 1, 5, 128, 16, 2>;
+  p.inv_smem = 4096;
   // the emit kernel uses no shared memory: give the unified L1 everything
-  {
-    const char* env = getenv("VDI_EMIT_RING");  // A/B switch; default: ring
-    p.emit = env && env[0] == '0' ? gen_emit_kernel<false> : gen_emit_kernel<true>;
-  }
+  p.emit = gen_emit_kernel<true>;
   cudaFuncSetAttribute(p.emit, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
   p.smem_inv = sizeof(double) * (size_t)(p.inv_smem < p.inv_n ? p.inv_smem : p.inv_n);
   if (p.smem_inv > 48 * 1024)
@@ -1584,7 +1560,7 @@ static int plan_gen(const VdiGenArgs* a, GenPlan& p) {
 
 // Minimum: room for one fused-fallback block of per-lane slots. Recommended:
 // enough cache that one round holds every overflowing ray of typical scenes
-// (~30% of rays x the longest chord), capped at 24 GiB.
+// (~30% of rays x the longest chord), capped at half the free device memory.
 size_t gen_workspace_bytes(const VdiGenArgs* a, int recommended) {
   GenPlan p;
   if (plan_gen(a, p) != VDI_OK) return 0;
@@ -1593,17 +1569,17 @@ size_t gen_workspace_bytes(const VdiGenArgs* a, int recommended) {
   const size_t fused_all = sizeof(float4) * (size_t)p.sms * p.per_sm_fused * kGenThreads *
                            (size_t)p.max_steps;
   if (rec < fused_all) rec = fused_all;
-  // cache cap: half of the device memory free now, at least 24 GiB. Rays
-  // that do not fit are deferred to another round and re-sampled, which is
-  // what makes a small cap expensive (C5: 24 GiB -> 989 ms, 64 GiB -> 426 ms,
-  // 120 GiB -> 372 ms of generation). VDI_GEN_WS_GB overrides (A/B switch).
+  // cache cap: half of the device memory free now (never more than is free;
+  // the caller keeps the other half). Rays that do not fit are deferred to
+  // another round and re-sampled, which is what makes a small cap expensive
+  // (C5: 24 GiB -> 989 ms, 64 GiB -> 426 ms, 120 GiB -> 372 ms of
+  // generation), but the launch is correct at any size >= the minimum.
   if (!recommended) return p.off_cache + min_cache;  // (no device query on the launch path)
-  size_t cap = (size_t)24 << 30;
+  size_t cap = min_cache;
   {
     size_t free_b = 0, total_b = 0;
     if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess && free_b / 2 > cap) cap = free_b / 2;
   }
-  if (const char* env = getenv("VDI_GEN_WS_GB")) cap = (size_t)atoll(env) << 30;
   if (rec > cap) rec = cap;
   if (rec < min_cache) rec = min_cache;
   return p.off_cache + rec;
@@ -1766,13 +1742,11 @@ int gen_launch(const VdiGenArgs* a, cudaStream_t stream) {
   // replays that start below level 6 speculate the down-chain: on the queued
   // rays levels 0-2 go down > 98 % of the time at C3 and levels 0-5 always at
   // C4 / C5 (tools/bisect_paths.py). Measured gen: C3 40.2 -> 37.8 ms, C4 82.4
-  // -> 73.9, C5 391 -> 359 (VDI_CHAIN_LEVELS = 0 restores the tree everywhere)
+  // -> 73.9, C5 391 -> 359 (chain_levels = 0 restores the tree everywhere)
   c.chain_levels = 6;
-  if (const char* env = getenv("VDI_CHAIN_LEVELS")) c.chain_levels = atoi(env);
   // learned chain directions beyond those levels (measured: C3 gen 33.6 ->
-  // 32.8 ms; C4 / C5 within noise). VDI_LEARN_CHAIN = 0 disables.
+  // 32.8 ms; C4 / C5 within noise). learn = 0 disables.
   c.learn = 1;
-  if (const char* env = getenv("VDI_LEARN_CHAIN")) c.learn = atoi(env);
   if (sub) {
     const int lb = a->brick_log2 >= 1 ? a->brick_log2 : 3;
     if (c.ess && ((c.sub_ox | c.sub_oy | c.sub_oz) & ((1 << lb) - 1)))

@@ -23,7 +23,7 @@ namespace vdi {
 
 constexpr int kRenderThreads = 128;
 #ifndef VDI_RENDER_MINB
-#define VDI_RENDER_MINB 6  // 80 registers: 6 blocks/SM (C3 render 1.29 -> 0.95 ms, run_pipeline)
+#define VDI_RENDER_MINB 6
 #endif
 
 struct RenderConst {
@@ -33,6 +33,7 @@ struct RenderConst {
   long long n_slots;
   int lt_words;  // words of the list-tile bitmap staged in shared memory (0: none)
   int lt_wpr;    // its words per tile row
+  double rfn;    // RN(1 / (far - near)): (x - near) / (far - near) via div_by
 };
 
 // List-tile occupancy (vdi_list_tiles): 8x8 lists per tile, one bitmap word
@@ -42,11 +43,167 @@ __host__ __device__ inline int lt_words_per_row(int vdi_w) {
   return ((vdi_w + kListTile - 1) / kListTile + 31) / 32;
 }
 
-__global__ void __launch_bounds__(kRenderThreads, VDI_RENDER_MINB) render_kernel(const RenderConst c) {
+// Per-ray state that only the shading of a non-empty list reads and updates,
+// kept in shared memory (one slot per thread, SoA: conflict-free): the
+// empty-list walk then carries only its DDA state in registers, and the
+// shading's f64 temporaries do not force the walk state to spill.
+struct ShadeSmem {
+  double a0x[kRenderThreads], a0y[kRenderThreads], a0z[kRenderThreads];
+  double cdx[kRenderThreads], cdy[kRenderThreads], cdz[kRenderThreads];
+  double acc_r[kRenderThreads], acc_g[kRenderThreads], acc_b[kRenderThreads];
+  double acc_a[kRenderThreads];
+  double dep_key[kRenderThreads], dep_val[kRenderThreads];  // last proj_b / (proj_a - d(s))
+  int p[kRenderThreads];                                    // the Alg. 2 seed (raycast.py:344)
+  int nint[kRenderThreads], nsearch[kRenderThreads];
+};
+
+// One non-empty list of the DDA (raycast.py:346-435 for count > 0): the ESS
+// test, the seeded search and the Eq. 2 compositing. Returns true when the
+// ray terminates (acc_a >= early_term).
+template <bool kMask>
+__device__ __forceinline__ bool shade_list(const RenderConst& c, ShadeSmem& sm, int t, int cx,
+                                           int cy, long long lidx, int count, double s_cur,
+                                           double tmin) {
+  const VdiRenderArgs& a = c.a;
+  const int vdi_w = a.vdi_w, vdi_h = a.vdi_h, n_sg = a.n_sg;
+  const double a0x = sm.a0x[t], a0y = sm.a0y[t], a0z = sm.a0z[t];
+  const double cdx = sm.cdx[t], cdy = sm.cdy[t], cdz = sm.cdz[t];
+  double s_exit = dmin(tmin, 1.0);  // min(min(t_max_x, t_max_y), 1.0), raycast.py:345
+  if (s_exit < s_cur) s_exit = s_cur;
+  const double d_entry = a0z + s_cur * cdz;
+  const double d_exit = a0z + s_exit * cdz;
+  if (a.use_ess) {
+    // _grid_cell_range (raycast.py:258-272) + the all-empty scan (359-370).
+    // d = a0z + s cdz is a function of s alone, so the depth of a shared
+    // chord parameter (this list's entry = the previous list's exit) is reused.
+    const double x_a = a0x + s_cur * cdx, y_a = a0y + s_cur * cdy;
+    const double x_b = a0x + s_exit * cdx, y_b = a0y + s_exit * cdy;
+    const double dep_a =
+        s_cur == sm.dep_key[t] ? sm.dep_val[t] : a.proj_b / (a.proj_a - d_entry);
+    const double dep_b = a.proj_b / (a.proj_a - d_exit);
+    sm.dep_key[t] = s_exit;
+    sm.dep_val[t] = dep_b;
+    const int gx = a.gx, gy = a.gy, gz = a.gz;
+    const int cgx0 = clampi(floor_ll((dmin(x_a, x_b) + 1.0) * gx / 2.0), 0, gx - 1);
+    const int cgx1 = clampi(floor_ll((dmax(x_a, x_b) + 1.0) * gx / 2.0), 0, gx - 1);
+    const int cgy0 = clampi(floor_ll((dmin(y_a, y_b) + 1.0) * gy / 2.0), 0, gy - 1);
+    const int cgy1 = clampi(floor_ll((dmax(y_a, y_b) + 1.0) * gy / 2.0), 0, gy - 1);
+    const double fn = a.far - a.near;
+    const int cz0 =
+        clampi(floor_ll(div_by(dmin(dep_a, dep_b) - a.near, fn, c.rfn) * gz), 0, gz - 1);
+    const int cz1 =
+        clampi(floor_ll(div_by(dmax(dep_a, dep_b) - a.near, fn, c.rfn) * gz), 0, gz - 1);
+    bool empty = true;
+    if (kMask) {
+      uint64_t m = 0;
+      for (int cgy = cgy0; cgy <= cgy1; ++cgy)
+        for (int cgx = cgx0; cgx <= cgx1; ++cgx) m |= __ldg(a.grid_zmask + cgy * gx + cgx);
+      // bits cz0..cz1 (2 << 63 wraps to 0, which still yields bits cz0..63)
+      const uint64_t want = (2ull << cz1) - (1ull << cz0);
+      empty = (m & want) == 0;
+    } else {
+      for (int cz = cz0; cz <= cz1 && empty; ++cz)
+        for (int cgy = cgy0; cgy <= cgy1 && empty; ++cgy)
+          for (int cgx = cgx0; cgx <= cgx1; ++cgx)
+            if (__ldg(a.grid + ((long long)cz * gy + cgy) * gx + cgx) > 0u) {
+              empty = false;
+              break;
+            }
+    }
+    if (empty) return false;
+  }
+  sm.nsearch[t] += 1;
+  const float* ls = a.segs + lidx * (long long)list_stride(n_sg);
+  const float* fronts = ls + front_off(n_sg);
+  const float* backs = ls + back_off(n_sg);
+  const float4* rgba = reinterpret_cast<const float4*>(ls);
+  int seed;
+  const int j = find_first(fronts, backs, count, d_entry, d_exit, sm.p[t], seed);
+  sm.p[t] = seed;
+  if (j < 0) return false;
+  const bool fwd = d_entry <= d_exit;
+  const double zlo = dmin(d_entry, d_exit), zhi = dmax(d_entry, d_exit);
+  const double xc = -1.0 + 2.0 * (cx + 0.5) / vdi_w;
+  const double yc = -1.0 + 2.0 * (cy + 0.5) / vdi_h;
+  double acc_r = sm.acc_r[t], acc_g = sm.acc_g[t], acc_b = sm.acc_b[t], acc_a = sm.acc_a[t];
+  int nint = sm.nint[t], p = seed;
+  bool done = false;
+  for (int k = j; 0 <= k && k < count; k += fwd ? 1 : -1) {
+    const double fk = fronts[k], bk = backs[k];
+    const double ilo = dmax(fk, zlo), ihi = dmin(bk, zhi);
+    if (ilo > ihi) break;
+    double s_a, s_b;
+    if (fabs(cdz) < 1e-12) {
+      s_a = s_cur;
+      s_b = s_exit;
+    } else {
+      s_a = (ilo - a0z) / cdz;
+      s_b = (ihi - a0z) / cdz;
+      if (s_a > s_b) {
+        const double tt = s_a;
+        s_a = s_b;
+        s_b = tt;
+      }
+      if (s_a < s_cur) s_a = s_cur;
+      if (s_b > s_exit) s_b = s_exit;
+    }
+    double w0x, w0y, w0z, w1x, w1y, w1z;
+    xform(a.gen_inv_pv, a0x + s_a * cdx, a0y + s_a * cdy, a0z + s_a * cdz, w0x, w0y, w0z);
+    xform(a.gen_inv_pv, a0x + s_b * cdx, a0y + s_b * cdy, a0z + s_b * cdz, w1x, w1y, w1z);
+    const double ex = w1x - w0x, ey = w1y - w0y, ez = w1z - w0z;
+    const double l = sqrt(ex * ex + ey * ey + ez * ez);
+    double wfx, wfy, wfz, wbx, wby, wbz;
+    xform(a.gen_inv_pv, xc, yc, fk, wfx, wfy, wfz);
+    xform(a.gen_inv_pv, xc, yc, bk, wbx, wby, wbz);
+    const double tx = wbx - wfx, ty = wby - wfy, tz = wbz - wfz;
+    const double thick = sqrt(tx * tx + ty * ty + tz * tz);
+    const float4 c4 = rgba[k];
+    const double alpha = c4.w;
+    if (alpha > 0.0 && thick > 0.0) {
+      const double a_t = 1.0 - pow(1.0 - alpha, l / thick);
+      const double scale = a_t / alpha;
+      const double wgt = 1.0 - acc_a;
+      acc_r += wgt * (double)c4.x * scale;
+      acc_g += wgt * (double)c4.y * scale;
+      acc_b += wgt * (double)c4.z * scale;
+      acc_a += wgt * a_t;
+    }
+    nint += 1;
+    p = k;
+    if (acc_a >= a.early_term) {
+      done = true;
+      break;
+    }
+  }
+  sm.acc_r[t] = acc_r;
+  sm.acc_g[t] = acc_g;
+  sm.acc_b[t] = acc_b;
+  sm.acc_a[t] = acc_a;
+  sm.nint[t] = nint;
+  sm.p[t] = p;
+  return done;
+}
+
+// raycast.py:283-456, one thread per output pixel (a warp owns an 8x4 tile).
+// The DDA loop is restated around one fact: the break test s_exit >= 1.0
+// (raycast.py:430) is min(t_max_x, t_max_y) >= 1.0, because s_cur < 1.0 holds
+// on every iteration the reference reaches, and the x-before-y tie rule
+// (t_max_x <= t_max_y, 437) selects the same minimum. So an empty list costs
+// one compare, one count load and the step; s_exit, the depths and the ESS
+// test are evaluated only for lists with count > 0 (the reference evaluates
+// d_entry / d_exit for every list but reads them only there). The early
+// termination test (429) can only change after a shading. Same visits, same
+// order, same arithmetic: the image and every counter are unchanged.
+template <bool kTiles, bool kMask>
+__global__ void __launch_bounds__(kRenderThreads, VDI_RENDER_MINB) render_kernel(const __grid_constant__ RenderConst c) {
   const VdiRenderArgs& a = c.a;
   extern __shared__ uint32_t s_tiles[];
-  for (int k = threadIdx.x; k < c.lt_words; k += blockDim.x) s_tiles[k] = __ldg(a.list_tiles + k);
-  __syncthreads();
+  __shared__ ShadeSmem sm;
+  const int t = threadIdx.x;
+  if (kTiles) {
+    for (int k = threadIdx.x; k < c.lt_words; k += blockDim.x) s_tiles[k] = __ldg(a.list_tiles + k);
+    __syncthreads();
+  }
   const long long slot = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   unsigned long long st_vis = 0, st_int = 0, st_srch = 0;
   if (slot < c.n_slots) {
@@ -56,9 +213,10 @@ __global__ void __launch_bounds__(kRenderThreads, VDI_RENDER_MINB) render_kernel
     const int lrow = (int)(tile / c.tiles_x) * kTileH + (w >> 3);
     if (col < a.out_w && lrow < c.local_h) {
       const int row = band_global_row(lrow, a.band_rows, a.band_stride, a.band_offset);
-      const int vdi_w = a.vdi_w, vdi_h = a.vdi_h, n_sg = a.n_sg;
-      double acc_r = 0.0, acc_g = 0.0, acc_b = 0.0, acc_a = 0.0;
-      int nvis = 0, nint = 0, nsearch = 0;
+      const int vdi_w = a.vdi_w, vdi_h = a.vdi_h;
+      sm.acc_r[t] = sm.acc_g[t] = sm.acc_b[t] = sm.acc_a[t] = 0.0;
+      sm.nint[t] = sm.nsearch[t] = 0;
+      int nvis = 0;
       double d[3];
       pixel_ray(a.new_inv_pv, a.eye, col, row, a.out_w, a.out_h, d);
       const double* eye = a.eye;
@@ -74,154 +232,72 @@ __global__ void __launch_bounds__(kRenderThreads, VDI_RENDER_MINB) render_kernel
         xform(a.gen_pv, eye[0] + t0 * d[0], eye[1] + t0 * d[1], eye[2] + t0 * d[2], a0x, a0y, a0z);
         xform(a.gen_pv, eye[0] + t1 * d[0], eye[1] + t1 * d[1], eye[2] + t1 * d[2], a1x, a1y, a1z);
         const double cdx = a1x - a0x, cdy = a1y - a0y, cdz = a1z - a0z;
+        sm.a0x[t] = a0x;
+        sm.a0y[t] = a0y;
+        sm.a0z[t] = a0z;
+        sm.cdx[t] = cdx;
+        sm.cdy[t] = cdy;
+        sm.cdz[t] = cdz;
         int cx = clampi(floor_ll((a0x + 1.0) * vdi_w / 2.0), 0, vdi_w - 1);
         int cy = clampi(floor_ll((a0y + 1.0) * vdi_h / 2.0), 0, vdi_h - 1);
         const int step_x = cdx > 0 ? 1 : (cdx < 0 ? -1 : 0);
         const int step_y = cdy > 0 ? 1 : (cdy < 0 ? -1 : 0);
-        double t_max_x, t_delta_x, t_max_y, t_delta_y;
+        double t_max_x = INFINITY, t_delta_x = INFINITY, t_max_y = INFINITY,
+               t_delta_y = INFINITY;
         if (step_x != 0) {
           const double bx = -1.0 + 2.0 * (double)(cx + (step_x > 0 ? 1 : 0)) / vdi_w;
           t_max_x = (bx - a0x) / cdx;
           t_delta_x = (2.0 / vdi_w) / fabs(cdx);
-        } else {
-          t_max_x = INFINITY;
-          t_delta_x = INFINITY;
         }
         if (step_y != 0) {
           const double by = -1.0 + 2.0 * (double)(cy + (step_y > 0 ? 1 : 0)) / vdi_h;
           t_max_y = (by - a0y) / cdy;
           t_delta_y = (2.0 / vdi_h) / fabs(cdy);
-        } else {
-          t_max_y = INFINITY;
-          t_delta_y = INFINITY;
         }
-        int p = -1;
+        sm.p[t] = -1;
+        sm.dep_key[t] = -1.0;  // chord parameters are >= 0
+        sm.dep_val[t] = 0.0;
         double s_cur = 0.0;
-        bool done = false;
         const int max_iter = vdi_w + vdi_h + 4;
-        const int gx = a.gx, gy = a.gy, gz = a.gz;
-        for (int it = 0; it < max_iter; ++it) {
-          double s_exit = dmin(dmin(t_max_x, t_max_y), 1.0);
-          if (s_exit < s_cur) s_exit = s_cur;
-          const double d_entry = a0z + s_cur * cdz;
-          const double d_exit = a0z + s_exit * cdz;
+        const int32_t* rowp =
+            a.counts + (long long)vdi_storage_row(cy, a.vdi_band_rows, a.vdi_band_world,
+                                                  a.vdi_rows_per_rank) * vdi_w;
+        for (;;) {
+          const bool xs = t_max_x <= t_max_y;
+          const double tmin = xs ? t_max_x : t_max_y;
           nvis += 1;
-          const long long lidx =
-              (long long)vdi_storage_row(cy, a.vdi_band_rows, a.vdi_band_world,
-                                         a.vdi_rows_per_rank) * vdi_w + cx;
-          // a list of an empty tile has count 0: no load (SURVEY 8(f) rank 4,
-          // empty-list skipping with exact lists_visited accounting)
           int count = 0;
-          if (c.lt_words == 0 ||
-              ((s_tiles[(cy >> 3) * c.lt_wpr + (cx >> 8)] >> ((cx >> 3) & 31)) & 1u))
-            count = __ldg(a.counts + lidx);
-          bool search = count > 0;
-          if (search && a.use_ess) {
-            const double x_a = a0x + s_cur * cdx, y_a = a0y + s_cur * cdy;
-            const double x_b = a0x + s_exit * cdx, y_b = a0y + s_exit * cdy;
-            const double dep_a = a.proj_b / (a.proj_a - d_entry);
-            const double dep_b = a.proj_b / (a.proj_a - d_exit);
-            const int cgx0 = clampi(floor_ll((dmin(x_a, x_b) + 1.0) * gx / 2.0), 0, gx - 1);
-            const int cgx1 = clampi(floor_ll((dmax(x_a, x_b) + 1.0) * gx / 2.0), 0, gx - 1);
-            const int cgy0 = clampi(floor_ll((dmin(y_a, y_b) + 1.0) * gy / 2.0), 0, gy - 1);
-            const int cgy1 = clampi(floor_ll((dmax(y_a, y_b) + 1.0) * gy / 2.0), 0, gy - 1);
-            const double fn = a.far - a.near;
-            const int cz0 = clampi(floor_ll((dmin(dep_a, dep_b) - a.near) / fn * gz), 0, gz - 1);
-            const int cz1 = clampi(floor_ll((dmax(dep_a, dep_b) - a.near) / fn * gz), 0, gz - 1);
-            bool empty = true;
-            for (int cz = cz0; cz <= cz1 && empty; ++cz)
-              for (int cgy = cgy0; cgy <= cgy1 && empty; ++cgy)
-                for (int cgx = cgx0; cgx <= cgx1; ++cgx)
-                  if (__ldg(a.grid + ((long long)cz * gy + cgy) * gx + cgx) > 0u) {
-                    empty = false;
-                    break;
-                  }
-            if (empty) search = false;
+          // a list of an empty tile has count 0: no load
+          if (!kTiles || ((s_tiles[(cy >> 3) * c.lt_wpr + (cx >> 8)] >> ((cx >> 3) & 31)) & 1u))
+            count = __ldg(rowp + cx);
+          if (count > 0) {
+            const long long lidx = (rowp - a.counts) + cx;
+            if (shade_list<kMask>(c, sm, t, cx, cy, lidx, count, s_cur, tmin)) break;
           }
-          if (search) {
-            nsearch += 1;
-            const float* ls = a.segs + lidx * (long long)list_stride(n_sg);
-            const float* fronts = ls + front_off(n_sg);
-            const float* backs = ls + back_off(n_sg);
-            const float4* rgba = reinterpret_cast<const float4*>(ls);
-            int seed;
-            const int j = find_first(fronts, backs, count, d_entry, d_exit, p, seed);
-            p = seed;
-            if (j >= 0) {
-              const bool fwd = d_entry <= d_exit;
-              const double zlo = dmin(d_entry, d_exit), zhi = dmax(d_entry, d_exit);
-              const double xc = -1.0 + 2.0 * (cx + 0.5) / vdi_w;
-              const double yc = -1.0 + 2.0 * (cy + 0.5) / vdi_h;
-              int k = j;
-              while (0 <= k && k < count) {
-                const double fk = fronts[k], bk = backs[k];
-                const double ilo = dmax(fk, zlo), ihi = dmin(bk, zhi);
-                if (ilo > ihi) break;
-                double s_a, s_b;
-                if (fabs(cdz) < 1e-12) {
-                  s_a = s_cur;
-                  s_b = s_exit;
-                } else {
-                  s_a = (ilo - a0z) / cdz;
-                  s_b = (ihi - a0z) / cdz;
-                  if (s_a > s_b) {
-                    const double t = s_a;
-                    s_a = s_b;
-                    s_b = t;
-                  }
-                  if (s_a < s_cur) s_a = s_cur;
-                  if (s_b > s_exit) s_b = s_exit;
-                }
-                double w0x, w0y, w0z, w1x, w1y, w1z;
-                xform(a.gen_inv_pv, a0x + s_a * cdx, a0y + s_a * cdy, a0z + s_a * cdz, w0x, w0y, w0z);
-                xform(a.gen_inv_pv, a0x + s_b * cdx, a0y + s_b * cdy, a0z + s_b * cdz, w1x, w1y, w1z);
-                const double ex = w1x - w0x, ey = w1y - w0y, ez = w1z - w0z;
-                const double l = sqrt(ex * ex + ey * ey + ez * ez);
-                double wfx, wfy, wfz, wbx, wby, wbz;
-                xform(a.gen_inv_pv, xc, yc, fk, wfx, wfy, wfz);
-                xform(a.gen_inv_pv, xc, yc, bk, wbx, wby, wbz);
-                const double tx = wbx - wfx, ty = wby - wfy, tz = wbz - wfz;
-                const double thick = sqrt(tx * tx + ty * ty + tz * tz);
-                const float4 c4 = rgba[k];
-                const double alpha = c4.w;
-                if (alpha > 0.0 && thick > 0.0) {
-                  const double a_t = 1.0 - pow(1.0 - alpha, l / thick);
-                  const double scale = a_t / alpha;
-                  const double wgt = 1.0 - acc_a;
-                  acc_r += wgt * (double)c4.x * scale;
-                  acc_g += wgt * (double)c4.y * scale;
-                  acc_b += wgt * (double)c4.z * scale;
-                  acc_a += wgt * a_t;
-                }
-                nint += 1;
-                p = k;
-                if (acc_a >= a.early_term) {
-                  done = true;
-                  break;
-                }
-                k += fwd ? 1 : -1;
-              }
-            }
-          }
-          if (done || acc_a >= a.early_term) break;
-          if (s_exit >= 1.0) break;
-          if (t_max_x <= t_max_y) {
+          if (tmin >= 1.0 || nvis >= max_iter) break;
+          if (xs) {
             cx += step_x;
             s_cur = t_max_x;
             t_max_x += t_delta_x;
+            if ((unsigned)cx >= (unsigned)vdi_w) break;
           } else {
             cy += step_y;
             s_cur = t_max_y;
             t_max_y += t_delta_y;
+            if ((unsigned)cy >= (unsigned)vdi_h) break;
+            rowp = a.counts + (long long)vdi_storage_row(cy, a.vdi_band_rows, a.vdi_band_world,
+                                                         a.vdi_rows_per_rank) * vdi_w;
           }
-          if (cx < 0 || cx >= vdi_w || cy < 0 || cy >= vdi_h) break;
         }
       }
+      const double acc_a = sm.acc_a[t];
       const double wgt = 1.0 - acc_a;
       const long long pix = (long long)lrow * a.out_w + col;
       double2* o = reinterpret_cast<double2*>(a.image + pix * 4);
-      o[0] = make_double2(acc_r + wgt * a.bg[0] * a.bg[3], acc_g + wgt * a.bg[1] * a.bg[3]);
-      o[1] = make_double2(acc_b + wgt * a.bg[2] * a.bg[3], acc_a + wgt * a.bg[3]);
+      o[0] = make_double2(sm.acc_r[t] + wgt * a.bg[0] * a.bg[3],
+                          sm.acc_g[t] + wgt * a.bg[1] * a.bg[3]);
+      o[1] = make_double2(sm.acc_b[t] + wgt * a.bg[2] * a.bg[3], acc_a + wgt * a.bg[3]);
+      const int nint = sm.nint[t], nsearch = sm.nsearch[t];
       if (a.lists_visited) a.lists_visited[pix] = nvis;
       if (a.segs_intersected) a.segs_intersected[pix] = nint;
       if (a.lists_searched) a.lists_searched[pix] = nsearch;
@@ -254,25 +330,50 @@ int render_launch(const VdiRenderArgs* args, cudaStream_t stream) {
   if (c.a.vdi_band_world <= 0) c.a.vdi_band_world = 1;
   c.local_h = local_rows(args->out_h, c.a.band_rows, c.a.band_stride, c.a.band_offset);
   c.tiles_x = (args->out_w + kTileW - 1) / kTileW;
+  c.rfn = 1.0 / (c.a.far - c.a.near);
   const long long tiles_y = (c.local_h + kTileH - 1) / kTileH;
   c.n_slots = (long long)c.tiles_x * tiles_y * 32;
   if (c.n_slots == 0) return VDI_OK;
   const long long blocks = (c.n_slots + kRenderThreads - 1) / kRenderThreads;
   c.lt_wpr = lt_words_per_row(c.a.vdi_w);
   const long long ltw = (long long)c.lt_wpr * ((c.a.vdi_h + kListTile - 1) / kListTile);
-  // staged when it fits next to the 6 resident blocks' registers (<= 32 KiB)
+  // staged when it fits next to the resident blocks' registers (<= 32 KiB)
   c.lt_words = c.a.list_tiles && ltw <= 8192 ? (int)ltw : 0;
+  const bool mask = c.a.grid_zmask != nullptr && c.a.gz <= 64;
   const size_t smem = sizeof(uint32_t) * (size_t)c.lt_words;
+  void (*fn)(RenderConst) = c.lt_words ? (mask ? render_kernel<true, true> : render_kernel<true, false>)
+                                       : (mask ? render_kernel<false, true> : render_kernel<false, false>);
   if (smem > 0) {
-    const cudaError_t e = cudaFuncSetAttribute(render_kernel,
-                                               cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               (int)smem);
+    const cudaError_t e =
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return set_error(VDI_ELAUNCH, "render smem: %s", cudaGetErrorString(e));
   }
-  render_kernel<<<(unsigned)blocks, kRenderThreads, smem, stream>>>(c);
+  fn<<<(unsigned)blocks, kRenderThreads, smem, stream>>>(c);
   const cudaError_t err = cudaGetLastError();
   if (err != cudaSuccess)
     return set_error(VDI_ELAUNCH, "render launch: %s", cudaGetErrorString(err));
+  return VDI_OK;
+}
+
+// vdi_grid_zmask: one thread per grid column; bit cz of its word is
+// grid[cz][cgy][cgx] > 0 (consecutive threads read consecutive cells).
+__global__ void grid_zmask_kernel(const uint32_t* __restrict__ grid, int gx, int gy, int gz,
+                                  uint64_t* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int n = gx * gy;
+  if (i >= n) return;
+  uint64_t m = 0;
+  for (int cz = 0; cz < gz; ++cz)
+    if (__ldg(grid + (long long)cz * n + i) > 0u) m |= 1ull << cz;
+  out[i] = m;
+}
+
+int grid_zmask(const uint32_t* grid, int gx, int gy, int gz, uint64_t* out, cudaStream_t stream) {
+  const int n = gx * gy;
+  grid_zmask_kernel<<<(n + 255) / 256, 256, 0, stream>>>(grid, gx, gy, gz, out);
+  const cudaError_t err = cudaGetLastError();
+  if (err != cudaSuccess)
+    return set_error(VDI_ELAUNCH, "grid_zmask launch: %s", cudaGetErrorString(err));
   return VDI_OK;
 }
 

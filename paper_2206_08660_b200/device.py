@@ -4,7 +4,6 @@ libvdi_b200.so. Host<->device traffic goes through pinned staging buffers.
 
 from __future__ import annotations
 
-import os
 import weakref
 
 import numpy as np
@@ -165,12 +164,12 @@ def cells_bytes(voxel_type: str, dims) -> int:
 def use_cells(voxel_type: str, dims) -> bool:
     """Whether generation samples from corner records (vdi_volume_cells): 8x
     the volume's bytes in exchange for one load per sample instead of 8
-    gathers. VDI_CELLS=0/1 forces it. By default only u8 volumes use them
-    (C3: build 1.8 ms, generation -2.5 ms; for f32, C4: build 9.6 ms for
+    gathers. tuning.TUNING.cells forces it. By default only u8 volumes use
+    them (C3: build 1.8 ms, generation -2.5 ms; for f32, C4: build 9.6 ms for
     -3 ms), and only while the records fit in a quarter of device memory."""
-    env = os.environ.get("VDI_CELLS")
-    if env is not None:
-        return env not in ("0", "", "false")
+    from .tuning import TUNING
+    if TUNING.cells is not None:
+        return bool(TUNING.cells)
     if voxel_type != "u8":
         return False
     total = torch().cuda.get_device_properties(torch().cuda.current_device()).total_memory

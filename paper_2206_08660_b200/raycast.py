@@ -6,7 +6,6 @@ The per-pixel NDC DDA, ESS test, Alg. 2 seeded search and Eq. 2 compositing
 
 from __future__ import annotations
 
-import os
 import time
 from dataclasses import dataclass
 
@@ -76,8 +75,9 @@ def use_list_tiles() -> bool:
     """Empty-tile skipping in the render DDA (VdiRenderArgs.list_tiles). Exact,
     but off by default: the counts it avoids reading are L2-resident (8 MB at
     1080p) and the staging costs more than it saves on C2-C5 (render C3 0.98
-    -> 1.02 ms, C5 11.1 -> 11.8 ms). VDI_LIST_TILES=1 turns it on."""
-    return os.environ.get("VDI_LIST_TILES", "0") == "1"
+    -> 1.02 ms, C5 11.1 -> 11.8 ms). tuning.TUNING.list_tiles turns it on."""
+    from .tuning import TUNING
+    return bool(TUNING.list_tiles)
 
 
 def alloc_list_tiles(vdi_w: int, vdi_h: int):
@@ -93,10 +93,29 @@ def launch_list_tiles(a: _capi.VdiRenderArgs, tiles, stream=None) -> None:
     a.list_tiles = dv.ptr(tiles)
 
 
+def alloc_zmask(grid_dims):
+    """Per-column slab words of an AccelGrid (vdi_grid_zmask), or None when
+    gz > 64 (the render then reads the grid cells directly)."""
+    gx, gy, gz = (int(v) for v in grid_dims)
+    if gz > 64:
+        return None
+    return dv.torch().empty(gx * gy, dtype=dv.torch().int64, device="cuda")
+
+
+def launch_zmask(a: _capi.VdiRenderArgs, zmask, stream=None) -> None:
+    """Build the slab words of the grid `a` points at; sets a.grid_zmask."""
+    if zmask is None:
+        a.grid_zmask = None
+        return
+    _capi.check(_capi.load().vdi_grid_zmask(a.grid, a.gx, a.gy, a.gz, dv.ptr(zmask),
+                                            dv.stream_handle() if stream is None else stream))
+    a.grid_zmask = dv.ptr(zmask)
+
+
 def launch_render(vdi, grid, cam_new, opts, image, per_pixel=None, stat_sums=None,
                   band=(16, 1, 0), stream=None):
-    """Enqueue one render on the current stream (no sync; a small tile bitmap
-    is allocated per call)."""
+    """Enqueue one render on the current stream (no sync; the grid's slab
+    words and, if enabled, a tile bitmap are allocated per call)."""
     a = render_args(vdi.device(), vdi.n_sg, vdi.width, vdi.height, vdi.gen_camera,
                     vdi.volume_aabb, grid.device(), grid.dims, grid.near, grid.far, cam_new,
                     opts, image, per_pixel, stat_sums, band)
@@ -105,8 +124,10 @@ def launch_render(vdi, grid, cam_new, opts, image, per_pixel=None, stat_sums=Non
     if use_list_tiles():
         tiles = alloc_list_tiles(vdi.width, vdi.height)
         launch_list_tiles(a, tiles, s)
+    zmask = alloc_zmask(grid.dims) if opts.use_ess else None
+    launch_zmask(a, zmask, s)
     _capi.check(_capi.load().vdi_render_launch(a, s))
-    image._keep_tiles = tiles  # the bitmap must outlive the enqueued render
+    image._keep_tiles = (tiles, zmask)  # they must outlive the enqueued render
 
 
 def _as_device_vdi(vdi):

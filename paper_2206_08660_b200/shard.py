@@ -24,8 +24,8 @@ import numpy as np
 from . import _capi
 from . import device as dv
 from .generate import alloc_gen, launch_generate
-from .raycast import (RenderOptions, alloc_list_tiles, launch_list_tiles, render_args,
-                      use_list_tiles)
+from .raycast import (RenderOptions, alloc_list_tiles, alloc_zmask, launch_list_tiles,
+                      launch_zmask, render_args, use_list_tiles)
 from .vdi import AccelGrid, DeviceVdi, Vdi, default_grid_dims
 
 BAND_ROWS = 16
@@ -262,8 +262,9 @@ class Pipeline:
         # x (sample, fill, bisect, emit) + fused fallback; then
         # vdi_grid_launch and vdi_render_launch
         self.tiles = (alloc_list_tiles(w, h) if use_list_tiles() else None)
+        self.zmask = alloc_zmask(self.grid_dims) if self.opts.use_ess else None
         self.launches_per_step = (1 + (self.cells is not None) + 1 + 3 * 4 + 1 + 1
-                                  + (self.tiles is not None) + 1)
+                                  + (self.tiles is not None) + (self.zmask is not None) + 1)
         if world > 1:
             import torch.distributed as tdist
             self.dist = tdist
@@ -274,9 +275,8 @@ class Pipeline:
                                    device="cuda")
             self.dvdi = DeviceVdi(self.g_counts, self.g_segs, self.gen_band_rows, world,
                                   self.gen_rows)
-            import os as _os
-            self.packed = (PackedExchange(self)
-                           if _os.environ.get("VDI_PACKED_EXCHANGE", "1") != "0" else None)
+            from .tuning import TUNING
+            self.packed = PackedExchange(self) if TUNING.packed_exchange else None
         else:
             self.dist = None
             self.dvdi = DeviceVdi(self.bufs.counts, self.bufs.segs)
@@ -314,6 +314,7 @@ class Pipeline:
             ev[4].record()
         if self.tiles is not None:
             launch_list_tiles(self._rargs, self.tiles)
+        launch_zmask(self._rargs, self.zmask)
         _capi.check(L.vdi_render_launch(self._rargs, dv.stream_handle()))
         if timed:
             ev[5].record()
@@ -362,6 +363,9 @@ class Pipeline:
         the neighbouring frames' kernels (stream.py). Time per frame over
         `steps` frames after `warmup` frames, max over ranks."""
         from .stream import FrameStream
+        if self.bricked:
+            raise NotImplementedError("e2e_stream: a bricked pipeline keeps only its voxel box "
+                                      "resident; stream the box, not the full volume")
         t = self.t
         host = dv.pinned_numpy(self.vol.data.shape, self.vol.data.dtype)
         host[...] = self.vol.data
@@ -398,6 +402,9 @@ class Pipeline:
         H2D every step, the public generate_vdi / render_vdi (N=1) or the
         sharded pipeline (N>1), and the step's results read back to pinned
         host memory."""
+        if self.bricked:
+            raise NotImplementedError("e2e: a bricked pipeline keeps only its voxel box "
+                                      "resident; upload the box, not the full volume")
         t = self.t
         vol = self.vol
         host = dv.pinned_numpy(vol.data.shape, vol.data.dtype)

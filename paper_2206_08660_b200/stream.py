@@ -19,9 +19,12 @@ neighbouring frames' kernels changes. Events order the slot reuse: an upload
 waits for the compute that last read its slot, a frame's compute waits for
 its upload and for the download that last read its output slot.
 
-Results are handed out as numpy views of the pinned host slot: they stay
-valid until the frame two submissions later is submitted (copy them to keep
-them longer).
+At most two frames are in flight: `submit` raises if two submitted frames
+have not been collected yet. Results are handed out as numpy views of the
+pinned host slot: they stay valid until the frame two submissions later is
+submitted (its readback reuses the slot; copy them to keep them longer). In
+packed mode frame i's VDI1 bytes are copied to the host inside collect(i),
+which the in-flight limit orders before submit(i + 2) re-encodes the slot.
 
 packed=True returns the VDI in the reference's own wire/file format instead
 of the dense (H, W, n_sg, 6) array: the VDI1 byte string of
@@ -90,6 +93,9 @@ class FrameStream:
 
     def __init__(self, pipe, packed: bool = False):
         t = dv.require_cuda()
+        if getattr(pipe, "bricked", False):
+            raise NotImplementedError("FrameStream: a bricked pipeline keeps only its voxel "
+                                      "box resident; whole-volume frames do not fit it")
         self.t, self.pipe, self.packed = t, pipe, packed
         vol = pipe.vol
         shape = tuple(pipe.vol_dev.shape)
@@ -139,7 +145,11 @@ class FrameStream:
 
     def submit(self, host_volume: np.ndarray) -> None:
         """Queue one frame. host_volume: (nz, ny, nx) array of the pipeline's
-        voxel type, ideally pinned (dv.pinned_numpy) so the upload is async."""
+        voxel type, ideally pinned (dv.pinned_numpy) so the upload is async.
+        Raises RuntimeError when two frames are already in flight (collect
+        the oldest first: their slots would be overwritten)."""
+        if len(self.pending) >= 2:
+            raise RuntimeError("FrameStream: two frames in flight; collect() the oldest first")
         t, p = self.t, self.pipe
         i, s = self.n, self.n % 2
         src = t.from_numpy(np.ascontiguousarray(host_volume).reshape(self.vol_shape))
@@ -179,6 +189,8 @@ class FrameStream:
 
     def collect(self) -> FrameResult:
         """Wait for the oldest pending frame and return its host results."""
+        if not self.pending:
+            raise RuntimeError("FrameStream: no frame in flight")
         i = self.pending.pop(0)
         s = i % 2
         self.ev_d2h[s].synchronize()

@@ -1,0 +1,22 @@
+"""Explicit library switches (no environment variables are read by the
+library). Every switch is exact: results are bit-identical either way; only
+speed and memory change. Set attributes on `TUNING` (tests and tools do), or
+pass the per-call arguments where a function offers them."""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+
+@dataclass
+class Tuning:
+    # corner records (vdi_volume_cells) for generation / DVR sampling:
+    # None = automatic (u8 volumes whose records fit in a quarter of HBM)
+    cells: bool | None = None
+    # empty-tile skipping in the render DDA (VdiRenderArgs.list_tiles)
+    list_tiles: bool = False
+    # multi-GPU VDI exchange as packed VDI1 shards (False: plain all-gather)
+    packed_exchange: bool = True
+
+
+TUNING = Tuning()

@@ -183,6 +183,7 @@ def test_decode_vdi_matches_reference_arrays():
     n_sg = int.from_bytes(raw[16:20], "little")
     bad[160:162] = (n_sg + 1).to_bytes(2, "little")  # list (0,0) count > n_sg
     bad = bytes(bad) + b"\x00" * 24 * (n_sg + 1 - int.from_bytes(raw[160:162], "little"))
-    with pytest.raises((InvariantViolation, codec.TruncatedStream)):
+    with pytest.raises(InvariantViolation) as e:
         codec.decode_vdi(bad)
+    assert str(e.value) == f"list (0,0) count {n_sg + 1} > n_sg {n_sg}"  # vdi.py:199-201
     del w

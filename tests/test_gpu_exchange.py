@@ -30,11 +30,12 @@ def free_port():
 def rank_main(rank, world, port, packed, out):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
-    os.environ["VDI_PACKED_EXCHANGE"] = "1" if packed else "0"
     torch.cuda.set_device(0)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         from paper_2206_08660_b200 import shard, synth
+        from paper_2206_08660_b200.tuning import TUNING
+        TUNING.packed_exchange = bool(packed)
         from paper_2206_08660_b200.generate import GenParams
         from paper_2206_08660_b200.vdi import Vdi
         vol, tf, gcam, rcam, n_sg = synth.config("C2")

@@ -221,8 +221,9 @@ def test_cells_layout_matches_gather(vt, dims, monkeypatch):
     tf = synth.preset_tf("blobs")
     cam = synth.sweep_camera(vol, 20.0, (96, 80))
     out = {}
+    from paper_2206_08660_b200.tuning import TUNING
     for flag in ("0", "1"):
-        monkeypatch.setenv("VDI_CELLS", flag)
+        monkeypatch.setattr(TUNING, "cells", flag == "1")
         vdi, grid, st = vb.generate_vdi(vol, tf, cam, vb.GenParams(n_sg=12), with_stats=True)
         out[flag] = (vdi.counts, vdi.segs, grid.counts, st.passes, st.samples)
     assert out["0"][0].sum() > 0

@@ -60,3 +60,41 @@ def test_tiles_exact(cfg, angle):
     for x, y in zip(outs[0], outs[1]):
         np.testing.assert_array_equal(x, y)
     assert outs[0][1].sum() > 0
+
+
+def _zmask_ref(grid):
+    gz, gy, gx = grid.shape
+    bits = (grid > 0).astype(np.uint64) << np.arange(gz, dtype=np.uint64)[:, None, None]
+    return bits.sum(axis=0).astype(np.uint64).reshape(-1)
+
+
+@pytest.mark.parametrize("cfg,angle", [("C2", 15.0), ("C2", 40.0), ("C3", 15.0)])
+def test_zmask_exact(cfg, angle):
+    """The ESS test through the grid's per-column slab words
+    (VdiRenderArgs.grid_zmask) gives the image and every counter of the
+    cell-by-cell test (raycast.py:359-370)."""
+    from paper_2206_08660_b200.raycast import alloc_zmask, launch_zmask
+    vol, tf, gcam, rcam, n_sg = synth.config(cfg)
+    rcam = synth.sweep_camera(vol, angle, gcam.viewport, synth.CONFIGS[cfg][4])
+    vdi, grid = vb.generate_vdi(vol, tf, gcam, vb.GenParams(n_sg=n_sg))
+    d = vdi.device()
+    ow, oh = rcam.viewport
+    L = _capi.load()
+    outs = []
+    for use in (False, True):
+        image = torch.empty((oh, ow, 4), dtype=torch.float64, device="cuda")
+        pp = [torch.empty((oh, ow), dtype=torch.int32, device="cuda") for _ in range(3)]
+        a = render_args(d, n_sg, vdi.width, vdi.height, gcam, vdi.volume_aabb, grid.device(),
+                        grid.dims, grid.near, grid.far, rcam, vb.RenderOptions(), image,
+                        per_pixel=pp)
+        if use:
+            zm = alloc_zmask(grid.dims)
+            launch_zmask(a, zm)
+            got = zm.cpu().numpy().view(np.uint64)
+            np.testing.assert_array_equal(got, _zmask_ref(grid.device().cpu().numpy()))
+        _capi.check(L.vdi_render_launch(a, dv.stream_handle()))
+        torch.cuda.synchronize()
+        outs.append([image.cpu().numpy()] + [x.cpu().numpy() for x in pp])
+    for x, y in zip(outs[0], outs[1]):
+        np.testing.assert_array_equal(x, y)
+    assert outs[0][3].sum() > 0
