@@ -844,8 +844,12 @@ __device__ __forceinline__ void count_reset(CountState& q, double gamma) {
 // selected so the G states of a lane run as straight-line FP64 code.
 //  * t = s - m is exactly -(m - s), so t*t reproduces R's dr*dr bit for bit and
 //    m + t*inv is R's `m += (s - m) * inv`;
-//  * 1/n comes from the table of host-identical IEEE quotients.
-template <bool kTrack = false>
+//  * 1/n comes from the table of host-identical IEEE quotients;
+//  * a resolved state (n >= 0) keeps stepping -- only its n and kend are
+//    frozen, and nothing else of it is read again -- so the update needs no
+//    guard (a guarded update compiled to a divergent branch per state).
+// kSmemOnly: every 1/n the ray can need is in the shared table.
+template <bool kTrack = false, bool kSmemOnly = false>
 __device__ __forceinline__ void count_sample(CountState& q, double sr, double sg, double sb,
                                              int k, int n_sg, int inv_n, const double* g_inv,
                                              unsigned s_inv, double* d2max = nullptr,
@@ -866,20 +870,18 @@ __device__ __forceinline__ void count_sample(CountState& q, double sr, double sg
   // nsamp <= max_steps, which the global table always covers; the shared copy
   // holds the first inv_n entries (selecting between two loads, never a
   // reciprocal sequence)
-  const double inv = ns < inv_n ? lds_f64(s_inv + 8u * (unsigned)ns) : __ldg(g_inv + ns);
+  const double inv = kSmemOnly ? lds_f64(s_inv + 8u * (unsigned)ns)
+                               : (ns < inv_n ? lds_f64(s_inv + 8u * (unsigned)ns)
+                                             : __ldg(g_inv + ns));
   const double nr = q.mr + tr * inv, ng = q.mg + tg * inv, nb = q.mb + tb * inv;
-  if (live && abort) {
-    q.n = n_sg + 1;
-    q.kend = k + 1;
-  }
-  if (live && !abort) {
-    q.count += split ? 1 : 0;
-    q.mr = merge ? nr : sr;
-    q.mg = merge ? ng : sg;
-    q.mb = merge ? nb : sb;
-    q.nsamp = merge ? ns : 1;
-    q.active = true;
-  }
+  q.n = live && abort ? n_sg + 1 : q.n;
+  q.kend = live && abort ? k + 1 : q.kend;
+  q.count += split ? 1 : 0;
+  q.mr = merge ? nr : sr;
+  q.mg = merge ? ng : sg;
+  q.mb = merge ? nb : sb;
+  q.nsamp = merge ? ns : 1;
+  q.active = true;
 }
 
 // kMode: how a lane streams its cache row -- 0 EntryPipe (register shift),
@@ -889,7 +891,7 @@ __device__ __forceinline__ void count_sample(CountState& q, double sr, double sg
 // a slot whose load is in flight (scoreboards are per warp: EntryRing's
 // select reads both slots and waits for both).
 template <int kLevels, int kDepth, int kPF, int kMinB = 1, int kThreads = kGenThreads,
-          int kAhead = 16, int kMode = 0>
+          int kAhead = 16, int kMode = 0, bool kSmemOnly = false>
 __global__ void __launch_bounds__(kThreads, kMinB) gen_bisect_kernel(const GenConst c) {
   constexpr int kG = (1 << kLevels) - 1;
   extern __shared__ double g_s_inv[];
@@ -1044,11 +1046,12 @@ __global__ void __launch_bounds__(kThreads, kMinB) gen_bisect_kernel(const GenCo
         if (run < 1) run = 1;
         if (run > stored - k) run = stored - k;
 #pragma unroll
-        for (int i = 0; i < kG; ++i)
-          if (q[i].n < 0 && q[i].active) {
-            q[i].count += 1;  // the transparent sample closes the segment
-            q[i].active = false;
-          }
+        for (int i = 0; i < kG; ++i) {
+          // the transparent sample closes the segment (resolved states may
+          // keep stepping, see count_sample)
+          q[i].count += q[i].active ? 1 : 0;
+          q[i].active = false;
+        }
       } else {
         const double a = (double)e.w;
         double a_adj;
@@ -1065,10 +1068,11 @@ __global__ void __launch_bounds__(kThreads, kMinB) gen_bisect_kernel(const GenCo
         const double sr = (double)fabsf(e.x) * a_adj;
         const double sg = (double)e.y * a_adj;
         const double sb = (double)e.z * a_adj;
-        count_sample<true>(q[0], sr, sg, sb, k, n_sg, inv_n, c.inv_tab, s_inv, &d2max0, &split0);
+        count_sample<true, kSmemOnly>(q[0], sr, sg, sb, k, n_sg, inv_n, c.inv_tab, s_inv,
+                                      &d2max0, &split0);
 #pragma unroll
         for (int i = 1; i < kG; ++i)
-          count_sample(q[i], sr, sg, sb, k, n_sg, inv_n, c.inv_tab, s_inv);
+          count_sample<false, kSmemOnly>(q[i], sr, sg, sb, k, n_sg, inv_n, c.inv_tab, s_inv);
       }
       return run;
     };
@@ -1168,10 +1172,11 @@ __global__ void __launch_bounds__(kThreads, kMinB) gen_bisect_kernel(const GenCo
         const double sr = (double)fabsf(e.x) * a_adj;
         const double sg = (double)e.y * a_adj;
         const double sb = (double)e.z * a_adj;
-        count_sample<true>(q[0], sr, sg, sb, k, n_sg, inv_n, c.inv_tab, s_inv, &d2max0, &split0);
+        count_sample<true, kSmemOnly>(q[0], sr, sg, sb, k, n_sg, inv_n, c.inv_tab, s_inv,
+                                      &d2max0, &split0);
 #pragma unroll
         for (int i = 1; i < kG; ++i)
-          count_sample(q[i], sr, sg, sb, k, n_sg, inv_n, c.inv_tab, s_inv);
+          count_sample<false, kSmemOnly>(q[i], sr, sg, sb, k, n_sg, inv_n, c.inv_tab, s_inv);
       }
       const int kold = k;
       k += run;
@@ -1528,8 +1533,9 @@ static int plan_gen(const VdiGenArgs* a, GenPlan& p) {
   // registers), 4096 shared 1/n entries (the variants measured in round 1 are
   // in profiles/r01_gen_v1_fused_cache.md)
   p.bisect_threads = kGenThreads;
-  p.bisect = gen_bisect_kernel<2, 2, 1, 5, 128, 16, 2>;
   p.inv_smem = 4096;
+  p.bisect = p.inv_n <= p.inv_smem ? gen_bisect_kernel<2, 2, 1, 5, 128, 16, 2, true>
+                                   : gen_bisect_kernel<2, 2, 1, 5, 128, 16, 2, false>;
   // the emit kernel uses no shared memory: give the unified L1 everything
   p.emit = gen_emit_kernel<true>;
   cudaFuncSetAttribute(p.emit, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
