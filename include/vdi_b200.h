@@ -20,8 +20,9 @@
  *                      preview through the AccelGrid)
  *   vdi_bilinear_upsample  replaces preview.py:208-223 bilinear_upsample
  *   vdi_encode_vdi1    replaces vdi.py:141-159    encode_vdi (VDI1 bytes, on device)
- *   vdi_lz4_compress   replaces lz4.py:51-114     _compress_kernel (a chunk-parallel
- *                      LZ4 block, decodable by lz4.py:117-168)
+ *   vdi_lz4_compress_exact replaces lz4.py:51-114 _compress_kernel (byte-identical)
+ *   vdi_lz4_compress   a chunk-parallel LZ4 block of the same format (decodable
+ *                      by lz4.py:117-168, not byte-identical; faster)
  *   vdi_validate       replaces vdi.py:116-134    validate_vdi
  *   vdi_gen_rays       replaces generate.py:371-407 generate_list / find_gamma
  *                      (single-ray passes / bisections, batched)
@@ -323,6 +324,13 @@ size_t vdi_lz4_workspace_bytes(size_t n_max);
 int vdi_lz4_compress(const uint8_t* src, size_t n_max, const unsigned long long* n_dev,
                      uint8_t* dst, unsigned long long* out_len, void* workspace,
                      size_t workspace_bytes, vdi_stream_t stream);
+/* The same contract, but the block is the reference's own: one serial greedy
+ * parse with lz4.py's 64 Ki-entry table, byte-identical to lz4.compress(src)
+ * (lz4.py:51-114). Slower than vdi_lz4_compress (one warp parses). */
+size_t vdi_lz4_exact_workspace_bytes(size_t n_max);
+int vdi_lz4_compress_exact(const uint8_t* src, size_t n_max, const unsigned long long* n_dev,
+                           uint8_t* dst, unsigned long long* out_len, void* workspace,
+                           size_t workspace_bytes, vdi_stream_t stream);
 
 int vdi_validate(const VdiValidateArgs* args, vdi_stream_t stream);
 

@@ -112,7 +112,8 @@ EXPORTS = ["vdi_last_error", "vdi_abi_version", "vdi_gen_workspace_bytes",
            "vdi_grid_launch", "vdi_render_launch", "vdi_dvr_launch",
            "vdi_preview_launch", "vdi_bilinear_upsample", "vdi_vdi1_max_bytes",
            "vdi_encode_workspace_bytes", "vdi_encode_vdi1", "vdi_lz4_max_bytes",
-           "vdi_lz4_workspace_bytes", "vdi_lz4_compress", "vdi_validate", "vdi_synth_rm_u8",
+           "vdi_lz4_workspace_bytes", "vdi_lz4_compress",
+           "vdi_lz4_exact_workspace_bytes", "vdi_lz4_compress_exact", "vdi_validate", "vdi_synth_rm_u8",
            "vdi_gen_rays", "vdi_composite_lists", "vdi_dda_cells", "vdi_project_rays",
            "vdi_decode_vdi1_lists", "vdi_find_first_batch",
            "vdi_volume_brick_max", "vdi_selftest_arith", "vdi_segs_to_aos",
@@ -156,6 +157,9 @@ def load():
     L.vdi_lz4_workspace_bytes.argtypes = [ctypes.c_size_t]
     L.vdi_lz4_workspace_bytes.restype = ctypes.c_size_t
     L.vdi_lz4_compress.argtypes = [_P, ctypes.c_size_t, _P, _P, _P, _P, ctypes.c_size_t, _P]
+    L.vdi_lz4_exact_workspace_bytes.argtypes = [ctypes.c_size_t]
+    L.vdi_lz4_exact_workspace_bytes.restype = ctypes.c_size_t
+    L.vdi_lz4_compress_exact.argtypes = [_P, ctypes.c_size_t, _P, _P, _P, _P, ctypes.c_size_t, _P]
     L.vdi_validate.argtypes = [ctypes.POINTER(VdiValidateArgs), _P]
     L.vdi_decode_vdi1_lists.argtypes = [_P, _I, _I, _I, _P, _P, _P, ctypes.c_size_t, _P]
     L.vdi_gen_rays.argtypes = [ctypes.POINTER(VdiGenArgs), _P, _P, ctypes.c_int64, _I, _P]
@@ -183,7 +187,8 @@ def load():
     L.vdi_segs_from_aos.argtypes = [_P, _P, ctypes.c_int64, _I, _P]
     for name in ("vdi_gen_launch", "vdi_grid_launch", "vdi_render_launch", "vdi_dvr_launch",
                  "vdi_preview_launch", "vdi_bilinear_upsample", "vdi_encode_vdi1",
-                 "vdi_decode_vdi1_lists", "vdi_lz4_compress", "vdi_validate", "vdi_synth_rm_u8",
+                 "vdi_decode_vdi1_lists", "vdi_lz4_compress", "vdi_lz4_compress_exact",
+                 "vdi_validate", "vdi_synth_rm_u8",
                  "vdi_gen_rays", "vdi_composite_lists", "vdi_dda_cells", "vdi_project_rays",
                  "vdi_find_first_batch", "vdi_segs_to_aos", "vdi_segs_from_aos",
                  "vdi_list_tiles", "vdi_grid_zmask"):

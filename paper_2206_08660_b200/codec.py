@@ -80,39 +80,46 @@ def encode_vdi(vdi, grid) -> bytes:
     return dv.to_host(out[:n]).tobytes()
 
 
-def compress_device(src, n_max: int, n_dev=None):
+def compress_device(src, n_max: int, n_dev=None, exact: bool = True):
     """LZ4-compress device bytes src[:n] (n = n_dev on the device, else
-    n_max). Returns (uint8 device buffer, device u64 length)."""
+    n_max). Returns (uint8 device buffer, device u64 length).
+
+    exact=True: the reference's block byte for byte (lz4.py:51-114: one
+    serial greedy parse, vdi_lz4_compress_exact). exact=False: the
+    chunk-parallel parse (vdi_lz4_compress) -- same format, decoded exactly by
+    lz4.decompress, about 2 % larger and much faster."""
     t = dv.require_cuda()
     L = _capi.load()
     dst = t.empty(int(L.vdi_lz4_max_bytes(n_max)), dtype=t.uint8, device="cuda")
     out_len = t.zeros(1, dtype=t.int64, device="cuda")
-    ws_bytes = int(L.vdi_lz4_workspace_bytes(n_max))
+    ws_fn = L.vdi_lz4_exact_workspace_bytes if exact else L.vdi_lz4_workspace_bytes
+    run = L.vdi_lz4_compress_exact if exact else L.vdi_lz4_compress
+    ws_bytes = int(ws_fn(n_max))
     ws = t.empty(ws_bytes, dtype=t.uint8, device="cuda")
-    _capi.check(L.vdi_lz4_compress(dv.ptr(src) if n_max else None, int(n_max), dv.ptr(n_dev),
-                                   dv.ptr(dst), dv.ptr(out_len), dv.ptr(ws), ws_bytes,
-                                   dv.stream_handle()))
+    _capi.check(run(dv.ptr(src) if n_max else None, int(n_max), dv.ptr(n_dev), dv.ptr(dst),
+                    dv.ptr(out_len), dv.ptr(ws), ws_bytes, dv.stream_handle()))
     dst._keep = ws
     return dst, out_len
 
 
-def compress(data: bytes) -> bytes:
-    """lz4.py:171-175 compress(): an LZ4 block that lz4.decompress inverts."""
+def compress(data: bytes, exact: bool = True) -> bytes:
+    """lz4.py:171-175 compress(): an LZ4 block that lz4.decompress inverts
+    (with exact=True, the reference's own bytes)."""
     n = len(data)
     if n == 0:
         return b""
     src = dv.to_device(np.frombuffer(data, dtype=np.uint8))
-    dst, out_len = compress_device(src, n)
+    dst, out_len = compress_device(src, n, exact=exact)
     m = int(dv.to_host(out_len)[0])
     return dv.to_host(dst[:m]).tobytes()
 
 
-def compress_vdi(vdi, grid):
+def compress_vdi(vdi, grid, exact: bool = True):
     """lz4.compress(encode_vdi(vdi, grid)) without the raw bytes leaving the
     device: returns (compressed block, uncompressed length), the two fields
     of the reference's VdiPacket (proto.py:66-86)."""
     raw, raw_len = encode_vdi_device(vdi, grid)
-    dst, out_len = compress_device(raw, int(raw.numel()), raw_len)
+    dst, out_len = compress_device(raw, int(raw.numel()), raw_len, exact=exact)
     lens = dv.to_host(dv.torch().cat([raw_len, out_len]))
     m = int(lens[1])
     return dv.to_host(dst[:m]).tobytes(), int(lens[0])

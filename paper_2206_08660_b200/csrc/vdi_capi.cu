@@ -184,6 +184,17 @@ int vdi_lz4_compress(const uint8_t* src, size_t n_max, const unsigned long long*
                            static_cast<cudaStream_t>(stream));
 }
 
+size_t vdi_lz4_exact_workspace_bytes(size_t n_max) { return vdi::lzx_workspace_bytes(n_max); }
+
+int vdi_lz4_compress_exact(const uint8_t* src, size_t n_max, const unsigned long long* n_dev,
+                           uint8_t* dst, unsigned long long* out_len, void* workspace,
+                           size_t workspace_bytes, vdi_stream_t stream) {
+  if ((!src && n_max) || !dst || !out_len || !workspace)
+    return set_error(VDI_EINVAL, "null device pointer");
+  return vdi::lzx_compress(src, n_max, n_dev, dst, out_len, workspace, workspace_bytes,
+                           static_cast<cudaStream_t>(stream));
+}
+
 int vdi_validate(const VdiValidateArgs* a, vdi_stream_t stream) {
   if (!a) return set_error(VDI_EINVAL, "null args");
   if (!a->segs || !a->counts || !a->result) return set_error(VDI_EINVAL, "null device pointer");

@@ -871,6 +871,297 @@ int lz4_compress(const uint8_t* src, size_t n_max, const unsigned long long* n_d
   return VDI_OK;
 }
 
+// ------------------------------------------------- LZ4, exact (serial) parse
+// lz4.py:51-114 reproduced byte for byte: ONE greedy parse over the whole
+// input with the reference's 64 Ki-entry table (_HASH_LOG 16), so the block
+// equals lz4.compress(data) exactly. The parse is inherently serial (each
+// decision depends on the table the previous ones left), so one warp runs it,
+// 32 positions per step with the same exact batch rule as the chunked parse:
+// lane j hashes position i + j, takes its candidate from the nearest lower
+// lane with the same hash (a later table write the serial loop would have
+// seen) or from the table, and the lowest lane with a verified match is the
+// serial decision; the table then receives the positions up to it, the last
+// writer of a hash winning.
+//
+// The table lives in shared memory as 24-bit positions (a u16 and a u8
+// array, 192 KiB). A stored value e decodes, at position p, to
+// p - ((p - e) mod 2^24); candidates with that distance in [1, 65535] are the
+// reference's in-window candidates. Every 2^22 positions the table is swept
+// and entries more than 2^22 behind are reset to a value 2^23 behind, so no
+// distance ever wraps (a match longer than 2^21 bytes leaves every entry out
+// of the window, and the table is reset after it). The sequences go to a
+// list; a prefix sum of their encoded sizes places them, and one warp per
+// sequence writes them.
+constexpr int kLzxHash = 16;
+constexpr unsigned kLzxMask = 0xffffffu;
+constexpr long long kLzxSweep = 1ll << 22;
+
+struct LzxSeq {
+  unsigned long long pos;     // match start (the final literal-only sequence: n)
+  unsigned long long anchor;  // first literal
+  unsigned off, mlen;         // mlen 0: the final sequence
+};
+
+struct LzxWs {
+  unsigned long long* n_dev;  // [0] input length, [1] sequences (incl. the final one)
+  LzxSeq* seqs;
+  unsigned long long* bsum;   // per emit block
+};
+
+constexpr int kLzxBlocks = 1184;  // emit blocks (8 per SM)
+
+__device__ __forceinline__ uint32_t lzx_hash(uint32_t v) { return (v * 2654435761u) >> 16; }
+
+__device__ __forceinline__ uint32_t window_load64(const uint8_t* s, long long n, long long i,
+                                                  int lane) {
+  const uint32_t* wb =
+      reinterpret_cast<const uint32_t*>(reinterpret_cast<uintptr_t>(s + i) & ~(uintptr_t)3);
+  return reinterpret_cast<const uint8_t*>(wb + lane) < s + n ? __ldg(wb + lane) : 0u;
+}
+
+__device__ __forceinline__ void lzx_reset(unsigned short* lo, uint8_t* hi, long long i,
+                                          bool keep_recent, int lane) {
+  const unsigned reset = (unsigned)((i - (1ll << 23)) & kLzxMask);
+  for (int k = lane; k < (1 << kLzxHash); k += 32) {
+    const unsigned e = lo[k] | ((unsigned)hi[k] << 16);
+    const unsigned d = ((unsigned)(i & kLzxMask) - e) & kLzxMask;
+    if (!keep_recent || d == 0 || d > (unsigned)kLzxSweep) {
+      lo[k] = (unsigned short)(reset & 0xffffu);
+      hi[k] = (uint8_t)(reset >> 16);
+    }
+  }
+  __syncwarp();
+}
+
+__global__ void __launch_bounds__(32) lzx_parse_kernel(const uint8_t* __restrict__ src, LzxWs ws) {
+  extern __shared__ unsigned short x_lo[];
+  uint8_t* x_hi = reinterpret_cast<uint8_t*>(x_lo + (1 << kLzxHash));
+  const int lane = threadIdx.x;
+  const long long n = (long long)ws.n_dev[0];
+  lzx_reset(x_lo, x_hi, 0, false, lane);
+  const long long limit = n - 12;  // lz4.py:62 (MFLIMIT)
+  const int o = (int)(reinterpret_cast<uintptr_t>(src) & 3);
+  long long i = 0, anchor = 0, next_sweep = kLzxSweep;
+  unsigned long long nseq = 0;
+  uint32_t wl = window_load64(src, n, 0, lane), w1 = window_load64(src, n, 32, lane);
+  while (i < limit) {
+    if (i >= next_sweep) {
+      lzx_reset(x_lo, x_hi, i, true, lane);
+      next_sweep = i + kLzxSweep;
+    }
+    const uint32_t w2 = window_load64(src, n, i + 64, lane);
+    const long long p = i + lane;
+    const bool valid = p < limit;
+    const uint32_t v = window_value(wl, (o + (int)(i & 3)) & 3, lane);
+    const uint32_t h = lzx_hash(v);
+    const unsigned e = valid ? (x_lo[h] | ((unsigned)x_hi[h] << 16)) : 0u;
+    const unsigned d = ((unsigned)(p & kLzxMask) - e) & kLzxMask;
+    const long long tc = valid && d != 0u && d <= 65535u ? p - (long long)d : -1;
+    const uint32_t tv = tc >= 0 ? rd32(src, tc) : ~v;
+    const unsigned key = valid ? h : (0x10000u + lane);
+    const unsigned peers = __match_any_sync(0xffffffffu, key);
+    const unsigned lt = (1u << lane) - 1u;
+    const unsigned lower = peers & lt;
+    const int pl = lower ? 31 - __clz(lower) : lane;
+    const uint32_t pv = __shfl_sync(0xffffffffu, v, pl);
+    const long long cand = lower ? i + pl : tc;
+    const bool match = valid && (lower ? pv == v : tv == v);
+    const unsigned mm = __ballot_sync(0xffffffffu, match);
+    const int w = mm ? __ffs(mm) - 1 : 31;
+    const unsigned upto = w == 31 ? 0xffffffffu : ((2u << w) - 1u);
+    __syncwarp();
+    if (valid && ((1u << lane) & upto) && !(peers & upto & ~lt & ~(1u << lane))) {
+      const unsigned pe = (unsigned)(p & kLzxMask);
+      x_lo[h] = (unsigned short)(pe & 0xffffu);
+      x_hi[h] = (uint8_t)(pe >> 16);
+    }
+    __syncwarp();
+    if (!mm) {
+      i += 32;
+      wl = w1;
+      w1 = w2;
+      continue;
+    }
+    const long long pw = i + w;
+    const long long cw = __shfl_sync(0xffffffffu, cand, w);
+    // extend (lz4.py:66-69), 32 bytes per step
+    long long mlen = 4;
+    const long long mmax = n - 5 - pw;
+    while (true) {
+      const long long k = mlen + lane;
+      const bool stop = k >= mmax || src[cw + k] != src[pw + k];
+      const unsigned sbits = __ballot_sync(0xffffffffu, stop);
+      if (sbits) {
+        mlen += __ffs(sbits) - 1;
+        break;
+      }
+      mlen += 32;
+    }
+    if (lane == 0)
+      ws.seqs[nseq] = LzxSeq{(unsigned long long)pw, (unsigned long long)anchor,
+                             (unsigned)(pw - cw), (unsigned)mlen};
+    nseq += 1;
+    i = pw + mlen;
+    anchor = i;
+    if (mlen > (1ll << 21)) {  // every entry is now out of the window
+      lzx_reset(x_lo, x_hi, i, false, lane);
+      next_sweep = i + kLzxSweep;
+    }
+    if (i < limit && lane == 0) {
+      const unsigned pe = (unsigned)((i - 2) & kLzxMask);
+      const uint32_t hh = lzx_hash(rd32(src, i - 2));
+      x_lo[hh] = (unsigned short)(pe & 0xffffu);
+      x_hi[hh] = (uint8_t)(pe >> 16);
+    }
+    __syncwarp();
+    wl = window_load64(src, n, i, lane);
+    w1 = window_load64(src, n, i + 32, lane);
+  }
+  if (lane == 0) {
+    if (n > 0) {
+      ws.seqs[nseq] = LzxSeq{(unsigned long long)n, (unsigned long long)anchor, 0u, 0u};
+      nseq += 1;
+    }
+    ws.n_dev[1] = nseq;
+  }
+}
+
+__device__ __forceinline__ unsigned long long lzx_size(const LzxSeq& q) {
+  const unsigned long long lit = q.pos - q.anchor;
+  unsigned long long sz = 1 + ext_len(lit) + lit;
+  if (q.mlen) sz += 2 + ext_len((unsigned long long)q.mlen - 4);
+  return sz;
+}
+
+__device__ __forceinline__ void lzx_range(const LzxWs& ws, long long& b0, long long& b1) {
+  const long long m = (long long)ws.n_dev[1];
+  const long long per = (m + kLzxBlocks - 1) / kLzxBlocks;
+  b0 = blockIdx.x * per;
+  b1 = b0 + per < m ? b0 + per : m;
+}
+
+__global__ void __launch_bounds__(1024) lzx_size_kernel(LzxWs ws) {
+  __shared__ unsigned long long s_w[32];
+  long long b0, b1;
+  lzx_range(ws, b0, b1);
+  unsigned long long sum = 0;
+  for (long long k = b0 + threadIdx.x; k < b1; k += blockDim.x) sum += lzx_size(ws.seqs[k]);
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
+  if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = sum;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    unsigned long long v = s_w[threadIdx.x];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    if (threadIdx.x == 0) ws.bsum[blockIdx.x] = v;
+  }
+}
+
+__device__ __forceinline__ unsigned long long lzx_put_len(uint8_t* dst, unsigned long long d,
+                                                          unsigned long long len) {
+  while (len >= 255) {  // lz4.py:43-49 _write_length
+    dst[d++] = 255;
+    len -= 255;
+  }
+  dst[d++] = (uint8_t)len;
+  return d;
+}
+
+// Block b writes its sequence range: sizes -> block scan (1024 at a time) ->
+// one warp per sequence (the header and extension bytes by lane 0, the
+// literals 32 bytes per step by the warp).
+__global__ void __launch_bounds__(1024) lzx_emit_kernel(const uint8_t* __restrict__ src,
+                                                        uint8_t* __restrict__ dst, LzxWs ws,
+                                                        unsigned long long* out_len) {
+  __shared__ unsigned long long s_off[1024];
+  __shared__ unsigned long long s_w[32];
+  long long b0, b1;
+  lzx_range(ws, b0, b1);
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  unsigned long long run = ws.bsum[blockIdx.x];
+  for (long long c0 = b0; c0 < b1; c0 += 1024) {
+    const long long k = c0 + t;
+    const unsigned long long sz = k < b1 ? lzx_size(ws.seqs[k]) : 0ull;
+    unsigned long long v = sz;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const unsigned long long u = __shfl_up_sync(0xffffffffu, v, off);
+      if (lane >= off) v += u;
+    }
+    if (lane == 31) s_w[wid] = v;
+    __syncthreads();
+    if (wid == 0) {
+      unsigned long long x = s_w[lane];
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const unsigned long long u = __shfl_up_sync(0xffffffffu, x, off);
+        if (lane >= off) x += u;
+      }
+      s_w[lane] = x;
+    }
+    __syncthreads();
+    s_off[t] = run + (wid > 0 ? s_w[wid - 1] : 0ull) + v - sz;
+    const unsigned long long total = s_w[31];
+    __syncthreads();
+    const long long cn = b1 - c0 < 1024 ? b1 - c0 : 1024;
+    for (long long j = wid; j < cn; j += 32) {
+      const LzxSeq q = ws.seqs[c0 + j];
+      unsigned long long d = s_off[j];
+      const unsigned long long lit = q.pos - q.anchor;
+      const unsigned lcode = lit >= 15 ? 15u : (unsigned)lit;
+      const unsigned mcode = q.mlen ? (q.mlen - 4 >= 15 ? 15u : q.mlen - 4) : 0u;
+      unsigned long long dl = d + 1;  // literals start
+      if (lane == 0) {
+        dst[d] = (uint8_t)((lcode << 4) | mcode);
+        if (lit >= 15) dl = lzx_put_len(dst, d + 1, lit - 15);
+      }
+      dl = __shfl_sync(0xffffffffu, dl, 0);
+      for (unsigned long long x = lane; x < lit; x += 32) dst[dl + x] = src[q.anchor + x];
+      if (q.mlen && lane == 0) {
+        unsigned long long e = dl + lit;
+        dst[e] = (uint8_t)(q.off & 0xff);
+        dst[e + 1] = (uint8_t)((q.off >> 8) & 0xff);
+        if (q.mlen - 4 >= 15) lzx_put_len(dst, e + 2, (unsigned long long)q.mlen - 4 - 15);
+      }
+    }
+    run += total;
+    __syncthreads();
+  }
+  if (blockIdx.x == kLzxBlocks - 1 && t == 0) *out_len = run;
+}
+
+size_t lzx_workspace_bytes(size_t n_max) {
+  return 256 + align256(sizeof(LzxSeq) * (n_max / 4 + 2)) +
+         align256(sizeof(unsigned long long) * kLzxBlocks);
+}
+
+int lzx_compress(const uint8_t* src, size_t n_max, const unsigned long long* n_dev, uint8_t* dst,
+                 unsigned long long* out_len, void* workspace, size_t ws_bytes,
+                 cudaStream_t stream) {
+  if (ws_bytes < lzx_workspace_bytes(n_max))
+    return set_error(VDI_EINVAL, "lz4 exact workspace too small");
+  char* w = static_cast<char*>(workspace);
+  LzxWs ws;
+  ws.n_dev = reinterpret_cast<unsigned long long*>(w);
+  size_t off = 256;
+  ws.seqs = reinterpret_cast<LzxSeq*>(w + off);
+  off += align256(sizeof(LzxSeq) * (n_max / 4 + 2));
+  ws.bsum = reinterpret_cast<unsigned long long*>(w + off);
+  set_u64_kernel<<<1, 1, 0, stream>>>(ws.n_dev, n_dev, n_max, 0ull);
+  const size_t smem = (sizeof(unsigned short) + 1) * ((size_t)1 << kLzxHash);
+  cudaError_t err =
+      cudaFuncSetAttribute(lzx_parse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (err != cudaSuccess) return set_error(VDI_ELAUNCH, "lz4x smem: %s", cudaGetErrorString(err));
+  lzx_parse_kernel<<<1, 32, smem, stream>>>(src, ws);
+  lzx_size_kernel<<<kLzxBlocks, 1024, 0, stream>>>(ws);
+  scan_blocks_kernel<<<1, 1024, 0, stream>>>(ws.bsum, kLzxBlocks);
+  lzx_emit_kernel<<<kLzxBlocks, 1024, 0, stream>>>(src, dst, ws, out_len);
+  err = cudaGetLastError();
+  if (err != cudaSuccess) return set_error(VDI_ELAUNCH, "lz4x launch: %s", cudaGetErrorString(err));
+  return VDI_OK;
+}
+
 // ------------------------------------------------------- validate_vdi
 
 // vdi.py:116-134 on the device. codes: 1 front >= back, 2 overlapping,

@@ -44,6 +44,10 @@ size_t lz4_workspace_bytes(size_t n_max);
 int lz4_compress(const uint8_t* src, size_t n_max, const unsigned long long* n_dev, uint8_t* dst,
                  unsigned long long* out_len, void* workspace, size_t ws_bytes,
                  cudaStream_t stream);
+size_t lzx_workspace_bytes(size_t n_max);
+int lzx_compress(const uint8_t* src, size_t n_max, const unsigned long long* n_dev, uint8_t* dst,
+                 unsigned long long* out_len, void* workspace, size_t ws_bytes,
+                 cudaStream_t stream);
 int validate_vdi(const VdiValidateArgs* a, cudaStream_t stream);
 int synth_rm_u8(uint8_t* out, int nx, int ny, int nz, const int32_t* box, const float* modes,
                 float band, uint32_t seed, cudaStream_t stream);

@@ -3,12 +3,16 @@ validator (vdi_validate) vs the reference.
 
 - encode_vdi: the VDI1 bytes equal the reference's (sha256 from codec.npz,
   made by vdikit.encode_vdi) and the oracle's, for every committed VDI.
-- LZ4: the device block is a different parse than the reference's serial
-  one, so parity is the transport's own property (test_acceptance.py A6):
-  the reference decoder (oracle.lz4_decompress, the pinned restatement of
-  lz4.py:117-168) returns the input exactly -- on the reference's byte
-  vectors, chunk-boundary sizes, and full C1 / C3 VDIs -- and the block
-  respects the format's end-of-block rules.
+- LZ4, exact mode (the default; vdi_lz4_compress_exact): the block equals
+  the reference's byte for byte -- its own blocks in codec.npz (made by
+  vdikit.lz4.compress) and, for generated inputs (chunk-boundary sizes,
+  unaligned sources, full C1 / C3 VDIs), the pinned oracle restatement of
+  lz4.py:51-114.
+- LZ4, fast mode (exact=False; vdi_lz4_compress, a chunk-parallel parse):
+  parity is the transport's own property (test_acceptance.py A6): the
+  reference decoder (oracle.lz4_decompress, the pinned restatement of
+  lz4.py:117-168) returns the input exactly, and the block respects the
+  format's end-of-block rules.
 - validate_vdi: the reference's InvariantViolation messages on 13 cases.
 """
 
@@ -56,22 +60,31 @@ def test_encode_vdi_matches_reference():
         vdi, grid, gen = _fixture(src)
         raw = codec.encode_vdi(vdi, grid)
         assert hashlib.sha256(raw).hexdigest() == str(g[f"v{k}_raw_sha256"]), src
-        comp = codec.compress(raw)
-        _check_block(comp, raw)
+        ref = g[f"v{k}_lz4"].tobytes()
+        assert codec.compress(raw) == ref, src  # the reference's own block
         comp2, n = codec.compress_vdi(vdi, grid)
-        assert n == len(raw)
-        _check_block(comp2, raw)
+        assert n == len(raw) and comp2 == ref, src
+        _check_block(codec.compress(raw, exact=False), raw)
+        comp3, n3 = codec.compress_vdi(vdi, grid, exact=False)
+        assert n3 == len(raw)
+        _check_block(comp3, raw)
 
 
-def test_lz4_roundtrip_reference_vectors():
+def test_lz4_reference_vectors():
+    """Exact mode reproduces the reference's blocks of every byte vector
+    (sizes around the 12-byte match limit and the 5-byte literal tail, runs,
+    255-run length extensions, random data); fast mode round-trips them."""
     g = gio.load("codec")
     for k in range(int(g["n_bytes_cases"])):
         raw = g[f"b{k}_in"].tobytes()
-        comp = codec.compress(raw)
-        if not raw:
-            assert comp == b""
-            continue
-        _check_block(comp, raw)
+        for exact in (True, False):
+            comp = codec.compress(raw, exact=exact)
+            if not raw:
+                assert comp == b""
+                continue
+            _check_block(comp, raw)
+            if exact:
+                assert comp == g[f"b{k}_lz4"].tobytes(), k
 
 
 @pytest.mark.parametrize("n", [12, 13, 17, 32767, 32768, 32769, 65536 + 5, 3 * 32768 + 7, 300001])
@@ -82,7 +95,8 @@ def test_lz4_chunk_boundaries(n):
     raw = b"".join(words[int(i)] for i in rng.integers(0, 40, n // 4 + 1))[:n]
     raw = raw[:n // 2] + b"\x00" * (n - n // 2)
     comp = codec.compress(raw)
-    _check_block(comp, raw)
+    assert comp == oracle.lz4_compress(raw)
+    _check_block(codec.compress(raw, exact=False), raw)
 
 
 @pytest.mark.parametrize("shift", [1, 2, 3])
@@ -95,9 +109,13 @@ def test_lz4_unaligned_source(shift):
     n = 4 * 32768 + 1001
     raw = b"".join(words[int(i)] for i in rng.integers(0, 40, n // 4 + 1))[:n]
     buf = dv.to_device(np.frombuffer(b"\x55" * shift + raw + b"\xaa" * 3, dtype=np.uint8))
-    dst, out_len = codec.compress_device(buf[shift:shift + n], n)
-    m = int(dv.to_host(out_len)[0])
-    _check_block(dv.to_host(dst[:m]).tobytes(), raw)
+    for exact in (True, False):
+        dst, out_len = codec.compress_device(buf[shift:shift + n], n, exact=exact)
+        m = int(dv.to_host(out_len)[0])
+        comp = dv.to_host(dst[:m]).tobytes()
+        _check_block(comp, raw)
+        if exact:
+            assert comp == oracle.lz4_compress(raw)
 
 
 def test_lz4_device_length_clamped_to_capacity():
@@ -108,9 +126,13 @@ def test_lz4_device_length_clamped_to_capacity():
     n_max = 65536 + 77
     src = dv.to_device(np.frombuffer(raw, dtype=np.uint8))
     n_dev = torch.tensor([len(raw) + 12345], dtype=torch.int64, device="cuda")
-    dst, out_len = codec.compress_device(src, n_max, n_dev)
-    m = int(dv.to_host(out_len)[0])
-    _check_block(dv.to_host(dst[:m]).tobytes(), raw[:n_max])
+    for exact in (True, False):
+        dst, out_len = codec.compress_device(src, n_max, n_dev, exact=exact)
+        m = int(dv.to_host(out_len)[0])
+        comp = dv.to_host(dst[:m]).tobytes()
+        _check_block(comp, raw[:n_max])
+        if exact:
+            assert comp == oracle.lz4_compress(raw[:n_max])
 
 
 def test_lz4_ratio_close_to_reference():
@@ -120,7 +142,7 @@ def test_lz4_ratio_close_to_reference():
         raw = g[f"b{k}_in"].tobytes()
         if len(raw) < 4096:
             continue
-        ours = len(codec.compress(raw))
+        ours = len(codec.compress(raw, exact=False))
         ref = len(g[f"b{k}_lz4"].tobytes())
         assert ours <= ref * 1.05 + 64, (k, ours, ref)
 
@@ -130,12 +152,14 @@ def test_compress_vdi_full_size(cfg):
     vol, tf, gcam, rcam, n_sg = synth.config(cfg)
     vdi, grid = vb.generate_vdi(vol, tf, gcam, vb.GenParams(n_sg=n_sg))
     comp, n = codec.compress_vdi(vdi, grid)
+    fast, n2 = codec.compress_vdi(vdi, grid, exact=False)
     cam = vdi.gen_camera
     ref_raw = oracle.encode_vdi(vdi.width, vdi.height, n_sg, vdi.counts, vdi.segs,
                                 (*cam.position, *cam.orientation, cam.fov_y, cam.near, cam.far),
                                 vdi.volume_aabb, grid.counts)
-    assert n == len(ref_raw)
-    assert oracle.lz4_decompress(comp, n) == ref_raw
+    assert n == len(ref_raw) and n2 == n
+    assert comp == oracle.lz4_compress(ref_raw)  # the reference's serial parse
+    assert oracle.lz4_decompress(fast, n) == ref_raw
     validate_vdi(vdi)
 
 

@@ -1,5 +1,6 @@
 """Time the device wire path on a config's VDI: VDI1 packing
-(vdi_encode_vdi1) and LZ4 (vdi_lz4_compress), device resident, CUDA events,
+(vdi_encode_vdi1) and LZ4 (vdi_lz4_compress, the chunk-parallel parse, and
+vdi_lz4_compress_exact, the reference's serial parse), device resident, CUDA events,
 median of --reps. Prints one JSON line with GB/s of raw VDI1 bytes, the
 compression ratio, and (with --cpu) the reference's serial compressor (the
 pinned C restatement of lz4.py:51-114, one core as in the reference) and the
@@ -48,13 +49,21 @@ def main():
     torch.cuda.synchronize()
     n = int(raw_len.item())
     enc_ms = timed(lambda: codec.encode_vdi_device(vdi, grid), a.reps)
-    comp, clen = codec.compress_device(raw, int(raw.numel()), raw_len)
+    comp, clen = codec.compress_device(raw, int(raw.numel()), raw_len, exact=False)
     torch.cuda.synchronize()
     m = int(clen.item())
-    lz_ms = timed(lambda: codec.compress_device(raw, int(raw.numel()), raw_len), a.reps)
+    lz_ms = timed(lambda: codec.compress_device(raw, int(raw.numel()), raw_len, exact=False),
+                  a.reps)
+    xcomp, xlen = codec.compress_device(raw, int(raw.numel()), raw_len, exact=True)
+    torch.cuda.synchronize()
+    mx = int(xlen.item())
+    lzx_ms = timed(lambda: codec.compress_device(raw, int(raw.numel()), raw_len, exact=True),
+                   max(1, a.reps // 2))
     line = {"tool": "bench_codec", "config": a.config, "raw_bytes": n, "lz4_bytes": m,
             "ratio": n / max(m, 1), "encode_ms": enc_ms, "encode_GBps": n / enc_ms / 1e6,
             "lz4_ms": lz_ms, "lz4_GBps": n / lz_ms / 1e6,
+            "lz4_exact": {"ms": lzx_ms, "bytes": mx, "ratio": n / max(mx, 1),
+                          "GBps": n / lzx_ms / 1e6},
             "counts_segs_read_bytes": 4 * vdi.width * vdi.height + 24 * (n - 160) // 26}
     if a.cpu:
         from oracle import oracle
@@ -66,6 +75,7 @@ def main():
                                 "ratio": n / max(len(ref), 1), "cores": 1, "kind": "port",
                                 "sample": "the whole VDI1 stream, reference serial parse"}
         assert oracle.lz4_decompress(dv.to_host(comp[:m]).tobytes(), n) == host
+        line["lz4_exact"]["equals_reference"] = dv.to_host(xcomp[:mx]).tobytes() == ref
     print(json.dumps(line), flush=True)
 
 
