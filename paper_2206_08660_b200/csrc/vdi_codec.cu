@@ -883,18 +883,34 @@ int lz4_compress(const uint8_t* src, size_t n_max, const unsigned long long* n_d
 // serial decision; the table then receives the positions up to it, the last
 // writer of a hash winning.
 //
-// The table lives in shared memory as 24-bit positions (a u16 and a u8
-// array, 192 KiB). A stored value e decodes, at position p, to
-// p - ((p - e) mod 2^24); candidates with that distance in [1, 65535] are the
-// reference's in-window candidates. Every 2^22 positions the table is swept
-// and entries more than 2^22 behind are reset to a value 2^23 behind, so no
-// distance ever wraps (a match longer than 2^21 bytes leaves every entry out
-// of the window, and the table is reset after it). The sequences go to a
-// list; a prefix sum of their encoded sizes places them, and one warp per
-// sequence writes them.
+// A serial parse is bound by the latency of its dependent reads, so all of
+// them are shared-memory reads (224 KiB):
+//  * the table: 17-bit positions (a u16 array and a bit array; a stored s
+//    decodes at position p to age (p - s) mod 2^17, and ages 1..65535 are
+//    the reference's in-window candidates) plus a valid bit per entry. A
+//    sweep every 32 Ki positions (and after a longer jump, with the jump
+//    added) drops entries 64 Ki or more behind -- out of the window, so the
+//    reference could not use them either -- so every valid age stays below
+//    2^17 and decodes exactly;
+//  * the input: a ring of 4 KiB segments holding the 64 KiB window behind
+//    the current segment, the segment and the next (candidates and the bytes
+//    a match extends over; beyond it -- long matches -- the bytes come from
+//    global memory).
+// Same-hash lanes of a batch are found with __match_any_sync only when a
+// cheap test says there may be some: each lane stores its lane id at a
+// 13-bit hash of its hash in a scratch table and reads it back; with no
+// other lane there, no lane shares its hash. (MATCH.ANY on 32 distinct keys
+// costs hundreds of cycles; two of the 32 16-bit hashes coincide in < 1 % of
+// batches, two 13-bit ones in ~6 %.)
+// The sequences go to a list; a prefix sum of their encoded sizes places
+// them, and one warp per sequence writes them.
 constexpr int kLzxHash = 16;
-constexpr unsigned kLzxMask = 0xffffffu;
-constexpr long long kLzxSweep = 1ll << 22;
+constexpr int kLzxSegLog = 12;
+constexpr int kLzxSeg = 1 << kLzxSegLog;  // ring segment bytes
+constexpr int kLzxSegs = 18;              // 64 KiB of window + the segment + the next
+constexpr int kLzxScratch = 8192;         // lane-collision scratch entries (u8)
+constexpr long long kLzxSweep = 32768;
+constexpr unsigned kLzxKeep = 65536;  // a sweep keeps entries younger than this (the window)
 
 struct LzxSeq {
   unsigned long long pos;     // match start (the final literal-only sequence: n)
@@ -912,54 +928,123 @@ constexpr int kLzxBlocks = 1184;  // emit blocks (8 per SM)
 
 __device__ __forceinline__ uint32_t lzx_hash(uint32_t v) { return (v * 2654435761u) >> 16; }
 
-__device__ __forceinline__ uint32_t window_load64(const uint8_t* s, long long n, long long i,
-                                                  int lane) {
-  const uint32_t* wb =
-      reinterpret_cast<const uint32_t*>(reinterpret_cast<uintptr_t>(s + i) & ~(uintptr_t)3);
-  return reinterpret_cast<const uint8_t*>(wb + lane) < s + n ? __ldg(wb + lane) : 0u;
+struct LzxSmem {
+  unsigned short* tab;  // [65536] position bits 0..15
+  uint32_t* hbits;      // [2048] position bit 16
+  uint32_t* vbits;      // [2048] valid
+  uint32_t* ring;       // [kLzxSeg * kLzxSegs / 4]
+  uint8_t* scratch;     // [kLzxScratch]
+};
+
+__device__ __forceinline__ uint32_t ring_word(const uint32_t* ring, long long q) {
+  const unsigned seg = (unsigned)(q >> kLzxSegLog);
+  return ring[(seg % kLzxSegs) * (kLzxSeg / 4) + (((unsigned)q & (kLzxSeg - 1)) >> 2)];
+}
+__device__ __forceinline__ uint32_t ring_rd32(const uint32_t* ring, long long p) {
+  const long long q = p & ~3ll;
+  return __funnelshift_r(ring_word(ring, q), ring_word(ring, q + 4), (unsigned)(p & 3) * 8);
 }
 
-__device__ __forceinline__ void lzx_reset(unsigned short* lo, uint8_t* hi, long long i,
-                                          bool keep_recent, int lane) {
-  const unsigned reset = (unsigned)((i - (1ll << 23)) & kLzxMask);
-  for (int k = lane; k < (1 << kLzxHash); k += 32) {
-    const unsigned e = lo[k] | ((unsigned)hi[k] << 16);
-    const unsigned d = ((unsigned)(i & kLzxMask) - e) & kLzxMask;
-    if (!keep_recent || d == 0 || d > (unsigned)kLzxSweep) {
-      lo[k] = (unsigned short)(reset & 0xffffu);
-      hi[k] = (uint8_t)(reset >> 16);
+// word q (4-aligned position) of the source, from the aligned words holding
+// it; words at or past the end read as 0 (a word holding a byte of the
+// buffer is mapped: allocations are aligned)
+__device__ __forceinline__ uint32_t src_word(const uint8_t* src, long long n, long long q) {
+  const uint8_t* a = src + q;
+  const uint32_t* w = reinterpret_cast<const uint32_t*>(reinterpret_cast<uintptr_t>(a) & ~(uintptr_t)3);
+  const unsigned sh = (unsigned)(reinterpret_cast<uintptr_t>(a) & 3) * 8;
+  const uint8_t* end = src + n;
+  const uint32_t lo = reinterpret_cast<const uint8_t*>(w) < end ? __ldg(w) : 0u;
+  if (!sh) return lo;
+  const uint32_t hi = reinterpret_cast<const uint8_t*>(w + 1) < end ? __ldg(w + 1) : 0u;
+  return __funnelshift_r(lo, hi, sh);
+}
+
+// Keep segments [seg(i) - 16, seg(i) + 2) in the ring (loaded: [seg_lo, seg_hi)).
+__device__ __forceinline__ void lzx_ensure(const LzxSmem& sm, const uint8_t* src, long long n,
+                                           long long i, long long& seg_lo, long long& seg_hi,
+                                           int lane) {
+  constexpr long long kBack = kLzxSegs - 2;
+  const long long cur = i >> kLzxSegLog;
+  const long long t_lo = cur - kBack > 0 ? cur - kBack : 0, t_hi = cur + 2;
+  if (seg_hi >= t_hi) return;
+  long long s0 = seg_hi > t_lo ? seg_hi : t_lo;
+  for (long long s = s0; s < t_hi; ++s) {
+    uint32_t* dst = sm.ring + (unsigned)(s % kLzxSegs) * (kLzxSeg / 4);
+    const long long base = s * kLzxSeg;
+#pragma unroll 8
+    for (int k = lane; k < kLzxSeg / 4; k += 32) dst[k] = src_word(src, n, base + 4ll * k);
+  }
+  seg_lo = t_lo;
+  seg_hi = t_hi;
+  __syncwarp();
+}
+
+// Drop entries whose age (relative to ref, plus extra) is >= kLzxKeep.
+__device__ __forceinline__ void lzx_sweep(const LzxSmem& sm, long long ref, long long extra,
+                                          int lane) {
+  const unsigned r17 = (unsigned)(ref & 0x1ffff);
+  for (int wd = lane; wd < (1 << kLzxHash) / 32; wd += 32) {
+    uint32_t bits = sm.vbits[wd];
+    const uint32_t hb = sm.hbits[wd];
+    uint32_t keep = bits;
+    while (bits) {
+      const int b = __ffs(bits) - 1;
+      bits &= bits - 1;
+      const unsigned s17 = sm.tab[wd * 32 + b] | (((hb >> b) & 1u) << 16);
+      const unsigned age = (r17 - s17) & 0x1ffffu;
+      if ((long long)age + extra >= (long long)kLzxKeep) keep &= ~(1u << b);
     }
+    sm.vbits[wd] = keep;
   }
   __syncwarp();
 }
 
+__device__ __forceinline__ void lzx_insert(const LzxSmem& sm, uint32_t h, long long p) {
+  sm.tab[h] = (unsigned short)(p & 0xffff);
+  const uint32_t bit = 1u << (h & 31);
+  if ((p >> 16) & 1) atomicOr(sm.hbits + (h >> 5), bit);
+  else atomicAnd(sm.hbits + (h >> 5), ~bit);
+  atomicOr(sm.vbits + (h >> 5), bit);
+}
+
 __global__ void __launch_bounds__(32) lzx_parse_kernel(const uint8_t* __restrict__ src, LzxWs ws) {
-  extern __shared__ unsigned short x_lo[];
-  uint8_t* x_hi = reinterpret_cast<uint8_t*>(x_lo + (1 << kLzxHash));
+  extern __shared__ uint32_t x_smem[];
+  LzxSmem sm;
+  sm.tab = reinterpret_cast<unsigned short*>(x_smem);
+  sm.hbits = x_smem + (1 << kLzxHash) / 2;
+  sm.vbits = sm.hbits + (1 << kLzxHash) / 32;
+  sm.ring = sm.vbits + (1 << kLzxHash) / 32;
+  sm.scratch = reinterpret_cast<uint8_t*>(sm.ring + kLzxSeg * kLzxSegs / 4);
   const int lane = threadIdx.x;
   const long long n = (long long)ws.n_dev[0];
-  lzx_reset(x_lo, x_hi, 0, false, lane);
+  for (int k = lane; k < (1 << kLzxHash) / 32; k += 32) sm.vbits[k] = sm.hbits[k] = 0u;
+  long long seg_lo = 0, seg_hi = 0;
+  lzx_ensure(sm, src, n, 0, seg_lo, seg_hi, lane);
   const long long limit = n - 12;  // lz4.py:62 (MFLIMIT)
-  const int o = (int)(reinterpret_cast<uintptr_t>(src) & 3);
   long long i = 0, anchor = 0, next_sweep = kLzxSweep;
   unsigned long long nseq = 0;
-  uint32_t wl = window_load64(src, n, 0, lane), w1 = window_load64(src, n, 32, lane);
   while (i < limit) {
     if (i >= next_sweep) {
-      lzx_reset(x_lo, x_hi, i, true, lane);
+      lzx_sweep(sm, i, 0, lane);
       next_sweep = i + kLzxSweep;
     }
-    const uint32_t w2 = window_load64(src, n, i + 64, lane);
+    lzx_ensure(sm, src, n, i, seg_lo, seg_hi, lane);
     const long long p = i + lane;
     const bool valid = p < limit;
-    const uint32_t v = window_value(wl, (o + (int)(i & 3)) & 3, lane);
+    const uint32_t v = ring_rd32(sm.ring, p);
     const uint32_t h = lzx_hash(v);
-    const unsigned e = valid ? (x_lo[h] | ((unsigned)x_hi[h] << 16)) : 0u;
-    const unsigned d = ((unsigned)(p & kLzxMask) - e) & kLzxMask;
-    const long long tc = valid && d != 0u && d <= 65535u ? p - (long long)d : -1;
-    const uint32_t tv = tc >= 0 ? rd32(src, tc) : ~v;
+    const unsigned st = sm.tab[h] | (((sm.hbits[h >> 5] >> (h & 31)) & 1u) << 16);
+    const bool vb = valid && ((sm.vbits[h >> 5] >> (h & 31)) & 1u);
+    const unsigned age = ((unsigned)(p & 0x1ffff) - st) & 0x1ffffu;
+    const long long tc = vb && age != 0u && age <= 65535u ? p - (long long)age : -1;
+    const uint32_t tv = tc >= 0 ? ring_rd32(sm.ring, tc) : ~v;
     const unsigned key = valid ? h : (0x10000u + lane);
-    const unsigned peers = __match_any_sync(0xffffffffu, key);
+    const unsigned sk = key & (kLzxScratch - 1);
+    sm.scratch[sk] = (uint8_t)lane;
+    __syncwarp();
+    const bool alone = sm.scratch[sk] == (uint8_t)lane;
+    const unsigned peers =
+        __all_sync(0xffffffffu, alone) ? (1u << lane) : __match_any_sync(0xffffffffu, key);
     const unsigned lt = (1u << lane) - 1u;
     const unsigned lower = peers & lt;
     const int pl = lower ? 31 - __clz(lower) : lane;
@@ -970,26 +1055,31 @@ __global__ void __launch_bounds__(32) lzx_parse_kernel(const uint8_t* __restrict
     const int w = mm ? __ffs(mm) - 1 : 31;
     const unsigned upto = w == 31 ? 0xffffffffu : ((2u << w) - 1u);
     __syncwarp();
-    if (valid && ((1u << lane) & upto) && !(peers & upto & ~lt & ~(1u << lane))) {
-      const unsigned pe = (unsigned)(p & kLzxMask);
-      x_lo[h] = (unsigned short)(pe & 0xffffu);
-      x_hi[h] = (uint8_t)(pe >> 16);
-    }
+    if (valid && ((1u << lane) & upto) && !(peers & upto & ~lt & ~(1u << lane)))
+      lzx_insert(sm, h, p);
     __syncwarp();
     if (!mm) {
       i += 32;
-      wl = w1;
-      w1 = w2;
       continue;
     }
     const long long pw = i + w;
     const long long cw = __shfl_sync(0xffffffffu, cand, w);
-    // extend (lz4.py:66-69), 32 bytes per step
+    // extend (lz4.py:66-69), 32 bytes per step; bytes past the ring's
+    // lookahead (long matches) come from global memory
     long long mlen = 4;
     const long long mmax = n - 5 - pw;
+    const long long hi_b = seg_hi * kLzxSeg;
     while (true) {
       const long long k = mlen + lane;
-      const bool stop = k >= mmax || src[cw + k] != src[pw + k];
+      bool stop = k >= mmax;
+      if (!stop) {
+        const long long xa = cw + k, xb = pw + k;
+        const unsigned ba = xa < hi_b ? (ring_word(sm.ring, xa & ~3ll) >> ((xa & 3) * 8)) & 0xffu
+                                      : (unsigned)src[xa];
+        const unsigned bb = xb < hi_b ? (ring_word(sm.ring, xb & ~3ll) >> ((xb & 3) * 8)) & 0xffu
+                                      : (unsigned)src[xb];
+        stop = ba != bb;
+      }
       const unsigned sbits = __ballot_sync(0xffffffffu, stop);
       if (sbits) {
         mlen += __ffs(sbits) - 1;
@@ -1003,19 +1093,15 @@ __global__ void __launch_bounds__(32) lzx_parse_kernel(const uint8_t* __restrict
     nseq += 1;
     i = pw + mlen;
     anchor = i;
-    if (mlen > (1ll << 21)) {  // every entry is now out of the window
-      lzx_reset(x_lo, x_hi, i, false, lane);
+    if (i >= next_sweep) {  // ages are exact relative to pw (the last insert)
+      lzx_sweep(sm, pw, i - pw, lane);
       next_sweep = i + kLzxSweep;
     }
-    if (i < limit && lane == 0) {
-      const unsigned pe = (unsigned)((i - 2) & kLzxMask);
-      const uint32_t hh = lzx_hash(rd32(src, i - 2));
-      x_lo[hh] = (unsigned short)(pe & 0xffffu);
-      x_hi[hh] = (uint8_t)(pe >> 16);
+    if (i < limit) {
+      lzx_ensure(sm, src, n, i, seg_lo, seg_hi, lane);
+      if (lane == 0) lzx_insert(sm, lzx_hash(ring_rd32(sm.ring, i - 2)), i - 2);
     }
     __syncwarp();
-    wl = window_load64(src, n, i, lane);
-    w1 = window_load64(src, n, i + 32, lane);
   }
   if (lane == 0) {
     if (n > 0) {
@@ -1149,7 +1235,9 @@ int lzx_compress(const uint8_t* src, size_t n_max, const unsigned long long* n_d
   off += align256(sizeof(LzxSeq) * (n_max / 4 + 2));
   ws.bsum = reinterpret_cast<unsigned long long*>(w + off);
   set_u64_kernel<<<1, 1, 0, stream>>>(ws.n_dev, n_dev, n_max, 0ull);
-  const size_t smem = (sizeof(unsigned short) + 1) * ((size_t)1 << kLzxHash);
+  const size_t smem = sizeof(unsigned short) * ((size_t)1 << kLzxHash) +
+                      2 * sizeof(uint32_t) * ((size_t)1 << kLzxHash) / 32 +
+                      (size_t)kLzxSeg * kLzxSegs + kLzxScratch;
   cudaError_t err =
       cudaFuncSetAttribute(lzx_parse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (err != cudaSuccess) return set_error(VDI_ELAUNCH, "lz4x smem: %s", cudaGetErrorString(err));
