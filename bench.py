@@ -45,6 +45,9 @@ def parse():
                    help="target CPU time of the bounded cpu_baseline sample")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--e2e-steps", type=int, default=8)
+    p.add_argument("--bricked", action="store_true",
+                   help="C5 placement: contiguous generation bands, each rank keeping only "
+                        "its voxel box resident (shard.band_volume_box)")
     return p.parse_args()
 
 
@@ -62,6 +65,25 @@ def peaks():
         return float(d["hbm_gbs"]), "measured"
     except Exception:
         return 6650.0, "fallback"
+
+
+def host_info(threads):
+    """CPU model and threading layer of the CPU legs."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"cpu_model": model, "threads": threads, "os_cpu_count": os.cpu_count(),
+            "threading_layer": "OpenMP (libgomp), rows split across threads",
+            "arm": "oracle/vdi_oracle.c, the C restatement of vdikit's numba kernels "
+                   "(bit-identical outputs); on C2 it runs generation in 1.34 s against "
+                   "the reference's own numba 7.25 s on 8 threads, so it is a faster "
+                   "(conservative) baseline than vdikit itself"}
 
 
 # ------------------------------------------------------------------ clocks
@@ -120,16 +142,17 @@ class ClockSampler:
 
 # ---------------------------------------------------------------- workload
 
-def gen_traffic(config):
-    """DRAM bytes (read + write) of one generation launch from the committed ncu
-    capture of the same workload (profiles/*_gen_traffic.json), or None."""
+def kernel_metrics(config):
+    """Per-kernel ncu metrics of one step of this workload, from the committed
+    capture (profiles/*_<config>_kernel_metrics.json, tools/ncu_metrics_json.py):
+    actual DRAM bytes, FP64 pipe utilisation, warp execution efficiency."""
     import glob
-    files = sorted(glob.glob(os.path.join(ROOT, "profiles", f"*_{config.lower()}_gen_traffic.json")))
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles",
+                                          f"*_{config.lower()}_kernel_metrics.json")))
     if not files:
         return None, None
     with open(files[-1]) as f:
-        d = json.load(f)
-    return float(d["gen_dram_bytes_per_launch"]), os.path.relpath(files[-1], ROOT)
+        return json.load(f), os.path.relpath(files[-1], ROOT)
 
 
 def workload(name):
@@ -150,16 +173,17 @@ def cpu_time_sample(vol, tf, gcam, rcam, n_sg, vdi_counts, vdi_segs, grid, rows,
     params = GenParams(n_sg=n_sg)
     delta, step, lref = params.resolve(vol)
     w, h = gcam.viewport
-    norm = vol.normalized
+    norm = vol.data if vol.voxel_type == "u8" else vol.normalized  # (normalised exactly)
     t0 = time.perf_counter()
-    oracle.generate(norm, tf.lut, gcam.proj_view(), gcam.inv_proj_view(),
-                    np.asarray(gcam.position), vol.aabb, w, h, n_sg, delta, params.epsilon,
-                    params.gamma_init, step, lref, rows=rows, threads=threads)
+    g = oracle.generate(norm, tf.lut, gcam.proj_view(), gcam.inv_proj_view(),
+                        np.asarray(gcam.position), vol.aabb, w, h, n_sg, delta, params.epsilon,
+                        params.gamma_init, step, lref, rows=rows, threads=threads, compact=True)
     t1 = time.perf_counter()
-    oracle.render(vdi_segs, vdi_counts, gcam.proj_view(), gcam.inv_proj_view(), vol.aabb,
-                  rcam.inv_proj_view(), np.asarray(rcam.position), *rcam.viewport, grid,
-                  gcam.near, gcam.far, rows=rows, threads=threads)
+    r = oracle.render(vdi_segs, vdi_counts, gcam.proj_view(), gcam.inv_proj_view(), vol.aabb,
+                      rcam.inv_proj_view(), np.asarray(rcam.position), *rcam.viewport, grid,
+                      gcam.near, gcam.far, rows=rows, threads=threads)
     t2 = time.perf_counter()
+    cpu_time_sample.last = (g, r)  # the outputs, for the parity block
     return t1 - t0, t2 - t1
 
 
@@ -184,7 +208,8 @@ def run_reference(args):
     params = GenParams(n_sg=n_sg)
     delta, step, lref = params.resolve(vol)
     # untimed setup: the full VDI the sampled render rows traverse
-    ref = oracle.generate(vol.normalized, tf.lut, gcam.proj_view(), gcam.inv_proj_view(),
+    src = vol.data if vol.voxel_type == "u8" else vol.normalized
+    ref = oracle.generate(src, tf.lut, gcam.proj_view(), gcam.inv_proj_view(),
                           np.asarray(gcam.position), vol.aabb, w, h, n_sg, delta,
                           params.epsilon, params.gamma_init, step, lref, threads=threads)
     from paper_2206_08660_b200.vdi import default_grid_dims
@@ -209,9 +234,9 @@ def run_reference(args):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": config_dict(args, gcam, n_sg, "oracle port (C, OpenMP) of vdikit kernels"),
+        "config": config_dict(args, gcam, n_sg),
         "cpu_baseline": {"value": value, "unit": "Mrays/s", "cores": threads, "kind": "port",
-                         "sample": sample},
+                         "sample": sample, "host": host_info(threads)},
         "e2e": {"value": value, "unit": "Mrays/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -223,19 +248,18 @@ DESCRIBE = {
     "C2": "256^3 f32 Gaussian blobs",
     "C3": "Kingsnake-shaped 1024x1024x795 u8",
     "C4": "Rayleigh-Taylor-shaped 1024^3 f32",
+    "C5": "Richtmyer-Meshkov-shaped 2048x2048x1920 u8",
 }
 
 
-def config_dict(args, gcam, n_sg, note=None):
+def config_dict(args, gcam, n_sg):
     w, h = gcam.viewport
-    d = {"workload": f"{args.config}: {DESCRIBE.get(args.config, args.config)}, {w}x{h}, "
-                     f"n_sg {n_sg}, generate @0deg + render @15deg",
-         "rays_per_step": 2 * w * h, "viewport": [w, h], "n_sg": n_sg,
-         "parallelism": f"ray-band shard x{args.gpus}",
-         "l2": "256 MiB L2-flush write between timed steps"}
-    if note:
-        d["note"] = note
-    return d
+    par = (f"bricked: contiguous generation bands + resident voxel boxes x{args.gpus}"
+           if args.bricked else f"ray-band shard x{args.gpus}")
+    return {"workload": f"{args.config}: {DESCRIBE.get(args.config, args.config)}, {w}x{h}, "
+                        f"n_sg {n_sg}, generate @0deg + render @15deg",
+            "rays_per_step": 2 * w * h, "viewport": [w, h], "n_sg": n_sg,
+            "parallelism": par, "l2": "256 MiB L2-flush write between timed steps"}
 
 
 # --------------------------------------------------------------------- B200
@@ -263,7 +287,12 @@ def run_b200(args):
     vol, tf, gcam, rcam, n_sg = workload(args.config)
     params = GenParams(n_sg=n_sg)
     w, h = gcam.viewport
-    pipe = shard.Pipeline(vol, tf, gcam, rcam, params, world=world, rank=rank)
+    box_volume = None
+    if args.config == "C5" and args.bricked:
+        from paper_2206_08660_b200 import synth
+        box_volume = lambda org, size: synth.rm_like(box=(org, size)).device_data  # noqa: E731
+    pipe = shard.Pipeline(vol, tf, gcam, rcam, params, world=world, rank=rank,
+                          bricked=args.bricked and world > 1, box_volume=box_volume)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device="cuda")
 
     def barrier():
@@ -313,12 +342,32 @@ def run_b200(args):
     ren_gbs = b_ren / (r_ms * 1e-3) / 1e9
     dominant = "vdi_gen" if g_ms >= r_ms else "vdi_render"
     ach = gen_gbs if dominant == "vdi_gen" else ren_gbs
-    # the committed ncu capture is of the full-frame (N=1) generation
-    traffic, traffic_src = (gen_traffic(args.config) if dominant == "vdi_gen" and world == 1
-                            else (None, None))
+    # the committed ncu capture is of the full-frame (N=1) step
+    km, km_src = kernel_metrics(args.config) if world == 1 else (None, None)
+    traffic = None
+    ncu = None
+    if km is not None:
+        ks = km["kernels"]
+        traffic = (km["gen_dram_bytes"] if dominant == "vdi_gen"
+                   else ks.get("render_kernel", {}).get("dram_bytes"))
+        ncu = {"source": km_src, "commit": km.get("commit"),
+               "dram_frac": (traffic / ((g_ms if dominant == "vdi_gen" else r_ms) * 1e-3)
+                             / (peak * 1e9)) if traffic else None,
+               "phases": {k: {"ms_ncu": round(v["ms"], 4),
+                              "dram_GB": round(v["dram_bytes"] / 1e9, 3),
+                              "dram_GBps": round(v["dram_GBps"], 1),
+                              "fp64_pipe_pct": round(v["fp64_pipe_pct"], 1),
+                              "warp_exec_eff": round(v["warp_exec_efficiency"], 3),
+                              "l2_hit_pct": round(v["l2_hit_pct"], 1)}
+                          for k, v in ks.items() if v["ms"] > 0.05},
+               "binding": "generation: FP64 dependency latency + issue at 16-20 warps/SM "
+                          "(fp64 pipe 20-36 %, dram 5-60 % per phase); render: latency of "
+                          "its per-list shading chains (dram ~3 %)"}
     roof = {"kernel": dominant, "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
             "frac": ach / peak, "peak_kind": peak_kind, "traffic": traffic,
-            "traffic_source": traffic_src,
+            "traffic_note": "actual DRAM bytes of the generation phases (ncu, one step); "
+                            "achieved/frac use the algorithmic bytes of SURVEY 8(d)",
+            "ncu": ncu,
             "algorithmic_bytes": b_gen if dominant == "vdi_gen" else b_ren,
             "gen": {"ms": g_ms, "bytes": b_gen, "GBps": gen_gbs, "frac": gen_gbs / peak,
                     "samples": S, "Gsamples_per_s": S / (g_ms * 1e-3) / 1e9},
@@ -329,9 +378,15 @@ def run_b200(args):
     # headline: the VDI comes back in the reference's VDI1 wire format
     # (encode_vdi bytes, packed on the device); "dense" reads back the full
     # (H, W, n_sg, 6) array instead, "serial" is one frame at a time
-    e2e = pipe.e2e_stream(args.e2e_steps, packed=True)
-    e2e["dense"] = pipe.e2e_stream(args.e2e_steps)
-    e2e["serial"] = pipe.e2e(min(args.e2e_steps, 3))
+    if args.bricked and world > 1:
+        e2e = {"value": None, "unit": "Mrays/s", "h2d_bytes_per_step": None,
+               "d2h_bytes_per_step": None,
+               "note": "bricked placement: each rank holds only its voxel box; the "
+                       "host-volume e2e path streams whole volumes (not built for boxes)"}
+    else:
+        e2e = pipe.e2e_stream(args.e2e_steps, packed=True)
+        e2e["dense"] = pipe.e2e_stream(args.e2e_steps)
+        e2e["serial"] = pipe.e2e(min(args.e2e_steps, 3))
 
     line = None
     if rank == 0:
@@ -349,7 +404,8 @@ def run_b200(args):
             "gpu_launches": pipe.launches_per_step * args.steps,
         }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = pipe_cpu_baseline(vol, tf, gcam, rcam, n_sg, pipe, args)
+        line["cpu_baseline"], line["parity"] = pipe_cpu_baseline(vol, tf, gcam, rcam, n_sg,
+                                                                 pipe, args)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -358,17 +414,40 @@ def run_b200(args):
 
 
 def pipe_cpu_baseline(vol, tf, gcam, rcam, n_sg, pipe, args):
+    """The oracle on evenly spaced rows of both passes (timed), and the parity
+    of those rows: the oracle's generation against the B200's, and the
+    oracle's render of the B200's VDI against the B200's render (image and
+    per-pixel counters)."""
+    from oracle import parity
     threads = os.cpu_count() or 1
     counts, segs, grid = pipe.host_vdi()
     w, h = gcam.viewport
     rows = calibrated_rows(vol, tf, gcam, rcam, n_sg, counts, segs, grid, threads,
                            args.cpu_seconds, h)
     tg, tr = cpu_time_sample(vol, tf, gcam, rcam, n_sg, counts, segs, grid, rows, threads)
+    g_ref, r_ref = cpu_time_sample.last
     rays = 2 * len(rows) * w
+    img, lv, si, ls = pipe.render_per_pixel()
+    gp = parity.generation(g_ref, counts[rows], segs[rows],
+                           pipe.bufs.passes.cpu().numpy()[rows],
+                           pipe.bufs.samples.cpu().numpy()[rows],
+                           pipe.bufs.gammas.cpu().numpy()[rows])
+    rp = parity.render(r_ref, img, lv, si, ls, rows=rows)
+    par = {"rows": int(len(rows)), "of": int(h),
+           "counts_equal_frac": gp["counts_equal_frac"], "segs_bit_exact": gp["segs_bit_exact"],
+           "max_depth_diff": gp["max_depth_diff"], "max_seg_rgba_diff": gp["max_rgba_diff"],
+           "passes_samples_gammas_equal": bool(gp["passes_equal"] and gp["samples_equal"]
+                                               and gp["gammas_bit_exact"]),
+           "max_rgba_diff": rp["max_rgba_diff"], "counters_equal": rp["counters_equal"],
+           "ok": bool(gp["ok"] and rp["ok"]),
+           "note": "oracle generation vs B200 generation on these rows; oracle render of "
+                   "the B200 VDI vs the B200 render on these rows (full-frame parity: "
+                   "tests/test_gpu_full_c3.py)"}
     return {"value": rays / (tg + tr) / 1e6, "unit": "Mrays/s", "cores": threads,
             "kind": "port",
             "sample": f"{len(rows)} of {h} evenly spaced rows of both passes "
-                      f"(gen {tg:.2f} s + render {tr:.2f} s)"}
+                      f"(gen {tg:.2f} s + render {tr:.2f} s)",
+            "host": host_info(threads)}, par
 
 
 def main():

@@ -117,6 +117,22 @@ def band_volume_box(vol, cam, row0: int, row1: int, margin: int = 2, align: int 
     return tuple(int(v) for v in org), tuple(int(v) for v in end - org)
 
 
+def brick_slabs(nz: int, world: int, log2: int = 3):
+    """Brick z-planes per rank for the sharded brick maxima: rank r computes
+    planes [r P, min((r + 1) P, nbz)) with P = ceil(nbz / world), from voxel
+    planes [8 r P, min(8 (r + 1) P + 1, nz)) (the +1: a brick's trilinear
+    halo). Returns (P, nbz, [(z0, z1, planes)] per rank)."""
+    b = 1 << log2
+    nbz = -(-nz // b)
+    per = -(-nbz // world)
+    out = []
+    for r in range(world):
+        p0, p1 = min(r * per, nbz), min((r + 1) * per, nbz)
+        z0, z1 = p0 * b, min(p1 * b + 1, nz)
+        out.append((z0, z1, p1 - p0))
+    return per, nbz, out
+
+
 class PackedExchange:
     """The VDI exchange as packed VDI1 shards instead of the padded list-SoA:
     each rank packs its rows (vdi_encode_vdi1: counts u16 + valid
@@ -141,6 +157,9 @@ class PackedExchange:
         self.enc_ws = t.empty(ws, dtype=t.uint8, device="cuda")
         self.dec_ws = t.empty(ws, dtype=t.uint8, device="cuda")
         self.dummy_grid = t.zeros(1, dtype=t.int32, device="cuda")
+        # the gather buffer at full capacity, allocated once (each frame
+        # gathers world x max(lens) bytes into its head)
+        self.g_buf = t.empty(pipe.world * self.cap, dtype=t.uint8, device="cuda")
         a = _capi.VdiEncodeArgs()
         a.segs, a.counts, a.grid = (dv.ptr(pipe.bufs.segs), dv.ptr(pipe.bufs.counts),
                                     dv.ptr(self.dummy_grid))
@@ -156,15 +175,17 @@ class PackedExchange:
         self.bytes_last = 0
 
     def __call__(self, dist, grid, g_counts, g_segs):
-        t = dv.torch()
         L = _capi.load()
         p = self.pipe
         dist.all_reduce(grid)
         _capi.check(L.vdi_encode_vdi1(self.args, dv.stream_handle()))
         dist.all_gather_into_tensor(self.lens, self.len)
-        lens = self.lens.cpu().tolist()  # sizes the gather (one small host sync)
+        # the gather is sized by the longest shard: one 8-byte-per-rank host
+        # read (NCCL sizes are host values). exchange_vdi is the sync-free
+        # alternative (the padded list-SoA, 5.4x the bytes at C3).
+        lens = self.lens.cpu().tolist()
         m = int(max(lens))
-        g_buf = t.empty(p.world * m, dtype=t.uint8, device="cuda")
+        g_buf = self.g_buf[:p.world * m]
         dist.all_gather_into_tensor(g_buf, self.buf[:m])
         w, rows, n_sg = p.w, p.gen_rows, p.params.n_sg
         stride = g_segs.shape[1]
@@ -242,8 +263,27 @@ class Pipeline:
         # step (a new timestep's volume needs new ones): brick maxima for
         # empty-space skipping and, when they fit, the corner records
         self.bricks = dv.alloc_bricks(self.vol_dev, self.res_dims)
+        # corner records save ~8 % of a full generation but cost a full-volume
+        # pass on every rank; with more than two ranks sharing the rays they
+        # cost more than they save (C3: 0.93 ms vs 2.5 ms / N), so only N <= 2
+        # builds them
         self.cells = (dv.alloc_cells(self.vt, self.res_dims)
-                      if dv.use_cells(self.vt, self.res_dims) else None)
+                      if dv.use_cells(self.vt, self.res_dims) and world <= 2 else None)
+        # N > 1 (replicated volume): each rank computes a z-slab of the brick
+        # maxima and the ranks all-gather them (1.6 MB at C3)
+        self.slabs = None
+        if world > 1 and not bricked:
+            per, nbz, plan = brick_slabs(int(vol.dims[2]), world, dv.BRICK_LOG2)
+            nby, nbx = self.bricks.shape[1], self.bricks.shape[2]
+            self.bricks_all = t.empty((world * per, nby, nbx), dtype=self.bricks.dtype,
+                                      device="cuda")
+            self.bricks = self.bricks_all[:nbz]
+            z0, z1, planes = plan[rank]
+            self.slab_local = t.zeros((per, nby, nbx), dtype=self.bricks.dtype, device="cuda")
+            self.slab_tmp = (t.empty((-(-(z1 - z0) // (1 << dv.BRICK_LOG2)), nby, nbx),
+                                     dtype=self.bricks.dtype, device="cuda")
+                             if z1 > z0 else None)
+            self.slabs = (z0, z1, planes)
         self.ess_max = dv.ess_threshold(tf.lut)
         self.aabb = np.asarray(vol.aabb, np.float64)
         self.band = (BAND_ROWS, world, rank)
@@ -295,9 +335,7 @@ class Pipeline:
         if timed:
             ev[0].record()
         self.sums.zero_()
-        dv.launch_bricks(vol_dev, self.vt, self.res_dims, self.bricks)
-        if self.cells is not None:
-            dv.launch_cells(vol_dev, self.vt, self.res_dims, self.cells, self.bricks, self.ess_max)
+        self.prep(vol_dev)
         launch_generate(vol_dev, self.vt, self.vol.dims, self.lut_dev, self.gcam,
                         self.aabb, self.params, self.resolved, self.bufs, self.grid_dims,
                         band=self.gen_band, split_events=ev, bricks=self.bricks,
@@ -331,13 +369,41 @@ class Pipeline:
                 "collective": ev[3].elapsed_time(ev[4]) + ev[5].elapsed_time(end),
                 "render": ev[4].elapsed_time(ev[5])}
 
-    def generate_only(self, vol_dev=None):
+    def prep(self, vol_dev, gather: bool = True):
+        """Per-volume acceleration data: brick maxima (sharded by z-slab and
+        all-gathered when N > 1 with a replicated volume) and, for N <= 2,
+        the corner records. gather=False leaves the other ranks' slabs as
+        they are (one-GPU timing of a rank's share)."""
+        if self.slabs is None:
+            dv.launch_bricks(vol_dev, self.vt, self.res_dims, self.bricks)
+        else:
+            z0, z1, planes = self.slabs
+            nx, ny = int(self.res_dims[0]), int(self.res_dims[1])
+            if planes > 0:
+                dv.launch_bricks(vol_dev[z0:z1], self.vt, (nx, ny, z1 - z0), self.slab_tmp)
+                self.slab_local[:planes].copy_(self.slab_tmp[:planes])
+            if gather:
+                self.dist.all_gather_into_tensor(self.bricks_all, self.slab_local)
+        if self.cells is not None:
+            dv.launch_cells(vol_dev, self.vt, self.res_dims, self.cells, self.bricks, self.ess_max)
+
+    def render_per_pixel(self):
+        """This rank's render again, with per-pixel counters (untimed):
+        host (image, lists_visited, segs_intersected, lists_searched)."""
+        t = self.t
+        pp = [t.empty((self.out_rows, self.ow), dtype=t.int32, device="cuda") for _ in range(3)]
+        a = render_args(self.dvdi, self.params.n_sg, self.w, self.h, self.gcam, self.aabb,
+                        self.bufs.grid, self.grid_dims, self.gcam.near, self.gcam.far,
+                        self.rcam, self.opts, self.image, per_pixel=pp, band=self.band)
+        launch_zmask(a, self.zmask)
+        _capi.check(_capi.load().vdi_render_launch(a, dv.stream_handle()))
+        return (dv.to_host(self.image),) + tuple(dv.to_host(x) for x in pp)
+
+    def generate_only(self, vol_dev=None, gather: bool = True):
         """This rank's volume prep + generation + partial grid (no exchange,
         no render), on the current stream."""
         vol_dev = self.vol_dev if vol_dev is None else vol_dev
-        dv.launch_bricks(vol_dev, self.vt, self.res_dims, self.bricks)
-        if self.cells is not None:
-            dv.launch_cells(vol_dev, self.vt, self.res_dims, self.cells, self.bricks, self.ess_max)
+        self.prep(vol_dev, gather)
         launch_generate(vol_dev, self.vt, self.vol.dims, self.lut_dev, self.gcam,
                         self.aabb, self.params, self.resolved, self.bufs, self.grid_dims,
                         band=self.gen_band, bricks=self.bricks, ess_max=self.ess_max,

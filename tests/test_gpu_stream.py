@@ -82,3 +82,37 @@ def test_stream_packed_vdi1_matches_encode_vdi():
         assert np.array_equal(r.image[:im.shape[0]], im)
 
     assert fs.run([hosts[i] for i in order], on_result=check) == len(order)
+
+
+@pytest.mark.parametrize("packed", [False, True])
+def test_stream_in_flight_limit(packed):
+    """At most two frames in flight: a third submit before a collect raises
+    (its slots would overwrite the oldest frame's results), and a collect
+    with nothing in flight raises; the two frames in flight stay correct."""
+    vol, tf, gcam, rcam, n_sg = synth.config("C1")
+    params = vb.GenParams(n_sg=n_sg)
+    vdi, grid = vb.generate_vdi(vol, tf, gcam, params)
+    pipe = shard.Pipeline(vol, tf, gcam, rcam, params)
+    fs = FrameStream(pipe, packed=packed)
+    h = dv.pinned_numpy(vol.data.shape, vol.data.dtype)
+    h[...] = vol.data
+    fs.submit(h)
+    fs.submit(h)
+    with pytest.raises(RuntimeError):
+        fs.submit(h)
+    for _ in range(2):
+        r = fs.collect()
+        c = r.decode()[0] if packed else r.counts
+        assert np.array_equal(c, vdi.counts)
+    with pytest.raises(RuntimeError):
+        fs.collect()
+
+
+def test_stream_rejects_bricked_pipeline():
+    vol, tf, gcam, rcam, n_sg = synth.config("C1")
+    pipe = shard.Pipeline(vol, tf, gcam, rcam, vb.GenParams(n_sg=n_sg), world=2, rank=0,
+                          bricked=True)
+    with pytest.raises(NotImplementedError):
+        FrameStream(pipe)
+    with pytest.raises(NotImplementedError):
+        pipe.e2e(1)
