@@ -68,6 +68,7 @@ constexpr int kGenThreads = 128;
 #define VDI_EMIT_MINB 6  // 80 registers: 6 blocks/SM (measured: 6.16 -> 5.64 ms at C3)
 #endif
 constexpr int kRounds = 3;
+constexpr long long kWideRays = 700000;  // launches below this many rays use the wide hand-off
 
 enum PassMode : int { kCount = 0, kCapped = 1, kRedo = 2 };
 
@@ -84,6 +85,9 @@ struct RayRec {
   int passes;       // passes so far (R semantics)
   int mode_final;   // kCount (window hit / cached high) or kCapped
   int pad;
+  // bisection state handed from a narrow replay lane to the wide phase
+  double low, high;
+  int last_n, high_n;
 };
 
 // Cache entry of a non-transparent sample: the classified f32 RGBA, with the
@@ -100,7 +104,8 @@ struct RoundCtl {
   unsigned long long ndefer;    // rays deferred to the next round
   unsigned long long efetch;    // emit-phase pool
   unsigned long long ffetch;    // fill-phase pool (one ray per warp)
-  unsigned long long pad[1];
+  unsigned long long nwide;     // rays handed to the wide bisect phase
+  unsigned long long wfetch;    // wide-phase pool (one ray per warp)
   // bisection decisions seen so far in this round, per level: [0] up, [1] down
   // (the bisect replays' learned speculation direction)
   unsigned dir[2][32];
@@ -133,6 +138,8 @@ struct GenConst {
   long long sub_sx, sub_sy, sub_voff, sub_boff;
   int sub_ox, sub_oy, sub_oz, sub_nx, sub_ny, sub_nz;
   unsigned* sub_oob;
+  int* wide;         // rays handed to the wide bisect phase (record indices)
+  int wide_after;    // replays a narrow lane runs on one ray before handing it off
   int chain_levels;  // bisect replays starting below this level use the down-chain shape
   int learn;         // learned chain directions at the later levels 
 };
@@ -918,6 +925,7 @@ __global__ void __launch_bounds__(kThreads, kMinB) gen_bisect_kernel(const GenCo
   double low = 0.0, high = 0.0;
   int last_n = 0, high_n = 0, passes = 0, samples = 0;
   bool chain = false;  // this replay's speculation shape (see the top of the loop)
+  int reps = 0;        // replays run on the current ray
   int cdir = 0;        // chain directions (bit i set: step i goes up)
   // No-split certificate: state 0 (this replay's largest gamma) records the
   // largest d^2 its split test saw and whether it split. With no split, its
@@ -948,6 +956,7 @@ __global__ void __launch_bounds__(kThreads, kMinB) gen_bisect_kernel(const GenCo
           samples = rec->samples;
           have = true;
           top = true;
+          reps = 0;
         }
       }
     }
@@ -1259,7 +1268,178 @@ __global__ void __launch_bounds__(kThreads, kMinB) gen_bisect_kernel(const GenCo
       have = false;
       continue;
     }
+    if (++reps >= c.wide_after && c.wide != nullptr) {
+      // a long bisection: hand the ray to the wide phase, where a warp
+      // replays 5 levels at once (one gamma per lane) -- it would otherwise
+      // be this lane's serial tail
+      rec->low = low;
+      rec->high = high;
+      rec->last_n = last_n;
+      rec->high_n = high_n;
+      rec->passes = passes;
+      rec->samples = samples;
+      c.wide[atomicAdd(&c.ctl->nwide, 1ull)] = (int)(rec - c.recs);
+      have = false;
+      continue;
+    }
     top = true;
+  }
+}
+
+// ---------------------------------------------------------- wide bisect
+// The bisections the narrow lanes handed off (gen_bisect_kernel, after
+// wide_after replays): one warp per ray, lane i < 31 the count state of node
+// i of the next five levels of the bisection tree (heap order; node i's
+// children 2i + 1 for n > n_sg (low = gamma) and 2i + 2 for n < n_sg - delta
+// (high = gamma), every gamma = 0.5 * (low + high) formed exactly as the
+// reference forms it). The lanes walk the cache row in step -- 32 entries
+// per coalesced load, broadcast by shuffles -- and R's control flow
+// (generate.py:237-273, epsilon exits included) is replayed over the 31
+// counts, so passes, samples and the deciding pass are the reference's.
+// A lane-per-ray replay of a long ray runs ~200 dependent instructions per
+// sample on one lane; here each lane runs one state (~40), and a replay
+// covers 5 levels instead of 2-3.
+template <bool kSmemOnly>
+__global__ void __launch_bounds__(kGenThreads) gen_bisect_wide_kernel(const GenConst c) {
+  extern __shared__ double g_s_inv[];
+  const int inv_n = c.inv_n < c.inv_smem ? c.inv_n : c.inv_smem;
+  for (int i = threadIdx.x; i < inv_n; i += blockDim.x) g_s_inv[i] = c.inv_tab[i];
+  unsigned s_inv;
+  asm volatile("mov.u32 %0, %1;\n" : "=r"(s_inv) : "r"((unsigned)__cvta_generic_to_shared(g_s_inv)));
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const long long nwide = (long long)c.ctl->nwide;
+  const int n_sg = c.a.n_sg;
+  constexpr int kG = 31;
+  while (true) {
+    long long wi = 0;
+    if (lane == 0) wi = (long long)atomicAdd(&c.ctl->wfetch, 1ull);
+    wi = __shfl_sync(0xffffffffu, wi, 0);
+    if (wi >= nwide) break;
+    RayRec* rec = c.recs + c.wide[wi];
+    const float4* cache = c.cache + rec->slot;
+    const int stored = rec->nsteps;
+    double low = rec->low, high = rec->high;
+    int last_n = rec->last_n, high_n = rec->high_n;
+    int passes = rec->passes, samples = rec->samples;
+    bool fin = false;
+    while (!fin) {
+      if (fabs(high - low) < c.a.eps) {  // generate.py:238-252 (as the narrow top)
+        if (last_n == 0) {
+          rec->g_final = low;
+          rec->mode_final = kCapped;
+          passes += 1;
+        } else if (high_n >= 0) {
+          rec->g_final = high;
+          rec->mode_final = kCount;
+        } else {
+          rec->g_final = high;
+          rec->mode_final = kCapped;
+          passes += 1;
+        }
+        break;
+      }
+      // this lane's node: its gamma from the bracket along the heap path
+      CountState q;
+      {
+        const unsigned x = (unsigned)(lane < kG ? lane : 0) + 1u;
+        const int d = 31 - __clz(x);
+        double lo = low, hi = high;
+        for (int b = d - 1; b >= 0; --b) {
+          const double g = 0.5 * (lo + hi);
+          if ((x >> b) & 1u) hi = g;
+          else lo = g;
+        }
+        count_reset(q, 0.5 * (lo + hi));
+      }
+      if (lane >= kG) q.n = 0;  // the spare lane is resolved from the start
+      // walk the row: lane j holds entry base + j of the current 32-entry
+      // chunk and base + 32 + j of the next (loaded a chunk ahead)
+      int k = 0;
+      int base = -64;
+      float4 ent = make_float4(0.f, 0.f, 0.f, 0.f), nxt = ent;
+      while (true) {
+        if (k >= stored) {
+          if (q.n < 0) {
+            q.n = q.count + (q.active ? 1 : 0);
+            q.kend = stored;
+          }
+          break;
+        }
+        if (k - base >= 32) {
+          if (k - base < 64) {
+            ent = nxt;
+            base += 32;
+          } else {  // start, or a transparent run past the next chunk
+            base = k;
+            if (base + lane < stored) ent = __ldg(cache + base + lane);
+          }
+          if (base + 32 + lane < stored) nxt = __ldg(cache + base + 32 + lane);
+        }
+        const int src = k - base;
+        float4 e;
+        e.x = __shfl_sync(0xffffffffu, ent.x, src);
+        e.y = __shfl_sync(0xffffffffu, ent.y, src);
+        e.z = __shfl_sync(0xffffffffu, ent.z, src);
+        e.w = __shfl_sync(0xffffffffu, ent.w, src);
+        int run = 1;
+        if (e.w <= 0.0f) {
+          run = __float_as_int(e.x);
+          if (run < 1) run = 1;
+          if (run > stored - k) run = stored - k;
+          q.count += q.active ? 1 : 0;  // the transparent sample closes the segment
+          q.active = false;
+        } else {
+          const double a = (double)e.w;
+          double a_adj;
+          if (entry_needs_pow(e)) {
+            const double ta = rec->t0 + (double)k * c.a.step;
+            double tb = ta + c.a.step;
+            if (tb > rec->t1) tb = rec->t1;
+            const double dt = tb - ta;
+            const double ex = c.lref_pow2 ? dt * c.inv_lref : dt / c.a.lref;
+            a_adj = 1.0 - pow(1.0 - a, ex);
+          } else {
+            a_adj = 1.0 - (1.0 - a);
+          }
+          const double sr = (double)fabsf(e.x) * a_adj;
+          const double sg = (double)e.y * a_adj;
+          const double sb = (double)e.z * a_adj;
+          count_sample<false, kSmemOnly>(q, sr, sg, sb, k, n_sg, inv_n, c.inv_tab, s_inv);
+        }
+        k += run;
+        if (__all_sync(0xffffffffu, q.n >= 0)) break;
+      }
+      // replay R's control flow over the 31 counts (generate.py:237-273)
+      int node = 0;
+      for (int lvl = 0; lvl < 5 && node >= 0; ++lvl) {
+        if (lvl > 0 && fabs(high - low) < c.a.eps) break;  // handled at the top
+        const int n = __shfl_sync(0xffffffffu, q.n, node);
+        const int kend = __shfl_sync(0xffffffffu, q.kend, node);
+        const double g = 0.5 * (low + high);
+        passes += 1;
+        samples += kend;
+        last_n = n;
+        if (n > n_sg) {
+          low = g;
+          node = 2 * node + 1 < kG ? 2 * node + 1 : -1;
+        } else if (n < n_sg - c.a.delta) {
+          high = g;
+          high_n = n;
+          node = 2 * node + 2 < kG ? 2 * node + 2 : -1;
+        } else {
+          rec->g_final = g;  // window hit: this pass's segments
+          rec->mode_final = kCount;
+          fin = true;
+          break;
+        }
+      }
+    }
+    if (lane == 0) {
+      rec->passes = passes;
+      rec->samples = samples;
+    }
+    __syncwarp();
   }
 }
 
@@ -1465,12 +1645,13 @@ struct GenPlan {
   void (*fused)(const GenConst);
   void (*fill)(const GenConst);
   void (*bisect)(const GenConst);
+  void (*wide)(const GenConst);
   void (*emit)(const GenConst);
-  int sms, per_sm_sample, per_sm_fill, per_sm_bisect, per_sm_emit, per_sm_fused;
+  int sms, per_sm_sample, per_sm_fill, per_sm_bisect, per_sm_emit, per_sm_fused, per_sm_wide;
   int bisect_threads, inv_smem;
   int max_steps, inv_n;
   long long n_rays;
-  size_t off_ctl, off_inv, off_recs, off_defer0, off_defer1, off_cache;
+  size_t off_ctl, off_inv, off_recs, off_defer0, off_defer1, off_wide, off_cache;
   size_t smem, smem_inv;
 };
 
@@ -1536,6 +1717,7 @@ static int plan_gen(const VdiGenArgs* a, GenPlan& p) {
   p.inv_smem = 4096;
   p.bisect = p.inv_n <= p.inv_smem ? gen_bisect_kernel<2, 2, 1, 5, 128, 16, 2, true>
                                    : gen_bisect_kernel<2, 2, 1, 5, 128, 16, 2, false>;
+  p.wide = p.inv_n <= p.inv_smem ? gen_bisect_wide_kernel<true> : gen_bisect_wide_kernel<false>;
   // the emit kernel uses no shared memory: give the unified L1 everything
   p.emit = gen_emit_kernel<true>;
   cudaFuncSetAttribute(p.emit, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
@@ -1544,6 +1726,10 @@ static int plan_gen(const VdiGenArgs* a, GenPlan& p) {
     cudaFuncSetAttribute(p.bisect, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem_inv);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p.per_sm_bisect, p.bisect, p.bisect_threads,
                                                 p.smem_inv);
+  if (p.smem_inv > 48 * 1024)
+    cudaFuncSetAttribute(p.wide, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem_inv);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p.per_sm_wide, p.wide, kGenThreads, p.smem_inv);
+  if (p.per_sm_wide < 1) p.per_sm_wide = 1;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p.per_sm_fused, p.fused, kGenThreads, p.smem);
   if (p.per_sm_sample < 1) p.per_sm_sample = 1;
   if (p.per_sm_bisect < 1) p.per_sm_bisect = 1;
@@ -1560,7 +1746,8 @@ static int plan_gen(const VdiGenArgs* a, GenPlan& p) {
   p.off_recs = up(p.off_inv + sizeof(double) * p.inv_n);
   p.off_defer0 = up(p.off_recs + sizeof(RayRec) * (size_t)p.n_rays);
   p.off_defer1 = up(p.off_defer0 + sizeof(int) * (size_t)p.n_rays);
-  p.off_cache = up(p.off_defer1 + sizeof(int) * (size_t)p.n_rays);
+  p.off_wide = up(p.off_defer1 + sizeof(int) * (size_t)p.n_rays);
+  p.off_cache = up(p.off_wide + sizeof(int) * (size_t)p.n_rays);
   return VDI_OK;
 }
 
@@ -1750,6 +1937,14 @@ int gen_launch(const VdiGenArgs* a, cudaStream_t stream) {
   // C4 / C5 (tools/bisect_paths.py). Measured gen: C3 40.2 -> 37.8 ms, C4 82.4
   // -> 73.9, C5 391 -> 359 (chain_levels = 0 restores the tree everywhere)
   c.chain_levels = 6;
+  // narrow replays per ray before the hand-off to the wide phase. The wide
+  // phase costs ~4x the instructions per bisection level, so it pays only
+  // when a launch has too few rays to hide its longest rays' serial replays
+  // (a band-sharded rank): C3 as 1 rank 31.5 ms without / 36.5 with; as one
+  // of 8 ranks 12.0 / 8.9 ms (profiles/r02_wide_ab.log).
+#ifndef VDI_WIDE_AFTER
+#define VDI_WIDE_AFTER 3
+#endif
   // learned chain directions beyond those levels (measured: C3 gen 33.6 ->
   // 32.8 ms; C4 / C5 within noise). learn = 0 disables.
   c.learn = 1;
@@ -1763,6 +1958,7 @@ int gen_launch(const VdiGenArgs* a, cudaStream_t stream) {
   if (c.local_h <= 0) return VDI_OK;
   GenPlan p;
   int rc = plan_gen(&c.a, p);
+  c.wide_after = p.n_rays < kWideRays ? VDI_WIDE_AFTER : (1 << 30);
   if (rc != VDI_OK) return rc;
   const size_t need = gen_workspace_bytes(&c.a, 0);
   if (a->workspace_bytes < need)
@@ -1775,6 +1971,7 @@ int gen_launch(const VdiGenArgs* a, cudaStream_t stream) {
   c.inv_smem = (int)(p.smem_inv / sizeof(double));
   c.max_steps = p.max_steps;
   c.recs = reinterpret_cast<RayRec*>(ws + p.off_recs);
+  c.wide = reinterpret_cast<int*>(ws + p.off_wide);
   c.cache = reinterpret_cast<float4*>(ws + p.off_cache);
   c.cache_cap = (a->workspace_bytes - p.off_cache) / sizeof(float4);
   int* defer[2] = {reinterpret_cast<int*>(ws + p.off_defer0),
@@ -1801,6 +1998,7 @@ int gen_launch(const VdiGenArgs* a, cudaStream_t stream) {
     p.sample<<<grid_for(p.per_sm_sample, r == 0 ? chunks : -1), kGenThreads, p.smem, stream>>>(c);
     p.fill<<<grid_for(p.per_sm_fill, -1), kGenThreads, p.smem, stream>>>(c);
     p.bisect<<<grid_for(p.per_sm_bisect, -1), p.bisect_threads, p.smem_inv, stream>>>(c);
+    p.wide<<<grid_for(p.per_sm_wide, -1), kGenThreads, p.smem_inv, stream>>>(c);
     p.emit<<<grid_for(p.per_sm_emit, -1), kGenThreads, 0, stream>>>(c);
   }
   // leftovers: the fused kernel over the last round's deferred rays

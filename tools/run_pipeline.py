@@ -26,6 +26,6 @@ ctl = pipe.bufs.workspace[:64].view(torch.int64).cpu().tolist()
 passes = pipe.bufs.passes.cpu()
 hit = int((passes > 0).sum())
 print(f"round0: queued rays {ctl[2]}, cached entries {ctl[1]} ({ctl[1]*16/1e9:.2f} GB), "
-      f"deferred {ctl[4]}; hit rays {hit} of {passes.numel()}, "
+      f"deferred {ctl[4]}, handed to the wide bisect {ctl[7]}; hit rays {hit} of {passes.numel()}, "
       f"mean passes (hit) {float(passes[passes > 0].float().mean()):.2f}, "
       f"1-pass rays {int((passes == 1).sum())}")
