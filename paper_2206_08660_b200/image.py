@@ -29,5 +29,10 @@ class Image:
     def height(self) -> int:
         return self.data.shape[0]
 
+    def __array__(self, dtype=None, copy=None):
+        """np.asarray(image): the (h, w, 4) data (the reference's metrics
+        accept an Image or an array; metrics.py:25)."""
+        return self.data if dtype is None else self.data.astype(dtype, copy=False)
+
     def rgb(self) -> np.ndarray:
         return np.clip(self.data[..., :3], 0.0, 1.0)
