@@ -131,19 +131,15 @@ def launch_render(vdi, grid, cam_new, opts, image, per_pixel=None, stat_sums=Non
 
 
 def _as_device_vdi(vdi):
-    """Accept our Vdi or any object with the reference Vdi's attributes."""
+    """Accept our Vdi or any object with the reference Vdi's attributes (a
+    frozen vdikit.Vdi of numpy arrays). A reference object is uploaded on
+    every call -- no device copy is cached on it, so an array the caller
+    mutates in place is never rendered stale."""
     if hasattr(vdi, "device"):
         return vdi
     from .vdi import Vdi
-    cached = getattr(vdi, "__b200_vdi", None)
-    if cached is None:
-        cached = Vdi(vdi.width, vdi.height, vdi.n_sg, vdi.counts, vdi.segs, vdi.gen_camera,
-                     vdi.volume_aabb)
-        try:
-            object.__setattr__(vdi, "__b200_vdi", cached)
-        except Exception:
-            pass
-    return cached
+    return Vdi(vdi.width, vdi.height, vdi.n_sg, vdi.counts, vdi.segs, vdi.gen_camera,
+               vdi.volume_aabb)
 
 
 def _as_device_grid(grid):
