@@ -106,6 +106,7 @@ struct RoundCtl {
   unsigned long long ffetch;    // fill-phase pool (one ray per warp)
   unsigned long long nwide;     // rays handed to the wide bisect phase
   unsigned long long wfetch;    // wide-phase pool (one ray per warp)
+  unsigned long long ntorder;   // rays appended in overflow order
   // bisection decisions seen so far in this round, per level: [0] up, [1] down
   // (the bisect replays' learned speculation direction)
   unsigned dir[2][32];
@@ -139,6 +140,12 @@ struct GenConst {
   int sub_ox, sub_oy, sub_oz, sub_nx, sub_ny, sub_nz;
   unsigned* sub_oob;
   int* wide;         // rays handed to the wide bisect phase (record indices)
+  // the round's queue: recs is indexed by local list; qbits marks the queued
+  // lists and qidx (built from it) lists them in image order
+  unsigned* qbits;
+  int* qidx;
+  int* torder;       // the same rays in the order they overflowed (bisect / emit)
+  unsigned long long* qsum;  // per compaction block
   int wide_after;    // replays a narrow lane runs on one ray before handing it off
   int chain_levels;  // bisect replays starting below this level use the down-chain shape
   int learn;         // learned chain directions at the later levels 
@@ -566,8 +573,9 @@ __global__ void __launch_bounds__(kGenThreads, VDI_SAMPLE_MINB) gen_sample_kerne
         have = false;
         continue;
       }
-      // queue it; gen_fill_kernel stores its samples one warp per ray
-      const unsigned long long j = atomicAdd(&c.ctl->nrec, 1ull);
+      // queue it (its record at its list index; the queue is compacted in
+      // image order after this phase); gen_fill_kernel stores its samples
+      // one warp per ray
       RayRec r;
       r.d[0] = s.d[0];
       r.d[1] = s.d[1];
@@ -582,7 +590,12 @@ __global__ void __launch_bounds__(kGenThreads, VDI_SAMPLE_MINB) gen_sample_kerne
       r.g_final = 0.0;
       r.mode_final = kCount;
       r.pad = 0;
-      c.recs[j] = r;
+      c.recs[s.list] = r;
+      atomicOr(c.qbits + (s.list >> 5), 1u << (s.list & 31));
+      // overflow order: rays that overflow together tend to have similar
+      // bisections, which keeps the replay warps coherent (image order made
+      // the bisect phase 17 % slower); the fill phase reads the image order
+      c.torder[atomicAdd(&c.ctl->ntorder, 1ull)] = s.list;
       have = false;
     }
   }
@@ -614,7 +627,7 @@ __global__ void VDI_FILL_BOUNDS gen_fill_kernel(const GenConst c) {
     if (lane == 0) idx = (long long)atomicAdd(&c.ctl->ffetch, 1ull);
     idx = __shfl_sync(0xffffffffu, idx, 0);
     if (idx >= nrec) break;
-    RayRec* rec = c.recs + idx;
+    RayRec* rec = c.recs + c.qidx[idx];
     s.d[0] = rec->d[0];
     s.d[1] = rec->d[1];
     s.d[2] = rec->d[2];
@@ -944,7 +957,7 @@ __global__ void __launch_bounds__(kThreads, kMinB) gen_bisect_kernel(const GenCo
         if (idx >= nrec) {
           done = true;
         } else {
-          rec = c.recs + idx;
+          rec = c.recs + c.torder[idx];
           cache = c.cache + rec->slot;
           stored = rec->nsteps;
           // state after the overflowing pass 1 (generate.py:253-273)
@@ -1469,7 +1482,7 @@ __global__ void __launch_bounds__(kGenThreads, VDI_EMIT_MINB) gen_emit_kernel(co
         if (idx >= nrec) {
           done = true;
         } else {
-          const RayRec r = c.recs[idx];
+          const RayRec r = c.recs[c.torder[idx]];
           s.list = r.list;
           s.seg = c.a.segs + (long long)r.list * list_stride(c.a.n_sg);
           s.o[0] = c.a.eye[0];
@@ -1633,6 +1646,57 @@ __global__ void __launch_bounds__(kGenThreads) gen_fused_kernel(const GenConst c
   }
 }
 
+// The round's queue in image order: qbits (bit l = local list l queued) ->
+// qidx[0, nrec). Neighbouring queue entries are then neighbouring rays, so
+// the fill warps running side by side sample the same record sectors (L2
+// reuse) and the replay warps hold rays of similar control flow.
+constexpr int kQBlock = 256;  // bit words per compaction block
+__global__ void queue_count_kernel(const GenConst c, int n_words) {
+  const int w = blockIdx.x * kQBlock + threadIdx.x;
+  int v = w < n_words ? __popc(c.qbits[w]) : 0;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+  __shared__ int s_w[kQBlock / 32];
+  if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int t = 0;
+    for (int k = 0; k < kQBlock / 32; ++k) t += s_w[k];
+    c.qsum[blockIdx.x] = (unsigned long long)t;
+  }
+}
+
+__global__ void queue_scan_kernel(const GenConst c, int nb) {
+  // one thread: nb is small (2 Mi rays -> 256 blocks)
+  unsigned long long run = 0;
+  for (int b = 0; b < nb; ++b) {
+    const unsigned long long v = c.qsum[b];
+    c.qsum[b] = run;
+    run += v;
+  }
+  c.ctl->nrec = run;
+}
+
+__global__ void queue_write_kernel(const GenConst c, int n_words) {
+  __shared__ int s_w[kQBlock / 32];
+  const int w = blockIdx.x * kQBlock + threadIdx.x;
+  const unsigned bits = w < n_words ? c.qbits[w] : 0u;
+  const int cnt = __popc(bits);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int incl = cnt;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const int u = __shfl_up_sync(0xffffffffu, incl, off);
+    if (lane >= off) incl += u;
+  }
+  if (lane == 31) s_w[wid] = incl;
+  __syncthreads();
+  int before = 0;
+  for (int k = 0; k < wid; ++k) before += s_w[k];
+  long long at = (long long)c.qsum[blockIdx.x] + before + incl - cnt;
+  for (unsigned b = bits; b; b &= b - 1) c.qidx[at++] = w * 32 + (__ffs(b) - 1);
+}
+
 __global__ void fill_inv_kernel(double* tab, int n) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) tab[i] = i > 0 ? 1.0 / (double)i : 0.0;
@@ -1651,7 +1715,9 @@ struct GenPlan {
   int bisect_threads, inv_smem;
   int max_steps, inv_n;
   long long n_rays;
-  size_t off_ctl, off_inv, off_recs, off_defer0, off_defer1, off_wide, off_cache;
+  size_t off_ctl, off_inv, off_recs, off_defer0, off_defer1, off_wide, off_qbits, off_qidx,
+      off_torder, off_qsum, off_cache;
+  int n_qwords, n_qblocks;
   size_t smem, smem_inv;
 };
 
@@ -1715,8 +1781,12 @@ static int plan_gen(const VdiGenArgs* a, GenPlan& p) {
   // in profiles/r01_gen_v1_fused_cache.md)
   p.bisect_threads = kGenThreads;
   p.inv_smem = 4096;
-  p.bisect = p.inv_n <= p.inv_smem ? gen_bisect_kernel<2, 2, 1, 5, 128, 16, 2, true>
-                                   : gen_bisect_kernel<2, 2, 1, 5, 128, 16, 2, false>;
+#ifndef VDI_BISECT_MINB
+#define VDI_BISECT_MINB 5
+#endif
+  p.bisect = p.inv_n <= p.inv_smem
+                 ? gen_bisect_kernel<2, 2, 1, VDI_BISECT_MINB, 128, 16, 2, true>
+                 : gen_bisect_kernel<2, 2, 1, VDI_BISECT_MINB, 128, 16, 2, false>;
   p.wide = p.inv_n <= p.inv_smem ? gen_bisect_wide_kernel<true> : gen_bisect_wide_kernel<false>;
   // the emit kernel uses no shared memory: give the unified L1 everything
   p.emit = gen_emit_kernel<true>;
@@ -1747,7 +1817,13 @@ static int plan_gen(const VdiGenArgs* a, GenPlan& p) {
   p.off_defer0 = up(p.off_recs + sizeof(RayRec) * (size_t)p.n_rays);
   p.off_defer1 = up(p.off_defer0 + sizeof(int) * (size_t)p.n_rays);
   p.off_wide = up(p.off_defer1 + sizeof(int) * (size_t)p.n_rays);
-  p.off_cache = up(p.off_wide + sizeof(int) * (size_t)p.n_rays);
+  p.n_qwords = (int)((p.n_rays + 31) / 32);
+  p.n_qblocks = (p.n_qwords + kQBlock - 1) / kQBlock;
+  p.off_qbits = up(p.off_wide + sizeof(int) * (size_t)p.n_rays);
+  p.off_qidx = up(p.off_qbits + sizeof(unsigned) * (size_t)p.n_qwords);
+  p.off_torder = up(p.off_qidx + sizeof(int) * (size_t)p.n_rays);
+  p.off_qsum = up(p.off_torder + sizeof(int) * (size_t)p.n_rays);
+  p.off_cache = up(p.off_qsum + sizeof(unsigned long long) * (size_t)(p.n_qblocks + 1));
   return VDI_OK;
 }
 
@@ -1972,6 +2048,10 @@ int gen_launch(const VdiGenArgs* a, cudaStream_t stream) {
   c.max_steps = p.max_steps;
   c.recs = reinterpret_cast<RayRec*>(ws + p.off_recs);
   c.wide = reinterpret_cast<int*>(ws + p.off_wide);
+  c.qbits = reinterpret_cast<unsigned*>(ws + p.off_qbits);
+  c.qidx = reinterpret_cast<int*>(ws + p.off_qidx);
+  c.torder = reinterpret_cast<int*>(ws + p.off_torder);
+  c.qsum = reinterpret_cast<unsigned long long*>(ws + p.off_qsum);
   c.cache = reinterpret_cast<float4*>(ws + p.off_cache);
   c.cache_cap = (a->workspace_bytes - p.off_cache) / sizeof(float4);
   int* defer[2] = {reinterpret_cast<int*>(ws + p.off_defer0),
@@ -1995,7 +2075,11 @@ int gen_launch(const VdiGenArgs* a, cudaStream_t stream) {
     c.prev = r > 0 ? ctl + r - 1 : ctl;
     c.defer_in = defer[(r + 1) & 1];
     c.defer_out = defer[r & 1];
+    cudaMemsetAsync(c.qbits, 0, sizeof(unsigned) * (size_t)p.n_qwords, stream);
     p.sample<<<grid_for(p.per_sm_sample, r == 0 ? chunks : -1), kGenThreads, p.smem, stream>>>(c);
+    queue_count_kernel<<<p.n_qblocks, kQBlock, 0, stream>>>(c, p.n_qwords);
+    queue_scan_kernel<<<1, 1, 0, stream>>>(c, p.n_qblocks);
+    queue_write_kernel<<<p.n_qblocks, kQBlock, 0, stream>>>(c, p.n_qwords);
     p.fill<<<grid_for(p.per_sm_fill, -1), kGenThreads, p.smem, stream>>>(c);
     p.bisect<<<grid_for(p.per_sm_bisect, -1), p.bisect_threads, p.smem_inv, stream>>>(c);
     p.wide<<<grid_for(p.per_sm_wide, -1), kGenThreads, p.smem_inv, stream>>>(c);
