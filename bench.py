@@ -303,7 +303,7 @@ def run_b200(args):
         pipe.step()
     torch.cuda.synchronize()
     S = pipe.samples_executed()            # this rank's executed samples (R semantics)
-    stats = pipe.render_stats()            # this rank's (L, K, L_s)
+    stats = pipe.exact_render_stats()      # this rank's (L, K, L_s), untimed
 
     clocks = ClockSampler(dev)
     step_ms, prep_ms, gen_ms, grid_ms, coll_ms, ren_ms = [], [], [], [], [], []

@@ -63,7 +63,7 @@
 extern "C" {
 #endif
 
-#define VDI_ABI_VERSION 4
+#define VDI_ABI_VERSION 5
 
 #define VDI_OK 0
 #define VDI_EINVAL (-1)
@@ -184,6 +184,16 @@ typedef struct VdiRenderArgs {
    * the words of its column range and tests its slab range in one compare
    * instead of reading every cell; the result is the same. */
   const uint64_t* grid_zmask;
+  /* 1: every list's fronts and backs are non-decreasing (true of generated
+   * VDIs: _emit clamps, generate.py:58-62). Then, for rays whose chord runs
+   * forward in depth, the Alg. 2 search result does not depend on its seed,
+   * and the kernel may search a list first and evaluate the ESS test only to
+   * confirm a hit (a miss composites nothing either way): same image, same
+   * lists_visited / segs_intersected, fewer ESS tests. lists_searched is then
+   * not counted (per-pixel array and stat_sums[2] are left unchanged) unless
+   * counters_exact is 1. 0: the reference's order (ESS, then search). */
+  int32_t lists_sorted;
+  int32_t counters_exact;
 } VdiRenderArgs;
 
 /* Ground-truth direct volume rendering (dvr.py:21-89): the generation ray,

@@ -57,13 +57,60 @@ struct ShadeSmem {
   int nint[kRenderThreads], nsearch[kRenderThreads];
 };
 
+// _grid_cell_range (raycast.py:258-272) + the all-empty scan (359-370):
+// true when every grid cell the chord piece [s_cur, s_exit] covers is empty.
+// d = a0z + s cdz is a function of s alone, so the depth of a shared chord
+// parameter (this list's entry = the previous list's exit) is reused.
+template <bool kMask>
+__device__ __forceinline__ bool ess_empty(const RenderConst& c, ShadeSmem& sm, int t, double a0x,
+                                          double a0y, double cdx, double cdy, double s_cur,
+                                          double s_exit, double d_entry, double d_exit) {
+  const VdiRenderArgs& a = c.a;
+  const double x_a = a0x + s_cur * cdx, y_a = a0y + s_cur * cdy;
+  const double x_b = a0x + s_exit * cdx, y_b = a0y + s_exit * cdy;
+  const double dep_a = s_cur == sm.dep_key[t] ? sm.dep_val[t] : a.proj_b / (a.proj_a - d_entry);
+  const double dep_b = a.proj_b / (a.proj_a - d_exit);
+  sm.dep_key[t] = s_exit;
+  sm.dep_val[t] = dep_b;
+  const int gx = a.gx, gy = a.gy, gz = a.gz;
+  const int cgx0 = clampi(floor_ll((dmin(x_a, x_b) + 1.0) * gx / 2.0), 0, gx - 1);
+  const int cgx1 = clampi(floor_ll((dmax(x_a, x_b) + 1.0) * gx / 2.0), 0, gx - 1);
+  const int cgy0 = clampi(floor_ll((dmin(y_a, y_b) + 1.0) * gy / 2.0), 0, gy - 1);
+  const int cgy1 = clampi(floor_ll((dmax(y_a, y_b) + 1.0) * gy / 2.0), 0, gy - 1);
+  const double fn = a.far - a.near;
+  const int cz0 = clampi(floor_ll(div_by(dmin(dep_a, dep_b) - a.near, fn, c.rfn) * gz), 0, gz - 1);
+  const int cz1 = clampi(floor_ll(div_by(dmax(dep_a, dep_b) - a.near, fn, c.rfn) * gz), 0, gz - 1);
+  if (kMask) {
+    uint64_t m = 0;
+    for (int cgy = cgy0; cgy <= cgy1; ++cgy)
+      for (int cgx = cgx0; cgx <= cgx1; ++cgx) m |= __ldg(a.grid_zmask + cgy * gx + cgx);
+    // bits cz0..cz1 (2 << 63 wraps to 0, which still yields bits cz0..63)
+    const uint64_t want = (2ull << cz1) - (1ull << cz0);
+    return (m & want) == 0;
+  }
+  for (int cz = cz0; cz <= cz1; ++cz)
+    for (int cgy = cgy0; cgy <= cgy1; ++cgy)
+      for (int cgx = cgx0; cgx <= cgx1; ++cgx)
+        if (__ldg(a.grid + ((long long)cz * gy + cgy) * gx + cgx) > 0u) return false;
+  return true;
+}
+
 // One non-empty list of the DDA (raycast.py:346-435 for count > 0): the ESS
 // test, the seeded search and the Eq. 2 compositing. Returns true when the
 // ray terminates (acc_a >= early_term).
+//
+// kFast (lists_sorted, a forward chord, lists_searched not counted): the
+// search runs first and the ESS test only confirms a hit. This is the same
+// result: with non-decreasing backs the forward search (raycast.py:88-121)
+// returns the first back >= d_entry (or the last list entry) whatever the
+// seed -- each seed interval either holds that index or prunes to a range
+// that does -- so searching a list R would have skipped changes no later
+// search; a miss composites nothing in either order; and a hit is
+// composited iff the ESS test passes, as in R.
 template <bool kMask>
 __device__ __forceinline__ bool shade_list(const RenderConst& c, ShadeSmem& sm, int t, int cx,
                                            int cy, long long lidx, int count, double s_cur,
-                                           double tmin) {
+                                           double tmin, bool fast) {
   const VdiRenderArgs& a = c.a;
   const int vdi_w = a.vdi_w, vdi_h = a.vdi_h, n_sg = a.n_sg;
   const double a0x = sm.a0x[t], a0y = sm.a0y[t], a0z = sm.a0z[t];
@@ -72,53 +119,27 @@ __device__ __forceinline__ bool shade_list(const RenderConst& c, ShadeSmem& sm, 
   if (s_exit < s_cur) s_exit = s_cur;
   const double d_entry = a0z + s_cur * cdz;
   const double d_exit = a0z + s_exit * cdz;
-  if (a.use_ess) {
-    // _grid_cell_range (raycast.py:258-272) + the all-empty scan (359-370).
-    // d = a0z + s cdz is a function of s alone, so the depth of a shared
-    // chord parameter (this list's entry = the previous list's exit) is reused.
-    const double x_a = a0x + s_cur * cdx, y_a = a0y + s_cur * cdy;
-    const double x_b = a0x + s_exit * cdx, y_b = a0y + s_exit * cdy;
-    const double dep_a =
-        s_cur == sm.dep_key[t] ? sm.dep_val[t] : a.proj_b / (a.proj_a - d_entry);
-    const double dep_b = a.proj_b / (a.proj_a - d_exit);
-    sm.dep_key[t] = s_exit;
-    sm.dep_val[t] = dep_b;
-    const int gx = a.gx, gy = a.gy, gz = a.gz;
-    const int cgx0 = clampi(floor_ll((dmin(x_a, x_b) + 1.0) * gx / 2.0), 0, gx - 1);
-    const int cgx1 = clampi(floor_ll((dmax(x_a, x_b) + 1.0) * gx / 2.0), 0, gx - 1);
-    const int cgy0 = clampi(floor_ll((dmin(y_a, y_b) + 1.0) * gy / 2.0), 0, gy - 1);
-    const int cgy1 = clampi(floor_ll((dmax(y_a, y_b) + 1.0) * gy / 2.0), 0, gy - 1);
-    const double fn = a.far - a.near;
-    const int cz0 =
-        clampi(floor_ll(div_by(dmin(dep_a, dep_b) - a.near, fn, c.rfn) * gz), 0, gz - 1);
-    const int cz1 =
-        clampi(floor_ll(div_by(dmax(dep_a, dep_b) - a.near, fn, c.rfn) * gz), 0, gz - 1);
-    bool empty = true;
-    if (kMask) {
-      uint64_t m = 0;
-      for (int cgy = cgy0; cgy <= cgy1; ++cgy)
-        for (int cgx = cgx0; cgx <= cgx1; ++cgx) m |= __ldg(a.grid_zmask + cgy * gx + cgx);
-      // bits cz0..cz1 (2 << 63 wraps to 0, which still yields bits cz0..63)
-      const uint64_t want = (2ull << cz1) - (1ull << cz0);
-      empty = (m & want) == 0;
-    } else {
-      for (int cz = cz0; cz <= cz1 && empty; ++cz)
-        for (int cgy = cgy0; cgy <= cgy1 && empty; ++cgy)
-          for (int cgx = cgx0; cgx <= cgx1; ++cgx)
-            if (__ldg(a.grid + ((long long)cz * gy + cgy) * gx + cgx) > 0u) {
-              empty = false;
-              break;
-            }
-    }
-    if (empty) return false;
-  }
-  sm.nsearch[t] += 1;
   const float* ls = a.segs + lidx * (long long)list_stride(n_sg);
   const float* fronts = ls + front_off(n_sg);
   const float* backs = ls + back_off(n_sg);
   const float4* rgba = reinterpret_cast<const float4*>(ls);
-  int seed;
-  const int j = find_first(fronts, backs, count, d_entry, d_exit, sm.p[t], seed);
+  int seed, j;
+  if (fast) {
+    j = find_first(fronts, backs, count, d_entry, d_exit, sm.p[t], seed);
+    if (j < 0) {
+      sm.p[t] = seed;
+      return false;
+    }
+    if (a.use_ess &&
+        ess_empty<kMask>(c, sm, t, a0x, a0y, cdx, cdy, s_cur, s_exit, d_entry, d_exit))
+      return false;
+  } else {
+    if (a.use_ess &&
+        ess_empty<kMask>(c, sm, t, a0x, a0y, cdx, cdy, s_cur, s_exit, d_entry, d_exit))
+      return false;
+    sm.nsearch[t] += 1;
+    j = find_first(fronts, backs, count, d_entry, d_exit, sm.p[t], seed);
+  }
   sm.p[t] = seed;
   if (j < 0) return false;
   const bool fwd = d_entry <= d_exit;
@@ -254,6 +275,9 @@ __global__ void __launch_bounds__(kRenderThreads, VDI_RENDER_MINB) render_kernel
           t_max_y = (by - a0y) / cdy;
           t_delta_y = (2.0 / vdi_h) / fabs(cdy);
         }
+        // search-first shading (shade_list kFast): sorted lists, a chord running
+        // forward in depth (d_entry <= d_exit on every list), uncounted searches
+        const bool fast = a.lists_sorted && !a.counters_exact && cdz >= 0.0;
         sm.p[t] = -1;
         sm.dep_key[t] = -1.0;  // chord parameters are >= 0
         sm.dep_val[t] = 0.0;
@@ -299,7 +323,7 @@ __global__ void __launch_bounds__(kRenderThreads, VDI_RENDER_MINB) render_kernel
           }
           if (cnt > 0) {
             const long long lidx = (rowp - a.counts) + cx;
-            if (shade_list<kMask>(c, sm, t, cx, cy, lidx, cnt, s_cur, tmin)) break;
+            if (shade_list<kMask>(c, sm, t, cx, cy, lidx, cnt, s_cur, tmin, fast)) break;
           }
           if (last) break;
           cx = ncx;
@@ -319,10 +343,10 @@ __global__ void __launch_bounds__(kRenderThreads, VDI_RENDER_MINB) render_kernel
       const int nint = sm.nint[t], nsearch = sm.nsearch[t];
       if (a.lists_visited) a.lists_visited[pix] = nvis;
       if (a.segs_intersected) a.segs_intersected[pix] = nint;
-      if (a.lists_searched) a.lists_searched[pix] = nsearch;
+      if (a.lists_searched && a.counters_exact) a.lists_searched[pix] = nsearch;
       st_vis = nvis;
       st_int = nint;
-      st_srch = nsearch;
+      st_srch = a.counters_exact ? nsearch : 0;
     }
   }
   if (a.stat_sums) {

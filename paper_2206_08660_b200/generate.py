@@ -229,7 +229,7 @@ def generate_vdi(vol, tf, cam, params: GenParams | None = None, grid_dims=None,
     cells = dv.volume_cells(vol_dev, vt, vol.dims) if dv.use_cells(vt, vol.dims) else None
     launch_generate(vol_dev, vt, vol.dims, lut_dev, cam, aabb, params, resolved, bufs,
                     grid_dims, bricks=bricks, ess_max=dv.ess_threshold(tf.lut), cells=cells)
-    dev = DeviceVdi(counts=bufs.counts, segs=bufs.segs)
+    dev = DeviceVdi(counts=bufs.counts, segs=bufs.segs, sorted=True)
     vdi = Vdi(width=width, height=height, n_sg=params.n_sg, counts=None, segs=None,
               gen_camera=cam, volume_aabb=aabb, _device=dev)
     grid = AccelGrid(dims=grid_dims, counts=None, near=cam.near, far=cam.far,

@@ -45,7 +45,11 @@ def opacity_correct(alpha: float, l: float) -> float:
 
 def render_args(dvdi, n_sg, vdi_w, vdi_h, gen_cam, aabb, grid_dev, grid_dims, grid_near,
                 grid_far, cam_new, opts, image, per_pixel=None, stat_sums=None,
-                band=(16, 1, 0)) -> _capi.VdiRenderArgs:
+                band=(16, 1, 0), counters_exact=None) -> _capi.VdiRenderArgs:
+    """counters_exact: count lists_searched exactly (the reference's ESS-then-
+    search order); default: exactly when per-pixel counters or stat sums are
+    requested. Image, lists_visited and segs_intersected are exact either
+    way."""
     a = _capi.VdiRenderArgs()
     a.segs, a.counts, a.grid, a.image = (dv.ptr(dvdi.segs), dv.ptr(dvdi.counts),
                                          dv.ptr(grid_dev), dv.ptr(image))
@@ -68,6 +72,10 @@ def render_args(dvdi, n_sg, vdi_w, vdi_h, gen_cam, aabb, grid_dev, grid_dims, gr
     a.vdi_band_rows, a.vdi_band_world = int(dvdi.band_rows), int(dvdi.world)
     a.vdi_rows_per_rank = int(dvdi.rows_per_rank)
     a.band_rows, a.band_stride, a.band_offset = (int(v) for v in band)
+    a.lists_sorted = int(bool(getattr(dvdi, "sorted", False)))
+    if counters_exact is None:
+        counters_exact = per_pixel is not None or stat_sums is not None
+    a.counters_exact = int(bool(counters_exact))
     return a
 
 

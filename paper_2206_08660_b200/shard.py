@@ -314,15 +314,19 @@ class Pipeline:
             self.g_image = t.empty((world * self.out_rows, ow, 4), dtype=t.float64,
                                    device="cuda")
             self.dvdi = DeviceVdi(self.g_counts, self.g_segs, self.gen_band_rows, world,
-                                  self.gen_rows)
+                                  self.gen_rows, sorted=True)
             from .tuning import TUNING
             self.packed = PackedExchange(self) if TUNING.packed_exchange else None
         else:
             self.dist = None
-            self.dvdi = DeviceVdi(self.bufs.counts, self.bufs.segs)
+            self.dvdi = DeviceVdi(self.bufs.counts, self.bufs.segs, sorted=True)
+        # the frame's render counts lists visited / supersegments intersected
+        # (R's RenderStats) but not lists searched (search-first shading,
+        # VdiRenderArgs.lists_sorted); exact_render_stats() counts all three
         self._rargs = render_args(self.dvdi, params.n_sg, w, h, gcam, self.aabb, self.bufs.grid,
                                   self.grid_dims, gcam.near, gcam.far, rcam, self.opts,
-                                  self.image, stat_sums=self.sums, band=self.band)
+                                  self.image, stat_sums=self.sums, band=self.band,
+                                  counters_exact=False)
 
     def step(self, timed: bool = False, vol_dev=None):
         """One frame on the current stream: volume prep, generation, grid,
@@ -386,6 +390,21 @@ class Pipeline:
                 self.dist.all_gather_into_tensor(self.bricks_all, self.slab_local)
         if self.cells is not None:
             dv.launch_cells(vol_dev, self.vt, self.res_dims, self.cells, self.bricks, self.ess_max)
+
+    def exact_render_stats(self):
+        """(lists visited, supersegments intersected, lists searched) of this
+        rank's render in the reference's ESS-then-search order (an extra,
+        untimed render)."""
+        t = self.t
+        sums = t.zeros(3, dtype=t.int64, device="cuda")
+        a = render_args(self.dvdi, self.params.n_sg, self.w, self.h, self.gcam, self.aabb,
+                        self.bufs.grid, self.grid_dims, self.gcam.near, self.gcam.far,
+                        self.rcam, self.opts, self.image, stat_sums=sums, band=self.band,
+                        counters_exact=True)
+        launch_zmask(a, self.zmask)
+        _capi.check(_capi.load().vdi_render_launch(a, dv.stream_handle()))
+        s = sums.cpu().numpy()
+        return int(s[0]), int(s[1]), int(s[2])
 
     def render_per_pixel(self):
         """This rank's render again, with per-pixel counters (untimed):

@@ -51,6 +51,10 @@ class DeviceVdi:
     band_rows: int = 16
     world: int = 1
     rows_per_rank: int = 0
+    # fronts and backs non-decreasing in every list: true of generated VDIs
+    # (_emit clamps, generate.py:58-62); lets the render search before the
+    # ESS test (VdiRenderArgs.lists_sorted)
+    sorted: bool = False
 
 
 class Vdi:

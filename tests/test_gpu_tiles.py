@@ -98,3 +98,40 @@ def test_zmask_exact(cfg, angle):
     for x, y in zip(outs[0], outs[1]):
         np.testing.assert_array_equal(x, y)
     assert outs[0][3].sum() > 0
+
+
+@pytest.mark.parametrize("cfg,angle", [("C2", 15.0), ("C2", 120.0), ("C2", 180.0),
+                                       ("C3", 15.0), ("C3", 100.0)])
+def test_search_first_shading_exact(cfg, angle):
+    """Search-first shading (VdiRenderArgs.lists_sorted, generated VDIs,
+    counters not exact) against the reference's ESS-then-search order: the
+    same image and the same lists_visited / supersegments_intersected per
+    pixel, forward chords (15 deg) and views behind the volume (reverse
+    chords take the reference order)."""
+    from paper_2206_08660_b200.raycast import alloc_zmask, launch_zmask
+    vol, tf, gcam, rcam, n_sg = synth.config(cfg)
+    rcam = synth.sweep_camera(vol, angle, gcam.viewport, synth.CONFIGS[cfg][4])
+    vdi, grid = vb.generate_vdi(vol, tf, gcam, vb.GenParams(n_sg=n_sg))
+    d = vdi.device()
+    assert d.sorted
+    ow, oh = rcam.viewport
+    L = _capi.load()
+    outs = []
+    for exact in (True, False):
+        image = torch.empty((oh, ow, 4), dtype=torch.float64, device="cuda")
+        pp = [torch.zeros((oh, ow), dtype=torch.int32, device="cuda") for _ in range(3)]
+        a = render_args(d, n_sg, vdi.width, vdi.height, gcam, vdi.volume_aabb, grid.device(),
+                        grid.dims, grid.near, grid.far, rcam, vb.RenderOptions(), image,
+                        per_pixel=pp, counters_exact=exact)
+        assert a.lists_sorted == 1
+        zm = alloc_zmask(grid.dims)
+        launch_zmask(a, zm)
+        _capi.check(L.vdi_render_launch(a, dv.stream_handle()))
+        torch.cuda.synchronize()
+        outs.append([image.cpu().numpy()] + [x.cpu().numpy() for x in pp[:2]])
+    for x, y in zip(outs[0], outs[1]):
+        np.testing.assert_array_equal(x, y)
+    assert outs[0][1].sum() > 0
+    # the public API without stats takes the search-first path
+    img = vb.render_vdi(vdi, grid, rcam)
+    np.testing.assert_array_equal(img.data, outs[0][0])

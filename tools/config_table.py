@@ -56,7 +56,7 @@ def main():
         r_ms = float(np.median([e["render"] for e in evs]))
         prep = float(np.median([e["prep"] for e in evs]))
         S = pipe.samples_executed()
-        L, K, Ls = pipe.render_stats()
+        L, K, Ls = pipe.exact_render_stats()
         w, h = gcam.viewport
         ow, oh = rcam.viewport
         gx, gy, gz = pipe.grid_dims

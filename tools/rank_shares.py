@@ -80,7 +80,7 @@ def main():
     ref = shard.Pipeline(vol, tf, gcam, rcam, params)
     ref.step()
     torch.cuda.synchronize()
-    full_vdi = DeviceVdi(ref.bufs.counts, ref.bufs.segs)
+    full_vdi = DeviceVdi(ref.bufs.counts, ref.bufs.segs, sorted=True)
     ref.bufs.workspace = None  # the ranks below size their own generation scratch
     torch.cuda.empty_cache()
     ref_grid = ref.bufs.grid

@@ -21,7 +21,7 @@ for _ in range(a.reps):
     ev = pipe.step(timed=True)
     print({k: round(v, 3) for k, v in ev.items()}, flush=True)
 torch.cuda.synchronize()
-print("samples", pipe.samples_executed(), "render stats", pipe.render_stats())
+print("samples", pipe.samples_executed(), "render stats", pipe.exact_render_stats())
 ctl = pipe.bufs.workspace[:64].view(torch.int64).cpu().tolist()
 passes = pipe.bufs.passes.cpu()
 hit = int((passes > 0).sum())
