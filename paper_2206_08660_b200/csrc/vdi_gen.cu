@@ -147,6 +147,7 @@ struct GenConst {
   int* torder;       // the same rays in the order they overflowed (bisect / emit)
   unsigned long long* qsum;  // per compaction block
   int wide_after;    // replays a narrow lane runs on one ray before handing it off
+  int wide_tail;     // also hand off every ray once the narrow queue is drained
   int chain_levels;  // bisect replays starting below this level use the down-chain shape
   int learn;         // learned chain directions at the later levels 
 };
@@ -1281,7 +1282,12 @@ __global__ void __launch_bounds__(kThreads, kMinB) gen_bisect_kernel(const GenCo
       have = false;
       continue;
     }
-    if (++reps >= c.wide_after && c.wide != nullptr) {
+    ++reps;
+    if (c.wide != nullptr &&
+        (reps >= c.wide_after ||
+         (c.wide_tail &&
+          *reinterpret_cast<volatile unsigned long long*>(&c.ctl->rfetch) >=
+              (unsigned long long)nrec))) {
       // a long bisection: hand the ray to the wide phase, where a warp
       // replays 5 levels at once (one gamma per lane) -- it would otherwise
       // be this lane's serial tail
@@ -1300,20 +1306,22 @@ __global__ void __launch_bounds__(kThreads, kMinB) gen_bisect_kernel(const GenCo
 }
 
 // ---------------------------------------------------------- wide bisect
-// The bisections the narrow lanes handed off (gen_bisect_kernel, after
-// wide_after replays): one warp per ray, lane i < 31 the count state of node
-// i of the next five levels of the bisection tree (heap order; node i's
+// The bisections the narrow lanes handed off (gen_bisect_kernel): a group of
+// kLanes lanes per ray, lane i < kLanes - 1 the count state of node i of the
+// next log2(kLanes) levels of the bisection tree (heap order; node i's
 // children 2i + 1 for n > n_sg (low = gamma) and 2i + 2 for n < n_sg - delta
 // (high = gamma), every gamma = 0.5 * (low + high) formed exactly as the
-// reference forms it). The lanes walk the cache row in step -- 32 entries
-// per coalesced load, broadcast by shuffles -- and R's control flow
-// (generate.py:237-273, epsilon exits included) is replayed over the 31
+// reference forms it). The group's lanes walk the cache row in step --
+// kLanes entries per coalesced load, broadcast by shuffles -- and R's control
+// flow (generate.py:237-273, epsilon exits included) is replayed over the
 // counts, so passes, samples and the deciding pass are the reference's.
-// A lane-per-ray replay of a long ray runs ~200 dependent instructions per
-// sample on one lane; here each lane runs one state (~40), and a replay
-// covers 5 levels instead of 2-3.
-template <bool kSmemOnly>
+// A narrow lane runs ~200 dependent instructions per sample for its 3
+// states; here each lane runs one state, so a ray's replay latency drops
+// ~3x (kLanes 8: the tail of a launch) and a replay covers 3 or 5 levels.
+template <int kLanes, bool kSmemOnly>
 __global__ void __launch_bounds__(kGenThreads) gen_bisect_wide_kernel(const GenConst c) {
+  constexpr int kG = kLanes - 1;
+  constexpr int kLevels = kLanes == 32 ? 5 : (kLanes == 16 ? 4 : (kLanes == 8 ? 3 : 2));
   extern __shared__ double g_s_inv[];
   const int inv_n = c.inv_n < c.inv_smem ? c.inv_n : c.inv_smem;
   for (int i = threadIdx.x; i < inv_n; i += blockDim.x) g_s_inv[i] = c.inv_tab[i];
@@ -1321,13 +1329,15 @@ __global__ void __launch_bounds__(kGenThreads) gen_bisect_wide_kernel(const GenC
   asm volatile("mov.u32 %0, %1;\n" : "=r"(s_inv) : "r"((unsigned)__cvta_generic_to_shared(g_s_inv)));
   __syncthreads();
   const int lane = threadIdx.x & 31;
+  const int sl = lane & (kLanes - 1);                    // lane within the group
+  const int g0 = lane & ~(kLanes - 1);                   // the group's first lane
+  const unsigned gm = kLanes == 32 ? 0xffffffffu : (((1u << kLanes) - 1u) << g0);
   const long long nwide = (long long)c.ctl->nwide;
   const int n_sg = c.a.n_sg;
-  constexpr int kG = 31;
   while (true) {
     long long wi = 0;
-    if (lane == 0) wi = (long long)atomicAdd(&c.ctl->wfetch, 1ull);
-    wi = __shfl_sync(0xffffffffu, wi, 0);
+    if (sl == 0) wi = (long long)atomicAdd(&c.ctl->wfetch, 1ull);
+    wi = __shfl_sync(gm, wi, g0);
     if (wi >= nwide) break;
     RayRec* rec = c.recs + c.wide[wi];
     const float4* cache = c.cache + rec->slot;
@@ -1338,24 +1348,25 @@ __global__ void __launch_bounds__(kGenThreads) gen_bisect_wide_kernel(const GenC
     bool fin = false;
     while (!fin) {
       if (fabs(high - low) < c.a.eps) {  // generate.py:238-252 (as the narrow top)
-        if (last_n == 0) {
-          rec->g_final = low;
-          rec->mode_final = kCapped;
-          passes += 1;
-        } else if (high_n >= 0) {
-          rec->g_final = high;
-          rec->mode_final = kCount;
-        } else {
-          rec->g_final = high;
-          rec->mode_final = kCapped;
-          passes += 1;
+        if (sl == 0) {
+          if (last_n == 0) {
+            rec->g_final = low;
+            rec->mode_final = kCapped;
+          } else if (high_n >= 0) {
+            rec->g_final = high;
+            rec->mode_final = kCount;
+          } else {
+            rec->g_final = high;
+            rec->mode_final = kCapped;
+          }
         }
+        if (last_n == 0 || high_n < 0) passes += 1;
         break;
       }
       // this lane's node: its gamma from the bracket along the heap path
       CountState q;
       {
-        const unsigned x = (unsigned)(lane < kG ? lane : 0) + 1u;
+        const unsigned x = (unsigned)(sl < kG ? sl : 0) + 1u;
         const int d = 31 - __clz(x);
         double lo = low, hi = high;
         for (int b = d - 1; b >= 0; --b) {
@@ -1365,11 +1376,11 @@ __global__ void __launch_bounds__(kGenThreads) gen_bisect_wide_kernel(const GenC
         }
         count_reset(q, 0.5 * (lo + hi));
       }
-      if (lane >= kG) q.n = 0;  // the spare lane is resolved from the start
-      // walk the row: lane j holds entry base + j of the current 32-entry
-      // chunk and base + 32 + j of the next (loaded a chunk ahead)
+      if (sl >= kG) q.n = 0;  // the spare lane is resolved from the start
+      // walk the row: lane sl holds entry base + sl of the current chunk of
+      // kLanes entries and base + kLanes + sl of the next (loaded ahead)
       int k = 0;
-      int base = -64;
+      int base = -2 * kLanes;
       float4 ent = make_float4(0.f, 0.f, 0.f, 0.f), nxt = ent;
       while (true) {
         if (k >= stored) {
@@ -1379,22 +1390,22 @@ __global__ void __launch_bounds__(kGenThreads) gen_bisect_wide_kernel(const GenC
           }
           break;
         }
-        if (k - base >= 32) {
-          if (k - base < 64) {
+        if (k - base >= kLanes) {
+          if (k - base < 2 * kLanes) {
             ent = nxt;
-            base += 32;
+            base += kLanes;
           } else {  // start, or a transparent run past the next chunk
             base = k;
-            if (base + lane < stored) ent = __ldg(cache + base + lane);
+            if (base + sl < stored) ent = __ldg(cache + base + sl);
           }
-          if (base + 32 + lane < stored) nxt = __ldg(cache + base + 32 + lane);
+          if (base + kLanes + sl < stored) nxt = __ldg(cache + base + kLanes + sl);
         }
-        const int src = k - base;
+        const int src = g0 + (k - base);
         float4 e;
-        e.x = __shfl_sync(0xffffffffu, ent.x, src);
-        e.y = __shfl_sync(0xffffffffu, ent.y, src);
-        e.z = __shfl_sync(0xffffffffu, ent.z, src);
-        e.w = __shfl_sync(0xffffffffu, ent.w, src);
+        e.x = __shfl_sync(gm, ent.x, src);
+        e.y = __shfl_sync(gm, ent.y, src);
+        e.z = __shfl_sync(gm, ent.z, src);
+        e.w = __shfl_sync(gm, ent.w, src);
         int run = 1;
         if (e.w <= 0.0f) {
           run = __float_as_int(e.x);
@@ -1421,14 +1432,14 @@ __global__ void __launch_bounds__(kGenThreads) gen_bisect_wide_kernel(const GenC
           count_sample<false, kSmemOnly>(q, sr, sg, sb, k, n_sg, inv_n, c.inv_tab, s_inv);
         }
         k += run;
-        if (__all_sync(0xffffffffu, q.n >= 0)) break;
+        if (__all_sync(gm, q.n >= 0)) break;
       }
-      // replay R's control flow over the 31 counts (generate.py:237-273)
+      // replay R's control flow over the counts (generate.py:237-273)
       int node = 0;
-      for (int lvl = 0; lvl < 5 && node >= 0; ++lvl) {
+      for (int lvl = 0; lvl < kLevels && node >= 0; ++lvl) {
         if (lvl > 0 && fabs(high - low) < c.a.eps) break;  // handled at the top
-        const int n = __shfl_sync(0xffffffffu, q.n, node);
-        const int kend = __shfl_sync(0xffffffffu, q.kend, node);
+        const int n = __shfl_sync(gm, q.n, g0 + node);
+        const int kend = __shfl_sync(gm, q.kend, g0 + node);
         const double g = 0.5 * (low + high);
         passes += 1;
         samples += kend;
@@ -1441,18 +1452,20 @@ __global__ void __launch_bounds__(kGenThreads) gen_bisect_wide_kernel(const GenC
           high_n = n;
           node = 2 * node + 2 < kG ? 2 * node + 2 : -1;
         } else {
-          rec->g_final = g;  // window hit: this pass's segments
-          rec->mode_final = kCount;
+          if (sl == 0) {
+            rec->g_final = g;  // window hit: this pass's segments
+            rec->mode_final = kCount;
+          }
           fin = true;
           break;
         }
       }
     }
-    if (lane == 0) {
+    if (sl == 0) {
       rec->passes = passes;
       rec->samples = samples;
     }
-    __syncwarp();
+    __syncwarp(gm);
   }
 }
 
@@ -1787,7 +1800,11 @@ static int plan_gen(const VdiGenArgs* a, GenPlan& p) {
   p.bisect = p.inv_n <= p.inv_smem
                  ? gen_bisect_kernel<2, 2, 1, VDI_BISECT_MINB, 128, 16, 2, true>
                  : gen_bisect_kernel<2, 2, 1, VDI_BISECT_MINB, 128, 16, 2, false>;
-  p.wide = p.inv_n <= p.inv_smem ? gen_bisect_wide_kernel<true> : gen_bisect_wide_kernel<false>;
+#ifndef VDI_WIDE_LANES
+#define VDI_WIDE_LANES 32
+#endif
+  p.wide = p.inv_n <= p.inv_smem ? gen_bisect_wide_kernel<VDI_WIDE_LANES, true>
+                                 : gen_bisect_wide_kernel<VDI_WIDE_LANES, false>;
   // the emit kernel uses no shared memory: give the unified L1 everything
   p.emit = gen_emit_kernel<true>;
   cudaFuncSetAttribute(p.emit, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
@@ -2035,6 +2052,10 @@ int gen_launch(const VdiGenArgs* a, cudaStream_t stream) {
   GenPlan p;
   int rc = plan_gen(&c.a, p);
   c.wide_after = p.n_rays < kWideRays ? VDI_WIDE_AFTER : (1 << 30);
+#ifndef VDI_WIDE_TAIL
+#define VDI_WIDE_TAIL 0
+#endif
+  c.wide_tail = VDI_WIDE_TAIL;
   if (rc != VDI_OK) return rc;
   const size_t need = gen_workspace_bytes(&c.a, 0);
   if (a->workspace_bytes < need)
