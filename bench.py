@@ -44,7 +44,9 @@ def parse():
     p.add_argument("--cpu-seconds", type=float, default=12.0,
                    help="target CPU time of the bounded cpu_baseline sample")
     p.add_argument("--no-cpu-baseline", action="store_true")
-    p.add_argument("--e2e-steps", type=int, default=8)
+    p.add_argument("--e2e-steps", type=int, default=20,
+                   help="frames per e2e measurement (the stream's first upload and last "
+                        "readback are not overlapped; more frames amortise them)")
     p.add_argument("--bricked", action="store_true",
                    help="C5 placement: contiguous generation bands, each rank keeping only "
                         "its voxel box resident (shard.band_volume_box)")

@@ -306,25 +306,42 @@ __global__ void dec_segs_kernel(const uint8_t* __restrict__ src, long long n, in
     s_tmp[lane] = w;
   }
   __syncthreads();
-  if (l >= n) return;
-  const long long excl = (long long)block_off[blockIdx.x] + (v - cnt) + (wid > 0 ? s_tmp[wid - 1] : 0);
-  const uint8_t* rec = src + kVdi1Header + 2 * n + 24 * excl;
-  float* ls = segs + l * (long long)list_stride(n_sg);
-  float4* c4 = reinterpret_cast<float4*>(ls);
-  for (int k = 0; k < n_sg; ++k) {
-    float f[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-    if (k < cnt) {
-      const uint8_t* r = rec + 24 * k;
-#pragma unroll
-      for (int j = 0; j < 6; ++j) {
-        const unsigned u = (unsigned)r[4 * j] | ((unsigned)r[4 * j + 1] << 8) |
-                           ((unsigned)r[4 * j + 2] << 16) | ((unsigned)r[4 * j + 3] << 24);
-        f[j] = __uint_as_float(u);
+  // one warp per list of the block: the list's list-SoA slot (stride
+  // floats, zero tail) written coalesced, its packed records read coalesced
+  __shared__ long long s_excl[kEncBlock];
+  __shared__ int s_cnt[kEncBlock];
+  s_excl[threadIdx.x] = (long long)block_off[blockIdx.x] + (v - cnt) + (wid > 0 ? s_tmp[wid - 1] : 0);
+  s_cnt[threadIdx.x] = cnt;
+  __syncthreads();
+  const int stride = list_stride(n_sg);
+  const long long l0 = (long long)blockIdx.x * kEncBlock;
+  // the records are 4-byte aligned when the stream is and 2 n is
+  const bool al4 = ((reinterpret_cast<uintptr_t>(src) + kVdi1Header + 2 * n) & 3) == 0;
+  for (int j = wid; j < kEncBlock && l0 + j < n; j += kEncBlock / 32) {
+    const int c = s_cnt[j];
+    const uint8_t* rec = src + kVdi1Header + 2 * n + 24 * s_excl[j];
+    float* ls = segs + (l0 + j) * (long long)stride;
+    for (int q = lane; q < stride; q += 32) {
+      int k, f;  // supersegment, field of its record [front, back, r, g, b, a]
+      if (q < 4 * n_sg) {
+        k = q >> 2;
+        f = 2 + (q & 3);
+      } else if (q < 5 * n_sg) {
+        k = q - 4 * n_sg;
+        f = 0;
+      } else {
+        k = q - 5 * n_sg;  // >= n_sg in the pad
+        f = 1;
       }
+      float val = 0.f;
+      if (k < c) {
+        const uint8_t* r = rec + 24 * k + 4 * f;
+        val = al4 ? __ldg(reinterpret_cast<const float*>(r))
+                  : __uint_as_float((unsigned)r[0] | ((unsigned)r[1] << 8) |
+                                    ((unsigned)r[2] << 16) | ((unsigned)r[3] << 24));
+      }
+      ls[q] = val;
     }
-    ls[front_off(n_sg) + k] = f[0];
-    ls[back_off(n_sg) + k] = f[1];
-    c4[k] = make_float4(f[2], f[3], f[4], f[5]);
   }
 }
 
