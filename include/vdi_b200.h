@@ -63,7 +63,7 @@
 extern "C" {
 #endif
 
-#define VDI_ABI_VERSION 5
+#define VDI_ABI_VERSION 6
 
 #define VDI_OK 0
 #define VDI_EINVAL (-1)
@@ -130,6 +130,11 @@ typedef struct VdiGenArgs {
   int32_t sub_origin[3];
   int32_t sub_dims[3];
   uint32_t* sub_oob;
+  /* Contiguous row range (a load-balanced band of a bricked placement):
+   * when row_count > 0, this launch's rays are image rows [row_base,
+   * row_base + row_count) and band_rows / band_stride / band_offset are
+   * ignored; local row j is image row row_base + j. */
+  int32_t row_base, row_count;
 } VdiGenArgs;
 
 /* AccelGrid: per-cell supersegment counts (generate.py:322-346). `grid` is
@@ -144,6 +149,7 @@ typedef struct VdiGridArgs {
   int32_t gx, gy, gz;
   int32_t band_rows, band_stride, band_offset;
   int32_t clear;
+  int32_t row_base, row_count;  /* as VdiGenArgs */
 } VdiGridArgs;
 
 /* Novel-view rendering (raycast.py:275-456). The VDI is read through a band
@@ -194,6 +200,10 @@ typedef struct VdiRenderArgs {
    * counters_exact is 1. 0: the reference's order (ESS, then search). */
   int32_t lists_sorted;
   int32_t counters_exact;
+  /* optional (may be NULL): storage row of every list row of the VDI
+   * (vdi_h entries), overriding the vdi_band_* map -- the gathered VDI of
+   * contiguous bands of unequal height (VdiGenArgs.row_count). */
+  const int32_t* vdi_row_map;
 } VdiRenderArgs;
 
 /* Ground-truth direct volume rendering (dvr.py:21-89): the generation ray,

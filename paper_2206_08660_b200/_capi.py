@@ -29,6 +29,7 @@ class VdiGenArgs(ctypes.Structure):
         ("width", _I), ("height", _I), ("n_sg", _I), ("delta", _I),
         ("band_rows", _I), ("band_stride", _I), ("band_offset", _I), ("brick_log2", _I),
         ("sub_origin", _I * 3), ("sub_dims", _I * 3), ("sub_oob", _P),
+        ("row_base", _I), ("row_count", _I),
     ]
 
 
@@ -38,6 +39,7 @@ class VdiGridArgs(ctypes.Structure):
         ("near", _D), ("far", _D), ("proj_a", _D), ("proj_b", _D),
         ("width", _I), ("height", _I), ("n_sg", _I), ("gx", _I), ("gy", _I), ("gz", _I),
         ("band_rows", _I), ("band_stride", _I), ("band_offset", _I), ("clear", _I),
+        ("row_base", _I), ("row_count", _I),
     ]
 
 
@@ -54,6 +56,7 @@ class VdiRenderArgs(ctypes.Structure):
         ("vdi_band_rows", _I), ("vdi_band_world", _I), ("vdi_rows_per_rank", _I),
         ("band_rows", _I), ("band_stride", _I), ("band_offset", _I),
         ("list_tiles", _P), ("grid_zmask", _P), ("lists_sorted", _I), ("counters_exact", _I),
+        ("vdi_row_map", _P),
     ]
 
 
@@ -193,7 +196,7 @@ def load():
                  "vdi_find_first_batch", "vdi_segs_to_aos", "vdi_segs_from_aos",
                  "vdi_list_tiles", "vdi_grid_zmask"):
         getattr(L, name).restype = ctypes.c_int
-    if L.vdi_abi_version() != 5:
+    if L.vdi_abi_version() != 6:
         raise VdiError("libvdi_b200.so ABI mismatch")
     _lib = L
     return L

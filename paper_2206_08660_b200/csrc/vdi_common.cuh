@@ -138,6 +138,14 @@ __device__ __forceinline__ int band_global_row(int local_row, int band_rows, int
   return (j * stride + offset) * band_rows + (local_row - j * band_rows);
 }
 
+// Local row -> image row, with the contiguous-range override
+// (VdiGenArgs.row_count > 0: rows [row_base, row_base + row_count)).
+__device__ __forceinline__ int image_row(int local_row, int band_rows, int stride, int offset,
+                                         int row_base, int row_count) {
+  return row_count > 0 ? row_base + local_row
+                       : band_global_row(local_row, band_rows, stride, offset);
+}
+
 // Storage row of list row r in an all-gathered band-sharded VDI.
 __device__ __forceinline__ int vdi_storage_row(int r, int band_rows, int world,
                                                int rows_per_rank) {

@@ -434,7 +434,8 @@ __device__ __forceinline__ void init_bisection(const GenConst& c, RayState& s) {
 // miss (the list is then published empty).
 __device__ bool setup_ray(const GenConst& c, RayState& s, int list) {
   const int lx = list % c.a.width, ly = list / c.a.width;
-  const int gy = band_global_row(ly, c.a.band_rows, c.a.band_stride, c.a.band_offset);
+  const int gy = image_row(ly, c.a.band_rows, c.a.band_stride, c.a.band_offset, c.a.row_base,
+                           c.a.row_count);
   s.list = list;
   s.seg = c.a.segs + (long long)list * list_stride(c.a.n_sg);
   pixel_ray(c.a.inv_pv, c.a.eye, lx, gy, c.a.width, c.a.height, s.d);
@@ -1825,8 +1826,8 @@ static int plan_gen(const VdiGenArgs* a, GenPlan& p) {
   if (p.per_sm_fused < 1) p.per_sm_fused = 1;
   const int bands = a->band_rows > 0 ? a->band_rows : 16;
   p.n_rays = (long long)a->width *
-             local_rows(a->height, bands, a->band_stride > 0 ? a->band_stride : 1,
-                        a->band_offset);
+             launch_rows(a->height, bands, a->band_stride > 0 ? a->band_stride : 1,
+                         a->band_offset, a->row_count);
   auto up = [](size_t x) { return (x + 255) & ~(size_t)255; };
   p.off_ctl = 0;
   p.off_inv = up(sizeof(RoundCtl) * (kRounds + 1));
@@ -2000,7 +2001,8 @@ int gen_launch(const VdiGenArgs* a, cudaStream_t stream) {
   const int band_rows = a->band_rows > 0 ? a->band_rows : 16;
   c.a.band_rows = band_rows;
   if (c.a.band_stride <= 0) c.a.band_stride = 1;
-  c.local_h = local_rows(a->height, band_rows, c.a.band_stride, c.a.band_offset);
+  c.local_h =
+      launch_rows(a->height, band_rows, c.a.band_stride, c.a.band_offset, c.a.row_count);
   c.tiles_x = (a->width + kTileW - 1) / kTileW;
   const long long tiles_y = (c.local_h + kTileH - 1) / kTileH;
   c.n_slots = (long long)c.tiles_x * tiles_y * 32;

@@ -23,7 +23,8 @@ __global__ void grid_kernel(const GridConst c) {
   const int n = a.counts[list];
   if (n == 0) return;
   const int lrow = (int)(list / a.width), lx = (int)(list % a.width);
-  const long long ly = band_global_row(lrow, a.band_rows, a.band_stride, a.band_offset);
+  const long long ly =
+      image_row(lrow, a.band_rows, a.band_stride, a.band_offset, a.row_base, a.row_count);
   const int cy0 = (int)((ly * a.gy) / a.height);
   const int cy1 = (int)(((ly + 1) * a.gy - 1) / a.height);
   const int cx0 = (int)(((long long)lx * a.gx) / a.width);
@@ -52,7 +53,8 @@ int grid_launch(const VdiGridArgs* args, cudaStream_t stream) {
   c.a = *args;
   if (c.a.band_rows <= 0) c.a.band_rows = 16;
   if (c.a.band_stride <= 0) c.a.band_stride = 1;
-  c.local_h = local_rows(args->height, c.a.band_rows, c.a.band_stride, c.a.band_offset);
+  c.local_h = launch_rows(args->height, c.a.band_rows, c.a.band_stride, c.a.band_offset,
+                          c.a.row_count);
   cudaError_t err;
   if (args->clear) {
     err = cudaMemsetAsync(args->grid, 0,

@@ -20,6 +20,11 @@ inline int local_rows(int h, int band_rows, int stride, int offset) {
   return n;
 }
 
+// Rows of a launch: the contiguous range when row_count > 0, else the band map.
+inline int launch_rows(int h, int band_rows, int stride, int offset, int row_count) {
+  return row_count > 0 ? row_count : local_rows(h, band_rows, stride, offset);
+}
+
 int gen_launch(const VdiGenArgs* a, cudaStream_t stream);
 size_t gen_workspace_bytes(const VdiGenArgs* a, int recommended);
 int grid_launch(const VdiGridArgs* a, cudaStream_t stream);

@@ -26,6 +26,14 @@ constexpr int kRenderThreads = 128;
 #define VDI_RENDER_MINB 5  // 96 registers, no spills (C3 0.93 ms; 6: 1.03, 4: 1.00)
 #endif
 
+// Storage row of VDI list row r: the explicit map when given
+// (VdiRenderArgs.vdi_row_map), else the band map.
+__device__ __forceinline__ int storage_row(const VdiRenderArgs& a, int r) {
+  return a.vdi_row_map ? __ldg(a.vdi_row_map + r)
+                       : vdi_storage_row(r, a.vdi_band_rows, a.vdi_band_world,
+                                         a.vdi_rows_per_rank);
+}
+
 struct RenderConst {
   VdiRenderArgs a;
   int tiles_x;
@@ -284,8 +292,7 @@ __global__ void __launch_bounds__(kRenderThreads, VDI_RENDER_MINB) render_kernel
         double s_cur = 0.0;
         const int max_iter = vdi_w + vdi_h + 4;
         const int32_t* rowp =
-            a.counts + (long long)vdi_storage_row(cy, a.vdi_band_rows, a.vdi_band_world,
-                                                  a.vdi_rows_per_rank) * vdi_w;
+            a.counts + (long long)storage_row(a, cy) * vdi_w;
         // a list of an empty tile has count 0: no load
         auto load_count = [&](const int32_t* rp, int x, int y) -> int {
           if (kTiles && !((s_tiles[(y >> 3) * c.lt_wpr + (x >> 8)] >> ((x >> 3) & 31)) & 1u))
@@ -315,9 +322,7 @@ __global__ void __launch_bounds__(kRenderThreads, VDI_RENDER_MINB) render_kernel
             if (!kBands) {
               nrowp = a.counts + (long long)ncy * vdi_w;
             } else if (!xs) {
-              nrowp = a.counts + (long long)vdi_storage_row(ncy, a.vdi_band_rows,
-                                                            a.vdi_band_world,
-                                                            a.vdi_rows_per_rank) * vdi_w;
+              nrowp = a.counts + (long long)storage_row(a, ncy) * vdi_w;
             }
             ncnt = load_count(nrowp, ncx, ncy);
           }
@@ -386,7 +391,7 @@ int render_launch(const VdiRenderArgs* args, cudaStream_t stream) {
   const size_t smem = sizeof(uint32_t) * (size_t)c.lt_words;
   // kBands: the VDI is an all-gathered band-sharded one (storage-row map)
   void (*fn)(RenderConst);
-  if (c.a.vdi_band_world > 1)
+  if (c.a.vdi_band_world > 1 || c.a.vdi_row_map)
     fn = c.lt_words ? (mask ? render_kernel<true, true, true> : render_kernel<true, false, true>)
                     : (mask ? render_kernel<false, true, true> : render_kernel<false, false, true>);
   else

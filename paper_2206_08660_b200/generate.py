@@ -101,9 +101,10 @@ def alloc_gen(width, rows, n_sg, grid_dims, stats=True):
 
 def gen_args(vol_dev, voxel_type, dims, lut_dev, cam, aabb, params_resolved, n_sg, eps,
              gamma_init, bufs: GenBuffers, band=(16, 1, 0), bricks=None,
-             ess_max=-1.0, cells=None, sub=None) -> _capi.VdiGenArgs:
+             ess_max=-1.0, cells=None, sub=None, rows=None) -> _capi.VdiGenArgs:
     """sub: (origin, box dims, oob flag tensor) when vol_dev holds only a
-    resident box of the dims volume (VdiGenArgs.sub_*)."""
+    resident box of the dims volume (VdiGenArgs.sub_*). rows: (row_base,
+    row_count), a contiguous range of image rows instead of the band map."""
     delta, step, lref = params_resolved
     width, height = cam.viewport
     a = _capi.VdiGenArgs()
@@ -131,11 +132,13 @@ def gen_args(vol_dev, voxel_type, dims, lut_dev, cam, aabb, params_resolved, n_s
             a.sub_origin[k] = int(org[k])
             a.sub_dims[k] = int(box[k])
         a.sub_oob = dv.ptr(oob)
+    if rows is not None:
+        a.row_base, a.row_count = int(rows[0]), int(rows[1])
     return a
 
 
 def grid_args(bufs: GenBuffers, cam, width, height, n_sg, grid_dims, band=(16, 1, 0),
-              clear=True) -> _capi.VdiGridArgs:
+              clear=True, rows=None) -> _capi.VdiGridArgs:
     pa, pb = depth_consts(cam.near, cam.far)
     g = _capi.VdiGridArgs()
     g.segs, g.counts, g.grid = dv.ptr(bufs.segs), dv.ptr(bufs.counts), dv.ptr(bufs.grid)
@@ -144,13 +147,15 @@ def grid_args(bufs: GenBuffers, cam, width, height, n_sg, grid_dims, band=(16, 1
     g.gx, g.gy, g.gz = (int(v) for v in grid_dims)
     g.band_rows, g.band_stride, g.band_offset = (int(v) for v in band)
     g.clear = int(clear)
+    if rows is not None:
+        g.row_base, g.row_count = int(rows[0]), int(rows[1])
     return g
 
 
 def launch_generate(vol_dev, voxel_type, dims, lut_dev, cam, aabb, params, resolved,
                     bufs: GenBuffers, grid_dims, band=(16, 1, 0), stream=None,
                     split_events=None, workspace_bytes=None, bricks=None, ess_max=-1.0,
-                    cells=None, sub=None):
+                    cells=None, sub=None, rows=None):
     """Enqueue generation + grid on the current stream (no sync, no alloc).
     split_events: optional CUDA events; [1] and [2] bracket the generation
     kernel (timing only). workspace_bytes overrides the recommended scratch
@@ -159,7 +164,7 @@ def launch_generate(vol_dev, voxel_type, dims, lut_dev, cam, aabb, params, resol
     L = _capi.load()
     s = dv.stream_handle() if stream is None else stream
     a = gen_args(vol_dev, voxel_type, dims, lut_dev, cam, aabb, resolved, params.n_sg,
-                 params.epsilon, params.gamma_init, bufs, band, bricks, ess_max, cells, sub)
+                 params.epsilon, params.gamma_init, bufs, band, bricks, ess_max, cells, sub, rows)
     if workspace_bytes == "min":
         need = int(L.vdi_gen_workspace_min_bytes(a))
     elif workspace_bytes is not None:
@@ -178,7 +183,7 @@ def launch_generate(vol_dev, voxel_type, dims, lut_dev, cam, aabb, params, resol
     if split_events:
         split_events[2].record()
     w, h = cam.viewport
-    g = grid_args(bufs, cam, w, h, params.n_sg, grid_dims, band)
+    g = grid_args(bufs, cam, w, h, params.n_sg, grid_dims, band, rows=rows)
     _capi.check(L.vdi_grid_launch(g, s))
 
 

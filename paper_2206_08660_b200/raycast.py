@@ -73,6 +73,7 @@ def render_args(dvdi, n_sg, vdi_w, vdi_h, gen_cam, aabb, grid_dev, grid_dims, gr
     a.vdi_rows_per_rank = int(dvdi.rows_per_rank)
     a.band_rows, a.band_stride, a.band_offset = (int(v) for v in band)
     a.lists_sorted = int(bool(getattr(dvdi, "sorted", False)))
+    a.vdi_row_map = dv.ptr(getattr(dvdi, "row_map", None))
     if counters_exact is None:
         counters_exact = per_pixel is not None or stat_sums is not None
     a.counters_exact = int(bool(counters_exact))

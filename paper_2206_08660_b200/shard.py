@@ -133,6 +133,33 @@ def brick_slabs(nz: int, world: int, log2: int = 3):
     return per, nbz, out
 
 
+def balance_bands(row_cost, world: int) -> list:
+    """Boundaries b_0 = 0 < ... < b_world = H of contiguous row bands with
+    near-equal total cost (row_cost: per-image-row work, e.g. the executed
+    samples of the previous frame's rows): b_r is the first row whose cost
+    prefix reaches r / world of the total. Every band keeps >= 1 row."""
+    c = np.asarray(row_cost, np.float64)
+    h = len(c)
+    pre = np.concatenate([[0.0], np.cumsum(np.maximum(c, 0.0) + 1e-9)])
+    tot = pre[-1]
+    b = [0]
+    for r in range(1, world):
+        k = int(np.searchsorted(pre, tot * r / world, side="left"))
+        b.append(min(max(k, b[-1] + 1), h - (world - r)))
+    b.append(h)
+    return b
+
+
+def row_storage_map(bounds, rows_per_rank: int) -> np.ndarray:
+    """Storage row of every image row after the all-gather of contiguous
+    bands padded to rows_per_rank (VdiRenderArgs.vdi_row_map)."""
+    out = np.empty(bounds[-1], np.int32)
+    for q in range(len(bounds) - 1):
+        r0, r1 = bounds[q], bounds[q + 1]
+        out[r0:r1] = q * rows_per_rank + np.arange(r1 - r0)
+    return out
+
+
 class PackedExchange:
     """The VDI exchange as packed VDI1 shards instead of the padded list-SoA:
     each rank packs its rows (vdi_encode_vdi1: counts u16 + valid
@@ -218,13 +245,16 @@ class Pipeline:
     image, device-resident, for one rank."""
 
     def __init__(self, vol, tf, gcam, rcam, params, world=1, rank=0, opts=None,
-                 bricked=False, box_volume=None):
+                 bricked=False, box_volume=None, band_bounds=None):
         """bricked: generation takes contiguous row bands (rank r: rows
         [r B, (r + 1) B), B = ceil(H / world)) and keeps only the voxel box
         those rays sample (band_volume_box) resident -- the C5 placement,
         "bricked across 8 x B200". box_volume(origin, size) -> device tensor
         (size[2], size[1], size[0]) supplies that box (default: sliced from
-        `vol`). Rendering keeps the interleaved 16-row bands."""
+        `vol`). band_bounds (bricked): world + 1 row boundaries of contiguous
+        bands of unequal height (balance_bands of the previous frame's
+        per-row cost) instead of equal ones. Rendering keeps the interleaved
+        16-row bands."""
         t = dv.require_cuda()
         self.t = t
         self.vol, self.tf, self.gcam, self.rcam, self.params = vol, tf, gcam, rcam, params
@@ -237,9 +267,18 @@ class Pipeline:
         self.bricked = bricked
         self.gen_band_rows = -(-h // world) if bricked else BAND_ROWS
         self.sub = None
+        self.gen_range = None  # (row_base, row_count) of unequal contiguous bands
+        self.band_bounds = None
+        if bricked and band_bounds is not None:
+            self.band_bounds = [int(x) for x in band_bounds]
+            assert len(self.band_bounds) == world + 1 and self.band_bounds[-1] == h
         if bricked:
-            r0 = rank * self.gen_band_rows
-            r1 = min(h, r0 + self.gen_band_rows)
+            if self.band_bounds is not None:
+                r0, r1 = self.band_bounds[rank], self.band_bounds[rank + 1]
+                self.gen_range = (r0, r1 - r0)
+            else:
+                r0 = rank * self.gen_band_rows
+                r1 = min(h, r0 + self.gen_band_rows)
             org, size = band_volume_box(vol, gcam, r0, max(r1, r0 + 1))
             self.box = (org, size)
             if box_volume is not None:
@@ -290,6 +329,10 @@ class Pipeline:
         self.gen_band = (self.gen_band_rows, world, rank)
         self.gen_rows = rows_per_rank(h, world, self.gen_band_rows)
         self.local_gen_rays = local_rows(h, world, rank, self.gen_band_rows) * w
+        if self.gen_range is not None:
+            b = self.band_bounds
+            self.gen_rows = max(b[q + 1] - b[q] for q in range(world))
+            self.local_gen_rays = self.gen_range[1] * w
         self.bufs = alloc_gen(w, self.gen_rows, params.n_sg, self.grid_dims, stats=True)
         self.bufs.counts.zero_()  # padding rows stay empty
         ow, oh = rcam.viewport
@@ -313,8 +356,11 @@ class Pipeline:
                                   dtype=t.float32, device="cuda")
             self.g_image = t.empty((world * self.out_rows, ow, 4), dtype=t.float64,
                                    device="cuda")
+            row_map = None
+            if self.gen_range is not None:
+                row_map = dv.to_device(row_storage_map(self.band_bounds, self.gen_rows))
             self.dvdi = DeviceVdi(self.g_counts, self.g_segs, self.gen_band_rows, world,
-                                  self.gen_rows, sorted=True)
+                                  self.gen_rows, sorted=True, row_map=row_map)
             from .tuning import TUNING
             self.packed = PackedExchange(self) if TUNING.packed_exchange else None
         else:
@@ -343,7 +389,8 @@ class Pipeline:
         launch_generate(vol_dev, self.vt, self.vol.dims, self.lut_dev, self.gcam,
                         self.aabb, self.params, self.resolved, self.bufs, self.grid_dims,
                         band=self.gen_band, split_events=ev, bricks=self.bricks,
-                        ess_max=self.ess_max, cells=self.cells, sub=self.sub)
+                        ess_max=self.ess_max, cells=self.cells, sub=self.sub,
+                        rows=self.gen_range)
         if timed:
             ev[3].record()
         if self.world > 1:
@@ -426,7 +473,7 @@ class Pipeline:
         launch_generate(vol_dev, self.vt, self.vol.dims, self.lut_dev, self.gcam,
                         self.aabb, self.params, self.resolved, self.bufs, self.grid_dims,
                         band=self.gen_band, bricks=self.bricks, ess_max=self.ess_max,
-                        cells=self.cells, sub=self.sub)
+                        cells=self.cells, sub=self.sub, rows=self.gen_range)
 
     def samples_executed(self) -> int:
         return int(self.bufs.samples.to(self.t.int64).sum().item())

@@ -55,6 +55,9 @@ class DeviceVdi:
     # (_emit clamps, generate.py:58-62); lets the render search before the
     # ESS test (VdiRenderArgs.lists_sorted)
     sorted: bool = False
+    # storage row of every list row (device int32), overriding the band map:
+    # the gathered VDI of contiguous bands of unequal height
+    row_map: object = None
 
 
 class Vdi:

@@ -23,7 +23,7 @@ from paper_2206_08660_b200 import generate as gen  # noqa: E402
 from paper_2206_08660_b200 import shard, synth  # noqa: E402
 
 
-def _check(cfg, world, box_volume=None, max_frac=0.75):
+def _check(cfg, world, box_volume=None, max_frac=0.75, balanced=False):
     vol, tf, gcam, rcam, n_sg = synth.config(cfg)
     params = vb.GenParams(n_sg=n_sg)
     vdi, grid, st = vb.generate_vdi(vol, tf, gcam, params, with_stats=True)
@@ -34,16 +34,23 @@ def _check(cfg, world, box_volume=None, max_frac=0.75):
     w, h = gcam.viewport
     full_bytes = int(np.prod(vol.dims)) * (1 if vol.voxel_type == "u8" else 4)
     grid_sum = torch.zeros_like(grid.device())
+    bounds = shard.balance_bands(st.samples.sum(axis=1), world) if balanced else None
+    shards = []
     for r in range(world):
         p = shard.Pipeline(vol, tf, gcam, rcam, params, world=world, rank=r, bricked=True,
-                           box_volume=box_volume)
+                           box_volume=box_volume, band_bounds=bounds)
         p.generate_only()
         torch.cuda.synchronize()
         assert int(p.oob.item()) == 0, f"rank {r}: sample outside the resident box {p.box}"
         res = p.vol_dev.numel() * p.vol_dev.element_size()
         assert res <= max_frac * full_bytes, (r, p.box)
-        r0 = r * p.gen_band_rows
-        n = min(h, r0 + p.gen_band_rows) - r0
+        if balanced:
+            r0, n = p.gen_range
+            per = p.gen_rows
+            shards.append((p.bufs.counts.clone(), p.bufs.segs.clone()))
+        else:
+            r0 = r * p.gen_band_rows
+            n = min(h, r0 + p.gen_band_rows) - r0
         assert torch.equal(p.bufs.counts[:n], d.counts[r0:r0 + n]), r
         seg_rows = p.bufs.segs.view(-1, w, p.bufs.segs.shape[1])[:n]
         full_rows = d.segs.view(-1, w, d.segs.shape[1])[r0:r0 + n]
@@ -53,10 +60,33 @@ def _check(cfg, world, box_volume=None, max_frac=0.75):
         del p
         torch.cuda.empty_cache()
     assert torch.equal(grid_sum, grid.device())  # the all-reduce of the partial grids
+    if balanced:
+        # the all-gathered storage (shards padded to the tallest band), read by
+        # the render through VdiRenderArgs.vdi_row_map: the natural render
+        from paper_2206_08660_b200 import device as dv
+        from paper_2206_08660_b200.vdi import DeviceVdi
+        g_counts = torch.cat([c for c, _ in shards])
+        g_segs = torch.cat([s_ for _, s_ in shards])
+        rmap = dv.to_device(shard.row_storage_map(bounds, per))
+        gvdi = vb.Vdi(w, h, n_sg, None, None, gcam, vol.aabb,
+                      _device=DeviceVdi(g_counts, g_segs, sorted=True, row_map=rmap))
+        ref_img = vb.render_vdi(vdi, grid, rcam).data
+        assert np.array_equal(vb.render_vdi(gvdi, grid, rcam).data, ref_img)
+        img2, st2 = vb.render_vdi(gvdi, grid, rcam, with_stats=True)
+        _, st1 = vb.render_vdi(vdi, grid, rcam, with_stats=True)
+        assert np.array_equal(img2.data, ref_img)
+        assert (st2.lists_visited, st2.supersegments_intersected, st2.lists_searched) == \
+            (st1.lists_visited, st1.supersegments_intersected, st1.lists_searched)
 
 
 def test_bricked_c3_four_ranks():
     _check("C3", 4)
+
+
+def test_bricked_c3_four_ranks_balanced():
+    """Contiguous bands of unequal height from the per-row executed samples
+    (shard.balance_bands), each rank with only its box resident."""
+    _check("C3", 4, balanced=True)
 
 
 def test_bricked_c5_eight_ranks():

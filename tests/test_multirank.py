@@ -7,10 +7,12 @@ pipeline uses (shard.exchange_vdi / shard.gather_rows). The gathered VDI,
 the all-reduced AccelGrid and the gathered image must equal a single-process
 run bit for bit.
 
-Layouts: "interleaved" (16-row bands, rank b % world) and "bricked"
+Layouts: "interleaved" (16-row bands, rank b % world), "bricked"
 (contiguous generation bands, each rank sampling a volume in which every
 voxel outside its planned resident box, shard.band_volume_box, is poisoned:
-any ray that reached outside the box would change the result).
+any ray that reached outside the box would change the result) and
+"balanced" (bricked, with contiguous bands of unequal height from
+shard.balance_bands, gathered through shard.row_storage_map).
 """
 
 import os
@@ -91,8 +93,17 @@ def rank_main(rank, world, port, out, layout="interleaved"):
         band = -(-h // world) if layout == "bricked" else shard.BAND_ROWS
         mine = shard.band_rows(h, world, rank, band)
         per = shard.rows_per_rank(h, world, band)
+        bounds = None
+        if layout == "balanced":
+            # contiguous bands of unequal height (shard.balance_bands of a
+            # per-row cost: here a made-up one that loads the middle rows)
+            cost = 1.0 + np.exp(-((np.arange(h) - 0.45 * h) / (0.12 * h)) ** 2) * 50
+            bounds = shard.balance_bands(cost, world)
+            mine = np.arange(bounds[rank], bounds[rank + 1])
+            per = max(bounds[q + 1] - bounds[q] for q in range(world))
+            assert len(set(bounds[q + 1] - bounds[q] for q in range(world))) > 1
         gvol = vol
-        if layout == "bricked":
+        if layout in ("bricked", "balanced"):
             box = shard.band_volume_box(vol, gcam, int(mine[0]), int(mine[-1]) + 1)
             assert box[1][1] < vol.dims[1]  # a real slab, not the whole volume
             gvol = poisoned(vol, box)
@@ -109,8 +120,10 @@ def rank_main(rank, world, port, out, layout="interleaved"):
         g_counts = torch.empty((world * per, w), dtype=torch.int32)
         g_segs = torch.empty((world * per * w, segs.shape[1]), dtype=torch.float32)
         shard.exchange_vdi(dist, t_counts, t_segs, t_grid, g_counts, g_segs)
-        # band-interleaved storage -> natural rows
-        st = shard.storage_rows(h, world, band)
+        # gathered storage -> natural rows (the render kernel reads the
+        # storage rows through the same maps)
+        st = (shard.storage_rows(h, world, band) if bounds is None
+              else shard.row_storage_map(bounds, per))
         full_counts = g_counts.numpy()[st]
         full_segs = from_list_soa(g_segs.numpy().reshape(world * per, w, -1)[st].reshape(h * w, -1),
                                   n_sg).reshape(h, w, n_sg, 6)
@@ -136,7 +149,8 @@ def free_port():
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("world,layout", [(2, "interleaved"), (2, "bricked")])
+@pytest.mark.parametrize("world,layout", [(2, "interleaved"), (2, "bricked"),
+                                          (2, "balanced"), (3, "balanced")])
 def test_sharded_generate_render_equals_single_process(tmp_path, world, layout):
     out = str(tmp_path / "rank0.npz")
     mp.start_processes(rank_main, args=(world, free_port(), out, layout), nprocs=world,

@@ -45,6 +45,8 @@ def ev():
 
 
 def timed(fn, reps):
+    fn()  # warm-up: first-call allocations (workspace, caches) are not timed
+    torch.cuda.synchronize()
     ts = []
     for _ in range(reps):
         a, b = ev(), ev()
@@ -69,6 +71,9 @@ def main():
     p.add_argument("--worlds", default="1,2,4,8")
     p.add_argument("--reps", type=int, default=3)
     p.add_argument("--bricked", action="store_true")
+    p.add_argument("--balanced", action="store_true",
+                   help="bricked bands of unequal height balanced on the per-row executed "
+                        "samples of the N = 1 step (as the previous frame would give them)")
     a = p.parse_args()
     vol, tf, gcam, rcam, n_sg = synth.config(a.config)
     params = GenParams(n_sg=n_sg)
@@ -81,6 +86,7 @@ def main():
     ref.step()
     torch.cuda.synchronize()
     full_vdi = DeviceVdi(ref.bufs.counts, ref.bufs.segs, sorted=True)
+    row_cost = ref.bufs.samples.sum(dim=1).double().cpu().numpy()
     ref.bufs.workspace = None  # the ranks below size their own generation scratch
     torch.cuda.empty_cache()
     ref_grid = ref.bufs.grid
@@ -93,8 +99,11 @@ def main():
         for r in range(world):
             gen.release_workspace()
             torch.cuda.empty_cache()
+            bounds = (shard.balance_bands(row_cost, world)
+                      if a.bricked and a.balanced and world > 1 else None)
             pipe = shard.Pipeline(vol, tf, gcam, rcam, params, world=world, rank=r,
-                                  bricked=a.bricked and world > 1, box_volume=box_volume)
+                                  bricked=a.bricked and world > 1, box_volume=box_volume,
+                                  band_bounds=bounds)
             if pipe.slabs is not None:  # the other ranks' slabs, as the all-gather leaves them
                 dv.launch_bricks(pipe.vol_dev, pipe.vt, pipe.res_dims, pipe.bricks)
             prep_ms = timed(lambda: pipe.prep(pipe.vol_dev, gather=False), a.reps)
@@ -103,7 +112,7 @@ def main():
                 launch_generate(pipe.vol_dev, pipe.vt, pipe.vol.dims, pipe.lut_dev, pipe.gcam,
                                 pipe.aabb, pipe.params, pipe.resolved, pipe.bufs, pipe.grid_dims,
                                 band=pipe.gen_band, bricks=pipe.bricks, ess_max=pipe.ess_max,
-                                cells=pipe.cells, sub=pipe.sub)
+                                cells=pipe.cells, sub=pipe.sub, rows=pipe.gen_range)
             gen_ms = timed(run_gen, a.reps)
             # exchange: pack this rank's rows, unpack N shards of its size
             enc_ms = dec_ms = 0.0
@@ -154,7 +163,8 @@ def main():
         step = max(kern) + sum(coll.values())
         if base_step is None:
             base_step = step
-        line = {"config": a.config, "bricked": a.bricked, "world": world,
+        line = {"config": a.config, "bricked": a.bricked, "balanced": a.balanced,
+                "world": world,
                 "step_ms": step, "kernels_ms_max": max(kern), "kernels_ms_min": min(kern),
                 "imbalance": max(kern) / max(min(kern), 1e-9), "collectives_ms": coll,
                 "projected_speedup": base_step / step, "ranks": ranks}
