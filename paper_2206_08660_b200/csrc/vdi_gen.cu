@@ -972,6 +972,14 @@ __global__ void __launch_bounds__(kThreads, kMinB) gen_bisect_kernel(const GenCo
           have = true;
           top = true;
           reps = 0;
+          if (c.wide_after == 0 && c.wide != nullptr) {  // straight to the wide phase
+            rec->low = low;
+            rec->high = high;
+            rec->last_n = last_n;
+            rec->high_n = high_n;
+            c.wide[atomicAdd(&c.ctl->nwide, 1ull)] = (int)(rec - c.recs);
+            have = false;
+          }
         }
       }
     }
