@@ -1,48 +1,80 @@
-"""Key numbers of one ncu --set full report: speed of light, occupancy, warp
-state, stall reasons, DRAM traffic, and the hottest SASS lines by stall samples.
+"""Markdown table of the key `ncu --set full` metrics of every kernel in a
+report (one column per launch):
 
-usage: python tools/ncu_summary.py report.ncu-rep [top_n]
+    python tools/ncu_summary.py gpurun_out/r02_gen_phases.ncu-rep
 """
 import csv
 import io
+import re
 import subprocess
 import sys
 
-rep = sys.argv[1]
-top_n = int(sys.argv[2]) if len(sys.argv) > 2 else 12
+KEYS = [
+    ("Duration", "duration"),
+    ("Registers Per Thread", "registers / thread"),
+    ("Theoretical Occupancy", "theoretical occupancy %"),
+    ("Achieved Active Warps Per SM", "achieved warps / SM"),
+    ("Compute (SM) Throughput", "compute (SM) throughput %"),
+    ("Issued Ipc Active", "issued IPC (active)"),
+    ("Issue Slots Busy", "issue slots busy %"),
+    ("Warp Cycles Per Issued Instruction", "warp cycles / issued inst"),
+    ("Avg. Active Threads Per Warp", "active threads / warp"),
+    ("Executed Instructions", "warp instructions"),
+    ("DRAM Throughput", "DRAM throughput % of peak"),
+    ("L1/TEX Hit Rate", "L1 hit %"),
+    ("L2 Hit Rate", "L2 hit %"),
+    ("SM Active Cycles", "SM active cycles"),
+    ("Elapsed Cycles", "elapsed cycles"),
+]
 
 
-def ncu(*args):
-    return subprocess.run(["ncu", "-i", rep, *args], capture_output=True, text=True).stdout
+def short(name):
+    m = re.search(r"(\w+)(<[^>]*>)?\(", name)
+    return (m.group(1) + (m.group(2) or "")) if m else name[:40]
 
 
-rows = list(csv.reader(io.StringIO(ncu("--page", "raw", "--csv"))))
-h, v = rows[0], rows[2] if len(rows) > 2 else rows[1]
-raw = dict(zip(h, v))
-keys = ["Kernel Name", "gpu__time_duration.sum", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
-        "gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed",
-        "dram__bytes_read.sum", "dram__bytes_write.sum", "lts__t_sector_hit_rate.pct",
-        "l1tex__t_sector_hit_rate.pct", "sm__warps_active.avg.pct_of_peak_sustained_active",
-        "smsp__issue_active.avg.pct_of_peak_sustained_active",
-        "smsp__thread_inst_executed_per_inst_executed.ratio", "smsp__inst_executed.sum",
-        "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
-        "launch__registers_per_thread", "launch__grid_size", "launch__block_size"]
-for k in keys:
-    if k in raw:
-        print(f"{k} = {raw[k]}")
-st = [(k, float(val)) for k, val in raw.items()
-      if k.startswith("smsp__average_warps_issue_stalled_") and k.endswith("_per_issue_active.ratio")
-      and val.replace(".", "", 1).isdigit()]
-st.sort(key=lambda x: -x[1])
-print("stalls per issue:", ", ".join(f"{k[34:-23]}={x:.2f}" for k, x in st[:8]))
-src = list(csv.reader(io.StringIO(ncu("--page", "source", "--csv", "--print-source", "sass"))))
-hh = src[1]
-data = src[2:]
-iA, iS, iT = hh.index("Address"), hh.index("Source"), hh.index("Warp Stall Sampling (All Samples)")
-tot = sum(float(r[iT] or 0) for r in data)
-print(f"stall samples: {tot:.0f}; hottest SASS:")
-reasons = [c for c in hh if c.startswith("stall_") and "Not Issued" not in c]
-for i in sorted(range(len(data)), key=lambda i: -float(data[i][iT] or 0))[:top_n]:
-    r = data[i]
-    why = max(reasons, key=lambda c: float(r[hh.index(c)] or 0))
-    print(f"  {r[iA][-5:]} {100 * float(r[iT]) / tot:5.1f}% {why:22s} {r[iS].strip()[:70]}")
+def main(path):
+    out = subprocess.run(["ncu", "-i", path, "--page", "details", "--csv"], capture_output=True,
+                         text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    h = rows[0]
+    iI, iK, iS, iM, iU, iV = (h.index(x) for x in ("ID", "Kernel Name", "Section Name",
+                                                  "Metric Name", "Metric Unit", "Metric Value"))
+    launches = {}
+    for r in rows[1:]:
+        if len(r) <= iV:
+            continue
+        d = launches.setdefault(r[iI], {"name": r[iK]})
+        key = r[iM]
+        if key == "Memory Throughput" and r[iU] != "Gbyte/s":
+            continue
+        d.setdefault(key, (r[iV], r[iU]))
+    # warp-state stall breakdown is in the raw page; keep the table to the details page
+    ids = list(launches)
+    print("| metric | " + " | ".join(f"#{i} {short(launches[i]['name'])}" for i in ids) + " |")
+    print("|---|" + "---|" * len(ids))
+    for k, label in KEYS:
+        vals = []
+        for i in ids:
+            v = launches[i].get(k)
+            vals.append(f"{v[0]} {v[1]}".strip() if v and k in ("Duration",) else (v[0] if v else ""))
+        print(f"| {label} | " + " | ".join(vals) + " |")
+    # stall reasons (PC samples) from the raw page, top 5 per launch
+    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
+                         text=True).stdout
+    rr = list(csv.reader(io.StringIO(raw)))
+    hh = rr[0]
+    tops = []
+    for r in rr[2:]:
+        d = dict(zip(hh, r))
+        st = {k.replace("smsp__pcsamp_warps_issue_stalled_", ""): float(v.replace(",", "") or 0)
+              for k, v in d.items()
+              if k.startswith("smsp__pcsamp_warps_issue_stalled_") and not k.endswith("not_issued")}
+        tot = sum(st.values()) or 1.0
+        top = sorted(st.items(), key=lambda x: -x[1])[:5]
+        tops.append(", ".join(f"{k} {100 * v / tot:.1f} %" for k, v in top))
+    print("| stall reasons (PC samples) | " + " | ".join(tops) + " |")
+
+
+if __name__ == "__main__":
+    main(sys.argv[1])
