@@ -63,7 +63,7 @@
 extern "C" {
 #endif
 
-#define VDI_ABI_VERSION 6
+#define VDI_ABI_VERSION 7
 
 #define VDI_OK 0
 #define VDI_EINVAL (-1)
@@ -204,6 +204,15 @@ typedef struct VdiRenderArgs {
    * (vdi_h entries), overriding the vdi_band_* map -- the gathered VDI of
    * contiguous bands of unequal height (VdiGenArgs.row_count). */
   const int32_t* vdi_row_map;
+  /* optional (may be NULL): vdi_list_ranges() of the VDI, two floats per
+   * storage list: (min front, max back), (+inf, -inf) for an empty list and
+   * (-inf, +inf) for a list holding a NaN depth. Used with lists_sorted on
+   * forward chords when counters_exact is 0: a list whose range the chord
+   * piece [d_entry, d_exit] misses (d_exit < min front or d_entry > max back)
+   * has no supersegment with back >= d_entry and front <= d_exit, so the
+   * search would miss; it is skipped without reading the list. Same image
+   * and counters. */
+  const float* list_range;
 } VdiRenderArgs;
 
 /* Ground-truth direct volume rendering (dvr.py:21-89): the generation ray,
@@ -314,6 +323,12 @@ int vdi_list_tiles(const VdiRenderArgs* args, uint32_t* tiles, vdi_stream_t stre
  * accelerator for vdi_render_launch (VdiRenderArgs.grid_zmask). */
 int vdi_grid_zmask(const uint32_t* grid, int32_t gx, int32_t gy, int32_t gz, uint64_t* out,
                    vdi_stream_t stream);
+/* Depth range of every list of a list-SoA VDI (n_lists storage lists):
+ * out[2 l] = min front, out[2 l + 1] = max back over its counts[l] entries;
+ * (+inf, -inf) when empty, (-inf, +inf) when a depth is NaN. An accelerator
+ * for vdi_render_launch (VdiRenderArgs.list_range). */
+int vdi_list_ranges(const float* segs, const int32_t* counts, int64_t n_lists, int32_t n_sg,
+                    float* out, vdi_stream_t stream);
 int vdi_dvr_launch(const VdiDvrArgs* args, vdi_stream_t stream);
 int vdi_preview_launch(const VdiPreviewArgs* args, vdi_stream_t stream);
 /* (h, w, channels) f64 -> (out_h, out_w, channels), preview.py:208-223

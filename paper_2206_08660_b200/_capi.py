@@ -56,7 +56,7 @@ class VdiRenderArgs(ctypes.Structure):
         ("vdi_band_rows", _I), ("vdi_band_world", _I), ("vdi_rows_per_rank", _I),
         ("band_rows", _I), ("band_stride", _I), ("band_offset", _I),
         ("list_tiles", _P), ("grid_zmask", _P), ("lists_sorted", _I), ("counters_exact", _I),
-        ("vdi_row_map", _P),
+        ("vdi_row_map", _P), ("list_range", _P),
     ]
 
 
@@ -121,7 +121,7 @@ EXPORTS = ["vdi_last_error", "vdi_abi_version", "vdi_gen_workspace_bytes",
            "vdi_decode_vdi1_lists", "vdi_find_first_batch",
            "vdi_volume_brick_max", "vdi_selftest_arith", "vdi_segs_to_aos",
            "vdi_segs_from_aos", "vdi_volume_cells_bytes", "vdi_volume_cells", "vdi_volume_cells_masked",
-           "vdi_list_tiles_words", "vdi_list_tiles", "vdi_grid_zmask"]
+           "vdi_list_tiles_words", "vdi_list_tiles", "vdi_grid_zmask", "vdi_list_ranges"]
 
 _lib = None
 
@@ -186,6 +186,7 @@ def load():
     L.vdi_list_tiles_words.argtypes = [_I, _I]
     L.vdi_list_tiles_words.restype = ctypes.c_size_t
     L.vdi_grid_zmask.argtypes = [_P, _I, _I, _I, _P, _P]
+    L.vdi_list_ranges.argtypes = [_P, _P, ctypes.c_int64, _I, _P, _P]
     L.vdi_segs_to_aos.argtypes = [_P, _P, ctypes.c_int64, _I, _P]
     L.vdi_segs_from_aos.argtypes = [_P, _P, ctypes.c_int64, _I, _P]
     for name in ("vdi_gen_launch", "vdi_grid_launch", "vdi_render_launch", "vdi_dvr_launch",
@@ -194,9 +195,9 @@ def load():
                  "vdi_validate", "vdi_synth_rm_u8",
                  "vdi_gen_rays", "vdi_composite_lists", "vdi_dda_cells", "vdi_project_rays",
                  "vdi_find_first_batch", "vdi_segs_to_aos", "vdi_segs_from_aos",
-                 "vdi_list_tiles", "vdi_grid_zmask"):
+                 "vdi_list_tiles", "vdi_grid_zmask", "vdi_list_ranges"):
         getattr(L, name).restype = ctypes.c_int
-    if L.vdi_abi_version() != 6:
+    if L.vdi_abi_version() != 7:
         raise VdiError("libvdi_b200.so ABI mismatch")
     _lib = L
     return L

@@ -95,6 +95,14 @@ int vdi_grid_zmask(const uint32_t* grid, int32_t gx, int32_t gy, int32_t gz, uin
   return vdi::grid_zmask(grid, gx, gy, gz, out, static_cast<cudaStream_t>(stream));
 }
 
+int vdi_list_ranges(const float* segs, const int32_t* counts, int64_t n_lists, int32_t n_sg,
+                    float* out, vdi_stream_t stream) {
+  if (n_lists < 0 || n_sg < 1) return set_error(VDI_EINVAL, "bad sizes");
+  if (n_lists == 0) return VDI_OK;
+  if (!segs || !counts || !out) return set_error(VDI_EINVAL, "null device pointer");
+  return vdi::list_ranges(segs, counts, n_lists, n_sg, out, static_cast<cudaStream_t>(stream));
+}
+
 int vdi_dvr_launch(const VdiDvrArgs* a, vdi_stream_t stream) {
   if (!a) return set_error(VDI_EINVAL, "null args");
   if (!a->volume || !a->lut || !a->image || !a->workspace)

@@ -32,6 +32,8 @@ int render_launch(const VdiRenderArgs* a, cudaStream_t stream);
 size_t list_tiles_words(int vdi_w, int vdi_h);
 int list_tiles(const VdiRenderArgs* args, uint32_t* tiles, cudaStream_t stream);
 int grid_zmask(const uint32_t* grid, int gx, int gy, int gz, uint64_t* out, cudaStream_t stream);
+int list_ranges(const float* segs, const int32_t* counts, long long n_lists, int n_sg, float* out,
+                cudaStream_t stream);
 int dvr_launch(const VdiDvrArgs* a, cudaStream_t stream);
 int gen_rays(const VdiGenArgs* a, const double* rays, const double* gammas_in, long long n,
              int mode, cudaStream_t stream);

@@ -133,6 +133,13 @@ __device__ __forceinline__ bool shade_list(const RenderConst& c, ShadeSmem& sm, 
   const float4* rgba = reinterpret_cast<const float4*>(ls);
   int seed, j;
   if (fast) {
+    if (a.list_range) {
+      // the chord piece misses the list's depth range: the search would miss
+      // (no back >= d_entry, or every front > d_exit); the seed is not read
+      // again on this ray (fast mode does not depend on it)
+      const float2 r = __ldg(reinterpret_cast<const float2*>(a.list_range) + lidx);
+      if (d_exit < (double)r.x || d_entry > (double)r.y) return false;
+    }
     j = find_first(fronts, backs, count, d_entry, d_exit, sm.p[t], seed);
     if (j < 0) {
       sm.p[t] = seed;
@@ -428,6 +435,39 @@ int grid_zmask(const uint32_t* grid, int gx, int gy, int gz, uint64_t* out, cuda
   const cudaError_t err = cudaGetLastError();
   if (err != cudaSuccess)
     return set_error(VDI_ELAUNCH, "grid_zmask launch: %s", cudaGetErrorString(err));
+  return VDI_OK;
+}
+
+// vdi_list_ranges: one thread per list; min front / max back over its
+// entries (fronts and backs are contiguous runs of the list-SoA slot).
+__global__ void list_ranges_kernel(const float* __restrict__ segs,
+                                   const int32_t* __restrict__ counts, long long n_lists, int n_sg,
+                                   float2* __restrict__ out) {
+  const long long l = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (l >= n_lists) return;
+  int n = __ldg(counts + l);
+  n = n < 0 ? 0 : (n > n_sg ? n_sg : n);
+  const float* ls = segs + l * (long long)list_stride(n_sg);
+  const float* fronts = ls + front_off(n_sg);
+  const float* backs = ls + back_off(n_sg);
+  float lo = INFINITY, hi = -INFINITY;
+  bool nan = false;
+  for (int k = 0; k < n; ++k) {
+    const float f = __ldg(fronts + k), b = __ldg(backs + k);
+    nan |= f != f || b != b;
+    lo = fminf(lo, f);
+    hi = fmaxf(hi, b);
+  }
+  out[l] = nan ? make_float2(-INFINITY, INFINITY) : make_float2(lo, hi);
+}
+
+int list_ranges(const float* segs, const int32_t* counts, long long n_lists, int n_sg, float* out,
+                cudaStream_t stream) {
+  list_ranges_kernel<<<(unsigned)((n_lists + 255) / 256), 256, 0, stream>>>(
+      segs, counts, n_lists, n_sg, reinterpret_cast<float2*>(out));
+  const cudaError_t err = cudaGetLastError();
+  if (err != cudaSuccess)
+    return set_error(VDI_ELAUNCH, "list_ranges launch: %s", cudaGetErrorString(err));
   return VDI_OK;
 }
 

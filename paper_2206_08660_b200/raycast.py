@@ -121,6 +121,29 @@ def launch_zmask(a: _capi.VdiRenderArgs, zmask, stream=None) -> None:
     a.grid_zmask = dv.ptr(zmask)
 
 
+def use_list_ranges(a: _capi.VdiRenderArgs) -> bool:
+    """Per-list depth ranges (VdiRenderArgs.list_range) pay only where the
+    kernel reads them: sorted lists without exact search counters."""
+    from .tuning import TUNING
+    return bool(TUNING.list_ranges) and bool(a.lists_sorted) and not a.counters_exact
+
+
+def alloc_ranges(n_lists: int):
+    return dv.torch().empty(2 * max(int(n_lists), 1), dtype=dv.torch().float32, device="cuda")
+
+
+def launch_ranges(a: _capi.VdiRenderArgs, ranges, n_lists: int, stream=None) -> None:
+    """(min front, max back) of every storage list of the VDI `a` points at
+    (vdi_list_ranges); sets a.list_range (None: a.list_range = NULL)."""
+    if ranges is None:
+        a.list_range = None
+        return
+    _capi.check(_capi.load().vdi_list_ranges(a.segs, a.counts, int(n_lists), a.n_sg,
+                                             dv.ptr(ranges), dv.stream_handle()
+                                             if stream is None else stream))
+    a.list_range = dv.ptr(ranges)
+
+
 def launch_render(vdi, grid, cam_new, opts, image, per_pixel=None, stat_sums=None,
                   band=(16, 1, 0), stream=None):
     """Enqueue one render on the current stream (no sync; the grid's slab
@@ -135,8 +158,13 @@ def launch_render(vdi, grid, cam_new, opts, image, per_pixel=None, stat_sums=Non
         launch_list_tiles(a, tiles, s)
     zmask = alloc_zmask(grid.dims) if opts.use_ess else None
     launch_zmask(a, zmask, s)
+    ranges = None
+    if use_list_ranges(a):
+        n_lists = vdi.device().counts.numel()
+        ranges = alloc_ranges(n_lists)
+        launch_ranges(a, ranges, n_lists, s)
     _capi.check(_capi.load().vdi_render_launch(a, s))
-    image._keep_tiles = (tiles, zmask)  # they must outlive the enqueued render
+    image._keep_tiles = (tiles, zmask, ranges)  # they must outlive the enqueued render
 
 
 def _as_device_vdi(vdi):

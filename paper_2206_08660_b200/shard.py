@@ -24,8 +24,9 @@ import numpy as np
 from . import _capi
 from . import device as dv
 from .generate import alloc_gen, launch_generate
-from .raycast import (RenderOptions, alloc_list_tiles, alloc_zmask, launch_list_tiles,
-                      launch_zmask, render_args, use_list_tiles)
+from .raycast import (RenderOptions, alloc_list_tiles, alloc_ranges, alloc_zmask,
+                      launch_list_tiles, launch_ranges, launch_zmask, render_args,
+                      use_list_ranges, use_list_tiles)
 from .vdi import AccelGrid, DeviceVdi, Vdi, default_grid_dims
 
 BAND_ROWS = 16
@@ -373,6 +374,10 @@ class Pipeline:
                                   self.grid_dims, gcam.near, gcam.far, rcam, self.opts,
                                   self.image, stat_sums=self.sums, band=self.band,
                                   counters_exact=False)
+        # per-list depth ranges of the exchanged VDI (search-first shading)
+        self.n_lists = int(self.dvdi.counts.numel())
+        self.ranges = alloc_ranges(self.n_lists) if use_list_ranges(self._rargs) else None
+        self.launches_per_step += self.ranges is not None
 
     def step(self, timed: bool = False, vol_dev=None):
         """One frame on the current stream: volume prep, generation, grid,
@@ -404,6 +409,7 @@ class Pipeline:
         if self.tiles is not None:
             launch_list_tiles(self._rargs, self.tiles)
         launch_zmask(self._rargs, self.zmask)
+        launch_ranges(self._rargs, self.ranges, self.n_lists)
         _capi.check(L.vdi_render_launch(self._rargs, dv.stream_handle()))
         if timed:
             ev[5].record()

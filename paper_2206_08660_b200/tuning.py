@@ -15,6 +15,9 @@ class Tuning:
     cells: bool | None = None
     # empty-tile skipping in the render DDA (VdiRenderArgs.list_tiles)
     list_tiles: bool = False
+    # per-list depth ranges for the render's search-first path
+    # (VdiRenderArgs.list_range)
+    list_ranges: bool = True
     # multi-GPU VDI exchange as packed VDI1 shards (False: plain all-gather)
     packed_exchange: bool = True
 

@@ -107,8 +107,10 @@ def test_search_first_shading_exact(cfg, angle):
     counters not exact) against the reference's ESS-then-search order: the
     same image and the same lists_visited / supersegments_intersected per
     pixel, forward chords (15 deg) and views behind the volume (reverse
-    chords take the reference order)."""
-    from paper_2206_08660_b200.raycast import alloc_zmask, launch_zmask
+    chords take the reference order); with and without the per-list depth
+    ranges (VdiRenderArgs.list_range) that skip lists the chord misses."""
+    from paper_2206_08660_b200.raycast import (alloc_ranges, alloc_zmask, launch_ranges,
+                                               launch_zmask)
     vol, tf, gcam, rcam, n_sg = synth.config(cfg)
     rcam = synth.sweep_camera(vol, angle, gcam.viewport, synth.CONFIGS[cfg][4])
     vdi, grid = vb.generate_vdi(vol, tf, gcam, vb.GenParams(n_sg=n_sg))
@@ -117,7 +119,7 @@ def test_search_first_shading_exact(cfg, angle):
     ow, oh = rcam.viewport
     L = _capi.load()
     outs = []
-    for exact in (True, False):
+    for exact, ranged in ((True, False), (False, False), (False, True)):
         image = torch.empty((oh, ow, 4), dtype=torch.float64, device="cuda")
         pp = [torch.zeros((oh, ow), dtype=torch.int32, device="cuda") for _ in range(3)]
         a = render_args(d, n_sg, vdi.width, vdi.height, gcam, vdi.volume_aabb, grid.device(),
@@ -126,12 +128,54 @@ def test_search_first_shading_exact(cfg, angle):
         assert a.lists_sorted == 1
         zm = alloc_zmask(grid.dims)
         launch_zmask(a, zm)
+        if ranged:
+            rg = alloc_ranges(d.counts.numel())
+            launch_ranges(a, rg, d.counts.numel())
         _capi.check(L.vdi_render_launch(a, dv.stream_handle()))
         torch.cuda.synchronize()
         outs.append([image.cpu().numpy()] + [x.cpu().numpy() for x in pp[:2]])
-    for x, y in zip(outs[0], outs[1]):
-        np.testing.assert_array_equal(x, y)
+    for other in outs[1:]:
+        for x, y in zip(outs[0], other):
+            np.testing.assert_array_equal(x, y)
     assert outs[0][1].sum() > 0
     # the public API without stats takes the search-first path
     img = vb.render_vdi(vdi, grid, rcam)
     np.testing.assert_array_equal(img.data, outs[0][0])
+
+
+def _ranges_ref(counts, segs_soa, n_sg):
+    n = counts.size
+    fr = segs_soa[:, 4 * n_sg:5 * n_sg]
+    bk = segs_soa[:, 5 * n_sg:6 * n_sg]
+    out = np.empty((n, 2), np.float32)
+    for i, c in enumerate(counts.reshape(-1)):
+        f, b = fr[i, :c], bk[i, :c]
+        if np.isnan(f).any() or np.isnan(b).any():
+            out[i] = (-np.inf, np.inf)
+        elif c == 0:
+            out[i] = (np.inf, -np.inf)
+        else:
+            out[i] = (f.min(), b.max())
+    return out
+
+
+def test_list_ranges_kernel():
+    """vdi_list_ranges: (min front, max back) per list, the empty and NaN
+    sentinels, counts beyond n_sg clamped."""
+    from paper_2206_08660_b200.raycast import alloc_ranges
+    rng = np.random.default_rng(5)
+    n_sg, n = 6, 5000
+    stride = (6 * n_sg + 3) & ~3
+    segs = rng.random((n, stride)).astype(np.float32)
+    counts = rng.integers(0, n_sg + 1, n).astype(np.int32)
+    segs[7, 4 * n_sg + 1] = np.nan
+    counts[7] = 3
+    segs[8, 5 * n_sg + 4] = np.nan
+    counts[8] = 4  # NaN beyond the count: ignored
+    want = _ranges_ref(counts, segs, n_sg)
+    out = alloc_ranges(n)
+    _capi.check(_capi.load().vdi_list_ranges(dv.ptr(dv.to_device(segs)),
+                                             dv.ptr(dv.to_device(counts)), n, n_sg,
+                                             dv.ptr(out), dv.stream_handle()))
+    np.testing.assert_array_equal(out.cpu().numpy().reshape(n, 2), want)
+    assert np.isinf(want[7]).all() and want[8, 0] < want[8, 1]

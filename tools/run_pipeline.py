@@ -14,7 +14,11 @@ from paper_2206_08660_b200.generate import GenParams  # noqa: E402
 p = argparse.ArgumentParser()
 p.add_argument("--config", default="C3")
 p.add_argument("--reps", type=int, default=2)
+p.add_argument("--no-ranges", action="store_true", help="render without VdiRenderArgs.list_range")
 a = p.parse_args()
+if a.no_ranges:
+    from paper_2206_08660_b200.tuning import TUNING
+    TUNING.list_ranges = False
 vol, tf, gcam, rcam, n_sg = synth.config(a.config)
 pipe = shard.Pipeline(vol, tf, gcam, rcam, GenParams(n_sg=n_sg))
 for _ in range(a.reps):
