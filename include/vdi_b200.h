@@ -63,7 +63,7 @@
 extern "C" {
 #endif
 
-#define VDI_ABI_VERSION 7
+#define VDI_ABI_VERSION 8
 
 #define VDI_OK 0
 #define VDI_EINVAL (-1)
@@ -213,6 +213,12 @@ typedef struct VdiRenderArgs {
    * search would miss; it is skipped without reading the list. Same image
    * and counters. */
   const float* list_range;
+  /* optional (may be NULL): two zeroed u32 owned by the caller. Then the
+   * render runs one resident grid whose warps take 8x4 pixel tiles from
+   * tile_counter[0] in image order; the last warp resets both words to 0, so
+   * the pair can be reused by the next launch on the same stream (not by a
+   * concurrent one). NULL: one tile per warp. Same image and counters. */
+  unsigned int* tile_counter;
 } VdiRenderArgs;
 
 /* Ground-truth direct volume rendering (dvr.py:21-89): the generation ray,

@@ -56,7 +56,7 @@ class VdiRenderArgs(ctypes.Structure):
         ("vdi_band_rows", _I), ("vdi_band_world", _I), ("vdi_rows_per_rank", _I),
         ("band_rows", _I), ("band_stride", _I), ("band_offset", _I),
         ("list_tiles", _P), ("grid_zmask", _P), ("lists_sorted", _I), ("counters_exact", _I),
-        ("vdi_row_map", _P), ("list_range", _P),
+        ("vdi_row_map", _P), ("list_range", _P), ("tile_counter", _P),
     ]
 
 
@@ -197,7 +197,7 @@ def load():
                  "vdi_find_first_batch", "vdi_segs_to_aos", "vdi_segs_from_aos",
                  "vdi_list_tiles", "vdi_grid_zmask", "vdi_list_ranges"):
         getattr(L, name).restype = ctypes.c_int
-    if L.vdi_abi_version() != 7:
+    if L.vdi_abi_version() != 8:
         raise VdiError("libvdi_b200.so ABI mismatch")
     _lib = L
     return L

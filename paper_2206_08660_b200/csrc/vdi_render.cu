@@ -21,9 +21,16 @@
 
 namespace vdi {
 
-constexpr int kRenderThreads = 128;
+#ifndef VDI_RENDER_THREADS
+#define VDI_RENDER_THREADS 128
+#endif
+constexpr int kRenderThreads = VDI_RENDER_THREADS;
+#ifndef VDI_RANGE_AHEAD
+#define VDI_RANGE_AHEAD 1  // 1: the walk loads the next list's depth range with its count
+#endif
 #ifndef VDI_RENDER_MINB
-#define VDI_RENDER_MINB 5  // 96 registers, no spills (C3 0.93 ms; 6: 1.03, 4: 1.00)
+// blocks per SM: 20 warps, 96 registers, no spills (C3 0.93 ms; 24 warps: 1.03, 16: 1.00)
+#define VDI_RENDER_MINB (640 / VDI_RENDER_THREADS)
 #endif
 
 // Storage row of VDI list row r: the explicit map when given
@@ -63,6 +70,7 @@ struct ShadeSmem {
   double dep_key[kRenderThreads], dep_val[kRenderThreads];  // last proj_b / (proj_a - d(s))
   int p[kRenderThreads];                                    // the Alg. 2 seed (raycast.py:344)
   int nint[kRenderThreads], nsearch[kRenderThreads];
+  unsigned long long sum_vis[kRenderThreads], sum_int[kRenderThreads], sum_srch[kRenderThreads];
 };
 
 // _grid_cell_range (raycast.py:258-272) + the all-empty scan (359-370):
@@ -118,7 +126,7 @@ __device__ __forceinline__ bool ess_empty(const RenderConst& c, ShadeSmem& sm, i
 template <bool kMask>
 __device__ __forceinline__ bool shade_list(const RenderConst& c, ShadeSmem& sm, int t, int cx,
                                            int cy, long long lidx, int count, double s_cur,
-                                           double tmin, bool fast) {
+                                           double tmin, bool fast, bool range_test = true) {
   const VdiRenderArgs& a = c.a;
   const int vdi_w = a.vdi_w, vdi_h = a.vdi_h, n_sg = a.n_sg;
   const double a0x = sm.a0x[t], a0y = sm.a0y[t], a0z = sm.a0z[t];
@@ -133,7 +141,7 @@ __device__ __forceinline__ bool shade_list(const RenderConst& c, ShadeSmem& sm, 
   const float4* rgba = reinterpret_cast<const float4*>(ls);
   int seed, j;
   if (fast) {
-    if (a.list_range) {
+    if (range_test && a.list_range) {
       // the chord piece misses the list's depth range: the search would miss
       // (no back >= d_entry, or every front > d_exit); the seed is not read
       // again on this ray (fast mode does not depend on it)
@@ -230,148 +238,200 @@ __device__ __forceinline__ bool shade_list(const RenderConst& c, ShadeSmem& sm, 
 // d_entry / d_exit for every list but reads them only there). The early
 // termination test (429) can only change after a shading. Same visits, same
 // order, same arithmetic: the image and every counter are unchanged.
+// One 8x4 tile of output pixels, lane w = pixel (w & 7, w >> 3) of the tile.
 template <bool kTiles, bool kMask, bool kBands>
+__device__ __forceinline__ void render_tile(const RenderConst& c, ShadeSmem& sm,
+                                            const uint32_t* s_tiles, int tile) {
+  const VdiRenderArgs& a = c.a;
+  const int t = threadIdx.x;
+  const int w = threadIdx.x & 31;
+  const int col = (int)(tile % c.tiles_x) * kTileW + (w & 7);
+  const int lrow = (int)(tile / c.tiles_x) * kTileH + (w >> 3);
+  if (col < a.out_w && lrow < c.local_h) {
+    const int row = band_global_row(lrow, a.band_rows, a.band_stride, a.band_offset);
+    const int vdi_w = a.vdi_w, vdi_h = a.vdi_h;
+    sm.acc_r[t] = sm.acc_g[t] = sm.acc_b[t] = sm.acc_a[t] = 0.0;
+    sm.nint[t] = sm.nsearch[t] = 0;
+    int nvis = 0;
+    double d[3];
+    pixel_ray(a.new_inv_pv, a.eye, col, row, a.out_w, a.out_h, d);
+    const double* eye = a.eye;
+    double ta, tb, fa, fb, t0 = 0.0, t1 = 0.0;
+    bool ok = false;
+    if (clip_aabb(eye, d, a.aabb, ta, tb) && clip_frustum(a.gen_pv, eye, d, fa, fb)) {
+      t0 = dmax(dmax(ta, fa), 0.0);
+      t1 = dmin(tb, fb);
+      ok = t1 > t0;
+    }
+    if (ok) {
+      double a0x, a0y, a0z, a1x, a1y, a1z;
+      xform(a.gen_pv, eye[0] + t0 * d[0], eye[1] + t0 * d[1], eye[2] + t0 * d[2], a0x, a0y, a0z);
+      xform(a.gen_pv, eye[0] + t1 * d[0], eye[1] + t1 * d[1], eye[2] + t1 * d[2], a1x, a1y, a1z);
+      const double cdx = a1x - a0x, cdy = a1y - a0y, cdz = a1z - a0z;
+      sm.a0x[t] = a0x;
+      sm.a0y[t] = a0y;
+      sm.a0z[t] = a0z;
+      sm.cdx[t] = cdx;
+      sm.cdy[t] = cdy;
+      sm.cdz[t] = cdz;
+      int cx = clampi(floor_ll((a0x + 1.0) * vdi_w / 2.0), 0, vdi_w - 1);
+      int cy = clampi(floor_ll((a0y + 1.0) * vdi_h / 2.0), 0, vdi_h - 1);
+      const int step_x = cdx > 0 ? 1 : (cdx < 0 ? -1 : 0);
+      const int step_y = cdy > 0 ? 1 : (cdy < 0 ? -1 : 0);
+      double t_max_x = INFINITY, t_delta_x = INFINITY, t_max_y = INFINITY,
+             t_delta_y = INFINITY;
+      if (step_x != 0) {
+        const double bx = -1.0 + 2.0 * (double)(cx + (step_x > 0 ? 1 : 0)) / vdi_w;
+        t_max_x = (bx - a0x) / cdx;
+        t_delta_x = (2.0 / vdi_w) / fabs(cdx);
+      }
+      if (step_y != 0) {
+        const double by = -1.0 + 2.0 * (double)(cy + (step_y > 0 ? 1 : 0)) / vdi_h;
+        t_max_y = (by - a0y) / cdy;
+        t_delta_y = (2.0 / vdi_h) / fabs(cdy);
+      }
+      // search-first shading (shade_list kFast): sorted lists, a chord running
+      // forward in depth (d_entry <= d_exit on every list), uncounted searches
+      const bool fast = a.lists_sorted && !a.counters_exact && cdz >= 0.0;
+      sm.p[t] = -1;
+      sm.dep_key[t] = -1.0;  // chord parameters are >= 0
+      sm.dep_val[t] = 0.0;
+      double s_cur = 0.0;
+      const int max_iter = vdi_w + vdi_h + 4;
+      const int32_t* rowp =
+          a.counts + (long long)storage_row(a, cy) * vdi_w;
+      // a list of an empty tile has count 0: no load
+      auto load_count = [&](const int32_t* rp, int x, int y) -> int {
+        if (kTiles && !((s_tiles[(y >> 3) * c.lt_wpr + (x >> 8)] >> ((x >> 3) & 31)) & 1u))
+          return 0;
+        return __ldg(rp + x);
+      };
+      // The count of the next list is requested before the current list is
+      // shaded (the DDA step does not depend on it), so its load latency
+      // overlaps an iteration instead of stalling the next one.
+      int cnt = load_count(rowp, cx, cy);
+      const bool ranged = VDI_RANGE_AHEAD && fast && a.list_range != nullptr;
+      const float2* rng_base = reinterpret_cast<const float2*>(a.list_range);
+      float2 rng = make_float2(0.f, 0.f);
+      if (ranged) rng = __ldg(rng_base + (rowp - a.counts) + cx);
+      for (;;) {
+        const bool xs = t_max_x <= t_max_y;
+        const double tmin = xs ? t_max_x : t_max_y;
+        nvis += 1;
+        // the step, branch-free (a divergent x / y branch serialises the
+        // warp on its few y-steppers); the crossed boundary is the next s_cur
+        const double nx = t_max_x + t_delta_x, ny = t_max_y + t_delta_y;
+        t_max_x = xs ? nx : t_max_x;
+        t_max_y = xs ? t_max_y : ny;
+        const int ncx = cx + (xs ? step_x : 0);
+        const int ncy = cy + (xs ? 0 : step_y);
+        const bool last = tmin >= 1.0 || nvis >= max_iter || (unsigned)ncx >= (unsigned)vdi_w ||
+                          (unsigned)ncy >= (unsigned)vdi_h;
+        const int32_t* nrowp = rowp;
+        int ncnt = 0;
+        if (!last) {
+          if (!kBands) {
+            nrowp = a.counts + (long long)ncy * vdi_w;
+          } else if (!xs) {
+            nrowp = a.counts + (long long)storage_row(a, ncy) * vdi_w;
+          }
+          ncnt = load_count(nrowp, ncx, ncy);
+        }
+        float2 nrng = rng;
+        if (ranged && !last) nrng = __ldg(rng_base + (nrowp - a.counts) + ncx);
+        if (cnt > 0) {
+          bool go = true;
+          if (ranged) {
+            // the range test of shade_list, on the prefetched range
+            double s_exit = dmin(tmin, 1.0);
+            if (s_exit < s_cur) s_exit = s_cur;
+            const double z0 = sm.a0z[t], dz = sm.cdz[t];
+            go = !(z0 + s_exit * dz < (double)rng.x || z0 + s_cur * dz > (double)rng.y);
+          }
+          const long long lidx = (rowp - a.counts) + cx;
+          if (go && shade_list<kMask>(c, sm, t, cx, cy, lidx, cnt, s_cur, tmin, fast, !ranged))
+            break;
+        }
+        if (last) break;
+        cx = ncx;
+        cy = ncy;
+        rowp = nrowp;
+        s_cur = tmin;
+        cnt = ncnt;
+        rng = nrng;
+      }
+    }
+    const double acc_a = sm.acc_a[t];
+    const double wgt = 1.0 - acc_a;
+    const long long pix = (long long)lrow * a.out_w + col;
+    double2* o = reinterpret_cast<double2*>(a.image + pix * 4);
+    o[0] = make_double2(sm.acc_r[t] + wgt * a.bg[0] * a.bg[3],
+                        sm.acc_g[t] + wgt * a.bg[1] * a.bg[3]);
+    o[1] = make_double2(sm.acc_b[t] + wgt * a.bg[2] * a.bg[3], acc_a + wgt * a.bg[3]);
+    const int nint = sm.nint[t], nsearch = sm.nsearch[t];
+    if (a.lists_visited) a.lists_visited[pix] = nvis;
+    if (a.segs_intersected) a.segs_intersected[pix] = nint;
+    if (a.lists_searched && a.counters_exact) a.lists_searched[pix] = nsearch;
+    if (a.stat_sums) {
+      sm.sum_vis[t] += nvis;
+      sm.sum_int[t] += nint;
+      sm.sum_srch[t] += a.counters_exact ? nsearch : 0;
+    }
+  }
+}
+
+template <bool kTiles, bool kMask, bool kBands, bool kDyn>
 __global__ void __launch_bounds__(kRenderThreads, VDI_RENDER_MINB) render_kernel(const __grid_constant__ RenderConst c) {
   const VdiRenderArgs& a = c.a;
   extern __shared__ uint32_t s_tiles[];
   __shared__ ShadeSmem sm;
-  const int t = threadIdx.x;
   if (kTiles) {
     for (int k = threadIdx.x; k < c.lt_words; k += blockDim.x) s_tiles[k] = __ldg(a.list_tiles + k);
     __syncthreads();
   }
-  const long long slot = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  unsigned long long st_vis = 0, st_int = 0, st_srch = 0;
-  if (slot < c.n_slots) {
-    const long long tile = slot >> 5;
-    const int w = (int)(slot & 31);
-    const int col = (int)(tile % c.tiles_x) * kTileW + (w & 7);
-    const int lrow = (int)(tile / c.tiles_x) * kTileH + (w >> 3);
-    if (col < a.out_w && lrow < c.local_h) {
-      const int row = band_global_row(lrow, a.band_rows, a.band_stride, a.band_offset);
-      const int vdi_w = a.vdi_w, vdi_h = a.vdi_h;
-      sm.acc_r[t] = sm.acc_g[t] = sm.acc_b[t] = sm.acc_a[t] = 0.0;
-      sm.nint[t] = sm.nsearch[t] = 0;
-      int nvis = 0;
-      double d[3];
-      pixel_ray(a.new_inv_pv, a.eye, col, row, a.out_w, a.out_h, d);
-      const double* eye = a.eye;
-      double ta, tb, fa, fb, t0 = 0.0, t1 = 0.0;
-      bool ok = false;
-      if (clip_aabb(eye, d, a.aabb, ta, tb) && clip_frustum(a.gen_pv, eye, d, fa, fb)) {
-        t0 = dmax(dmax(ta, fa), 0.0);
-        t1 = dmin(tb, fb);
-        ok = t1 > t0;
-      }
-      if (ok) {
-        double a0x, a0y, a0z, a1x, a1y, a1z;
-        xform(a.gen_pv, eye[0] + t0 * d[0], eye[1] + t0 * d[1], eye[2] + t0 * d[2], a0x, a0y, a0z);
-        xform(a.gen_pv, eye[0] + t1 * d[0], eye[1] + t1 * d[1], eye[2] + t1 * d[2], a1x, a1y, a1z);
-        const double cdx = a1x - a0x, cdy = a1y - a0y, cdz = a1z - a0z;
-        sm.a0x[t] = a0x;
-        sm.a0y[t] = a0y;
-        sm.a0z[t] = a0z;
-        sm.cdx[t] = cdx;
-        sm.cdy[t] = cdy;
-        sm.cdz[t] = cdz;
-        int cx = clampi(floor_ll((a0x + 1.0) * vdi_w / 2.0), 0, vdi_w - 1);
-        int cy = clampi(floor_ll((a0y + 1.0) * vdi_h / 2.0), 0, vdi_h - 1);
-        const int step_x = cdx > 0 ? 1 : (cdx < 0 ? -1 : 0);
-        const int step_y = cdy > 0 ? 1 : (cdy < 0 ? -1 : 0);
-        double t_max_x = INFINITY, t_delta_x = INFINITY, t_max_y = INFINITY,
-               t_delta_y = INFINITY;
-        if (step_x != 0) {
-          const double bx = -1.0 + 2.0 * (double)(cx + (step_x > 0 ? 1 : 0)) / vdi_w;
-          t_max_x = (bx - a0x) / cdx;
-          t_delta_x = (2.0 / vdi_w) / fabs(cdx);
-        }
-        if (step_y != 0) {
-          const double by = -1.0 + 2.0 * (double)(cy + (step_y > 0 ? 1 : 0)) / vdi_h;
-          t_max_y = (by - a0y) / cdy;
-          t_delta_y = (2.0 / vdi_h) / fabs(cdy);
-        }
-        // search-first shading (shade_list kFast): sorted lists, a chord running
-        // forward in depth (d_entry <= d_exit on every list), uncounted searches
-        const bool fast = a.lists_sorted && !a.counters_exact && cdz >= 0.0;
-        sm.p[t] = -1;
-        sm.dep_key[t] = -1.0;  // chord parameters are >= 0
-        sm.dep_val[t] = 0.0;
-        double s_cur = 0.0;
-        const int max_iter = vdi_w + vdi_h + 4;
-        const int32_t* rowp =
-            a.counts + (long long)storage_row(a, cy) * vdi_w;
-        // a list of an empty tile has count 0: no load
-        auto load_count = [&](const int32_t* rp, int x, int y) -> int {
-          if (kTiles && !((s_tiles[(y >> 3) * c.lt_wpr + (x >> 8)] >> ((x >> 3) & 31)) & 1u))
-            return 0;
-          return __ldg(rp + x);
-        };
-        // The count of the next list is requested before the current list is
-        // shaded (the DDA step does not depend on it), so its load latency
-        // overlaps an iteration instead of stalling the next one.
-        int cnt = load_count(rowp, cx, cy);
-        for (;;) {
-          const bool xs = t_max_x <= t_max_y;
-          const double tmin = xs ? t_max_x : t_max_y;
-          nvis += 1;
-          // the step, branch-free (a divergent x / y branch serialises the
-          // warp on its few y-steppers); the crossed boundary is the next s_cur
-          const double nx = t_max_x + t_delta_x, ny = t_max_y + t_delta_y;
-          t_max_x = xs ? nx : t_max_x;
-          t_max_y = xs ? t_max_y : ny;
-          const int ncx = cx + (xs ? step_x : 0);
-          const int ncy = cy + (xs ? 0 : step_y);
-          const bool last = tmin >= 1.0 || nvis >= max_iter || (unsigned)ncx >= (unsigned)vdi_w ||
-                            (unsigned)ncy >= (unsigned)vdi_h;
-          const int32_t* nrowp = rowp;
-          int ncnt = 0;
-          if (!last) {
-            if (!kBands) {
-              nrowp = a.counts + (long long)ncy * vdi_w;
-            } else if (!xs) {
-              nrowp = a.counts + (long long)storage_row(a, ncy) * vdi_w;
-            }
-            ncnt = load_count(nrowp, ncx, ncy);
-          }
-          if (cnt > 0) {
-            const long long lidx = (rowp - a.counts) + cx;
-            if (shade_list<kMask>(c, sm, t, cx, cy, lidx, cnt, s_cur, tmin, fast)) break;
-          }
-          if (last) break;
-          cx = ncx;
-          cy = ncy;
-          rowp = nrowp;
-          s_cur = tmin;
-          cnt = ncnt;
-        }
-      }
-      const double acc_a = sm.acc_a[t];
-      const double wgt = 1.0 - acc_a;
-      const long long pix = (long long)lrow * a.out_w + col;
-      double2* o = reinterpret_cast<double2*>(a.image + pix * 4);
-      o[0] = make_double2(sm.acc_r[t] + wgt * a.bg[0] * a.bg[3],
-                          sm.acc_g[t] + wgt * a.bg[1] * a.bg[3]);
-      o[1] = make_double2(sm.acc_b[t] + wgt * a.bg[2] * a.bg[3], acc_a + wgt * a.bg[3]);
-      const int nint = sm.nint[t], nsearch = sm.nsearch[t];
-      if (a.lists_visited) a.lists_visited[pix] = nvis;
-      if (a.segs_intersected) a.segs_intersected[pix] = nint;
-      if (a.lists_searched && a.counters_exact) a.lists_searched[pix] = nsearch;
-      st_vis = nvis;
-      st_int = nint;
-      st_srch = a.counters_exact ? nsearch : 0;
+  // per-thread counter sums across the thread's tiles
+  sm.sum_vis[threadIdx.x] = sm.sum_int[threadIdx.x] = sm.sum_srch[threadIdx.x] = 0ull;
+  const int n_tiles = (int)(c.n_slots >> 5);
+  if (kDyn) {
+    // resident grid; each warp takes the next tile from a.tile_counter, so
+    // the tiles in flight stay a compact front of the image (as the block
+    // scheduler keeps them) while no block waits on its slowest warp
+    const int lane = threadIdx.x & 31;
+    for (;;) {
+      unsigned tile = 0;
+      if (lane == 0) tile = atomicAdd(a.tile_counter, 1u);
+      tile = __shfl_sync(0xffffffffu, tile, 0);
+      if (tile >= (unsigned)n_tiles) break;
+      render_tile<kTiles, kMask, kBands>(c, sm, s_tiles, (int)tile);
     }
+    // the last warp out resets the counter for the next launch
+    if (lane == 0) {
+      __threadfence();
+      const unsigned total = gridDim.x * (blockDim.x >> 5);
+      if (atomicAdd(a.tile_counter + 1, 1u) == total - 1) {
+        a.tile_counter[0] = 0u;
+        a.tile_counter[1] = 0u;
+        __threadfence();
+      }
+    }
+  } else {
+    const int tile = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    if (tile < n_tiles)
+      render_tile<kTiles, kMask, kBands>(c, sm, s_tiles, tile);
   }
   if (a.stat_sums) {
+    unsigned long long sv = sm.sum_vis[threadIdx.x], si = sm.sum_int[threadIdx.x],
+                       ss = sm.sum_srch[threadIdx.x];
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
-      st_vis += __shfl_xor_sync(0xffffffffu, st_vis, off);
-      st_int += __shfl_xor_sync(0xffffffffu, st_int, off);
-      st_srch += __shfl_xor_sync(0xffffffffu, st_srch, off);
+      sv += __shfl_xor_sync(0xffffffffu, sv, off);
+      si += __shfl_xor_sync(0xffffffffu, si, off);
+      ss += __shfl_xor_sync(0xffffffffu, ss, off);
     }
     if ((threadIdx.x & 31) == 0) {
-      atomicAdd(a.stat_sums + 0, st_vis);
-      atomicAdd(a.stat_sums + 1, st_int);
-      atomicAdd(a.stat_sums + 2, st_srch);
+      atomicAdd(a.stat_sums + 0, sv);
+      atomicAdd(a.stat_sums + 1, si);
+      atomicAdd(a.stat_sums + 2, ss);
     }
   }
 }
@@ -398,18 +458,35 @@ int render_launch(const VdiRenderArgs* args, cudaStream_t stream) {
   const size_t smem = sizeof(uint32_t) * (size_t)c.lt_words;
   // kBands: the VDI is an all-gathered band-sharded one (storage-row map)
   void (*fn)(RenderConst);
-  if (c.a.vdi_band_world > 1 || c.a.vdi_row_map)
-    fn = c.lt_words ? (mask ? render_kernel<true, true, true> : render_kernel<true, false, true>)
-                    : (mask ? render_kernel<false, true, true> : render_kernel<false, false, true>);
+  const bool bands = c.a.vdi_band_world > 1 || c.a.vdi_row_map;
+  const bool dyn = c.a.tile_counter != nullptr;
+#define VDI_RK(T, M, B) \
+  (dyn ? render_kernel<T, M, B, true> : render_kernel<T, M, B, false>)
+  if (bands)
+    fn = c.lt_words ? (mask ? VDI_RK(true, true, true) : VDI_RK(true, false, true))
+                    : (mask ? VDI_RK(false, true, true) : VDI_RK(false, false, true));
   else
-    fn = c.lt_words ? (mask ? render_kernel<true, true, false> : render_kernel<true, false, false>)
-                    : (mask ? render_kernel<false, true, false> : render_kernel<false, false, false>);
+    fn = c.lt_words ? (mask ? VDI_RK(true, true, false) : VDI_RK(true, false, false))
+                    : (mask ? VDI_RK(false, true, false) : VDI_RK(false, false, false));
+#undef VDI_RK
   if (smem > 0) {
     const cudaError_t e =
         cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return set_error(VDI_ELAUNCH, "render smem: %s", cudaGetErrorString(e));
   }
-  fn<<<(unsigned)blocks, kRenderThreads, smem, stream>>>(c);
+  long long grid = blocks;
+  if (dyn) {
+    int dev = 0, sms = 0, per_sm = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kRenderThreads, smem) !=
+            cudaSuccess)
+      return set_error(VDI_ELAUNCH, "render occupancy query: %s",
+                       cudaGetErrorString(cudaGetLastError()));
+    const long long resident = (long long)sms * (per_sm > 0 ? per_sm : 1);
+    if (grid > resident) grid = resident;
+  }
+  fn<<<(unsigned)grid, kRenderThreads, smem, stream>>>(c);
   const cudaError_t err = cudaGetLastError();
   if (err != cudaSuccess)
     return set_error(VDI_ELAUNCH, "render launch: %s", cudaGetErrorString(err));

@@ -144,6 +144,19 @@ def launch_ranges(a: _capi.VdiRenderArgs, ranges, n_lists: int, stream=None) -> 
     a.list_range = dv.ptr(ranges)
 
 
+def alloc_tile_counter():
+    """The render's tile counter (VdiRenderArgs.tile_counter), or None when
+    tuning.TUNING.dyn_tiles is off. Zeroed here; every launch leaves it zero."""
+    from .tuning import TUNING
+    if not TUNING.dyn_tiles:
+        return None
+    return dv.torch().zeros(2, dtype=dv.torch().int32, device="cuda")
+
+
+def set_tile_counter(a: _capi.VdiRenderArgs, counter) -> None:
+    a.tile_counter = dv.ptr(counter) if counter is not None else None
+
+
 def launch_render(vdi, grid, cam_new, opts, image, per_pixel=None, stat_sums=None,
                   band=(16, 1, 0), stream=None):
     """Enqueue one render on the current stream (no sync; the grid's slab
@@ -163,8 +176,11 @@ def launch_render(vdi, grid, cam_new, opts, image, per_pixel=None, stat_sums=Non
         n_lists = vdi.device().counts.numel()
         ranges = alloc_ranges(n_lists)
         launch_ranges(a, ranges, n_lists, s)
+    counter = alloc_tile_counter()
+    set_tile_counter(a, counter)
     _capi.check(_capi.load().vdi_render_launch(a, s))
-    image._keep_tiles = (tiles, zmask, ranges)  # they must outlive the enqueued render
+    # they must outlive the enqueued render
+    image._keep_tiles = (tiles, zmask, ranges, counter)
 
 
 def _as_device_vdi(vdi):

@@ -24,9 +24,9 @@ import numpy as np
 from . import _capi
 from . import device as dv
 from .generate import alloc_gen, launch_generate
-from .raycast import (RenderOptions, alloc_list_tiles, alloc_ranges, alloc_zmask,
-                      launch_list_tiles, launch_ranges, launch_zmask, render_args,
-                      use_list_ranges, use_list_tiles)
+from .raycast import (RenderOptions, alloc_list_tiles, alloc_ranges, alloc_tile_counter,
+                      alloc_zmask, launch_list_tiles, launch_ranges, launch_zmask, render_args,
+                      set_tile_counter, use_list_ranges, use_list_tiles)
 from .vdi import AccelGrid, DeviceVdi, Vdi, default_grid_dims
 
 BAND_ROWS = 16
@@ -378,6 +378,8 @@ class Pipeline:
         self.n_lists = int(self.dvdi.counts.numel())
         self.ranges = alloc_ranges(self.n_lists) if use_list_ranges(self._rargs) else None
         self.launches_per_step += self.ranges is not None
+        self.tile_counter = alloc_tile_counter()
+        set_tile_counter(self._rargs, self.tile_counter)
 
     def step(self, timed: bool = False, vol_dev=None):
         """One frame on the current stream: volume prep, generation, grid,
@@ -455,6 +457,7 @@ class Pipeline:
                         self.rcam, self.opts, self.image, stat_sums=sums, band=self.band,
                         counters_exact=True)
         launch_zmask(a, self.zmask)
+        set_tile_counter(a, self.tile_counter)
         _capi.check(_capi.load().vdi_render_launch(a, dv.stream_handle()))
         s = sums.cpu().numpy()
         return int(s[0]), int(s[1]), int(s[2])
@@ -468,6 +471,7 @@ class Pipeline:
                         self.bufs.grid, self.grid_dims, self.gcam.near, self.gcam.far,
                         self.rcam, self.opts, self.image, per_pixel=pp, band=self.band)
         launch_zmask(a, self.zmask)
+        set_tile_counter(a, self.tile_counter)
         _capi.check(_capi.load().vdi_render_launch(a, dv.stream_handle()))
         return (dv.to_host(self.image),) + tuple(dv.to_host(x) for x in pp)
 

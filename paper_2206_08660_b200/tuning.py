@@ -18,6 +18,9 @@ class Tuning:
     # per-list depth ranges for the render's search-first path
     # (VdiRenderArgs.list_range)
     list_ranges: bool = True
+    # render as one resident grid taking 8x4 tiles from a counter
+    # (VdiRenderArgs.tile_counter)
+    dyn_tiles: bool = False
     # multi-GPU VDI exchange as packed VDI1 shards (False: plain all-gather)
     packed_exchange: bool = True
 

@@ -57,7 +57,7 @@ def test_every_entry_point_has_a_prototype(lib):
 
 
 def test_abi_version(lib):
-    assert lib.vdi_abi_version() == 7
+    assert lib.vdi_abi_version() == 8
 
 
 PROBE = r"""

@@ -179,3 +179,38 @@ def test_list_ranges_kernel():
                                              dv.ptr(out), dv.stream_handle()))
     np.testing.assert_array_equal(out.cpu().numpy().reshape(n, 2), want)
     assert np.isinf(want[7]).all() and want[8, 0] < want[8, 1]
+
+
+@pytest.mark.parametrize("cfg,angle", [("C2", 15.0), ("C2", 180.0), ("C3", 15.0)])
+def test_dynamic_tiles_exact(cfg, angle):
+    """The resident render grid taking tiles from a counter
+    (VdiRenderArgs.tile_counter) gives the image, the per-pixel counters and
+    the counter sums of the one-tile-per-warp grid, and leaves the counter
+    zeroed for the next launch (three launches on one counter)."""
+    from paper_2206_08660_b200.raycast import alloc_zmask, launch_zmask
+    vol, tf, gcam, rcam, n_sg = synth.config(cfg)
+    rcam = synth.sweep_camera(vol, angle, gcam.viewport, synth.CONFIGS[cfg][4])
+    vdi, grid = vb.generate_vdi(vol, tf, gcam, vb.GenParams(n_sg=n_sg))
+    d = vdi.device()
+    ow, oh = rcam.viewport
+    L = _capi.load()
+    counter = torch.zeros(2, dtype=torch.int32, device="cuda")
+    outs = []
+    for dyn in (False, True, True, True):
+        image = torch.empty((oh, ow, 4), dtype=torch.float64, device="cuda")
+        pp = [torch.zeros((oh, ow), dtype=torch.int32, device="cuda") for _ in range(3)]
+        sums = torch.zeros(3, dtype=torch.int64, device="cuda")
+        a = render_args(d, n_sg, vdi.width, vdi.height, gcam, vdi.volume_aabb, grid.device(),
+                        grid.dims, grid.near, grid.far, rcam, vb.RenderOptions(), image,
+                        per_pixel=pp, stat_sums=sums)
+        zm = alloc_zmask(grid.dims)
+        launch_zmask(a, zm)
+        a.tile_counter = dv.ptr(counter) if dyn else None
+        _capi.check(L.vdi_render_launch(a, dv.stream_handle()))
+        torch.cuda.synchronize()
+        assert counter.cpu().tolist() == [0, 0]
+        outs.append([image.cpu().numpy()] + [x.cpu().numpy() for x in pp] + [sums.cpu().numpy()])
+    for other in outs[1:]:
+        for x, y in zip(outs[0], other):
+            np.testing.assert_array_equal(x, y)
+    assert outs[0][4][0] == outs[0][1].sum() > 0

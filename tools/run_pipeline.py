@@ -15,10 +15,13 @@ p = argparse.ArgumentParser()
 p.add_argument("--config", default="C3")
 p.add_argument("--reps", type=int, default=2)
 p.add_argument("--no-ranges", action="store_true", help="render without VdiRenderArgs.list_range")
+p.add_argument("--no-dyn", action="store_true", help="render without VdiRenderArgs.tile_counter")
 a = p.parse_args()
+from paper_2206_08660_b200.tuning import TUNING  # noqa: E402
 if a.no_ranges:
-    from paper_2206_08660_b200.tuning import TUNING
     TUNING.list_ranges = False
+if a.no_dyn:
+    TUNING.dyn_tiles = False
 vol, tf, gcam, rcam, n_sg = synth.config(a.config)
 pipe = shard.Pipeline(vol, tf, gcam, rcam, GenParams(n_sg=n_sg))
 for _ in range(a.reps):
