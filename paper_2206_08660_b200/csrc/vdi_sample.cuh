@@ -169,6 +169,9 @@ __device__ __forceinline__ double trilinear(const C& c, const double* tab, doubl
 // Returns how many samples from this one on (>= 1, <= max_run) are known to
 // be transparent, or 0 when this sample's brick is not an empty one.
 // inv_ext / ext_pow2 / c.a.aabb as in the sampler; only with c.ess.
+#ifndef VDI_RUN_F32
+#define VDI_RUN_F32 1
+#endif
 template <int VT, class C>
 __device__ __forceinline__ int empty_run(const C& c, const double* tab, const double o[3],
                                          const double d[3], double tm, double step,
@@ -202,11 +205,24 @@ __device__ __forceinline__ int empty_run(const C& c, const double* tab, const do
     const double lo = b0 == 0 ? -INFINITY : (double)b0;
     const double hi = b0 + B - 1 >= n[a] - 2 ? INFINITY : (double)(b0 + B);
     const double dg = d[a] * step * (double)(n[a] - 1) * c.inv_ext[a];
+#if VDI_RUN_F32
+    // the run only has to be a lower bound: an f32 quotient (relative error
+    // < 1e-6 after the two conversions) scaled by 1 - 2^-16 never exceeds
+    // the exact one, and a shorter run only re-enters this test
+    float lim = INFINITY;
+    if (dg > 0.0)
+      lim = __fdividef((float)(hi - 1e-6 - g[a]), (float)dg) * (1.0f - 0x1p-16f);
+    else if (dg < 0.0)
+      lim = __fdividef((float)(g[a] - lo - 1e-6), (float)-dg) * (1.0f - 0x1p-16f);
+    if (!(lim >= 0.0f)) return 1;  // within the margin of the brick's edge
+    if ((double)lim < (double)m) m = (long long)lim;
+#else
     double lim = INFINITY;
     if (dg > 0.0) lim = (hi - 1e-6 - g[a]) / dg;
     else if (dg < 0.0) lim = (g[a] - lo - 1e-6) / -dg;
     if (!(lim >= 0.0)) return 1;  // within the margin of the brick's edge
     if (lim < (double)m) m = (long long)lim;
+#endif
   }
   return 1 + (int)m;
 }
