@@ -107,6 +107,9 @@ struct RoundCtl {
   unsigned long long nwide;     // rays handed to the wide bisect phase
   unsigned long long wfetch;    // wide-phase pool (one ray per warp)
   unsigned long long ntorder;   // rays appended in overflow order
+  // VDI_BISECT_STATS builds only: narrow-replay steps on visible entries, on
+  // transparent runs, the entries the runs covered, replays started
+  unsigned long long st_vis, st_run, st_run_entries, st_replays;
   // bisection decisions seen so far in this round, per level: [0] up, [1] down
   // (the bisect replays' learned speculation direction)
   unsigned dir[2][32];
@@ -950,6 +953,9 @@ __global__ void __launch_bounds__(kThreads, kMinB) gen_bisect_kernel(const GenCo
   double d2max0 = 0.0;
   bool split0 = false;
   CountState q[kG];
+#ifdef VDI_BISECT_STATS
+  unsigned long long st_vis = 0, st_run = 0, st_run_entries = 0, st_replays = 0;
+#endif
 
   while (true) {
     const unsigned need = __ballot_sync(0xffffffffu, !have && !done);
@@ -1058,6 +1064,9 @@ __global__ void __launch_bounds__(kThreads, kMinB) gen_bisect_kernel(const GenCo
       }
       d2max0 = 0.0;
       split0 = false;
+#ifdef VDI_BISECT_STATS
+      st_replays += 1;
+#endif
       k = 0;
       if (kMode == 2) {
         ld_pred(b0, cache, 0 < stored);
@@ -1077,6 +1086,10 @@ __global__ void __launch_bounds__(kThreads, kMinB) gen_bisect_kernel(const GenCo
         run = __float_as_int(e.x);
         if (run < 1) run = 1;
         if (run > stored - k) run = stored - k;
+#ifdef VDI_BISECT_STATS
+        st_run += 1;
+        st_run_entries += run;
+#endif
 #pragma unroll
         for (int i = 0; i < kG; ++i) {
           // the transparent sample closes the segment (resolved states may
@@ -1105,6 +1118,9 @@ __global__ void __launch_bounds__(kThreads, kMinB) gen_bisect_kernel(const GenCo
 #pragma unroll
         for (int i = 1; i < kG; ++i)
           count_sample<false, kSmemOnly>(q[i], sr, sg, sb, k, n_sg, inv_n, c.inv_tab, s_inv);
+#ifdef VDI_BISECT_STATS
+        st_vis += 1;
+#endif
       }
       return run;
     };
@@ -1312,6 +1328,12 @@ __global__ void __launch_bounds__(kThreads, kMinB) gen_bisect_kernel(const GenCo
     }
     top = true;
   }
+#ifdef VDI_BISECT_STATS
+  atomicAdd(&c.ctl->st_vis, st_vis);
+  atomicAdd(&c.ctl->st_run, st_run);
+  atomicAdd(&c.ctl->st_run_entries, st_run_entries);
+  atomicAdd(&c.ctl->st_replays, st_replays);
+#endif
 }
 
 // ---------------------------------------------------------- wide bisect

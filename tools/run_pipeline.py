@@ -29,10 +29,13 @@ for _ in range(a.reps):
     print({k: round(v, 3) for k, v in ev.items()}, flush=True)
 torch.cuda.synchronize()
 print("samples", pipe.samples_executed(), "render stats", pipe.exact_render_stats())
-ctl = pipe.bufs.workspace[:64].view(torch.int64).cpu().tolist()
+ctl = pipe.bufs.workspace[:512].view(torch.int64).cpu().tolist()
 passes = pipe.bufs.passes.cpu()
 hit = int((passes > 0).sum())
 print(f"round0: queued rays {ctl[2]}, cached entries {ctl[1]} ({ctl[1]*16/1e9:.2f} GB), "
       f"deferred {ctl[4]}, handed to the wide bisect {ctl[7]}; hit rays {hit} of {passes.numel()}, "
       f"mean passes (hit) {float(passes[passes > 0].float().mean()):.2f}, "
       f"1-pass rays {int((passes == 1).sum())}")
+if any(ctl[10:14]):
+    print(f"bisect replays {ctl[13]}: visible steps {ctl[10]}, run steps {ctl[11]} "
+          f"covering {ctl[12]} entries")
