@@ -90,6 +90,23 @@ struct RayRec {
   int last_n, high_n;
 };
 
+// Where a queued ray's cache run is allocated: 0 = bump-allocated in the
+// sample phase when the ray overflows (overflow order), 1 = after the queue
+// compaction, by a prefix sum of row lengths in image order (rays past the
+// capacity are then a suffix of the queue, deferred to the next round).
+#ifndef VDI_ALLOC_IMAGE
+#define VDI_ALLOC_IMAGE 1
+#endif
+// The order the bisect / emit phases take the queue in: 0 = overflow order
+// (torder), 1 = image order (qidx). The two must agree: replay lanes run side
+// by side on neighbouring queue entries, and their cache rows have to be
+// neighbours in memory too. Measured C3 / C4 generation (ms): overflow /
+// overflow 30.6 / 78.6, image / overflow 35.0 / 87.3, overflow / image 35.0 /
+// 86.4, image / image 30.5 / 77.0 (a longest-row-first order: 40.0 / 88.4).
+#ifndef VDI_REPLAY_ORDER
+#define VDI_REPLAY_ORDER 1
+#endif
+
 // Cache entry of a non-transparent sample: the classified f32 RGBA, with the
 // sign bit of r (r >= 0 always) set when the step's opacity exponent
 // (tb - ta) / lref is not exactly 1, i.e. when the replay needs pow().
@@ -151,6 +168,7 @@ struct GenConst {
   unsigned long long* qsum;  // per compaction block
   int wide_after;    // replays a narrow lane runs on one ray before handing it off
   int wide_tail;     // also hand off every ray once the narrow queue is drained
+  int n_qblocks;     // queue compaction blocks (qsum holds 2 x (n_qblocks + 1))
   int chain_levels;  // bisect replays starting below this level use the down-chain shape
   int learn;         // learned chain directions at the later levels 
 };
@@ -571,8 +589,9 @@ __global__ void __launch_bounds__(kGenThreads, VDI_SAMPLE_MINB) gen_sample_kerne
         continue;
       }
       // overflow: needs the bisection -> reserve its cache run
-      const unsigned long long at = atomicAdd(&c.ctl->bump, (unsigned long long)s.nsteps);
-      if (at + (unsigned long long)s.nsteps > c.cache_cap) {
+      const unsigned long long at =
+          VDI_ALLOC_IMAGE ? 0ull : atomicAdd(&c.ctl->bump, (unsigned long long)s.nsteps);
+      if (!VDI_ALLOC_IMAGE && at + (unsigned long long)s.nsteps > c.cache_cap) {
         const unsigned long long j = atomicAdd(&c.ctl->ndefer, 1ull);
         c.defer_out[j] = s.list;
         have = false;
@@ -597,13 +616,22 @@ __global__ void __launch_bounds__(kGenThreads, VDI_SAMPLE_MINB) gen_sample_kerne
       r.pad = 0;
       c.recs[s.list] = r;
       atomicOr(c.qbits + (s.list >> 5), 1u << (s.list & 31));
-      // overflow order: rays that overflow together tend to have similar
-      // bisections, which keeps the replay warps coherent (image order made
-      // the bisect phase 17 % slower); the fill phase reads the image order
-      c.torder[atomicAdd(&c.ctl->ntorder, 1ull)] = s.list;
+      // overflow order (VDI_REPLAY_ORDER 0 only)
+      if (!VDI_REPLAY_ORDER) c.torder[atomicAdd(&c.ctl->ntorder, 1ull)] = s.list;
       have = false;
     }
   }
+}
+
+// The bisect / emit queue: its length and its idx-th ray (see VDI_REPLAY_ORDER;
+// with image-order allocation the overflow order also lists the deferred
+// rays, whose slot is -1).
+__device__ __forceinline__ long long replay_queue_len(const GenConst& c) {
+  return (long long)(VDI_REPLAY_ORDER ? c.ctl->nrec
+                                      : (VDI_ALLOC_IMAGE ? c.ctl->ntorder : c.ctl->nrec));
+}
+__device__ __forceinline__ int replay_queue_at(const GenConst& c, long long idx) {
+  return VDI_REPLAY_ORDER ? c.qidx[idx] : c.torder[idx];
 }
 
 // -------------------------------------------------------------- fill phase
@@ -929,7 +957,7 @@ __global__ void __launch_bounds__(kThreads, kMinB) gen_bisect_kernel(const GenCo
   asm volatile("mov.u32 %0, %1;\n" : "=r"(s_inv) : "r"((unsigned)__cvta_generic_to_shared(g_s_inv)));
   __syncthreads();
   const int lane = threadIdx.x & 31;
-  const long long nrec = (long long)c.ctl->nrec;
+  const long long nrec = replay_queue_len(c);
   const int n_sg = c.a.n_sg;
   WarpPool pool;
   bool have = false, done = false, top = false;
@@ -964,8 +992,8 @@ __global__ void __launch_bounds__(kThreads, kMinB) gen_bisect_kernel(const GenCo
       if ((need >> lane) & 1u) {
         if (idx >= nrec) {
           done = true;
-        } else {
-          rec = c.recs + c.torder[idx];
+        } else if (c.recs[replay_queue_at(c, idx)].slot >= 0) {  // (deferred: slot -1)
+          rec = c.recs + replay_queue_at(c, idx);
           cache = c.cache + rec->slot;
           stored = rec->nsteps;
           // state after the overflowing pass 1 (generate.py:253-273)
@@ -1509,7 +1537,7 @@ template <bool kRing>
 __global__ void __launch_bounds__(kGenThreads, VDI_EMIT_MINB) gen_emit_kernel(const GenConst c) {
   const int lane = threadIdx.x & 31;
   const double step = c.a.step;
-  const long long nrec = (long long)c.ctl->nrec;
+  const long long nrec = replay_queue_len(c);
   WarpPool pool;
   bool have = false, done = false;
   const float4* cache = nullptr;
@@ -1525,8 +1553,8 @@ __global__ void __launch_bounds__(kGenThreads, VDI_EMIT_MINB) gen_emit_kernel(co
       if ((need >> lane) & 1u) {
         if (idx >= nrec) {
           done = true;
-        } else {
-          const RayRec r = c.recs[c.torder[idx]];
+        } else if (c.recs[replay_queue_at(c, idx)].slot >= 0) {  // (deferred: slot -1)
+          const RayRec r = c.recs[replay_queue_at(c, idx)];
           s.list = r.list;
           s.seg = c.a.segs + (long long)r.list * list_stride(c.a.n_sg);
           s.o[0] = c.a.eye[0];
@@ -1695,50 +1723,111 @@ __global__ void __launch_bounds__(kGenThreads) gen_fused_kernel(const GenConst c
 // the fill warps running side by side sample the same record sectors (L2
 // reuse) and the replay warps hold rays of similar control flow.
 constexpr int kQBlock = 256;  // bit words per compaction block
+// bits of word w's queued lists and (VDI_ALLOC_IMAGE) the sum of their rows
+__device__ __forceinline__ unsigned long long word_steps(const GenConst& c, int w,
+                                                         unsigned bits) {
+  unsigned long long t = 0;
+  for (unsigned b = bits; b; b &= b - 1) t += (unsigned)c.recs[w * 32 + (__ffs(b) - 1)].nsteps;
+  return t;
+}
+
 __global__ void queue_count_kernel(const GenConst c, int n_words) {
   const int w = blockIdx.x * kQBlock + threadIdx.x;
-  int v = w < n_words ? __popc(c.qbits[w]) : 0;
+  const unsigned bits = w < n_words ? c.qbits[w] : 0u;
+  int v = __popc(bits);
+  unsigned long long st = VDI_ALLOC_IMAGE ? word_steps(c, w, bits) : 0ull;
 #pragma unroll
-  for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+  for (int off = 16; off > 0; off >>= 1) {
+    v += __shfl_xor_sync(0xffffffffu, v, off);
+    if (VDI_ALLOC_IMAGE) st += __shfl_xor_sync(0xffffffffu, st, off);
+  }
   __shared__ int s_w[kQBlock / 32];
-  if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = v;
+  __shared__ unsigned long long s_st[kQBlock / 32];
+  if ((threadIdx.x & 31) == 0) {
+    s_w[threadIdx.x >> 5] = v;
+    s_st[threadIdx.x >> 5] = st;
+  }
   __syncthreads();
   if (threadIdx.x == 0) {
     int t = 0;
-    for (int k = 0; k < kQBlock / 32; ++k) t += s_w[k];
+    unsigned long long ts = 0;
+    for (int k = 0; k < kQBlock / 32; ++k) {
+      t += s_w[k];
+      ts += s_st[k];
+    }
     c.qsum[blockIdx.x] = (unsigned long long)t;
+    if (VDI_ALLOC_IMAGE) c.qsum[c.n_qblocks + 1 + blockIdx.x] = ts;
   }
 }
 
 __global__ void queue_scan_kernel(const GenConst c, int nb) {
   // one thread: nb is small (2 Mi rays -> 256 blocks)
-  unsigned long long run = 0;
+  unsigned long long run = 0, srun = 0;
   for (int b = 0; b < nb; ++b) {
     const unsigned long long v = c.qsum[b];
     c.qsum[b] = run;
     run += v;
+    if (VDI_ALLOC_IMAGE) {
+      const unsigned long long u = c.qsum[c.n_qblocks + 1 + b];
+      c.qsum[c.n_qblocks + 1 + b] = srun;
+      srun += u;
+    }
   }
-  c.ctl->nrec = run;
+  c.ctl->nrec = run;  // VDI_ALLOC_IMAGE: lowered to the rays that fit by queue_write
+  if (VDI_ALLOC_IMAGE) c.ctl->bump = srun < c.cache_cap ? srun : c.cache_cap;
 }
 
 __global__ void queue_write_kernel(const GenConst c, int n_words) {
   __shared__ int s_w[kQBlock / 32];
+  __shared__ unsigned long long s_st[kQBlock / 32];
   const int w = blockIdx.x * kQBlock + threadIdx.x;
   const unsigned bits = w < n_words ? c.qbits[w] : 0u;
   const int cnt = __popc(bits);
+  const unsigned long long st = VDI_ALLOC_IMAGE ? word_steps(c, w, bits) : 0ull;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   int incl = cnt;
+  unsigned long long sincl = st;
 #pragma unroll
   for (int off = 1; off < 32; off <<= 1) {
     const int u = __shfl_up_sync(0xffffffffu, incl, off);
     if (lane >= off) incl += u;
+    if (VDI_ALLOC_IMAGE) {
+      const unsigned long long su = __shfl_up_sync(0xffffffffu, sincl, off);
+      if (lane >= off) sincl += su;
+    }
   }
-  if (lane == 31) s_w[wid] = incl;
+  if (lane == 31) {
+    s_w[wid] = incl;
+    s_st[wid] = sincl;
+  }
   __syncthreads();
   int before = 0;
-  for (int k = 0; k < wid; ++k) before += s_w[k];
+  unsigned long long sbefore = 0;
+  for (int k = 0; k < wid; ++k) {
+    before += s_w[k];
+    sbefore += s_st[k];
+  }
   long long at = (long long)c.qsum[blockIdx.x] + before + incl - cnt;
-  for (unsigned b = bits; b; b &= b - 1) c.qidx[at++] = w * 32 + (__ffs(b) - 1);
+  if (!VDI_ALLOC_IMAGE) {
+    for (unsigned b = bits; b; b &= b - 1) c.qidx[at++] = w * 32 + (__ffs(b) - 1);
+    return;
+  }
+  unsigned long long slot = c.qsum[c.n_qblocks + 1 + blockIdx.x] + sbefore + sincl - st;
+  for (unsigned b = bits; b; b &= b - 1) {
+    const int list = w * 32 + (__ffs(b) - 1);
+    RayRec* r = c.recs + list;
+    const unsigned long long n = (unsigned)r->nsteps;
+    if (slot + n <= c.cache_cap) {
+      r->slot = (long long)slot;
+      c.qidx[at] = list;
+    } else {  // past the capacity: this and every later ray of the queue
+      r->slot = -1;
+      c.defer_out[atomicAdd(&c.ctl->ndefer, 1ull)] = list;
+      atomicMin(&c.ctl->nrec, (unsigned long long)at);
+    }
+    ++at;
+    slot += n;
+  }
 }
 
 __global__ void fill_inv_kernel(double* tab, int n) {
@@ -1871,7 +1960,7 @@ static int plan_gen(const VdiGenArgs* a, GenPlan& p) {
   p.off_qidx = up(p.off_qbits + sizeof(unsigned) * (size_t)p.n_qwords);
   p.off_torder = up(p.off_qidx + sizeof(int) * (size_t)p.n_rays);
   p.off_qsum = up(p.off_torder + sizeof(int) * (size_t)p.n_rays);
-  p.off_cache = up(p.off_qsum + sizeof(unsigned long long) * (size_t)(p.n_qblocks + 1));
+  p.off_cache = up(p.off_qsum + sizeof(unsigned long long) * (size_t)(2 * (p.n_qblocks + 1)));
   return VDI_OK;
 }
 
@@ -2105,6 +2194,7 @@ int gen_launch(const VdiGenArgs* a, cudaStream_t stream) {
   c.qidx = reinterpret_cast<int*>(ws + p.off_qidx);
   c.torder = reinterpret_cast<int*>(ws + p.off_torder);
   c.qsum = reinterpret_cast<unsigned long long*>(ws + p.off_qsum);
+  c.n_qblocks = p.n_qblocks;
   c.cache = reinterpret_cast<float4*>(ws + p.off_cache);
   c.cache_cap = (a->workspace_bytes - p.off_cache) / sizeof(float4);
   int* defer[2] = {reinterpret_cast<int*>(ws + p.off_defer0),
