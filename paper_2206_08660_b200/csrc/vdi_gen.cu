@@ -64,6 +64,9 @@ constexpr int kGenThreads = 128;
 #else
 #define VDI_FILL_BOUNDS __launch_bounds__(kGenThreads)
 #endif
+#ifndef VDI_EMIT_PF
+#define VDI_EMIT_PF 1
+#endif
 #ifndef VDI_EMIT_MINB
 #define VDI_EMIT_MINB 6  // 80 registers: 6 blocks/SM (measured: 6.16 -> 5.64 ms at C3)
 #endif
@@ -1605,6 +1608,10 @@ __global__ void __launch_bounds__(kGenThreads, VDI_EMIT_MINB) gen_emit_kernel(co
     if (!kRing) {
       ended = s.k >= stored ? 0 : entry_step(cache[s.k]);
     } else {
+      // (VDI_EMIT_PF: an L1 prefetch of the line kEmitAhead entries ahead
+      // whenever that point crosses a line, as in the bisect replays -- the
+      // last rays of a launch run alone and wait out every miss)
+      constexpr int kEmitAhead = 16;
       for (int it = 0; it < 4; ++it) {
         if (s.k >= stored) {
           ended = 0;
@@ -1617,9 +1624,13 @@ __global__ void __launch_bounds__(kGenThreads, VDI_EMIT_MINB) gen_emit_kernel(co
         if (s.k != kold + 1) {
           ld_pred(b0, cache + s.k, s.k < stored);
           ld_pred(b1, cache + s.k + 1, s.k + 1 < stored);
+          if (VDI_EMIT_PF) prefetch_l1(cache + (s.k & ~7) + 8);
           continue;
         }
         ld_pred(b0, cache + s.k + 1, s.k + 1 < stored);
+        if (VDI_EMIT_PF && (((kold + kEmitAhead) ^ (s.k + kEmitAhead)) & ~7) != 0 &&
+            s.k + kEmitAhead < stored)
+          prefetch_l1(cache + s.k + kEmitAhead);
         // step B: b1 = entry k, b0 = entry k + 1 (s.k < stored: the pass goes on)
         kold = s.k;
         ended = entry_step(b1);
@@ -1627,9 +1638,13 @@ __global__ void __launch_bounds__(kGenThreads, VDI_EMIT_MINB) gen_emit_kernel(co
         if (s.k != kold + 1) {
           ld_pred(b0, cache + s.k, s.k < stored);
           ld_pred(b1, cache + s.k + 1, s.k + 1 < stored);
+          if (VDI_EMIT_PF) prefetch_l1(cache + (s.k & ~7) + 8);
           continue;
         }
         ld_pred(b1, cache + s.k + 1, s.k + 1 < stored);
+        if (VDI_EMIT_PF && (((kold + kEmitAhead) ^ (s.k + kEmitAhead)) & ~7) != 0 &&
+            s.k + kEmitAhead < stored)
+          prefetch_l1(cache + s.k + kEmitAhead);
       }
     }
     if (ended >= 0) {
