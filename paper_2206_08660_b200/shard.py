@@ -348,10 +348,11 @@ class Pipeline:
         self.tiles = (alloc_list_tiles(w, h) if use_list_tiles() else None)
         self.zmask = alloc_zmask(self.grid_dims) if self.opts.use_ess else None
         # this package's kernels per step: brick maxima (+ corner records);
-        # vdi_gen_launch = fill_inv + 3 rounds x (sample, queue count / scan /
-        # write, fill, bisect, wide bisect, emit) + the fused fallback; grid;
-        # the render's slab words (+ tile bitmap, + list ranges) and the render
-        self.launches_per_step = (1 + (self.cells is not None) + 1 + 3 * 8 + 1 + 1
+        # vdi_gen_launch = fill_inv + ray setup + 3 rounds x (sample, queue
+        # count / scan / write, fill, bisect, wide bisect, emit) + the fused
+        # fallback; grid; the render's slab words (+ tile bitmap, + list
+        # ranges) and the render
+        self.launches_per_step = (1 + (self.cells is not None) + 2 + 3 * 8 + 1 + 1
                                   + (self.tiles is not None) + (self.zmask is not None) + 1)
         if world > 1:
             import torch.distributed as tdist
