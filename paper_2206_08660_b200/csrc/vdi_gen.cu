@@ -457,7 +457,8 @@ __device__ __forceinline__ void init_bisection(const GenConst& c, RayState& s) {
 }
 
 // Ray setup (generate.py:282-309) for local list `list`. Returns false on a
-// miss (the list is then published empty).
+// miss (the list is then published empty, unless kPublishMiss is false).
+template <bool kPublishMiss = true>
 __device__ bool setup_ray(const GenConst& c, RayState& s, int list) {
   const int lx = list % c.a.width, ly = list / c.a.width;
   const int gy = image_row(ly, c.a.band_rows, c.a.band_stride, c.a.band_offset, c.a.row_base,
@@ -478,7 +479,7 @@ __device__ bool setup_ray(const GenConst& c, RayState& s, int list) {
   }
   init_bisection(c, s);
   if (!hit) {
-    finish_ray(c, s, 0.0, 0);
+    if (kPublishMiss) finish_ray(c, s, 0.0, 0);
     return false;
   }
   s.t0 = t0;
@@ -578,8 +579,13 @@ __global__ void __launch_bounds__(kGenThreads) gen_setup_kernel(const GenConst c
   bool hit = false;
   if (list >= 0) {
     RayState s;
-    hit = setup_ray(c, s, list);
-    if (hit) {
+    hit = setup_ray<false>(c, s, list);
+    if (!hit) {  // finish_ray's per-list outputs; the slot is zeroed below
+      c.a.counts[list] = 0;
+      if (c.a.gammas) c.a.gammas[list] = 0.0;
+      if (c.a.passes) c.a.passes[list] = 0;
+      if (c.a.samples) c.a.samples[list] = 0;
+    } else {
       RayRec* r = c.recs + list;
       r->d[0] = s.d[0];
       r->d[1] = s.d[1];
@@ -589,6 +595,14 @@ __global__ void __launch_bounds__(kGenThreads) gen_setup_kernel(const GenConst c
       r->nsteps = s.nsteps;
       r->list = list;
     }
+  }
+  // the misses' list slots zeroed by the whole warp, one coalesced slot at a
+  // time (finish_ray's zero-fill of all n_sg entries; the slot's padding too)
+  const int stride = list_stride(c.a.n_sg);
+  for (unsigned mm = __ballot_sync(0xffffffffu, list >= 0 && !hit); mm; mm &= mm - 1) {
+    const int l = __shfl_sync(0xffffffffu, list, __ffs(mm) - 1);
+    float4* slot4 = reinterpret_cast<float4*>(c.a.segs + (long long)l * stride);
+    for (int i = lane; i < stride / 4; i += 32) slot4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
   }
   const unsigned m = __ballot_sync(0xffffffffu, hit);
   unsigned long long base = 0;
