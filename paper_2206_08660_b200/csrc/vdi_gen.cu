@@ -963,16 +963,22 @@ __device__ __forceinline__ double lds_f64(unsigned addr) {
   return v;
 }
 
+// opened = the segments opened so far = R's count + (a segment is open): a
+// transparent sample only closes (opened unchanged), a visible one that does
+// not merge opens one (a split closes one and opens one), and R aborts a
+// counting pass exactly when a visible sample would open segment n_sg + 1
+// (generate.py:146-150, 176-180), i.e. !merge && opened >= n_sg. At the
+// natural end R's n = count + active = opened.
 struct CountState {
   double mr, mg, mb, thr;
-  int count, nsamp, kend, n;  // n >= 0 once resolved
+  int opened, nsamp, kend, n;  // n >= 0 once resolved
   bool active;
 };
 
 __device__ __forceinline__ void count_reset(CountState& q, double gamma) {
   q.thr = split_threshold(gamma);
   q.mr = q.mg = q.mb = 0.0;
-  q.count = 0;
+  q.opened = 0;
   q.nsamp = 0;
   q.kend = 0;
   q.n = -1;
@@ -999,13 +1005,12 @@ __device__ __forceinline__ void count_sample(CountState& q, double sr, double sg
   const bool far = d2 >= q.thr;
   const bool live = q.n < 0;
   const bool merge = q.active && !far;
-  const bool split = q.active && far;
   if (kTrack) {
     // the split test's d^2 along this state's trajectory (see gen_bisect_kernel)
     if (live && q.active && d2 > *d2max) *d2max = d2;
-    if (live && split) *split_seen = true;
+    if (live && q.active && far) *split_seen = true;
   }
-  const bool abort = (!q.active && q.count >= n_sg) || (split && q.count + 1 >= n_sg);
+  const bool abort = !merge && q.opened >= n_sg;
   const int ns = q.nsamp + 1;
   // nsamp <= max_steps, which the global table always covers; the shared copy
   // holds the first inv_n entries (selecting between two loads, never a
@@ -1016,7 +1021,7 @@ __device__ __forceinline__ void count_sample(CountState& q, double sr, double sg
   const double nr = q.mr + tr * inv, ng = q.mg + tg * inv, nb = q.mb + tb * inv;
   q.n = live && abort ? n_sg + 1 : q.n;
   q.kend = live && abort ? k + 1 : q.kend;
-  q.count += split ? 1 : 0;
+  q.opened += merge ? 0 : 1;
   q.mr = merge ? nr : sr;
   q.mg = merge ? ng : sg;
   q.mb = merge ? nb : sb;
@@ -1209,7 +1214,6 @@ __global__ void __launch_bounds__(kThreads, kMinB) gen_bisect_kernel(const GenCo
         for (int i = 0; i < kG; ++i) {
           // the transparent sample closes the segment (resolved states may
           // keep stepping, see count_sample)
-          q[i].count += q[i].active ? 1 : 0;
           q[i].active = false;
         }
       } else {
@@ -1250,7 +1254,7 @@ __global__ void __launch_bounds__(kThreads, kMinB) gen_bisect_kernel(const GenCo
 #pragma unroll
       for (int i = 0; i < kG; ++i)
         if (q[i].n < 0) {
-          q[i].n = q[i].count + (q[i].active ? 1 : 0);
+          q[i].n = q[i].opened;
           q[i].kend = stored;
         }
     };
@@ -1261,13 +1265,11 @@ __global__ void __launch_bounds__(kThreads, kMinB) gen_bisect_kernel(const GenCo
           resolved = true;
           break;
         }
-        // step A: b0 = entry k, b1 = entry k + 1
+        // step A: b0 = entry k, b1 = entry k + 1 (resolution is tested after
+        // step B only: a resolved state's n and kend are frozen, so one more
+        // step costs a step, not a result)
         int kold = k;
         k += consume(b0);
-        if (all_resolved()) {
-          resolved = true;
-          break;
-        }
         if (k != kold + 1) {  // skipped a transparent run: refill both slots
           ld_pred(b0, cache + k, k < stored);
           ld_pred(b1, cache + k + 1, k + 1 < stored);
@@ -1302,7 +1304,7 @@ __global__ void __launch_bounds__(kThreads, kMinB) gen_bisect_kernel(const GenCo
 #pragma unroll
       for (int i = 0; i < kG; ++i)
         if (q[i].n < 0) {
-          q[i].n = q[i].count + (q[i].active ? 1 : 0);
+          q[i].n = q[i].opened;
           q[i].kend = stored;
         }
       resolved = true;
@@ -1315,10 +1317,7 @@ __global__ void __launch_bounds__(kThreads, kMinB) gen_bisect_kernel(const GenCo
         if (run > stored - k) run = stored - k;
 #pragma unroll
         for (int i = 0; i < kG; ++i)
-          if (q[i].n < 0 && q[i].active) {
-            q[i].count += 1;  // the transparent sample closes the segment
-            q[i].active = false;
-          }
+          q[i].active = false;  // the transparent sample closes the segment
       } else {
         const double a = (double)e.w;
         double a_adj;
@@ -1531,7 +1530,7 @@ __global__ void __launch_bounds__(kGenThreads) gen_bisect_wide_kernel(const GenC
       while (true) {
         if (k >= stored) {
           if (q.n < 0) {
-            q.n = q.count + (q.active ? 1 : 0);
+            q.n = q.opened;
             q.kend = stored;
           }
           break;
@@ -1557,7 +1556,7 @@ __global__ void __launch_bounds__(kGenThreads) gen_bisect_wide_kernel(const GenC
           run = __float_as_int(e.x);
           if (run < 1) run = 1;
           if (run > stored - k) run = stored - k;
-          q.count += q.active ? 1 : 0;  // the transparent sample closes the segment
+          // the transparent sample closes the segment (opened unchanged)
           q.active = false;
         } else {
           const double a = (double)e.w;
