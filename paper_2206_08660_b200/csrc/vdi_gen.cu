@@ -969,19 +969,21 @@ __device__ __forceinline__ double lds_f64(unsigned addr) {
 // counting pass exactly when a visible sample would open segment n_sg + 1
 // (generate.py:146-150, 176-180), i.e. !merge && opened >= n_sg. At the
 // natural end R's n = count + active = opened.
+// kend == 0 while the state is live; an abort sets kend = k + 1 (n stays
+// n_sg + 1), the natural end sets kend = stored and n = opened.
 struct CountState {
   double mr, mg, mb, thr;
-  int opened, nsamp, kend, n;  // n >= 0 once resolved
+  int opened, nsamp, kend, n;
   bool active;
 };
 
-__device__ __forceinline__ void count_reset(CountState& q, double gamma) {
+__device__ __forceinline__ void count_reset(CountState& q, double gamma, int n_sg) {
   q.thr = split_threshold(gamma);
   q.mr = q.mg = q.mb = 0.0;
   q.opened = 0;
   q.nsamp = 0;
   q.kend = 0;
-  q.n = -1;
+  q.n = n_sg + 1;
   q.active = false;
 }
 
@@ -1003,12 +1005,14 @@ __device__ __forceinline__ void count_sample(CountState& q, double sr, double sg
   const double tr = sr - q.mr, tg = sg - q.mg, tb = sb - q.mb;
   const double d2 = tr * tr + tg * tg + tb * tb;
   const bool far = d2 >= q.thr;
-  const bool live = q.n < 0;
+  const bool live = q.kend == 0;
   const bool merge = q.active && !far;
   if (kTrack) {
-    // the split test's d^2 along this state's trajectory (see gen_bisect_kernel)
-    if (live && q.active && d2 > *d2max) *d2max = d2;
-    if (live && q.active && far) *split_seen = true;
+    // the split test's d^2 along this state's trajectory (see gen_bisect_kernel;
+    // read only when the state ran to the natural end, i.e. was live on
+    // every step, so the steps after an abort need no guard)
+    if (q.active && d2 > *d2max) *d2max = d2;
+    if (q.active && far) *split_seen = true;
   }
   const bool abort = !merge && q.opened >= n_sg;
   const int ns = q.nsamp + 1;
@@ -1019,7 +1023,6 @@ __device__ __forceinline__ void count_sample(CountState& q, double sr, double sg
                                : (ns < inv_n ? lds_f64(s_inv + 8u * (unsigned)ns)
                                              : __ldg(g_inv + ns));
   const double nr = q.mr + tr * inv, ng = q.mg + tg * inv, nb = q.mb + tb * inv;
-  q.n = live && abort ? n_sg + 1 : q.n;
   q.kend = live && abort ? k + 1 : q.kend;
   q.opened += merge ? 0 : 1;
   q.mr = merge ? nr : sr;
@@ -1180,7 +1183,7 @@ __global__ void __launch_bounds__(kThreads, kMinB) gen_bisect_kernel(const GenCo
           lo[2 * i + 2] = lo[i];
           hi[2 * i + 2] = gam[i];
         }
-        count_reset(q[i], gam[i]);
+        count_reset(q[i], gam[i], n_sg);
       }
       d2max0 = 0.0;
       split0 = false;
@@ -1246,14 +1249,14 @@ __global__ void __launch_bounds__(kThreads, kMinB) gen_bisect_kernel(const GenCo
     auto all_resolved = [&]() {
       bool r = true;
 #pragma unroll
-      for (int i = 0; i < kG; ++i) r = r && q[i].n >= 0;
+      for (int i = 0; i < kG; ++i) r = r && q[i].kend != 0;
       return r;
     };
     auto natural_end = [&]() {
       // natural end (or the tb <= ta break)
 #pragma unroll
       for (int i = 0; i < kG; ++i)
-        if (q[i].n < 0) {
+        if (q[i].kend == 0) {
           q[i].n = q[i].opened;
           q[i].kend = stored;
         }
@@ -1303,7 +1306,7 @@ __global__ void __launch_bounds__(kThreads, kMinB) gen_bisect_kernel(const GenCo
       // natural end (or the tb <= ta break)
 #pragma unroll
       for (int i = 0; i < kG; ++i)
-        if (q[i].n < 0) {
+        if (q[i].kend == 0) {
           q[i].n = q[i].opened;
           q[i].kend = stored;
         }
@@ -1345,7 +1348,7 @@ __global__ void __launch_bounds__(kThreads, kMinB) gen_bisect_kernel(const GenCo
       pipe.advance(cache, kold, k, stored);
       resolved = true;
 #pragma unroll
-      for (int i = 0; i < kG; ++i) resolved = resolved && q[i].n >= 0;
+      for (int i = 0; i < kG; ++i) resolved = resolved && q[i].kend != 0;
      }
     }
     if (!resolved) continue;
@@ -1391,7 +1394,7 @@ __global__ void __launch_bounds__(kThreads, kMinB) gen_bisect_kernel(const GenCo
         break;
       }
     }
-    if (!fin && !split0 && q[0].n >= 0 && q[0].n <= n_sg && q[0].kend == stored) {
+    if (!fin && !split0 && q[0].n <= n_sg && q[0].kend == stored) {
       // levels whose gamma is above the certified no-split bound: n = q[0].n,
       // a full pass each (generate.py:237-273 with the known count)
       const double dstar = sqrt(d2max0);
@@ -1519,9 +1522,9 @@ __global__ void __launch_bounds__(kGenThreads) gen_bisect_wide_kernel(const GenC
           if ((x >> b) & 1u) hi = g;
           else lo = g;
         }
-        count_reset(q, 0.5 * (lo + hi));
+        count_reset(q, 0.5 * (lo + hi), n_sg);
       }
-      if (sl >= kG) q.n = 0;  // the spare lane is resolved from the start
+      if (sl >= kG) q.kend = 1;  // the spare lane is resolved from the start
       // walk the row: lane sl holds entry base + sl of the current chunk of
       // kLanes entries and base + kLanes + sl of the next (loaded ahead)
       int k = 0;
@@ -1529,7 +1532,7 @@ __global__ void __launch_bounds__(kGenThreads) gen_bisect_wide_kernel(const GenC
       float4 ent = make_float4(0.f, 0.f, 0.f, 0.f), nxt = ent;
       while (true) {
         if (k >= stored) {
-          if (q.n < 0) {
+          if (q.kend == 0) {
             q.n = q.opened;
             q.kend = stored;
           }
@@ -1577,7 +1580,7 @@ __global__ void __launch_bounds__(kGenThreads) gen_bisect_wide_kernel(const GenC
           count_sample<false, kSmemOnly>(q, sr, sg, sb, k, n_sg, inv_n, c.inv_tab, s_inv);
         }
         k += run;
-        if (__all_sync(gm, q.n >= 0)) break;
+        if (__all_sync(gm, q.kend != 0)) break;
       }
       // replay R's control flow over the counts (generate.py:237-273)
       int node = 0;
