@@ -64,6 +64,12 @@ constexpr int kGenThreads = 128;
 #else
 #define VDI_FILL_BOUNDS __launch_bounds__(kGenThreads)
 #endif
+#ifndef VDI_BISECT_PF
+#define VDI_BISECT_PF 1     // cache-row prefetch of the replays: 1 L1, 2 L2, 3 L1 + bulk L2
+#endif
+#ifndef VDI_BISECT_AHEAD
+#define VDI_BISECT_AHEAD 16  // entries ahead of the L1 prefetch
+#endif
 #ifndef VDI_EMIT_PF
 #define VDI_EMIT_PF 1
 #endif
@@ -1861,21 +1867,58 @@ __global__ void queue_count_kernel(const GenConst c, int n_words) {
   }
 }
 
-__global__ void queue_scan_kernel(const GenConst c, int nb) {
-  // one thread: nb is small (2 Mi rays -> 256 blocks)
+// Exclusive scans of the per-block counts (and row-length sums) in place: one
+// block of kScanThreads threads, kScanThreads block entries per chunk.
+constexpr int kScanThreads = 1024;
+__device__ __forceinline__ unsigned long long block_excl_scan(unsigned long long v,
+                                                              unsigned long long* s_w,
+                                                              unsigned long long& total) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  unsigned long long incl = v;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const unsigned long long u = __shfl_up_sync(0xffffffffu, incl, off);
+    if (lane >= off) incl += u;
+  }
+  if (lane == 31) s_w[wid] = incl;
+  __syncthreads();
+  if (wid == 0) {
+    unsigned long long w = lane < kScanThreads / 32 ? s_w[lane] : 0ull;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const unsigned long long u = __shfl_up_sync(0xffffffffu, w, off);
+      if (lane >= off) w += u;
+    }
+    if (lane < kScanThreads / 32) s_w[lane] = w;  // inclusive per-warp totals
+  }
+  __syncthreads();
+  total = s_w[kScanThreads / 32 - 1];
+  const unsigned long long before = wid > 0 ? s_w[wid - 1] : 0ull;
+  __syncthreads();  // s_w is reused by the next call
+  return before + incl - v;
+}
+
+__global__ void __launch_bounds__(kScanThreads) queue_scan_kernel(const GenConst c, int nb) {
+  __shared__ unsigned long long s_w[kScanThreads / 32];
   unsigned long long run = 0, srun = 0;
-  for (int b = 0; b < nb; ++b) {
-    const unsigned long long v = c.qsum[b];
-    c.qsum[b] = run;
-    run += v;
+  for (int b0 = 0; b0 < nb; b0 += kScanThreads) {
+    const int b = b0 + threadIdx.x;
+    unsigned long long tot = 0;
+    const unsigned long long v = b < nb ? c.qsum[b] : 0ull;
+    const unsigned long long ex = block_excl_scan(v, s_w, tot);
+    if (b < nb) c.qsum[b] = run + ex;
+    run += tot;
     if (VDI_ALLOC_IMAGE) {
-      const unsigned long long u = c.qsum[c.n_qblocks + 1 + b];
-      c.qsum[c.n_qblocks + 1 + b] = srun;
-      srun += u;
+      const unsigned long long u = b < nb ? c.qsum[c.n_qblocks + 1 + b] : 0ull;
+      const unsigned long long sx = block_excl_scan(u, s_w, tot);
+      if (b < nb) c.qsum[c.n_qblocks + 1 + b] = srun + sx;
+      srun += tot;
     }
   }
-  c.ctl->nrec = run;  // VDI_ALLOC_IMAGE: lowered to the rays that fit by queue_write
-  if (VDI_ALLOC_IMAGE) c.ctl->bump = srun < c.cache_cap ? srun : c.cache_cap;
+  if (threadIdx.x == 0) {
+    c.ctl->nrec = run;  // VDI_ALLOC_IMAGE: lowered to the rays that fit by queue_write
+    if (VDI_ALLOC_IMAGE) c.ctl->bump = srun < c.cache_cap ? srun : c.cache_cap;
+  }
 }
 
 __global__ void queue_write_kernel(const GenConst c, int n_words) {
@@ -2019,8 +2062,8 @@ static int plan_gen(const VdiGenArgs* a, GenPlan& p) {
 #define VDI_BISECT_MINB 5
 #endif
   p.bisect = p.inv_n <= p.inv_smem
-                 ? gen_bisect_kernel<2, 2, 1, VDI_BISECT_MINB, 128, 16, 2, true>
-                 : gen_bisect_kernel<2, 2, 1, VDI_BISECT_MINB, 128, 16, 2, false>;
+                 ? gen_bisect_kernel<2, 2, VDI_BISECT_PF, VDI_BISECT_MINB, 128, VDI_BISECT_AHEAD, 2, true>
+                 : gen_bisect_kernel<2, 2, VDI_BISECT_PF, VDI_BISECT_MINB, 128, VDI_BISECT_AHEAD, 2, false>;
 #ifndef VDI_WIDE_LANES
 #define VDI_WIDE_LANES 32
 #endif
@@ -2327,7 +2370,7 @@ int gen_launch(const VdiGenArgs* a, cudaStream_t stream) {
                          stream>>>(c);
     p.sample<<<grid_for(p.per_sm_sample, r == 0 ? chunks : -1), kGenThreads, p.smem, stream>>>(c);
     queue_count_kernel<<<p.n_qblocks, kQBlock, 0, stream>>>(c, p.n_qwords);
-    queue_scan_kernel<<<1, 1, 0, stream>>>(c, p.n_qblocks);
+    queue_scan_kernel<<<1, kScanThreads, 0, stream>>>(c, p.n_qblocks);
     queue_write_kernel<<<p.n_qblocks, kQBlock, 0, stream>>>(c, p.n_qwords);
     p.fill<<<grid_for(p.per_sm_fill, -1), kGenThreads, p.smem, stream>>>(c);
     p.bisect<<<grid_for(p.per_sm_bisect, -1), p.bisect_threads, p.smem_inv, stream>>>(c);

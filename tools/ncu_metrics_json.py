@@ -13,9 +13,11 @@ import subprocess
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-PHASES = ["brick_max", "cells", "fill_inv", "gen_sample", "gen_fill", "gen_bisect", "gen_emit",
-          "gen_fused", "grid_kernel", "grid_zmask", "render_kernel"]
-GEN = ("fill_inv", "gen_sample", "gen_fill", "gen_bisect", "gen_emit", "gen_fused")
+PHASES = ["brick_max", "cells", "fill_inv", "gen_setup", "gen_sample", "queue_", "gen_fill",
+          "gen_bisect_wide", "gen_bisect", "gen_emit", "gen_fused", "grid_kernel", "grid_zmask",
+          "list_ranges", "render_kernel"]
+GEN = ("fill_inv", "gen_setup", "gen_sample", "queue_", "gen_fill", "gen_bisect_wide",
+       "gen_bisect", "gen_emit", "gen_fused")
 
 
 def phase_of(name):
