@@ -190,17 +190,26 @@ def launch_generate(vol_dev, voxel_type, dims, lut_dev, cam, aabb, params, resol
 _shared_ws = {}
 
 
-def shared_workspace(nbytes: int):
+def shared_workspace(nbytes: int, min_bytes: int | None = None):
     """One generation scratch buffer per device, reused by every
     generate_vdi call (in stream order) and grown when a call needs more:
     the recommended size can be tens of GB, and allocating it per call
-    thrashes the caching allocator."""
+    thrashes the caching allocator. If `nbytes` cannot be allocated (other
+    allocations on the device), falls back to `min_bytes`: the kernels then
+    defer the rays that do not fit to later rounds (same results)."""
     t = dv.torch()
     dev = t.cuda.current_device()
     ws = _shared_ws.get(dev)
     if ws is None or ws.numel() < nbytes:
         _shared_ws.pop(dev, None)
-        ws = t.empty(nbytes, dtype=t.uint8, device="cuda")
+        ws = None
+        try:
+            ws = t.empty(nbytes, dtype=t.uint8, device="cuda")
+        except t.OutOfMemoryError:
+            if min_bytes is None or min_bytes >= nbytes:
+                raise
+            t.cuda.empty_cache()
+            ws = t.empty(min_bytes, dtype=t.uint8, device="cuda")
         _shared_ws[dev] = ws
     return ws
 
@@ -229,7 +238,9 @@ def generate_vdi(vol, tf, cam, params: GenParams | None = None, grid_dims=None,
     bufs = alloc_gen(width, height, params.n_sg, grid_dims, stats=with_stats)
     a = gen_args(vol_dev, vt, vol.dims, lut_dev, cam, aabb, resolved, params.n_sg,
                  params.epsilon, params.gamma_init, bufs)
-    bufs.workspace = shared_workspace(int(_capi.load().vdi_gen_workspace_bytes(a)))
+    L = _capi.load()
+    bufs.workspace = shared_workspace(int(L.vdi_gen_workspace_bytes(a)),
+                                      int(L.vdi_gen_workspace_min_bytes(a)))
     bricks = dv.volume_bricks(vol_dev, vt, vol.dims)
     cells = dv.volume_cells(vol_dev, vt, vol.dims) if dv.use_cells(vt, vol.dims) else None
     launch_generate(vol_dev, vt, vol.dims, lut_dev, cam, aabb, params, resolved, bufs,
