@@ -67,6 +67,15 @@ constexpr int kGenThreads = 128;
 #ifndef VDI_BISECT_PF
 #define VDI_BISECT_PF 1     // cache-row prefetch of the replays: 1 L1, 2 L2, 3 L1 + bulk L2
 #endif
+#ifndef VDI_BISECT_MODE
+// cache stream: 2 A/B register slots + L1 prefetch, 3 cp.async ring in shared
+// memory (measured C3 / C4 gen: 26.8 / 68.2 ms -> 23.1 / 61.6 ms with a ring
+// of 4 at 4 blocks/SM; ring 8: 23.2 / 61.9)
+#define VDI_BISECT_MODE 3
+#endif
+#ifndef VDI_BISECT_RING
+#define VDI_BISECT_RING 4   // kMode 3: ring entries per lane (power of two)
+#endif
 #ifndef VDI_BISECT_AHEAD
 #define VDI_BISECT_AHEAD 16  // entries ahead of the L1 prefetch
 #endif
@@ -910,6 +919,31 @@ struct EntryPipe {
 // predicated 16-B load into the registers of `v` itself (left unchanged when
 // !pred): written in PTX so the compiler cannot load into a temporary and
 // select afterwards
+// Asynchronous 16-B copies global -> shared (LDGSTS), for the kMode 3 rings:
+// a lane keeps its next cache entries in flight in shared memory instead of
+// registers. src-size 0 copies nothing (zero-fills), so the issue needs no
+// branch past the end of a row.
+__device__ __forceinline__ void cp_async16(unsigned dst, const void* src, bool pred) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src),
+               "r"(pred ? 16 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ float4 lds128(unsigned addr) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];\n"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(addr)
+               : "memory");
+  return v;
+}
+
 __device__ __forceinline__ void ld_pred(float4& v, const float4* p, bool pred) {
   asm volatile(
       "{\n .reg .pred q;\n setp.ne.b32 q, %5, 0;\n"
@@ -1055,6 +1089,22 @@ __global__ void __launch_bounds__(kThreads, kMinB) gen_bisect_kernel(const GenCo
   // rematerialise it from SR_CgaCtaId at every use
   unsigned s_inv;
   asm volatile("mov.u32 %0, %1;\n" : "=r"(s_inv) : "r"((unsigned)__cvta_generic_to_shared(g_s_inv)));
+  // kMode 3: this lane's ring of kDepth cache entries, slot-major (slot j of
+  // thread t at (j * kThreads + t) * 16: conflict-free across the warp)
+  __shared__ float4 s_ring[kMode == 3 ? kDepth * kThreads : 1];
+  const unsigned ring0 = (unsigned)__cvta_generic_to_shared(s_ring) + 16u * threadIdx.x;
+  auto ring_at = [&](int k) -> unsigned {
+    return ring0 + 16u * (unsigned)kThreads * (unsigned)(k & (kDepth - 1));
+  };
+  // entries k .. k + kDepth - 2 in flight, one commit group each
+  auto ring_fill = [&](const float4* row, int k, int stored) {
+    cp_async_wait<0>();  // a stale copy must not land over a new one
+#pragma unroll
+    for (int j = 0; j < kDepth - 1; ++j) {
+      cp_async16(ring_at(k + j), row + (k + j < stored ? k + j : 0), k + j < stored);
+      cp_async_commit();
+    }
+  };
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const long long nrec = replay_queue_len(c);
@@ -1196,7 +1246,9 @@ __global__ void __launch_bounds__(kThreads, kMinB) gen_bisect_kernel(const GenCo
       st_replays += 1;
 #endif
       k = 0;
-      if (kMode == 2) {
+      if (kMode == 3) {
+        ring_fill(cache, 0, stored);
+      } else if (kMode == 2) {
         ld_pred(b0, cache, 0 < stored);
         ld_pred(b1, cache + 1, 1 < stored);
         if (kPF) prefetch_l1(cache + 8);
@@ -1266,6 +1318,31 @@ __global__ void __launch_bounds__(kThreads, kMinB) gen_bisect_kernel(const GenCo
           q[i].kend = stored;
         }
     };
+    if (kMode == 3) {
+      for (int it = 0; it < 16; ++it) {
+        if (k >= stored) {
+          natural_end();
+          resolved = true;
+          break;
+        }
+        cp_async_wait<kDepth - 2>();  // entry k's group has landed
+        const float4 e = lds128(ring_at(k));
+        const int kold = k;
+        k += consume(e);
+        if (k != kold + 1) {  // skipped a transparent run: restart the ring at k
+          ring_fill(cache, k, stored);
+          continue;
+        }
+        // entry k + kDepth - 2 into the slot entry k - 2 vacated
+        const int kn = k + kDepth - 2;
+        cp_async16(ring_at(kn), cache + (kn < stored ? kn : 0), kn < stored);
+        cp_async_commit();
+        if ((it & 1) && all_resolved()) {  // tested every other step (see kMode 2)
+          resolved = true;
+          break;
+        }
+      }
+    }
     if (kMode == 2) {
       for (int it = 0; it < 8; ++it) {
         if (k >= stored) {
@@ -1306,7 +1383,7 @@ __global__ void __launch_bounds__(kThreads, kMinB) gen_bisect_kernel(const GenCo
           prefetch_l1(cache + k + kAhead);
       }
     }
-    for (int it = 0; kMode != 2 && it < 16 && !resolved; ++it) {
+    for (int it = 0; kMode < 2 && it < 16 && !resolved; ++it) {
      if (k >= stored) {
       // natural end (or the tb <= ta break)
 #pragma unroll
@@ -1450,6 +1527,7 @@ __global__ void __launch_bounds__(kThreads, kMinB) gen_bisect_kernel(const GenCo
     }
     top = true;
   }
+  if (kMode == 3) cp_async_wait<0>();
 #ifdef VDI_BISECT_STATS
   atomicAdd(&c.ctl->st_vis, st_vis);
   atomicAdd(&c.ctl->st_run, st_run);
@@ -2058,11 +2136,15 @@ static int plan_gen(const VdiGenArgs* a, GenPlan& p) {
   p.bisect_threads = kGenThreads;
   p.inv_smem = 4096;
 #ifndef VDI_BISECT_MINB
-#define VDI_BISECT_MINB 5
+// blocks per SM: 4 (128 registers) with the cp.async ring; the register
+// stream (kMode 2) was best at 5 (96 registers)
+#define VDI_BISECT_MINB 4
 #endif
   p.bisect = p.inv_n <= p.inv_smem
-                 ? gen_bisect_kernel<2, 2, VDI_BISECT_PF, VDI_BISECT_MINB, 128, VDI_BISECT_AHEAD, 2, true>
-                 : gen_bisect_kernel<2, 2, VDI_BISECT_PF, VDI_BISECT_MINB, 128, VDI_BISECT_AHEAD, 2, false>;
+                 ? gen_bisect_kernel<2, VDI_BISECT_RING, VDI_BISECT_PF, VDI_BISECT_MINB, 128,
+                                     VDI_BISECT_AHEAD, VDI_BISECT_MODE, true>
+                 : gen_bisect_kernel<2, VDI_BISECT_RING, VDI_BISECT_PF, VDI_BISECT_MINB, 128,
+                                     VDI_BISECT_AHEAD, VDI_BISECT_MODE, false>;
 #ifndef VDI_WIDE_LANES
 #define VDI_WIDE_LANES 32
 #endif
