@@ -83,7 +83,7 @@ constexpr int kGenThreads = 128;
 #define VDI_EMIT_PF 1
 #endif
 #ifndef VDI_EMIT_MINB
-#define VDI_EMIT_MINB 6  // 80 registers: 6 blocks/SM (measured: 6.16 -> 5.64 ms at C3)
+#define VDI_EMIT_MINB 5  // 96 registers (A/B stream: 6 blocks best, 6.16 -> 5.64 ms; ring: 5)
 #endif
 constexpr int kRounds = 3;
 constexpr long long kWideRays = 700000;  // launches below this many rays use the wide hand-off
@@ -1705,8 +1705,25 @@ __global__ void __launch_bounds__(kGenThreads) gen_bisect_wide_kernel(const GenC
 // _gen_list_pass logic: segments, counts, gammas, passes, samples.
 // kRing: entries k, k + 1 in two register slots read by an A/B-unrolled loop
 // (see gen_bisect_kernel kMode 2); otherwise one load per sample.
-template <bool kRing>
+// kStream 2: a per-lane cp.async ring of kEmitRing entries in shared memory
+// (as the bisect replays' kMode 3).
+constexpr int kEmitRing = 4;
+template <int kStream>
 __global__ void __launch_bounds__(kGenThreads, VDI_EMIT_MINB) gen_emit_kernel(const GenConst c) {
+  constexpr bool kRing = kStream == 1;
+  __shared__ float4 s_ring[kStream == 2 ? kEmitRing * kGenThreads : 1];
+  const unsigned ring0 = (unsigned)__cvta_generic_to_shared(s_ring) + 16u * threadIdx.x;
+  auto ring_at = [&](int k) -> unsigned {
+    return ring0 + 16u * (unsigned)kGenThreads * (unsigned)(k & (kEmitRing - 1));
+  };
+  auto ring_fill = [&](const float4* row, int k, int stored) {
+    cp_async_wait<0>();
+#pragma unroll
+    for (int j = 0; j < kEmitRing - 1; ++j) {
+      cp_async16(ring_at(k + j), row + (k + j < stored ? k + j : 0), k + j < stored);
+      cp_async_commit();
+    }
+  };
   const int lane = threadIdx.x & 31;
   const double step = c.a.step;
   const long long nrec = replay_queue_len(c);
@@ -1747,6 +1764,7 @@ __global__ void __launch_bounds__(kGenThreads, VDI_EMIT_MINB) gen_emit_kernel(co
           // window hit / cached high: a counting pass that R does not count
           // again (kRedo); capped: R's final capped pass (counted)
           start_pass(s, g, r.mode_final == kCapped ? kCapped : kRedo);
+          if (kStream == 2) ring_fill(cache, 0, stored);
           if (kRing) {
             ld_pred(b0, cache, 0 < stored);
             ld_pred(b1, cache + 1, 1 < stored);
@@ -1774,7 +1792,25 @@ __global__ void __launch_bounds__(kGenThreads, VDI_EMIT_MINB) gen_emit_kernel(co
       return segment_step(c, s, rgba, ta, tb, run);
     };
     int ended = -1;
-    if (!kRing) {
+    if (kStream == 2) {
+      for (int it = 0; it < 8; ++it) {
+        if (s.k >= stored) {
+          ended = 0;
+          break;
+        }
+        cp_async_wait<kEmitRing - 2>();  // entry k's group has landed
+        const int kold = s.k;
+        ended = entry_step(lds128(ring_at(s.k)));
+        if (ended >= 0) break;
+        if (s.k != kold + 1) {  // a transparent run: restart the ring at k
+          ring_fill(cache, s.k, stored);
+          continue;
+        }
+        const int kn = s.k + kEmitRing - 2;
+        cp_async16(ring_at(kn), cache + (kn < stored ? kn : 0), kn < stored);
+        cp_async_commit();
+      }
+    } else if (!kRing) {
       ended = s.k >= stored ? 0 : entry_step(cache[s.k]);
     } else {
       // (VDI_EMIT_PF: an L1 prefetch of the line kEmitAhead entries ahead
@@ -1822,6 +1858,7 @@ __global__ void __launch_bounds__(kGenThreads, VDI_EMIT_MINB) gen_emit_kernel(co
       have = false;
     }
   }
+  if (kStream == 2) cp_async_wait<0>();
 }
 
 // ---------------------------------------------------------- fused fallback
@@ -2150,9 +2187,13 @@ static int plan_gen(const VdiGenArgs* a, GenPlan& p) {
 #endif
   p.wide = p.inv_n <= p.inv_smem ? gen_bisect_wide_kernel<VDI_WIDE_LANES, true>
                                  : gen_bisect_wide_kernel<VDI_WIDE_LANES, false>;
-  // the emit kernel uses no shared memory: give the unified L1 everything
-  p.emit = gen_emit_kernel<true>;
-  cudaFuncSetAttribute(p.emit, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
+  // the A/B emit kernel uses no shared memory: give the unified L1 everything
+#ifndef VDI_EMIT_STREAM
+#define VDI_EMIT_STREAM 2  // 1: A/B register slots + L1 prefetch, 2: cp.async ring
+#endif
+  p.emit = gen_emit_kernel<VDI_EMIT_STREAM>;
+  if (VDI_EMIT_STREAM != 2)
+    cudaFuncSetAttribute(p.emit, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
   p.smem_inv = sizeof(double) * (size_t)(p.inv_smem < p.inv_n ? p.inv_smem : p.inv_n);
   if (p.smem_inv > 48 * 1024)
     cudaFuncSetAttribute(p.bisect, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem_inv);
