@@ -2427,9 +2427,11 @@ int gen_launch(const VdiGenArgs* a, cudaStream_t stream) {
   // phase costs ~4x the instructions per bisection level, so it pays only
   // when a launch has too few rays to hide its longest rays' serial replays
   // (a band-sharded rank): C3 as 1 rank 31.5 ms without / 36.5 with; as one
-  // of 8 ranks 12.0 / 8.9 ms (profiles/r02_wide_ab.log).
+  // of 8 ranks 12.0 / 8.9 ms (profiles/r02_wide_ab.log). With the cp.async
+  // replays, one of 8 C3 ranks: after 2 / 3 / 4 / 6 / never: 7.25 / 6.93 /
+  // 6.58 / 7.14 / 8.0 ms.
 #ifndef VDI_WIDE_AFTER
-#define VDI_WIDE_AFTER 3
+#define VDI_WIDE_AFTER 4
 #endif
   // learned chain directions beyond those levels (measured: C3 gen 33.6 ->
   // 32.8 ms; C4 / C5 within noise). learn = 0 disables.
