@@ -392,17 +392,12 @@ class Pipeline:
         pipeline's own copy)."""
         t = self.t
         vol_dev = self.vol_dev if vol_dev is None else vol_dev
-        L = _capi.load()
         ev = [t.cuda.Event(enable_timing=True) for _ in range(6)] if timed else None
         if timed:
             ev[0].record()
         self.sums.zero_()
         self.prep(vol_dev)
-        launch_generate(vol_dev, self.vt, self.vol.dims, self.lut_dev, self.gcam,
-                        self.aabb, self.params, self.resolved, self.bufs, self.grid_dims,
-                        band=self.gen_band, split_events=ev, bricks=self.bricks,
-                        ess_max=self.ess_max, cells=self.cells, sub=self.sub,
-                        rows=self.gen_range)
+        self.launch_gen(vol_dev, split_events=ev)
         if timed:
             ev[3].record()
         if self.world > 1:
@@ -413,11 +408,7 @@ class Pipeline:
                              self.g_counts, self.g_segs)
         if timed:
             ev[4].record()
-        if self.tiles is not None:
-            launch_list_tiles(self._rargs, self.tiles)
-        launch_zmask(self._rargs, self.zmask)
-        launch_ranges(self._rargs, self.ranges, self.n_lists)
-        _capi.check(L.vdi_render_launch(self._rargs, dv.stream_handle()))
+        self.launch_render(zero_sums=False)
         if timed:
             ev[5].record()
         if self.world > 1:
@@ -432,6 +423,26 @@ class Pipeline:
                 "grid": ev[2].elapsed_time(ev[3]),
                 "collective": ev[3].elapsed_time(ev[4]) + ev[5].elapsed_time(end),
                 "render": ev[4].elapsed_time(ev[5])}
+
+    def launch_gen(self, vol_dev, split_events=None):
+        """This rank's generation + partial AccelGrid of `vol_dev` (prep done),
+        on the current stream."""
+        launch_generate(vol_dev, self.vt, self.vol.dims, self.lut_dev, self.gcam,
+                        self.aabb, self.params, self.resolved, self.bufs, self.grid_dims,
+                        band=self.gen_band, split_events=split_events, bricks=self.bricks,
+                        ess_max=self.ess_max, cells=self.cells, sub=self.sub,
+                        rows=self.gen_range)
+
+    def launch_render(self, zero_sums: bool = True):
+        """This rank's render of the exchanged VDI into self.image (slab words,
+        list ranges, render), on the current stream."""
+        if zero_sums:
+            self.sums.zero_()
+        if self.tiles is not None:
+            launch_list_tiles(self._rargs, self.tiles)
+        launch_zmask(self._rargs, self.zmask)
+        launch_ranges(self._rargs, self.ranges, self.n_lists)
+        _capi.check(_capi.load().vdi_render_launch(self._rargs, dv.stream_handle()))
 
     def prep(self, vol_dev, gather: bool = True):
         """Per-volume acceleration data: brick maxima (sharded by z-slab and

@@ -9,10 +9,16 @@ nearly doubles the frame time. FrameStream runs three CUDA streams over
 double-buffered HBM and pinned host slots:
 
     h2d     : volume i+1  host -> HBM slot (i+1) % 2
-    compute : volume prep, generation, grid, (exchange,) render of frame i,
-              then the results are packed into output slot i % 2 (counts,
-              AoS segs, AccelGrid, image)
+    compute : volume prep, generation, grid of frame i
+    render  : render of frame i, then the results are packed into output
+              slot i % 2 (counts, AoS segs or VDI1 bytes, AccelGrid, image)
     d2h     : results of frame i-1  HBM slot -> pinned host slot (i-1) % 2
+
+With one rank the render of frame i runs on its own stream, beside the
+volume prep of frame i+1 (which reads neither the VDI nor the image); the
+generation of frame i+1 waits for it (one set of generation buffers). With
+N > 1 ranks the whole step, collectives included, stays on the compute
+stream.
 
 Every frame still performs its full H2D and D2H; only their overlap with the
 neighbouring frames' kernels changes. Events order the slot reuse: an upload
@@ -100,6 +106,9 @@ class FrameStream:
         vol = pipe.vol
         shape = tuple(pipe.vol_dev.shape)
         self.h2d, self.comp, self.d2h = (t.cuda.Stream() for _ in range(3))
+        # one rank: the render and the packing of frame i beside frame i+1's prep
+        self.split = getattr(pipe, "world", 1) == 1
+        self.rend = t.cuda.Stream() if self.split else self.comp
         # packed mode: the variable-length VDI1 copy gets its own stream, so it
         # does not queue behind the next frame's fixed-size readback (which
         # waits for that frame's kernels)
@@ -133,6 +142,9 @@ class FrameStream:
                               for k, v in o.items()})
         ev = lambda: t.cuda.Event()  # noqa: E731
         self.ev_h2d = [ev(), ev()]       # upload of slot s done
+        self.ev_vol = [ev(), ev()]       # the kernels that read vol slot s are done
+        self.ev_gen = ev()               # the last frame's generation is done
+        self.ev_rend = ev()              # the last frame's render / packing is done
         self.ev_comp = [ev(), ev()]      # compute that read vol slot / wrote out slot s done
         self.ev_d2h = [ev(), ev()]       # download of out slot s done
         self.used_vol = [False, False]
@@ -155,7 +167,7 @@ class FrameStream:
         src = t.from_numpy(np.ascontiguousarray(host_volume).reshape(self.vol_shape))
         with t.cuda.stream(self.h2d):
             if self.used_vol[s]:
-                self.h2d.wait_event(self.ev_comp[s])
+                self.h2d.wait_event(self.ev_vol[s])
             self.vol_slots[s].copy_(src, non_blocking=True)
             self.ev_h2d[s].record(self.h2d)
         self.used_vol[s] = True
@@ -163,9 +175,23 @@ class FrameStream:
         out = self.out[s]
         with t.cuda.stream(self.comp):
             self.comp.wait_event(self.ev_h2d[s])
-            if self.used_out[s]:
-                self.comp.wait_event(self.ev_d2h[s])
-            p.step(vol_dev=self.vol_slots[s])
+            if self.split:
+                p.prep(self.vol_slots[s])
+                # the generation rewrites the VDI the previous render reads
+                self.comp.wait_event(self.ev_rend)
+                p.launch_gen(self.vol_slots[s])
+                self.ev_gen.record(self.comp)
+            else:
+                if self.used_out[s]:
+                    self.comp.wait_event(self.ev_d2h[s])
+                p.step(vol_dev=self.vol_slots[s])
+            self.ev_vol[s].record(self.comp)
+        with t.cuda.stream(self.rend):
+            if self.split:
+                self.rend.wait_event(self.ev_gen)
+                if self.used_out[s]:
+                    self.rend.wait_event(self.ev_d2h[s])
+                p.launch_render()
             L = _capi.load()
             if self.packed:
                 _capi.check(L.vdi_encode_vdi1(self._enc_args(out), dv.stream_handle()))
@@ -176,7 +202,8 @@ class FrameStream:
                 out["counts"].copy_(p.bufs.counts, non_blocking=True)
                 out["grid"].copy_(p.bufs.grid, non_blocking=True)
             out["image"].copy_(p.image, non_blocking=True)
-            self.ev_comp[s].record(self.comp)
+            self.ev_comp[s].record(self.rend)
+            self.ev_rend.record(self.rend)
         self.used_out[s] = True
         with t.cuda.stream(self.d2h):
             self.d2h.wait_event(self.ev_comp[s])
