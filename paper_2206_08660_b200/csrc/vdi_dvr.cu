@@ -33,6 +33,7 @@ struct DvrConst {
   double inv_lref;
   int lref_pow2;
   int ess, bnx, bny;
+  int ess_u8;      // u8 volumes: ess_max as a byte threshold (brick_empty)
   int tiles_x, local_h;
   long long n_slots;
   unsigned long long* fetch;
@@ -210,6 +211,9 @@ int dvr_launch(const VdiDvrArgs* a, cudaStream_t stream) {
   const long long tiles_y = (c.local_h + kTileH - 1) / kTileH;
   c.n_slots = (long long)c.tiles_x * tiles_y * 32;
   c.ess = a->brick_max != nullptr && a->ess_max >= 0.0 && a->brick_log2 >= 1;
+  c.ess_u8 = -1;  // the largest v with (double)((float)v / 255) <= ess_max
+  for (int v = 0; v < 256; ++v)
+    if ((double)((float)v / 255.0f) <= a->ess_max) c.ess_u8 = v;
   if (c.ess) {
     const int B = 1 << a->brick_log2;
     c.bnx = (a->nx + B - 1) / B;

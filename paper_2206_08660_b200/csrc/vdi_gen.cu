@@ -172,6 +172,7 @@ struct GenConst {
   RoundCtl* prev;  // previous round (its ndefer sizes defer_in)
   int round;
   int ess;         // empty-space skipping enabled
+  int ess_u8;      // u8 volumes: ess_max as a byte threshold (brick_empty)
   int bnx, bny;    // brick grid x / y extent (of the resident box in kVoxelSub variants)
   // resident box (kVoxelSub variants): row strides, index rebases, origin, extent
   long long sub_sx, sub_sy, sub_voff, sub_boff;
@@ -2398,6 +2399,9 @@ int gen_launch(const VdiGenArgs* a, cudaStream_t stream) {
   const long long tiles_y = (c.local_h + kTileH - 1) / kTileH;
   c.n_slots = (long long)c.tiles_x * tiles_y * 32;
   c.ess = a->brick_max != nullptr && a->ess_max >= 0.0 && a->brick_log2 >= 1;
+  c.ess_u8 = -1;  // the largest v with (double)((float)v / 255) <= ess_max
+  for (int v = 0; v < 256; ++v)
+    if ((double)((float)v / 255.0f) <= a->ess_max) c.ess_u8 = v;
   const bool sub = a->sub_dims[0] > 0;
   const int rx = sub ? a->sub_dims[0] : a->nx, ry = sub ? a->sub_dims[1] : a->ny;
   if (c.ess) {

@@ -79,6 +79,18 @@ struct Cell<VDI_VOXEL_F32> {
   }
 };
 
+// Brick bi of brick_max classifies as always transparent (its maximum <=
+// ess_max). u8: the raw byte against c.ess_u8, the largest v with v / 255
+// (the f32 quotient of volume.py:48-50, widened) <= ess_max -- the same test,
+// since the quotient grows with v -- without the table load and f64 compare.
+template <int VT, class C>
+__device__ __forceinline__ bool brick_empty(const C& c, long long bi, const double* tab) {
+  if constexpr ((VT & 15) == VDI_VOXEL_U8)
+    return (int)__ldg(static_cast<const unsigned char*>(c.a.brick_max) + bi) <= c.ess_u8;
+  else
+    return Voxel<(VT & 15)>::get(c.a.brick_max, bi, tab) <= c.a.ess_max;
+}
+
 // Kernel-variant flag (not part of the C ABI): the volume in memory is only
 // a resident box of the full grid (VdiGenArgs.sub_origin / sub_dims), e.g.
 // one rank's slab of a volume bricked across GPUs. Sample positions and cell
@@ -123,9 +135,9 @@ __device__ __forceinline__ double trilinear(const C& c, const double* tab, doubl
     // exceeds its largest input by more than a few ulps. -1 classifies to LUT
     // row 0, whose alpha is 0: the sample is transparent, as in the reference.
     const int lb = c.a.brick_log2;
-    const long long bi =
-        ((long long)(iz >> lb) * c.bny + (iy >> lb)) * c.bnx + (ix >> lb) - boff;
-    if (Voxel<(VT & 15)>::get(c.a.brick_max, bi, tab) <= c.a.ess_max) return -1.0;
+    // brick counts fit 32 bits (a 2^31-brick grid would be 2^40 voxels)
+    const long long bi = (long long)(((iz >> lb) * c.bny + (iy >> lb)) * c.bnx + (ix >> lb)) - boff;
+    if (brick_empty<VT>(c, bi, tab)) return -1.0;
   }
   const double fx = gx - ix, fy = gy - iy, fz = gz - iz;
   if (VT & VDI_VOXEL_CELLS) {
@@ -195,7 +207,7 @@ __device__ __forceinline__ int empty_run(const C& c, const double* tab, const do
   if constexpr ((VT & kVoxelSub) != 0) boff = c.sub_boff;
   const long long bi = ((long long)(cell[2] >> lb) * c.bny + (cell[1] >> lb)) * c.bnx +
                        (cell[0] >> lb) - boff;
-  if (!(Voxel<(VT & 15)>::get(c.a.brick_max, bi, tab) <= c.a.ess_max)) return 0;
+  if (!brick_empty<VT>(c, bi, tab)) return 0;
   const int B = 1 << lb;
   long long m = max_run - 1;
 #pragma unroll
