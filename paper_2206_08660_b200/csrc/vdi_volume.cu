@@ -229,6 +229,92 @@ __global__ void cells_u8x4_kernel(const uint8_t* __restrict__ vol, uint4* __rest
   }
 }
 
+// The same records, a thread walking its 4-cell group down z: rows (y, z+1)
+// and (y+1, z+1) of one step are rows (y, z) and (y+1, z) of the next, so a
+// step loads two row words (+ their next bytes) instead of four, and the row
+// index math is paid once per z run. An empty brick's z range is skipped
+// without loads (the window is reloaded at the next non-empty brick).
+// Item = (y, chunk of kCellsZ slices); threads over the x groups.
+constexpr int kCellsZ = 32;
+constexpr int kCellsBatch = 4;
+__global__ void cells_u8x4z_kernel(const uint8_t* __restrict__ vol, uint4* __restrict__ out,
+                                   int nx, int ny, int nz, const uint8_t* __restrict__ bmax,
+                                   int lb, int bnx, int bny, int skip_max) {
+  const int qx = nx >> 2;
+  const int nzc = (nz + kCellsZ - 1) / kCellsZ;
+  const long long plane = (long long)nx * ny;
+  for (int item = blockIdx.x; item < ny * nzc; item += gridDim.x) {
+    const int y = item % ny, zb = (item / ny) * kCellsZ;
+    const int ze = min(zb + kCellsZ, nz);
+    const long long dy = y + 1 < ny ? nx : 0;
+    for (int q = threadIdx.x; q < qx; q += blockDim.x) {
+      const int x = q * 4;
+      const bool last = x + 4 >= nx;
+      const uint8_t* col = vol + (long long)y * nx + x;  // (x, y, z = 0)
+      // voxels x .. x+3 (one word) and x + 4 (clamped to x + 3 at the row end)
+      auto word = [&](const uint8_t* p, unsigned& w, unsigned& e) {
+        w = __ldg(reinterpret_cast<const unsigned*>(p));
+        e = last ? (w >> 24) : (unsigned)__ldg(p + 4);
+      };
+      unsigned w0 = 0, w1 = 0, e0 = 0, e1 = 0;  // rows (y, z), (y + 1, z)
+      bool have = false;
+      int z = zb;
+      while (z < ze) {
+        const int zend = min(((z >> lb) + 1) << lb, ze);  // this brick's slices
+        if (bmax && (int)__ldg(bmax + ((long long)(z >> lb) * bny + (y >> lb)) * bnx +
+                               (x >> lb)) <= skip_max) {
+          z = zend;
+          have = false;
+          continue;
+        }
+        if (!have) {
+          word(col + (long long)z * plane, w0, e0);
+          word(col + (long long)z * plane + dy, w1, e1);
+          have = true;
+        }
+        // kCellsBatch slices per batch: their row words are all requested
+        // before the first record is built (memory-level parallelism)
+        while (z < zend) {
+          const int nb = zend - z < kCellsBatch ? zend - z : kCellsBatch;
+          unsigned wa[kCellsBatch], ea[kCellsBatch], wb[kCellsBatch], eb[kCellsBatch];
+#pragma unroll
+          for (int j = 0; j < kCellsBatch; ++j) {
+            if (j < nb) {
+              const int zz = z + j;
+              const long long dz = zz + 1 < nz ? plane : 0;
+              const uint8_t* r0 = col + (long long)zz * plane + dz;  // rows (y, zz + 1)
+              word(r0, wa[j], ea[j]);
+              word(r0 + dy, wb[j], eb[j]);                            // and (y + 1, zz + 1)
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < kCellsBatch; ++j) {
+            if (j < nb) {
+              const unsigned w2 = wa[j], e2 = ea[j], w3 = wb[j], e3 = eb[j];
+              const unsigned n0 = __funnelshift_r(w0, e0, 8), n1 = __funnelshift_r(w1, e1, 8);
+              const unsigned n2 = __funnelshift_r(w2, e2, 8), n3 = __funnelshift_r(w3, e3, 8);
+              const uint4 o0 =
+                  make_uint4(__byte_perm(w0, w1, 0x5410), __byte_perm(w2, w3, 0x5410),
+                             __byte_perm(w0, w1, 0x6521), __byte_perm(w2, w3, 0x6521));
+              const uint4 o1 =
+                  make_uint4(__byte_perm(w0, w1, 0x7632), __byte_perm(w2, w3, 0x7632),
+                             __byte_perm(n0, n1, 0x7632), __byte_perm(n2, n3, 0x7632));
+              uint4* o = out + 2 * ((long long)(((z + j) * ny + y)) * (nx >> 2) + q);
+              o[0] = o0;
+              o[1] = o1;
+              w0 = w2;
+              w1 = w3;
+              e0 = e2;
+              e1 = e3;
+            }
+          }
+          z += nb;
+        }
+      }
+    }
+  }
+}
+
 int volume_cells(const void* volume, int voxel_type, int nx, int ny, int nz, void* out,
                  cudaStream_t stream, const void* brick_max, int brick_log2, double ess_max) {
   const bool masked = brick_max != nullptr && ess_max >= 0.0 && brick_log2 >= 2;
@@ -253,11 +339,24 @@ int volume_cells(const void* volume, int voxel_type, int nx, int ny, int nz, voi
         if (masked)
           for (int v = 0; v < 256; ++v)
             if ((double)((float)v / 255.0f) <= ess_max) skip_max = v;
-        cells_u8x4_kernel<<<(unsigned)std::min<long long>((long long)ny * nz, (long long)sms * 32),
-                            256, 0, stream>>>(
-            static_cast<const uint8_t*>(volume), static_cast<uint4*>(out), nx, ny, nz,
-            masked ? static_cast<const uint8_t*>(brick_max) : nullptr, brick_log2, bnx, bny,
-            skip_max);
+#ifndef VDI_CELLS_Z
+#define VDI_CELLS_Z 1  // 1: cells_u8x4z_kernel (z walks), 0: one (y, z) row per block pass
+#endif
+        if (VDI_CELLS_Z) {
+          const long long items = (long long)ny * ((nz + kCellsZ - 1) / kCellsZ);
+          cells_u8x4z_kernel<<<(unsigned)std::min<long long>(items, (long long)sms * 16), 256, 0,
+                               stream>>>(
+              static_cast<const uint8_t*>(volume), static_cast<uint4*>(out), nx, ny, nz,
+              masked ? static_cast<const uint8_t*>(brick_max) : nullptr,
+              brick_log2 > 0 ? brick_log2 : 3, bnx, bny, skip_max);
+        } else {
+          cells_u8x4_kernel<<<(unsigned)std::min<long long>((long long)ny * nz,
+                                                            (long long)sms * 32),
+                              256, 0, stream>>>(
+              static_cast<const uint8_t*>(volume), static_cast<uint4*>(out), nx, ny, nz,
+              masked ? static_cast<const uint8_t*>(brick_max) : nullptr, brick_log2, bnx, bny,
+              skip_max);
+        }
       }
       else
         cells_kernel<<<(unsigned)blocks, 256, 0, stream>>>(static_cast<const uint8_t*>(volume),
