@@ -145,6 +145,9 @@ struct RoundCtl {
   // VDI_BISECT_STATS builds only: narrow-replay steps on visible entries, on
   // transparent runs, the entries the runs covered, replays started
   unsigned long long st_vis, st_run, st_run_entries, st_replays;
+  // VDI_FILL_STATS builds only: fill chunks, chunks whose valid samples all
+  // lie in empty bricks, chunks whose valid samples are all transparent
+  unsigned long long st_chunks, st_chunks_empty, st_chunks_transp;
   // bisection decisions seen so far in this round, per level: [0] up, [1] down
   // (the bisect replays' learned speculation direction)
   unsigned dir[2][32];
@@ -736,6 +739,12 @@ __device__ __forceinline__ int replay_queue_at(const GenConst& c, long long idx)
   return VDI_REPLAY_ORDER ? c.qidx[idx] : c.torder[idx];
 }
 
+// Fill: VDI_FILL_SPARSE writes only the head entry of a transparent run (the
+// replays jump over runs, so the other entries are never read).
+#ifndef VDI_FILL_SPARSE
+#define VDI_FILL_SPARSE 1
+#endif
+
 // -------------------------------------------------------------- fill phase
 // One warp per queued ray: lane j classifies sample kb + j of 32-sample chunks
 // and stores it in the ray's cache run (coalesced 512 B per chunk, coherent
@@ -787,7 +796,20 @@ __global__ void VDI_FILL_BOUNDS gen_fill_kernel(const GenConst c) {
       if (broke) stored = kb + __ffs(broke) - 1;
       valid = k < stored;
       float4 rgba = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (valid) rgba = sample_at<VT>(c, s_lut, s_u8, s, ta, tb);
+      bool in_empty = false;
+      if (valid) rgba = sample_at<VT>(c, s_lut, s_u8, s, ta, tb, &in_empty);
+#ifdef VDI_FILL_STATS
+      {
+        const unsigned vmask = __ballot_sync(0xffffffffu, valid);
+        const unsigned emask = __ballot_sync(0xffffffffu, valid && in_empty);
+        const unsigned tmask = __ballot_sync(0xffffffffu, valid && rgba.w <= 0.0f);
+        if (lane == 0 && vmask) {
+          atomicAdd(&c.ctl->st_chunks, 1ull);
+          if (emask == vmask) atomicAdd(&c.ctl->st_chunks_empty, 1ull);
+          if (tmask == vmask) atomicAdd(&c.ctl->st_chunks_transp, 1ull);
+        }
+      }
+#endif
       const bool transp = valid && rgba.w <= 0.0f;
       const unsigned tm = __ballot_sync(0xffffffffu, transp);
       const unsigned vm = __ballot_sync(0xffffffffu, valid);
@@ -801,7 +823,8 @@ __global__ void VDI_FILL_BOUNDS gen_fill_kernel(const GenConst c) {
           cache[open_head].x = __int_as_float(kb + __ffs(nt) - 1 - open_head);
         open_head = -1;
       }
-      if (valid) {
+      // a run's non-head entries are never read (VDI_FILL_SPARSE: not written)
+      if (valid && (!VDI_FILL_SPARSE || !transp || ((heads >> lane) & 1u))) {
         float4 st;
         if (transp) {
           int len = 1;

@@ -36,7 +36,9 @@ print(f"round0: queued rays {ctl[2]}, cached entries {ctl[1]} ({ctl[1]*16/1e9:.2
       f"deferred {ctl[4]}, handed to the wide bisect {ctl[7]}; hit rays {hit} of {passes.numel()}, "
       f"mean passes (hit) {float(passes[passes > 0].float().mean()):.2f}, "
       f"1-pass rays {int((passes == 1).sum())}")
-# RoundCtl words 11..14: the VDI_BISECT_STATS counters
-if any(ctl[11:15]):
-    print(f"bisect replays {ctl[14]}: visible steps {ctl[11]}, run steps {ctl[12]} "
-          f"covering {ctl[13]} entries")
+# RoundCtl words 10..13: the VDI_BISECT_STATS counters, 14..16 VDI_FILL_STATS
+if any(ctl[10:14]):
+    print(f"bisect replays {ctl[13]}: visible steps {ctl[10]}, run steps {ctl[11]} "
+          f"covering {ctl[12]} entries")
+if any(ctl[14:17]):
+    print(f"fill chunks {ctl[14]}: all in empty bricks {ctl[15]}, all transparent {ctl[16]}")
