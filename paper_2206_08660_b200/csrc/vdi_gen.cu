@@ -102,7 +102,7 @@ struct RayRec {
   int samples;      // samples executed so far (R semantics)
   int passes;       // passes so far (R semantics)
   int mode_final;   // kCount (window hit / cached high) or kCapped
-  int pad;
+  int first_vis;    // the first non-transparent sample (pass 1 of the sample phase)
   // bisection state handed from a narrow replay lane to the wide phase
   double low, high;
   int last_n, high_n;
@@ -209,6 +209,7 @@ struct RayState {
   // bisection (generate.py:230-236)
   double low, high, bis_gamma;
   int first, last_n, high_n, passes, buf_is_high, samples;
+  int first_vis;  // sample phase: the first non-transparent sample of pass 1 (-1: none yet)
 };
 
 // Smallest double s >= 0 with sqrt_rn(s) >= g, so that sqrt_rn(d2) >= g <=>
@@ -504,6 +505,7 @@ __device__ bool setup_ray(const GenConst& c, RayState& s, int list) {
   s.t1 = t1;
   s.nsteps = (int)ceil((t1 - t0) / c.a.step);
   start_pass(s, s.bis_gamma, kCount);
+  s.first_vis = -1;
   return true;
 }
 
@@ -586,6 +588,7 @@ __device__ __forceinline__ bool load_ray(const GenConst& c, RayState& s, int lis
   s.nsteps = r->nsteps;
   init_bisection(c, s);
   start_pass(s, s.bis_gamma, kCount);
+  s.first_vis = -1;
   return true;
 }
 
@@ -676,6 +679,7 @@ __global__ void __launch_bounds__(kGenThreads, VDI_SAMPLE_MINB) gen_sample_kerne
       if (tb > ta) {
         bool ess_hit = false;
         const float4 rgba = sample_at<VT>(c, s_lut, s_u8, s, ta, tb, &ess_hit);
+        if (s.first_vis < 0 && rgba.w > 0.0f) s.first_vis = s.k;
         int run = 1;
         if (ess_hit) {
           // a run of samples in an empty brick: transparent, counted, not
@@ -718,7 +722,7 @@ __global__ void __launch_bounds__(kGenThreads, VDI_SAMPLE_MINB) gen_sample_kerne
       r.passes = 1;
       r.g_final = 0.0;
       r.mode_final = kCount;
-      r.pad = 0;
+      r.first_vis = s.first_vis;
       c.recs[s.list] = r;
       atomicOr(c.qbits + (s.list >> 5), 1u << (s.list & 31));
       // overflow order (VDI_REPLAY_ORDER 0 only)
@@ -739,8 +743,12 @@ __device__ __forceinline__ int replay_queue_at(const GenConst& c, long long idx)
   return VDI_REPLAY_ORDER ? c.qidx[idx] : c.torder[idx];
 }
 
-// Fill: VDI_FILL_SPARSE writes only the head entry of a transparent run (the
+// Fill: VDI_FILL_FROM_VISIBLE starts at the chunk of pass 1's first visible
+// sample; VDI_FILL_SPARSE writes only the head entry of a transparent run (the
 // replays jump over runs, so the other entries are never read).
+#ifndef VDI_FILL_FROM_VISIBLE
+#define VDI_FILL_FROM_VISIBLE 1
+#endif
 #ifndef VDI_FILL_SPARSE
 #define VDI_FILL_SPARSE 1
 #endif
@@ -781,7 +789,17 @@ __global__ void VDI_FILL_BOUNDS gen_fill_kernel(const GenConst c) {
     float4* cache = c.cache + rec->slot;
     int open_head = -1;  // warp-uniform
     int stored = nsteps;
-    for (int kb = 0; kb < stored; kb += 32) {
+    // pass 1 (the sample phase) found samples 0 .. first_vis - 1 transparent
+    // (the same classification): one run from 0, so the fill starts at the
+    // chunk of the first visible sample and patches the run's head there
+    int kb0 = 0;
+    const int fv = VDI_FILL_FROM_VISIBLE ? rec->first_vis : -1;
+    if (fv >= 32 && fv < stored) {
+      if (lane == 0) cache[0] = make_float4(__int_as_float(1), 0.f, 0.f, 0.f);
+      open_head = 0;
+      kb0 = fv & ~31;
+    }
+    for (int kb = kb0; kb < stored; kb += 32) {
       const int k = kb + lane;
       bool valid = k < stored;
       double ta = 0.0, tb = 0.0;
