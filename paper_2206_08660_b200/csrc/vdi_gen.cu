@@ -1289,7 +1289,12 @@ __global__ void __launch_bounds__(kThreads, kMinB) gen_bisect_kernel(const GenCo
 #endif
       k = 0;
       if (kMode == 3) {
-        ring_fill(cache, 0, stored);
+        // samples before pass 1's first visible one are one transparent run
+        // from 0 (the fill's head entry): a replay may start past it with the
+        // same (reset) count states
+        const int k0 = rec->first_vis;
+        if (k0 > 0 && k0 < stored) k = k0;
+        ring_fill(cache, k, stored);
       } else if (kMode == 2) {
         ld_pred(b0, cache, 0 < stored);
         ld_pred(b1, cache + 1, 1 < stored);
