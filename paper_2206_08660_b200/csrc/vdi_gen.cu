@@ -1811,7 +1811,16 @@ __global__ void __launch_bounds__(kGenThreads, VDI_EMIT_MINB) gen_emit_kernel(co
           // window hit / cached high: a counting pass that R does not count
           // again (kRedo); capped: R's final capped pass (counted)
           start_pass(s, g, r.mode_final == kCapped ? kCapped : kRedo);
-          if (kStream == 2) ring_fill(cache, 0, stored);
+          if (kStream == 2) {
+            // past pass 1's first visible sample: the run before it only
+            // counts its samples (a closed segment stays closed)
+            const int k0 = r.first_vis;
+            if (k0 > 0 && k0 < stored) {
+              s.k = k0;
+              if (s.mode != kRedo) s.samples += k0;
+            }
+            ring_fill(cache, s.k, stored);
+          }
           if (kRing) {
             ld_pred(b0, cache, 0 < stored);
             ld_pred(b1, cache + 1, 1 < stored);
