@@ -2509,7 +2509,7 @@ int gen_launch(const VdiGenArgs* a, cudaStream_t stream) {
 #ifndef VDI_WIDE_TAIL
 #define VDI_WIDE_TAIL 0
 #endif
-  c.wide_tail = VDI_WIDE_TAIL;
+  c.wide_tail = p.n_rays < kWideRays ? VDI_WIDE_TAIL : 0;
   if (rc != VDI_OK) return rc;
   const size_t need = gen_workspace_bytes(&c.a, 0);
   if (a->workspace_bytes < need)
