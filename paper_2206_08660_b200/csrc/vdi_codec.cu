@@ -320,27 +320,31 @@ __global__ void dec_segs_kernel(const uint8_t* __restrict__ src, long long n, in
   for (int j = wid; j < kEncBlock && l0 + j < n; j += kEncBlock / 32) {
     const int c = s_cnt[j];
     const uint8_t* rec = src + kVdi1Header + 2 * n + 24 * s_excl[j];
-    float* ls = segs + (l0 + j) * (long long)stride;
-    for (int q = lane; q < stride; q += 32) {
-      int k, f;  // supersegment, field of its record [front, back, r, g, b, a]
-      if (q < 4 * n_sg) {
-        k = q >> 2;
-        f = 2 + (q & 3);
-      } else if (q < 5 * n_sg) {
-        k = q - 4 * n_sg;
-        f = 0;
+    // four floats per lane and store: the rgba float4 of one record, or four
+    // consecutive fronts / backs (pad zeros)
+    float4* ls4 = reinterpret_cast<float4*>(segs + (l0 + j) * (long long)stride);
+    auto field = [&](int k, int f) -> float {
+      if (k >= c) return 0.f;
+      const uint8_t* r = rec + 24 * k + 4 * f;
+      return al4 ? __ldg(reinterpret_cast<const float*>(r))
+                 : __uint_as_float((unsigned)r[0] | ((unsigned)r[1] << 8) |
+                                   ((unsigned)r[2] << 16) | ((unsigned)r[3] << 24));
+    };
+    for (int q4 = lane; q4 < (stride >> 2); q4 += 32) {
+      float4 v;
+      if (q4 < n_sg) {
+        v = make_float4(field(q4, 2), field(q4, 3), field(q4, 4), field(q4, 5));
       } else {
-        k = q - 5 * n_sg;  // >= n_sg in the pad
-        f = 1;
+        float t[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int q = 4 * q4 + e;
+          // fronts [4 n_sg, 5 n_sg), backs [5 n_sg, 6 n_sg), then the pad
+          t[e] = q < 5 * n_sg ? field(q - 4 * n_sg, 0) : field(q - 5 * n_sg, 1);
+        }
+        v = make_float4(t[0], t[1], t[2], t[3]);
       }
-      float val = 0.f;
-      if (k < c) {
-        const uint8_t* r = rec + 24 * k + 4 * f;
-        val = al4 ? __ldg(reinterpret_cast<const float*>(r))
-                  : __uint_as_float((unsigned)r[0] | ((unsigned)r[1] << 8) |
-                                    ((unsigned)r[2] << 16) | ((unsigned)r[3] << 24));
-      }
-      ls[q] = val;
+      ls4[q4] = v;
     }
   }
 }
