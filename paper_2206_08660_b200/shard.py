@@ -307,8 +307,10 @@ class Pipeline:
         # pass on every rank; with more than two ranks sharing the rays they
         # cost more than they save (C3: 0.93 ms vs 2.5 ms / N), so only N <= 2
         # builds them
+        from .tuning import TUNING
         self.cells = (dv.alloc_cells(self.vt, self.res_dims)
-                      if dv.use_cells(self.vt, self.res_dims) and world <= 2 else None)
+                      if dv.use_cells(self.vt, self.res_dims)
+                      and (world <= TUNING.cells_max_world) else None)
         # N > 1 (replicated volume): each rank computes a z-slab of the brick
         # maxima and the ranks all-gather them (1.6 MB at C3)
         self.slabs = None

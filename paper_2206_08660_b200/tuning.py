@@ -13,6 +13,9 @@ class Tuning:
     # corner records (vdi_volume_cells) for generation / DVR sampling:
     # None = automatic (u8 volumes whose records fit in a quarter of HBM)
     cells: bool | None = None
+    # the largest band-sharded world whose ranks still build the corner
+    # records (each rank builds them for the whole volume)
+    cells_max_world: int = 2
     # empty-tile skipping in the render DDA (VdiRenderArgs.list_tiles)
     list_tiles: bool = False
     # per-list depth ranges for the render's search-first path

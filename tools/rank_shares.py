@@ -74,7 +74,12 @@ def main():
     p.add_argument("--balanced", action="store_true",
                    help="bricked bands of unequal height balanced on the per-row executed "
                         "samples of the N = 1 step (as the previous frame would give them)")
+    p.add_argument("--cells-max-world", type=int, default=None,
+                   help="tuning.TUNING.cells_max_world (corner records on ranks up to this N)")
     a = p.parse_args()
+    if a.cells_max_world is not None:
+        from paper_2206_08660_b200.tuning import TUNING
+        TUNING.cells_max_world = a.cells_max_world
     vol, tf, gcam, rcam, n_sg = synth.config(a.config)
     params = GenParams(n_sg=n_sg)
     L = _capi.load()
