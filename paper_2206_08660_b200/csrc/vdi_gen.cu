@@ -1754,7 +1754,10 @@ __global__ void __launch_bounds__(kGenThreads) gen_bisect_wide_kernel(const GenC
 // (see gen_bisect_kernel kMode 2); otherwise one load per sample.
 // kStream 2: a per-lane cp.async ring of kEmitRing entries in shared memory
 // (as the bisect replays' kMode 3).
-constexpr int kEmitRing = 4;
+#ifndef VDI_EMIT_RING
+#define VDI_EMIT_RING 4
+#endif
+constexpr int kEmitRing = VDI_EMIT_RING;
 template <int kStream>
 __global__ void __launch_bounds__(kGenThreads, VDI_EMIT_MINB) gen_emit_kernel(const GenConst c) {
   constexpr bool kRing = kStream == 1;
